@@ -1,0 +1,363 @@
+// capi.cu — the exported C ABI of libdc (include/dc.h): argument checks, handle state
+// machine, context plumbing. Every compute step runs in the kernels of the other files.
+#include <stdarg.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "prim.cuh"
+
+namespace dc {
+dc_status intern_frames(Ctx* c, const dc_frame_key* keys, uint64_t n, uint32_t* out_ids, dc_dict** out);
+dc_status dict_from_sorted(Ctx* c, const dc_frame_key* keys, uint64_t D, dc_dict** out);
+dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_frames, uint32_t* out_leaf, dc_cct** out);
+dc_status attribute_metrics(Ctx* c, dc_cct* t, const uint32_t* leaf, uint64_t R, const uint64_t* X, uint32_t M, uint64_t ld);
+dc_status rollup(Ctx* c, dc_cct* t);
+dc_status pc_attribute(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, const uint32_t* launch_leaf, uint64_t n_launch,
+                       const uint64_t* launch_off, uint32_t S);
+dc_status hotspots_topk(Ctx* c, const dc_cct* t, dc_view view, uint32_t metric, uint32_t kind_mask, double threshold,
+                        uint32_t k, uint32_t stall_node, dc_topk_entry* out_h, uint32_t* n_out_h);
+dc_status derived(Ctx* c, const dc_cct* t, uint32_t metric, int incl, double* mean, double* stdv);
+
+dc_status fail(Ctx* c, dc_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return s;
+}
+
+dc_status cuda_fail(Ctx* c, cudaError_t e, const char* what) {
+  return fail(c, DC_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+dc_status readback(Ctx* c, const void* dev, size_t bytes, void* host) {
+  if (bytes == 0) return DC_OK;
+  if (bytes <= 4096) {
+    DC_CUDA(c, cudaMemcpyAsync(c->h_pinned, dev, bytes, cudaMemcpyDeviceToHost, c->stream));
+    DC_CUDA(c, cudaStreamSynchronize(c->stream));
+    memcpy(host, c->h_pinned, bytes);
+  } else {
+    DC_CUDA(c, cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, c->stream));
+    DC_CUDA(c, cudaStreamSynchronize(c->stream));
+  }
+  return DC_OK;
+}
+
+dc_status check_flags(Ctx* c) {
+  uint32_t f = 0;
+  DC_TRY(readback(c, c->d_flags, 4, &f));
+  if (f) {
+    const char* why = (f & FLAG_BAD_FRAME)    ? "frame id >= n_frames"
+                      : (f & FLAG_BAD_KEY)    ? "raw frame key with reserved kind 0xFFFFFFFF"
+                      : (f & FLAG_TOO_DEEP)   ? "call path deeper than DC_MAX_DEPTH"
+                      : (f & FLAG_BAD_LEAF)   ? "leaf / launch_leaf entry is not a node of the tree"
+                      : (f & FLAG_BAD_OFFSETS)? "record offsets are not non-decreasing"
+                                              : "internal error";
+    return fail(c, DC_ERR_TRACE, "malformed trace (flags 0x%x): %s", f, why);
+  }
+  return DC_OK;
+}
+
+__global__ void k_add_diag(unsigned long long* dst, const unsigned long long* src) {
+  if (threadIdx.x < DG_N) dst[threadIdx.x] += src[threadIdx.x];
+}
+
+dc_status add_diag(Ctx* c, const unsigned long long* src_dev) {
+  k_add_diag<<<1, 32, 0, c->stream>>>((unsigned long long*)c->d_diag, src_dev);
+  DC_LAUNCHED(c);
+  return DC_OK;
+}
+
+}  // namespace dc
+
+using namespace dc;
+
+#define CHECK_CTX(ctx) \
+  if (!(ctx)) return DC_ERR_ARG
+#define ARG(cond, ...)                                     \
+  do {                                                     \
+    if (!(cond)) return fail(ctx, DC_ERR_ARG, __VA_ARGS__); \
+  } while (0)
+#define ON_DEVICE(ctx) DC_CUDA(ctx, cudaSetDevice((ctx)->device))
+
+extern "C" {
+
+dc_status dc_ctx_create(int device, void* cuda_stream, dc_ctx** out) {
+  if (!out) return DC_ERR_ARG;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    cudaGetLastError();
+    return DC_ERR_CUDA;
+  }
+  dc_ctx* ctx = new dc_ctx();
+  ctx->device = device;
+  if (cudaSetDevice(device) != cudaSuccess) {
+    delete ctx;
+    return DC_ERR_CUDA;
+  }
+  if (cuda_stream) {
+    ctx->stream = (cudaStream_t)cuda_stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete ctx;
+      return DC_ERR_CUDA;
+    }
+    ctx->own_stream = true;
+  }
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, device);
+  ctx->num_sms = prop.multiProcessorCount;
+  if (const char* w = getenv("DC_TEST_WEAK_HASH")) {  // test-only fault injection (collision paths)
+    int b = atoi(w);
+    if (b > 0 && b < 64) ctx->hash_mask = (1ull << b) - 1ull;
+  }
+  ctx->smem_optin = prop.sharedMemPerBlockOptin;
+  // keep freed pool memory cached (stream-ordered allocations are reused across calls)
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  if (cudaMalloc(&ctx->d_flags, 4) != cudaSuccess || cudaMalloc(&ctx->d_diag, DG_N * 8) != cudaSuccess ||
+      cudaMallocHost(&ctx->h_pinned, 4096) != cudaSuccess) {
+    cudaGetLastError();
+    delete ctx;
+    return DC_ERR_OOM;
+  }
+  cudaMemsetAsync(ctx->d_flags, 0, 4, ctx->stream);
+  cudaMemsetAsync(ctx->d_diag, 0, DG_N * 8, ctx->stream);
+  cudaStreamSynchronize(ctx->stream);
+  *out = ctx;
+  return DC_OK;
+}
+
+dc_status dc_ctx_sync(dc_ctx* ctx) {
+  CHECK_CTX(ctx);
+  ON_DEVICE(ctx);
+  DC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return check_flags(ctx);
+}
+
+dc_status dc_ctx_diag(dc_ctx* ctx, dc_diag* out_h) {
+  CHECK_CTX(ctx);
+  ARG(out_h, "out_h is NULL");
+  ON_DEVICE(ctx);
+  uint64_t d[DG_N];
+  DC_TRY(readback(ctx, ctx->d_diag, sizeof d, d));
+  out_h->empty_paths = d[DG_EMPTY];
+  out_h->samples_bad_launch = d[DG_BAD_LAUNCH];
+  out_h->samples_bad_stall = d[DG_BAD_STALL];
+  out_h->samples_zero_count = d[DG_ZERO];
+  out_h->collisions_detected = d[DG_COLL] + ctx->host_collisions;
+  out_h->levels_built = ctx->host_levels;
+  out_h->max_depth_seen = d[DG_MAXDEPTH];
+  out_h->bytes_moved_est = ctx->bytes_host;
+  return DC_OK;
+}
+
+void dc_ctx_destroy(dc_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  cudaFree(ctx->d_flags);
+  cudaFree(ctx->d_diag);
+  cudaFreeHost(ctx->h_pinned);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* dc_last_error(const dc_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+uint64_t dc_ctx_launch_count(const dc_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+dc_status dc_ctx_set_timing(dc_ctx* ctx, int on) {
+  CHECK_CTX(ctx);
+  ctx->timing = on != 0;
+  return DC_OK;
+}
+
+dc_status dc_ctx_timer_report(dc_ctx* ctx, char* buf, size_t len) {
+  CHECK_CTX(ctx);
+  ARG(buf && len, "buf is NULL");
+  ON_DEVICE(ctx);
+  DC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  std::vector<std::string> names;
+  std::vector<double> tot;
+  std::vector<uint64_t> cnt;
+  for (auto& t : ctx->timed) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, t.a, t.b);
+    size_t i = 0;
+    while (i < names.size() && names[i] != t.name) ++i;
+    if (i == names.size()) {
+      names.push_back(t.name);
+      tot.push_back(0);
+      cnt.push_back(0);
+    }
+    tot[i] += ms;
+    cnt[i] += 1;
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  ctx->timed.clear();
+  std::string s;
+  char line[256];
+  for (size_t i = 0; i < names.size(); ++i) {
+    snprintf(line, sizeof line, "%s %llu %.6f\n", names[i].c_str(), (unsigned long long)cnt[i], tot[i]);
+    s += line;
+  }
+  snprintf(buf, len, "%s", s.c_str());
+  return DC_OK;
+}
+
+dc_status dc_intern_frames(dc_ctx* ctx, const dc_frame_key* keys, uint64_t n, uint32_t* out_ids, dc_dict** out_dict) {
+  CHECK_CTX(ctx);
+  ARG(out_dict, "out_dict is NULL");
+  ARG(n == 0 || (keys && out_ids), "keys/out_ids must be device pointers when n > 0");
+  ARG(((uintptr_t)keys & 15) == 0, "keys must be 16-byte aligned");
+  ON_DEVICE(ctx);
+  Region rg(ctx, "intern");
+  return intern_frames(ctx, keys, n, out_ids, out_dict);
+}
+
+dc_status dc_dict_from_sorted(dc_ctx* ctx, const dc_frame_key* keys, uint64_t D, dc_dict** out_dict) {
+  CHECK_CTX(ctx);
+  ARG(out_dict && (D == 0 || keys), "bad arguments");
+  ON_DEVICE(ctx);
+  return dict_from_sorted(ctx, keys, D, out_dict);
+}
+
+uint64_t dc_dict_size(const dc_dict* d) { return d ? d->D : 0; }
+
+dc_status dc_dict_arrays(const dc_dict* d, const dc_frame_key** keys_dev, const uint8_t** kinds_dev) {
+  if (!d) return DC_ERR_ARG;
+  if (keys_dev) *keys_dev = d->keys;
+  if (kinds_dev) *kinds_dev = d->kinds;
+  return DC_OK;
+}
+
+void dc_dict_free(dc_dict* d) {
+  if (!d) return;
+  cudaSetDevice(d->device);
+  cudaFree(d->keys);
+  cudaFree(d->kinds);
+  delete d;
+}
+
+dc_status dc_cct_build(dc_ctx* ctx, const dc_paths* paths, const dc_dict* dict, uint32_t n_frames, uint32_t* out_leaf,
+                       dc_cct** out) {
+  CHECK_CTX(ctx);
+  ARG(paths && out, "paths/out is NULL");
+  ARG(paths->offsets, "paths->offsets is NULL");
+  ARG(paths->n_records == 0 || paths->frames || true, "");
+  ARG(!dict || dict->D == n_frames, "dictionary size %llu != n_frames %u", (unsigned long long)(dict ? dict->D : 0), n_frames);
+  ARG(n_frames < 0xFFFFFFFFu, "n_frames must be < 2^32-1");
+  ON_DEVICE(ctx);
+  Region rg(ctx, "build");
+  return cct_build(ctx, paths, dict, n_frames, out_leaf, out);
+}
+
+dc_status dc_cct_attribute_metrics(dc_ctx* ctx, dc_cct* cct, const uint32_t* leaf, uint64_t n_records, const uint64_t* metrics,
+                                   uint32_t M, uint64_t ld) {
+  CHECK_CTX(ctx);
+  ARG(cct, "cct is NULL");
+  ARG(M > 0 && M <= 64, "M must be in [1, 64]");
+  ARG(n_records == 0 || (leaf && metrics), "leaf/metrics must be device pointers");
+  ARG(ld >= n_records, "ld < n_records");
+  ON_DEVICE(ctx);
+  Region rg(ctx, "attribute");
+  return attribute_metrics(ctx, cct, leaf, n_records, metrics, M, ld);
+}
+
+dc_status dc_cct_rollup(dc_ctx* ctx, dc_cct* cct) {
+  CHECK_CTX(ctx);
+  ARG(cct, "cct is NULL");
+  ON_DEVICE(ctx);
+  Region rg(ctx, "rollup");
+  return rollup(ctx, cct);
+}
+
+dc_status dc_pc_sample_attribute(dc_ctx* ctx, dc_cct* cct, const dc_pc_sample* s, uint64_t n, const uint32_t* launch_leaf,
+                                 uint64_t n_launch, const uint64_t* launch_sample_off, uint32_t n_stall) {
+  CHECK_CTX(ctx);
+  ARG(cct, "cct is NULL");
+  ARG(n_stall >= 1 && n_stall <= DC_MAX_STALL, "n_stall must be in [1, %u]", DC_MAX_STALL);
+  ARG(n == 0 || s, "samples pointer is NULL");
+  ARG(n_launch == 0 || launch_leaf, "launch_leaf is NULL");
+  ARG(((uintptr_t)s & 15) == 0, "samples must be 16-byte aligned");
+  if (cct->pc_done) return fail(ctx, DC_ERR_STATE, "dc_pc_sample_attribute already called on this tree");
+  ON_DEVICE(ctx);
+  Region rg(ctx, "pc");
+  return pc_attribute(ctx, cct, s, n, launch_leaf, n_launch, launch_sample_off, n_stall);
+}
+
+dc_status dc_hotspots_topk(dc_ctx* ctx, const dc_cct* cct, dc_view view, uint32_t metric, uint32_t kind_mask, double threshold,
+                           uint32_t k, uint32_t stall_node, dc_topk_entry* out_h, uint32_t* n_out_h) {
+  CHECK_CTX(ctx);
+  ARG(cct && n_out_h && (k == 0 || out_h), "bad arguments");
+  ON_DEVICE(ctx);
+  Region rg(ctx, "topk");
+  return hotspots_topk(ctx, cct, view, metric, kind_mask, threshold, k, stall_node, out_h, n_out_h);
+}
+
+dc_status dc_cct_derived(dc_ctx* ctx, const dc_cct* cct, uint32_t metric, int incl, double* out_mean, double* out_std) {
+  CHECK_CTX(ctx);
+  ARG(cct && out_mean && out_std, "bad arguments");
+  ON_DEVICE(ctx);
+  return derived(ctx, cct, metric, incl, out_mean, out_std);
+}
+
+dc_status dc_cct_view_get(const dc_cct* t, dc_cct_view* v) {
+  if (!t || !v) return DC_ERR_ARG;
+  memset(v, 0, sizeof *v);
+  v->n_nodes = t->N;
+  v->n_pc_nodes = t->Npc;
+  v->n_bins = t->Nbins;
+  v->n_records = t->R;
+  v->n_metrics = t->M;
+  v->n_stall = t->S;
+  v->max_depth = t->max_depth;
+  v->n_frames = t->n_frames;
+  v->parent = t->parent;
+  v->frame = t->frame;
+  v->depth = t->depth;
+  v->level_off = t->level_off;
+  v->xcnt = t->xcnt;
+  v->icnt = t->icnt;
+  if (t->mcols) {
+    v->xsum = t->col(C_XSUM, 0);
+    v->xmin = t->col(C_XMIN, 0);
+    v->xsq_lo = t->col(C_XSQLO, 0);
+    v->xsq_hi = t->col(C_XSQHI, 0);
+    v->isum = t->col(C_ISUM, 0);
+    v->imin = t->col(C_IMIN, 0);
+    v->isq_lo = t->col(C_ISQLO, 0);
+    v->isq_hi = t->col(C_ISQHI, 0);
+  }
+  v->xsamples = t->xsamples;
+  v->isamples = t->isamples;
+  v->xstall = t->xstall;
+  v->istall = t->istall;
+  v->pc_ctx = t->pc_ctx;
+  v->pc_off = t->pc_off;
+  v->bin_pcnode = t->bin_pcnode;
+  v->bin_stall = t->bin_stall;
+  v->bin_count = t->bin_count;
+  v->state = t->state;
+  return DC_OK;
+}
+
+void dc_cct_free(dc_cct* t) {
+  if (!t) return;
+  cudaSetDevice(t->device);
+  void* ps[] = {t->parent, t->frame, t->level_off, t->depth, t->frame_kind, t->xcnt, t->icnt, t->mcols, t->xsamples,
+                t->isamples, t->xstall, t->istall, t->pc_ctx, t->pc_off, t->bin_pcnode, t->bin_stall, t->bin_count};
+  cudaDeviceSynchronize();
+  for (void* p : ps)
+    if (p) cudaFree(p);
+  delete t;
+}
+
+}  // extern "C"

@@ -1,0 +1,209 @@
+// columns.cu — a4 exclusive attribution, a5 inclusive rollup, a8 derived floats.
+//
+// a4: record r's metrics go to node leaf[r]: count, sum, min and the
+//    128-bit sum of squares, with integer atomics (order-independent, so deterministic).
+// a5: incl = excl (+) excl of all descendants. Implemented as the paper
+//    states it, in bulk: every node holding exclusive content pushes it to each ancestor on
+//    its path to the root (one thread per (node, column group); integer atomics), which
+//    needs no per-level barrier — depth-256 trees cost one launch.
+// a8: mean/std from the exact integers with single roundings (reading R18).
+#include "prim.cuh"
+
+namespace dc {
+
+__global__ void k_fill_u64(uint64_t* a, uint64_t n, uint64_t v) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) a[i] = v;
+}
+
+__global__ void k_attribute(const uint32_t* __restrict__ leaf, uint64_t R, const uint64_t* __restrict__ X, uint32_t M,
+                            uint64_t ld, uint64_t N, unsigned long long* __restrict__ xcnt, unsigned long long* __restrict__ mcols,
+                            uint32_t* d_flags) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < R; r += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t n = leaf[r];
+    if (n >= N) {
+      atomicOr(d_flags, FLAG_BAD_LEAF);
+      continue;
+    }
+    atomicAdd(xcnt + n, 1ull);
+    for (uint32_t m = 0; m < M; ++m) {
+      uint64_t x = X[m * ld + r];
+      atomicAdd(mcols + ((uint64_t)C_XSUM * M + m) * N + n, (unsigned long long)x);
+      atomicMin(mcols + ((uint64_t)C_XMIN * M + m) * N + n, (unsigned long long)x);
+      uint64_t sq_lo = x * x, sq_hi = __umul64hi(x, x);
+      atomic_add_u128(mcols + ((uint64_t)C_XSQLO * M + m) * N + n, mcols + ((uint64_t)C_XSQHI * M + m) * N + n, sq_lo, sq_hi);
+    }
+  }
+}
+
+dc_status ensure_metric_cols(Ctx* c, dc_cct* t, uint32_t M) {
+  if (t->mcols) {
+    if (t->M != M) return fail(c, DC_ERR_ARG, "metric count %u differs from the first call's %u", M, t->M);
+    return DC_OK;
+  }
+  t->M = M;
+  const uint64_t N = t->N;
+  DC_TRY(palloc(c, t->mcols, (uint64_t)8 * M * N));
+  DC_CUDA(c, cudaMemsetAsync(t->mcols, 0, (uint64_t)8 * M * N * 8, c->stream));
+  for (uint32_t m = 0; m < M; ++m) {
+    k_fill_u64<<<grid_for(c, N, 256), 256, 0, c->stream>>>(t->col(C_XMIN, m), N, ~0ull);
+    DC_LAUNCHED(c);
+    k_fill_u64<<<grid_for(c, N, 256), 256, 0, c->stream>>>(t->col(C_IMIN, m), N, ~0ull);
+    DC_LAUNCHED(c);
+  }
+  return DC_OK;
+}
+
+dc_status attribute_metrics(Ctx* c, dc_cct* t, const uint32_t* leaf, uint64_t R, const uint64_t* X, uint32_t M, uint64_t ld) {
+  DC_TRY(ensure_metric_cols(c, t, M));
+  if (R) {
+    k_attribute<<<grid_for(c, R, 256), 256, 0, c->stream>>>(leaf, R, X, M, ld, t->N, (unsigned long long*)t->xcnt,
+                                                            (unsigned long long*)t->mcols, c->d_flags);
+    DC_LAUNCHED(c);
+  }
+  t->state = 1;
+  c->bytes_host += 8ull * M * R + 4 * R + (8 + 32ull * M) * t->N;
+  return DC_OK;
+}
+
+// --------------------------------------------------------------------------- a5 rollup
+// column groups: 0 = count; 1..M = metric m-1 (sum, min, sq); M+1 = samples; M+2+s = stall s
+__global__ void k_push(const uint32_t* __restrict__ parent, uint64_t N, uint32_t M, uint32_t S, uint32_t G,
+                       const uint64_t* __restrict__ xcnt, unsigned long long* __restrict__ icnt,
+                       unsigned long long* __restrict__ mcols, const uint64_t* __restrict__ xsamples,
+                       unsigned long long* __restrict__ isamples, const uint64_t* __restrict__ xstall,
+                       unsigned long long* __restrict__ istall) {
+  const uint64_t total = (N - 1) * (uint64_t)G;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t n = 1 + t / G;
+    const uint32_t g = (uint32_t)(t % G);
+    if (g == 0) {
+      uint64_t v = xcnt[n];
+      if (!v) continue;
+      for (uint32_t a = parent[n];; a = parent[a]) {
+        atomicAdd(icnt + a, (unsigned long long)v);
+        if (a == 0) break;
+      }
+    } else if (g <= M) {
+      if (!xcnt[n]) continue;
+      const uint32_t m = g - 1;
+      uint64_t s = mcols[((uint64_t)C_XSUM * M + m) * N + n];
+      uint64_t mn = mcols[((uint64_t)C_XMIN * M + m) * N + n];
+      uint64_t qlo = mcols[((uint64_t)C_XSQLO * M + m) * N + n];
+      uint64_t qhi = mcols[((uint64_t)C_XSQHI * M + m) * N + n];
+      for (uint32_t a = parent[n];; a = parent[a]) {
+        if (s) atomicAdd(mcols + ((uint64_t)C_ISUM * M + m) * N + a, (unsigned long long)s);
+        atomicMin(mcols + ((uint64_t)C_IMIN * M + m) * N + a, (unsigned long long)mn);
+        if (qlo | qhi)
+          atomic_add_u128(mcols + ((uint64_t)C_ISQLO * M + m) * N + a, mcols + ((uint64_t)C_ISQHI * M + m) * N + a, qlo, qhi);
+        if (a == 0) break;
+      }
+    } else if (g == M + 1) {
+      uint64_t v = xsamples[n];
+      if (!v) continue;
+      for (uint32_t a = parent[n];; a = parent[a]) {
+        atomicAdd(isamples + a, (unsigned long long)v);
+        if (a == 0) break;
+      }
+    } else {
+      const uint32_t s = g - M - 2;
+      uint64_t v = xstall[(uint64_t)s * N + n];
+      if (!v) continue;
+      for (uint32_t a = parent[n];; a = parent[a]) {
+        atomicAdd(istall + (uint64_t)s * N + a, (unsigned long long)v);
+        if (a == 0) break;
+      }
+    }
+  }
+}
+
+dc_status rollup(Ctx* c, dc_cct* t) {
+  const uint64_t N = t->N;
+  const uint32_t M = t->M, S = t->S;
+  cudaStream_t s = c->stream;
+  DC_CUDA(c, cudaMemcpyAsync(t->icnt, t->xcnt, N * 8, cudaMemcpyDeviceToDevice, s));
+  for (uint32_t m = 0; m < M; ++m) {
+    DC_CUDA(c, cudaMemcpyAsync(t->col(C_ISUM, m), t->col(C_XSUM, m), N * 8, cudaMemcpyDeviceToDevice, s));
+    DC_CUDA(c, cudaMemcpyAsync(t->col(C_IMIN, m), t->col(C_XMIN, m), N * 8, cudaMemcpyDeviceToDevice, s));
+    DC_CUDA(c, cudaMemcpyAsync(t->col(C_ISQLO, m), t->col(C_XSQLO, m), N * 8, cudaMemcpyDeviceToDevice, s));
+    DC_CUDA(c, cudaMemcpyAsync(t->col(C_ISQHI, m), t->col(C_XSQHI, m), N * 8, cudaMemcpyDeviceToDevice, s));
+  }
+  if (t->xsamples) {
+    DC_CUDA(c, cudaMemcpyAsync(t->isamples, t->xsamples, N * 8, cudaMemcpyDeviceToDevice, s));
+    DC_CUDA(c, cudaMemcpyAsync(t->istall, t->xstall, (uint64_t)S * N * 8, cudaMemcpyDeviceToDevice, s));
+  }
+  if (N > 1) {
+    const uint32_t G = 1 + M + (t->xsamples ? 1 + S : 0);
+    k_push<<<grid_for(c, (N - 1) * G, 256, 16), 256, 0, s>>>(t->parent, N, M, S, G, t->xcnt, (unsigned long long*)t->icnt,
+                                                             (unsigned long long*)t->mcols, t->xsamples,
+                                                             (unsigned long long*)t->isamples, t->xstall,
+                                                             (unsigned long long*)t->istall);
+    DC_LAUNCHED(c);
+  }
+  t->state = 2;
+  c->bytes_host += (2 * (8 + 32ull * M) + 4) * N;
+  return DC_OK;
+}
+
+// --------------------------------------------------------------------------- a8 derived
+// u192 -> double, round to nearest even: normalise the top 64 bits, fold the rest into a
+// sticky bit at bit 0 (below the rounding position), convert with __ull2double_rn, scale.
+__device__ double u192_to_double_rn(uint64_t w2, uint64_t w1, uint64_t w0) {
+  if (w2) {
+    int lz = __clzll(w2);
+    uint64_t top = lz ? (w2 << lz) | (w1 >> (64 - lz)) : w2;
+    uint64_t rest1 = lz ? (w1 << lz) : w1;
+    uint64_t sticky = (rest1 | w0) ? 1u : 0u;
+    return scalbn(__ull2double_rn(top | sticky), 128 - lz);
+  }
+  if (w1) {
+    int lz = __clzll(w1);
+    uint64_t top = lz ? (w1 << lz) | (w0 >> (64 - lz)) : w1;
+    uint64_t sticky = (lz ? (w0 << lz) : w0) ? 1u : 0u;
+    return scalbn(__ull2double_rn(top | sticky), 64 - lz);
+  }
+  return __ull2double_rn(w0);
+}
+
+__global__ void k_derived(const uint64_t* __restrict__ cnt, const uint64_t* __restrict__ sum, const uint64_t* __restrict__ sq_lo,
+                          const uint64_t* __restrict__ sq_hi, uint64_t N, double* __restrict__ mean, double* __restrict__ stdv) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < N; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t n = cnt[i];
+    if (!n) {
+      mean[i] = 0.0;
+      stdv[i] = 0.0;
+      continue;
+    }
+    uint64_t s = sum[i], ql = sq_lo[i], qh = sq_hi[i];
+    double dn = __ull2double_rn(n);
+    mean[i] = __ddiv_rn(__ull2double_rn(s), dn);
+    // n * (qh:ql) -> 192 bits
+    uint64_t p0l = n * ql, p0h = __umul64hi(n, ql);
+    uint64_t p1l = n * qh, p1h = __umul64hi(n, qh);
+    uint64_t w0 = p0l;
+    uint64_t w1 = p0h + p1l;
+    uint64_t w2 = p1h + (w1 < p0h ? 1u : 0u);
+    // minus s^2 (128 bits)
+    uint64_t s2l = s * s, s2h = __umul64hi(s, s);
+    uint64_t b0 = w0 < s2l ? 1u : 0u;
+    w0 -= s2l;
+    uint64_t sub1 = s2h + b0;
+    uint64_t b1 = (w1 < sub1 || (b0 && sub1 == 0)) ? 1u : 0u;
+    w1 -= sub1;
+    w2 -= b1;
+    double D = u192_to_double_rn(w2, w1, w0);
+    stdv[i] = __ddiv_rn(__dsqrt_rn(D), dn);
+  }
+}
+
+dc_status derived(Ctx* c, const dc_cct* t, uint32_t metric, int incl, double* mean, double* stdv) {
+  if (metric >= t->M) return fail(c, DC_ERR_ARG, "metric %u >= M = %u", metric, t->M);
+  if (incl && t->state != 2) return fail(c, DC_ERR_STATE, "inclusive derived values need dc_cct_rollup first");
+  const uint64_t* cnt = incl ? t->icnt : t->xcnt;
+  k_derived<<<grid_for(c, t->N, 256), 256, 0, c->stream>>>(cnt, t->col(incl ? C_ISUM : C_XSUM, metric),
+                                                           t->col(incl ? C_ISQLO : C_XSQLO, metric),
+                                                           t->col(incl ? C_ISQHI : C_XSQHI, metric), t->N, mean, stdv);
+  DC_LAUNCHED(c);
+  return DC_OK;
+}
+
+}  // namespace dc

@@ -1,0 +1,233 @@
+// common.cuh — context, handles, error plumbing and small device helpers of libdc.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string>
+#include <vector>
+
+#include "../../include/dc.h"
+
+namespace dc {
+
+// device-side data-error flag bits (reported as DC_ERR_TRACE)
+enum : uint32_t {
+  FLAG_BAD_FRAME = 1u,      // frame id >= n_frames
+  FLAG_BAD_KEY = 2u,        // raw key with reserved kind
+  FLAG_TOO_DEEP = 4u,       // path longer than DC_MAX_DEPTH
+  FLAG_BAD_LEAF = 8u,       // launch_leaf / leaf entry not a node
+  FLAG_BAD_OFFSETS = 16u,   // offsets not monotone
+  FLAG_INTERNAL = 0x80000000u,
+};
+
+// device diag slots
+enum { DG_EMPTY = 0, DG_BAD_LAUNCH, DG_BAD_STALL, DG_ZERO, DG_COLL, DG_LEVELS, DG_MAXDEPTH, DG_BYTES, DG_N };
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+  uint32_t* d_flags = nullptr;   // [1]
+  uint64_t* d_diag = nullptr;    // [DG_N]
+  uint64_t* h_pinned = nullptr;  // small pinned readback buffer
+  int num_sms = 148;
+  size_t smem_optin = 0;
+  uint64_t launches = 0;
+  uint64_t bytes_host = 0;       // host-accumulated algorithmic bytes
+  uint64_t host_levels = 0;      // tree levels built
+  uint64_t host_collisions = 0;  // path-hash collisions resolved exactly
+  uint64_t hash_mask = ~0ull;    // fault injection: DC_TEST_WEAK_HASH=bits shortens path hashes
+  // optional CUDA-event timers (dc_ctx_set_timing): (name, start, stop) per timed region
+  bool timing = false;
+  struct Timed { const char* name; cudaEvent_t a, b; };
+  std::vector<Timed> timed;
+};
+
+// RAII CUDA-event timer of a region on the context stream (no-op unless timing is on)
+struct Region {
+  Ctx* c;
+  const char* name;
+  cudaEvent_t a = nullptr;
+  Region(Ctx* ctx, const char* n) : c(ctx), name(n) {
+    if (c->timing) {
+      cudaEventCreate(&a);
+      cudaEventRecord(a, c->stream);
+    }
+  }
+  ~Region() {
+    if (c->timing && a) {
+      cudaEvent_t b;
+      cudaEventCreate(&b);
+      cudaEventRecord(b, c->stream);
+      c->timed.push_back({name, a, b});
+    }
+  }
+};
+
+}  // namespace dc
+
+struct dc_ctx : dc::Ctx {};
+
+struct dc_dict {
+  int device = 0;
+  uint64_t D = 0;
+  dc_frame_key* keys = nullptr;  // dev [D]
+  uint8_t* kinds = nullptr;      // dev [D]
+};
+
+struct dc_cct {
+  int device = 0;
+  uint64_t N = 0, Npc = 0, Nbins = 0, R = 0;
+  uint32_t M = 0, S = 0, max_depth = 0, n_frames = 0;
+  int state = 0;  // 0 BUILT, 1 DIRTY, 2 ROLLED
+  bool pc_done = false;
+  // structure
+  uint32_t *parent = nullptr, *frame = nullptr, *level_off = nullptr;
+  uint16_t* depth = nullptr;
+  uint8_t* frame_kind = nullptr;  // dev [n_frames] or null
+  // columns (one allocation each group)
+  uint64_t *xcnt = nullptr, *icnt = nullptr;
+  uint64_t* mcols = nullptr;  // [8][M][N]: xsum,xmin,xsq_lo,xsq_hi,isum,imin,isq_lo,isq_hi
+  uint64_t *xsamples = nullptr, *isamples = nullptr, *xstall = nullptr, *istall = nullptr;
+  uint32_t *pc_ctx = nullptr, *pc_off = nullptr, *bin_pcnode = nullptr;
+  uint16_t* bin_stall = nullptr;
+  uint64_t* bin_count = nullptr;
+  uint64_t* col(int which, uint32_t m) const { return mcols + ((uint64_t)which * M + m) * N; }
+};
+enum { C_XSUM = 0, C_XMIN, C_XSQLO, C_XSQHI, C_ISUM, C_IMIN, C_ISQLO, C_ISQHI };
+
+namespace dc {
+
+#define DC_TRY(expr)                      \
+  do {                                    \
+    dc_status _s = (expr);                \
+    if (_s != DC_OK) return _s;           \
+  } while (0)
+
+dc_status cuda_fail(Ctx* c, cudaError_t e, const char* what);
+dc_status fail(Ctx* c, dc_status s, const char* fmt, ...);
+
+#define DC_CUDA(ctx, expr)                                           \
+  do {                                                               \
+    cudaError_t _e = (expr);                                         \
+    if (_e != cudaSuccess) return ::dc::cuda_fail((ctx), _e, #expr); \
+  } while (0)
+
+// after a kernel launch: count it and check the launch error
+#define DC_LAUNCHED(ctx)                                                         \
+  do {                                                                           \
+    (ctx)->launches++;                                                           \
+    cudaError_t _e = cudaGetLastError();                                         \
+    if (_e != cudaSuccess) return ::dc::cuda_fail((ctx), _e, "kernel launch");   \
+  } while (0)
+
+// stream-ordered device allocation (memory pool); RAII buffer
+template <class T>
+struct Buf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  Buf() = default;
+  Buf(const Buf&) = delete;
+  Buf& operator=(const Buf&) = delete;
+  ~Buf() { release(); }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  T* release_ownership() {
+    T* q = p;
+    p = nullptr;
+    n = 0;
+    return q;
+  }
+};
+
+template <class T>
+dc_status alloc(Ctx* c, Buf<T>& b, size_t n) {
+  b.release();
+  b.s = c->stream;
+  b.n = n;
+  if (n == 0) n = 1;
+  cudaError_t e = cudaMallocAsync((void**)&b.p, n * sizeof(T), c->stream);
+  if (e != cudaSuccess) {
+    b.p = nullptr;
+    cudaGetLastError();
+    return fail(c, DC_ERR_OOM, "device allocation of %zu bytes failed: %s", n * sizeof(T), cudaGetErrorString(e));
+  }
+  return DC_OK;
+}
+template <class T>
+dc_status alloc_zero(Ctx* c, Buf<T>& b, size_t n) {
+  DC_TRY(alloc(c, b, n));
+  DC_CUDA(c, cudaMemsetAsync(b.p, 0, (n ? n : 1) * sizeof(T), c->stream));
+  return DC_OK;
+}
+// persistent (handle-owned) allocation
+template <class T>
+dc_status palloc(Ctx* c, T*& p, size_t n) {
+  cudaError_t e = cudaMallocAsync((void**)&p, (n ? n : 1) * sizeof(T), c->stream);
+  if (e != cudaSuccess) {
+    p = nullptr;
+    cudaGetLastError();
+    return fail(c, DC_ERR_OOM, "device allocation of %zu bytes failed", n * sizeof(T));
+  }
+  return DC_OK;
+}
+
+// synchronous small readback through the pinned buffer
+dc_status readback(Ctx* c, const void* dev, size_t bytes, void* host);
+dc_status check_flags(Ctx* c);  // synchronizes; DC_ERR_TRACE if a flag is set
+dc_status add_diag(Ctx* c, const unsigned long long* src_dev);  // d_diag[i] += src[i], i < DG_N
+
+inline int grid_for(Ctx* c, uint64_t work, int per_block, int waves = 8) {
+  uint64_t g = (work + per_block - 1) / per_block;
+  uint64_t cap = (uint64_t)c->num_sms * waves;
+  if (g > cap) g = cap;
+  return g ? (int)g : 1;
+}
+
+inline int bits_for(uint64_t v) {  // bits needed to represent values < v+1 (0 -> 0)
+  int b = 0;
+  while (b < 64 && (v >> b)) ++b;
+  return b;
+}
+
+// ---------------------------------------------------------------- device helpers
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z ^= z >> 31;
+  z *= 0x7FB5D329728EA185ull;
+  z ^= z >> 27;
+  z *= 0x81DADEF4BC2DD44Dull;
+  z ^= z >> 33;
+  return z;
+}
+// 16-B relaxed load at GPU scope (sees other CTAs' atomics; not guaranteed single-copy atomic,
+// callers treat a half-empty result as "possibly torn" and resolve it with atomicCAS)
+__device__ __forceinline__ ulonglong2 ld_relaxed_v2(const ulonglong2* p) {
+  ulonglong2 v;
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// 128-bit add into (lo, hi) device words with exact carry
+__device__ __forceinline__ void atomic_add_u128(unsigned long long* lo, unsigned long long* hi, uint64_t add_lo,
+                                                uint64_t add_hi) {
+  unsigned long long old = atomicAdd(lo, (unsigned long long)add_lo);
+  uint64_t carry = (old + add_lo) < old ? 1u : 0u;
+  if (add_hi + carry) atomicAdd(hi, (unsigned long long)(add_hi + carry));
+}
+
+}  // namespace dc

@@ -1,0 +1,214 @@
+// intern.cu — a1: frame interning (§4.2 frame identity/unification).
+//
+// K1 insert: one raw 16-B key per thread (vector load), open-addressing table of 16-B slots
+//    in L2, read-first probing so repeated keys (the common case: a few hundred distinct
+//    frames among tens of millions of entries) cost one L2 read, 128-bit atomicCAS only to
+//    claim an empty slot. Emits the slot of each key into out_ids (reused as scratch).
+// K2 canon: compact the D occupied slots, stable LSD radix sort by (addr) then
+//    (kind<<32|str_id) -> lexicographic rank; slot -> rank table.
+// K3 remap: out_ids[j] = rank[slot[j]].
+#include "prim.cuh"
+
+namespace dc {
+
+static constexpr uint64_t EMPTY = ~0ull;
+
+__device__ __forceinline__ uint64_t key_lo(const dc_frame_key& k) { return (uint64_t)k.kind | ((uint64_t)k.str_id << 32); }
+
+__global__ void k_intern_insert(const dc_frame_key* __restrict__ keys, uint64_t n, ulonglong2* table, uint64_t mask,
+                                uint32_t* __restrict__ out_slot, unsigned long long* d_count, uint32_t* d_overflow,
+                                uint32_t* d_flags) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
+    ulonglong2 kv = __ldg(reinterpret_cast<const ulonglong2*>(keys) + j);  // 16-B coalesced load
+    const uint64_t lo = kv.x, hi = kv.y;                                    // lo = kind | str<<32, hi = addr
+    if ((uint32_t)lo == 0xFFFFFFFFu) {
+      atomicOr(d_flags, FLAG_BAD_KEY);
+      out_slot[j] = 0;
+      continue;
+    }
+    uint64_t h = mix64(lo ^ mix64(hi + 0x9E3779B97F4A7C15ull));
+    uint64_t s = h & mask;
+    uint32_t found = 0xFFFFFFFFu;
+    for (uint64_t probe = 0; probe <= mask; ++probe, s = (s + 1) & mask) {
+      ulonglong2 cur = ld_relaxed_v2(table + s);
+      if (cur.x == lo && cur.y == hi && hi != EMPTY) { found = (uint32_t)s; break; }
+      bool maybe_partial = ((uint32_t)cur.x == 0xFFFFFFFFu) || cur.y == EMPTY;  // empty, or a torn read of a claim
+      if (!maybe_partial) continue;                                          // a different, fully written key
+      unsigned __int128 expect = ((unsigned __int128)EMPTY << 64) | EMPTY;
+      unsigned __int128 want = ((unsigned __int128)hi << 64) | lo;
+      unsigned __int128 old = atomicCAS(reinterpret_cast<unsigned __int128*>(table + s), expect, want);
+      if (old == expect) {
+        atomicAdd(d_count, 1ull);
+        found = (uint32_t)s;
+        break;
+      }
+      if ((uint64_t)old == lo && (uint64_t)(old >> 64) == hi) { found = (uint32_t)s; break; }
+    }
+    if (found == 0xFFFFFFFFu) {
+      atomicOr(d_overflow, 1u);
+      found = 0;
+    }
+    out_slot[j] = found;
+  }
+}
+
+__global__ void k_intern_compact(const ulonglong2* __restrict__ table, uint64_t cap, uint64_t* __restrict__ addr_key,
+                                 uint64_t* __restrict__ ks_key, uint32_t* __restrict__ slot_of, unsigned int* d_pos,
+                                 unsigned long long* d_max) {
+  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < cap; s += (uint64_t)gridDim.x * blockDim.x) {
+    ulonglong2 cur = table[s];
+    if ((uint32_t)cur.x == 0xFFFFFFFFu) continue;
+    unsigned p = atomicAdd(d_pos, 1u);
+    addr_key[p] = cur.y;
+    uint32_t kind = (uint32_t)cur.x, str = (uint32_t)(cur.x >> 32);
+    ks_key[p] = ((uint64_t)kind << 32) | str;
+    slot_of[p] = (uint32_t)s;
+    atomicMax(&d_max[0], (unsigned long long)cur.y);
+    atomicMax(&d_max[1], (unsigned long long)ks_key[p]);
+  }
+}
+
+__global__ void k_gather_u64(const uint64_t* __restrict__ src, const uint32_t* __restrict__ idx, uint64_t* __restrict__ dst,
+                             uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = src[idx[i]];
+}
+
+// rank r -> dictionary key; slot -> rank
+__global__ void k_intern_rank(const uint32_t* __restrict__ order, const uint32_t* __restrict__ slot_of,
+                              const ulonglong2* __restrict__ table, uint32_t* __restrict__ rank_of_slot,
+                              dc_frame_key* __restrict__ dict, uint8_t* __restrict__ kinds, uint64_t D) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < D; r += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t s = slot_of[order[r]];
+    rank_of_slot[s] = (uint32_t)r;
+    ulonglong2 cur = table[s];
+    dc_frame_key k;
+    k.kind = (uint32_t)cur.x;
+    k.str_id = (uint32_t)(cur.x >> 32);
+    k.addr = cur.y;
+    dict[r] = k;
+    kinds[r] = (uint8_t)(k.kind < 255 ? k.kind : 255);
+  }
+}
+
+__global__ void k_intern_remap(uint32_t* ids, uint64_t n, const uint32_t* __restrict__ rank_of_slot) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x)
+    ids[j] = rank_of_slot[ids[j]];
+}
+
+__global__ void k_iota(uint32_t* a, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    a[i] = (uint32_t)i;
+}
+
+__global__ void k_kinds_of(const dc_frame_key* __restrict__ dict, uint8_t* kinds, uint64_t D) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < D; i += (uint64_t)gridDim.x * blockDim.x)
+    kinds[i] = (uint8_t)(dict[i].kind < 255 ? dict[i].kind : 255);
+}
+
+static uint64_t next_pow2(uint64_t v) {
+  uint64_t p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+dc_status intern_frames(Ctx* c, const dc_frame_key* keys, uint64_t n, uint32_t* out_ids, dc_dict** out) {
+  dc_dict* d = new dc_dict();
+  d->device = c->device;
+  *out = nullptr;
+  if (n == 0) {
+    d->D = 0;
+    DC_TRY(palloc(c, d->keys, 1));
+    DC_TRY(palloc(c, d->kinds, 1));
+    *out = d;
+    return DC_OK;
+  }
+  if (n >= (1ull << 32)) {
+    delete d;
+    return fail(c, DC_ERR_CAPACITY, "dc_intern_frames: n >= 2^32 keys");
+  }
+  Buf<ulonglong2> table;
+  Buf<unsigned long long> cnt;
+  Buf<uint32_t> ovf;
+  uint64_t cap = next_pow2(2 * (n < (1ull << 20) ? n : (1ull << 20)));
+  if (cap < 1024) cap = 1024;
+  uint64_t D = 0;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    DC_TRY(alloc(c, table, cap));
+    DC_CUDA(c, cudaMemsetAsync(table.p, 0xFF, cap * sizeof(ulonglong2), c->stream));
+    DC_TRY(alloc_zero(c, cnt, 1));
+    DC_TRY(alloc_zero(c, ovf, 1));
+    k_intern_insert<<<grid_for(c, n, 256), 256, 0, c->stream>>>(keys, n, table.p, cap - 1, out_ids, cnt.p, ovf.p,
+                                                                 c->d_flags);
+    DC_LAUNCHED(c);
+    uint64_t h[2];
+    DC_TRY(readback(c, cnt.p, 8, &h[0]));
+    DC_TRY(readback(c, ovf.p, 4, &h[1]));
+    D = h[0];
+    bool overflow = (uint32_t)h[1] != 0;
+    if (!overflow && D * 2 <= cap) break;
+    if (attempt == 1) {
+      delete d;
+      return fail(c, DC_ERR_CAPACITY, "dc_intern_frames: hash table overflow");
+    }
+    cap = next_pow2(2 * n);
+    if (cap < 1024) cap = 1024;
+  }
+  d->D = D;
+  Buf<uint64_t> ka, kb, ka2;
+  Buf<uint32_t> slot_of, ord0, ord1, rank_of_slot;
+  Buf<unsigned long long> mx;
+  Buf<unsigned int> pos;
+  DC_TRY(alloc(c, ka, D));
+  DC_TRY(alloc(c, kb, D));
+  DC_TRY(alloc(c, ka2, D));
+  DC_TRY(alloc(c, slot_of, D));
+  DC_TRY(alloc(c, ord0, D));
+  DC_TRY(alloc(c, ord1, D));
+  DC_TRY(alloc(c, rank_of_slot, cap));
+  DC_TRY(alloc_zero(c, mx, 2));
+  DC_TRY(alloc_zero(c, pos, 1));
+  k_intern_compact<<<grid_for(c, cap, 256), 256, 0, c->stream>>>(table.p, cap, ka.p, kb.p, slot_of.p, pos.p, mx.p);
+  DC_LAUNCHED(c);
+  uint64_t mxh[2];
+  DC_TRY(readback(c, mx.p, 16, mxh));
+  k_iota<<<grid_for(c, D, 256), 256, 0, c->stream>>>(ord0.p, D);
+  DC_LAUNCHED(c);
+  // LSD: by addr, then (stable) by kind<<32|str  ==> lexicographic (kind, str_id, addr)
+  bool in1 = false;
+  DC_TRY(radix_sort_pairs(c, ka.p, ord0.p, ka2.p, ord1.p, D, 0, bits_for(mxh[0]), &in1));
+  uint32_t* ord = in1 ? ord1.p : ord0.p;
+  uint32_t* ord_alt = in1 ? ord0.p : ord1.p;
+  k_gather_u64<<<grid_for(c, D, 256), 256, 0, c->stream>>>(kb.p, ord, ka.p, D);  // ka <- kb[ord]
+  DC_LAUNCHED(c);
+  bool in1b = false;
+  DC_TRY(radix_sort_pairs(c, ka.p, ord, ka2.p, ord_alt, D, 0, bits_for(mxh[1]), &in1b));
+  uint32_t* final_ord = in1b ? ord_alt : ord;
+  DC_TRY(palloc(c, d->keys, D));
+  DC_TRY(palloc(c, d->kinds, D));
+  k_intern_rank<<<grid_for(c, D, 256), 256, 0, c->stream>>>(final_ord, slot_of.p, table.p, rank_of_slot.p, d->keys,
+                                                            d->kinds, D);
+  DC_LAUNCHED(c);
+  k_intern_remap<<<grid_for(c, n, 256), 256, 0, c->stream>>>(out_ids, n, rank_of_slot.p);
+  DC_LAUNCHED(c);
+  c->bytes_host += 20 * n + 16 * D;
+  *out = d;
+  return DC_OK;
+}
+
+dc_status dict_from_sorted(Ctx* c, const dc_frame_key* keys, uint64_t D, dc_dict** out) {
+  dc_dict* d = new dc_dict();
+  d->device = c->device;
+  d->D = D;
+  DC_TRY(palloc(c, d->keys, D));
+  DC_TRY(palloc(c, d->kinds, D));
+  if (D) {
+    DC_CUDA(c, cudaMemcpyAsync(d->keys, keys, D * sizeof(dc_frame_key), cudaMemcpyDeviceToDevice, c->stream));
+    k_kinds_of<<<grid_for(c, D, 256), 256, 0, c->stream>>>(d->keys, d->kinds, D);
+    DC_LAUNCHED(c);
+  }
+  *out = d;
+  return DC_OK;
+}
+
+}  // namespace dc

@@ -1,0 +1,248 @@
+// pc.cu — a6: PC-sampling attribution ("extend the call path by inserting the
+// PC of each instruction collected"; stall reasons PAPER.md:414-416).
+//
+// Output: PC nodes = distinct (ctx, pc_off), ids N + rank in (ctx, pc_off) order; bins
+// (pc node, stall, count) sorted; per-ctx exclusive samples / stall[s] columns.
+//
+// Generic schedule (any sample order): every valid sample updates its (ctx, pc, stall) bin
+// in an L2-resident open-addressing table (16-B keys, u64 counts, read-first probing). The
+// distinct bins are then compacted, radix-sorted into canonical order and run-length
+// encoded into PC nodes. The context-owner schedule (pc_owner.cu) replaces the table pass
+// when per-launch sample offsets are given.
+#include "prim.cuh"
+
+namespace dc {
+
+dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, const uint32_t* launch_leaf,
+                        uint64_t n_launch, const uint64_t* launch_off, uint32_t S, uint64_t* keys_out_dev,
+                        uint64_t* cnt_out_dev, uint64_t* n_bins_out, int* handled);
+
+__device__ __forceinline__ void block_diag_add(unsigned long long* d_diag, uint32_t bad_l, uint32_t bad_s, uint32_t zero) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    bad_l += __shfl_xor_sync(0xffffffffu, bad_l, o);
+    bad_s += __shfl_xor_sync(0xffffffffu, bad_s, o);
+    zero += __shfl_xor_sync(0xffffffffu, zero, o);
+  }
+  if (lane_id() == 0) {
+    if (bad_l) atomicAdd(d_diag + DG_BAD_LAUNCH, (unsigned long long)bad_l);
+    if (bad_s) atomicAdd(d_diag + DG_BAD_STALL, (unsigned long long)bad_s);
+    if (zero) atomicAdd(d_diag + DG_ZERO, (unsigned long long)zero);
+  }
+}
+
+// key layout in the table: x = (ctx << 32) | pc_off, y = stall; EMPTY = all ones
+__global__ void k_pc_table(const dc_pc_sample* __restrict__ smp, uint64_t n, const uint32_t* __restrict__ launch_leaf,
+                           uint64_t n_launch, uint32_t S, uint64_t N, ulonglong2* table, unsigned long long* tcnt,
+                           uint64_t mask, unsigned int* d_distinct, unsigned int* d_overflow, unsigned long long* d_diag,
+                           uint32_t* d_flags) {
+  uint32_t bad_l = 0, bad_s = 0, zero = 0;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
+    uint4 q = __ldg(reinterpret_cast<const uint4*>(smp) + j);  // {launch, pc_off, stall|flags<<16, count}
+    const uint32_t launch = q.x, pc = q.y, stall = q.z & 0xFFFFu, count = q.w;
+    if (launch >= n_launch) { ++bad_l; continue; }
+    if (stall >= S) { ++bad_s; continue; }
+    if (count == 0) { ++zero; continue; }
+    const uint32_t ctx = __ldg(launch_leaf + launch);
+    if (ctx >= N) { atomicOr(d_flags, FLAG_BAD_LEAF); continue; }
+    const uint64_t kx = ((uint64_t)ctx << 32) | pc, ky = stall;
+    uint64_t s = mix64(kx * 0x9E3779B97F4A7C15ull + ky) & mask;
+    bool done = false;
+    for (uint64_t probe = 0; probe <= mask; ++probe, s = (s + 1) & mask) {
+      ulonglong2 cur = ld_relaxed_v2(table + s);
+      if (cur.x == kx && cur.y == ky) { done = true; break; }
+      if (cur.x != ~0ull && cur.y != ~0ull) continue;
+      unsigned __int128 expect = ~(unsigned __int128)0;
+      unsigned __int128 want = ((unsigned __int128)ky << 64) | kx;
+      unsigned __int128 old = atomicCAS(reinterpret_cast<unsigned __int128*>(table + s), expect, want);
+      if (old == expect) { atomicAdd(d_distinct, 1u); done = true; break; }
+      if (old == want) { done = true; break; }
+    }
+    if (!done) { atomicOr(d_overflow, 1u); continue; }
+    atomicAdd(tcnt + s, (unsigned long long)count);
+  }
+  block_diag_add(d_diag, bad_l, bad_s, zero);
+}
+
+// compact the table into (sort key, count) with key = ((ctx << pcb | pc) << 5) | stall
+__global__ void k_pc_compact(const ulonglong2* __restrict__ table, const unsigned long long* __restrict__ tcnt, uint64_t cap,
+                             int pcb, uint64_t* __restrict__ keys, uint64_t* __restrict__ cnts, unsigned int* d_pos) {
+  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < cap; s += (uint64_t)gridDim.x * blockDim.x) {
+    ulonglong2 cur = table[s];
+    if (cur.x == ~0ull) continue;
+    unsigned p = atomicAdd(d_pos, 1u);
+    uint64_t ctx = cur.x >> 32, pc = cur.x & 0xFFFFFFFFull;
+    keys[p] = (((ctx << pcb) | pc) << 5) | cur.y;
+    cnts[p] = tcnt[s];
+  }
+}
+
+__global__ void k_pc_maxpc(const ulonglong2* __restrict__ table, uint64_t cap, unsigned int* d_max) {
+  uint32_t m = 0;
+  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < cap; s += (uint64_t)gridDim.x * blockDim.x) {
+    ulonglong2 cur = table[s];
+    if (cur.x != ~0ull) m = max(m, (uint32_t)cur.x);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane_id() == 0 && m) atomicMax(d_max, m);
+}
+
+__global__ void k_iota32(uint32_t* a, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) a[i] = (uint32_t)i;
+}
+
+// heads of (ctx, pc) runs among sorted bins
+__global__ void k_pc_heads(const uint64_t* __restrict__ keys, uint64_t nb, uint32_t* __restrict__ head) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nb; i += (uint64_t)gridDim.x * blockDim.x)
+    head[i] = (i == 0 || (keys[i - 1] >> 5) != (keys[i] >> 5)) ? 1u : 0u;
+}
+
+__global__ void k_pc_emit(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ order, const uint64_t* __restrict__ cnts,
+                          uint64_t nb, int pcb, const uint32_t* __restrict__ head, const uint32_t* __restrict__ run_excl,
+                          uint64_t N, uint64_t S, uint32_t* __restrict__ pc_ctx, uint32_t* __restrict__ pc_off,
+                          uint32_t* __restrict__ bin_pcnode, uint16_t* __restrict__ bin_stall, uint64_t* __restrict__ bin_count,
+                          unsigned long long* __restrict__ xsamples, unsigned long long* __restrict__ xstall) {
+  const uint64_t pcmask = (1ull << pcb) - 1ull;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nb; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t k = keys[i];
+    uint32_t stall = (uint32_t)(k & 31u);
+    uint64_t cp = k >> 5;
+    uint32_t ctx = (uint32_t)(cp >> pcb), pc = (uint32_t)(cp & pcmask);
+    uint32_t pidx = run_excl[i] + head[i] - 1u;
+    if (head[i]) {
+      pc_ctx[pidx] = ctx;
+      pc_off[pidx] = pc;
+    }
+    uint64_t cnt = cnts[order ? order[i] : i];
+    bin_pcnode[i] = (uint32_t)(N + pidx);
+    bin_stall[i] = (uint16_t)stall;
+    bin_count[i] = cnt;
+    atomicAdd(xsamples + ctx, (unsigned long long)cnt);
+    atomicAdd(xstall + (uint64_t)stall * N + ctx, (unsigned long long)cnt);
+  }
+}
+
+static uint64_t np2(uint64_t v) {
+  uint64_t p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+dc_status pc_attribute(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, const uint32_t* launch_leaf, uint64_t n_launch,
+                       const uint64_t* launch_off, uint32_t S) {
+  const uint64_t N = t->N;
+  t->S = S;
+  DC_TRY(palloc(c, t->xsamples, N));
+  DC_TRY(palloc(c, t->isamples, N));
+  DC_TRY(palloc(c, t->xstall, (uint64_t)S * N));
+  DC_TRY(palloc(c, t->istall, (uint64_t)S * N));
+  DC_CUDA(c, cudaMemsetAsync(t->xsamples, 0, N * 8, c->stream));
+  DC_CUDA(c, cudaMemsetAsync(t->isamples, 0, N * 8, c->stream));
+  DC_CUDA(c, cudaMemsetAsync(t->xstall, 0, (uint64_t)S * N * 8, c->stream));
+  DC_CUDA(c, cudaMemsetAsync(t->istall, 0, (uint64_t)S * N * 8, c->stream));
+  // -------- histogram into (sort key, count) pairs
+  Buf<uint64_t> keys, cnts, keys2;
+  uint64_t nb = 0;
+  int pcb = 32;
+  int handled = 0;
+  Buf<ulonglong2> table;
+  Buf<unsigned long long> tcnt;
+  if (launch_off) {
+    // context-owner schedule (pc_owner.cu); handled == 0 means "not applicable, use generic"
+    DC_TRY(pc_owner_hist(c, t, s, n, launch_leaf, n_launch, launch_off, S, nullptr, nullptr, &nb, &handled));
+    if (handled) {
+      t->pc_done = true;
+      t->state = 1;
+      c->bytes_host += 16 * n + 16 * nb + 8 * t->Npc;
+      return DC_OK;
+    }
+  }
+  if (!handled) {
+    uint64_t cap = np2(2 * (n < (1ull << 22) ? n : (1ull << 22)));
+    if (cap < 1024) cap = 1024;
+    Buf<unsigned int> ctr;
+    Buf<unsigned long long> ldiag;  // this call's diag counts (a retry recounts every sample)
+    for (int attempt = 0;; ++attempt) {
+      DC_TRY(alloc(c, table, cap));
+      DC_TRY(alloc_zero(c, tcnt, cap));
+      DC_TRY(alloc_zero(c, ctr, 4));
+      DC_TRY(alloc_zero(c, ldiag, DG_N));
+      DC_CUDA(c, cudaMemsetAsync(table.p, 0xFF, cap * 16, c->stream));
+      {
+        Region rk(c, "k:pc_table");
+        k_pc_table<<<grid_for(c, n, 256, 16), 256, 0, c->stream>>>(s, n, launch_leaf, n_launch, S, N, table.p, tcnt.p,
+                                                                    cap - 1, ctr.p, ctr.p + 1, ldiag.p, c->d_flags);
+      DC_LAUNCHED(c);
+      }
+      uint32_t h[2];
+      DC_TRY(readback(c, ctr.p, 8, h));
+      if (!h[1] && (uint64_t)h[0] * 2 <= cap) {
+        nb = h[0];
+        break;
+      }
+      if (attempt) return fail(c, DC_ERR_CAPACITY, "PC bin table overflow (%u distinct bins)", h[0]);
+      cap = np2(4 * (uint64_t)(h[0] > n ? h[0] : n));
+      if (cap > (1ull << 31)) return fail(c, DC_ERR_CAPACITY, "PC bin table would exceed 2^31 slots");
+    }
+    DC_TRY(add_diag(c, ldiag.p));
+    Buf<unsigned int> mx;
+    DC_TRY(alloc_zero(c, mx, 2));
+    k_pc_maxpc<<<grid_for(c, cap, 256), 256, 0, c->stream>>>(table.p, cap, mx.p);
+    DC_LAUNCHED(c);
+    uint32_t hm[2];
+    DC_TRY(readback(c, mx.p, 8, hm));
+    pcb = bits_for(hm[0]);
+    if (pcb == 0) pcb = 1;
+    if (bits_for(N > 1 ? N - 1 : 1) + pcb + 5 > 64)
+      return fail(c, DC_ERR_CAPACITY, "PC bin sort key exceeds 64 bits");
+    DC_TRY(alloc(c, keys, nb));
+    DC_TRY(alloc(c, cnts, nb));
+    k_pc_compact<<<grid_for(c, cap, 256), 256, 0, c->stream>>>(table.p, tcnt.p, cap, pcb, keys.p, cnts.p, mx.p + 1);
+    DC_LAUNCHED(c);
+    table.release();
+    tcnt.release();
+  } else {
+    return fail(c, DC_ERR_STATE, "internal: context-owner output not wired");
+  }
+  // -------- canonical order: sort bins by (ctx, pc, stall)
+  Buf<uint32_t> ord0, ord1, head, runs;
+  DC_TRY(alloc(c, keys2, nb));
+  DC_TRY(alloc(c, ord0, nb));
+  DC_TRY(alloc(c, ord1, nb));
+  k_iota32<<<grid_for(c, nb, 256), 256, 0, c->stream>>>(ord0.p, nb);
+  DC_LAUNCHED(c);
+  bool in1 = false;
+  const int kbits = bits_for(N > 1 ? N - 1 : 1) + pcb + 5;
+  DC_TRY(radix_sort_pairs(c, keys.p, ord0.p, keys2.p, ord1.p, nb, 0, kbits, &in1));
+  uint64_t* sk = in1 ? keys2.p : keys.p;
+  uint32_t* so = in1 ? ord1.p : ord0.p;
+  DC_TRY(alloc(c, head, nb));
+  DC_TRY(alloc(c, runs, nb));
+  k_pc_heads<<<grid_for(c, nb, 256), 256, 0, c->stream>>>(sk, nb, head.p);
+  DC_LAUNCHED(c);
+  Buf<uint32_t> npc;
+  DC_TRY(alloc(c, npc, 1));
+  DC_TRY(excl_scan<uint32_t>(c, head.p, runs.p, nb, npc.p));
+  uint32_t hnpc = 0;
+  DC_TRY(readback(c, npc.p, 4, &hnpc));
+  t->Npc = hnpc;
+  t->Nbins = nb;
+  DC_TRY(palloc(c, t->pc_ctx, hnpc));
+  DC_TRY(palloc(c, t->pc_off, hnpc));
+  DC_TRY(palloc(c, t->bin_pcnode, nb));
+  DC_TRY(palloc(c, t->bin_stall, nb));
+  DC_TRY(palloc(c, t->bin_count, nb));
+  if (nb) {
+    k_pc_emit<<<grid_for(c, nb, 256), 256, 0, c->stream>>>(sk, so, cnts.p, nb, pcb, head.p, runs.p, N, S, t->pc_ctx,
+                                                           t->pc_off, t->bin_pcnode, t->bin_stall, t->bin_count,
+                                                           (unsigned long long*)t->xsamples, (unsigned long long*)t->xstall);
+    DC_LAUNCHED(c);
+  }
+  t->pc_done = true;
+  t->state = 1;
+  c->bytes_host += 16 * n + 16 * nb + 8 * hnpc;
+  return DC_OK;
+}
+
+}  // namespace dc

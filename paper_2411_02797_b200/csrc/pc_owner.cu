@@ -1,0 +1,675 @@
+// pc_owner.cu — a6, context-owner schedule of the (context, pc, stall) histogram.
+//
+// When samples arrive contiguous per launch (launch_sample_off given, "flushes the metrics"
+// per activity buffer), launches are ordered by their context node and the
+// resulting ctx-ordered virtual sample stream is cut into num_SMs equal ranges, one
+// persistent CTA per SM:
+//   * one producer warp streams the range's launch segments into shared memory with TMA bulk
+//     copies (cp.async.bulk + mbarrier, 3 x 32 KB stages);
+//   * 16 consumer warps aggregate (pc_off, stall) -> count in a 16384-slot shared-memory hash
+//     table (32-bit keys/counts, native shared atomics), deduplicating equal keys inside each
+//     warp (__match_any_sync) first, so hot PCs cost one atomic per warp;
+//   * when the context changes (or the table passes 75 % load) the table is flushed once to a
+//     partial list in HBM: every bin is written once per (CTA, context) segment — no global
+//     atomics on bins, no L2 hash table.
+// k_own_reduce then merges each context's segments in shared memory (sort + reduce, stable
+// radix sort), producing canonical (pc, stall) order, PC node counts and the context's
+// exclusive samples / stall[s] totals; k_own_place writes the final SoA arrays.
+// Any sample this schedule cannot take (a valid launch that disagrees with its segment,
+// pc_off >= 2^27, a context whose partial list does not fit shared memory) makes the call
+// fall back to the generic schedule (pc.cu) for the whole input — same result, exact.
+#include "prim.cuh"
+
+namespace dc {
+
+constexpr int OW_CONS_WARPS = 16;
+constexpr int OW_CONS = 32 * OW_CONS_WARPS;  // 512 consumer threads
+constexpr int OW_THREADS = OW_CONS + 32;     // + producer warp
+constexpr int OW_STAGES = 3;
+constexpr int OW_STAGE = 2048;  // samples per stage (32 KB)
+constexpr int OW_TAB = 16384;   // shared hash table slots
+constexpr uint32_t OW_FLUSH = OW_TAB * 3 / 4;  // flush when distinct > this before a stage
+constexpr uint32_t EMPTY32 = 0xFFFFFFFFu;
+constexpr uint32_t OW_DONE = 0xFFFFFFFFu;
+
+enum { OWF_FALLBACK = 1, OWF_OVERFLOW = 2 };
+
+struct OwMeta {
+  uint32_t launch, ctx, count, pad;
+};
+
+struct OwnSmem {
+  uint4 stage[OW_STAGES][OW_STAGE];
+  uint32_t key[OW_TAB];
+  uint32_t cnt[OW_TAB];
+  unsigned long long full[OW_STAGES], empty[OW_STAGES];
+  OwMeta meta[OW_STAGES];
+  uint32_t distinct;
+  uint32_t warp_cnt[OW_CONS_WARPS];
+  unsigned long long seg_base;
+};
+
+// ---------------------------------------------------------------- PTX helpers (sm_90+)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void cons_sync() { asm volatile("bar.sync 1, %0;" ::"n"(OW_CONS) : "memory"); }
+
+// ---------------------------------------------------------------- prep kernels
+__global__ void k_own_check(const uint64_t* __restrict__ off, uint64_t n_launch, uint64_t n, uint32_t* bad) {
+  for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < n_launch; l += (uint64_t)gridDim.x * blockDim.x)
+    if (off[l + 1] < off[l]) atomicOr(bad, 1u);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (off[0] != 0 || off[n_launch] != n)) atomicOr(bad, 1u);
+}
+
+__global__ void k_own_keys(const uint32_t* __restrict__ leaf, uint64_t n_launch, uint64_t N, uint64_t* __restrict__ key,
+                           uint32_t* __restrict__ val) {
+  for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < n_launch; l += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t c = leaf[l];
+    key[l] = c < N ? c : N;
+    val[l] = (uint32_t)l;
+  }
+}
+
+__global__ void k_own_cnt(const uint64_t* __restrict__ off, const uint32_t* __restrict__ order, uint64_t n_launch,
+                          uint64_t* __restrict__ cnt) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n_launch; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t l = order[i];
+    cnt[i] = off[l + 1] - off[l];
+  }
+}
+
+// ---------------------------------------------------------------- main kernel
+struct OwnArgs {
+  const dc_pc_sample* smp;
+  const uint64_t* launch_off;  // [n_launch+1]
+  const uint32_t* order;       // launches sorted by ctx
+  const uint64_t* lkey;        // sorted ctx key per sorted launch (N = invalid)
+  const uint64_t* cum;         // [n_launch+1] exclusive scan of sorted launch sample counts
+  uint64_t n_launch, N, total;
+  uint32_t S;
+  uint32_t* pkey;              // partial entries: key
+  unsigned long long* pcnt;    //                  count
+  uint64_t cap_entries;
+  uint4* seg;                  // {ctx, n, base_lo, base_hi}
+  uint32_t cap_segs;
+  unsigned long long* g_entries;
+  unsigned int* g_segs;
+  uint32_t* g_flags;
+  uint32_t* trace_flags;       // ctx->d_flags (DC_ERR_TRACE conditions)
+  unsigned long long* ldiag;
+};
+
+__device__ __forceinline__ void own_flush(OwnSmem& sm, const OwnArgs& a, uint32_t ctx, uint32_t ctid) {
+  const uint32_t n = sm.distinct;
+  const uint32_t w = ctid >> 5, lane = ctid & 31;
+  if (ctid == 0) {
+    unsigned long long base = atomicAdd(a.g_entries, (unsigned long long)n);
+    unsigned si = atomicAdd(a.g_segs, 1u);
+    if (si < a.cap_segs && base + n <= a.cap_entries) {
+      a.seg[si] = make_uint4(ctx, n, (uint32_t)base, (uint32_t)(base >> 32));
+    } else {
+      atomicOr(a.g_flags, (uint32_t)OWF_OVERFLOW);
+      base = ~0ull;
+    }
+    sm.seg_base = base;
+  }
+  constexpr uint32_t PER_WARP = OW_TAB / OW_CONS_WARPS;
+  uint32_t c = 0;
+  for (uint32_t s = w * PER_WARP + lane; s < (w + 1) * PER_WARP; s += 32) c += __popc(__ballot_sync(0xffffffffu, sm.key[s] != EMPTY32));
+  if (lane == 0) sm.warp_cnt[w] = c;
+  cons_sync();
+  const unsigned long long base = sm.seg_base;
+  uint32_t pos = 0;
+  for (uint32_t ww = 0; ww < w; ++ww) pos += sm.warp_cnt[ww];
+  for (uint32_t s0 = w * PER_WARP; s0 < (w + 1) * PER_WARP; s0 += 32) {
+    const uint32_t s = s0 + lane;
+    const uint32_t k = sm.key[s];
+    const bool occ = k != EMPTY32;
+    const uint32_t m = __ballot_sync(0xffffffffu, occ);
+    if (occ && base != ~0ull) {
+      const unsigned long long o = base + pos + __popc(m & lanemask_lt());
+      a.pkey[o] = k;
+      a.pcnt[o] = sm.cnt[s];
+    }
+    pos += __popc(m);
+    sm.key[s] = EMPTY32;
+    sm.cnt[s] = 0;
+  }
+  cons_sync();
+  if (ctid == 0) sm.distinct = 0;
+  cons_sync();
+}
+
+__device__ __forceinline__ void own_insert(OwnSmem& sm, const OwnArgs& a, uint32_t key, uint32_t add, uint32_t ctx) {
+  uint32_t h = (key * 0x9E3779B1u) >> (32 - 14);  // log2(OW_TAB) = 14
+  volatile uint32_t* vk = sm.key;
+  while (true) {
+    uint32_t k = vk[h];
+    if (k == key) break;
+    if (k == EMPTY32) {
+      uint32_t old = atomicCAS(&sm.key[h], EMPTY32, key);
+      if (old == EMPTY32) {
+        atomicAdd(&sm.distinct, 1u);
+        break;
+      }
+      if (old == key) break;
+    }
+    h = (h + 1) & (OW_TAB - 1);
+  }
+  uint32_t old = atomicAdd(&sm.cnt[h], add);
+  if (old + add < old) {  // 32-bit wrap: emit the 2^32 carry as its own one-entry segment
+    unsigned long long base = atomicAdd(a.g_entries, 1ull);
+    unsigned si = atomicAdd(a.g_segs, 1u);
+    if (si < a.cap_segs && base + 1 <= a.cap_entries) {
+      a.pkey[base] = key;
+      a.pcnt[base] = 1ull << 32;
+      a.seg[si] = make_uint4(ctx, 1u, (uint32_t)base, (uint32_t)(base >> 32));
+    } else {
+      atomicOr(a.g_flags, (uint32_t)OWF_OVERFLOW);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  OwnSmem& sm = *reinterpret_cast<OwnSmem*>(smem_raw);
+  const uint32_t tid = threadIdx.x;
+  // range of this CTA in the ctx-ordered virtual stream
+  const uint64_t G = gridDim.x;
+  const uint64_t r0 = a.total * blockIdx.x / G, r1 = a.total * (blockIdx.x + 1) / G;
+  for (uint32_t s = tid; s < OW_TAB; s += OW_THREADS) {
+    sm.key[s] = EMPTY32;
+    sm.cnt[s] = 0;
+  }
+  if (tid == 0) {
+    for (int s = 0; s < OW_STAGES; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], OW_CONS_WARPS);
+    }
+    sm.distinct = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid < 32) {
+    // ------------------------------------------------ producer warp (lane 0 issues)
+    if (tid == 0) {
+      // first sorted launch whose segment contains r0: largest i with cum[i] <= r0
+      uint64_t lo = 0, hi = a.n_launch;
+      while (lo < hi) {
+        uint64_t mid = (lo + hi + 1) >> 1;
+        if (a.cum[mid] <= r0) lo = mid;
+        else hi = mid - 1;
+      }
+      uint64_t i = lo, pos = r0;
+      uint32_t st = 0, ph = 0;
+      while (pos < r1) {
+        const uint64_t seg_end = a.cum[i + 1];
+        if (seg_end <= pos) {
+          ++i;
+          continue;
+        }
+        const uint32_t l = a.order[i];
+        uint64_t chunk = seg_end - pos;
+        if (r1 - pos < chunk) chunk = r1 - pos;
+        if (chunk > OW_STAGE) chunk = OW_STAGE;
+        mbar_wait(&sm.empty[st], ph ^ 1u);
+        const uint64_t key = a.lkey[i];
+        sm.meta[st] = OwMeta{l, (uint32_t)key, (uint32_t)chunk, 0};
+        const dc_pc_sample* src = a.smp + a.launch_off[l] + (pos - a.cum[i]);
+        mbar_expect_tx(&sm.full[st], (uint32_t)chunk * 16u);
+        tma_bulk_g2s(&sm.stage[st][0], src, (uint32_t)chunk * 16u, &sm.full[st]);
+        pos += chunk;
+        if (pos == seg_end) ++i;
+        if (++st == OW_STAGES) {
+          st = 0;
+          ph ^= 1u;
+        }
+      }
+      mbar_wait(&sm.empty[st], ph ^ 1u);
+      sm.meta[st] = OwMeta{0, OW_DONE, 0, 0};
+      mbar_arrive(&sm.full[st]);
+    }
+    return;
+  }
+  // -------------------------------------------------- consumer warps
+  const uint32_t ctid = tid - 32, lane = ctid & 31;
+  uint32_t cur_ctx = OW_DONE, st = 0, ph = 0;
+  uint32_t bad_l = 0, bad_s = 0, zero = 0, fallback = 0;
+  while (true) {
+    mbar_wait(&sm.full[st], ph);
+    const OwMeta m = sm.meta[st];
+    cons_sync();  // every consumer finished the previous stage
+    if (m.ctx == OW_DONE) break;
+    if (sm.distinct > 0 && (m.ctx != cur_ctx || sm.distinct > OW_FLUSH)) own_flush(sm, a, cur_ctx, ctid);
+    cur_ctx = m.ctx;
+    const bool ctx_ok = m.ctx < a.N;
+    for (uint32_t j0 = 0; j0 < m.count; j0 += OW_CONS) {
+      const uint32_t j = j0 + ctid;
+      uint32_t key = EMPTY32, c = 0;
+      bool valid = false;
+      if (j < m.count) {
+        const uint4 q = sm.stage[st][j];
+        const uint32_t stall = q.z & 0xFFFFu;
+        c = q.w;
+        if (q.x >= a.n_launch) ++bad_l;
+        else if (q.x != m.launch) fallback = 1;  // misplaced sample: generic schedule
+        else if (stall >= a.S) ++bad_s;
+        else if (c == 0) ++zero;
+        else if (!ctx_ok) atomicOr(a.trace_flags, (uint32_t)FLAG_BAD_LEAF);
+        else if (q.y >= (1u << 27)) fallback = 1;
+        else {
+          key = (q.y << 5) | stall;
+          valid = key != EMPTY32;
+          if (!valid) fallback = 1;
+        }
+      }
+      const uint32_t peers = __match_any_sync(0xffffffffu, key);
+      const bool ones = __all_sync(0xffffffffu, !valid || c == 1);
+      if (valid) {
+        if (ones) {
+          if ((peers & lanemask_lt()) == 0) own_insert(sm, a, key, __popc(peers), m.ctx);
+        } else {
+          own_insert(sm, a, key, c, m.ctx);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[st]);
+    if (++st == OW_STAGES) {
+      st = 0;
+      ph ^= 1u;
+    }
+  }
+  if (sm.distinct > 0) own_flush(sm, a, cur_ctx, ctid);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    bad_l += __shfl_xor_sync(0xffffffffu, bad_l, o);
+    bad_s += __shfl_xor_sync(0xffffffffu, bad_s, o);
+    zero += __shfl_xor_sync(0xffffffffu, zero, o);
+    fallback |= __shfl_xor_sync(0xffffffffu, fallback, o);
+  }
+  if (lane == 0) {
+    if (bad_l) atomicAdd(a.ldiag + DG_BAD_LAUNCH, (unsigned long long)bad_l);
+    if (bad_s) atomicAdd(a.ldiag + DG_BAD_STALL, (unsigned long long)bad_s);
+    if (zero) atomicAdd(a.ldiag + DG_ZERO, (unsigned long long)zero);
+    if (fallback) atomicOr(a.g_flags, (uint32_t)OWF_FALLBACK);
+  }
+}
+
+// ---------------------------------------------------------------- per-context reduce
+constexpr int RD_THREADS = 1024;
+constexpr uint32_t RD_CAP = 12288;  // entries of one context sorted in shared memory
+
+struct RedSmem {
+  uint32_t k[2][RD_CAP];
+  uint32_t v[2][RD_CAP];
+  uint32_t wcnt[32][256];
+  unsigned long long stall_tot[32];
+};
+
+// groups: per context, segments [gs, ge) in seg_sorted (by ctx)
+__global__ void __launch_bounds__(RD_THREADS, 1) k_own_reduce(
+    const uint4* __restrict__ seg, const uint32_t* __restrict__ seg_order, const uint32_t* __restrict__ grp_start,
+    uint32_t n_groups, const uint64_t* __restrict__ grp_out, const uint32_t* __restrict__ pkey,
+    const unsigned long long* __restrict__ pcnt, int kbits, uint64_t N, uint32_t* __restrict__ okey,
+    unsigned long long* __restrict__ ocnt, uint32_t* __restrict__ g_nbins, uint32_t* __restrict__ g_npcs,
+    uint32_t* __restrict__ g_ctx, unsigned long long* __restrict__ xsamples, unsigned long long* __restrict__ xstall,
+    uint32_t S, uint32_t* g_flags) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  RedSmem& sm = *reinterpret_cast<RedSmem*>(smem_raw);
+  const uint32_t tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  for (uint32_t g = blockIdx.x; g < n_groups; g += gridDim.x) {
+    const uint32_t gs = grp_start[g], ge = grp_start[g + 1];
+    const uint32_t ctx = seg[seg_order[gs]].x;
+    // gather (key, global index) of all entries of this context
+    uint32_t n = 0;
+    bool too_big = false;
+    for (uint32_t si = gs; si < ge; ++si) {
+      const uint4 sg = seg[seg_order[si]];
+      const uint64_t base = (uint64_t)sg.z | ((uint64_t)sg.w << 32);
+      if (n + sg.y > RD_CAP) {
+        too_big = true;
+        break;
+      }
+      for (uint32_t j = tid; j < sg.y; j += RD_THREADS) {
+        sm.k[0][n + j] = pkey[base + j];
+        sm.v[0][n + j] = (uint32_t)(base + j);
+      }
+      n += sg.y;
+    }
+    if (too_big) {
+      if (tid == 0) atomicOr(g_flags, (uint32_t)OWF_FALLBACK);
+      __syncthreads();
+      continue;
+    }
+    if (tid < 32) sm.stall_tot[tid] = 0;
+    __syncthreads();
+    // stable LSD radix sort of (key, index) by the key's kbits significant bits
+    int cur = 0;
+    const uint32_t per_warp = (n + 31) / 32;
+    for (int shift = 0; shift < kbits; shift += 8) {
+      const int nb = kbits - shift < 8 ? kbits - shift : 8;
+      const uint32_t mask = (1u << nb) - 1u;
+      for (int i = tid; i < 32 * 256; i += RD_THREADS) (&sm.wcnt[0][0])[i] = 0;
+      __syncthreads();
+      const uint32_t b0 = w * per_warp, b1 = min(n, b0 + per_warp);
+      for (uint32_t base = b0; base < b1; base += 32) {
+        const uint32_t j = base + lane;
+        const bool ok = j < b1;
+        const uint32_t d = ok ? (sm.k[cur][j] >> shift) & mask : 0xFFFFFFFFu;
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        if (ok && (peers & lanemask_lt()) == 0) sm.wcnt[w][d] += __popc(peers);
+        __syncwarp();
+      }
+      __syncthreads();
+      uint32_t tot = 0;
+      if (tid < 256)
+        for (int ww = 0; ww < 32; ++ww) tot += sm.wcnt[ww][tid];
+      const uint32_t ex = block_excl_scan<uint32_t, RD_THREADS>(tid < 256 ? tot : 0u, nullptr);
+      if (tid < 256) {
+        uint32_t run = ex;
+        for (int ww = 0; ww < 32; ++ww) {
+          const uint32_t c = sm.wcnt[ww][tid];
+          sm.wcnt[ww][tid] = run;
+          run += c;
+        }
+      }
+      __syncthreads();
+      for (uint32_t base = b0; base < b1; base += 32) {
+        const uint32_t j = base + lane;
+        const bool ok = j < b1;
+        const uint32_t kk = ok ? sm.k[cur][j] : 0, vv = ok ? sm.v[cur][j] : 0;
+        const uint32_t d = ok ? (kk >> shift) & mask : 0xFFFFFFFFu;
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t pos = ok ? sm.wcnt[w][d] + __popc(peers & lanemask_lt()) : 0;
+        __syncwarp();
+        if (ok && (peers & lanemask_lt()) == 0) sm.wcnt[w][d] += __popc(peers);
+        __syncwarp();
+        if (ok) {
+          sm.k[cur ^ 1][pos] = kk;
+          sm.v[cur ^ 1][pos] = vv;
+        }
+      }
+      __syncthreads();
+      cur ^= 1;
+    }
+    // reduce runs of equal keys: heads, then per-head sum over the run (runs are short)
+    const uint64_t obase = grp_out[g];
+    uint32_t n_out = 0, n_pc = 0;
+    for (uint32_t base = 0; base < n; base += RD_THREADS) {
+      const uint32_t j = base + tid;
+      const bool ok = j < n;
+      const uint32_t kk = ok ? sm.k[cur][j] : 0;
+      const uint32_t head = ok && (j == 0 || sm.k[cur][j - 1] != kk) ? 1u : 0u;
+      const uint32_t pchead = ok && (j == 0 || (sm.k[cur][j - 1] >> 5) != (kk >> 5)) ? 1u : 0u;
+      uint32_t tot_h, tot_p;
+      const uint32_t ex = block_excl_scan<uint32_t, RD_THREADS>(head, &tot_h);
+      block_excl_scan<uint32_t, RD_THREADS>(pchead, &tot_p);
+      if (head) {
+        unsigned long long s = 0;
+        for (uint32_t t = j; t < n && sm.k[cur][t] == kk; ++t) s += pcnt[sm.v[cur][t]];
+        okey[obase + n_out + ex] = kk;
+        ocnt[obase + n_out + ex] = s;
+        atomicAdd(&sm.stall_tot[kk & 31u], s);
+      }
+      n_out += tot_h;
+      n_pc += tot_p;
+      __syncthreads();
+    }
+    if (tid == 0) {
+      g_nbins[g] = n_out;
+      g_npcs[g] = n_pc;
+      g_ctx[g] = ctx;
+    }
+    if (tid < S && ctx < N) xstall[(uint64_t)tid * N + ctx] = sm.stall_tot[tid];
+    if (tid == 0 && ctx < N) {
+      unsigned long long s = 0;
+      for (uint32_t q = 0; q < S; ++q) s += sm.stall_tot[q];
+      xsamples[ctx] = s;
+    }
+    __syncthreads();
+  }
+}
+
+// final SoA: one block per group
+__global__ void k_own_place(const uint64_t* __restrict__ grp_out, const uint32_t* __restrict__ g_nbins,
+                            const uint32_t* __restrict__ bin_base, const uint32_t* __restrict__ pc_base,
+                            const uint32_t* __restrict__ g_ctx, uint32_t n_groups, const uint32_t* __restrict__ okey,
+                            const unsigned long long* __restrict__ ocnt, uint64_t N, uint32_t* __restrict__ pc_ctx,
+                            uint32_t* __restrict__ pc_off, uint32_t* __restrict__ bin_pcnode, uint16_t* __restrict__ bin_stall,
+                            uint64_t* __restrict__ bin_count) {
+  for (uint32_t g = blockIdx.x; g < n_groups; g += gridDim.x) {
+    const uint64_t ib = grp_out[g];
+    const uint32_t nb = g_nbins[g], ob = bin_base[g], pb = pc_base[g], ctx = g_ctx[g];
+    uint32_t run = 0;  // pc index carried across chunks
+    for (uint32_t base = 0; base < nb; base += blockDim.x) {
+      const uint32_t j = base + threadIdx.x;
+      const bool ok = j < nb;
+      const uint32_t kk = ok ? okey[ib + j] : 0;
+      const uint32_t pchead = ok && (j == 0 || (okey[ib + j - 1] >> 5) != (kk >> 5)) ? 1u : 0u;
+      uint32_t tot;
+      const uint32_t ex = block_excl_scan<uint32_t, 256>(pchead, &tot);
+      if (ok) {
+        const uint32_t pidx = pb + run + ex + pchead - 1u;
+        if (pchead) {
+          pc_ctx[pidx] = ctx;
+          pc_off[pidx] = kk >> 5;
+        }
+        bin_pcnode[ob + j] = (uint32_t)(N + pidx);
+        bin_stall[ob + j] = (uint16_t)(kk & 31u);
+        bin_count[ob + j] = ocnt[ib + j];
+      }
+      run += tot;
+    }
+  }
+}
+
+__global__ void k_own_groups(const uint64_t* __restrict__ skey, uint32_t n, uint32_t* __restrict__ head) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    head[i] = (i == 0 || skey[i - 1] != skey[i]) ? 1u : 0u;
+}
+__global__ void k_own_gstart(const uint32_t* __restrict__ head, const uint32_t* __restrict__ hex, uint32_t n,
+                             uint32_t* __restrict__ grp_start, uint32_t n_groups) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    if (head[i]) grp_start[hex[i]] = i;
+  if (blockIdx.x == 0 && threadIdx.x == 0) grp_start[n_groups] = n;
+}
+__global__ void k_own_segkeys(const uint4* __restrict__ seg, uint32_t n, uint64_t* __restrict__ key, uint32_t* __restrict__ val,
+                              uint64_t* __restrict__ gsz_in) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    key[i] = seg[i].x;
+    val[i] = i;
+  }
+}
+__global__ void k_own_gsize(const uint4* __restrict__ seg, const uint32_t* __restrict__ order, const uint32_t* __restrict__ grp_start,
+                            uint32_t n_groups, uint64_t* __restrict__ gsz) {
+  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < n_groups; g += gridDim.x * blockDim.x) {
+    uint64_t s = 0;
+    for (uint32_t i = grp_start[g]; i < grp_start[g + 1]; ++i) s += seg[order[i]].y;
+    gsz[g] = s;
+  }
+}
+
+dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, const uint32_t* launch_leaf,
+                        uint64_t n_launch, const uint64_t* launch_off, uint32_t S, uint64_t*, uint64_t*,
+                        uint64_t* n_bins_out, int* handled) {
+  *handled = 0;
+  if (n == 0 || n_launch == 0 || n_launch >= (1ull << 31)) return DC_OK;
+  const uint64_t N = t->N;
+  Buf<uint32_t> bad;
+  DC_TRY(alloc_zero(c, bad, 1));
+  k_own_check<<<grid_for(c, n_launch, 256), 256, 0, c->stream>>>(launch_off, n_launch, n, bad.p);
+  DC_LAUNCHED(c);
+  // launches ordered by context
+  Buf<uint64_t> k0, k1, cum;
+  Buf<uint32_t> v0, v1;
+  DC_TRY(alloc(c, k0, n_launch));
+  DC_TRY(alloc(c, k1, n_launch));
+  DC_TRY(alloc(c, v0, n_launch));
+  DC_TRY(alloc(c, v1, n_launch));
+  DC_TRY(alloc(c, cum, n_launch + 1));
+  k_own_keys<<<grid_for(c, n_launch, 256), 256, 0, c->stream>>>(launch_leaf, n_launch, N, k0.p, v0.p);
+  DC_LAUNCHED(c);
+  bool in1 = false;
+  DC_TRY(radix_sort_pairs(c, k0.p, v0.p, k1.p, v1.p, n_launch, 0, bits_for(N), &in1));
+  uint64_t* lkey = in1 ? k1.p : k0.p;
+  uint32_t* order = in1 ? v1.p : v0.p;
+  uint64_t* cnt = in1 ? k0.p : k1.p;  // free buffer
+  k_own_cnt<<<grid_for(c, n_launch, 256), 256, 0, c->stream>>>(launch_off, order, n_launch, cnt);
+  DC_LAUNCHED(c);
+  DC_TRY(excl_scan<uint64_t>(c, cnt, cum.p, n_launch, cum.p + n_launch));
+  uint32_t hbad = 0;
+  DC_TRY(readback(c, bad.p, 4, &hbad));
+  if (hbad) return DC_OK;  // offsets inconsistent: generic schedule
+  // partial outputs
+  const uint32_t G = (uint32_t)c->num_sms;
+  const uint64_t cap_entries = n + 1;
+  const uint32_t cap_segs = (uint32_t)(n_launch + 4ull * G + n / 4096 + 1024);
+  Buf<uint32_t> pkey, flags;
+  Buf<unsigned long long> pcnt, ctr, ldiag;
+  Buf<uint4> seg;
+  DC_TRY(alloc(c, pkey, cap_entries));
+  DC_TRY(alloc(c, pcnt, cap_entries));
+  DC_TRY(alloc(c, seg, cap_segs));
+  DC_TRY(alloc_zero(c, ctr, 2));
+  DC_TRY(alloc_zero(c, flags, 2));
+  DC_TRY(alloc_zero(c, ldiag, DG_N));
+  OwnArgs a;
+  a.smp = s;
+  a.launch_off = launch_off;
+  a.order = order;
+  a.lkey = lkey;
+  a.cum = cum.p;
+  a.n_launch = n_launch;
+  a.N = N;
+  a.total = n;
+  a.S = S;
+  a.pkey = pkey.p;
+  a.pcnt = pcnt.p;
+  a.cap_entries = cap_entries;
+  a.seg = seg.p;
+  a.cap_segs = cap_segs;
+  a.g_entries = ctr.p;
+  a.g_segs = (unsigned int*)(ctr.p + 1);
+  a.g_flags = flags.p;
+  a.trace_flags = c->d_flags;
+  a.ldiag = ldiag.p;
+  const size_t smem = sizeof(OwnSmem);
+  DC_CUDA(c, cudaFuncSetAttribute(k_pc_owner, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  {
+    Region rk(c, "k:pc_owner");
+    k_pc_owner<<<G, OW_THREADS, smem, c->stream>>>(a);
+    DC_LAUNCHED(c);
+  }
+  uint64_t hc[2];
+  uint32_t hf[2];
+  DC_TRY(readback(c, ctr.p, 16, hc));
+  DC_TRY(readback(c, flags.p, 8, hf));
+  if (hf[0]) return DC_OK;  // fallback / overflow -> generic schedule (diag of this pass discarded)
+  const uint32_t n_segs = (uint32_t)(hc[1] & 0xFFFFFFFFu);
+  // group segments by context
+  Buf<uint64_t> sk0, sk1;
+  Buf<uint32_t> sv0, sv1, head, hex, grp_start;
+  DC_TRY(alloc(c, sk0, n_segs));
+  DC_TRY(alloc(c, sk1, n_segs));
+  DC_TRY(alloc(c, sv0, n_segs));
+  DC_TRY(alloc(c, sv1, n_segs));
+  DC_TRY(alloc(c, head, n_segs));
+  DC_TRY(alloc(c, hex, n_segs));
+  k_own_segkeys<<<grid_for(c, n_segs, 256), 256, 0, c->stream>>>(seg.p, n_segs, sk0.p, sv0.p, nullptr);
+  DC_LAUNCHED(c);
+  bool sin1 = false;
+  DC_TRY(radix_sort_pairs(c, sk0.p, sv0.p, sk1.p, sv1.p, n_segs, 0, bits_for(N), &sin1));
+  uint64_t* ssk = sin1 ? sk1.p : sk0.p;
+  uint32_t* sso = sin1 ? sv1.p : sv0.p;
+  k_own_groups<<<grid_for(c, n_segs, 256), 256, 0, c->stream>>>(ssk, n_segs, head.p);
+  DC_LAUNCHED(c);
+  Buf<uint32_t> ng;
+  DC_TRY(alloc(c, ng, 1));
+  DC_TRY(excl_scan<uint32_t>(c, head.p, hex.p, n_segs, ng.p));
+  uint32_t n_groups = 0;
+  DC_TRY(readback(c, ng.p, 4, &n_groups));
+  DC_TRY(alloc(c, grp_start, n_groups + 1));
+  k_own_gstart<<<grid_for(c, n_segs, 256), 256, 0, c->stream>>>(head.p, hex.p, n_segs, grp_start.p, n_groups);
+  DC_LAUNCHED(c);
+  Buf<uint64_t> gsz, gout;
+  DC_TRY(alloc(c, gsz, n_groups));
+  DC_TRY(alloc(c, gout, n_groups + 1));
+  k_own_gsize<<<grid_for(c, n_groups, 128), 128, 0, c->stream>>>(seg.p, sso, grp_start.p, n_groups, gsz.p);
+  DC_LAUNCHED(c);
+  DC_TRY(excl_scan<uint64_t>(c, gsz.p, gout.p, n_groups, gout.p + n_groups));
+  // per-context reduce
+  Buf<uint32_t> okey, gnb, gnp, gctx, bbase, pbase;
+  Buf<unsigned long long> ocnt;
+  Buf<uint32_t> tots;
+  DC_TRY(alloc(c, okey, hc[0]));
+  DC_TRY(alloc(c, ocnt, hc[0]));
+  DC_TRY(alloc(c, gnb, n_groups));
+  DC_TRY(alloc(c, gnp, n_groups));
+  DC_TRY(alloc(c, gctx, n_groups));
+  DC_TRY(alloc(c, bbase, n_groups));
+  DC_TRY(alloc(c, pbase, n_groups));
+  DC_TRY(alloc(c, tots, 2));
+  // key bits: pc_off < 2^27 -> key < 2^32; use all 32 (4 passes) — cheap in shared memory
+  const int kbits = 32;
+  const size_t rsmem = sizeof(RedSmem);
+  DC_CUDA(c, cudaFuncSetAttribute(k_own_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem));
+  k_own_reduce<<<n_groups < (uint32_t)G ? n_groups : G, RD_THREADS, rsmem, c->stream>>>(
+      seg.p, sso, grp_start.p, n_groups, gout.p, pkey.p, pcnt.p, kbits, N, okey.p, ocnt.p, gnb.p, gnp.p, gctx.p,
+      (unsigned long long*)t->xsamples, (unsigned long long*)t->xstall, S, flags.p);
+  DC_LAUNCHED(c);
+  DC_TRY(readback(c, flags.p, 4, hf));
+  if (hf[0]) {  // a context too large for the shared-memory reduce: generic schedule
+    DC_CUDA(c, cudaMemsetAsync(t->xsamples, 0, N * 8, c->stream));
+    DC_CUDA(c, cudaMemsetAsync(t->xstall, 0, (uint64_t)S * N * 8, c->stream));
+    return DC_OK;
+  }
+  DC_TRY(excl_scan<uint32_t>(c, gnb.p, bbase.p, n_groups, tots.p));
+  DC_TRY(excl_scan<uint32_t>(c, gnp.p, pbase.p, n_groups, tots.p + 1));
+  uint32_t ht[2];
+  DC_TRY(readback(c, tots.p, 8, ht));
+  const uint64_t nb = ht[0], npc = ht[1];
+  t->Npc = npc;
+  t->Nbins = nb;
+  DC_TRY(palloc(c, t->pc_ctx, npc));
+  DC_TRY(palloc(c, t->pc_off, npc));
+  DC_TRY(palloc(c, t->bin_pcnode, nb));
+  DC_TRY(palloc(c, t->bin_stall, nb));
+  DC_TRY(palloc(c, t->bin_count, nb));
+  k_own_place<<<n_groups < 4u * G ? (n_groups ? n_groups : 1) : 4 * G, 256, 0, c->stream>>>(
+      gout.p, gnb.p, bbase.p, pbase.p, gctx.p, n_groups, okey.p, ocnt.p, N, t->pc_ctx, t->pc_off, t->bin_pcnode,
+      t->bin_stall, t->bin_count);
+  DC_LAUNCHED(c);
+  DC_TRY(add_diag(c, ldiag.p));
+  *n_bins_out = nb;
+  *handled = 1;
+  return DC_OK;
+}
+
+}  // namespace dc

@@ -1,0 +1,238 @@
+// prim.cuh — device-wide primitives of libdc (own implementations, no CUB on the hot path):
+// exclusive scan (reduce-then-scan, 3 phases) and a stable LSD radix sort of
+// (u64 key, u32 value) pairs over the significant bit range only.
+#pragma once
+#include "common.cuh"
+
+namespace dc {
+
+constexpr int SCAN_THREADS = 256;
+constexpr int SCAN_ITEMS = 16;
+constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
+
+template <class T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T u = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane_id() >= (uint32_t)o) v += u;
+  }
+  return v;
+}
+
+// block-wide exclusive scan of one value per thread; returns exclusive prefix, *total = block sum
+template <class T, int NT>
+__device__ __forceinline__ T block_excl_scan(T v, T* total) {
+  __shared__ T warp_sums[NT / 32];
+  T inc = warp_incl_scan(v);
+  const int w = threadIdx.x >> 5;
+  if (lane_id() == 31) warp_sums[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    T s = lane_id() < (uint32_t)(NT / 32) ? warp_sums[lane_id()] : T(0);
+    T si = warp_incl_scan(s);
+    if (lane_id() < (uint32_t)(NT / 32)) warp_sums[lane_id()] = si - s;
+  }
+  __syncthreads();
+  T excl = warp_sums[w] + inc - v;
+  if (total) {
+    __shared__ T tot;
+    if (threadIdx.x == NT - 1) tot = excl + v;
+    __syncthreads();
+    *total = tot;
+  }
+  __syncthreads();
+  return excl;
+}
+
+template <class T>
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_reduce(const T* __restrict__ in, uint64_t n, T* __restrict__ sums) {
+  const uint64_t base = (uint64_t)blockIdx.x * SCAN_TILE;
+  T s = 0;
+#pragma unroll
+  for (int i = 0; i < SCAN_ITEMS; ++i) {
+    uint64_t j = base + (uint64_t)i * SCAN_THREADS + threadIdx.x;
+    if (j < n) s += in[j];
+  }
+  T tot;
+  block_excl_scan<T, SCAN_THREADS>(s, &tot);
+  if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+}
+
+// single-block scan of a (short) array, in place; optionally stores the total
+template <class T>
+__global__ void __launch_bounds__(1024) k_scan_single(T* a, uint64_t n, T* total) {
+  __shared__ T carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (uint64_t base = 0; base < n; base += 1024) {
+    uint64_t j = base + threadIdx.x;
+    T v = j < n ? a[j] : T(0);
+    T tot;
+    T ex = block_excl_scan<T, 1024>(v, &tot);
+    if (j < n) a[j] = carry + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  if (total && threadIdx.x == 0) *total = carry;
+}
+
+template <class T>
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_down(const T* __restrict__ in, T* out, uint64_t n,
+                                                            const T* __restrict__ offs) {
+  // each thread owns SCAN_ITEMS consecutive elements of the tile
+  const uint64_t base = (uint64_t)blockIdx.x * SCAN_TILE + (uint64_t)threadIdx.x * SCAN_ITEMS;
+  T v[SCAN_ITEMS];
+  T s = 0;
+#pragma unroll
+  for (int i = 0; i < SCAN_ITEMS; ++i) {
+    uint64_t j = base + i;
+    v[i] = j < n ? in[j] : T(0);
+    s += v[i];
+  }
+  T ex = block_excl_scan<T, SCAN_THREADS>(s, nullptr) + offs[blockIdx.x];
+#pragma unroll
+  for (int i = 0; i < SCAN_ITEMS; ++i) {
+    uint64_t j = base + i;
+    if (j < n) out[j] = ex;
+    ex += v[i];
+  }
+}
+
+// out[i] = sum(in[0..i)); total (device) optional. in may equal out.
+template <class T>
+dc_status excl_scan(Ctx* c, const T* in, T* out, uint64_t n, T* total_dev) {
+  if (n == 0) {
+    if (total_dev) DC_CUDA(c, cudaMemsetAsync(total_dev, 0, sizeof(T), c->stream));
+    return DC_OK;
+  }
+  uint64_t nt = (n + SCAN_TILE - 1) / SCAN_TILE;
+  if (nt == 1) {
+    if (in != out) DC_CUDA(c, cudaMemcpyAsync(out, in, n * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
+    k_scan_single<T><<<1, 1024, 0, c->stream>>>(out, n, total_dev);
+    DC_LAUNCHED(c);
+    return DC_OK;
+  }
+  Buf<T> sums;
+  DC_TRY(alloc(c, sums, nt));
+  k_scan_reduce<T><<<(unsigned)nt, SCAN_THREADS, 0, c->stream>>>(in, n, sums.p);
+  DC_LAUNCHED(c);
+  DC_TRY(excl_scan<T>(c, sums.p, sums.p, nt, total_dev));
+  k_scan_down<T><<<(unsigned)nt, SCAN_THREADS, 0, c->stream>>>(in, out, n, sums.p);
+  DC_LAUNCHED(c);
+  return DC_OK;
+}
+
+// ------------------------------------------------------------------ radix sort (pairs)
+constexpr int RS_THREADS = 256;
+constexpr int RS_WARPS = RS_THREADS / 32;
+constexpr int RS_ROUNDS = 8;                      // keys per lane
+constexpr int RS_WARP_KEYS = 32 * RS_ROUNDS;      // contiguous keys owned by one warp
+constexpr int RS_TILE = RS_WARPS * RS_WARP_KEYS;  // 2048
+
+__device__ __forceinline__ uint32_t rs_digit(uint64_t k, int shift, uint32_t mask) {
+  return (uint32_t)(k >> shift) & mask;
+}
+
+// per-tile digit histogram, digit-major: hist[d * n_tiles + tile]
+static __global__ void __launch_bounds__(RS_THREADS) k_rs_count(const uint64_t* __restrict__ keys, uint32_t n, int shift,
+                                                         uint32_t mask, uint32_t* __restrict__ hist, uint32_t n_tiles) {
+  __shared__ uint32_t cnt[256];
+  cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const uint32_t w = threadIdx.x >> 5, lane = lane_id();
+  const uint32_t base = blockIdx.x * RS_TILE + w * RS_WARP_KEYS;
+#pragma unroll
+  for (int r = 0; r < RS_ROUNDS; ++r) {
+    uint32_t j = base + r * 32 + lane;
+    bool ok = j < n;
+    uint32_t d = ok ? rs_digit(keys[j], shift, mask) : 0xFFFFFFFFu;
+    uint32_t peers = __match_any_sync(0xffffffffu, d);
+    if (ok && (peers & lanemask_lt()) == 0) atomicAdd(&cnt[d], __popc(peers));
+  }
+  __syncthreads();
+  hist[threadIdx.x * n_tiles + blockIdx.x] = cnt[threadIdx.x];
+}
+
+static __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+                                                           uint64_t* __restrict__ okeys, uint32_t* __restrict__ ovals, uint32_t n,
+                                                           int shift, uint32_t mask, const uint32_t* __restrict__ offs,
+                                                           uint32_t n_tiles) {
+  __shared__ uint32_t wcnt[RS_WARPS][256];
+  for (int i = threadIdx.x; i < RS_WARPS * 256; i += RS_THREADS) (&wcnt[0][0])[i] = 0;
+  __syncthreads();
+  const uint32_t w = threadIdx.x >> 5, lane = lane_id();
+  const uint32_t base = blockIdx.x * RS_TILE + w * RS_WARP_KEYS;
+  uint64_t k[RS_ROUNDS];
+  uint32_t v[RS_ROUNDS];
+  uint32_t d[RS_ROUNDS];
+#pragma unroll
+  for (int r = 0; r < RS_ROUNDS; ++r) {
+    uint32_t j = base + r * 32 + lane;
+    bool ok = j < n;
+    k[r] = ok ? keys[j] : 0;
+    v[r] = ok ? vals[j] : 0;
+    d[r] = ok ? rs_digit(k[r], shift, mask) : 0xFFFFFFFFu;
+    uint32_t peers = __match_any_sync(0xffffffffu, d[r]);
+    if (ok && (peers & lanemask_lt()) == 0) wcnt[w][d[r]] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  {  // per digit: exclusive prefix over warps + global tile offset
+    uint32_t dg = threadIdx.x;
+    uint32_t run = offs[dg * n_tiles + blockIdx.x];
+#pragma unroll
+    for (int ww = 0; ww < RS_WARPS; ++ww) {
+      uint32_t c = wcnt[ww][dg];
+      wcnt[ww][dg] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < RS_ROUNDS; ++r) {
+    uint32_t peers = __match_any_sync(0xffffffffu, d[r]);
+    bool ok = d[r] != 0xFFFFFFFFu;
+    uint32_t pos = 0;
+    if (ok) pos = wcnt[w][d[r]] + __popc(peers & lanemask_lt());
+    __syncwarp();
+    if (ok && (peers & lanemask_lt()) == 0) wcnt[w][d[r]] += __popc(peers);
+    __syncwarp();
+    if (ok) {
+      okeys[pos] = k[r];
+      ovals[pos] = v[r];
+    }
+  }
+}
+
+// Stable sort of n pairs by bits [begin_bit, end_bit) of the key. Ping-pongs between
+// (k0,v0) and (k1,v1); *result_in_1 tells where the sorted data ended up.
+inline dc_status radix_sort_pairs(Ctx* c, uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, uint64_t n,
+                                  int begin_bit, int end_bit, bool* result_in_1) {
+  *result_in_1 = false;
+  if (n <= 1 || end_bit <= begin_bit) return DC_OK;
+  if (n >= (1ull << 31)) return fail(c, DC_ERR_CAPACITY, "radix sort of %llu > 2^31 keys", (unsigned long long)n);
+  uint32_t nt = (uint32_t)((n + RS_TILE - 1) / RS_TILE);
+  Buf<uint32_t> hist;
+  DC_TRY(alloc(c, hist, (size_t)256 * nt));
+  bool in1 = false;
+  for (int shift = begin_bit; shift < end_bit; shift += 8) {
+    int nb = end_bit - shift < 8 ? end_bit - shift : 8;
+    uint32_t mask = (1u << nb) - 1u;
+    const uint64_t* ik = in1 ? k1 : k0;
+    const uint32_t* iv = in1 ? v1 : v0;
+    uint64_t* ok = in1 ? k0 : k1;
+    uint32_t* ov = in1 ? v0 : v1;
+    k_rs_count<<<nt, RS_THREADS, 0, c->stream>>>(ik, (uint32_t)n, shift, mask, hist.p, nt);
+    DC_LAUNCHED(c);
+    DC_TRY(excl_scan<uint32_t>(c, hist.p, hist.p, (uint64_t)256 * nt, nullptr));
+    k_rs_scatter<<<nt, RS_THREADS, 0, c->stream>>>(ik, iv, ok, ov, (uint32_t)n, shift, mask, hist.p, nt);
+    DC_LAUNCHED(c);
+    in1 = !in1;
+  }
+  *result_in_1 = in1;
+  return DC_OK;
+}
+
+}  // namespace dc

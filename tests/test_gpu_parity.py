@@ -1,0 +1,278 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle, element by element, on the
+same seeded inputs. Integer outputs bit-exact; derived floats within 1e-12 relative
+(BASELINE.json north_star)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from pipeline import CMP_KEYS, as_u64, assert_same, gpu_run, oracle_run
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _csr(paths):
+    off = np.zeros(len(paths) + 1, np.uint64)
+    off[1:] = np.cumsum([len(p) for p in paths])
+    fr = np.asarray([f for p in paths for f in p], np.uint32)
+    return off, fr
+
+
+def _samples(lst):
+    s = np.zeros(len(lst), oracle.SAMPLE_DTYPE)
+    for i, (l, pc, st, c) in enumerate(lst):
+        s[i] = (l, pc, st, 0, c)
+    return s
+
+
+def test_f1_fixture_gpu():
+    g = json.load(open(os.path.join(GOLD, "f1.json")))
+    keys = np.zeros(0, oracle.KEY_DTYPE)
+    # records as raw keys (interned on the GPU)
+    kk = np.asarray([tuple(g["raw_keys"][f]) for p in g["paths"] for f in p], oracle.KEY_DTYPE)
+    off, _ = _csr(g["paths"])
+    a = gpu_run(off, keys=kk, metrics=np.asarray(g["metrics"], np.uint64), samples=_samples(g["samples"]), n_stall=24)
+    for k in ["leaf", "parent", "depth", "frame", "xcnt", "icnt", "xsamples", "isamples"]:
+        assert np.asarray(a[k]).tolist() == g[k], k
+    assert a["isum"][0].tolist() == g["isum_ns"] and a["imin"][0].tolist() == g["imin_ns"]
+    import paper_2411_02797_b200 as dc
+    ctx, cct = a["_ctx"], a["_cct"]
+    mean, std = dc.dc_cct_derived(ctx, cct, 0, True)
+    assert mean.cpu().numpy().tolist() == g["imean_ns"]
+    np.testing.assert_allclose(std.cpu().numpy(), g["istd_ns"], rtol=1e-12, atol=0)
+    hot = dc.dc_hotspots_topk(ctx, cct, dc.DC_VIEW_INCLUSIVE, 0, 1 << dc.DC_KIND_KERNEL, 0.1, 3)
+    assert [list(e) for e in hot] == g["hotspot_kernels_incl_ns_theta0.1_k3"]
+    bu = dc.dc_hotspots_topk(ctx, cct, dc.DC_VIEW_BOTTOM_UP, 0, 0xFFFFFFFF, 0.0, 10)
+    assert [[i, v] for i, v, _ in bu] == g["bottom_up_excl_ns"]
+    for node, key in [(8, "stall_top2_node8"), (10, "stall_top2_node10")]:
+        st = dc.dc_hotspots_topk(ctx, cct, dc.DC_VIEW_STALL, k=2, stall_node=node)
+        assert [list(e) for e in st] == g[key]
+    assert list(map(list, zip(a["bin_pcnode"].tolist(), a["bin_stall"].tolist(), a["bin_count"].tolist()))) == g["bins"]
+    d = ctx.diag()
+    assert (d["samples_bad_launch"], d["samples_bad_stall"], d["samples_zero_count"], d["empty_paths"]) == (1, 1, 1, 1)
+
+
+def _rand_trace(rng, R_max=300, A_max=40):
+    R = int(rng.integers(1, R_max))
+    A = int(rng.integers(2, A_max))
+    paths = []
+    for _ in range(R):
+        L = int(rng.integers(0, 20))
+        if paths and rng.random() < 0.4:
+            base = list(paths[int(rng.integers(0, len(paths)))])
+            p = base[: min(L, len(base))] + [int(rng.integers(0, A)) for _ in range(max(0, L - len(base)))]
+        else:
+            p = [int(rng.integers(0, A)) for _ in range(L)]
+        if p and rng.random() < 0.1:
+            i = int(rng.integers(0, len(p)))
+            p = p[: i + 1] + [p[i]] * 2 + p[i + 1:]
+        paths.append(tuple(p))
+    M = int(rng.integers(1, 4))
+    X = rng.integers(0, 2**40 if rng.random() < 0.3 else 10**6, size=(M, R), dtype=np.uint64)
+    if rng.random() < 0.2:
+        X[:, : max(1, R // 7)] = np.uint64(2**63 // max(R, 1))  # large values: u128 sums of squares
+    S = int(rng.integers(1, 33))
+    ns = int(rng.integers(0, 400))
+    smp = _samples([(int(rng.integers(0, R + 2)), int(rng.integers(0, 50)) * 16, int(rng.integers(0, S + 2)),
+                     int(rng.integers(0, 5))) for _ in range(ns)])
+    return paths, X, smp, S, A
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_traces_vs_oracle(seed):
+    rng = np.random.default_rng(500 + seed)
+    import paper_2411_02797_b200 as dc
+    ctx = dc.Context(0)
+    for it in range(25):
+        paths, X, smp, S, A = _rand_trace(rng)
+        off, fr = _csr(paths)
+        a = gpu_run(off, fr, X, n_frames=A, samples=smp, n_stall=S, ctx=ctx)
+        ref = oracle_run(off, fr, X, X.shape[0], smp, len(paths), S).arrays()
+        assert_same(a, ref, ctx=f"seed {seed} it {it}")
+        # views vs oracle
+        fk = rng.integers(0, 6, size=A).astype(np.uint8)
+        o = oracle_run(off, fr, X, X.shape[0], smp, len(paths), S)
+        for view in [0, 1, 3]:
+            th = float(rng.choice([-1.0, 0.0, 0.01, 0.2]))
+            k = int(rng.integers(1, 12))
+            m = int(rng.integers(0, X.shape[0]))
+            node = int(rng.integers(0, a["n_nodes"]))
+            got = dc.dc_hotspots_topk(ctx, a["_cct"], view, m, 0xFFFFFFFF, th, k, node)
+            exp = o.topk(view, m, 0xFFFFFFFF, None, th, k, node)
+            assert got == [(int(e["id"]), int(e["value"]), float(e["fraction"])) for e in exp], (view, th, k)
+        # derived
+        for m in range(X.shape[0]):
+            for incl in (True, False):
+                mg, sg = dc.dc_cct_derived(ctx, a["_cct"], m, incl)
+                mo, so = o.derived(m, incl)
+                np.testing.assert_allclose(mg.cpu().numpy(), mo, rtol=1e-12, atol=0)
+                np.testing.assert_allclose(sg.cpu().numpy(), so, rtol=1e-12, atol=0)
+
+
+def test_kind_mask_and_bottom_up_with_dict():
+    p = gen.programs.program(1)
+    tr = gen.make_trace(p)
+    a = gpu_run(tr.offsets.numpy(), keys=tr.keys.numpy(), metrics=tr.metrics.numpy())
+    import paper_2411_02797_b200 as dc
+    oids, odict = oracle.intern(tr.keys.numpy())
+    o = oracle_run(tr.offsets.numpy(), oids, tr.metrics.numpy(), 2)
+    fk = np.asarray(odict["kind"], np.uint8)
+    assert np.array_equal(a["ids"], oids)
+    assert np.array_equal(a["_dict"].kinds(), fk)
+    for view in [0, 1, 2]:
+        for mask in [1 << 4, (1 << 0) | (1 << 2), 0xFFFFFFFF]:
+            for th in [0.0, 0.001, 0.05]:
+                got = dc.dc_hotspots_topk(a["_ctx"], a["_cct"], view, 0, mask, th, 20)
+                exp = o.topk(view, 0, mask, fk, th, 20)
+                assert got == [(int(e["id"]), int(e["value"]), float(e["fraction"])) for e in exp]
+
+
+@pytest.mark.parametrize("cfg,R", [(1, None), (2, 200_000), (3, None)])
+def test_configs_vs_oracle(cfg, R):
+    p = gen.programs.program(cfg) if cfg != 3 else gen.programs.config3(n_samples=4_000_000)
+    tr = gen.make_trace(p, n_records=R, pc=(cfg == 3), bad_per_million=500 if cfg == 3 else 0)
+    kw = {}
+    if cfg == 3:
+        kw = dict(samples=tr.samples.numpy(), launch_off=tr.launch_off.numpy(), n_launch=tr.n_launch)
+    a = gpu_run(tr.offsets.numpy(), keys=tr.keys.numpy(), metrics=tr.metrics.numpy(), **kw)
+    oids, _ = oracle.intern(tr.keys.numpy())
+    assert np.array_equal(a["ids"], oids)
+    ref = oracle_run(tr.offsets.numpy(), oids, tr.metrics.numpy(), p.n_metrics,
+                     tr.samples.numpy() if cfg == 3 else None, tr.n_launch if cfg == 3 else 0).arrays()
+    ref["leaf"] = ref["leaf"]
+    assert_same(a, ref, ctx=f"cfg{cfg}")
+
+
+def test_generic_schedule_equals_owner_schedule():
+    """launch_sample_off given vs NULL: identical results (and oracle)."""
+    p = gen.programs.config3(n_samples=2_000_000)
+    tr = gen.make_trace(p, pc=True, bad_per_million=1000)
+    kw = dict(keys=tr.keys.numpy(), metrics=tr.metrics.numpy(), samples=tr.samples.numpy(), n_launch=tr.n_launch)
+    a = gpu_run(tr.offsets.numpy(), launch_off=tr.launch_off.numpy(), **kw)
+    b = gpu_run(tr.offsets.numpy(), launch_off=None, **kw)
+    assert_same(a, b, ctx="owner vs generic")
+
+
+def test_edge_cases():
+    # empty trace
+    a = gpu_run(np.zeros(1, np.uint64), np.zeros(0, np.uint32), np.zeros((1, 0), np.uint64), n_frames=5)
+    assert a["n_nodes"] == 1 and a["icnt"].tolist() == [0]
+    # all empty paths
+    off = np.zeros(5, np.uint64)
+    a = gpu_run(off, np.zeros(0, np.uint32), np.arange(4, dtype=np.uint64)[None], n_frames=1)
+    assert a["n_nodes"] == 1 and a["xcnt"].tolist() == [4] and a["isum"][0].tolist() == [6]
+    # single record, single frame
+    a = gpu_run(np.array([0, 1], np.uint64), np.array([0], np.uint32), np.array([[7]], np.uint64), n_frames=1)
+    assert a["parent"].tolist() == [0xFFFFFFFF, 0] and a["isum"][0].tolist() == [7, 7]
+    # depth == DC_MAX_DEPTH (1024) recursion chain; prefix-of-another; all identical
+    K = 1024
+    paths = [tuple([3] * k) for k in range(1, K + 1)] + [tuple([3] * 10)] * 50
+    off, fr = _csr(paths)
+    X = np.ones((1, len(paths)), np.uint64)
+    a = gpu_run(off, fr, X, n_frames=4)
+    ref = oracle_run(off, fr, X, 1).arrays()
+    assert_same(a, ref, ctx="chain")
+    assert a["max_depth"] == K
+
+
+def test_too_deep_and_bad_frame_are_trace_errors():
+    import paper_2411_02797_b200 as dc
+    off, fr = _csr([tuple([1] * 1025)])
+    with pytest.raises(dc.DcError) as e:
+        gpu_run(off, fr, np.ones((1, 1), np.uint64), n_frames=2)
+    assert e.value.status == 6
+    off, fr = _csr([(0, 9)])
+    with pytest.raises(dc.DcError) as e:
+        gpu_run(off, fr, np.ones((1, 1), np.uint64), n_frames=5)
+    assert e.value.status == 6
+
+
+def test_large_P_multikernel_build():
+    """> 4096 distinct paths takes the per-level multi-kernel build."""
+    rng = np.random.default_rng(3)
+    paths = [tuple(int(x) for x in rng.integers(0, 30, size=int(rng.integers(1, 12)))) for _ in range(20_000)]
+    paths += paths[:5000]
+    off, fr = _csr(paths)
+    X = rng.integers(0, 10**9, size=(2, len(paths)), dtype=np.uint64)
+    a = gpu_run(off, fr, X, n_frames=30)
+    ref = oracle_run(off, fr, X, 2).arrays()
+    assert_same(a, ref, ctx="largeP")
+
+
+def test_hash_collisions_resolved_exactly(monkeypatch):
+    """DC_TEST_WEAK_HASH=6 keeps 6 bits of the path hash: thousands of collisions, same tree."""
+    monkeypatch.setenv("DC_TEST_WEAK_HASH", "6")
+    import paper_2411_02797_b200 as dc
+    ctx = dc.Context(0)
+    rng = np.random.default_rng(4)
+    paths = [tuple(int(x) for x in rng.integers(0, 8, size=int(rng.integers(0, 9)))) for _ in range(3000)]
+    off, fr = _csr(paths)
+    X = rng.integers(0, 1000, size=(1, len(paths)), dtype=np.uint64)
+    a = gpu_run(off, fr, X, n_frames=8, ctx=ctx)
+    ref = oracle_run(off, fr, X, 1).arrays()
+    assert_same(a, ref, ctx="weak hash")
+    assert ctx.diag()["collisions_detected"] > 0
+
+
+def test_permutation_invariance_and_determinism():
+    p = gen.programs.program(1)
+    tr = gen.make_trace(p)
+    off = tr.offsets.numpy().view(np.uint64)
+    ids = tr.ids.numpy().view(np.uint32)
+    X = as_u64(tr.metrics.numpy())
+    R = len(off) - 1
+    perm = np.random.default_rng(9).permutation(R)
+    paths = [ids[off[r]:off[r + 1]] for r in perm]
+    off2 = np.zeros(R + 1, np.uint64)
+    off2[1:] = np.cumsum([len(q) for q in paths])
+    fr2 = np.concatenate(paths).astype(np.uint32)
+    a = gpu_run(off, ids, X, n_frames=tr.n_frames)
+    b = gpu_run(off2, fr2, X[:, perm], n_frames=tr.n_frames)
+    c = gpu_run(off, ids, X, n_frames=tr.n_frames)
+    assert_same(a, b, keys=[k for k in CMP_KEYS if "samples" not in k and "stall" not in k and "pc" not in k and "bin" not in k])
+    assert_same(a, c)
+    assert np.array_equal(a["leaf"][perm], b["leaf"])
+
+
+def test_full_size_config3_sampled_contexts():
+    """BASELINE config 3 at full size (100M samples) in the bench's launch configuration:
+    exact per-context parity for sampled contexts (the oracle on just those launches' samples),
+    conservation for the rest."""
+    import torch
+    import paper_2411_02797_b200 as dc
+    p = gen.programs.config3()
+    tr = gen.make_trace(p, pc=True, device="cuda")
+    ctx = dc.Context(0)
+    ids, d = dc.dc_intern_frames(ctx, tr.keys)
+    cct, leaf = dc.dc_cct_build(ctx, tr.offsets, ids, d.size, d)
+    dc.dc_cct_attribute_metrics(ctx, cct, leaf, tr.metrics)
+    dc.dc_pc_sample_attribute(ctx, cct, tr.samples, leaf, tr.launch_off, n_stall=24)
+    dc.dc_cct_rollup(ctx, cct)
+    a = cct.to_numpy()
+    assert int(a["bin_count"].sum()) == 100_000_000 == int(a["isamples"][0])
+    leaf_np = leaf.cpu().numpy().view(np.uint32)
+    lo = tr.launch_off.cpu().numpy().view(np.uint64)
+    S = tr.samples.cpu().numpy()
+    rng = np.random.default_rng(0)
+    ctxs = rng.choice(np.unique(leaf_np), size=4, replace=False)
+    for cnode in ctxs:
+        launches = np.nonzero(leaf_np == cnode)[0]
+        sub = np.concatenate([S[lo[l]:lo[l + 1]] for l in launches])
+        # oracle over a single record with that context's path -> bins of that context
+        o = oracle.OracleCCT(1, 24).insert(np.array([0, 1], np.uint64), np.array([0], np.uint32), np.zeros((1, 1), np.uint64))
+        sub = sub.copy()
+        sub[:, 0] = 0
+        o.pc(sub, 1)
+        r = o.finalize().arrays()
+        sel = a["pc_ctx"] == cnode
+        pcnodes = np.nonzero(sel)[0] + a["n_nodes"]
+        assert np.array_equal(a["pc_off"][sel], r["pc_off"])
+        bsel = np.isin(a["bin_pcnode"], pcnodes)
+        assert np.array_equal(a["bin_stall"][bsel], r["bin_stall"])
+        assert np.array_equal(a["bin_count"][bsel], r["bin_count"])
+        assert a["xsamples"][cnode] == r["xsamples"][1]
+    del torch
