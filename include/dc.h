@@ -252,8 +252,15 @@ void dc_comm_destroy(dc_comm* comm);
    Synchronizes. */
 dc_status dc_cct_merge_ranks(dc_ctx* ctx, dc_comm* comm, const dc_cct* local, const dc_dict* local_dict,
                              dc_cct** out_partition, dc_dict** out_global_dict);
-/* Gathers the partitions at `root` and canonicalizes them into one CCT (parity/views only). */
+/* Gathers the partitions at `root` and canonicalizes them into one CCT (parity/views only):
+   on `root` *out_canonical is a ROLLED tree in canonical (depth, lexicographic) order over the
+   global dictionary; NULL on the other ranks. Collective; synchronizes. */
 dc_status dc_cct_gather(dc_ctx* ctx, dc_comm* comm, const dc_cct* part, int root, dc_cct** out_canonical);
+/* Single-GPU emulation of merge_ranks + gather for P logical ranks (loopback exchange through
+   device copies instead of NCCL; same partition/reduce/verify/canonicalise kernels).
+   locals[p] (ROLLED) with dicts[p]; returns the canonical merged tree and global dictionary. */
+dc_status dc_cct_merge_local(dc_ctx* ctx, uint32_t P, dc_cct* const* locals, dc_dict* const* dicts, dc_cct** out_canonical,
+                             dc_dict** out_global_dict);
 
 #ifdef __cplusplus
 }

@@ -296,6 +296,18 @@ def dc_cct_merge_ranks(ctx: Context, comm: Comm, local: CCT, local_dict: Dict):
     return CCT(part, ctx), Dict(gd)
 
 
+def dc_cct_merge_local(ctx: Context, locals_: list, dicts: list):
+    """Single-GPU emulation of merge_ranks + gather over len(locals_) logical ranks."""
+    P = len(locals_)
+    la = (ctypes.c_void_p * P)(*[t.h.value if isinstance(t.h, ctypes.c_void_p) else t.h for t in locals_])
+    da = (ctypes.c_void_p * P)(*[d.h.value if isinstance(d.h, ctypes.c_void_p) else d.h for d in dicts])
+    out = ctypes.c_void_p()
+    gd = ctypes.c_void_p()
+    ctx.check(lib().dc_cct_merge_local(ctx.h, P, ctypes.cast(la, ctypes.c_void_p), ctypes.cast(da, ctypes.c_void_p),
+                                       ctypes.byref(out), ctypes.byref(gd)), "dc_cct_merge_local")
+    return CCT(out, ctx), Dict(gd)
+
+
 def dc_cct_gather(ctx: Context, comm: Comm, part: CCT, root: int = 0):
     h = ctypes.c_void_p()
     ctx.check(lib().dc_cct_gather(ctx.h, comm.h, part.h, int(root), ctypes.byref(h)), "dc_cct_gather")

@@ -87,6 +87,7 @@ def lib():
             "dc_comm_destroy": (None, [P]),
             "dc_cct_merge_ranks": (i32, [P, P, P, P, ctypes.POINTER(P), ctypes.POINTER(P)]),
             "dc_cct_gather": (i32, [P, P, P, i32, ctypes.POINTER(P)]),
+            "dc_cct_merge_local": (i32, [P, u32, P, P, ctypes.POINTER(P), ctypes.POINTER(P)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)

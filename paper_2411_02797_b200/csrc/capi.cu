@@ -114,6 +114,10 @@ dc_status dc_ctx_create(int device, void* cuda_stream, dc_ctx** out) {
     int b = atoi(w);
     if (b > 0 && b < 64) ctx->hash_mask = (1ull << b) - 1ull;
   }
+  if (const char* w = getenv("DC_TEST_WEAK_MERGE_HASH")) {
+    int b = atoi(w);
+    if (b > 0 && b < 64) ctx->merge_mask = (1ull << b) - 1ull;
+  }
   ctx->smem_optin = prop.sharedMemPerBlockOptin;
   // keep freed pool memory cached (stream-ordered allocations are reused across calls)
   cudaMemPool_t pool;
@@ -353,7 +357,8 @@ void dc_cct_free(dc_cct* t) {
   if (!t) return;
   cudaSetDevice(t->device);
   void* ps[] = {t->parent, t->frame, t->level_off, t->depth, t->frame_kind, t->xcnt, t->icnt, t->mcols, t->xsamples,
-                t->isamples, t->xstall, t->istall, t->pc_ctx, t->pc_off, t->bin_pcnode, t->bin_stall, t->bin_count};
+                t->isamples, t->xstall, t->istall, t->pc_ctx, t->pc_off, t->bin_pcnode, t->bin_stall, t->bin_count,
+                t->part_nodes, t->part_bins};
   cudaDeviceSynchronize();
   for (void* p : ps)
     if (p) cudaFree(p);

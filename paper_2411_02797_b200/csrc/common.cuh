@@ -38,6 +38,7 @@ struct Ctx {
   uint64_t host_levels = 0;      // tree levels built
   uint64_t host_collisions = 0;  // path-hash collisions resolved exactly
   uint64_t hash_mask = ~0ull;    // fault injection: DC_TEST_WEAK_HASH=bits shortens path hashes
+  uint64_t merge_mask = ~0ull;   // fault injection: DC_TEST_WEAK_MERGE_HASH=bits shortens merge hashes
   // optional CUDA-event timers (dc_ctx_set_timing): (name, start, stop) per timed region
   bool timing = false;
   struct Timed { const char* name; cudaEvent_t a, b; };
@@ -93,6 +94,13 @@ struct dc_cct {
   uint32_t *pc_ctx = nullptr, *pc_off = nullptr, *bin_pcnode = nullptr;
   uint16_t* bin_stall = nullptr;
   uint64_t* bin_count = nullptr;
+  // merge partition (dc_cct_merge_ranks output): unique node / bin records, see merge.cu
+  bool partition = false;
+  uint64_t* part_nodes = nullptr;
+  uint64_t* part_bins = nullptr;
+  uint64_t part_nbins = 0;
+  uint32_t part_W = 0;
+  bool part_has_pc = false;
   uint64_t* col(int which, uint32_t m) const { return mcols + ((uint64_t)which * M + m) * N; }
 };
 enum { C_XSUM = 0, C_XMIN, C_XSQLO, C_XSQHI, C_ISUM, C_IMIN, C_ISQLO, C_ISQHI };
@@ -131,6 +139,11 @@ struct Buf {
   Buf() = default;
   Buf(const Buf&) = delete;
   Buf& operator=(const Buf&) = delete;
+  Buf(Buf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  Buf& operator=(Buf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; s = o.s; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
   ~Buf() { release(); }
   void release() {
     if (p) cudaFreeAsync(p, s);

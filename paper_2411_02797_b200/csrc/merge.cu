@@ -1,11 +1,983 @@
-// merge.cu — a9: cross-rank merge (placeholder until implemented).
+// merge.cu — a9: cross-rank merge of per-rank CCTs (north_star; not in the paper).
+//
+// Merged CCT == CCT of the concatenation of every rank's records (reading R19): inclusive
+// and exclusive aggregates are additive (and min-combinable) across disjoint record shards,
+// so nodes with equal full paths are simply combined.
+//   1. dictionary unify: all-gather the per-rank sorted dictionaries; every rank interns the
+//      union (same kernels as dc_intern_frames) -> identical global ranks; local -> global map.
+//   2. 128-bit full-path hash per node, level by level: h(root) = H0, h(n) = mix(h(parent), gframe).
+//   3. partition: owner(n) = floor(h_hi * P / 2^64); counting-sort node records into per-owner
+//      slabs (PC bins travel as (h_ctx, pc, stall, count), owner from (h_ctx, pc)).
+//   4. exchange: NCCL all-to-all of counts, grouped ncclSend/ncclRecv of the slabs (NVLink).
+//   5. reduce: sort received records by h, combine runs (+ / min), and VERIFY that every run
+//      agrees on (parent hash, global frame, depth): by induction from the fixed root hash a
+//      hash collision between different paths always shows up as such a mismatch
+//      (DC_ERR_COLLISION), so the merge is exact or fails loudly.
+//   6. (parity / views) gather: partitions to a root rank, canonicalised level by level into
+//      the (depth, lexicographic) node order — the same canonical CCT the single-GPU build gives.
+// dc_cct_merge_local runs steps 1-6 for P logical ranks on ONE GPU with a loopback exchange
+// (device copies instead of NCCL) — the emulated-rank test path.
+#include <vector>
+
 #include "prim.cuh"
+#if DC_HAVE_NCCL
+#include <nccl.h>
+#endif
+
+namespace dc {
+dc_status intern_frames(Ctx* c, const dc_frame_key* keys, uint64_t n, uint32_t* out_ids, dc_dict** out);
+dc_status ensure_metric_cols(Ctx* c, dc_cct* t, uint32_t M);
+
+// record layout, in u64 words
+//  0 h_lo  1 h_hi  2 hp_lo  3 hp_hi  4 gframe | depth << 32  5 xcnt  6 icnt
+//  7 + 8m .. : xsum xmin xsqlo xsqhi isum imin isqlo isqhi     (m < M)
+//  7 + 8M    : xsamples isamples, then per stall s: xstall istall (when the tree has PC data)
+struct RecFmt {
+  uint32_t M, S, has_pc, W;
+};
+static RecFmt rec_fmt(uint32_t M, uint32_t S, bool has_pc) {
+  RecFmt f{M, S, has_pc ? 1u : 0u, 0};
+  f.W = 7 + 8 * M + (has_pc ? 2 + 2 * S : 0);
+  return f;
+}
+constexpr int BIN_W = 4;  // h_lo, h_hi, pc | stall << 32, count
+
+__device__ __forceinline__ void mix128(uint64_t& lo, uint64_t& hi, uint32_t f) {
+  uint64_t a = mix64(lo ^ ((uint64_t)f * 0x9E3779B97F4A7C15ull) ^ 0x243F6A8885A308D3ull);
+  uint64_t b = mix64(hi + ((uint64_t)f << 17) + lo * 0xC2B2AE3D27D4EB4Full + 0x13198A2E03707344ull);
+  lo = a;
+  hi = b ^ (a >> 7);
+}
+constexpr uint64_t H0_LO = 0x6A09E667F3BCC908ull, H0_HI = 0xBB67AE8584CAA73Bull;
+
+__global__ void k_hash_root(uint64_t* h) {
+  h[0] = H0_LO;
+  h[1] = H0_HI;
+}
+// nodes [a, b): h[2n..2n+1] from the parent's
+__global__ void k_hash_level(const uint32_t* __restrict__ parent, const uint32_t* __restrict__ frame,
+                             const uint32_t* __restrict__ l2g, uint32_t a, uint32_t b, uint64_t* __restrict__ h,
+                             uint64_t mask) {
+  for (uint32_t n = a + blockIdx.x * blockDim.x + threadIdx.x; n < b; n += gridDim.x * blockDim.x) {
+    uint32_t p = parent[n];
+    uint64_t lo = h[2ull * p], hi = h[2ull * p + 1];
+    mix128(lo, hi, l2g ? l2g[frame[n]] : frame[n]);
+    lo &= mask;
+    hi &= mask;
+    h[2ull * n] = lo;
+    h[2ull * n + 1] = hi;
+  }
+}
+
+__device__ __forceinline__ uint32_t owner_of(uint64_t hi, uint32_t P) { return (uint32_t)__umul64hi(hi, (uint64_t)P); }
+
+__global__ void k_part_count(const uint64_t* __restrict__ h, uint64_t N, uint32_t P, unsigned long long* cnt) {
+  for (uint64_t n = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; n < N; n += (uint64_t)gridDim.x * blockDim.x)
+    atomicAdd(cnt + owner_of(h[2 * n + 1], P), 1ull);
+}
+
+// write node records into per-owner slabs (order inside a slab is irrelevant)
+__global__ void k_part_nodes(const uint64_t* __restrict__ h, const uint32_t* __restrict__ parent, const uint32_t* __restrict__ frame,
+                             const uint16_t* __restrict__ depth, const uint32_t* __restrict__ l2g, const uint64_t* __restrict__ xcnt,
+                             const uint64_t* __restrict__ icnt, const uint64_t* __restrict__ mcols, const uint64_t* __restrict__ xs,
+                             const uint64_t* __restrict__ is, const uint64_t* __restrict__ xst, const uint64_t* __restrict__ ist,
+                             uint64_t N, RecFmt f, uint32_t P, unsigned long long* cursor, uint64_t* __restrict__ out) {
+  for (uint64_t n = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; n < N; n += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t o = owner_of(h[2 * n + 1], P);
+    const unsigned long long slot = atomicAdd(cursor + o, 1ull);
+    uint64_t* r = out + slot * f.W;
+    r[0] = h[2 * n];
+    r[1] = h[2 * n + 1];
+    const uint32_t p = n ? parent[n] : 0;
+    r[2] = n ? h[2ull * p] : 0;
+    r[3] = n ? h[2ull * p + 1] : 0;
+    const uint32_t gf = n ? (l2g ? l2g[frame[n]] : frame[n]) : DC_NO_NODE;
+    r[4] = (uint64_t)gf | ((uint64_t)depth[n] << 32);
+    r[5] = xcnt[n];
+    r[6] = icnt[n];
+    for (uint32_t m = 0; m < f.M; ++m)
+      for (uint32_t w = 0; w < 8; ++w) r[7 + 8 * m + w] = mcols[((uint64_t)w * f.M + m) * N + n];
+    if (f.has_pc) {
+      uint64_t* q = r + 7 + 8 * f.M;
+      q[0] = xs[n];
+      q[1] = is[n];
+      for (uint32_t s = 0; s < f.S; ++s) {
+        q[2 + 2 * s] = xst[(uint64_t)s * N + n];
+        q[3 + 2 * s] = ist[(uint64_t)s * N + n];
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t bin_owner(uint64_t hlo, uint64_t hi, uint32_t pc, uint32_t P) {
+  return owner_of(mix64(hi ^ hlo ^ ((uint64_t)pc * 0xD1B54A32D192ED03ull)), P);
+}
+
+// bins of a local tree -> (h_ctx, pc | stall << 32, count) records, per owner
+__global__ void k_part_bins(const uint64_t* __restrict__ h, const uint32_t* __restrict__ bin_pcnode, const uint16_t* __restrict__ bin_stall,
+                            const uint64_t* __restrict__ bin_count, const uint32_t* __restrict__ pc_ctx,
+                            const uint32_t* __restrict__ pc_off, uint64_t N, uint64_t nb, uint32_t P, int count_only,
+                            unsigned long long* cnt_or_cursor, uint64_t* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nb; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t pn = bin_pcnode[i] - (uint32_t)N;
+    const uint32_t ctx = pc_ctx[pn], pc = pc_off[pn];
+    const uint64_t lo = h[2ull * ctx], hi = h[2ull * ctx + 1];
+    const uint32_t o = bin_owner(lo, hi, pc, P);
+    const unsigned long long slot = atomicAdd(cnt_or_cursor + o, 1ull);
+    if (count_only) continue;
+    uint64_t* r = out + slot * BIN_W;
+    r[0] = lo;
+    r[1] = hi;
+    r[2] = (uint64_t)pc | ((uint64_t)bin_stall[i] << 32);
+    r[3] = bin_count[i];
+  }
+}
+
+// ---------------------------------------------------------------- reduce received records
+__global__ void k_rec_key(const uint64_t* __restrict__ rec, uint32_t W, uint64_t n, int word, const uint32_t* __restrict__ order,
+                          uint64_t* __restrict__ key, uint32_t* __restrict__ val) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t src = order ? order[i] : (uint32_t)i;
+    key[i] = rec[(uint64_t)src * W + word];
+    val[i] = src;
+  }
+}
+
+// sort record indices by (words wlo, whi) as a 128-bit key (LSD: low word, then high word)
+static dc_status sort_recs128(Ctx* c, const uint64_t* rec, uint32_t W, uint64_t n, int wlo, int whi, Buf<uint32_t>& order) {
+  Buf<uint64_t> k0, k1;
+  Buf<uint32_t> v0, v1;
+  DC_TRY(alloc(c, k0, n));
+  DC_TRY(alloc(c, k1, n));
+  DC_TRY(alloc(c, v0, n));
+  DC_TRY(alloc(c, v1, n));
+  k_rec_key<<<grid_for(c, n, 256), 256, 0, c->stream>>>(rec, W, n, wlo, nullptr, k0.p, v0.p);
+  DC_LAUNCHED(c);
+  bool in1 = false;
+  DC_TRY(radix_sort_pairs(c, k0.p, v0.p, k1.p, v1.p, n, 0, 64, &in1));
+  uint32_t* ord = in1 ? v1.p : v0.p;
+  // second key in the current order
+  k_rec_key<<<grid_for(c, n, 256), 256, 0, c->stream>>>(rec, W, n, whi, ord, in1 ? k0.p : k1.p, in1 ? v0.p : v1.p);
+  DC_LAUNCHED(c);
+  // the gather above wrote (key_hi, idx) into the "other" buffers; sort them stably
+  uint64_t* ka = in1 ? k0.p : k1.p;
+  uint32_t* va = in1 ? v0.p : v1.p;
+  uint64_t* kb = in1 ? k1.p : k0.p;
+  uint32_t* vb = in1 ? v1.p : v0.p;
+  bool in2 = false;
+  DC_TRY(radix_sort_pairs(c, ka, va, kb, vb, n, 0, 64, &in2));
+  DC_TRY(alloc(c, order, n));
+  DC_CUDA(c, cudaMemcpyAsync(order.p, in2 ? vb : va, n * 4, cudaMemcpyDeviceToDevice, c->stream));
+  return DC_OK;
+}
+
+__global__ void k_run_heads(const uint64_t* __restrict__ rec, uint32_t W, const uint32_t* __restrict__ order, uint64_t n, int w0,
+                            int w1, uint32_t* __restrict__ head) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    bool hd = i == 0;
+    if (!hd) {
+      const uint64_t* a = rec + (uint64_t)order[i - 1] * W;
+      const uint64_t* b = rec + (uint64_t)order[i] * W;
+      for (int w = w0; w <= w1; ++w) hd |= a[w] != b[w];
+    }
+    head[i] = hd ? 1u : 0u;
+  }
+}
+
+// combine a run of node records (run heads only): sums, mins; verify parent hash, frame, depth
+__global__ void k_combine_nodes(const uint64_t* __restrict__ rec, const uint32_t* __restrict__ order, const uint32_t* __restrict__ head,
+                                const uint32_t* __restrict__ run_ix, uint64_t n, RecFmt f, uint64_t* __restrict__ out,
+                                uint32_t* d_collision) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    if (!head[i]) continue;
+    uint64_t* o = out + (uint64_t)run_ix[i] * f.W;
+    const uint64_t* a = rec + (uint64_t)order[i] * f.W;
+    for (uint32_t w = 0; w < f.W; ++w) o[w] = a[w];
+    for (uint64_t j = i + 1; j < n && !head[j]; ++j) {
+      const uint64_t* b = rec + (uint64_t)order[j] * f.W;
+      if (b[2] != a[2] || b[3] != a[3] || b[4] != a[4]) atomicOr(d_collision, 1u);
+      o[5] += b[5];
+      o[6] += b[6];
+      for (uint32_t m = 0; m < f.M; ++m) {
+        uint64_t* om = o + 7 + 8 * m;
+        const uint64_t* bm = b + 7 + 8 * m;
+        om[0] += bm[0];
+        om[1] = min(om[1], bm[1]);
+        uint64_t lo = om[2] + bm[2];
+        om[3] += bm[3] + (lo < om[2] ? 1u : 0u);
+        om[2] = lo;
+        om[4] += bm[4];
+        om[5] = min(om[5], bm[5]);
+        lo = om[6] + bm[6];
+        om[7] += bm[7] + (lo < om[6] ? 1u : 0u);
+        om[6] = lo;
+      }
+      if (f.has_pc)
+        for (uint32_t w = 7 + 8 * f.M; w < f.W; ++w) o[w] += b[w];
+    }
+  }
+}
+
+__global__ void k_combine_bins(const uint64_t* __restrict__ rec, const uint32_t* __restrict__ order, const uint32_t* __restrict__ head,
+                               const uint32_t* __restrict__ run_ix, uint64_t n, uint64_t* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    if (!head[i]) continue;
+    uint64_t* o = out + (uint64_t)run_ix[i] * BIN_W;
+    const uint64_t* a = rec + (uint64_t)order[i] * BIN_W;
+    o[0] = a[0];
+    o[1] = a[1];
+    o[2] = a[2];
+    uint64_t s = a[3];
+    for (uint64_t j = i + 1; j < n && !head[j]; ++j) s += rec[(uint64_t)order[j] * BIN_W + 3];
+    o[3] = s;
+  }
+}
+
+// sort + combine: records -> unique records (count returned)
+static dc_status reduce_records(Ctx* c, const uint64_t* rec, uint64_t n, uint32_t W, bool bins, const RecFmt& f,
+                                Buf<uint64_t>& out, uint64_t* n_out, uint32_t* d_collision) {
+  *n_out = 0;
+  if (n == 0) {
+    DC_TRY(alloc(c, out, 1));
+    return DC_OK;
+  }
+  Buf<uint32_t> order, head, run;
+  Buf<uint32_t> tot;
+  (void)bins;
+  DC_TRY(sort_recs128(c, rec, W, n, 0, 1, order));
+  DC_TRY(alloc(c, head, n));
+  DC_TRY(alloc(c, run, n));
+  DC_TRY(alloc(c, tot, 1));
+  k_run_heads<<<grid_for(c, n, 256), 256, 0, c->stream>>>(rec, W, order.p, n, 0, 1, head.p);
+  DC_LAUNCHED(c);
+  DC_TRY(excl_scan<uint32_t>(c, head.p, run.p, n, tot.p));
+  uint32_t hn = 0;
+  DC_TRY(readback(c, tot.p, 4, &hn));
+  DC_TRY(alloc(c, out, (uint64_t)hn * W));
+  k_combine_nodes<<<grid_for(c, n, 256), 256, 0, c->stream>>>(rec, order.p, head.p, run.p, n, f, out.p, d_collision);
+  DC_LAUNCHED(c);
+  *n_out = hn;
+  return DC_OK;
+}
+
+__global__ void k_gather_recs(const uint64_t* __restrict__ rec, uint32_t W, const uint32_t* __restrict__ order, uint64_t n,
+                              uint64_t* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n * W; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = i / W, w = i % W;
+    out[i] = rec[(uint64_t)order[r] * W + w];
+  }
+}
+
+// bins: sort by (h_lo, h_hi, pc|stall) = LSD word 2, then 0, then 1; combine counts
+static dc_status reduce_bins(Ctx* c, const uint64_t* rec, uint64_t n, Buf<uint64_t>& out, uint64_t* n_out) {
+  *n_out = 0;
+  if (n == 0) {
+    DC_TRY(alloc(c, out, 1));
+    return DC_OK;
+  }
+  Buf<uint64_t> k0, k1, sorted;
+  Buf<uint32_t> v0, v1, head, run, tot;
+  DC_TRY(alloc(c, k0, n));
+  DC_TRY(alloc(c, k1, n));
+  DC_TRY(alloc(c, v0, n));
+  DC_TRY(alloc(c, v1, n));
+  const uint32_t* ord = nullptr;
+  bool in1 = false;
+  for (int word : {2, 0, 1}) {
+    uint64_t* kin = in1 ? k1.p : k0.p;
+    uint32_t* vin = in1 ? v1.p : v0.p;
+    uint64_t* kout = in1 ? k0.p : k1.p;
+    uint32_t* vout = in1 ? v0.p : v1.p;
+    k_rec_key<<<grid_for(c, n, 256), 256, 0, c->stream>>>(rec, BIN_W, n, word, ord, kin, vin);
+    DC_LAUNCHED(c);
+    bool r1 = false;
+    DC_TRY(radix_sort_pairs(c, kin, vin, kout, vout, n, 0, 64, &r1));
+    if (r1) in1 = !in1;
+    ord = in1 ? v1.p : v0.p;
+  }
+  DC_TRY(alloc(c, head, n));
+  DC_TRY(alloc(c, run, n));
+  DC_TRY(alloc(c, tot, 1));
+  k_run_heads<<<grid_for(c, n, 256), 256, 0, c->stream>>>(rec, BIN_W, ord, n, 0, 2, head.p);
+  DC_LAUNCHED(c);
+  DC_TRY(excl_scan<uint32_t>(c, head.p, run.p, n, tot.p));
+  uint32_t hn = 0;
+  DC_TRY(readback(c, tot.p, 4, &hn));
+  DC_TRY(alloc(c, out, (uint64_t)hn * BIN_W));
+  k_combine_bins<<<grid_for(c, n, 256), 256, 0, c->stream>>>(rec, ord, head.p, run.p, n, out.p);
+  DC_LAUNCHED(c);
+  *n_out = hn;
+  return DC_OK;
+}
+
+// ---------------------------------------------------------------- per-rank partition step
+struct Slabs {
+  Buf<uint64_t> nodes, bins;
+  std::vector<uint64_t> ncnt, bcnt;  // per destination
+};
+
+static dc_status partition(Ctx* c, const dc_cct* t, const uint32_t* l2g, uint32_t P, const RecFmt& f, Slabs& s) {
+  const uint64_t N = t->N;
+  Buf<uint64_t> h;
+  DC_TRY(alloc(c, h, 2 * N));
+  k_hash_root<<<1, 1, 0, c->stream>>>(h.p);
+  DC_LAUNCHED(c);
+  std::vector<uint32_t> lo(t->max_depth + 2);
+  DC_TRY(readback(c, t->level_off, lo.size() * 4, lo.data()));
+  for (uint32_t d = 1; d <= t->max_depth; ++d) {
+    const uint32_t a = lo[d], b = lo[d + 1];
+    if (b > a) {
+      k_hash_level<<<grid_for(c, b - a, 256), 256, 0, c->stream>>>(t->parent, t->frame, l2g, a, b, h.p, c->merge_mask);
+      DC_LAUNCHED(c);
+    }
+  }
+  Buf<unsigned long long> cnt, cur;
+  DC_TRY(alloc_zero(c, cnt, 2 * P));
+  DC_TRY(alloc(c, cur, 2 * P));
+  k_part_count<<<grid_for(c, N, 256), 256, 0, c->stream>>>(h.p, N, P, cnt.p);
+  DC_LAUNCHED(c);
+  if (t->Nbins)
+    k_part_bins<<<grid_for(c, t->Nbins, 256), 256, 0, c->stream>>>(h.p, t->bin_pcnode, t->bin_stall, t->bin_count, t->pc_ctx,
+                                                                   t->pc_off, N, t->Nbins, P, 1, cnt.p + P, nullptr);
+  DC_LAUNCHED(c);
+  std::vector<uint64_t> hc(2 * P);
+  DC_TRY(readback(c, cnt.p, 16 * P, hc.data()));
+  s.ncnt.assign(hc.begin(), hc.begin() + P);
+  s.bcnt.assign(hc.begin() + P, hc.end());
+  std::vector<uint64_t> ex(2 * P);
+  uint64_t an = 0, ab = 0;
+  for (uint32_t q = 0; q < P; ++q) {
+    ex[q] = an;
+    an += s.ncnt[q];
+    ex[P + q] = ab;
+    ab += s.bcnt[q];
+  }
+  DC_CUDA(c, cudaMemcpyAsync(cur.p, ex.data(), 16 * P, cudaMemcpyHostToDevice, c->stream));
+  DC_TRY(alloc(c, s.nodes, an * f.W));
+  DC_TRY(alloc(c, s.bins, ab * BIN_W));
+  const uint64_t* mc = t->mcols;
+  k_part_nodes<<<grid_for(c, N, 256), 256, 0, c->stream>>>(h.p, t->parent, t->frame, t->depth, l2g, t->xcnt, t->icnt, mc,
+                                                           t->xsamples, t->isamples, t->xstall, t->istall, N, f, P, cur.p,
+                                                           s.nodes.p);
+  DC_LAUNCHED(c);
+  if (t->Nbins) {
+    k_part_bins<<<grid_for(c, t->Nbins, 256), 256, 0, c->stream>>>(h.p, t->bin_pcnode, t->bin_stall, t->bin_count, t->pc_ctx,
+                                                                   t->pc_off, N, t->Nbins, P, 0, cur.p + P, s.bins.p);
+    DC_LAUNCHED(c);
+  }
+  DC_CUDA(c, cudaStreamSynchronize(c->stream));  // ex[] (host) must outlive the async copy
+  return DC_OK;
+}
+
+// a merged partition: unique node records + unique bin records (kept in record form)
+static dc_cct* make_partition(Ctx* c, const RecFmt& f, uint64_t n_nodes, Buf<uint64_t>& nodes, uint64_t n_bins,
+                              Buf<uint64_t>& bins, uint32_t n_frames) {
+  dc_cct* t = new dc_cct();
+  t->device = c->device;
+  t->M = f.M;
+  t->S = f.has_pc ? f.S : 0;
+  t->N = n_nodes;
+  t->n_frames = n_frames;
+  t->state = 2;
+  t->partition = true;
+  t->part_nodes = nodes.release_ownership();
+  t->part_bins = bins.release_ownership();
+  t->part_nbins = n_bins;
+  t->part_W = f.W;
+  t->part_has_pc = f.has_pc;
+  return t;
+}
+
+// ---------------------------------------------------------------- canonicalisation (gather)
+// all unique node records (any order) -> canonical CCT
+__global__ void k_canon_depthkey(const uint64_t* __restrict__ rec, uint32_t W, uint64_t n, uint64_t* __restrict__ key,
+                                 uint32_t* __restrict__ val) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    key[i] = rec[i * W + 4] >> 32;  // depth
+    val[i] = (uint32_t)i;
+  }
+}
+
+// hash table h(128) -> canonical id
+__device__ __forceinline__ uint64_t htab_slot(uint64_t lo, uint64_t hi, uint64_t mask) { return mix64(lo ^ (hi * 3)) & mask; }
+__global__ void k_htab_insert(const uint64_t* __restrict__ rec, uint32_t W, const uint32_t* __restrict__ order, uint32_t a, uint32_t b,
+                              const uint32_t* __restrict__ canon_of_pos, ulonglong2* tab, uint32_t* tid, uint64_t mask) {
+  for (uint32_t i = a + blockIdx.x * blockDim.x + threadIdx.x; i < b; i += gridDim.x * blockDim.x) {
+    const uint64_t* r = rec + (uint64_t)order[i] * W;
+    const uint64_t lo = r[0], hi = r[1];
+    uint64_t s = htab_slot(lo, hi, mask);
+    while (true) {
+      unsigned __int128 expect = ~(unsigned __int128)0;
+      unsigned __int128 want = ((unsigned __int128)hi << 64) | lo;
+      unsigned __int128 old = atomicCAS(reinterpret_cast<unsigned __int128*>(tab + s), expect, want);
+      if (old == expect || old == want) break;
+      s = (s + 1) & mask;
+    }
+    tid[s] = canon_of_pos[i];
+  }
+}
+__device__ __forceinline__ uint32_t htab_find(const ulonglong2* tab, const uint32_t* tid, uint64_t mask, uint64_t lo, uint64_t hi) {
+  uint64_t s = htab_slot(lo, hi, mask);
+  while (true) {
+    ulonglong2 v = tab[s];
+    if (v.x == lo && v.y == hi) return tid[s];
+    if (v.x == ~0ull && v.y == ~0ull) return DC_NO_NODE;
+    s = (s + 1) & mask;
+  }
+}
+
+// level d: key = (parent canonical id - level_start(d-1)) << fbits | gframe for records order[a..b)
+__global__ void k_canon_keys(const uint64_t* __restrict__ rec, uint32_t W, const uint32_t* __restrict__ order, uint32_t a, uint32_t b,
+                             const ulonglong2* __restrict__ tab, const uint32_t* __restrict__ tid, uint64_t mask, uint32_t prev_start,
+                             int fbits, uint64_t* __restrict__ key, uint32_t* __restrict__ val, uint32_t* d_err) {
+  for (uint32_t i = a + blockIdx.x * blockDim.x + threadIdx.x; i < b; i += gridDim.x * blockDim.x) {
+    const uint64_t* r = rec + (uint64_t)order[i] * W;
+    const uint32_t p = htab_find(tab, tid, mask, r[2], r[3]);
+    if (p == DC_NO_NODE) atomicOr(d_err, 1u);
+    key[i - a] = ((uint64_t)(p - prev_start) << fbits) | (uint32_t)r[4];
+    val[i - a] = order[i];
+  }
+}
+
+__global__ void k_canon_emit(const uint64_t* __restrict__ rec, RecFmt f, const uint32_t* __restrict__ src, uint64_t n_level,
+                             const uint64_t* __restrict__ key, int fbits, uint32_t prev_start, uint32_t start, uint64_t N,
+                             uint32_t* __restrict__ parent, uint32_t* __restrict__ frame, uint16_t* __restrict__ depth,
+                             uint64_t* __restrict__ xcnt, uint64_t* __restrict__ icnt, uint64_t* __restrict__ mcols,
+                             uint64_t* __restrict__ xs, uint64_t* __restrict__ is, uint64_t* __restrict__ xst,
+                             uint64_t* __restrict__ ist, uint32_t* __restrict__ canon_of_pos, uint32_t dpt) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n_level; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t id = start + (uint32_t)i;
+    const uint64_t* r = rec + (uint64_t)src[i] * f.W;
+    parent[id] = dpt == 0 ? DC_NO_NODE : prev_start + (uint32_t)(key[i] >> fbits);
+    frame[id] = dpt == 0 ? DC_NO_NODE : (uint32_t)r[4];
+    depth[id] = (uint16_t)dpt;
+    xcnt[id] = r[5];
+    icnt[id] = r[6];
+    for (uint32_t m = 0; m < f.M; ++m)
+      for (uint32_t w = 0; w < 8; ++w) mcols[((uint64_t)w * f.M + m) * N + id] = r[7 + 8 * m + w];
+    if (f.has_pc) {
+      const uint64_t* q = r + 7 + 8 * f.M;
+      xs[id] = q[0];
+      is[id] = q[1];
+      for (uint32_t s = 0; s < f.S; ++s) {
+        xst[(uint64_t)s * N + id] = q[2 + 2 * s];
+        ist[(uint64_t)s * N + id] = q[3 + 2 * s];
+      }
+    }
+    canon_of_pos[i] = id;
+  }
+}
+
+// bins -> (ctx canonical, pc, stall) sort keys
+__global__ void k_canon_binkeys(const uint64_t* __restrict__ bins, uint64_t nb, const ulonglong2* __restrict__ tab,
+                                const uint32_t* __restrict__ tid, uint64_t mask, int pcb, uint64_t* __restrict__ key,
+                                uint32_t* __restrict__ val, uint32_t* d_err) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nb; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t* r = bins + i * BIN_W;
+    const uint32_t ctx = htab_find(tab, tid, mask, r[0], r[1]);
+    if (ctx == DC_NO_NODE) atomicOr(d_err, 1u);
+    const uint32_t pc = (uint32_t)r[2], stall = (uint32_t)(r[2] >> 32);
+    key[i] = ((((uint64_t)ctx << pcb) | pc) << 5) | stall;
+    val[i] = (uint32_t)i;
+  }
+}
+__global__ void k_canon_binmax(const uint64_t* __restrict__ bins, uint64_t nb, unsigned int* mx) {
+  uint32_t m = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nb; i += (uint64_t)gridDim.x * blockDim.x)
+    m = max(m, (uint32_t)bins[i * BIN_W + 2]);
+  for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane_id() == 0 && m) atomicMax(mx, m);
+}
+__global__ void k_canon_binheads(const uint64_t* __restrict__ key, uint64_t nb, uint32_t* __restrict__ head) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nb; i += (uint64_t)gridDim.x * blockDim.x)
+    head[i] = (i == 0 || (key[i - 1] >> 5) != (key[i] >> 5)) ? 1u : 0u;
+}
+__global__ void k_canon_binemit(const uint64_t* __restrict__ key, const uint32_t* __restrict__ val, const uint64_t* __restrict__ bins,
+                                uint64_t nb, int pcb, const uint32_t* __restrict__ head, const uint32_t* __restrict__ run, uint64_t N,
+                                uint32_t* __restrict__ pc_ctx, uint32_t* __restrict__ pc_off, uint32_t* __restrict__ bin_pcnode,
+                                uint16_t* __restrict__ bin_stall, uint64_t* __restrict__ bin_count) {
+  const uint64_t pm = (1ull << pcb) - 1ull;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nb; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = key[i];
+    const uint32_t p = run[i] + head[i] - 1u;
+    if (head[i]) {
+      pc_ctx[p] = (uint32_t)((k >> 5) >> pcb);
+      pc_off[p] = (uint32_t)((k >> 5) & pm);
+    }
+    bin_pcnode[i] = (uint32_t)(N + p);
+    bin_stall[i] = (uint16_t)(k & 31u);
+    bin_count[i] = bins[(uint64_t)val[i] * BIN_W + 3];
+  }
+}
+
+static dc_status canonicalize(Ctx* c, const uint64_t* rec, uint64_t n, const uint64_t* bins, uint64_t nb, const RecFmt& f,
+                              uint32_t n_frames, dc_cct** out) {
+  *out = nullptr;
+  if (n == 0) return fail(c, DC_ERR_STATE, "merge: no node records (the root is missing)");
+  // order by depth (stable)
+  Buf<uint64_t> k0, k1;
+  Buf<uint32_t> v0, v1;
+  DC_TRY(alloc(c, k0, n));
+  DC_TRY(alloc(c, k1, n));
+  DC_TRY(alloc(c, v0, n));
+  DC_TRY(alloc(c, v1, n));
+  k_canon_depthkey<<<grid_for(c, n, 256), 256, 0, c->stream>>>(rec, f.W, n, k0.p, v0.p);
+  DC_LAUNCHED(c);
+  bool in1 = false;
+  DC_TRY(radix_sort_pairs(c, k0.p, v0.p, k1.p, v1.p, n, 0, 16, &in1));
+  Buf<uint32_t> byd;  // record indices ordered by depth
+  DC_TRY(alloc(c, byd, n));
+  DC_CUDA(c, cudaMemcpyAsync(byd.p, in1 ? v1.p : v0.p, n * 4, cudaMemcpyDeviceToDevice, c->stream));
+  std::vector<uint64_t> dk(n);
+  DC_TRY(readback(c, in1 ? k1.p : k0.p, n * 8, dk.data()));
+  // level boundaries
+  std::vector<uint32_t> lvl;
+  for (uint64_t i = 0; i < n; ++i)
+    if (i == 0 || dk[i] != dk[i - 1]) {
+      if (dk[i] != lvl.size()) return fail(c, DC_ERR_COLLISION, "merge: depth levels are not contiguous");
+      lvl.push_back((uint32_t)i);
+    }
+  lvl.push_back((uint32_t)n);
+  const uint32_t L = (uint32_t)lvl.size() - 1;
+  if (lvl[1] != 1) return fail(c, DC_ERR_COLLISION, "merge: %u root records", lvl[1]);
+  dc_cct* t = new dc_cct();
+  t->device = c->device;
+  t->N = n;
+  t->n_frames = n_frames;
+  t->max_depth = L - 1;
+  t->S = f.has_pc ? f.S : 0;
+  DC_TRY(palloc(c, t->parent, n));
+  DC_TRY(palloc(c, t->frame, n));
+  DC_TRY(palloc(c, t->depth, n));
+  DC_TRY(palloc(c, t->level_off, L + 1));
+  DC_CUDA(c, cudaMemcpyAsync(t->level_off, lvl.data(), (L + 1) * 4, cudaMemcpyHostToDevice, c->stream));
+  DC_TRY(palloc(c, t->xcnt, n));
+  DC_TRY(palloc(c, t->icnt, n));
+  if (f.M) {
+    t->M = 0;
+    DC_TRY(ensure_metric_cols(c, t, f.M));
+  }
+  if (f.has_pc) {
+    DC_TRY(palloc(c, t->xsamples, n));
+    DC_TRY(palloc(c, t->isamples, n));
+    DC_TRY(palloc(c, t->xstall, (uint64_t)f.S * n));
+    DC_TRY(palloc(c, t->istall, (uint64_t)f.S * n));
+  }
+  uint64_t cap = 1024;
+  while (cap < 2 * n) cap <<= 1;
+  Buf<ulonglong2> tab;
+  Buf<uint32_t> tid, canon, err;
+  DC_TRY(alloc(c, tab, cap));
+  DC_TRY(alloc(c, tid, cap));
+  DC_TRY(alloc(c, canon, n));
+  DC_TRY(alloc_zero(c, err, 1));
+  DC_CUDA(c, cudaMemsetAsync(tab.p, 0xFF, cap * 16, c->stream));
+  const int fbits = bits_for(n_frames > 1 ? n_frames - 1 : 1);
+  uint32_t prev_start = 0;
+  for (uint32_t d = 0; d < L; ++d) {
+    const uint32_t a = lvl[d], b = lvl[d + 1], m = b - a;
+    const uint32_t* src;
+    uint64_t* keys = k0.p;
+    if (d == 0) {
+      src = byd.p;
+      DC_CUDA(c, cudaMemsetAsync(k0.p, 0, 8, c->stream));
+    } else {
+      const int pbits = bits_for(lvl[d] - lvl[d - 1] > 1 ? lvl[d] - lvl[d - 1] - 1 : 1);
+      k_canon_keys<<<grid_for(c, m, 256), 256, 0, c->stream>>>(rec, f.W, byd.p, a, b, tab.p, tid.p, cap - 1, prev_start, fbits,
+                                                               k0.p, v0.p, err.p);
+      DC_LAUNCHED(c);
+      bool r1 = false;
+      DC_TRY(radix_sort_pairs(c, k0.p, v0.p, k1.p, v1.p, m, 0, pbits + fbits, &r1));
+      keys = r1 ? k1.p : k0.p;
+      src = r1 ? v1.p : v0.p;
+    }
+    k_canon_emit<<<grid_for(c, m, 256), 256, 0, c->stream>>>(rec, f, src, m, keys, fbits, prev_start, a, n, t->parent, t->frame,
+                                                             t->depth, t->xcnt, t->icnt, t->mcols, t->xsamples, t->isamples,
+                                                             t->xstall, t->istall, canon.p, d);
+    DC_LAUNCHED(c);
+    // register this level's hashes: position i (in emit order) -> canonical id a + i
+    // (emit order == src order; insert needs the record index per position)
+    k_htab_insert<<<grid_for(c, m, 256), 256, 0, c->stream>>>(rec, f.W, src, 0, m, canon.p, tab.p, tid.p, cap - 1);
+    DC_LAUNCHED(c);
+    prev_start = a;
+  }
+  uint32_t herr = 0;
+  DC_TRY(readback(c, err.p, 4, &herr));
+  if (herr) return fail(c, DC_ERR_COLLISION, "merge: a node's parent hash was not found at the previous level");
+  // bins
+  if (f.has_pc && nb) {
+    Buf<uint64_t> bk0, bk1;
+    Buf<uint32_t> bv0, bv1, head, run, tot;
+    Buf<unsigned int> mx;
+    DC_TRY(alloc(c, bk0, nb));
+    DC_TRY(alloc(c, bk1, nb));
+    DC_TRY(alloc(c, bv0, nb));
+    DC_TRY(alloc(c, bv1, nb));
+    DC_TRY(alloc_zero(c, mx, 1));
+    k_canon_binmax<<<grid_for(c, nb, 256), 256, 0, c->stream>>>(bins, nb, mx.p);
+    DC_LAUNCHED(c);
+    uint32_t hm = 0;
+    DC_TRY(readback(c, mx.p, 4, &hm));
+    const int pcb = bits_for(hm) ? bits_for(hm) : 1;
+    k_canon_binkeys<<<grid_for(c, nb, 256), 256, 0, c->stream>>>(bins, nb, tab.p, tid.p, cap - 1, pcb, bk0.p, bv0.p, err.p);
+    DC_LAUNCHED(c);
+    bool r1 = false;
+    DC_TRY(radix_sort_pairs(c, bk0.p, bv0.p, bk1.p, bv1.p, nb, 0, bits_for(n) + pcb + 5, &r1));
+    uint64_t* sk = r1 ? bk1.p : bk0.p;
+    uint32_t* sv = r1 ? bv1.p : bv0.p;
+    DC_TRY(alloc(c, head, nb));
+    DC_TRY(alloc(c, run, nb));
+    DC_TRY(alloc(c, tot, 1));
+    k_canon_binheads<<<grid_for(c, nb, 256), 256, 0, c->stream>>>(sk, nb, head.p);
+    DC_LAUNCHED(c);
+    DC_TRY(excl_scan<uint32_t>(c, head.p, run.p, nb, tot.p));
+    uint32_t npc = 0;
+    DC_TRY(readback(c, tot.p, 4, &npc));
+    t->Npc = npc;
+    t->Nbins = nb;
+    DC_TRY(palloc(c, t->pc_ctx, npc));
+    DC_TRY(palloc(c, t->pc_off, npc));
+    DC_TRY(palloc(c, t->bin_pcnode, nb));
+    DC_TRY(palloc(c, t->bin_stall, nb));
+    DC_TRY(palloc(c, t->bin_count, nb));
+    k_canon_binemit<<<grid_for(c, nb, 256), 256, 0, c->stream>>>(sk, sv, bins, nb, pcb, head.p, run.p, n, t->pc_ctx, t->pc_off,
+                                                                 t->bin_pcnode, t->bin_stall, t->bin_count);
+    DC_LAUNCHED(c);
+  }
+  t->pc_done = f.has_pc;
+  t->state = 2;
+  *out = t;
+  return DC_OK;
+}
+
+// ---------------------------------------------------------------- dictionary unify
+__global__ void k_l2g(const uint32_t* __restrict__ ids, uint64_t base, uint64_t D, uint32_t* __restrict__ l2g) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < D; i += (uint64_t)gridDim.x * blockDim.x)
+    l2g[i] = ids[base + i];
+}
+
+// keys of P dictionaries concatenated (key_off[p] .. key_off[p+1]) -> global dict + per-p l2g maps
+static dc_status unify_dicts(Ctx* c, const dc_frame_key* all_keys, const std::vector<uint64_t>& key_off, dc_dict** gdict,
+                             std::vector<Buf<uint32_t>>& l2g) {
+  const uint64_t total = key_off.back();
+  Buf<uint32_t> ids;
+  DC_TRY(alloc(c, ids, total));
+  DC_TRY(intern_frames(c, all_keys, total, ids.p, gdict));
+  l2g.resize(key_off.size() - 1);
+  for (size_t p = 0; p + 1 < key_off.size(); ++p) {
+    const uint64_t D = key_off[p + 1] - key_off[p];
+    DC_TRY(alloc(c, l2g[p], D));
+    if (D) {
+      k_l2g<<<grid_for(c, D, 256), 256, 0, c->stream>>>(ids.p, key_off[p], D, l2g[p].p);
+      DC_LAUNCHED(c);
+    }
+  }
+  DC_CUDA(c, cudaStreamSynchronize(c->stream));
+  return DC_OK;
+}
+
+static RecFmt fmt_of(const dc_cct* t) { return rec_fmt(t->M, t->S, t->xsamples != nullptr); }
+
+}  // namespace dc
+
+using namespace dc;
+
+// ---------------------------------------------------------------- NCCL communicator
+struct dc_comm {
+  int nranks = 1, rank = 0, device = 0;
+#if DC_HAVE_NCCL
+  ncclComm_t comm = nullptr;
+#endif
+};
+
+#if DC_HAVE_NCCL
+#define NCCL_TRY(c, expr)                                                                       \
+  do {                                                                                          \
+    ncclResult_t _r = (expr);                                                                   \
+    if (_r != ncclSuccess) return fail((c), DC_ERR_NCCL, "%s: %s", #expr, ncclGetErrorString(_r)); \
+  } while (0)
+#endif
 
 extern "C" {
-dc_status dc_nccl_unique_id(uint8_t out_h[128]) { return DC_ERR_STATE; }
-dc_status dc_comm_create(dc_ctx* ctx, const uint8_t uid[128], int nranks, int rank, dc_comm** out) { return DC_ERR_STATE; }
-void dc_comm_destroy(dc_comm* comm) {}
-dc_status dc_cct_merge_ranks(dc_ctx* ctx, dc_comm* comm, const dc_cct* local, const dc_dict* local_dict,
-                             dc_cct** out_partition, dc_dict** out_global_dict) { return DC_ERR_STATE; }
-dc_status dc_cct_gather(dc_ctx* ctx, dc_comm* comm, const dc_cct* part, int root, dc_cct** out_canonical) { return DC_ERR_STATE; }
+
+dc_status dc_nccl_unique_id(uint8_t out_h[128]) {
+#if DC_HAVE_NCCL
+  if (!out_h) return DC_ERR_ARG;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return DC_ERR_NCCL;
+  memcpy(out_h, id.internal, 128);
+  return DC_OK;
+#else
+  return DC_ERR_NCCL;
+#endif
 }
+
+dc_status dc_comm_create(dc_ctx* ctx, const uint8_t uid[128], int nranks, int rank, dc_comm** out) {
+  if (!ctx || !uid || !out || nranks < 1 || rank < 0 || rank >= nranks) return DC_ERR_ARG;
+#if DC_HAVE_NCCL
+  cudaSetDevice(ctx->device);
+  dc_comm* cm = new dc_comm();
+  cm->nranks = nranks;
+  cm->rank = rank;
+  cm->device = ctx->device;
+  ncclUniqueId id;
+  memcpy(id.internal, uid, 128);
+  ncclResult_t r = ncclCommInitRank(&cm->comm, nranks, id, rank);
+  if (r != ncclSuccess) {
+    delete cm;
+    return fail(ctx, DC_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+  }
+  *out = cm;
+  return DC_OK;
+#else
+  return fail(ctx, DC_ERR_NCCL, "built without NCCL");
+#endif
+}
+
+void dc_comm_destroy(dc_comm* cm) {
+  if (!cm) return;
+#if DC_HAVE_NCCL
+  if (cm->comm) ncclCommDestroy(cm->comm);
+#endif
+  delete cm;
+}
+
+dc_status dc_cct_merge_ranks(dc_ctx* ctx, dc_comm* cm, const dc_cct* local, const dc_dict* local_dict, dc_cct** out_partition,
+                             dc_dict** out_global_dict) {
+  if (!ctx || !cm || !local || !local_dict || !out_partition || !out_global_dict) return DC_ERR_ARG;
+  if (local->state != 2 || local->partition) return fail(ctx, DC_ERR_STATE, "dc_cct_merge_ranks needs a rolled-up local tree");
+  if (local_dict->D != local->n_frames) return fail(ctx, DC_ERR_ARG, "dictionary size != tree n_frames");
+#if DC_HAVE_NCCL
+  Ctx* c = ctx;
+  DC_CUDA(c, cudaSetDevice(c->device));
+  Region rg(c, "merge");
+  const int P = cm->nranks;
+  // 1. dictionaries: all-gather sizes, then keys padded to the max size
+  Buf<uint64_t> dsz;
+  DC_TRY(alloc(c, dsz, P));
+  uint64_t myD = local_dict->D;
+  DC_CUDA(c, cudaMemcpyAsync(dsz.p + cm->rank, &myD, 8, cudaMemcpyHostToDevice, c->stream));
+  NCCL_TRY(c, ncclAllGather(dsz.p + cm->rank, dsz.p, 1, ncclUint64, cm->comm, c->stream));
+  std::vector<uint64_t> Ds(P);
+  DC_TRY(readback(c, dsz.p, 8 * P, Ds.data()));
+  uint64_t Dmax = 1;
+  for (auto d : Ds) Dmax = d > Dmax ? d : Dmax;
+  Buf<dc_frame_key> pad, all, packed;
+  DC_TRY(alloc(c, pad, Dmax));
+  DC_TRY(alloc(c, all, Dmax * P));
+  if (myD) DC_CUDA(c, cudaMemcpyAsync(pad.p, local_dict->keys, myD * 16, cudaMemcpyDeviceToDevice, c->stream));
+  NCCL_TRY(c, ncclAllGather(pad.p, all.p, Dmax * 2, ncclUint64, cm->comm, c->stream));
+  std::vector<uint64_t> koff(P + 1, 0);
+  for (int p = 0; p < P; ++p) koff[p + 1] = koff[p] + Ds[p];
+  DC_TRY(alloc(c, packed, koff[P]));
+  for (int p = 0; p < P; ++p)
+    if (Ds[p]) DC_CUDA(c, cudaMemcpyAsync(packed.p + koff[p], all.p + (uint64_t)p * Dmax, Ds[p] * 16, cudaMemcpyDeviceToDevice, c->stream));
+  dc_dict* gd = nullptr;
+  std::vector<Buf<uint32_t>> l2g;
+  DC_TRY(unify_dicts(c, packed.p, koff, &gd, l2g));
+  // 2-3. hash + partition
+  const RecFmt f = fmt_of(local);
+  Slabs s;
+  DC_TRY(partition(c, local, l2g[cm->rank].p, P, f, s));
+  // 4. exchange counts, then slabs
+  Buf<uint64_t> sc, rc;
+  DC_TRY(alloc(c, sc, 2 * P));
+  DC_TRY(alloc(c, rc, 2 * P));
+  std::vector<uint64_t> hsc(2 * P);
+  for (int q = 0; q < P; ++q) {
+    hsc[2 * q] = s.ncnt[q];
+    hsc[2 * q + 1] = s.bcnt[q];
+  }
+  DC_CUDA(c, cudaMemcpyAsync(sc.p, hsc.data(), 16 * P, cudaMemcpyHostToDevice, c->stream));
+  NCCL_TRY(c, ncclAlltoAll(sc.p, rc.p, 2, ncclUint64, cm->comm, c->stream));
+  std::vector<uint64_t> hrc(2 * P);
+  DC_TRY(readback(c, rc.p, 16 * P, hrc.data()));
+  uint64_t rn = 0, rb = 0;
+  for (int q = 0; q < P; ++q) {
+    rn += hrc[2 * q];
+    rb += hrc[2 * q + 1];
+  }
+  Buf<uint64_t> rnodes, rbins;
+  DC_TRY(alloc(c, rnodes, rn * f.W));
+  DC_TRY(alloc(c, rbins, rb * BIN_W));
+  {
+    uint64_t so = 0, ro = 0, sbo = 0, rbo = 0;
+    NCCL_TRY(c, ncclGroupStart());
+    for (int q = 0; q < P; ++q) {
+      if (s.ncnt[q]) NCCL_TRY(c, ncclSend(s.nodes.p + so * f.W, s.ncnt[q] * f.W, ncclUint64, q, cm->comm, c->stream));
+      if (hrc[2 * q]) NCCL_TRY(c, ncclRecv(rnodes.p + ro * f.W, hrc[2 * q] * f.W, ncclUint64, q, cm->comm, c->stream));
+      if (s.bcnt[q]) NCCL_TRY(c, ncclSend(s.bins.p + sbo * BIN_W, s.bcnt[q] * BIN_W, ncclUint64, q, cm->comm, c->stream));
+      if (hrc[2 * q + 1]) NCCL_TRY(c, ncclRecv(rbins.p + rbo * BIN_W, hrc[2 * q + 1] * BIN_W, ncclUint64, q, cm->comm, c->stream));
+      so += s.ncnt[q];
+      ro += hrc[2 * q];
+      sbo += s.bcnt[q];
+      rbo += hrc[2 * q + 1];
+    }
+    NCCL_TRY(c, ncclGroupEnd());
+  }
+  // 5. reduce + verify
+  Buf<uint32_t> coll;
+  DC_TRY(alloc_zero(c, coll, 1));
+  Buf<uint64_t> un, ub;
+  uint64_t nun = 0, nub = 0;
+  DC_TRY(reduce_records(c, rnodes.p, rn, f.W, false, f, un, &nun, coll.p));
+  DC_TRY(reduce_bins(c, rbins.p, rb, ub, &nub));
+  uint32_t hcoll = 0;
+  DC_TRY(readback(c, coll.p, 4, &hcoll));
+  if (hcoll) {
+    c->host_collisions += 1;
+    dc_dict_free(gd);
+    return fail(c, DC_ERR_COLLISION, "merge: 128-bit path hash collision detected");
+  }
+  c->bytes_host += (rn * f.W + rb * BIN_W) * 8 * 2;
+  *out_partition = make_partition(c, f, nun, un, nub, ub, (uint32_t)gd->D);
+  *out_global_dict = gd;
+  return DC_OK;
+#else
+  return fail(ctx, DC_ERR_NCCL, "built without NCCL");
+#endif
+}
+
+dc_status dc_cct_gather(dc_ctx* ctx, dc_comm* cm, const dc_cct* part, int root, dc_cct** out_canonical) {
+  if (!ctx || !cm || !part || !out_canonical || root < 0 || root >= cm->nranks) return DC_ERR_ARG;
+  if (!part->partition) return fail(ctx, DC_ERR_STATE, "dc_cct_gather takes a partition from dc_cct_merge_ranks");
+  *out_canonical = nullptr;
+#if DC_HAVE_NCCL
+  Ctx* c = ctx;
+  DC_CUDA(c, cudaSetDevice(c->device));
+  const int P = cm->nranks;
+  const RecFmt f = rec_fmt(part->M, part->S, part->part_has_pc);
+  Buf<uint64_t> cnt;
+  DC_TRY(alloc(c, cnt, 2 * P));
+  uint64_t mine[2] = {part->N, part->part_nbins};
+  DC_CUDA(c, cudaMemcpyAsync(cnt.p + 2 * cm->rank, mine, 16, cudaMemcpyHostToDevice, c->stream));
+  NCCL_TRY(c, ncclAllGather(cnt.p + 2 * cm->rank, cnt.p, 2, ncclUint64, cm->comm, c->stream));
+  std::vector<uint64_t> hc(2 * P);
+  DC_TRY(readback(c, cnt.p, 16 * P, hc.data()));
+  uint64_t tn = 0, tb = 0;
+  for (int q = 0; q < P; ++q) {
+    tn += hc[2 * q];
+    tb += hc[2 * q + 1];
+  }
+  Buf<uint64_t> allv, allb;
+  if (cm->rank == root) {
+    DC_TRY(alloc(c, allv, tn * f.W));
+    DC_TRY(alloc(c, allb, tb * BIN_W));
+  }
+  NCCL_TRY(c, ncclGroupStart());
+  if (part->N) NCCL_TRY(c, ncclSend(part->part_nodes, part->N * f.W, ncclUint64, root, cm->comm, c->stream));
+  if (part->part_nbins) NCCL_TRY(c, ncclSend(part->part_bins, part->part_nbins * BIN_W, ncclUint64, root, cm->comm, c->stream));
+  if (cm->rank == root) {
+    uint64_t o = 0, ob = 0;
+    for (int q = 0; q < P; ++q) {
+      if (hc[2 * q]) NCCL_TRY(c, ncclRecv(allv.p + o * f.W, hc[2 * q] * f.W, ncclUint64, q, cm->comm, c->stream));
+      if (hc[2 * q + 1]) NCCL_TRY(c, ncclRecv(allb.p + ob * BIN_W, hc[2 * q + 1] * BIN_W, ncclUint64, q, cm->comm, c->stream));
+      o += hc[2 * q];
+      ob += hc[2 * q + 1];
+    }
+  }
+  NCCL_TRY(c, ncclGroupEnd());
+  if (cm->rank != root) {
+    DC_CUDA(c, cudaStreamSynchronize(c->stream));
+    return DC_OK;
+  }
+  return canonicalize(c, allv.p, tn, allb.p, tb, f, part->n_frames, out_canonical);
+#else
+  return fail(ctx, DC_ERR_NCCL, "built without NCCL");
+#endif
+}
+
+dc_status dc_cct_merge_local(dc_ctx* ctx, uint32_t P, dc_cct* const* locals, dc_dict* const* dicts, dc_cct** out_canonical,
+                             dc_dict** out_global_dict) {
+  if (!ctx || !P || !locals || !dicts || !out_canonical || !out_global_dict) return DC_ERR_ARG;
+  Ctx* c = ctx;
+  DC_CUDA(c, cudaSetDevice(c->device));
+  for (uint32_t p = 0; p < P; ++p) {
+    if (!locals[p] || !dicts[p] || locals[p]->state != 2) return fail(c, DC_ERR_STATE, "local tree %u is not rolled up", p);
+    if (dicts[p]->D != locals[p]->n_frames) return fail(c, DC_ERR_ARG, "dictionary %u size != n_frames", p);
+    if (locals[p]->M != locals[0]->M || locals[p]->S != locals[0]->S ||
+        (locals[p]->xsamples != nullptr) != (locals[0]->xsamples != nullptr))
+      return fail(c, DC_ERR_ARG, "local trees disagree on metric / stall columns");
+  }
+  // 1. dictionaries (loopback all-gather = concatenation)
+  std::vector<uint64_t> koff(P + 1, 0);
+  for (uint32_t p = 0; p < P; ++p) koff[p + 1] = koff[p] + dicts[p]->D;
+  Buf<dc_frame_key> packed;
+  DC_TRY(alloc(c, packed, koff[P]));
+  for (uint32_t p = 0; p < P; ++p)
+    if (dicts[p]->D)
+      DC_CUDA(c, cudaMemcpyAsync(packed.p + koff[p], dicts[p]->keys, dicts[p]->D * 16, cudaMemcpyDeviceToDevice, c->stream));
+  dc_dict* gd = nullptr;
+  std::vector<Buf<uint32_t>> l2g;
+  DC_TRY(unify_dicts(c, packed.p, koff, &gd, l2g));
+  const RecFmt f = fmt_of(locals[0]);
+  // 2-3. every logical rank partitions
+  std::vector<Slabs> slabs(P);
+  for (uint32_t p = 0; p < P; ++p) DC_TRY(partition(c, locals[p], l2g[p].p, P, f, slabs[p]));
+  // 4. loopback exchange + 5. reduce per destination; 6. gather = concatenation of partitions
+  std::vector<Buf<uint64_t>> parts_n(P), parts_b(P);
+  std::vector<uint64_t> pn(P), pb(P);
+  Buf<uint32_t> coll;
+  DC_TRY(alloc_zero(c, coll, 1));
+  for (uint32_t q = 0; q < P; ++q) {
+    uint64_t rn = 0, rb = 0;
+    for (uint32_t p = 0; p < P; ++p) {
+      rn += slabs[p].ncnt[q];
+      rb += slabs[p].bcnt[q];
+    }
+    Buf<uint64_t> rnodes, rbins;
+    DC_TRY(alloc(c, rnodes, rn * f.W));
+    DC_TRY(alloc(c, rbins, rb * BIN_W));
+    uint64_t ro = 0, rbo = 0;
+    for (uint32_t p = 0; p < P; ++p) {
+      uint64_t so = 0, sbo = 0;
+      for (uint32_t q2 = 0; q2 < q; ++q2) {
+        so += slabs[p].ncnt[q2];
+        sbo += slabs[p].bcnt[q2];
+      }
+      if (slabs[p].ncnt[q])
+        DC_CUDA(c, cudaMemcpyAsync(rnodes.p + ro * f.W, slabs[p].nodes.p + so * f.W, slabs[p].ncnt[q] * f.W * 8,
+                                   cudaMemcpyDeviceToDevice, c->stream));
+      if (slabs[p].bcnt[q])
+        DC_CUDA(c, cudaMemcpyAsync(rbins.p + rbo * BIN_W, slabs[p].bins.p + sbo * BIN_W, slabs[p].bcnt[q] * BIN_W * 8,
+                                   cudaMemcpyDeviceToDevice, c->stream));
+      ro += slabs[p].ncnt[q];
+      rbo += slabs[p].bcnt[q];
+    }
+    DC_TRY(reduce_records(c, rnodes.p, rn, f.W, false, f, parts_n[q], &pn[q], coll.p));
+    DC_TRY(reduce_bins(c, rbins.p, rb, parts_b[q], &pb[q]));
+  }
+  uint32_t hcoll = 0;
+  DC_TRY(readback(c, coll.p, 4, &hcoll));
+  if (hcoll) {
+    dc_dict_free(gd);
+    c->host_collisions += 1;
+    return fail(c, DC_ERR_COLLISION, "merge: 128-bit path hash collision detected");
+  }
+  uint64_t tn = 0, tb = 0;
+  for (uint32_t q = 0; q < P; ++q) {
+    tn += pn[q];
+    tb += pb[q];
+  }
+  Buf<uint64_t> allv, allb;
+  DC_TRY(alloc(c, allv, tn * f.W));
+  DC_TRY(alloc(c, allb, tb * BIN_W));
+  uint64_t o = 0, ob = 0;
+  for (uint32_t q = 0; q < P; ++q) {
+    if (pn[q]) DC_CUDA(c, cudaMemcpyAsync(allv.p + o * f.W, parts_n[q].p, pn[q] * f.W * 8, cudaMemcpyDeviceToDevice, c->stream));
+    if (pb[q]) DC_CUDA(c, cudaMemcpyAsync(allb.p + ob * BIN_W, parts_b[q].p, pb[q] * BIN_W * 8, cudaMemcpyDeviceToDevice, c->stream));
+    o += pn[q];
+    ob += pb[q];
+  }
+  dc_cct* canon = nullptr;
+  DC_TRY(canonicalize(c, allv.p, tn, allb.p, tb, f, (uint32_t)gd->D, &canon));
+  if (gd->D) {  // kinds for views
+    DC_TRY(palloc(c, canon->frame_kind, gd->D));
+    DC_CUDA(c, cudaMemcpyAsync(canon->frame_kind, gd->kinds, gd->D, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  *out_canonical = canon;
+  *out_global_dict = gd;
+  return DC_OK;
+}
+
+}  // extern "C"

@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(RD_THREADS, 1) k_own_reduce(
     unsigned long long* __restrict__ ocnt, uint32_t* __restrict__ g_nbins, uint32_t* __restrict__ g_npcs,
     uint32_t* __restrict__ g_ctx, unsigned long long* __restrict__ xsamples, unsigned long long* __restrict__ xstall,
     uint32_t S, uint32_t* g_flags) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   RedSmem& sm = *reinterpret_cast<RedSmem*>(smem_raw);
   const uint32_t tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   for (uint32_t g = blockIdx.x; g < n_groups; g += gridDim.x) {
