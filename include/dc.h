@@ -74,8 +74,9 @@ typedef struct {
 } dc_diag;
 
 /* ---------------------------------------------------------------------------- context */
-/* device: CUDA ordinal. cuda_stream: cudaStream_t to run on, or NULL to create a private
-   non-blocking stream. */
+/* device: CUDA ordinal. cuda_stream: the cudaStream_t every call of this context runs on,
+   used as given (NULL = the legacy default stream); inputs produced and outputs consumed on
+   that stream need no further synchronization. */
 dc_status dc_ctx_create(int device, void* cuda_stream, dc_ctx** out);
 /* Waits for the stream; returns DC_ERR_TRACE if a device data-error flag is set. */
 dc_status dc_ctx_sync(dc_ctx* ctx);

@@ -57,6 +57,7 @@ __global__ void k_path_hash(const uint64_t* __restrict__ off, const uint32_t* __
     maxd = max(maxd, (uint32_t)L);
     empties += (L == 0);
   }
+  flags = __reduce_or_sync(0xffffffffu, flags);  // a bad frame may be seen by any lane
   if (lane == 0) {
     if (maxd) atomicMax(&d_diag[DG_MAXDEPTH], (unsigned long long)maxd);
     if (empties) atomicAdd(&d_diag[DG_EMPTY], (unsigned long long)empties);
@@ -69,17 +70,24 @@ __global__ void k_path_insert(const uint64_t* __restrict__ hash, uint64_t R, uns
   for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < R; r += (uint64_t)gridDim.x * blockDim.x) {
     uint64_t h = hash[r];
     uint64_t s = (h * 0x9E3779B97F4A7C15ull >> 17) & mask;
-    for (;; s = (s + 1) & mask) {
+    bool found = false;
+    for (uint64_t probe = 0; probe <= mask; ++probe, s = (s + 1) & mask) {
       unsigned long long cur = ld_relaxed_u64(htab + s);
-      if (cur == h) break;
+      if (cur == h) { found = true; break; }
       if (cur == ~0ull) {
         unsigned long long old = atomicCAS(htab + s, ~0ull, (unsigned long long)h);
         if (old == ~0ull) {
           atomicAdd(d_count, 1u);
+          found = true;
           break;
         }
-        if (old == h) break;
+        if (old == h) { found = true; break; }
       }
+    }
+    if (!found) {  // table full: the host retries with a larger table
+      atomicOr(d_count + 3, 1u);
+      slot_of_rec[r] = 0;
+      continue;
     }
     atomicMin(rtab + s, (uint32_t)r);
     slot_of_rec[r] = (uint32_t)s;
@@ -464,16 +472,25 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
   k_path_hash<<<grid_for(c, R * 32, 256), 256, 0, c->stream>>>(p->offsets, p->frames, R, n_frames, hash.p, len.p,
                                                                 c->d_flags, (unsigned long long*)c->d_diag, c->hash_mask);
   DC_LAUNCHED(c);
+  // path table sized for the distinct paths, not the records (retry once if it fills up)
   uint64_t cap = 1024;
-  while (cap < 2 * R) cap <<= 1;
-  if (cap > (1ull << 31)) cap = 1ull << 31;
-  DC_TRY(alloc(c, htab, cap));
-  DC_TRY(alloc(c, rtab, cap));
-  DC_CUDA(c, cudaMemsetAsync(htab.p, 0xFF, cap * 8, c->stream));
-  DC_CUDA(c, cudaMemsetAsync(rtab.p, 0xFF, cap * 4, c->stream));
-  DC_TRY(alloc_zero(c, cnt, 4));  // [0] distinct, [1] extra, [2] compact pos
-  k_path_insert<<<grid_for(c, R, 256), 256, 0, c->stream>>>(hash.p, R, htab.p, rtab.p, cap - 1, slot_of_rec.p, cnt.p);
-  DC_LAUNCHED(c);
+  while (cap < 2 * (R < (1ull << 20) ? R : (1ull << 20))) cap <<= 1;
+  for (int attempt = 0;; ++attempt) {
+    DC_TRY(alloc(c, htab, cap));
+    DC_TRY(alloc(c, rtab, cap));
+    DC_CUDA(c, cudaMemsetAsync(htab.p, 0xFF, cap * 8, c->stream));
+    DC_CUDA(c, cudaMemsetAsync(rtab.p, 0xFF, cap * 4, c->stream));
+    DC_TRY(alloc_zero(c, cnt, 4));  // [0] distinct, [1] extra, [2] compact pos, [3] overflow
+    k_path_insert<<<grid_for(c, R, 256), 256, 0, c->stream>>>(hash.p, R, htab.p, rtab.p, cap - 1, slot_of_rec.p, cnt.p);
+    DC_LAUNCHED(c);
+    uint32_t hcnt[4];
+    DC_TRY(readback(c, cnt.p, 16, hcnt));
+    if (!hcnt[3] && (uint64_t)hcnt[0] * 2 <= cap) break;
+    if (attempt || cap >= (1ull << 31)) return fail(c, DC_ERR_CAPACITY, "dc_cct_build: path table overflow");
+    cap = 1024;
+    while (cap < 2 * R) cap <<= 1;
+    if (cap > (1ull << 31)) cap = 1ull << 31;
+  }
   DC_TRY(alloc(c, extra_rec, R));
   k_path_verify<<<grid_for(c, R * 32, 256), 256, 0, c->stream>>>(p->offsets, p->frames, len.p, R, rtab.p, slot_of_rec.p,
                                                                   extra_rec.p, cnt.p + 1, cap);

@@ -98,15 +98,10 @@ dc_status dc_ctx_create(int device, void* cuda_stream, dc_ctx** out) {
     delete ctx;
     return DC_ERR_CUDA;
   }
-  if (cuda_stream) {
-    ctx->stream = (cudaStream_t)cuda_stream;
-  } else {
-    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
-      delete ctx;
-      return DC_ERR_CUDA;
-    }
-    ctx->own_stream = true;
-  }
+  // the caller's stream, used as given (NULL = the legacy default stream), so the library is
+  // ordered with the caller's producers/consumers of the device buffers on that stream
+  ctx->stream = (cudaStream_t)cuda_stream;
+  ctx->own_stream = false;
   cudaDeviceProp prop;
   cudaGetDeviceProperties(&prop, device);
   ctx->num_sms = prop.multiProcessorCount;

@@ -79,7 +79,8 @@ __global__ void k_push(const uint32_t* __restrict__ parent, uint64_t N, uint32_t
     if (g == 0) {
       uint64_t v = xcnt[n];
       if (!v) continue;
-      for (uint32_t a = parent[n];; a = parent[a]) {
+      // ids strictly decrease towards the root (parent[n] < n), which also bounds the walk
+      for (uint32_t a = parent[n], prev = (uint32_t)n; a < prev; prev = a, a = parent[a]) {
         atomicAdd(icnt + a, (unsigned long long)v);
         if (a == 0) break;
       }
@@ -90,7 +91,8 @@ __global__ void k_push(const uint32_t* __restrict__ parent, uint64_t N, uint32_t
       uint64_t mn = mcols[((uint64_t)C_XMIN * M + m) * N + n];
       uint64_t qlo = mcols[((uint64_t)C_XSQLO * M + m) * N + n];
       uint64_t qhi = mcols[((uint64_t)C_XSQHI * M + m) * N + n];
-      for (uint32_t a = parent[n];; a = parent[a]) {
+      // ids strictly decrease towards the root (parent[n] < n), which also bounds the walk
+      for (uint32_t a = parent[n], prev = (uint32_t)n; a < prev; prev = a, a = parent[a]) {
         if (s) atomicAdd(mcols + ((uint64_t)C_ISUM * M + m) * N + a, (unsigned long long)s);
         atomicMin(mcols + ((uint64_t)C_IMIN * M + m) * N + a, (unsigned long long)mn);
         if (qlo | qhi)
@@ -100,7 +102,8 @@ __global__ void k_push(const uint32_t* __restrict__ parent, uint64_t N, uint32_t
     } else if (g == M + 1) {
       uint64_t v = xsamples[n];
       if (!v) continue;
-      for (uint32_t a = parent[n];; a = parent[a]) {
+      // ids strictly decrease towards the root (parent[n] < n), which also bounds the walk
+      for (uint32_t a = parent[n], prev = (uint32_t)n; a < prev; prev = a, a = parent[a]) {
         atomicAdd(isamples + a, (unsigned long long)v);
         if (a == 0) break;
       }
@@ -108,7 +111,8 @@ __global__ void k_push(const uint32_t* __restrict__ parent, uint64_t N, uint32_t
       const uint32_t s = g - M - 2;
       uint64_t v = xstall[(uint64_t)s * N + n];
       if (!v) continue;
-      for (uint32_t a = parent[n];; a = parent[a]) {
+      // ids strictly decrease towards the root (parent[n] < n), which also bounds the walk
+      for (uint32_t a = parent[n], prev = (uint32_t)n; a < prev; prev = a, a = parent[a]) {
         atomicAdd(istall + (uint64_t)s * N + a, (unsigned long long)v);
         if (a == 0) break;
       }

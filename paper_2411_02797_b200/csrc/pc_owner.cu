@@ -3,39 +3,42 @@
 // When samples arrive contiguous per launch (launch_sample_off given, "flushes the metrics"
 // per activity buffer), launches are ordered by their context node and the
 // resulting ctx-ordered virtual sample stream is cut into num_SMs equal ranges, one
-// persistent CTA per SM:
-//   * one producer warp streams the range's launch segments into shared memory with TMA bulk
-//     copies (cp.async.bulk + mbarrier, 3 x 32 KB stages);
-//   * 16 consumer warps aggregate (pc_off, stall) -> count in a 16384-slot shared-memory hash
+// persistent 1024-thread CTA per SM:
+//   * warp 0 (one lane) streams the range's launch segments into shared memory with TMA bulk
+//     copies (cp.async.bulk + mbarrier, 3 x 31 KB stages) and decides the flush points;
+//   * 31 consumer warps aggregate (pc_off, stall) -> count in a 16384-slot shared-memory hash
 //     table (32-bit keys/counts, native shared atomics), deduplicating equal keys inside each
-//     warp (__match_any_sync) first, so hot PCs cost one atomic per warp;
-//   * when the context changes (or the table passes 75 % load) the table is flushed once to a
-//     partial list in HBM: every bin is written once per (CTA, context) segment — no global
+//     warp (__match_any_sync) first, so a hot PC costs one atomic per warp; warps run free
+//     (no per-stage CTA barrier) and only meet at flushes;
+//   * on a context change (or when the table passes half load) the table is flushed once to
+//     a partial list in HBM: each bin is written once per (CTA, context) segment — no global
 //     atomics on bins, no L2 hash table.
-// k_own_reduce then merges each context's segments in shared memory (sort + reduce, stable
-// radix sort), producing canonical (pc, stall) order, PC node counts and the context's
-// exclusive samples / stall[s] totals; k_own_place writes the final SoA arrays.
+// k_own_reduce then merges each context's segments in shared memory (stable radix sort +
+// reduce), producing canonical (pc, stall) order, PC node counts and the context's exclusive
+// samples / stall[s] totals; k_own_place writes the final SoA arrays.
 // Any sample this schedule cannot take (a valid launch that disagrees with its segment,
-// pc_off >= 2^27, a context whose partial list does not fit shared memory) makes the call
-// fall back to the generic schedule (pc.cu) for the whole input — same result, exact.
+// pc_off >= 2^27, a context whose partial list cannot be chunked into shared memory) makes
+// the call fall back to the generic schedule (pc.cu) for the whole input — same result.
 #include "prim.cuh"
 
 namespace dc {
 
-constexpr int OW_CONS_WARPS = 16;
-constexpr int OW_CONS = 32 * OW_CONS_WARPS;  // 512 consumer threads
-constexpr int OW_THREADS = OW_CONS + 32;     // + producer warp
+constexpr int OW_CONS_WARPS = 31;
+constexpr int OW_CONS = 32 * OW_CONS_WARPS;   // 992 consumer threads
+constexpr int OW_THREADS = OW_CONS + 32;      // + producer warp = 1024
 constexpr int OW_STAGES = 3;
-constexpr int OW_STAGE = 2048;  // samples per stage (32 KB)
-constexpr int OW_TAB = 16384;   // shared hash table slots
-constexpr uint32_t OW_FLUSH = OW_TAB * 3 / 4;  // flush when distinct > this before a stage
+constexpr int OW_STAGE = 2 * OW_CONS;         // 1984 samples per stage (31 KB): 2 per consumer thread
+constexpr int OW_TAB = 16384;                 // shared hash table slots
+// a flush is requested at this many distinct keys; at most (OW_STAGES + 1) more stages can
+// be inserted before the flush point the producer marks -> never more than OW_TAB - 1 keys
+constexpr uint32_t OW_FLUSH_REQ = OW_TAB - (OW_STAGES + 1) * OW_STAGE - 1;
 constexpr uint32_t EMPTY32 = 0xFFFFFFFFu;
 constexpr uint32_t OW_DONE = 0xFFFFFFFFu;
 
 enum { OWF_FALLBACK = 1, OWF_OVERFLOW = 2 };
 
 struct OwMeta {
-  uint32_t launch, ctx, count, pad;
+  uint32_t launch, ctx, count, flush;
 };
 
 struct OwnSmem {
@@ -45,6 +48,7 @@ struct OwnSmem {
   unsigned long long full[OW_STAGES], empty[OW_STAGES];
   OwMeta meta[OW_STAGES];
   uint32_t distinct;
+  uint32_t flush_req;
   uint32_t warp_cnt[OW_CONS_WARPS];
   unsigned long long seg_base;
 };
@@ -125,6 +129,7 @@ struct OwnArgs {
   unsigned long long* ldiag;
 };
 
+// all consumer threads; the caller has synchronised the consumers (every insert is done)
 __device__ __forceinline__ void own_flush(OwnSmem& sm, const OwnArgs& a, uint32_t ctx, uint32_t ctid) {
   const uint32_t n = sm.distinct;
   const uint32_t w = ctid >> 5, lane = ctid & 31;
@@ -139,15 +144,16 @@ __device__ __forceinline__ void own_flush(OwnSmem& sm, const OwnArgs& a, uint32_
     }
     sm.seg_base = base;
   }
-  constexpr uint32_t PER_WARP = OW_TAB / OW_CONS_WARPS;
+  constexpr uint32_t PER_WARP = (OW_TAB / 32 + OW_CONS_WARPS - 1) / OW_CONS_WARPS * 32;  // 544 slots, multiple of 32
+  const uint32_t s_lo = w * PER_WARP, s_hi = min((uint32_t)OW_TAB, s_lo + PER_WARP);
   uint32_t c = 0;
-  for (uint32_t s = w * PER_WARP + lane; s < (w + 1) * PER_WARP; s += 32) c += __popc(__ballot_sync(0xffffffffu, sm.key[s] != EMPTY32));
+  for (uint32_t s = s_lo + lane; s < s_hi; s += 32) c += __popc(__ballot_sync(0xffffffffu, sm.key[s] != EMPTY32));
   if (lane == 0) sm.warp_cnt[w] = c;
   cons_sync();
   const unsigned long long base = sm.seg_base;
   uint32_t pos = 0;
   for (uint32_t ww = 0; ww < w; ++ww) pos += sm.warp_cnt[ww];
-  for (uint32_t s0 = w * PER_WARP; s0 < (w + 1) * PER_WARP; s0 += 32) {
+  for (uint32_t s0 = s_lo; s0 < s_hi; s0 += 32) {
     const uint32_t s = s0 + lane;
     const uint32_t k = sm.key[s];
     const bool occ = k != EMPTY32;
@@ -170,28 +176,61 @@ __device__ __forceinline__ void own_insert(OwnSmem& sm, const OwnArgs& a, uint32
   uint32_t h = (key * 0x9E3779B1u) >> (32 - 14);  // log2(OW_TAB) = 14
   volatile uint32_t* vk = sm.key;
   while (true) {
-    uint32_t k = vk[h];
+    const uint32_t k = vk[h];
     if (k == key) break;
     if (k == EMPTY32) {
-      uint32_t old = atomicCAS(&sm.key[h], EMPTY32, key);
+      const uint32_t old = atomicCAS(&sm.key[h], EMPTY32, key);
       if (old == EMPTY32) {
-        atomicAdd(&sm.distinct, 1u);
+        if (atomicAdd(&sm.distinct, 1u) == OW_FLUSH_REQ) *(volatile uint32_t*)&sm.flush_req = 1u;
         break;
       }
       if (old == key) break;
     }
     h = (h + 1) & (OW_TAB - 1);
   }
-  uint32_t old = atomicAdd(&sm.cnt[h], add);
+  const uint32_t old = atomicAdd(&sm.cnt[h], add);
   if (old + add < old) {  // 32-bit wrap: emit the 2^32 carry as its own one-entry segment
-    unsigned long long base = atomicAdd(a.g_entries, 1ull);
-    unsigned si = atomicAdd(a.g_segs, 1u);
+    const unsigned long long base = atomicAdd(a.g_entries, 1ull);
+    const unsigned si = atomicAdd(a.g_segs, 1u);
     if (si < a.cap_segs && base + 1 <= a.cap_entries) {
       a.pkey[base] = key;
       a.pcnt[base] = 1ull << 32;
       a.seg[si] = make_uint4(ctx, 1u, (uint32_t)base, (uint32_t)(base >> 32));
     } else {
       atomicOr(a.g_flags, (uint32_t)OWF_OVERFLOW);
+    }
+  }
+}
+
+struct OwCounters {
+  uint32_t bad_l, bad_s, zero, fallback;
+};
+
+// classify one staged sample; returns its key (EMPTY32 when it is not aggregated)
+__device__ __forceinline__ uint32_t own_classify(const uint4 q, const OwMeta& m, const OwnArgs& a, bool ctx_ok, OwCounters& k,
+                                                 uint32_t& c) {
+  const uint32_t stall = q.z & 0xFFFFu;
+  c = q.w;
+  if (q.x >= a.n_launch) { ++k.bad_l; return EMPTY32; }
+  if (q.x != m.launch) { k.fallback = 1; return EMPTY32; }  // misplaced sample: generic schedule
+  if (stall >= a.S) { ++k.bad_s; return EMPTY32; }
+  if (c == 0) { ++k.zero; return EMPTY32; }
+  if (!ctx_ok) { atomicOr(a.trace_flags, (uint32_t)FLAG_BAD_LEAF); return EMPTY32; }
+  if (q.y >= (1u << 27)) { k.fallback = 1; return EMPTY32; }
+  const uint32_t key = (q.y << 5) | stall;
+  if (key == EMPTY32) k.fallback = 1;
+  return key;
+}
+
+__device__ __forceinline__ void own_aggregate(OwnSmem& sm, const OwnArgs& a, uint32_t key, uint32_t c, uint32_t ctx) {
+  const bool valid = key != EMPTY32;
+  const uint32_t peers = __match_any_sync(0xffffffffu, key);
+  const bool ones = __all_sync(0xffffffffu, !valid || c == 1);
+  if (valid) {
+    if (ones) {
+      if ((peers & lanemask_lt()) == 0) own_insert(sm, a, key, __popc(peers), ctx);
+    } else {
+      own_insert(sm, a, key, c, ctx);
     }
   }
 }
@@ -213,6 +252,7 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
       mbar_init(&sm.empty[s], OW_CONS_WARPS);
     }
     sm.distinct = 0;
+    sm.flush_req = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -222,12 +262,13 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
       // first sorted launch whose segment contains r0: largest i with cum[i] <= r0
       uint64_t lo = 0, hi = a.n_launch;
       while (lo < hi) {
-        uint64_t mid = (lo + hi + 1) >> 1;
+        const uint64_t mid = (lo + hi + 1) >> 1;
         if (a.cum[mid] <= r0) lo = mid;
         else hi = mid - 1;
       }
       uint64_t i = lo, pos = r0;
-      uint32_t st = 0, ph = 0;
+      uint32_t st = 0, ph = 0, prev_ctx = OW_DONE;
+      volatile uint32_t* freq = &sm.flush_req;
       while (pos < r1) {
         const uint64_t seg_end = a.cum[i + 1];
         if (seg_end <= pos) {
@@ -239,8 +280,14 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
         if (r1 - pos < chunk) chunk = r1 - pos;
         if (chunk > OW_STAGE) chunk = OW_STAGE;
         mbar_wait(&sm.empty[st], ph ^ 1u);
-        const uint64_t key = a.lkey[i];
-        sm.meta[st] = OwMeta{l, (uint32_t)key, (uint32_t)chunk, 0};
+        const uint32_t ctx = (uint32_t)a.lkey[i];
+        uint32_t flush = ctx != prev_ctx ? 1u : 0u;
+        if (*freq) {
+          *freq = 0u;
+          flush = 1u;
+        }
+        prev_ctx = ctx;
+        sm.meta[st] = OwMeta{l, ctx, (uint32_t)chunk, flush};
         const dc_pc_sample* src = a.smp + a.launch_off[l] + (pos - a.cum[i]);
         mbar_expect_tx(&sm.full[st], (uint32_t)chunk * 16u);
         tma_bulk_g2s(&sm.stage[st][0], src, (uint32_t)chunk * 16u, &sm.full[st]);
@@ -252,61 +299,42 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
         }
       }
       mbar_wait(&sm.empty[st], ph ^ 1u);
-      sm.meta[st] = OwMeta{0, OW_DONE, 0, 0};
+      sm.meta[st] = OwMeta{0, OW_DONE, 0, 1};
       mbar_arrive(&sm.full[st]);
     }
     return;
   }
-  // -------------------------------------------------- consumer warps
+  // -------------------------------------------------- consumer warps (free-running)
   const uint32_t ctid = tid - 32, lane = ctid & 31;
   uint32_t cur_ctx = OW_DONE, st = 0, ph = 0;
-  uint32_t bad_l = 0, bad_s = 0, zero = 0, fallback = 0;
+  OwCounters k{0, 0, 0, 0};
   while (true) {
     mbar_wait(&sm.full[st], ph);
     const OwMeta m = sm.meta[st];
-    cons_sync();  // every consumer finished the previous stage
+    if (m.flush) {  // uniform: every consumer sees the same meta
+      cons_sync();  // every consumer finished all previous stages
+      if (sm.distinct > 0) own_flush(sm, a, cur_ctx, ctid);
+    }
     if (m.ctx == OW_DONE) break;
-    if (sm.distinct > 0 && (m.ctx != cur_ctx || sm.distinct > OW_FLUSH)) own_flush(sm, a, cur_ctx, ctid);
     cur_ctx = m.ctx;
     const bool ctx_ok = m.ctx < a.N;
-    for (uint32_t j0 = 0; j0 < m.count; j0 += OW_CONS) {
-      const uint32_t j = j0 + ctid;
-      uint32_t key = EMPTY32, c = 0;
-      bool valid = false;
-      if (j < m.count) {
-        const uint4 q = sm.stage[st][j];
-        const uint32_t stall = q.z & 0xFFFFu;
-        c = q.w;
-        if (q.x >= a.n_launch) ++bad_l;
-        else if (q.x != m.launch) fallback = 1;  // misplaced sample: generic schedule
-        else if (stall >= a.S) ++bad_s;
-        else if (c == 0) ++zero;
-        else if (!ctx_ok) atomicOr(a.trace_flags, (uint32_t)FLAG_BAD_LEAF);
-        else if (q.y >= (1u << 27)) fallback = 1;
-        else {
-          key = (q.y << 5) | stall;
-          valid = key != EMPTY32;
-          if (!valid) fallback = 1;
-        }
-      }
-      const uint32_t peers = __match_any_sync(0xffffffffu, key);
-      const bool ones = __all_sync(0xffffffffu, !valid || c == 1);
-      if (valid) {
-        if (ones) {
-          if ((peers & lanemask_lt()) == 0) own_insert(sm, a, key, __popc(peers), m.ctx);
-        } else {
-          own_insert(sm, a, key, c, m.ctx);
-        }
-      }
-    }
+    // two samples per consumer thread (OW_STAGE = 2 * OW_CONS)
+    const uint32_t j0 = ctid, j1 = ctid + OW_CONS;
+    const uint4 q0 = j0 < m.count ? sm.stage[st][j0] : make_uint4(0, 0, 0, 0);
+    const uint4 q1 = j1 < m.count ? sm.stage[st][j1] : make_uint4(0, 0, 0, 0);
     __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.empty[st]);
+    if (lane == 0) mbar_arrive(&sm.empty[st]);  // the stage is consumed into registers: release it early
+    uint32_t c0 = 0, c1 = 0;
+    const uint32_t key0 = j0 < m.count ? own_classify(q0, m, a, ctx_ok, k, c0) : EMPTY32;
+    const uint32_t key1 = j1 < m.count ? own_classify(q1, m, a, ctx_ok, k, c1) : EMPTY32;
+    own_aggregate(sm, a, key0, c0, m.ctx);
+    own_aggregate(sm, a, key1, c1, m.ctx);
     if (++st == OW_STAGES) {
       st = 0;
       ph ^= 1u;
     }
   }
-  if (sm.distinct > 0) own_flush(sm, a, cur_ctx, ctid);
+  uint32_t bad_l = k.bad_l, bad_s = k.bad_s, zero = k.zero, fallback = k.fallback;
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
     bad_l += __shfl_xor_sync(0xffffffffu, bad_l, o);
@@ -323,123 +351,187 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
 }
 
 // ---------------------------------------------------------------- per-context reduce
+// One CTA per context. Its partial entries (all segments of the context: several CTAs of the
+// main kernel and several flushes) are processed in key-range chunks of at most RD_CAP
+// entries (one chunk for almost every context); each chunk is gathered into shared memory,
+// stably radix-sorted, reduced (equal keys summed) and appended, so the output is sorted.
 constexpr int RD_THREADS = 1024;
-constexpr uint32_t RD_CAP = 12288;  // entries of one context sorted in shared memory
+constexpr uint32_t RD_CAP = 10240;  // entries sorted in shared memory at once
+constexpr int RD_BUCKETS = 4096;
 
 struct RedSmem {
   uint32_t k[2][RD_CAP];
   uint32_t v[2][RD_CAP];
   uint32_t wcnt[32][256];
+  uint32_t hist[RD_BUCKETS];
+  uint16_t bchunk[RD_BUCKETS];
   unsigned long long stall_tot[32];
+  uint32_t fill, maxkey, prev_key, total, bad;
 };
 
-// groups: per context, segments [gs, ge) in seg_sorted (by ctx)
 __global__ void __launch_bounds__(RD_THREADS, 1) k_own_reduce(
     const uint4* __restrict__ seg, const uint32_t* __restrict__ seg_order, const uint32_t* __restrict__ grp_start,
     uint32_t n_groups, const uint64_t* __restrict__ grp_out, const uint32_t* __restrict__ pkey,
-    const unsigned long long* __restrict__ pcnt, int kbits, uint64_t N, uint32_t* __restrict__ okey,
+    const unsigned long long* __restrict__ pcnt, uint64_t N, uint32_t* __restrict__ okey,
     unsigned long long* __restrict__ ocnt, uint32_t* __restrict__ g_nbins, uint32_t* __restrict__ g_npcs,
     uint32_t* __restrict__ g_ctx, unsigned long long* __restrict__ xsamples, unsigned long long* __restrict__ xstall,
     uint32_t S, uint32_t* g_flags) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   RedSmem& sm = *reinterpret_cast<RedSmem*>(smem_raw);
   const uint32_t tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  constexpr uint32_t HALF = RD_CAP / 2;
   for (uint32_t g = blockIdx.x; g < n_groups; g += gridDim.x) {
     const uint32_t gs = grp_start[g], ge = grp_start[g + 1];
     const uint32_t ctx = seg[seg_order[gs]].x;
-    // gather (key, global index) of all entries of this context
-    uint32_t n = 0;
-    bool too_big = false;
+    if (tid < 32) sm.stall_tot[tid] = 0;
+    if (tid == 0) {
+      sm.maxkey = 0;
+      sm.bad = 0;
+      sm.prev_key = 0xFFFFFFFFu;
+      uint32_t tot = 0;
+      for (uint32_t si = gs; si < ge; ++si) tot += seg[seg_order[si]].y;
+      sm.total = tot;
+    }
+    __syncthreads();
+    const uint32_t E = sm.total;
+    // key range (sort width)
+    uint32_t mk = 0;
     for (uint32_t si = gs; si < ge; ++si) {
       const uint4 sg = seg[seg_order[si]];
       const uint64_t base = (uint64_t)sg.z | ((uint64_t)sg.w << 32);
-      if (n + sg.y > RD_CAP) {
-        too_big = true;
-        break;
-      }
-      for (uint32_t j = tid; j < sg.y; j += RD_THREADS) {
-        sm.k[0][n + j] = pkey[base + j];
-        sm.v[0][n + j] = (uint32_t)(base + j);
-      }
-      n += sg.y;
+      for (uint32_t j = tid; j < sg.y; j += RD_THREADS) mk = max(mk, pkey[base + j]);
     }
-    if (too_big) {
-      if (tid == 0) atomicOr(g_flags, (uint32_t)OWF_FALLBACK);
-      __syncthreads();
-      continue;
-    }
-    if (tid < 32) sm.stall_tot[tid] = 0;
+    mk = __reduce_max_sync(0xffffffffu, mk);
+    if (lane == 0) atomicMax(&sm.maxkey, mk);
     __syncthreads();
-    // stable LSD radix sort of (key, index) by the key's kbits significant bits
-    int cur = 0;
-    const uint32_t per_warp = (n + 31) / 32;
-    for (int shift = 0; shift < kbits; shift += 8) {
-      const int nb = kbits - shift < 8 ? kbits - shift : 8;
-      const uint32_t mask = (1u << nb) - 1u;
-      for (int i = tid; i < 32 * 256; i += RD_THREADS) (&sm.wcnt[0][0])[i] = 0;
+    const int kb = sm.maxkey ? 32 - __clz(sm.maxkey) : 1;
+    const int bshift = kb > 12 ? kb - 12 : 0;
+    uint32_t nchunks = 1;
+    if (E > RD_CAP) {
+      // chunk c holds the buckets whose exclusive prefix lies in [c*HALF, (c+1)*HALF): with every
+      // bucket <= HALF, a chunk holds <= RD_CAP entries
+      for (uint32_t b = tid; b < RD_BUCKETS; b += RD_THREADS) sm.hist[b] = 0;
       __syncthreads();
-      const uint32_t b0 = w * per_warp, b1 = min(n, b0 + per_warp);
-      for (uint32_t base = b0; base < b1; base += 32) {
-        const uint32_t j = base + lane;
-        const bool ok = j < b1;
-        const uint32_t d = ok ? (sm.k[cur][j] >> shift) & mask : 0xFFFFFFFFu;
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
-        if (ok && (peers & lanemask_lt()) == 0) sm.wcnt[w][d] += __popc(peers);
-        __syncwarp();
+      for (uint32_t si = gs; si < ge; ++si) {
+        const uint4 sg = seg[seg_order[si]];
+        const uint64_t base = (uint64_t)sg.z | ((uint64_t)sg.w << 32);
+        for (uint32_t j = tid; j < sg.y; j += RD_THREADS) atomicAdd(&sm.hist[pkey[base + j] >> bshift], 1u);
       }
       __syncthreads();
-      uint32_t tot = 0;
-      if (tid < 256)
-        for (int ww = 0; ww < 32; ++ww) tot += sm.wcnt[ww][tid];
-      const uint32_t ex = block_excl_scan<uint32_t, RD_THREADS>(tid < 256 ? tot : 0u, nullptr);
-      if (tid < 256) {
-        uint32_t run = ex;
-        for (int ww = 0; ww < 32; ++ww) {
-          const uint32_t c = sm.wcnt[ww][tid];
-          sm.wcnt[ww][tid] = run;
-          run += c;
-        }
+      uint32_t h4[4], s4 = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        h4[q] = sm.hist[tid * 4 + q];
+        s4 += h4[q];
+        if (h4[q] > HALF) sm.bad = 1;
+      }
+      uint32_t ex = block_excl_scan<uint32_t, RD_THREADS>(s4, nullptr);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        sm.bchunk[tid * 4 + q] = (uint16_t)(ex / HALF);
+        ex += h4[q];
       }
       __syncthreads();
-      for (uint32_t base = b0; base < b1; base += 32) {
-        const uint32_t j = base + lane;
-        const bool ok = j < b1;
-        const uint32_t kk = ok ? sm.k[cur][j] : 0, vv = ok ? sm.v[cur][j] : 0;
-        const uint32_t d = ok ? (kk >> shift) & mask : 0xFFFFFFFFu;
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
-        const uint32_t pos = ok ? sm.wcnt[w][d] + __popc(peers & lanemask_lt()) : 0;
-        __syncwarp();
-        if (ok && (peers & lanemask_lt()) == 0) sm.wcnt[w][d] += __popc(peers);
-        __syncwarp();
-        if (ok) {
-          sm.k[cur ^ 1][pos] = kk;
-          sm.v[cur ^ 1][pos] = vv;
-        }
+      if (sm.bad) {
+        if (tid == 0) atomicOr(g_flags, (uint32_t)OWF_FALLBACK);
+        __syncthreads();
+        continue;
       }
-      __syncthreads();
-      cur ^= 1;
+      nchunks = (E - 1) / HALF + 1;
     }
-    // reduce runs of equal keys: heads, then per-head sum over the run (runs are short)
     const uint64_t obase = grp_out[g];
     uint32_t n_out = 0, n_pc = 0;
-    for (uint32_t base = 0; base < n; base += RD_THREADS) {
-      const uint32_t j = base + tid;
-      const bool ok = j < n;
-      const uint32_t kk = ok ? sm.k[cur][j] : 0;
-      const uint32_t head = ok && (j == 0 || sm.k[cur][j - 1] != kk) ? 1u : 0u;
-      const uint32_t pchead = ok && (j == 0 || (sm.k[cur][j - 1] >> 5) != (kk >> 5)) ? 1u : 0u;
-      uint32_t tot_h, tot_p;
-      const uint32_t ex = block_excl_scan<uint32_t, RD_THREADS>(head, &tot_h);
-      block_excl_scan<uint32_t, RD_THREADS>(pchead, &tot_p);
-      if (head) {
-        unsigned long long s = 0;
-        for (uint32_t t = j; t < n && sm.k[cur][t] == kk; ++t) s += pcnt[sm.v[cur][t]];
-        okey[obase + n_out + ex] = kk;
-        ocnt[obase + n_out + ex] = s;
-        atomicAdd(&sm.stall_tot[kk & 31u], s);
+    for (uint32_t ch = 0; ch < nchunks; ++ch) {
+      if (tid == 0) sm.fill = 0;
+      __syncthreads();
+      for (uint32_t si = gs; si < ge; ++si) {
+        const uint4 sg = seg[seg_order[si]];
+        const uint64_t base = (uint64_t)sg.z | ((uint64_t)sg.w << 32);
+        for (uint32_t j = tid; j < sg.y; j += RD_THREADS) {
+          const uint32_t kk = pkey[base + j];
+          if (nchunks == 1 || sm.bchunk[kk >> bshift] == ch) {
+            const uint32_t slot = atomicAdd(&sm.fill, 1u);
+            sm.k[0][slot] = kk;
+            sm.v[0][slot] = (uint32_t)(base + j);
+          }
+        }
       }
-      n_out += tot_h;
-      n_pc += tot_p;
+      __syncthreads();
+      const uint32_t n = sm.fill;
+      // stable LSD radix sort of (key, global index) over kb bits (equal keys are summed, so
+      // their relative order does not matter)
+      int cur = 0;
+      const uint32_t per_warp = (n + 31) / 32;
+      for (int shift = 0; shift < kb; shift += 8) {
+        const int nb = kb - shift < 8 ? kb - shift : 8;
+        const uint32_t mask = (1u << nb) - 1u;
+        for (int i = tid; i < 32 * 256; i += RD_THREADS) (&sm.wcnt[0][0])[i] = 0;
+        __syncthreads();
+        const uint32_t b0 = w * per_warp, b1 = min(n, b0 + per_warp);
+        for (uint32_t bs = b0; bs < b1; bs += 32) {
+          const uint32_t j = bs + lane;
+          const bool ok = j < b1;
+          const uint32_t d = ok ? (sm.k[cur][j] >> shift) & mask : 0xFFFFFFFFu;
+          const uint32_t peers = __match_any_sync(0xffffffffu, d);
+          if (ok && (peers & lanemask_lt()) == 0) sm.wcnt[w][d] += __popc(peers);
+          __syncwarp();
+        }
+        __syncthreads();
+        uint32_t tot = 0;
+        if (tid < 256)
+          for (int ww = 0; ww < 32; ++ww) tot += sm.wcnt[ww][tid];
+        const uint32_t ex = block_excl_scan<uint32_t, RD_THREADS>(tid < 256 ? tot : 0u, nullptr);
+        if (tid < 256) {
+          uint32_t run = ex;
+          for (int ww = 0; ww < 32; ++ww) {
+            const uint32_t c = sm.wcnt[ww][tid];
+            sm.wcnt[ww][tid] = run;
+            run += c;
+          }
+        }
+        __syncthreads();
+        for (uint32_t bs = b0; bs < b1; bs += 32) {
+          const uint32_t j = bs + lane;
+          const bool ok = j < b1;
+          const uint32_t kk = ok ? sm.k[cur][j] : 0, vv = ok ? sm.v[cur][j] : 0;
+          const uint32_t d = ok ? (kk >> shift) & mask : 0xFFFFFFFFu;
+          const uint32_t peers = __match_any_sync(0xffffffffu, d);
+          const uint32_t pos = ok ? sm.wcnt[w][d] + __popc(peers & lanemask_lt()) : 0;
+          __syncwarp();
+          if (ok && (peers & lanemask_lt()) == 0) sm.wcnt[w][d] += __popc(peers);
+          __syncwarp();
+          if (ok) {
+            sm.k[cur ^ 1][pos] = kk;
+            sm.v[cur ^ 1][pos] = vv;
+          }
+        }
+        __syncthreads();
+        cur ^= 1;
+      }
+      // reduce runs of equal keys; PC-node heads continue across chunk boundaries
+      const uint32_t prev = sm.prev_key;
+      for (uint32_t bs = 0; bs < n; bs += RD_THREADS) {
+        const uint32_t j = bs + tid;
+        const bool ok = j < n;
+        const uint32_t kk = ok ? sm.k[cur][j] : 0;
+        const uint32_t pk = j == 0 ? prev : (ok ? sm.k[cur][j - 1] : 0);
+        const uint32_t head = ok && (pk != kk) ? 1u : 0u;
+        const uint32_t pchead = ok && (pk == 0xFFFFFFFFu || (pk >> 5) != (kk >> 5)) ? 1u : 0u;
+        uint32_t tot_h, tot_p;
+        const uint32_t ex = block_excl_scan<uint32_t, RD_THREADS>(head, &tot_h);
+        block_excl_scan<uint32_t, RD_THREADS>(pchead, &tot_p);
+        if (head) {
+          unsigned long long s = 0;
+          for (uint32_t t = j; t < n && sm.k[cur][t] == kk; ++t) s += pcnt[sm.v[cur][t]];
+          okey[obase + n_out + ex] = kk;
+          ocnt[obase + n_out + ex] = s;
+          atomicAdd(&sm.stall_tot[kk & 31u], s);
+        }
+        n_out += tot_h;
+        n_pc += tot_p;
+        __syncthreads();
+      }
+      if (tid == 0 && n) sm.prev_key = sm.k[cur][n - 1];
       __syncthreads();
     }
     if (tid == 0) {
@@ -500,8 +592,7 @@ __global__ void k_own_gstart(const uint32_t* __restrict__ head, const uint32_t* 
     if (head[i]) grp_start[hex[i]] = i;
   if (blockIdx.x == 0 && threadIdx.x == 0) grp_start[n_groups] = n;
 }
-__global__ void k_own_segkeys(const uint4* __restrict__ seg, uint32_t n, uint64_t* __restrict__ key, uint32_t* __restrict__ val,
-                              uint64_t* __restrict__ gsz_in) {
+__global__ void k_own_segkeys(const uint4* __restrict__ seg, uint32_t n, uint64_t* __restrict__ key, uint32_t* __restrict__ val) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     key[i] = seg[i].x;
     val[i] = i;
@@ -523,30 +614,35 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
   if (n == 0 || n_launch == 0 || n_launch >= (1ull << 31)) return DC_OK;
   const uint64_t N = t->N;
   Buf<uint32_t> bad;
-  DC_TRY(alloc_zero(c, bad, 1));
-  k_own_check<<<grid_for(c, n_launch, 256), 256, 0, c->stream>>>(launch_off, n_launch, n, bad.p);
-  DC_LAUNCHED(c);
-  // launches ordered by context
   Buf<uint64_t> k0, k1, cum;
   Buf<uint32_t> v0, v1;
-  DC_TRY(alloc(c, k0, n_launch));
-  DC_TRY(alloc(c, k1, n_launch));
-  DC_TRY(alloc(c, v0, n_launch));
-  DC_TRY(alloc(c, v1, n_launch));
-  DC_TRY(alloc(c, cum, n_launch + 1));
-  k_own_keys<<<grid_for(c, n_launch, 256), 256, 0, c->stream>>>(launch_leaf, n_launch, N, k0.p, v0.p);
-  DC_LAUNCHED(c);
-  bool in1 = false;
-  DC_TRY(radix_sort_pairs(c, k0.p, v0.p, k1.p, v1.p, n_launch, 0, bits_for(N), &in1));
-  uint64_t* lkey = in1 ? k1.p : k0.p;
-  uint32_t* order = in1 ? v1.p : v0.p;
-  uint64_t* cnt = in1 ? k0.p : k1.p;  // free buffer
-  k_own_cnt<<<grid_for(c, n_launch, 256), 256, 0, c->stream>>>(launch_off, order, n_launch, cnt);
-  DC_LAUNCHED(c);
-  DC_TRY(excl_scan<uint64_t>(c, cnt, cum.p, n_launch, cum.p + n_launch));
-  uint32_t hbad = 0;
-  DC_TRY(readback(c, bad.p, 4, &hbad));
-  if (hbad) return DC_OK;  // offsets inconsistent: generic schedule
+  uint64_t* lkey = nullptr;
+  uint32_t* order = nullptr;
+  {
+    Region rp(c, "pc:prep");
+    DC_TRY(alloc_zero(c, bad, 1));
+    k_own_check<<<grid_for(c, n_launch, 256), 256, 0, c->stream>>>(launch_off, n_launch, n, bad.p);
+    DC_LAUNCHED(c);
+    // launches ordered by context
+    DC_TRY(alloc(c, k0, n_launch));
+    DC_TRY(alloc(c, k1, n_launch));
+    DC_TRY(alloc(c, v0, n_launch));
+    DC_TRY(alloc(c, v1, n_launch));
+    DC_TRY(alloc(c, cum, n_launch + 1));
+    k_own_keys<<<grid_for(c, n_launch, 256), 256, 0, c->stream>>>(launch_leaf, n_launch, N, k0.p, v0.p);
+    DC_LAUNCHED(c);
+    bool in1 = false;
+    DC_TRY(radix_sort_pairs(c, k0.p, v0.p, k1.p, v1.p, n_launch, 0, bits_for(N), &in1));
+    lkey = in1 ? k1.p : k0.p;
+    order = in1 ? v1.p : v0.p;
+    uint64_t* cnt = in1 ? k0.p : k1.p;  // free buffer
+    k_own_cnt<<<grid_for(c, n_launch, 256), 256, 0, c->stream>>>(launch_off, order, n_launch, cnt);
+    DC_LAUNCHED(c);
+    DC_TRY(excl_scan<uint64_t>(c, cnt, cum.p, n_launch, cum.p + n_launch));
+    uint32_t hbad = 0;
+    DC_TRY(readback(c, bad.p, 4, &hbad));
+    if (hbad) return DC_OK;  // offsets inconsistent: generic schedule
+  }
   // partial outputs
   const uint32_t G = (uint32_t)c->num_sms;
   const uint64_t cap_entries = n + 1;
@@ -554,45 +650,53 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
   Buf<uint32_t> pkey, flags;
   Buf<unsigned long long> pcnt, ctr, ldiag;
   Buf<uint4> seg;
-  DC_TRY(alloc(c, pkey, cap_entries));
-  DC_TRY(alloc(c, pcnt, cap_entries));
-  DC_TRY(alloc(c, seg, cap_segs));
-  DC_TRY(alloc_zero(c, ctr, 2));
-  DC_TRY(alloc_zero(c, flags, 2));
-  DC_TRY(alloc_zero(c, ldiag, DG_N));
-  OwnArgs a;
-  a.smp = s;
-  a.launch_off = launch_off;
-  a.order = order;
-  a.lkey = lkey;
-  a.cum = cum.p;
-  a.n_launch = n_launch;
-  a.N = N;
-  a.total = n;
-  a.S = S;
-  a.pkey = pkey.p;
-  a.pcnt = pcnt.p;
-  a.cap_entries = cap_entries;
-  a.seg = seg.p;
-  a.cap_segs = cap_segs;
-  a.g_entries = ctr.p;
-  a.g_segs = (unsigned int*)(ctr.p + 1);
-  a.g_flags = flags.p;
-  a.trace_flags = c->d_flags;
-  a.ldiag = ldiag.p;
-  const size_t smem = sizeof(OwnSmem);
-  DC_CUDA(c, cudaFuncSetAttribute(k_pc_owner, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  {
-    Region rk(c, "k:pc_owner");
-    k_pc_owner<<<G, OW_THREADS, smem, c->stream>>>(a);
-    DC_LAUNCHED(c);
-  }
   uint64_t hc[2];
   uint32_t hf[2];
-  DC_TRY(readback(c, ctr.p, 16, hc));
-  DC_TRY(readback(c, flags.p, 8, hf));
+  {
+    Region rp(c, "pc:main");
+    DC_TRY(alloc(c, pkey, cap_entries));
+    DC_TRY(alloc(c, pcnt, cap_entries));
+    DC_TRY(alloc(c, seg, cap_segs));
+    DC_TRY(alloc_zero(c, ctr, 2));
+    DC_TRY(alloc_zero(c, flags, 2));
+    DC_TRY(alloc_zero(c, ldiag, DG_N));
+    OwnArgs a;
+    a.smp = s;
+    a.launch_off = launch_off;
+    a.order = order;
+    a.lkey = lkey;
+    a.cum = cum.p;
+    a.n_launch = n_launch;
+    a.N = N;
+    a.total = n;
+    a.S = S;
+    a.pkey = pkey.p;
+    a.pcnt = pcnt.p;
+    a.cap_entries = cap_entries;
+    a.seg = seg.p;
+    a.cap_segs = cap_segs;
+    a.g_entries = ctr.p;
+    a.g_segs = (unsigned int*)(ctr.p + 1);
+    a.g_flags = flags.p;
+    a.trace_flags = c->d_flags;
+    a.ldiag = ldiag.p;
+    const size_t smem = sizeof(OwnSmem);
+    static bool attr_set = false;
+    if (!attr_set) {
+      DC_CUDA(c, cudaFuncSetAttribute(k_pc_owner, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr_set = true;
+    }
+    {
+      Region rk(c, "k:pc_owner");
+      k_pc_owner<<<G, OW_THREADS, smem, c->stream>>>(a);
+      DC_LAUNCHED(c);
+    }
+    DC_TRY(readback(c, ctr.p, 16, hc));
+    DC_TRY(readback(c, flags.p, 8, hf));
+  }
   if (hf[0]) return DC_OK;  // fallback / overflow -> generic schedule (diag of this pass discarded)
   const uint32_t n_segs = (uint32_t)(hc[1] & 0xFFFFFFFFu);
+  Region rr(c, "pc:reduce");
   // group segments by context
   Buf<uint64_t> sk0, sk1;
   Buf<uint32_t> sv0, sv1, head, hex, grp_start;
@@ -602,7 +706,7 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
   DC_TRY(alloc(c, sv1, n_segs));
   DC_TRY(alloc(c, head, n_segs));
   DC_TRY(alloc(c, hex, n_segs));
-  k_own_segkeys<<<grid_for(c, n_segs, 256), 256, 0, c->stream>>>(seg.p, n_segs, sk0.p, sv0.p, nullptr);
+  k_own_segkeys<<<grid_for(c, n_segs, 256), 256, 0, c->stream>>>(seg.p, n_segs, sk0.p, sv0.p);
   DC_LAUNCHED(c);
   bool sin1 = false;
   DC_TRY(radix_sort_pairs(c, sk0.p, sv0.p, sk1.p, sv1.p, n_segs, 0, bits_for(N), &sin1));
@@ -636,16 +740,21 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
   DC_TRY(alloc(c, bbase, n_groups));
   DC_TRY(alloc(c, pbase, n_groups));
   DC_TRY(alloc(c, tots, 2));
-  // key bits: pc_off < 2^27 -> key < 2^32; use all 32 (4 passes) — cheap in shared memory
-  const int kbits = 32;
   const size_t rsmem = sizeof(RedSmem);
-  DC_CUDA(c, cudaFuncSetAttribute(k_own_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem));
-  k_own_reduce<<<n_groups < (uint32_t)G ? n_groups : G, RD_THREADS, rsmem, c->stream>>>(
-      seg.p, sso, grp_start.p, n_groups, gout.p, pkey.p, pcnt.p, kbits, N, okey.p, ocnt.p, gnb.p, gnp.p, gctx.p,
-      (unsigned long long*)t->xsamples, (unsigned long long*)t->xstall, S, flags.p);
-  DC_LAUNCHED(c);
+  static bool rattr_set = false;
+  if (!rattr_set) {
+    DC_CUDA(c, cudaFuncSetAttribute(k_own_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem));
+    rattr_set = true;
+  }
+  {
+    Region rk(c, "k:own_reduce");
+    k_own_reduce<<<n_groups < (uint32_t)G ? n_groups : G, RD_THREADS, rsmem, c->stream>>>(
+        seg.p, sso, grp_start.p, n_groups, gout.p, pkey.p, pcnt.p, N, okey.p, ocnt.p, gnb.p, gnp.p, gctx.p,
+        (unsigned long long*)t->xsamples, (unsigned long long*)t->xstall, S, flags.p);
+    DC_LAUNCHED(c);
+  }
   DC_TRY(readback(c, flags.p, 4, hf));
-  if (hf[0]) {  // a context too large for the shared-memory reduce: generic schedule
+  if (hf[0]) {  // a context that cannot be chunked into shared memory: generic schedule
     DC_CUDA(c, cudaMemsetAsync(t->xsamples, 0, N * 8, c->stream));
     DC_CUDA(c, cudaMemsetAsync(t->xstall, 0, (uint64_t)S * N * 8, c->stream));
     return DC_OK;

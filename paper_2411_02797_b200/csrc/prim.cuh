@@ -206,12 +206,98 @@ static __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const uint64_t
   }
 }
 
+// Small sorts (n <= SS_MAX): every pass in one 1024-thread CTA in shared memory, one launch.
+constexpr int SS_THREADS = 1024;
+constexpr uint32_t SS_MAX = 4096;
+struct SmallSortSmem {
+  uint64_t k[2][SS_MAX];
+  uint32_t v[2][SS_MAX];
+  uint32_t wcnt[32][256];
+};
+
+static __global__ void __launch_bounds__(SS_THREADS, 1) k_sort_small(const uint64_t* __restrict__ ik, const uint32_t* __restrict__ iv,
+                                                                  uint64_t* __restrict__ ok, uint32_t* __restrict__ ov, uint32_t n,
+                                                                  int begin_bit, int end_bit) {
+  extern __shared__ __align__(128) unsigned char ss_raw[];
+  SmallSortSmem& sm = *reinterpret_cast<SmallSortSmem*>(ss_raw);
+  const uint32_t tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  for (uint32_t i = tid; i < n; i += SS_THREADS) {
+    sm.k[0][i] = ik[i];
+    sm.v[0][i] = iv[i];
+  }
+  __syncthreads();
+  int cur = 0;
+  const uint32_t per_warp = (n + 31) / 32;
+  for (int shift = begin_bit; shift < end_bit; shift += 8) {
+    const int nb = end_bit - shift < 8 ? end_bit - shift : 8;
+    const uint32_t mask = (1u << nb) - 1u;
+    for (int i = tid; i < 32 * 256; i += SS_THREADS) (&sm.wcnt[0][0])[i] = 0;
+    __syncthreads();
+    const uint32_t b0 = w * per_warp, b1 = min(n, b0 + per_warp);
+    for (uint32_t bs = b0; bs < b1; bs += 32) {
+      const uint32_t j = bs + lane;
+      const bool okk = j < b1;
+      const uint32_t d = okk ? (uint32_t)(sm.k[cur][j] >> shift) & mask : 0xFFFFFFFFu;
+      const uint32_t peers = __match_any_sync(0xffffffffu, d);
+      if (okk && (peers & lanemask_lt()) == 0) sm.wcnt[w][d] += __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+    uint32_t tot = 0;
+    if (tid < 256)
+      for (int ww = 0; ww < 32; ++ww) tot += sm.wcnt[ww][tid];
+    const uint32_t ex = block_excl_scan<uint32_t, SS_THREADS>(tid < 256 ? tot : 0u, nullptr);
+    if (tid < 256) {
+      uint32_t run = ex;
+      for (int ww = 0; ww < 32; ++ww) {
+        const uint32_t cc = sm.wcnt[ww][tid];
+        sm.wcnt[ww][tid] = run;
+        run += cc;
+      }
+    }
+    __syncthreads();
+    for (uint32_t bs = b0; bs < b1; bs += 32) {
+      const uint32_t j = bs + lane;
+      const bool okk = j < b1;
+      const uint64_t kk = okk ? sm.k[cur][j] : 0;
+      const uint32_t vv = okk ? sm.v[cur][j] : 0;
+      const uint32_t d = okk ? (uint32_t)(kk >> shift) & mask : 0xFFFFFFFFu;
+      const uint32_t peers = __match_any_sync(0xffffffffu, d);
+      const uint32_t pos = okk ? sm.wcnt[w][d] + __popc(peers & lanemask_lt()) : 0;
+      __syncwarp();
+      if (okk && (peers & lanemask_lt()) == 0) sm.wcnt[w][d] += __popc(peers);
+      __syncwarp();
+      if (okk) {
+        sm.k[cur ^ 1][pos] = kk;
+        sm.v[cur ^ 1][pos] = vv;
+      }
+    }
+    __syncthreads();
+    cur ^= 1;
+  }
+  for (uint32_t i = tid; i < n; i += SS_THREADS) {
+    ok[i] = sm.k[cur][i];
+    ov[i] = sm.v[cur][i];
+  }
+}
+
 // Stable sort of n pairs by bits [begin_bit, end_bit) of the key. Ping-pongs between
 // (k0,v0) and (k1,v1); *result_in_1 tells where the sorted data ended up.
-inline dc_status radix_sort_pairs(Ctx* c, uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, uint64_t n,
+static inline dc_status radix_sort_pairs(Ctx* c, uint64_t* k0, uint32_t* v0, uint64_t* k1, uint32_t* v1, uint64_t n,
                                   int begin_bit, int end_bit, bool* result_in_1) {
   *result_in_1 = false;
   if (n <= 1 || end_bit <= begin_bit) return DC_OK;
+  if (n <= SS_MAX) {
+    static bool attr = false;
+    if (!attr) {
+      DC_CUDA(c, cudaFuncSetAttribute(k_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SmallSortSmem)));
+      attr = true;
+    }
+    k_sort_small<<<1, SS_THREADS, sizeof(SmallSortSmem), c->stream>>>(k0, v0, k1, v1, (uint32_t)n, begin_bit, end_bit);
+    DC_LAUNCHED(c);
+    *result_in_1 = true;
+    return DC_OK;
+  }
   if (n >= (1ull << 31)) return fail(c, DC_ERR_CAPACITY, "radix sort of %llu > 2^31 keys", (unsigned long long)n);
   uint32_t nt = (uint32_t)((n + RS_TILE - 1) / RS_TILE);
   Buf<uint32_t> hist;

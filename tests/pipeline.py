@@ -54,6 +54,8 @@ def gpu_run(offsets, frames=None, metrics=None, keys=None, n_frames=None, sample
 
 
 def oracle_run(offsets, frames, metrics, n_metrics, samples=None, n_launch=0, n_stall=24):
+    if samples is None:
+        n_stall = 0  # no PC columns, as on the GPU side
     o = oracle.OracleCCT(n_metrics, n_stall).insert(np.asarray(offsets).view(np.uint64) if np.asarray(offsets).dtype == np.int64
                                                     else offsets, frames, as_u64(metrics))
     if samples is not None:
