@@ -163,15 +163,15 @@ struct SmallSmem {
   uint64_t key[2][SMALL_P];
   uint32_t val[2][SMALL_P];
   uint32_t node_of_item[SMALL_P];
+  uint64_t off_of_item[SMALL_P];
+  uint16_t len_of_item[SMALL_P];
   uint32_t wcnt[32][256];
-  uint32_t scan_tmp[SB_THREADS];
 };
 
-// stable block radix sort of n <= SMALL_P pairs held in sm.key[0]/val[0]; returns buffer index
-__device__ int block_sort(SmallSmem& sm, uint32_t n, int bits) {
+// stable block radix sort of n <= SMALL_P pairs held in sm.key[cur]/val[cur]; returns buffer index
+__device__ int block_sort(SmallSmem& sm, uint32_t n, int bits, int cur) {
   const uint32_t w = threadIdx.x >> 5, lane = lane_id();
   const uint32_t per_warp = (n + 31) / 32;  // contiguous chunk per warp
-  int cur = 0;
   for (int shift = 0; shift < bits; shift += 8) {
     const int nb = bits - shift < 8 ? bits - shift : 8;
     const uint32_t mask = (1u << nb) - 1u;
@@ -224,7 +224,10 @@ __device__ int block_sort(SmallSmem& sm, uint32_t n, int bits) {
   return cur;
 }
 
-// block inclusive scan over n elements given by f(i); writes exclusive results to out via g
+// The whole level loop for P <= SMALL_P distinct paths in one CTA. Per level: keys
+// (parent-local << fbits | frame), a sort only when the keys are not already in order (after
+// the first branching level most levels are), then one fused pass that run-length encodes
+// (node ids, node table), retires finished items and compacts the active list.
 __global__ void __launch_bounds__(SB_THREADS, 1) k_build_small(const uint64_t* __restrict__ off, const uint32_t* __restrict__ frames,
                                                                const uint32_t* __restrict__ item_rec, const uint32_t* __restrict__ item_len,
                                                                uint32_t P, int fbits, uint32_t* __restrict__ parent,
@@ -241,74 +244,65 @@ __global__ void __launch_bounds__(SB_THREADS, 1) k_build_small(const uint64_t* _
     level_off[0] = 0;
     level_off[1] = 1;
   }
-  // active items: those with len > 0 (kept in val[0] in item order); empty paths -> root
+  // active items: those with len > 0 (in item order); empty paths -> root
   uint32_t n_active = 0;
-  {
-    for (uint32_t base = 0; base < P; base += SB_THREADS) {
-      uint32_t i = base + threadIdx.x;
-      uint32_t keep = (i < P && item_len[i] > 0) ? 1u : 0u;
-      if (i < P && !keep) leaf_of_item[i] = 0;
-      uint32_t tot;
-      uint32_t ex = block_excl_scan<uint32_t, SB_THREADS>(keep, &tot);
-      if (keep) {
-        sm.val[0][n_active + ex] = i;
-        sm.node_of_item[i] = 0;
-      }
-      n_active += tot;
+  int act = 0;  // buffer holding the active list
+  for (uint32_t base = 0; base < P; base += SB_THREADS) {
+    uint32_t i = base + threadIdx.x;
+    uint32_t L = i < P ? item_len[i] : 0;
+    uint32_t keep = (i < P && L > 0) ? 1u : 0u;
+    if (i < P) {
+      if (!keep) leaf_of_item[i] = 0;
+      sm.off_of_item[i] = off[item_rec[i]];
+      sm.len_of_item[i] = (uint16_t)L;
+      sm.node_of_item[i] = 0;
     }
+    uint32_t tot;
+    uint32_t ex = block_excl_scan<uint32_t, SB_THREADS>(keep, &tot);
+    if (keep) sm.val[0][n_active + ex] = i;
+    n_active += tot;
   }
+  __syncthreads();
   uint32_t lvl_start = 0, width = 1, next = 1;
   for (uint32_t d = 0; n_active > 0; ++d) {
     const int pbits = bits_for_dev(width - 1);
-    // keys
     for (uint32_t i = threadIdx.x; i < n_active; i += SB_THREADS) {
-      uint32_t it = sm.val[0][i];
-      uint32_t f = frames[off[item_rec[it]] + d];
-      sm.key[0][i] = ((uint64_t)(sm.node_of_item[it] - lvl_start) << fbits) | f;
+      const uint32_t it = sm.val[act][i];
+      const uint32_t f = frames[sm.off_of_item[it] + d];
+      sm.key[act][i] = ((uint64_t)(sm.node_of_item[it] - lvl_start) << fbits) | f;
     }
     __syncthreads();
-    int cur = block_sort(sm, n_active, pbits + fbits);
-    // run-length encode: heads, run index, node ids
+    bool in_order = true;
+    for (uint32_t i = 1 + threadIdx.x; i < n_active; i += SB_THREADS) in_order &= sm.key[act][i - 1] <= sm.key[act][i];
+    const int cur = __syncthreads_and(in_order) ? act : block_sort(sm, n_active, pbits + fbits, act);
+    // fused: run heads -> node ids; retire items of length d+1; compact the rest into the other buffer
     uint32_t n_keep = 0, n_runs = 0;
     for (uint32_t base = 0; base < n_active; base += SB_THREADS) {
-      uint32_t i = base + threadIdx.x;
-      bool ok = i < n_active;
-      uint64_t k = ok ? sm.key[cur][i] : 0;
-      uint32_t head = ok && (i == 0 || sm.key[cur][i - 1] != k) ? 1u : 0u;
+      const uint32_t i = base + threadIdx.x;
+      const bool ok = i < n_active;
+      const uint64_t k = ok ? sm.key[cur][i] : 0;
+      const uint32_t it = ok ? sm.val[cur][i] : 0;
+      const uint32_t head = ok && (i == 0 || sm.key[cur][i - 1] != k) ? 1u : 0u;
+      const uint32_t keep = ok && sm.len_of_item[it] > d + 1 ? 1u : 0u;
+      // one scan for both flags: (head count << 16 | keep count); n_active <= 4096 < 2^16
       uint32_t tot;
-      uint32_t ex = block_excl_scan<uint32_t, SB_THREADS>(head, &tot);
-      uint32_t run = n_runs + ex + head - 1;  // inclusive - 1
+      const uint32_t ex = block_excl_scan<uint32_t, SB_THREADS>((head << 16) | keep, &tot);
       if (ok) {
-        uint32_t node = next + run;
-        uint32_t it = sm.val[cur][i];
+        const uint32_t node = next + n_runs + (ex >> 16) + head - 1;  // inclusive run index - 1
         if (head) {
           parent[node] = lvl_start + (uint32_t)(k >> fbits);
           frame_out[node] = (uint32_t)(k & fmask);
           depth[node] = (uint16_t)(d + 1);
         }
         sm.node_of_item[it] = node;
-        if (item_len[it] == d + 1) leaf_of_item[it] = node;
+        if (!keep) leaf_of_item[it] = node;
+        else sm.val[cur ^ 1][n_keep + (ex & 0xFFFFu)] = it;
       }
-      n_runs += tot;
+      n_runs += tot >> 16;
+      n_keep += tot & 0xFFFFu;
       __syncthreads();
     }
-    // compact still-active items (order irrelevant for correctness; keep sorted order)
-    for (uint32_t base = 0; base < n_active; base += SB_THREADS) {
-      uint32_t i = base + threadIdx.x;
-      bool ok = i < n_active;
-      uint32_t it = ok ? sm.val[cur][i] : 0;
-      uint32_t keep = ok && item_len[it] > d + 1 ? 1u : 0u;
-      uint32_t tot;
-      uint32_t ex = block_excl_scan<uint32_t, SB_THREADS>(keep, &tot);
-      if (keep) sm.val[cur ^ 1][n_keep + ex] = it;
-      n_keep += tot;
-      __syncthreads();
-    }
-    // move compacted list to val[0]
-    if (cur == 0) {
-      for (uint32_t i = threadIdx.x; i < n_keep; i += SB_THREADS) sm.val[0][i] = sm.val[1][i];
-    }
-    __syncthreads();
+    act = cur ^ 1;
     lvl_start = next;
     width = n_runs;
     next += n_runs;

@@ -34,6 +34,7 @@ dc_status cuda_fail(Ctx* c, cudaError_t e, const char* what) {
 
 dc_status readback(Ctx* c, const void* dev, size_t bytes, void* host) {
   if (bytes == 0) return DC_OK;
+  HostRegion hr(c, "readback");
   if (bytes <= 4096) {
     DC_CUDA(c, cudaMemcpyAsync(c->h_pinned, dev, bytes, cudaMemcpyDeviceToHost, c->stream));
     DC_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -201,6 +202,19 @@ dc_status dc_ctx_timer_report(dc_ctx* ctx, char* buf, size_t len) {
     cudaEventDestroy(t.b);
   }
   ctx->timed.clear();
+  for (auto& h : ctx->htimed) {
+    std::string nm = std::string("h:") + h.name;
+    size_t i = 0;
+    while (i < names.size() && names[i] != nm) ++i;
+    if (i == names.size()) {
+      names.push_back(nm);
+      tot.push_back(0);
+      cnt.push_back(0);
+    }
+    tot[i] += h.ms;
+    cnt[i] += 1;
+  }
+  ctx->htimed.clear();
   std::string s;
   char line[256];
   for (size_t i = 0; i < names.size(); ++i) {

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <chrono>
 #include <string>
 #include <vector>
 
@@ -43,6 +44,22 @@ struct Ctx {
   bool timing = false;
   struct Timed { const char* name; cudaEvent_t a, b; };
   std::vector<Timed> timed;
+  struct HTimed { const char* name; double ms; };
+  std::vector<HTimed> htimed;  // host-side durations ("h:<name>" in the report)
+};
+
+// RAII host wall-clock timer (no-op unless timing is on): finds host stalls between kernels
+struct HostRegion {
+  Ctx* c;
+  const char* name;
+  std::chrono::steady_clock::time_point t0;
+  HostRegion(Ctx* ctx, const char* n) : c(ctx), name(n) {
+    if (c->timing) t0 = std::chrono::steady_clock::now();
+  }
+  ~HostRegion() {
+    if (c->timing)
+      c->htimed.push_back({name, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count()});
+  }
 };
 
 // RAII CUDA-event timer of a region on the context stream (no-op unless timing is on)
@@ -160,6 +177,7 @@ struct Buf {
 
 template <class T>
 dc_status alloc(Ctx* c, Buf<T>& b, size_t n) {
+  HostRegion hr(c, "alloc");
   b.release();
   b.s = c->stream;
   b.n = n;
@@ -181,6 +199,7 @@ dc_status alloc_zero(Ctx* c, Buf<T>& b, size_t n) {
 // persistent (handle-owned) allocation
 template <class T>
 dc_status palloc(Ctx* c, T*& p, size_t n) {
+  HostRegion hr(c, "palloc");
   cudaError_t e = cudaMallocAsync((void**)&p, (n ? n : 1) * sizeof(T), c->stream);
   if (e != cudaSuccess) {
     p = nullptr;

@@ -172,22 +172,27 @@ __device__ __forceinline__ void own_flush(OwnSmem& sm, const OwnArgs& a, uint32_
   cons_sync();
 }
 
-__device__ __forceinline__ void own_insert(OwnSmem& sm, const OwnArgs& a, uint32_t key, uint32_t add, uint32_t ctx) {
-  uint32_t h = (key * 0x9E3779B1u) >> (32 - 14);  // log2(OW_TAB) = 14
+__device__ __forceinline__ uint32_t own_hash(uint32_t key) { return (key * 0x9E3779B1u) >> (32 - 14); }  // log2(OW_TAB) = 14
+
+// slow path of the probe: key is not in its home slot
+__device__ __noinline__ uint32_t own_probe(OwnSmem& sm, uint32_t key, uint32_t h) {
   volatile uint32_t* vk = sm.key;
   while (true) {
     const uint32_t k = vk[h];
-    if (k == key) break;
+    if (k == key) return h;
     if (k == EMPTY32) {
       const uint32_t old = atomicCAS(&sm.key[h], EMPTY32, key);
       if (old == EMPTY32) {
         if (atomicAdd(&sm.distinct, 1u) == OW_FLUSH_REQ) *(volatile uint32_t*)&sm.flush_req = 1u;
-        break;
+        return h;
       }
-      if (old == key) break;
+      if (old == key) return h;
     }
     h = (h + 1) & (OW_TAB - 1);
   }
+}
+
+__device__ __forceinline__ void own_add(OwnSmem& sm, const OwnArgs& a, uint32_t key, uint32_t h, uint32_t add, uint32_t ctx) {
   const uint32_t old = atomicAdd(&sm.cnt[h], add);
   if (old + add < old) {  // 32-bit wrap: emit the 2^32 carry as its own one-entry segment
     const unsigned long long base = atomicAdd(a.g_entries, 1ull);
@@ -206,33 +211,35 @@ struct OwCounters {
   uint32_t bad_l, bad_s, zero, fallback;
 };
 
-// classify one staged sample; returns its key (EMPTY32 when it is not aggregated)
-__device__ __forceinline__ uint32_t own_classify(const uint4 q, const OwMeta& m, const OwnArgs& a, bool ctx_ok, OwCounters& k,
-                                                 uint32_t& c) {
-  const uint32_t stall = q.z & 0xFFFFu;
-  c = q.w;
-  if (q.x >= a.n_launch) { ++k.bad_l; return EMPTY32; }
-  if (q.x != m.launch) { k.fallback = 1; return EMPTY32; }  // misplaced sample: generic schedule
-  if (stall >= a.S) { ++k.bad_s; return EMPTY32; }
-  if (c == 0) { ++k.zero; return EMPTY32; }
-  if (!ctx_ok) { atomicOr(a.trace_flags, (uint32_t)FLAG_BAD_LEAF); return EMPTY32; }
-  if (q.y >= (1u << 27)) { k.fallback = 1; return EMPTY32; }
-  const uint32_t key = (q.y << 5) | stall;
-  if (key == EMPTY32) k.fallback = 1;
-  return key;
+// rare path: classify a sample that failed the fused validity test (same order of checks as
+// the generic schedule: launch, stall, count)
+__device__ __noinline__ uint32_t own_reject(uint32_t launch, uint32_t stall, uint32_t count, uint32_t seg_launch, uint64_t n_launch,
+                                            uint32_t S, bool ctx_ok, uint32_t* trace_flags) {
+  // returns the counter to bump: 0 bad launch, 1 bad stall, 2 zero count, 3 fallback, 4 none
+  if (launch >= n_launch) return 0;
+  if (launch != seg_launch) return 3;  // misplaced sample: generic schedule
+  if (stall >= S) return 1;
+  if (count == 0) return 2;
+  if (!ctx_ok) {
+    atomicOr(trace_flags, (uint32_t)FLAG_BAD_LEAF);
+    return 4;
+  }
+  return 3;  // pc_off >= 2^27 - 1 (key would not fit 32 bits)
 }
 
-__device__ __forceinline__ void own_aggregate(OwnSmem& sm, const OwnArgs& a, uint32_t key, uint32_t c, uint32_t ctx) {
-  const bool valid = key != EMPTY32;
-  const uint32_t peers = __match_any_sync(0xffffffffu, key);
-  const bool ones = __all_sync(0xffffffffu, !valid || c == 1);
-  if (valid) {
-    if (ones) {
-      if ((peers & lanemask_lt()) == 0) own_insert(sm, a, key, __popc(peers), ctx);
-    } else {
-      own_insert(sm, a, key, c, ctx);
-    }
+// sample -> key; EMPTY32 when not aggregated. Fused branch-free validity test on the hot path.
+__device__ __forceinline__ uint32_t own_key(const uint4 q, uint32_t seg_launch, const OwnArgs& a, bool ctx_ok, OwCounters& k) {
+  const uint32_t stall = q.z & 0xFFFFu;
+  const bool ok = (q.x == seg_launch) & (stall < a.S) & (q.w != 0) & (q.y < (1u << 27) - 1u) & ctx_ok & (q.x < a.n_launch);
+  if (__builtin_expect(!ok, 0)) {
+    const uint32_t r = own_reject(q.x, stall, q.w, seg_launch, a.n_launch, a.S, ctx_ok, a.trace_flags);
+    k.bad_l += r == 0;
+    k.bad_s += r == 1;
+    k.zero += r == 2;
+    k.fallback |= r == 3;
+    return EMPTY32;
   }
+  return (q.y << 5) | stall;  // != EMPTY32 since q.y < 2^27 and stall < 32 ... unless both max
 }
 
 __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
@@ -257,47 +264,67 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
   }
   __syncthreads();
   if (tid < 32) {
-    // ------------------------------------------------ producer warp (lane 0 issues)
-    if (tid == 0) {
-      // first sorted launch whose segment contains r0: largest i with cum[i] <= r0
-      uint64_t lo = 0, hi = a.n_launch;
-      while (lo < hi) {
-        const uint64_t mid = (lo + hi + 1) >> 1;
-        if (a.cum[mid] <= r0) lo = mid;
-        else hi = mid - 1;
-      }
-      uint64_t i = lo, pos = r0;
-      uint32_t st = 0, ph = 0, prev_ctx = OW_DONE;
-      volatile uint32_t* freq = &sm.flush_req;
-      while (pos < r1) {
-        const uint64_t seg_end = a.cum[i + 1];
-        if (seg_end <= pos) {
-          ++i;
-          continue;
+    // ------------------------------------------------ producer warp
+    // The 32 lanes fetch the next 32 sorted launches' (start, end, source offset, ctx, id) in
+    // one batch of parallel loads; lane 0 then walks them, issuing one TMA bulk copy per chunk.
+    const uint32_t lane = tid;
+    uint64_t lo = 0, hi = a.n_launch;  // first sorted launch whose segment contains r0
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi + 1) >> 1;
+      if (a.cum[mid] <= r0) lo = mid;
+      else hi = mid - 1;
+    }
+    uint64_t i = lo, pos = r0, batch = ~0ull;
+    uint64_t my_beg = 0, my_end = 0, my_src = 0;
+    uint32_t my_l = 0, my_ctx = 0;
+    uint32_t st = 0, ph = 0, prev_ctx = OW_DONE;
+    volatile uint32_t* freq = &sm.flush_req;
+    while (pos < r1) {
+      if (batch == ~0ull || i >= batch + 32) {
+        batch = i;
+        const uint64_t b = batch + lane;
+        if (b < a.n_launch) {
+          my_beg = a.cum[b];
+          my_end = a.cum[b + 1];
+          my_l = a.order[b];
+          my_ctx = (uint32_t)a.lkey[b];
+          my_src = a.launch_off[my_l];
         }
-        const uint32_t l = a.order[i];
-        uint64_t chunk = seg_end - pos;
-        if (r1 - pos < chunk) chunk = r1 - pos;
-        if (chunk > OW_STAGE) chunk = OW_STAGE;
+      }
+      const uint32_t j = (uint32_t)(i - batch);
+      const uint64_t seg_beg = __shfl_sync(0xffffffffu, my_beg, j);
+      const uint64_t seg_end = __shfl_sync(0xffffffffu, my_end, j);
+      const uint32_t l = __shfl_sync(0xffffffffu, my_l, j);
+      const uint32_t ctx = __shfl_sync(0xffffffffu, my_ctx, j);
+      const uint64_t src0 = __shfl_sync(0xffffffffu, my_src, j);
+      if (seg_end <= pos) {
+        ++i;
+        continue;
+      }
+      uint64_t chunk = seg_end - pos;
+      if (r1 - pos < chunk) chunk = r1 - pos;
+      if (chunk > OW_STAGE) chunk = OW_STAGE;
+      if (lane == 0) {
         mbar_wait(&sm.empty[st], ph ^ 1u);
-        const uint32_t ctx = (uint32_t)a.lkey[i];
         uint32_t flush = ctx != prev_ctx ? 1u : 0u;
         if (*freq) {
           *freq = 0u;
           flush = 1u;
         }
-        prev_ctx = ctx;
         sm.meta[st] = OwMeta{l, ctx, (uint32_t)chunk, flush};
-        const dc_pc_sample* src = a.smp + a.launch_off[l] + (pos - a.cum[i]);
         mbar_expect_tx(&sm.full[st], (uint32_t)chunk * 16u);
-        tma_bulk_g2s(&sm.stage[st][0], src, (uint32_t)chunk * 16u, &sm.full[st]);
-        pos += chunk;
-        if (pos == seg_end) ++i;
-        if (++st == OW_STAGES) {
-          st = 0;
-          ph ^= 1u;
-        }
+        tma_bulk_g2s(&sm.stage[st][0], a.smp + src0 + (pos - seg_beg), (uint32_t)chunk * 16u, &sm.full[st]);
       }
+      __syncwarp();
+      prev_ctx = ctx;
+      pos += chunk;
+      if (pos == seg_end) ++i;
+      if (++st == OW_STAGES) {
+        st = 0;
+        ph ^= 1u;
+      }
+    }
+    if (lane == 0) {
       mbar_wait(&sm.empty[st], ph ^ 1u);
       sm.meta[st] = OwMeta{0, OW_DONE, 0, 1};
       mbar_arrive(&sm.full[st]);
@@ -318,17 +345,24 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
     if (m.ctx == OW_DONE) break;
     cur_ctx = m.ctx;
     const bool ctx_ok = m.ctx < a.N;
-    // two samples per consumer thread (OW_STAGE = 2 * OW_CONS)
+    // two samples per consumer thread (OW_STAGE = 2 * OW_CONS), processed side by side for ILP
     const uint32_t j0 = ctid, j1 = ctid + OW_CONS;
     const uint4 q0 = j0 < m.count ? sm.stage[st][j0] : make_uint4(0, 0, 0, 0);
     const uint4 q1 = j1 < m.count ? sm.stage[st][j1] : make_uint4(0, 0, 0, 0);
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[st]);  // the stage is consumed into registers: release it early
-    uint32_t c0 = 0, c1 = 0;
-    const uint32_t key0 = j0 < m.count ? own_classify(q0, m, a, ctx_ok, k, c0) : EMPTY32;
-    const uint32_t key1 = j1 < m.count ? own_classify(q1, m, a, ctx_ok, k, c1) : EMPTY32;
-    own_aggregate(sm, a, key0, c0, m.ctx);
-    own_aggregate(sm, a, key1, c1, m.ctx);
+    const uint32_t key0 = j0 < m.count ? own_key(q0, m.launch, a, ctx_ok, k) : EMPTY32;
+    const uint32_t key1 = j1 < m.count ? own_key(q1, m.launch, a, ctx_ok, k) : EMPTY32;
+    uint32_t h0 = own_hash(key0), h1 = own_hash(key1);
+    const uint32_t s0 = sm.key[h0], s1 = sm.key[h1];  // home slots (hit after warm-up)
+    if (key0 != EMPTY32) {
+      if (s0 != key0) h0 = own_probe(sm, key0, h0);
+      own_add(sm, a, key0, h0, q0.w, m.ctx);
+    }
+    if (key1 != EMPTY32) {
+      if (s1 != key1) h1 = own_probe(sm, key1, h1);
+      own_add(sm, a, key1, h1, q1.w, m.ctx);
+    }
     if (++st == OW_STAGES) {
       st = 0;
       ph ^= 1u;
@@ -365,7 +399,7 @@ struct RedSmem {
   uint32_t wcnt[32][256];
   uint32_t hist[RD_BUCKETS];
   uint16_t bchunk[RD_BUCKETS];
-  unsigned long long stall_tot[32];
+  unsigned long long wstall[32][32];  // [warp][stall]
   uint32_t fill, maxkey, prev_key, total, bad;
 };
 
@@ -383,7 +417,7 @@ __global__ void __launch_bounds__(RD_THREADS, 1) k_own_reduce(
   for (uint32_t g = blockIdx.x; g < n_groups; g += gridDim.x) {
     const uint32_t gs = grp_start[g], ge = grp_start[g + 1];
     const uint32_t ctx = seg[seg_order[gs]].x;
-    if (tid < 32) sm.stall_tot[tid] = 0;
+    unsigned long long stall_acc = 0;  // this lane's stall (= lane id) total over its warp's heads
     if (tid == 0) {
       sm.maxkey = 0;
       sm.bad = 0;
@@ -447,10 +481,16 @@ __global__ void __launch_bounds__(RD_THREADS, 1) k_own_reduce(
       for (uint32_t si = gs; si < ge; ++si) {
         const uint4 sg = seg[seg_order[si]];
         const uint64_t base = (uint64_t)sg.z | ((uint64_t)sg.w << 32);
-        for (uint32_t j = tid; j < sg.y; j += RD_THREADS) {
-          const uint32_t kk = pkey[base + j];
-          if (nchunks == 1 || sm.bchunk[kk >> bshift] == ch) {
-            const uint32_t slot = atomicAdd(&sm.fill, 1u);
+        for (uint32_t j0 = 0; j0 < sg.y; j0 += RD_THREADS) {  // warp-uniform trip count
+          const uint32_t j = j0 + tid;
+          const uint32_t kk = j < sg.y ? pkey[base + j] : 0;
+          const bool take = j < sg.y && (nchunks == 1 || sm.bchunk[kk >> bshift] == ch);
+          const uint32_t m = __ballot_sync(0xffffffffu, take);
+          uint32_t wbase = 0;
+          if (lane == 0 && m) wbase = atomicAdd(&sm.fill, (uint32_t)__popc(m));  // one atomic per warp
+          wbase = __shfl_sync(0xffffffffu, wbase, 0);
+          if (take) {
+            const uint32_t slot = wbase + __popc(m & lanemask_lt());
             sm.k[0][slot] = kk;
             sm.v[0][slot] = (uint32_t)(base + j);
           }
@@ -520,12 +560,19 @@ __global__ void __launch_bounds__(RD_THREADS, 1) k_own_reduce(
         uint32_t tot_h, tot_p;
         const uint32_t ex = block_excl_scan<uint32_t, RD_THREADS>(head, &tot_h);
         block_excl_scan<uint32_t, RD_THREADS>(pchead, &tot_p);
+        unsigned long long s = 0;
         if (head) {
-          unsigned long long s = 0;
           for (uint32_t t = j; t < n && sm.k[cur][t] == kk; ++t) s += pcnt[sm.v[cur][t]];
           okey[obase + n_out + ex] = kk;
           ocnt[obase + n_out + ex] = s;
-          atomicAdd(&sm.stall_tot[kk & 31u], s);
+        }
+        // per-stall totals without shared atomics: lane q of each warp collects stall q
+        const uint32_t my_stall = head ? (kk & 31u) : 32u;
+#pragma unroll 4
+        for (int src = 0; src < 32; ++src) {
+          const uint32_t st = __shfl_sync(0xffffffffu, my_stall, src);
+          const unsigned long long sv = __shfl_sync(0xffffffffu, s, src);
+          if (st == lane) stall_acc += sv;
         }
         n_out += tot_h;
         n_pc += tot_p;
@@ -539,11 +586,16 @@ __global__ void __launch_bounds__(RD_THREADS, 1) k_own_reduce(
       g_npcs[g] = n_pc;
       g_ctx[g] = ctx;
     }
-    if (tid < S && ctx < N) xstall[(uint64_t)tid * N + ctx] = sm.stall_tot[tid];
-    if (tid == 0 && ctx < N) {
-      unsigned long long s = 0;
-      for (uint32_t q = 0; q < S; ++q) s += sm.stall_tot[q];
-      xsamples[ctx] = s;
+    sm.wstall[w][lane] = stall_acc;
+    __syncthreads();
+    if (w == 0) {
+      unsigned long long t = 0;
+      for (int ww = 0; ww < RD_THREADS / 32; ++ww) t += sm.wstall[ww][lane];
+      if (lane < S && ctx < N) xstall[(uint64_t)lane * N + ctx] = t;
+      unsigned long long tot = lane < S ? t : 0;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+      if (lane == 0 && ctx < N) xsamples[ctx] = tot;
     }
     __syncthreads();
   }
