@@ -26,12 +26,15 @@ namespace dc {
 constexpr int OW_CONS_WARPS = 31;
 constexpr int OW_CONS = 32 * OW_CONS_WARPS;   // 992 consumer threads
 constexpr int OW_THREADS = OW_CONS + 32;      // + producer warp = 1024
-constexpr int OW_STAGES = 3;
+constexpr int OW_STAGES = 4;
 constexpr int OW_STAGE = 2 * OW_CONS;         // 1984 samples per stage (31 KB): 2 per consumer thread
-constexpr int OW_TAB = 16384;                 // shared hash table slots
-// a flush is requested at this many distinct keys; at most (OW_STAGES + 1) more stages can
-// be inserted before the flush point the producer marks -> never more than OW_TAB - 1 keys
-constexpr uint32_t OW_FLUSH_REQ = OW_TAB - (OW_STAGES + 1) * OW_STAGE - 1;
+constexpr int OW_TAB = 12288;                 // shared hash table slots (96 KB)
+// a flush is requested at half load; past OW_SPILL_AT distinct keys new keys are not inserted
+// but appended to the CTA's spill region in HBM (kept as partial entries), so the table can
+// never overflow whatever the key cardinality
+constexpr uint32_t OW_FLUSH_REQ = OW_TAB / 2;
+constexpr uint32_t OW_SPILL_AT = OW_TAB - 1024 - OW_CONS;
+constexpr uint32_t OW_SPILL_CAP = 16384;      // spill entries per CTA
 constexpr uint32_t EMPTY32 = 0xFFFFFFFFu;
 constexpr uint32_t OW_DONE = 0xFFFFFFFFu;
 
@@ -49,6 +52,7 @@ struct OwnSmem {
   OwMeta meta[OW_STAGES];
   uint32_t distinct;
   uint32_t flush_req;
+  uint32_t spill_n, spill_seg;  // spill entries written / already covered by a segment
   uint32_t warp_cnt[OW_CONS_WARPS];
   unsigned long long seg_base;
 };
@@ -127,6 +131,7 @@ struct OwnArgs {
   uint32_t* g_flags;
   uint32_t* trace_flags;       // ctx->d_flags (DC_ERR_TRACE conditions)
   unsigned long long* ldiag;
+  uint64_t spill_base0;        // CTA b spills into pkey/pcnt[spill_base0 + b * OW_SPILL_CAP ...]
 };
 
 // all consumer threads; the caller has synchronised the consumers (every insert is done)
@@ -143,8 +148,16 @@ __device__ __forceinline__ void own_flush(OwnSmem& sm, const OwnArgs& a, uint32_
       base = ~0ull;
     }
     sm.seg_base = base;
+    if (sm.spill_n > sm.spill_seg) {  // spilled entries of this context form their own segment
+      const uint32_t ns = min(sm.spill_n, OW_SPILL_CAP) - sm.spill_seg;
+      const uint64_t sb = a.spill_base0 + (uint64_t)blockIdx.x * OW_SPILL_CAP + sm.spill_seg;
+      const unsigned si2 = atomicAdd(a.g_segs, 1u);
+      if (si2 < a.cap_segs) a.seg[si2] = make_uint4(ctx, ns, (uint32_t)sb, (uint32_t)(sb >> 32));
+      else atomicOr(a.g_flags, (uint32_t)OWF_OVERFLOW);
+      sm.spill_seg = sm.spill_n;
+    }
   }
-  constexpr uint32_t PER_WARP = (OW_TAB / 32 + OW_CONS_WARPS - 1) / OW_CONS_WARPS * 32;  // 544 slots, multiple of 32
+  constexpr uint32_t PER_WARP = (OW_TAB / 32 + OW_CONS_WARPS - 1) / OW_CONS_WARPS * 32;  // 416 slots, multiple of 32
   const uint32_t s_lo = w * PER_WARP, s_hi = min((uint32_t)OW_TAB, s_lo + PER_WARP);
   uint32_t c = 0;
   for (uint32_t s = s_lo + lane; s < s_hi; s += 32) c += __popc(__ballot_sync(0xffffffffu, sm.key[s] != EMPTY32));
@@ -172,15 +185,17 @@ __device__ __forceinline__ void own_flush(OwnSmem& sm, const OwnArgs& a, uint32_
   cons_sync();
 }
 
-__device__ __forceinline__ uint32_t own_hash(uint32_t key) { return (key * 0x9E3779B1u) >> (32 - 14); }  // log2(OW_TAB) = 14
+__device__ __forceinline__ uint32_t own_hash(uint32_t key) { return __umulhi(key * 0x9E3779B1u, (uint32_t)OW_TAB); }
 
-// slow path of the probe: key is not in its home slot
+// slow path of the probe: key is not in its home slot. Returns the slot, or OW_TAB when the
+// table is near full (the sample then goes to the spill region).
 __device__ __noinline__ uint32_t own_probe(OwnSmem& sm, uint32_t key, uint32_t h) {
   volatile uint32_t* vk = sm.key;
   while (true) {
     const uint32_t k = vk[h];
     if (k == key) return h;
     if (k == EMPTY32) {
+      if (*(volatile uint32_t*)&sm.distinct >= OW_SPILL_AT) return OW_TAB;
       const uint32_t old = atomicCAS(&sm.key[h], EMPTY32, key);
       if (old == EMPTY32) {
         if (atomicAdd(&sm.distinct, 1u) == OW_FLUSH_REQ) *(volatile uint32_t*)&sm.flush_req = 1u;
@@ -188,11 +203,22 @@ __device__ __noinline__ uint32_t own_probe(OwnSmem& sm, uint32_t key, uint32_t h
       }
       if (old == key) return h;
     }
-    h = (h + 1) & (OW_TAB - 1);
+    h = h + 1 == (uint32_t)OW_TAB ? 0u : h + 1;
   }
 }
 
 __device__ __forceinline__ void own_add(OwnSmem& sm, const OwnArgs& a, uint32_t key, uint32_t h, uint32_t add, uint32_t ctx) {
+  if (h == (uint32_t)OW_TAB) {  // spill: one partial entry in this CTA's region
+    const uint32_t i = atomicAdd(&sm.spill_n, 1u);
+    if (i < OW_SPILL_CAP) {
+      const uint64_t o = a.spill_base0 + (uint64_t)blockIdx.x * OW_SPILL_CAP + i;
+      a.pkey[o] = key;
+      a.pcnt[o] = add;
+    } else {
+      atomicOr(a.g_flags, (uint32_t)OWF_OVERFLOW);
+    }
+    return;
+  }
   const uint32_t old = atomicAdd(&sm.cnt[h], add);
   if (old + add < old) {  // 32-bit wrap: emit the 2^32 carry as its own one-entry segment
     const unsigned long long base = atomicAdd(a.g_entries, 1ull);
@@ -260,6 +286,8 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
     }
     sm.distinct = 0;
     sm.flush_req = 0;
+    sm.spill_n = 0;
+    sm.spill_seg = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -393,14 +421,27 @@ constexpr int RD_THREADS = 1024;
 constexpr uint32_t RD_CAP = 10240;  // entries sorted in shared memory at once
 constexpr int RD_BUCKETS = 4096;
 
+// Bitmap path: with pc' = pc_off >> (common trailing zero bits of the context's PCs), every
+// (pc', stall) key is bit (pc' << 5 | stall) and every PC is exactly one 32-bit word, so a
+// presence bitmap + word prefix sums give each distinct key its rank in (pc, stall) order
+// directly — no sort. Used whenever the context's pc' range fits BM_WORDS words.
+constexpr uint32_t BM_WORDS = 16384;  // 2^19 key bits, PCs with pc' < 16384
 struct RedSmem {
-  uint32_t k[2][RD_CAP];
-  uint32_t v[2][RD_CAP];
-  uint32_t wcnt[32][256];
-  uint32_t hist[RD_BUCKETS];
-  uint16_t bchunk[RD_BUCKETS];
+  union {
+    struct {
+      uint32_t k[2][RD_CAP];
+      uint32_t v[2][RD_CAP];
+      uint32_t wcnt[32][256];
+      uint32_t hist[RD_BUCKETS];
+      uint16_t bchunk[RD_BUCKETS];
+    } r;
+    struct {
+      uint32_t bm[BM_WORDS];
+      uint32_t pre[BM_WORDS];
+    } b;
+  };
   unsigned long long wstall[32][32];  // [warp][stall]
-  uint32_t fill, maxkey, prev_key, total, bad;
+  uint32_t fill, maxkey, prev_key, total, bad, orpc;
 };
 
 __global__ void __launch_bounds__(RD_THREADS, 1) k_own_reduce(
@@ -420,6 +461,7 @@ __global__ void __launch_bounds__(RD_THREADS, 1) k_own_reduce(
     unsigned long long stall_acc = 0;  // this lane's stall (= lane id) total over its warp's heads
     if (tid == 0) {
       sm.maxkey = 0;
+      sm.orpc = 0;
       sm.bad = 0;
       sm.prev_key = 0xFFFFFFFFu;
       uint32_t tot = 0;
@@ -429,40 +471,117 @@ __global__ void __launch_bounds__(RD_THREADS, 1) k_own_reduce(
     __syncthreads();
     const uint32_t E = sm.total;
     // key range (sort width)
-    uint32_t mk = 0;
+    uint32_t mk = 0, orp = 0;
     for (uint32_t si = gs; si < ge; ++si) {
       const uint4 sg = seg[seg_order[si]];
       const uint64_t base = (uint64_t)sg.z | ((uint64_t)sg.w << 32);
-      for (uint32_t j = tid; j < sg.y; j += RD_THREADS) mk = max(mk, pkey[base + j]);
+      for (uint32_t j = tid; j < sg.y; j += RD_THREADS) {
+        const uint32_t kk = pkey[base + j];
+        mk = max(mk, kk);
+        orp |= kk >> 5;
+      }
     }
     mk = __reduce_max_sync(0xffffffffu, mk);
-    if (lane == 0) atomicMax(&sm.maxkey, mk);
+    orp = __reduce_or_sync(0xffffffffu, orp);
+    if (lane == 0) {
+      atomicMax(&sm.maxkey, mk);
+      atomicOr(&sm.orpc, orp);
+    }
     __syncthreads();
+    const uint64_t obase = grp_out[g];
+    uint32_t n_out = 0, n_pc = 0;
+    const int pshift = sm.orpc ? __ffs(sm.orpc) - 1 : 0;  // common trailing zero bits of the PCs
+    const uint32_t nwords = ((sm.maxkey >> 5) >> pshift) + 1;
+    if (nwords <= BM_WORDS) {
+      // ---------------- bitmap path: bit (pc' << 5 | stall), one word per PC
+      for (uint32_t wd = tid; wd < nwords; wd += RD_THREADS) sm.b.bm[wd] = 0;
+      __syncthreads();
+      for (uint32_t si = gs; si < ge; ++si) {
+        const uint4 sg = seg[seg_order[si]];
+        const uint64_t base = (uint64_t)sg.z | ((uint64_t)sg.w << 32);
+        for (uint32_t j = tid; j < sg.y; j += RD_THREADS) {
+          const uint32_t kk = pkey[base + j];
+          atomicOr(&sm.b.bm[(kk >> 5) >> pshift], 1u << (kk & 31u));
+        }
+      }
+      __syncthreads();
+      // word prefix sums (rank of the first key of each PC) and PC count
+      constexpr uint32_t WPT = BM_WORDS / RD_THREADS;  // 16 words per thread
+      uint32_t cnt = 0, npc_t = 0;
+#pragma unroll
+      for (uint32_t q = 0; q < WPT; ++q) {
+        const uint32_t wd = tid * WPT + q;
+        const uint32_t bits = wd < nwords ? sm.b.bm[wd] : 0u;
+        cnt += __popc(bits);
+        npc_t += bits != 0;
+      }
+      uint32_t tot_bins, tot_pcs;
+      uint32_t run = block_excl_scan<uint32_t, RD_THREADS>(cnt, &tot_bins);
+      block_excl_scan<uint32_t, RD_THREADS>(npc_t, &tot_pcs);
+      for (uint32_t q = 0; q < WPT; ++q) {
+        const uint32_t wd = tid * WPT + q;
+        if (wd >= nwords) break;
+        uint32_t bits = sm.b.bm[wd];
+        sm.b.pre[wd] = run;
+        while (bits) {  // emit the PC's keys in stall order; counts start at 0
+          const uint32_t b = __ffs(bits) - 1;
+          bits &= bits - 1;
+          okey[obase + run] = ((wd << pshift) << 5) | b;
+          ocnt[obase + run] = 0;
+          ++run;
+        }
+      }
+      __syncthreads();  // orders the zeroing above before the atomics below (same CTA)
+      for (uint32_t si = gs; si < ge; ++si) {
+        const uint4 sg = seg[seg_order[si]];
+        const uint64_t base = (uint64_t)sg.z | ((uint64_t)sg.w << 32);
+        for (uint32_t j0 = 0; j0 < sg.y; j0 += RD_THREADS) {  // warp-uniform trip count
+          const uint32_t j = j0 + tid;
+          const bool ok = j < sg.y;
+          const uint32_t kk = ok ? pkey[base + j] : 0;
+          const unsigned long long cv = ok ? pcnt[base + j] : 0;
+          if (ok) {
+            const uint32_t wd = (kk >> 5) >> pshift, b = kk & 31u;
+            const uint32_t rank = sm.b.pre[wd] + __popc(sm.b.bm[wd] & ((1u << b) - 1u));
+            atomicAdd(&ocnt[obase + rank], cv);
+          }
+          const uint32_t my_stall = ok ? (kk & 31u) : 32u;
+#pragma unroll 4
+          for (int src = 0; src < 32; ++src) {
+            const uint32_t st = __shfl_sync(0xffffffffu, my_stall, src);
+            const unsigned long long sv = __shfl_sync(0xffffffffu, cv, src);
+            if (st == lane) stall_acc += sv;
+          }
+        }
+      }
+      n_out = tot_bins;
+      n_pc = tot_pcs;
+    } else {
     const int kb = sm.maxkey ? 32 - __clz(sm.maxkey) : 1;
     const int bshift = kb > 12 ? kb - 12 : 0;
     uint32_t nchunks = 1;
     if (E > RD_CAP) {
       // chunk c holds the buckets whose exclusive prefix lies in [c*HALF, (c+1)*HALF): with every
       // bucket <= HALF, a chunk holds <= RD_CAP entries
-      for (uint32_t b = tid; b < RD_BUCKETS; b += RD_THREADS) sm.hist[b] = 0;
+      for (uint32_t b = tid; b < RD_BUCKETS; b += RD_THREADS) sm.r.hist[b] = 0;
       __syncthreads();
       for (uint32_t si = gs; si < ge; ++si) {
         const uint4 sg = seg[seg_order[si]];
         const uint64_t base = (uint64_t)sg.z | ((uint64_t)sg.w << 32);
-        for (uint32_t j = tid; j < sg.y; j += RD_THREADS) atomicAdd(&sm.hist[pkey[base + j] >> bshift], 1u);
+        for (uint32_t j = tid; j < sg.y; j += RD_THREADS) atomicAdd(&sm.r.hist[pkey[base + j] >> bshift], 1u);
       }
       __syncthreads();
       uint32_t h4[4], s4 = 0;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        h4[q] = sm.hist[tid * 4 + q];
+        h4[q] = sm.r.hist[tid * 4 + q];
         s4 += h4[q];
         if (h4[q] > HALF) sm.bad = 1;
       }
       uint32_t ex = block_excl_scan<uint32_t, RD_THREADS>(s4, nullptr);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        sm.bchunk[tid * 4 + q] = (uint16_t)(ex / HALF);
+        sm.r.bchunk[tid * 4 + q] = (uint16_t)(ex / HALF);
         ex += h4[q];
       }
       __syncthreads();
@@ -473,8 +592,6 @@ __global__ void __launch_bounds__(RD_THREADS, 1) k_own_reduce(
       }
       nchunks = (E - 1) / HALF + 1;
     }
-    const uint64_t obase = grp_out[g];
-    uint32_t n_out = 0, n_pc = 0;
     for (uint32_t ch = 0; ch < nchunks; ++ch) {
       if (tid == 0) sm.fill = 0;
       __syncthreads();
@@ -484,15 +601,15 @@ __global__ void __launch_bounds__(RD_THREADS, 1) k_own_reduce(
         for (uint32_t j0 = 0; j0 < sg.y; j0 += RD_THREADS) {  // warp-uniform trip count
           const uint32_t j = j0 + tid;
           const uint32_t kk = j < sg.y ? pkey[base + j] : 0;
-          const bool take = j < sg.y && (nchunks == 1 || sm.bchunk[kk >> bshift] == ch);
+          const bool take = j < sg.y && (nchunks == 1 || sm.r.bchunk[kk >> bshift] == ch);
           const uint32_t m = __ballot_sync(0xffffffffu, take);
           uint32_t wbase = 0;
           if (lane == 0 && m) wbase = atomicAdd(&sm.fill, (uint32_t)__popc(m));  // one atomic per warp
           wbase = __shfl_sync(0xffffffffu, wbase, 0);
           if (take) {
             const uint32_t slot = wbase + __popc(m & lanemask_lt());
-            sm.k[0][slot] = kk;
-            sm.v[0][slot] = (uint32_t)(base + j);
+            sm.r.k[0][slot] = kk;
+            sm.r.v[0][slot] = (uint32_t)(base + j);
           }
         }
       }
@@ -505,27 +622,27 @@ __global__ void __launch_bounds__(RD_THREADS, 1) k_own_reduce(
       for (int shift = 0; shift < kb; shift += 8) {
         const int nb = kb - shift < 8 ? kb - shift : 8;
         const uint32_t mask = (1u << nb) - 1u;
-        for (int i = tid; i < 32 * 256; i += RD_THREADS) (&sm.wcnt[0][0])[i] = 0;
+        for (int i = tid; i < 32 * 256; i += RD_THREADS) (&sm.r.wcnt[0][0])[i] = 0;
         __syncthreads();
         const uint32_t b0 = w * per_warp, b1 = min(n, b0 + per_warp);
         for (uint32_t bs = b0; bs < b1; bs += 32) {
           const uint32_t j = bs + lane;
           const bool ok = j < b1;
-          const uint32_t d = ok ? (sm.k[cur][j] >> shift) & mask : 0xFFFFFFFFu;
+          const uint32_t d = ok ? (sm.r.k[cur][j] >> shift) & mask : 0xFFFFFFFFu;
           const uint32_t peers = __match_any_sync(0xffffffffu, d);
-          if (ok && (peers & lanemask_lt()) == 0) sm.wcnt[w][d] += __popc(peers);
+          if (ok && (peers & lanemask_lt()) == 0) sm.r.wcnt[w][d] += __popc(peers);
           __syncwarp();
         }
         __syncthreads();
         uint32_t tot = 0;
         if (tid < 256)
-          for (int ww = 0; ww < 32; ++ww) tot += sm.wcnt[ww][tid];
+          for (int ww = 0; ww < 32; ++ww) tot += sm.r.wcnt[ww][tid];
         const uint32_t ex = block_excl_scan<uint32_t, RD_THREADS>(tid < 256 ? tot : 0u, nullptr);
         if (tid < 256) {
           uint32_t run = ex;
           for (int ww = 0; ww < 32; ++ww) {
-            const uint32_t c = sm.wcnt[ww][tid];
-            sm.wcnt[ww][tid] = run;
+            const uint32_t c = sm.r.wcnt[ww][tid];
+            sm.r.wcnt[ww][tid] = run;
             run += c;
           }
         }
@@ -533,16 +650,16 @@ __global__ void __launch_bounds__(RD_THREADS, 1) k_own_reduce(
         for (uint32_t bs = b0; bs < b1; bs += 32) {
           const uint32_t j = bs + lane;
           const bool ok = j < b1;
-          const uint32_t kk = ok ? sm.k[cur][j] : 0, vv = ok ? sm.v[cur][j] : 0;
+          const uint32_t kk = ok ? sm.r.k[cur][j] : 0, vv = ok ? sm.r.v[cur][j] : 0;
           const uint32_t d = ok ? (kk >> shift) & mask : 0xFFFFFFFFu;
           const uint32_t peers = __match_any_sync(0xffffffffu, d);
-          const uint32_t pos = ok ? sm.wcnt[w][d] + __popc(peers & lanemask_lt()) : 0;
+          const uint32_t pos = ok ? sm.r.wcnt[w][d] + __popc(peers & lanemask_lt()) : 0;
           __syncwarp();
-          if (ok && (peers & lanemask_lt()) == 0) sm.wcnt[w][d] += __popc(peers);
+          if (ok && (peers & lanemask_lt()) == 0) sm.r.wcnt[w][d] += __popc(peers);
           __syncwarp();
           if (ok) {
-            sm.k[cur ^ 1][pos] = kk;
-            sm.v[cur ^ 1][pos] = vv;
+            sm.r.k[cur ^ 1][pos] = kk;
+            sm.r.v[cur ^ 1][pos] = vv;
           }
         }
         __syncthreads();
@@ -553,8 +670,8 @@ __global__ void __launch_bounds__(RD_THREADS, 1) k_own_reduce(
       for (uint32_t bs = 0; bs < n; bs += RD_THREADS) {
         const uint32_t j = bs + tid;
         const bool ok = j < n;
-        const uint32_t kk = ok ? sm.k[cur][j] : 0;
-        const uint32_t pk = j == 0 ? prev : (ok ? sm.k[cur][j - 1] : 0);
+        const uint32_t kk = ok ? sm.r.k[cur][j] : 0;
+        const uint32_t pk = j == 0 ? prev : (ok ? sm.r.k[cur][j - 1] : 0);
         const uint32_t head = ok && (pk != kk) ? 1u : 0u;
         const uint32_t pchead = ok && (pk == 0xFFFFFFFFu || (pk >> 5) != (kk >> 5)) ? 1u : 0u;
         uint32_t tot_h, tot_p;
@@ -562,7 +679,7 @@ __global__ void __launch_bounds__(RD_THREADS, 1) k_own_reduce(
         block_excl_scan<uint32_t, RD_THREADS>(pchead, &tot_p);
         unsigned long long s = 0;
         if (head) {
-          for (uint32_t t = j; t < n && sm.k[cur][t] == kk; ++t) s += pcnt[sm.v[cur][t]];
+          for (uint32_t t = j; t < n && sm.r.k[cur][t] == kk; ++t) s += pcnt[sm.r.v[cur][t]];
           okey[obase + n_out + ex] = kk;
           ocnt[obase + n_out + ex] = s;
         }
@@ -578,9 +695,10 @@ __global__ void __launch_bounds__(RD_THREADS, 1) k_own_reduce(
         n_pc += tot_p;
         __syncthreads();
       }
-      if (tid == 0 && n) sm.prev_key = sm.k[cur][n - 1];
+      if (tid == 0 && n) sm.prev_key = sm.r.k[cur][n - 1];
       __syncthreads();
     }
+    }  // radix path
     if (tid == 0) {
       g_nbins[g] = n_out;
       g_npcs[g] = n_pc;
@@ -706,8 +824,8 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
   uint32_t hf[2];
   {
     Region rp(c, "pc:main");
-    DC_TRY(alloc(c, pkey, cap_entries));
-    DC_TRY(alloc(c, pcnt, cap_entries));
+    DC_TRY(alloc(c, pkey, cap_entries + (uint64_t)G * OW_SPILL_CAP));
+    DC_TRY(alloc(c, pcnt, cap_entries + (uint64_t)G * OW_SPILL_CAP));
     DC_TRY(alloc(c, seg, cap_segs));
     DC_TRY(alloc_zero(c, ctr, 2));
     DC_TRY(alloc_zero(c, flags, 2));
@@ -732,6 +850,7 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
     a.g_flags = flags.p;
     a.trace_flags = c->d_flags;
     a.ldiag = ldiag.p;
+    a.spill_base0 = cap_entries;
     const size_t smem = sizeof(OwnSmem);
     static bool attr_set = false;
     if (!attr_set) {
@@ -784,8 +903,8 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
   Buf<uint32_t> okey, gnb, gnp, gctx, bbase, pbase;
   Buf<unsigned long long> ocnt;
   Buf<uint32_t> tots;
-  DC_TRY(alloc(c, okey, hc[0]));
-  DC_TRY(alloc(c, ocnt, hc[0]));
+  DC_TRY(alloc(c, okey, hc[0] + (uint64_t)G * OW_SPILL_CAP));  // table entries + spills
+  DC_TRY(alloc(c, ocnt, hc[0] + (uint64_t)G * OW_SPILL_CAP));
   DC_TRY(alloc(c, gnb, n_groups));
   DC_TRY(alloc(c, gnp, n_groups));
   DC_TRY(alloc(c, gctx, n_groups));

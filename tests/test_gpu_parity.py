@@ -157,6 +157,24 @@ def test_generic_schedule_equals_owner_schedule():
     assert_same(a, b, ctx="owner vs generic")
 
 
+@pytest.mark.parametrize("n,npc,big", [(3_000_000, 2000, False), (400_000, 20_000, False), (200_000, 300, True)])
+def test_owner_high_cardinality_flush_spill_and_wrap(n, npc, big):
+    """One context with up to 480k (pc, stall) keys: mid-context flushes and spills in the
+    context-owner schedule; big=True uses counts up to 2^31 (32-bit shared-counter carries)."""
+    rng = np.random.default_rng(n)
+    s = np.zeros(n, oracle.SAMPLE_DTYPE)
+    s["launch"] = 0
+    s["pc_off"] = 16 * rng.integers(0, npc, n)
+    s["stall"] = rng.integers(0, 24, n)
+    s["count"] = rng.integers(1, 2**31, n) if big else 1
+    off, fr = _csr([(0, 1)])
+    X = np.ones((1, 1), np.uint64)
+    lo = np.array([0, n], np.uint64)
+    a = gpu_run(off, fr, X, n_frames=2, samples=s, launch_off=lo, n_stall=24)
+    ref = oracle_run(off, fr, X, 1, s, 1, 24).arrays()
+    assert_same(a, ref, ctx=f"owner n={n} npc={npc}")
+
+
 def test_edge_cases():
     # empty trace
     a = gpu_run(np.zeros(1, np.uint64), np.zeros(0, np.uint32), np.zeros((1, 0), np.uint64), n_frames=5)
