@@ -140,11 +140,13 @@ dc_status fail(Ctx* c, dc_status s, const char* fmt, ...);
   } while (0)
 
 // after a kernel launch: count it and check the launch error
-#define DC_LAUNCHED(ctx)                                                         \
-  do {                                                                           \
-    (ctx)->launches++;                                                           \
-    cudaError_t _e = cudaGetLastError();                                         \
-    if (_e != cudaSuccess) return ::dc::cuda_fail((ctx), _e, "kernel launch");   \
+#define DC_STR2(x) #x
+#define DC_STR(x) DC_STR2(x)
+#define DC_LAUNCHED(ctx)                                                                              \
+  do {                                                                                                \
+    (ctx)->launches++;                                                                                \
+    cudaError_t _e = cudaGetLastError();                                                              \
+    if (_e != cudaSuccess) return ::dc::cuda_fail((ctx), _e, "kernel launch at " __FILE__ ":" DC_STR(__LINE__)); \
   } while (0)
 
 // stream-ordered device allocation (memory pool); RAII buffer

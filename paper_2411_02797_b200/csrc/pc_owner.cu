@@ -19,21 +19,27 @@
 // Any sample this schedule cannot take (a valid launch that disagrees with its segment,
 // pc_off >= 2^27, a context whose partial list cannot be chunked into shared memory) makes
 // the call fall back to the generic schedule (pc.cu) for the whole input — same result.
+#include <stdlib.h>
+
 #include "prim.cuh"
 
 namespace dc {
 
-constexpr int OW_CONS_WARPS = 31;
-constexpr int OW_CONS = 32 * OW_CONS_WARPS;   // 992 consumer threads
-constexpr int OW_THREADS = OW_CONS + 32;      // + producer warp = 1024
+constexpr int OW_CONS_WARPS = 16;
+constexpr int OW_CONS = 32 * OW_CONS_WARPS;   // 512 consumer threads
+constexpr int OW_THREADS = OW_CONS + 32;      // + producer warp
 constexpr int OW_STAGES = 4;
-constexpr int OW_STAGE = 2 * OW_CONS;         // 1984 samples per stage (31 KB): 2 per consumer thread
+constexpr int OW_PER_LANE = 4;                // samples per lane per stage
+constexpr int OW_ROUND = 32 * OW_PER_LANE;    // samples per warp per stage
+constexpr int OW_STAGE = OW_CONS_WARPS * OW_ROUND;  // 2048 samples per stage (32 KB)
+constexpr int OW_SUBS = 8;                    // launches packed into one stage at most
 constexpr int OW_TAB = 12288;                 // shared hash table slots (96 KB)
-// a flush is requested at half load; past OW_SPILL_AT distinct keys new keys are not inserted
+// a flush is requested at 2/3 load; past OW_SPILL_AT distinct keys new keys are not inserted
 // but appended to the CTA's spill region in HBM (kept as partial entries), so the table can
-// never overflow whatever the key cardinality
-constexpr uint32_t OW_FLUSH_REQ = OW_TAB / 2;
-constexpr uint32_t OW_SPILL_AT = OW_TAB - 1024 - OW_CONS;
+// never overflow whatever the key cardinality. `distinct` lags by at most one round per warp.
+constexpr uint32_t OW_FLUSH_REQ = OW_TAB * 2 / 3;
+constexpr uint32_t OW_SPILL_AT = OW_TAB - OW_CONS_WARPS * OW_ROUND - 1;
+constexpr uint32_t OW_MISS = 0xFFFFFFFEu;
 constexpr uint32_t OW_SPILL_CAP = 16384;      // spill entries per CTA
 constexpr uint32_t EMPTY32 = 0xFFFFFFFFu;
 constexpr uint32_t OW_DONE = 0xFFFFFFFFu;
@@ -41,7 +47,9 @@ constexpr uint32_t OW_DONE = 0xFFFFFFFFu;
 enum { OWF_FALLBACK = 1, OWF_OVERFLOW = 2 };
 
 struct OwMeta {
-  uint32_t launch, ctx, count, flush;
+  uint32_t ctx, count, flush, nsub;
+  uint32_t sub_end[OW_SUBS];     // exclusive end (stage position) of each launch piece
+  uint32_t sub_launch[OW_SUBS];  // launch of each piece
 };
 
 struct OwnSmem {
@@ -132,6 +140,8 @@ struct OwnArgs {
   uint32_t* trace_flags;       // ctx->d_flags (DC_ERR_TRACE conditions)
   unsigned long long* ldiag;
   uint64_t spill_base0;        // CTA b spills into pkey/pcnt[spill_base0 + b * OW_SPILL_CAP ...]
+  uint32_t probe_mode;         // measurement only (DC_OWN_MODE): 1 = stream + keys, no table
+  uint32_t* sink;
 };
 
 // all consumer threads; the caller has synchronised the consumers (every insert is done)
@@ -139,13 +149,16 @@ __device__ __forceinline__ void own_flush(OwnSmem& sm, const OwnArgs& a, uint32_
   const uint32_t n = sm.distinct;
   const uint32_t w = ctid >> 5, lane = ctid & 31;
   if (ctid == 0) {
-    unsigned long long base = atomicAdd(a.g_entries, (unsigned long long)n);
-    unsigned si = atomicAdd(a.g_segs, 1u);
-    if (si < a.cap_segs && base + n <= a.cap_entries) {
-      a.seg[si] = make_uint4(ctx, n, (uint32_t)base, (uint32_t)(base >> 32));
-    } else {
-      atomicOr(a.g_flags, (uint32_t)OWF_OVERFLOW);
-      base = ~0ull;
+    unsigned long long base = ~0ull;
+    if (n > 0) {
+      base = atomicAdd(a.g_entries, (unsigned long long)n);
+      const unsigned si = atomicAdd(a.g_segs, 1u);
+      if (si < a.cap_segs && base + n <= a.cap_entries) {
+        a.seg[si] = make_uint4(ctx, n, (uint32_t)base, (uint32_t)(base >> 32));
+      } else {
+        atomicOr(a.g_flags, (uint32_t)OWF_OVERFLOW);
+        base = ~0ull;
+      }
     }
     sm.seg_base = base;
     if (sm.spill_n > sm.spill_seg) {  // spilled entries of this context form their own segment
@@ -185,25 +198,42 @@ __device__ __forceinline__ void own_flush(OwnSmem& sm, const OwnArgs& a, uint32_
   cons_sync();
 }
 
-__device__ __forceinline__ uint32_t own_hash(uint32_t key) { return __umulhi(key * 0x9E3779B1u, (uint32_t)OW_TAB); }
+// The table is probed in 4-slot buckets: one 16-B shared load compares a key with a whole
+// bucket, so a key displaced from its home slot usually still costs a single load.
+constexpr uint32_t OW_NB = OW_TAB / 4;
+__device__ __forceinline__ uint32_t own_bucket(uint32_t key) { return __umulhi(key * 0x9E3779B1u, OW_NB); }
+__device__ __forceinline__ int bucket_match(const uint4 v, uint32_t key) {
+  return v.x == key ? 0 : v.y == key ? 1 : v.z == key ? 2 : v.w == key ? 3 : -1;
+}
+__device__ __forceinline__ uint4 ld_shared_v4_volatile(const uint32_t* p) {
+  uint4 v;
+  asm volatile("ld.volatile.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(smem_u32(p)));
+  return v;
+}
 
-// slow path of the probe: key is not in its home slot. Returns the slot, or OW_TAB when the
-// table is near full (the sample then goes to the spill region).
-__device__ __noinline__ uint32_t own_probe(OwnSmem& sm, uint32_t key, uint32_t h) {
-  volatile uint32_t* vk = sm.key;
+// slow path: the key is not in its home bucket (new key, or displaced). Returns the slot, or
+// OW_TAB when the table is near full (the sample then goes to the spill region).
+// returns slot | (1 << 31 if this call inserted the key)
+__device__ __noinline__ uint32_t own_probe(OwnSmem& sm, uint32_t key, uint32_t b) {
+  // `distinct` is refreshed once per warp round (not per insert), hence the margin in OW_SPILL_AT
+  const bool full = *(volatile uint32_t*)&sm.distinct >= OW_SPILL_AT;
   while (true) {
-    const uint32_t k = vk[h];
-    if (k == key) return h;
-    if (k == EMPTY32) {
-      if (*(volatile uint32_t*)&sm.distinct >= OW_SPILL_AT) return OW_TAB;
-      const uint32_t old = atomicCAS(&sm.key[h], EMPTY32, key);
-      if (old == EMPTY32) {
-        if (atomicAdd(&sm.distinct, 1u) == OW_FLUSH_REQ) *(volatile uint32_t*)&sm.flush_req = 1u;
-        return h;
-      }
-      if (old == key) return h;
+    const uint4 v = ld_shared_v4_volatile(&sm.key[4 * b]);
+    const int j = bucket_match(v, key);
+    if (j >= 0) return 4 * b + j;
+    uint32_t empt = (v.x == EMPTY32 ? 1u : 0u) | (v.y == EMPTY32 ? 2u : 0u) | (v.z == EMPTY32 ? 4u : 0u) |
+                    (v.w == EMPTY32 ? 8u : 0u);
+    if (empt && full) return OW_TAB;
+    while (empt) {
+      const uint32_t q = __ffs(empt) - 1;
+      empt &= empt - 1;
+      const uint32_t old = atomicCAS(&sm.key[4 * b + q], EMPTY32, key);
+      if (old == EMPTY32) return (4 * b + q) | 0x80000000u;
+      if (old == key) return 4 * b + q;
     }
-    h = h + 1 == (uint32_t)OW_TAB ? 0u : h + 1;
+    b = b + 1 == OW_NB ? 0u : b + 1;
   }
 }
 
@@ -219,17 +249,21 @@ __device__ __forceinline__ void own_add(OwnSmem& sm, const OwnArgs& a, uint32_t 
     }
     return;
   }
-  const uint32_t old = atomicAdd(&sm.cnt[h], add);
-  if (old + add < old) {  // 32-bit wrap: emit the 2^32 carry as its own one-entry segment
-    const unsigned long long base = atomicAdd(a.g_entries, 1ull);
-    const unsigned si = atomicAdd(a.g_segs, 1u);
-    if (si < a.cap_segs && base + 1 <= a.cap_entries) {
-      a.pkey[base] = key;
-      a.pcnt[base] = 1ull << 32;
-      a.seg[si] = make_uint4(ctx, 1u, (uint32_t)base, (uint32_t)(base >> 32));
-    } else {
-      atomicOr(a.g_flags, (uint32_t)OWF_OVERFLOW);
-    }
+  // Fire-and-forget shared reduction. Only samples with count == 1 reach the table (others
+  // go to the spill region), so a counter gains at most one per sample of the CTA's range
+  // between flushes and can never wrap: the range is < 2^32 samples.
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(smem_u32(&sm.cnt[h])), "r"(add) : "memory");
+}
+
+// a sample whose count is not 1 is kept exactly as its own partial entry (HBM), not in the table
+__device__ __forceinline__ void own_spill(OwnSmem& sm, const OwnArgs& a, uint32_t key, uint32_t count) {
+  const uint32_t i = atomicAdd(&sm.spill_n, 1u);
+  if (i < OW_SPILL_CAP) {
+    const uint64_t o = a.spill_base0 + (uint64_t)blockIdx.x * OW_SPILL_CAP + i;
+    a.pkey[o] = key;
+    a.pcnt[o] = count;
+  } else {
+    atomicOr(a.g_flags, (uint32_t)OWF_OVERFLOW);
   }
 }
 
@@ -254,18 +288,25 @@ __device__ __noinline__ uint32_t own_reject(uint32_t launch, uint32_t stall, uin
 }
 
 // sample -> key; EMPTY32 when not aggregated. Fused branch-free validity test on the hot path.
-__device__ __forceinline__ uint32_t own_key(const uint4 q, uint32_t seg_launch, const OwnArgs& a, bool ctx_ok, OwCounters& k) {
+// Hot path: a raw sample (count 1) of its segment's launch with a valid stall. Everything
+// else takes the slow path: invalid samples are classified and counted, samples with count > 1
+// (aggregated records) are kept exactly as partial entries in the spill region.
+__device__ __forceinline__ uint32_t own_key(const uint4 q, uint32_t seg_launch, const OwnArgs& a, bool ctx_ok, OwCounters& k,
+                                            OwnSmem& sm) {
   const uint32_t stall = q.z & 0xFFFFu;
+  const bool hot = (q.x == seg_launch) & (stall < a.S) & (q.w == 1u) & (q.y < (1u << 27) - 1u);
+  if (__builtin_expect(hot && ctx_ok, 1)) return (q.y << 5) | stall;  // seg_launch < n_launch
   const bool ok = (q.x == seg_launch) & (stall < a.S) & (q.w != 0) & (q.y < (1u << 27) - 1u) & ctx_ok & (q.x < a.n_launch);
-  if (__builtin_expect(!ok, 0)) {
-    const uint32_t r = own_reject(q.x, stall, q.w, seg_launch, a.n_launch, a.S, ctx_ok, a.trace_flags);
-    k.bad_l += r == 0;
-    k.bad_s += r == 1;
-    k.zero += r == 2;
-    k.fallback |= r == 3;
+  if (ok) {  // valid sample with count > 1
+    own_spill(sm, a, (q.y << 5) | stall, q.w);
     return EMPTY32;
   }
-  return (q.y << 5) | stall;  // != EMPTY32 since q.y < 2^27 and stall < 32 ... unless both max
+  const uint32_t r = own_reject(q.x, stall, q.w, seg_launch, a.n_launch, a.S, ctx_ok, a.trace_flags);
+  k.bad_l += r == 0;
+  k.bad_s += r == 1;
+  k.zero += r == 2;
+  k.fallback |= r == 3;
+  return EMPTY32;
 }
 
 __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
@@ -294,7 +335,8 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
   if (tid < 32) {
     // ------------------------------------------------ producer warp
     // The 32 lanes fetch the next 32 sorted launches' (start, end, source offset, ctx, id) in
-    // one batch of parallel loads; lane 0 then walks them, issuing one TMA bulk copy per chunk.
+    // one batch of parallel loads; lane 0 packs consecutive pieces of the same context into a
+    // stage (up to OW_SUBS launches per stage) and issues one TMA bulk copy per piece.
     const uint32_t lane = tid;
     uint64_t lo = 0, hi = a.n_launch;  // first sorted launch whose segment contains r0
     while (lo < hi) {
@@ -308,45 +350,72 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
     uint32_t st = 0, ph = 0, prev_ctx = OW_DONE;
     volatile uint32_t* freq = &sm.flush_req;
     while (pos < r1) {
-      if (batch == ~0ull || i >= batch + 32) {
-        batch = i;
-        const uint64_t b = batch + lane;
-        if (b < a.n_launch) {
-          my_beg = a.cum[b];
-          my_end = a.cum[b + 1];
-          my_l = a.order[b];
-          my_ctx = (uint32_t)a.lkey[b];
-          my_src = a.launch_off[my_l];
+      // ---- compose one stage: pieces of consecutive launches of one context
+      uint32_t fill = 0, nsub = 0, ctx0 = OW_DONE;
+      OwMeta m;
+      uint64_t src_of[OW_SUBS];
+      uint32_t len_of[OW_SUBS];
+      while (pos < r1 && fill < (uint32_t)OW_STAGE && nsub < (uint32_t)OW_SUBS) {
+        if (batch == ~0ull || i >= batch + 32) {
+          batch = i;
+          const uint64_t b = batch + lane;
+          if (b < a.n_launch) {
+            my_beg = a.cum[b];
+            my_end = a.cum[b + 1];
+            my_l = a.order[b];
+            my_ctx = (uint32_t)a.lkey[b];
+            my_src = a.launch_off[my_l];
+          }
         }
+        const uint32_t j = (uint32_t)(i - batch);
+        const uint64_t seg_beg = __shfl_sync(0xffffffffu, my_beg, j);
+        const uint64_t seg_end = __shfl_sync(0xffffffffu, my_end, j);
+        const uint32_t l = __shfl_sync(0xffffffffu, my_l, j);
+        const uint32_t ctx = __shfl_sync(0xffffffffu, my_ctx, j);
+        const uint64_t src0 = __shfl_sync(0xffffffffu, my_src, j);
+        if (seg_end <= pos) {
+          ++i;
+          continue;
+        }
+        if (nsub > 0 && ctx != ctx0) break;  // a stage never mixes contexts
+        uint64_t chunk = seg_end - pos;
+        if (r1 - pos < chunk) chunk = r1 - pos;
+        if (chunk > (uint64_t)(OW_STAGE - fill)) chunk = OW_STAGE - fill;
+        ctx0 = ctx;
+        src_of[nsub] = src0 + (pos - seg_beg);
+        len_of[nsub] = (uint32_t)chunk;
+        m.sub_launch[nsub] = l;
+        fill += (uint32_t)chunk;
+        m.sub_end[nsub] = fill;
+        ++nsub;
+        pos += chunk;
+        if (pos == seg_end) ++i;
       }
-      const uint32_t j = (uint32_t)(i - batch);
-      const uint64_t seg_beg = __shfl_sync(0xffffffffu, my_beg, j);
-      const uint64_t seg_end = __shfl_sync(0xffffffffu, my_end, j);
-      const uint32_t l = __shfl_sync(0xffffffffu, my_l, j);
-      const uint32_t ctx = __shfl_sync(0xffffffffu, my_ctx, j);
-      const uint64_t src0 = __shfl_sync(0xffffffffu, my_src, j);
-      if (seg_end <= pos) {
-        ++i;
-        continue;
+      for (uint32_t q = nsub; q < (uint32_t)OW_SUBS; ++q) {
+        m.sub_end[q] = 0xFFFFFFFFu;
+        m.sub_launch[q] = 0xFFFFFFFFu;
       }
-      uint64_t chunk = seg_end - pos;
-      if (r1 - pos < chunk) chunk = r1 - pos;
-      if (chunk > OW_STAGE) chunk = OW_STAGE;
       if (lane == 0) {
         mbar_wait(&sm.empty[st], ph ^ 1u);
-        uint32_t flush = ctx != prev_ctx ? 1u : 0u;
+        uint32_t flush = ctx0 != prev_ctx ? 1u : 0u;
         if (*freq) {
           *freq = 0u;
           flush = 1u;
         }
-        sm.meta[st] = OwMeta{l, ctx, (uint32_t)chunk, flush};
-        mbar_expect_tx(&sm.full[st], (uint32_t)chunk * 16u);
-        tma_bulk_g2s(&sm.stage[st][0], a.smp + src0 + (pos - seg_beg), (uint32_t)chunk * 16u, &sm.full[st]);
+        m.ctx = ctx0;
+        m.count = fill;
+        m.flush = flush;
+        m.nsub = nsub;
+        sm.meta[st] = m;
+        mbar_expect_tx(&sm.full[st], fill * 16u);
+        uint32_t off = 0;
+        for (uint32_t q = 0; q < nsub; ++q) {
+          tma_bulk_g2s(&sm.stage[st][off], a.smp + src_of[q], len_of[q] * 16u, &sm.full[st]);
+          off += len_of[q];
+        }
       }
       __syncwarp();
-      prev_ctx = ctx;
-      pos += chunk;
-      if (pos == seg_end) ++i;
+      prev_ctx = ctx0;
       if (++st == OW_STAGES) {
         st = 0;
         ph ^= 1u;
@@ -354,42 +423,113 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
     }
     if (lane == 0) {
       mbar_wait(&sm.empty[st], ph ^ 1u);
-      sm.meta[st] = OwMeta{0, OW_DONE, 0, 1};
+      OwMeta m;
+      m.ctx = OW_DONE;
+      m.count = 0;
+      m.flush = 1;
+      m.nsub = 0;
+      sm.meta[st] = m;
       mbar_arrive(&sm.full[st]);
     }
     return;
   }
-  // -------------------------------------------------- consumer warps (free-running)
-  const uint32_t ctid = tid - 32, lane = ctid & 31;
+  // -------------------------------------------------- consumer warps
+  // warp w takes samples [w*OW_ROUND, (w+1)*OW_ROUND) of every stage (OW_STAGE = 16 rounds),
+  // loads them into registers, releases the stage, then aggregates them
+  const uint32_t ctid = tid - 32, lane = ctid & 31, w = ctid >> 5;
   uint32_t cur_ctx = OW_DONE, st = 0, ph = 0;
   OwCounters k{0, 0, 0, 0};
+  uint32_t sinkv = 0;
   while (true) {
     mbar_wait(&sm.full[st], ph);
-    const OwMeta m = sm.meta[st];
-    if (m.flush) {  // uniform: every consumer sees the same meta
+    const uint32_t flush = sm.meta[st].flush, mctx = sm.meta[st].ctx, count = sm.meta[st].count, nsub = sm.meta[st].nsub;
+    if (flush) {  // uniform: every consumer sees the same meta
       cons_sync();  // every consumer finished all previous stages
-      if (sm.distinct > 0) own_flush(sm, a, cur_ctx, ctid);
+      // always entered by every consumer (its barriers are uniform); empty tables emit nothing.
+      own_flush(sm, a, cur_ctx, ctid);
     }
-    if (m.ctx == OW_DONE) break;
-    cur_ctx = m.ctx;
-    const bool ctx_ok = m.ctx < a.N;
-    // two samples per consumer thread (OW_STAGE = 2 * OW_CONS), processed side by side for ILP
-    const uint32_t j0 = ctid, j1 = ctid + OW_CONS;
-    const uint4 q0 = j0 < m.count ? sm.stage[st][j0] : make_uint4(0, 0, 0, 0);
-    const uint4 q1 = j1 < m.count ? sm.stage[st][j1] : make_uint4(0, 0, 0, 0);
+    if (mctx == OW_DONE) break;
+    cur_ctx = mctx;
+    const bool ctx_ok = mctx < a.N;
+    uint4 q[OW_PER_LANE];
+    uint32_t lch[OW_PER_LANE];
+#pragma unroll
+    for (int i = 0; i < OW_PER_LANE; ++i) {
+      const uint32_t j = w * OW_ROUND + 32 * i + lane;
+      q[i] = j < count ? sm.stage[st][j] : make_uint4(0, 0, 0, 0);
+      // the launch this stage position belongs to (sub-segments in stage order; nsub is
+      // warp-uniform and usually 1-2)
+      uint32_t l = sm.meta[st].sub_launch[0];
+      for (uint32_t s2 = 1; s2 < nsub; ++s2)
+        if (j >= sm.meta[st].sub_end[s2 - 1]) l = sm.meta[st].sub_launch[s2];
+      lch[i] = l;
+    }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.empty[st]);  // the stage is consumed into registers: release it early
-    const uint32_t key0 = j0 < m.count ? own_key(q0, m.launch, a, ctx_ok, k) : EMPTY32;
-    const uint32_t key1 = j1 < m.count ? own_key(q1, m.launch, a, ctx_ok, k) : EMPTY32;
-    uint32_t h0 = own_hash(key0), h1 = own_hash(key1);
-    const uint32_t s0 = sm.key[h0], s1 = sm.key[h1];  // home slots (hit after warm-up)
-    if (key0 != EMPTY32) {
-      if (s0 != key0) h0 = own_probe(sm, key0, h0);
-      own_add(sm, a, key0, h0, q0.w, m.ctx);
+    if (lane == 0) mbar_arrive(&sm.empty[st]);  // the stage is in registers: release it early
+    uint32_t t[OW_PER_LANE], b[OW_PER_LANE];
+#pragma unroll
+    for (int i = 0; i < OW_PER_LANE; ++i) {
+      const uint32_t j = w * OW_ROUND + 32 * i + lane;
+      t[i] = j < count ? own_key(q[i], lch[i], a, ctx_ok, k, sm) : EMPTY32;
     }
-    if (key1 != EMPTY32) {
-      if (s1 != key1) h1 = own_probe(sm, key1, h1);
-      own_add(sm, a, key1, h1, q1.w, m.ctx);
+    if (a.probe_mode == 1) {  // measurement: data movement + classification only
+#pragma unroll
+      for (int i = 0; i < OW_PER_LANE; ++i) sinkv ^= t[i] * (2 * i + 1);
+    } else {
+      uint32_t slot[OW_PER_LANE], inserted = 0;
+#pragma unroll
+      for (int i = 0; i < OW_PER_LANE; ++i) {
+        b[i] = own_bucket(t[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < OW_PER_LANE; ++i) {
+        const uint4 v = *reinterpret_cast<const uint4*>(&sm.key[4 * b[i]]);  // home bucket
+        const int jm = bucket_match(v, t[i]);
+        slot[i] = jm >= 0 ? 4 * b[i] + jm : OW_MISS;
+      }
+      // hits: add directly. Misses (new or displaced keys, ~3 % of samples) are compacted
+      // across the warp and probed together, so the slow path runs once per round with the
+      // missing keys spread over the lanes instead of once per sample slot with 1-2 lanes active.
+      uint32_t mm[OW_PER_LANE], cum[OW_PER_LANE + 1];
+      cum[0] = 0;
+#pragma unroll
+      for (int i = 0; i < OW_PER_LANE; ++i) {
+        const bool miss = t[i] != EMPTY32 && slot[i] == OW_MISS;
+        if (t[i] != EMPTY32 && !miss) own_add(sm, a, t[i], slot[i], 1u, mctx);
+        mm[i] = __ballot_sync(0xffffffffu, miss);
+        cum[i + 1] = cum[i] + __popc(mm[i]);
+      }
+      for (uint32_t base = 0; base < cum[OW_PER_LANE]; base += 32) {
+        const uint32_t d = base + lane;
+        const bool active = d < cum[OW_PER_LANE];
+        int ii = 0;
+        uint32_t mi = mm[0], ci = 0;
+#pragma unroll
+        for (int i = 1; i < OW_PER_LANE; ++i)
+          if (d >= cum[i]) {
+            ii = i;
+            mi = mm[i];
+            ci = cum[i];
+          }
+        const uint32_t src = active ? __fns(mi, 0, (int)(d - ci) + 1) : 0u;
+        uint32_t key = EMPTY32;
+#pragma unroll
+        for (int i = 0; i < OW_PER_LANE; ++i) {
+          const uint32_t ki = __shfl_sync(0xffffffffu, t[i], src);
+          if (i == ii) key = ki;
+        }
+        if (active) {
+          const uint32_t r = own_probe(sm, key, own_bucket(key));
+          inserted += r >> 31;
+          own_add(sm, a, key, r & 0x7FFFFFFFu, 1u, mctx);
+        }
+      }
+      // one `distinct` update per warp round (flush request when it crosses OW_FLUSH_REQ)
+      const uint32_t ins = __reduce_add_sync(0xffffffffu, inserted);
+      if (lane == 0 && ins) {
+        const uint32_t before = atomicAdd(&sm.distinct, ins);
+        if (before < OW_FLUSH_REQ && before + ins >= OW_FLUSH_REQ) *(volatile uint32_t*)&sm.flush_req = 1u;
+      }
     }
     if (++st == OW_STAGES) {
       st = 0;
@@ -409,6 +549,7 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
     if (bad_s) atomicAdd(a.ldiag + DG_BAD_STALL, (unsigned long long)bad_s);
     if (zero) atomicAdd(a.ldiag + DG_ZERO, (unsigned long long)zero);
     if (fallback) atomicOr(a.g_flags, (uint32_t)OWF_FALLBACK);
+    if (a.probe_mode && sinkv == 0x12345678u) a.sink[0] = sinkv;
   }
 }
 
@@ -851,6 +992,9 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
     a.trace_flags = c->d_flags;
     a.ldiag = ldiag.p;
     a.spill_base0 = cap_entries;
+    a.probe_mode = 0;
+    a.sink = flags.p;
+    if (const char* pm = getenv("DC_OWN_MODE")) a.probe_mode = (uint32_t)atoi(pm);  // measurement only
     const size_t smem = sizeof(OwnSmem);
     static bool attr_set = false;
     if (!attr_set) {
@@ -890,6 +1034,18 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
   DC_TRY(excl_scan<uint32_t>(c, head.p, hex.p, n_segs, ng.p));
   uint32_t n_groups = 0;
   DC_TRY(readback(c, ng.p, 4, &n_groups));
+  if (n_groups == 0) {  // no valid sample: no PC nodes, no bins
+    t->Npc = t->Nbins = 0;
+    DC_TRY(palloc(c, t->pc_ctx, 1));
+    DC_TRY(palloc(c, t->pc_off, 1));
+    DC_TRY(palloc(c, t->bin_pcnode, 1));
+    DC_TRY(palloc(c, t->bin_stall, 1));
+    DC_TRY(palloc(c, t->bin_count, 1));
+    DC_TRY(add_diag(c, ldiag.p));
+    *n_bins_out = 0;
+    *handled = 1;
+    return DC_OK;
+  }
   DC_TRY(alloc(c, grp_start, n_groups + 1));
   k_own_gstart<<<grid_for(c, n_segs, 256), 256, 0, c->stream>>>(head.p, hex.p, n_segs, grp_start.p, n_groups);
   DC_LAUNCHED(c);
