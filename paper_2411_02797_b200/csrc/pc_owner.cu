@@ -32,7 +32,7 @@ constexpr int OW_STAGES = 4;
 constexpr int OW_PER_LANE = 4;                // samples per lane per stage
 constexpr int OW_ROUND = 32 * OW_PER_LANE;    // samples per warp per stage
 constexpr int OW_STAGE = OW_CONS_WARPS * OW_ROUND;  // 2048 samples per stage (32 KB)
-constexpr int OW_SUBS = 8;                    // launches packed into one stage at most
+constexpr int OW_MAXP = 16;                   // launch pieces packed into one stage at most
 constexpr int OW_TAB = 12288;                 // shared hash table slots (96 KB)
 // a flush is requested at 2/3 load; past OW_SPILL_AT distinct keys new keys are not inserted
 // but appended to the CTA's spill region in HBM (kept as partial entries), so the table can
@@ -46,10 +46,11 @@ constexpr uint32_t OW_DONE = 0xFFFFFFFFu;
 
 enum { OWF_FALLBACK = 1, OWF_OVERFLOW = 2 };
 
+constexpr int OW_ROWS = OW_STAGE / 32;        // 32-sample rows per stage
 struct OwMeta {
-  uint32_t ctx, count, flush, nsub;
-  uint32_t sub_end[OW_SUBS];     // exclusive end (stage position) of each launch piece
-  uint32_t sub_launch[OW_SUBS];  // launch of each piece
+  uint32_t ctx, count, flush, pad;
+  uint32_t row_launch[OW_ROWS];  // launch of each 32-sample row (pieces start on row boundaries)
+  uint8_t row_valid[OW_ROWS];    // valid samples in the row (a launch's tail row is partial)
 };
 
 struct OwnSmem {
@@ -336,7 +337,7 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
     // ------------------------------------------------ producer warp
     // The 32 lanes fetch the next 32 sorted launches' (start, end, source offset, ctx, id) in
     // one batch of parallel loads; lane 0 packs consecutive pieces of the same context into a
-    // stage (up to OW_SUBS launches per stage) and issues one TMA bulk copy per piece.
+    // stage (up to OW_MAXP pieces per stage, each on a 32-sample row boundary) and issues one TMA bulk copy per piece.
     const uint32_t lane = tid;
     uint64_t lo = 0, hi = a.n_launch;  // first sorted launch whose segment contains r0
     while (lo < hi) {
@@ -350,12 +351,16 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
     uint32_t st = 0, ph = 0, prev_ctx = OW_DONE;
     volatile uint32_t* freq = &sm.flush_req;
     while (pos < r1) {
-      // ---- compose one stage: pieces of consecutive launches of one context
-      uint32_t fill = 0, nsub = 0, ctx0 = OW_DONE;
-      OwMeta m;
-      uint64_t src_of[OW_SUBS];
-      uint32_t len_of[OW_SUBS];
-      while (pos < r1 && fill < (uint32_t)OW_STAGE && nsub < (uint32_t)OW_SUBS) {
+      // ---- compose one stage from pieces of consecutive launches of one context. Every piece
+      // starts on a 32-sample row boundary, so each row belongs to one launch (the row's last
+      // samples may be unused): consumers look the launch up per row, not per sample.
+      uint32_t fill = 0, ctx0 = OW_DONE, npieces = 0;
+      if (lane == 0) mbar_wait(&sm.empty[st], ph ^ 1u);  // the slot (and its meta) is free
+      __syncwarp();
+      OwMeta* mp = &sm.meta[st];
+      uint64_t src_of[OW_MAXP];
+      uint32_t len_of[OW_MAXP], at_of[OW_MAXP];
+      while (pos < r1 && fill < (uint32_t)OW_STAGE && npieces < (uint32_t)OW_MAXP) {
         if (batch == ~0ull || i >= batch + 32) {
           batch = i;
           const uint64_t b = batch + lane;
@@ -377,42 +382,42 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
           ++i;
           continue;
         }
-        if (nsub > 0 && ctx != ctx0) break;  // a stage never mixes contexts
+        if (npieces > 0 && ctx != ctx0) break;  // a stage never mixes contexts
         uint64_t chunk = seg_end - pos;
         if (r1 - pos < chunk) chunk = r1 - pos;
         if (chunk > (uint64_t)(OW_STAGE - fill)) chunk = OW_STAGE - fill;
         ctx0 = ctx;
-        src_of[nsub] = src0 + (pos - seg_beg);
-        len_of[nsub] = (uint32_t)chunk;
-        m.sub_launch[nsub] = l;
-        fill += (uint32_t)chunk;
-        m.sub_end[nsub] = fill;
-        ++nsub;
+        // rows [fill/32, ceil((fill+chunk)/32)) belong to launch l (lanes write them)
+        const uint32_t r_lo = fill >> 5, r_hi = (fill + (uint32_t)chunk + 31) >> 5;
+        for (uint32_t r = r_lo + lane; r < r_hi; r += 32) {
+          mp->row_launch[r] = l;
+          const uint32_t end = fill + (uint32_t)chunk;
+          mp->row_valid[r] = (uint8_t)min(32u, end - 32 * r);
+        }
+        src_of[npieces] = src0 + (pos - seg_beg);
+        len_of[npieces] = (uint32_t)chunk;
+        at_of[npieces] = fill;
+        ++npieces;
+        fill = (fill + (uint32_t)chunk + 31) & ~31u;  // next piece starts on a row boundary
         pos += chunk;
         if (pos == seg_end) ++i;
       }
-      for (uint32_t q = nsub; q < (uint32_t)OW_SUBS; ++q) {
-        m.sub_end[q] = 0xFFFFFFFFu;
-        m.sub_launch[q] = 0xFFFFFFFFu;
-      }
+      for (uint32_t r = (fill >> 5) + lane; r < (uint32_t)OW_ROWS; r += 32) mp->row_valid[r] = 0;
+      __syncwarp();
       if (lane == 0) {
-        mbar_wait(&sm.empty[st], ph ^ 1u);
         uint32_t flush = ctx0 != prev_ctx ? 1u : 0u;
         if (*freq) {
           *freq = 0u;
           flush = 1u;
         }
-        m.ctx = ctx0;
-        m.count = fill;
-        m.flush = flush;
-        m.nsub = nsub;
-        sm.meta[st] = m;
-        mbar_expect_tx(&sm.full[st], fill * 16u);
-        uint32_t off = 0;
-        for (uint32_t q = 0; q < nsub; ++q) {
-          tma_bulk_g2s(&sm.stage[st][off], a.smp + src_of[q], len_of[q] * 16u, &sm.full[st]);
-          off += len_of[q];
-        }
+        mp->ctx = ctx0;
+        mp->count = fill;
+        mp->flush = flush;
+        uint32_t bytes = 0;
+        for (uint32_t q = 0; q < npieces; ++q) bytes += len_of[q] * 16u;
+        mbar_expect_tx(&sm.full[st], bytes);  // release: orders the meta writes above
+        for (uint32_t q = 0; q < npieces; ++q)
+          tma_bulk_g2s(&sm.stage[st][at_of[q]], a.smp + src_of[q], len_of[q] * 16u, &sm.full[st]);
       }
       __syncwarp();
       prev_ctx = ctx0;
@@ -423,12 +428,9 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
     }
     if (lane == 0) {
       mbar_wait(&sm.empty[st], ph ^ 1u);
-      OwMeta m;
-      m.ctx = OW_DONE;
-      m.count = 0;
-      m.flush = 1;
-      m.nsub = 0;
-      sm.meta[st] = m;
+      sm.meta[st].ctx = OW_DONE;
+      sm.meta[st].count = 0;
+      sm.meta[st].flush = 1;
       mbar_arrive(&sm.full[st]);
     }
     return;
@@ -440,38 +442,43 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
   uint32_t cur_ctx = OW_DONE, st = 0, ph = 0;
   OwCounters k{0, 0, 0, 0};
   uint32_t sinkv = 0;
+  long long t_wait = 0, t_flush = 0, t_work = 0, n_stage = 0, t_key = 0, t_bucket = 0, t_add = 0;  // probe_mode 9 only
   while (true) {
+    const long long c_0 = a.probe_mode == 9 ? clock64() : 0;
     mbar_wait(&sm.full[st], ph);
-    const uint32_t flush = sm.meta[st].flush, mctx = sm.meta[st].ctx, count = sm.meta[st].count, nsub = sm.meta[st].nsub;
+    const long long c_1 = a.probe_mode == 9 ? clock64() : 0;
+    const uint32_t flush = sm.meta[st].flush, mctx = sm.meta[st].ctx;
     if (flush) {  // uniform: every consumer sees the same meta
       cons_sync();  // every consumer finished all previous stages
       // always entered by every consumer (its barriers are uniform); empty tables emit nothing.
       own_flush(sm, a, cur_ctx, ctid);
+    }
+    if (a.probe_mode == 9) {
+      t_wait += c_1 - c_0;
+      t_flush += clock64() - c_1;
     }
     if (mctx == OW_DONE) break;
     cur_ctx = mctx;
     const bool ctx_ok = mctx < a.N;
     uint4 q[OW_PER_LANE];
     uint32_t lch[OW_PER_LANE];
+    bool vld[OW_PER_LANE];
 #pragma unroll
     for (int i = 0; i < OW_PER_LANE; ++i) {
-      const uint32_t j = w * OW_ROUND + 32 * i + lane;
-      q[i] = j < count ? sm.stage[st][j] : make_uint4(0, 0, 0, 0);
-      // the launch this stage position belongs to (sub-segments in stage order; nsub is
-      // warp-uniform and usually 1-2)
-      uint32_t l = sm.meta[st].sub_launch[0];
-      for (uint32_t s2 = 1; s2 < nsub; ++s2)
-        if (j >= sm.meta[st].sub_end[s2 - 1]) l = sm.meta[st].sub_launch[s2];
-      lch[i] = l;
+      const uint32_t row = w * OW_PER_LANE + i;  // warp w owns rows [4w, 4w+4) of the stage
+      lch[i] = sm.meta[st].row_launch[row];      // row-uniform: one broadcast load
+      vld[i] = lane < sm.meta[st].row_valid[row];
+      q[i] = vld[i] ? sm.stage[st][32 * row + lane] : make_uint4(0, 0, 0, 0);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[st]);  // the stage is in registers: release it early
     uint32_t t[OW_PER_LANE], b[OW_PER_LANE];
 #pragma unroll
     for (int i = 0; i < OW_PER_LANE; ++i) {
-      const uint32_t j = w * OW_ROUND + 32 * i + lane;
-      t[i] = j < count ? own_key(q[i], lch[i], a, ctx_ok, k, sm) : EMPTY32;
+      t[i] = vld[i] ? own_key(q[i], lch[i], a, ctx_ok, k, sm) : EMPTY32;
     }
+    const long long c_2 = a.probe_mode == 9 ? clock64() : 0;
+    if (a.probe_mode == 9) t_key += c_2 - c_1;
     if (a.probe_mode == 1) {  // measurement: data movement + classification only
 #pragma unroll
       for (int i = 0; i < OW_PER_LANE; ++i) sinkv ^= t[i] * (2 * i + 1);
@@ -487,6 +494,8 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
         const int jm = bucket_match(v, t[i]);
         slot[i] = jm >= 0 ? 4 * b[i] + jm : OW_MISS;
       }
+      const long long c_3 = a.probe_mode == 9 ? clock64() : 0;
+      if (a.probe_mode == 9) t_bucket += c_3 - c_2;
       // hits: add directly. Misses (new or displaced keys, ~3 % of samples) are compacted
       // across the warp and probed together, so the slow path runs once per round with the
       // missing keys spread over the lanes instead of once per sample slot with 1-2 lanes active.
@@ -524,6 +533,7 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
           own_add(sm, a, key, r & 0x7FFFFFFFu, 1u, mctx);
         }
       }
+      if (a.probe_mode == 9) t_add += clock64() - c_3;
       // one `distinct` update per warp round (flush request when it crosses OW_FLUSH_REQ)
       const uint32_t ins = __reduce_add_sync(0xffffffffu, inserted);
       if (lane == 0 && ins) {
@@ -531,10 +541,24 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
         if (before < OW_FLUSH_REQ && before + ins >= OW_FLUSH_REQ) *(volatile uint32_t*)&sm.flush_req = 1u;
       }
     }
+    if (a.probe_mode == 9) {
+      t_work += clock64() - c_1;
+      ++n_stage;
+    }
     if (++st == OW_STAGES) {
       st = 0;
       ph ^= 1u;
     }
+  }
+  if (a.probe_mode == 9 && lane == 0) {  // measurement: per-warp cycle split (wait / flush / work)
+    unsigned long long* dbg = reinterpret_cast<unsigned long long*>(a.sink) + 8 * (blockIdx.x * OW_CONS_WARPS + w);
+    dbg[0] = t_wait;
+    dbg[1] = t_flush;
+    dbg[2] = t_work - t_flush;
+    dbg[3] = n_stage;
+    dbg[4] = t_key;
+    dbg[5] = t_bucket;
+    dbg[6] = t_add;
   }
   uint32_t bad_l = k.bad_l, bad_s = k.bad_s, zero = k.zero, fallback = k.fallback;
 #pragma unroll
@@ -995,6 +1019,11 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
     a.probe_mode = 0;
     a.sink = flags.p;
     if (const char* pm = getenv("DC_OWN_MODE")) a.probe_mode = (uint32_t)atoi(pm);  // measurement only
+    Buf<unsigned long long> dbg;
+    if (a.probe_mode == 9) {
+      DC_TRY(alloc_zero(c, dbg, (uint64_t)G * OW_CONS_WARPS * 8));
+      a.sink = reinterpret_cast<uint32_t*>(dbg.p);
+    }
     const size_t smem = sizeof(OwnSmem);
     static bool attr_set = false;
     if (!attr_set) {
@@ -1005,6 +1034,17 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
       Region rk(c, "k:pc_owner");
       k_pc_owner<<<G, OW_THREADS, smem, c->stream>>>(a);
       DC_LAUNCHED(c);
+    }
+    if (a.probe_mode == 9) {  // measurement only: print the consumer cycle split
+      std::vector<unsigned long long> h((size_t)G * OW_CONS_WARPS * 8);
+      DC_TRY(readback(c, dbg.p, h.size() * 8, h.data()));
+      double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (size_t i = 0; i < h.size(); ++i) s[i % 8] += (double)h[i];
+      const double nw = (double)G * OW_CONS_WARPS;
+      fprintf(stderr,
+              "{\"own_split\": {\"wait_cyc\": %.0f, \"flush_cyc\": %.0f, \"work_cyc\": %.0f, \"stages\": %.1f, "
+              "\"key_cyc\": %.0f, \"bucket_cyc\": %.0f, \"add_cyc\": %.0f}}\n",
+              s[0] / nw, s[1] / nw, s[2] / nw, s[3] / nw, s[4] / nw, s[5] / nw, s[6] / nw);
     }
     DC_TRY(readback(c, ctr.p, 16, hc));
     DC_TRY(readback(c, flags.p, 8, hf));
