@@ -32,7 +32,6 @@ constexpr int OW_STAGES = 4;
 constexpr int OW_PER_LANE = 4;                // samples per lane per stage
 constexpr int OW_ROUND = 32 * OW_PER_LANE;    // samples per warp per stage
 constexpr int OW_STAGE = OW_CONS_WARPS * OW_ROUND;  // 2048 samples per stage (32 KB)
-constexpr int OW_MAXP = 16;                   // launch pieces packed into one stage at most
 constexpr int OW_TAB = 12288;                 // shared hash table slots (96 KB)
 // a flush is requested at 2/3 load; past OW_SPILL_AT distinct keys new keys are not inserted
 // but appended to the CTA's spill region in HBM (kept as partial entries), so the table can
@@ -47,7 +46,7 @@ constexpr uint32_t OW_DONE = 0xFFFFFFFFu;
 enum { OWF_FALLBACK = 1, OWF_OVERFLOW = 2 };
 
 constexpr int OW_ROWS = OW_STAGE / 32;        // 32-sample rows per stage
-struct OwMeta {
+struct __align__(16) OwMeta {
   uint32_t ctx, count, flush, pad;
   uint32_t row_launch[OW_ROWS];  // launch of each 32-sample row (pieces start on row boundaries)
   uint8_t row_valid[OW_ROWS];    // valid samples in the row (a launch's tail row is partial)
@@ -113,22 +112,89 @@ __global__ void k_own_keys(const uint32_t* __restrict__ leaf, uint64_t n_launch,
   }
 }
 
-__global__ void k_own_cnt(const uint64_t* __restrict__ off, const uint32_t* __restrict__ order, uint64_t n_launch,
-                          uint64_t* __restrict__ cnt) {
+// ---- stage plan. The ctx-ordered launches are laid out as a stream of 32-sample rows: launch i
+// takes rows_i = ceil(cnt_i / 32) rows (its last row partial), the launches of one context are
+// contiguous and every context starts on a stage boundary (64 rows), so a stage holds one
+// context and every row one launch. Per row the plan stores the launch id and the number of
+// valid samples (0 for padding); per stage, its first launch and context.
+__global__ void k_plan_launch(const uint64_t* __restrict__ off, const uint32_t* __restrict__ order,
+                              const uint64_t* __restrict__ lkey, uint64_t n_launch, uint64_t* __restrict__ lrow,
+                              uint32_t* __restrict__ lflag, uint64_t* __restrict__ lsrc, uint64_t* __restrict__ lcnt) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n_launch; i += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t l = order[i];
-    cnt[i] = off[l + 1] - off[l];
+    const uint32_t l = order[i];
+    const uint64_t b = off[l], e = off[l + 1];
+    const uint64_t c = e > b ? e - b : 0;  // inconsistent offsets are rejected before the main kernel
+    lrow[i] = (c + 31) / 32;
+    lflag[i] = (i == 0 || lkey[i] != lkey[i - 1]) ? 1u : 0u;
+    lsrc[i] = b;
+    lcnt[i] = c;
+  }
+}
+
+// gfirst[g] = first sorted launch of context group g; gfirst[NG] = n_launch
+__global__ void k_plan_gfirst(const uint64_t* __restrict__ lkey, const uint32_t* __restrict__ gx, const uint32_t* ng,
+                              uint64_t n_launch, uint32_t* __restrict__ gfirst) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n_launch; i += (uint64_t)gridDim.x * blockDim.x) {
+    if (i == 0 || lkey[i] != lkey[i - 1]) gfirst[gx[i]] = (uint32_t)i;
+    if (i == n_launch - 1) gfirst[*ng] = (uint32_t)n_launch;
+  }
+}
+
+// stages per group (0 past the last group, so the scan can run over the n_launch bound)
+__global__ void k_plan_gstages(const uint64_t* __restrict__ E, const uint32_t* __restrict__ gfirst, const uint32_t* ng,
+                               uint64_t n_launch, uint64_t* __restrict__ gst) {
+  const uint32_t NG = *ng;
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < n_launch; g += (uint64_t)gridDim.x * blockDim.x)
+    gst[g] = g < NG ? (E[gfirst[g + 1]] - E[gfirst[g]] + 63) / 64 : 0;
+}
+
+// one warp per launch: row position, row meta, stage starts
+__global__ void k_plan_rows(const uint64_t* __restrict__ E, const uint32_t* __restrict__ gx,
+                            const uint32_t* __restrict__ gfirst, const uint64_t* __restrict__ SB,
+                            const uint64_t* __restrict__ lkey, const uint32_t* __restrict__ order,
+                            const uint64_t* __restrict__ lcnt, uint64_t n_launch, uint64_t row_cap,
+                            uint64_t* __restrict__ rowpos, uint32_t* __restrict__ row_launch, uint8_t* __restrict__ row_valid,
+                            uint32_t* __restrict__ st_first, uint32_t* __restrict__ st_ctx) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5, nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t i = wid; i < n_launch; i += nw) {
+    const uint32_t flag = (i == 0 || lkey[i] != lkey[i - 1]) ? 1u : 0u;
+    const uint32_t g = gx[i] + flag - 1;
+    const uint64_t rp = 64 * SB[g] + E[i] - E[gfirst[g]];
+    const uint64_t rows = E[i + 1] - E[i], c = lcnt[i];
+    const uint32_t l = order[i], ctx = (uint32_t)lkey[i];
+    if (lane == 0) rowpos[i] = rp;
+    for (uint64_t k = lane; k < rows; k += 32) {
+      const uint64_t R = rp + k;
+      if (R < row_cap) {
+        row_launch[R] = l;
+        row_valid[R] = (uint8_t)(c - 32 * k < 32 ? c - 32 * k : 32);
+      }
+    }
+    if (rows > 0) {  // stages whose first row lies in this launch
+      const uint64_t s_lo = (rp + 63) / 64, s_hi = (rp + rows - 1) / 64;
+      for (uint64_t st = s_lo + lane; st <= s_hi; st += 32)
+        if (64 * st < row_cap) {
+          st_first[st] = (uint32_t)i;
+          st_ctx[st] = ctx;
+        }
+    }
   }
 }
 
 // ---------------------------------------------------------------- main kernel
 struct OwnArgs {
   const dc_pc_sample* smp;
-  const uint64_t* launch_off;  // [n_launch+1]
-  const uint32_t* order;       // launches sorted by ctx
-  const uint64_t* lkey;        // sorted ctx key per sorted launch (N = invalid)
-  const uint64_t* cum;         // [n_launch+1] exclusive scan of sorted launch sample counts
-  uint64_t n_launch, N, total;
+  // stage plan (k_plan_*), per ctx-sorted launch i: first row, first sample, sample count
+  const uint64_t* rowpos;
+  const uint64_t* lsrc;
+  const uint64_t* lcnt;
+  const uint32_t* st_first;    // per stage: first launch, context
+  const uint32_t* st_ctx;
+  const uint32_t* row_launch;  // per row: launch id, valid samples
+  const uint8_t* row_valid;
+  const uint64_t* st_total;    // number of stages (device)
+  uint64_t n_launch, N;
   uint32_t S;
   uint32_t* pkey;              // partial entries: key
   unsigned long long* pcnt;    //                  count
@@ -214,6 +280,15 @@ __device__ __forceinline__ uint4 ld_shared_v4_volatile(const uint32_t* p) {
   return v;
 }
 
+// branch-free home-bucket lookup: keys are unique in the table, so at most one compare holds
+__device__ __forceinline__ uint32_t bucket_slot(const uint4 v, uint32_t key, uint32_t b) {
+  const uint32_t j = (v.y == key ? 1u : 0u) | (v.z == key ? 2u : 0u) | (v.w == key ? 3u : 0u);
+  return (v.x == key) | (j != 0u) ? 4 * b + j : (uint32_t)OW_MISS;
+}
+__device__ __forceinline__ void red_shared_inc(uint32_t* p) {
+  asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(smem_u32(p)) : "memory");
+}
+
 // slow path: the key is not in its home bucket (new key, or displaced). Returns the slot, or
 // OW_TAB when the table is near full (the sample then goes to the spill region).
 // returns slot | (1 << 31 if this call inserted the key)
@@ -288,35 +363,34 @@ __device__ __noinline__ uint32_t own_reject(uint32_t launch, uint32_t stall, uin
   return 3;  // pc_off >= 2^27 - 1 (key would not fit 32 bits)
 }
 
-// sample -> key; EMPTY32 when not aggregated. Fused branch-free validity test on the hot path.
-// Hot path: a raw sample (count 1) of its segment's launch with a valid stall. Everything
-// else takes the slow path: invalid samples are classified and counted, samples with count > 1
-// (aggregated records) are kept exactly as partial entries in the spill region.
-__device__ __forceinline__ uint32_t own_key(const uint4 q, uint32_t seg_launch, const OwnArgs& a, bool ctx_ok, OwCounters& k,
-                                            OwnSmem& sm) {
+// Hot path: a raw sample (count 1) of its row's launch with a valid stall -> key (pc_off << 5 |
+// stall). Everything else takes own_cold: invalid samples are classified and counted, samples
+// with count > 1 (aggregated records) are kept exactly as partial entries in the spill region.
+__device__ __forceinline__ bool own_hot(const uint4 q, uint32_t row_launch, uint32_t S) {
+  return (q.x == row_launch) & ((q.z & 0xFFFFu) < S) & (q.w == 1u) & (q.y < (1u << 27) - 1u);
+}
+__device__ __noinline__ void own_cold(const uint4 q, uint32_t seg_launch, const OwnArgs& a, bool ctx_ok, OwCounters& k,
+                                      OwnSmem& sm) {
   const uint32_t stall = q.z & 0xFFFFu;
-  const bool hot = (q.x == seg_launch) & (stall < a.S) & (q.w == 1u) & (q.y < (1u << 27) - 1u);
-  if (__builtin_expect(hot && ctx_ok, 1)) return (q.y << 5) | stall;  // seg_launch < n_launch
   const bool ok = (q.x == seg_launch) & (stall < a.S) & (q.w != 0) & (q.y < (1u << 27) - 1u) & ctx_ok & (q.x < a.n_launch);
   if (ok) {  // valid sample with count > 1
     own_spill(sm, a, (q.y << 5) | stall, q.w);
-    return EMPTY32;
+    return;
   }
   const uint32_t r = own_reject(q.x, stall, q.w, seg_launch, a.n_launch, a.S, ctx_ok, a.trace_flags);
   k.bad_l += r == 0;
   k.bad_s += r == 1;
   k.zero += r == 2;
   k.fallback |= r == 3;
-  return EMPTY32;
 }
 
 __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   OwnSmem& sm = *reinterpret_cast<OwnSmem*>(smem_raw);
   const uint32_t tid = threadIdx.x;
-  // range of this CTA in the ctx-ordered virtual stream
-  const uint64_t G = gridDim.x;
-  const uint64_t r0 = a.total * blockIdx.x / G, r1 = a.total * (blockIdx.x + 1) / G;
+  // range of this CTA: stages [s0, s1) of the plan
+  const uint64_t G = gridDim.x, ST = *a.st_total;
+  const uint64_t s0 = ST * blockIdx.x / G, s1 = ST * (blockIdx.x + 1) / G;
   for (uint32_t s = tid; s < OW_TAB; s += OW_THREADS) {
     sm.key[s] = EMPTY32;
     sm.cnt[s] = 0;
@@ -335,92 +409,115 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
   __syncthreads();
   if (tid < 32) {
     // ------------------------------------------------ producer warp
-    // The 32 lanes fetch the next 32 sorted launches' (start, end, source offset, ctx, id) in
-    // one batch of parallel loads; lane 0 packs consecutive pieces of the same context into a
-    // stage (up to OW_MAXP pieces per stage, each on a 32-sample row boundary) and issues one TMA bulk copy per piece.
+    // Per stage s the plan gives the first launch f; lane j cuts launch f + j to the stage's rows
+    // [64 s, 64 s + 64) and issues its own TMA bulk copy, lane 0 copies the stage's row meta.
+    // The launch fields of stage s + 1 are loaded while stage s is issued (and the per-stage
+    // first-launch / context words 32 stages at a time, one batch ahead).
     const uint32_t lane = tid;
-    uint64_t lo = 0, hi = a.n_launch;  // first sorted launch whose segment contains r0
-    while (lo < hi) {
-      const uint64_t mid = (lo + hi + 1) >> 1;
-      if (a.cum[mid] <= r0) lo = mid;
-      else hi = mid - 1;
-    }
-    uint64_t i = lo, pos = r0, batch = ~0ull;
-    uint64_t my_beg = 0, my_end = 0, my_src = 0;
-    uint32_t my_l = 0, my_ctx = 0;
     uint32_t st = 0, ph = 0, prev_ctx = OW_DONE;
     volatile uint32_t* freq = &sm.flush_req;
-    while (pos < r1) {
-      // ---- compose one stage from pieces of consecutive launches of one context. Every piece
-      // starts on a 32-sample row boundary, so each row belongs to one launch (the row's last
-      // samples may be unused): consumers look the launch up per row, not per sample.
-      uint32_t fill = 0, ctx0 = OW_DONE, npieces = 0;
+    const bool prof = a.probe_mode == 2 || a.probe_mode == 9;  // measurement only
+    long long p_wait = 0, p_comp = 0, p_stages = 0, p_pieces = 0;
+    const long long p_t0 = prof ? clock64() : 0;
+    // stage batches: cb = stages [bs, bs + 32), nb = [bs + 32, bs + 64)
+    uint64_t bs = s0;
+    uint32_t cb_first = 0, cb_ctx = 0, nb_first = 0, nb_ctx = 0;
+    if (s0 + lane < s1) {
+      cb_first = a.st_first[s0 + lane];
+      cb_ctx = a.st_ctx[s0 + lane];
+    }
+    if (s0 + 32 + lane < s1) {
+      nb_first = a.st_first[s0 + 32 + lane];
+      nb_ctx = a.st_ctx[s0 + 32 + lane];
+    }
+    // launch fields of the next stage to issue
+    uint64_t x_rp = ~0ull, x_src = 0, x_cnt = 0;
+    auto load_launch = [&](uint64_t s) {
+      const uint32_t f = __shfl_sync(0xffffffffu, s - bs < 32 ? cb_first : nb_first, (uint32_t)(s - bs) & 31);
+      const uint64_t li = (uint64_t)f + lane;
+      x_rp = ~0ull;
+      if (li < a.n_launch) {
+        x_rp = a.rowpos[li];
+        x_src = a.lsrc[li];
+        x_cnt = a.lcnt[li];
+      }
+    };
+    if (s0 < s1) load_launch(s0);
+    for (uint64_t s = s0; s < s1; ++s) {
+      const long long pc0 = prof ? clock64() : 0;
+      const uint32_t ctx = __shfl_sync(0xffffffffu, s - bs < 32 ? cb_ctx : nb_ctx, (uint32_t)(s - bs) & 31);
+      const uint32_t f = __shfl_sync(0xffffffffu, s - bs < 32 ? cb_first : nb_first, (uint32_t)(s - bs) & 31);
+      uint64_t rp = x_rp, src = x_src, cnt = x_cnt;
+      if (s + 1 - bs == 32) {  // advance the stage batches (the next one is loaded ahead)
+        bs += 32;
+        cb_first = nb_first;
+        cb_ctx = nb_ctx;
+        if (bs + 32 + lane < s1) {
+          nb_first = a.st_first[bs + 32 + lane];
+          nb_ctx = a.st_ctx[bs + 32 + lane];
+        }
+      }
+      if (s + 1 < s1) load_launch(s + 1);
       if (lane == 0) mbar_wait(&sm.empty[st], ph ^ 1u);  // the slot (and its meta) is free
       __syncwarp();
-      OwMeta* mp = &sm.meta[st];
-      uint64_t src_of[OW_MAXP];
-      uint32_t len_of[OW_MAXP], at_of[OW_MAXP];
-      while (pos < r1 && fill < (uint32_t)OW_STAGE && npieces < (uint32_t)OW_MAXP) {
-        if (batch == ~0ull || i >= batch + 32) {
-          batch = i;
-          const uint64_t b = batch + lane;
-          if (b < a.n_launch) {
-            my_beg = a.cum[b];
-            my_end = a.cum[b + 1];
-            my_l = a.order[b];
-            my_ctx = (uint32_t)a.lkey[b];
-            my_src = a.launch_off[my_l];
-          }
-        }
-        const uint32_t j = (uint32_t)(i - batch);
-        const uint64_t seg_beg = __shfl_sync(0xffffffffu, my_beg, j);
-        const uint64_t seg_end = __shfl_sync(0xffffffffu, my_end, j);
-        const uint32_t l = __shfl_sync(0xffffffffu, my_l, j);
-        const uint32_t ctx = __shfl_sync(0xffffffffu, my_ctx, j);
-        const uint64_t src0 = __shfl_sync(0xffffffffu, my_src, j);
-        if (seg_end <= pos) {
-          ++i;
-          continue;
-        }
-        if (npieces > 0 && ctx != ctx0) break;  // a stage never mixes contexts
-        uint64_t chunk = seg_end - pos;
-        if (r1 - pos < chunk) chunk = r1 - pos;
-        if (chunk > (uint64_t)(OW_STAGE - fill)) chunk = OW_STAGE - fill;
-        ctx0 = ctx;
-        // rows [fill/32, ceil((fill+chunk)/32)) belong to launch l (lanes write them)
-        const uint32_t r_lo = fill >> 5, r_hi = (fill + (uint32_t)chunk + 31) >> 5;
-        for (uint32_t r = r_lo + lane; r < r_hi; r += 32) {
-          mp->row_launch[r] = l;
-          const uint32_t end = fill + (uint32_t)chunk;
-          mp->row_valid[r] = (uint8_t)min(32u, end - 32 * r);
-        }
-        src_of[npieces] = src0 + (pos - seg_beg);
-        len_of[npieces] = (uint32_t)chunk;
-        at_of[npieces] = fill;
-        ++npieces;
-        fill = (fill + (uint32_t)chunk + 31) & ~31u;  // next piece starts on a row boundary
-        pos += chunk;
-        if (pos == seg_end) ++i;
-      }
-      for (uint32_t r = (fill >> 5) + lane; r < (uint32_t)OW_ROWS; r += 32) mp->row_valid[r] = 0;
-      __syncwarp();
+      const long long pc1 = prof ? clock64() : 0;
+      const uint64_t R0 = 64 * s, R1 = R0 + 64;
       if (lane == 0) {
-        uint32_t flush = ctx0 != prev_ctx ? 1u : 0u;
+        uint32_t flush = ctx != prev_ctx ? 1u : 0u;
         if (*freq) {
           *freq = 0u;
           flush = 1u;
         }
-        mp->ctx = ctx0;
-        mp->count = fill;
-        mp->flush = flush;
-        uint32_t bytes = 0;
-        for (uint32_t q = 0; q < npieces; ++q) bytes += len_of[q] * 16u;
-        mbar_expect_tx(&sm.full[st], bytes);  // release: orders the meta writes above
-        for (uint32_t q = 0; q < npieces; ++q)
-          tma_bulk_g2s(&sm.stage[st][at_of[q]], a.smp + src_of[q], len_of[q] * 16u, &sm.full[st]);
+        sm.meta[st].ctx = ctx;
+        sm.meta[st].flush = flush;
+      }
+      uint32_t npieces = 0;
+      for (uint64_t base = f;; base += 32) {  // launches of this stage, 32 at a time (one batch normally)
+        if (base != f) {  // rare: a stage with more than 32 launches
+          const uint64_t li = base + lane;
+          rp = ~0ull;
+          if (li < a.n_launch) {
+            rp = a.rowpos[li];
+            src = a.lsrc[li];
+            cnt = a.lcnt[li];
+          }
+        }
+        const uint64_t rows = (cnt + 31) / 32;
+        const bool in = rp != ~0ull && rp < R1 && rp + rows > R0 && rows > 0;
+        uint64_t lo = 0, len = 0, dst = 0;
+        if (in) {
+          const uint64_t r_lo = rp > R0 ? rp : R0;
+          const uint64_t r_hi = rp + rows < R1 ? rp + rows : R1;
+          lo = 32 * (r_lo - rp);
+          const uint64_t hi = 32 * (r_hi - rp) < cnt ? 32 * (r_hi - rp) : cnt;
+          len = hi - lo;
+          dst = 32 * (r_lo - R0);
+        }
+        const uint32_t bytes = __reduce_add_sync(0xffffffffu, (uint32_t)len * 16u);
+        const uint32_t m = __ballot_sync(0xffffffffu, in);
+        // expect_tx before the arrive (below) keeps the phase open however early a copy lands
+        if (lane == 0 && bytes)
+          asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&sm.full[st])), "r"(bytes) : "memory");
+        __syncwarp();
+        if (in) tma_bulk_g2s(&sm.stage[st][dst], a.smp + src + lo, (uint32_t)len * 16u, &sm.full[st]);
+        npieces += __popc(m);
+        // the batch's last launch ends inside the stage: more launches may follow
+        const bool more = (rp != ~0ull) & (rp + rows < R1) & (base + 32 < a.n_launch);
+        if (!__shfl_sync(0xffffffffu, more, 31)) break;
+      }
+      if (lane == 0) {  // row meta; the arrive releases the ctx / flush words written above
+        mbar_expect_tx(&sm.full[st], (uint32_t)(OW_ROWS * 5));
+        tma_bulk_g2s(sm.meta[st].row_launch, a.row_launch + R0, OW_ROWS * 4, &sm.full[st]);
+        tma_bulk_g2s(sm.meta[st].row_valid, a.row_valid + R0, OW_ROWS, &sm.full[st]);
       }
       __syncwarp();
-      prev_ctx = ctx0;
+      if (prof) {
+        p_wait += pc1 - pc0;
+        p_comp += clock64() - pc1;
+        ++p_stages;
+        p_pieces += npieces;
+      }
+      prev_ctx = ctx;
       if (++st == OW_STAGES) {
         st = 0;
         ph ^= 1u;
@@ -433,6 +530,14 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
       sm.meta[st].flush = 1;
       mbar_arrive(&sm.full[st]);
     }
+    if (prof && lane == 0) {
+      unsigned long long* dbg = reinterpret_cast<unsigned long long*>(a.sink) + 8 * ((uint64_t)gridDim.x * OW_CONS_WARPS + blockIdx.x);
+      dbg[0] = p_wait;
+      dbg[1] = p_comp;
+      dbg[2] = p_stages;
+      dbg[3] = p_pieces;
+      dbg[4] = clock64() - p_t0;
+    }
     return;
   }
   // -------------------------------------------------- consumer warps
@@ -442,7 +547,7 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
   uint32_t cur_ctx = OW_DONE, st = 0, ph = 0;
   OwCounters k{0, 0, 0, 0};
   uint32_t sinkv = 0;
-  long long t_wait = 0, t_flush = 0, t_work = 0, n_stage = 0, t_key = 0, t_bucket = 0, t_add = 0;  // probe_mode 9 only
+  long long t_wait = 0, t_flush = 0, t_work = 0, n_stage = 0, t_key = 0, t_bucket = 0, t_add = 0, n_miss = 0;  // probe_mode 9 only
   while (true) {
     const long long c_0 = a.probe_mode == 9 ? clock64() : 0;
     mbar_wait(&sm.full[st], ph);
@@ -460,6 +565,15 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
     if (mctx == OW_DONE) break;
     cur_ctx = mctx;
     const bool ctx_ok = mctx < a.N;
+    if (a.probe_mode == 2) {  // measurement only: the TMA pipeline alone (stage released unread)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.empty[st]);
+      if (++st == OW_STAGES) {
+        st = 0;
+        ph ^= 1u;
+      }
+      continue;
+    }
     uint4 q[OW_PER_LANE];
     uint32_t lch[OW_PER_LANE];
     bool vld[OW_PER_LANE];
@@ -473,9 +587,17 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[st]);  // the stage is in registers: release it early
     uint32_t t[OW_PER_LANE], b[OW_PER_LANE];
+    bool cold = false;
 #pragma unroll
     for (int i = 0; i < OW_PER_LANE; ++i) {
-      t[i] = vld[i] ? own_key(q[i], lch[i], a, ctx_ok, k, sm) : EMPTY32;
+      const bool hot = vld[i] & own_hot(q[i], lch[i], a.S) & ctx_ok;
+      t[i] = hot ? (q[i].y << 5) | (q[i].z & 0xFFFFu) : EMPTY32;
+      cold |= vld[i] & !hot;
+    }
+    if (__any_sync(0xffffffffu, cold)) {  // rare: spills and invalid samples
+#pragma unroll
+      for (int i = 0; i < OW_PER_LANE; ++i)
+        if (vld[i] && t[i] == EMPTY32) own_cold(q[i], lch[i], a, ctx_ok, k, sm);
     }
     const long long c_2 = a.probe_mode == 9 ? clock64() : 0;
     if (a.probe_mode == 9) t_key += c_2 - c_1;
@@ -491,8 +613,7 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
 #pragma unroll
       for (int i = 0; i < OW_PER_LANE; ++i) {
         const uint4 v = *reinterpret_cast<const uint4*>(&sm.key[4 * b[i]]);  // home bucket
-        const int jm = bucket_match(v, t[i]);
-        slot[i] = jm >= 0 ? 4 * b[i] + jm : OW_MISS;
+        slot[i] = bucket_slot(v, t[i], b[i]);
       }
       const long long c_3 = a.probe_mode == 9 ? clock64() : 0;
       if (a.probe_mode == 9) t_bucket += c_3 - c_2;
@@ -504,11 +625,13 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
 #pragma unroll
       for (int i = 0; i < OW_PER_LANE; ++i) {
         const bool miss = t[i] != EMPTY32 && slot[i] == OW_MISS;
-        if (t[i] != EMPTY32 && !miss) own_add(sm, a, t[i], slot[i], 1u, mctx);
+        if (t[i] != EMPTY32 && !miss) red_shared_inc(&sm.cnt[slot[i]]);  // hit: never the spill slot
         mm[i] = __ballot_sync(0xffffffffu, miss);
         cum[i + 1] = cum[i] + __popc(mm[i]);
       }
-      for (uint32_t base = 0; base < cum[OW_PER_LANE]; base += 32) {
+      const uint32_t nmiss = a.probe_mode == 3 ? 0u : cum[OW_PER_LANE];  // mode 3: measurement only (misses dropped)
+      if (a.probe_mode == 9 && lane == 0) n_miss += nmiss;
+      for (uint32_t base = 0; base < nmiss; base += 32) {
         const uint32_t d = base + lane;
         const bool active = d < cum[OW_PER_LANE];
         int ii = 0;
@@ -559,6 +682,7 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
     dbg[4] = t_key;
     dbg[5] = t_bucket;
     dbg[6] = t_add;
+    dbg[7] = n_miss;
   }
   uint32_t bad_l = k.bad_l, bad_s = k.bad_s, zero = k.zero, fallback = k.fallback;
 #pragma unroll
@@ -949,10 +1073,15 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
   if (n == 0 || n_launch == 0 || n_launch >= (1ull << 31)) return DC_OK;
   const uint64_t N = t->N;
   Buf<uint32_t> bad;
-  Buf<uint64_t> k0, k1, cum;
+  Buf<uint64_t> k0, k1;
   Buf<uint32_t> v0, v1;
-  uint64_t* lkey = nullptr;
-  uint32_t* order = nullptr;
+  // stage plan
+  Buf<uint64_t> lrow, lsrc, lcnt, gst, rowpos, tot;
+  Buf<uint32_t> lflag, gx, gfirst, row_launch, st_first, st_ctx;
+  Buf<uint8_t> row_valid;
+  // rows: sum ceil(cnt/32) <= n/32 + n_launch; context padding < 64 rows per context (<= n_launch)
+  const uint64_t st_cap = (n / 32 + n_launch + 63) / 64 + n_launch + 1;
+  const uint64_t row_cap = 64 * st_cap;
   {
     Region rp(c, "pc:prep");
     DC_TRY(alloc_zero(c, bad, 1));
@@ -963,17 +1092,39 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
     DC_TRY(alloc(c, k1, n_launch));
     DC_TRY(alloc(c, v0, n_launch));
     DC_TRY(alloc(c, v1, n_launch));
-    DC_TRY(alloc(c, cum, n_launch + 1));
     k_own_keys<<<grid_for(c, n_launch, 256), 256, 0, c->stream>>>(launch_leaf, n_launch, N, k0.p, v0.p);
     DC_LAUNCHED(c);
     bool in1 = false;
     DC_TRY(radix_sort_pairs(c, k0.p, v0.p, k1.p, v1.p, n_launch, 0, bits_for(N), &in1));
-    lkey = in1 ? k1.p : k0.p;
-    order = in1 ? v1.p : v0.p;
-    uint64_t* cnt = in1 ? k0.p : k1.p;  // free buffer
-    k_own_cnt<<<grid_for(c, n_launch, 256), 256, 0, c->stream>>>(launch_off, order, n_launch, cnt);
+    const uint64_t* lkey = in1 ? k1.p : k0.p;
+    const uint32_t* order = in1 ? v1.p : v0.p;
+    DC_TRY(alloc(c, lrow, n_launch + 1));
+    DC_TRY(alloc(c, lsrc, n_launch));
+    DC_TRY(alloc(c, lcnt, n_launch));
+    DC_TRY(alloc(c, lflag, n_launch + 1));
+    DC_TRY(alloc(c, gx, n_launch + 1));
+    DC_TRY(alloc(c, gfirst, n_launch + 1));
+    DC_TRY(alloc(c, gst, n_launch + 1));
+    DC_TRY(alloc(c, rowpos, n_launch));
+    DC_TRY(alloc(c, tot, 1));
+    DC_TRY(alloc(c, row_launch, row_cap));
+    DC_TRY(alloc_zero(c, row_valid, row_cap));
+    DC_TRY(alloc(c, st_first, st_cap));
+    DC_TRY(alloc(c, st_ctx, st_cap));
+    k_plan_launch<<<grid_for(c, n_launch, 256), 256, 0, c->stream>>>(launch_off, order, lkey, n_launch, lrow.p, lflag.p,
+                                                                    lsrc.p, lcnt.p);
     DC_LAUNCHED(c);
-    DC_TRY(excl_scan<uint64_t>(c, cnt, cum.p, n_launch, cum.p + n_launch));
+    DC_TRY(excl_scan<uint64_t>(c, lrow.p, lrow.p, n_launch, lrow.p + n_launch));  // E: first row within the stream
+    DC_TRY(excl_scan<uint32_t>(c, lflag.p, gx.p, n_launch, gx.p + n_launch));      // group index, NG at gx[n]
+    k_plan_gfirst<<<grid_for(c, n_launch, 256), 256, 0, c->stream>>>(lkey, gx.p, gx.p + n_launch, n_launch, gfirst.p);
+    DC_LAUNCHED(c);
+    k_plan_gstages<<<grid_for(c, n_launch, 256), 256, 0, c->stream>>>(lrow.p, gfirst.p, gx.p + n_launch, n_launch, gst.p);
+    DC_LAUNCHED(c);
+    DC_TRY(excl_scan<uint64_t>(c, gst.p, gst.p, n_launch, tot.p));  // first stage per group, total stages
+    k_plan_rows<<<grid_for(c, n_launch * 32, 256), 256, 0, c->stream>>>(lrow.p, gx.p, gfirst.p, gst.p, lkey, order, lcnt.p,
+                                                                       n_launch, row_cap, rowpos.p, row_launch.p,
+                                                                       row_valid.p, st_first.p, st_ctx.p);
+    DC_LAUNCHED(c);
     uint32_t hbad = 0;
     DC_TRY(readback(c, bad.p, 4, &hbad));
     if (hbad) return DC_OK;  // offsets inconsistent: generic schedule
@@ -997,13 +1148,16 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
     DC_TRY(alloc_zero(c, ldiag, DG_N));
     OwnArgs a;
     a.smp = s;
-    a.launch_off = launch_off;
-    a.order = order;
-    a.lkey = lkey;
-    a.cum = cum.p;
+    a.rowpos = rowpos.p;
+    a.lsrc = lsrc.p;
+    a.lcnt = lcnt.p;
+    a.st_first = st_first.p;
+    a.st_ctx = st_ctx.p;
+    a.row_launch = row_launch.p;
+    a.row_valid = row_valid.p;
+    a.st_total = tot.p;
     a.n_launch = n_launch;
     a.N = N;
-    a.total = n;
     a.S = S;
     a.pkey = pkey.p;
     a.pcnt = pcnt.p;
@@ -1020,8 +1174,8 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
     a.sink = flags.p;
     if (const char* pm = getenv("DC_OWN_MODE")) a.probe_mode = (uint32_t)atoi(pm);  // measurement only
     Buf<unsigned long long> dbg;
-    if (a.probe_mode == 9) {
-      DC_TRY(alloc_zero(c, dbg, (uint64_t)G * OW_CONS_WARPS * 8));
+    if (a.probe_mode == 9 || a.probe_mode == 2) {
+      DC_TRY(alloc_zero(c, dbg, (uint64_t)G * (OW_CONS_WARPS + 1) * 8));
       a.sink = reinterpret_cast<uint32_t*>(dbg.p);
     }
     const size_t smem = sizeof(OwnSmem);
@@ -1035,6 +1189,17 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
       k_pc_owner<<<G, OW_THREADS, smem, c->stream>>>(a);
       DC_LAUNCHED(c);
     }
+    if (a.probe_mode == 9 || a.probe_mode == 2) {  // measurement only: print the cycle splits
+      std::vector<unsigned long long> hp((size_t)G * 8);
+      DC_TRY(readback(c, dbg.p + (size_t)G * OW_CONS_WARPS * 8, hp.size() * 8, hp.data()));
+      double ps[8] = {0, 0, 0, 0, 0, 0, 0, 0}, pmax = 0;
+      for (size_t i = 0; i < hp.size(); ++i) ps[i % 8] += (double)hp[i];
+      for (uint32_t g = 0; g < G; ++g) pmax = std::max(pmax, (double)hp[8 * g + 4]);
+      fprintf(stderr,
+              "{\"own_producer\": {\"wait_empty_cyc\": %.0f, \"compose_cyc\": %.0f, \"stages\": %.1f, \"pieces\": %.1f, "
+              "\"total_cyc\": %.0f, \"max_total_cyc\": %.0f}}\n",
+              ps[0] / G, ps[1] / G, ps[2] / G, ps[3] / G, ps[4] / G, pmax);
+    }
     if (a.probe_mode == 9) {  // measurement only: print the consumer cycle split
       std::vector<unsigned long long> h((size_t)G * OW_CONS_WARPS * 8);
       DC_TRY(readback(c, dbg.p, h.size() * 8, h.data()));
@@ -1043,8 +1208,8 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
       const double nw = (double)G * OW_CONS_WARPS;
       fprintf(stderr,
               "{\"own_split\": {\"wait_cyc\": %.0f, \"flush_cyc\": %.0f, \"work_cyc\": %.0f, \"stages\": %.1f, "
-              "\"key_cyc\": %.0f, \"bucket_cyc\": %.0f, \"add_cyc\": %.0f}}\n",
-              s[0] / nw, s[1] / nw, s[2] / nw, s[3] / nw, s[4] / nw, s[5] / nw, s[6] / nw);
+              "\"key_cyc\": %.0f, \"bucket_cyc\": %.0f, \"add_cyc\": %.0f, \"misses\": %.0f}}\n",
+              s[0] / nw, s[1] / nw, s[2] / nw, s[3] / nw, s[4] / nw, s[5] / nw, s[6] / nw, s[7]);
     }
     DC_TRY(readback(c, ctr.p, 16, hc));
     DC_TRY(readback(c, flags.p, 8, hf));
