@@ -32,12 +32,13 @@ constexpr int OW_STAGES = 4;
 constexpr int OW_PER_LANE = 4;                // samples per lane per stage
 constexpr int OW_ROUND = 32 * OW_PER_LANE;    // samples per warp per stage
 constexpr int OW_STAGE = OW_CONS_WARPS * OW_ROUND;  // 2048 samples per stage (32 KB)
-constexpr int OW_TAB = 12288;                 // shared hash table slots (96 KB)
+constexpr int OW_TAB = 11136;                 // shared hash table slots (87 KB)
+constexpr int OW_PEND = OW_ROUND + 32;        // per-warp queue of missed keys (probed 32 at a time)
 // a flush is requested at 2/3 load; past OW_SPILL_AT distinct keys new keys are not inserted
 // but appended to the CTA's spill region in HBM (kept as partial entries), so the table can
 // never overflow whatever the key cardinality. `distinct` lags by at most one round per warp.
 constexpr uint32_t OW_FLUSH_REQ = OW_TAB * 2 / 3;
-constexpr uint32_t OW_SPILL_AT = OW_TAB - OW_CONS_WARPS * OW_ROUND - 1;
+constexpr uint32_t OW_SPILL_AT = OW_TAB - OW_CONS_WARPS * OW_PEND - 1;
 constexpr uint32_t OW_MISS = 0xFFFFFFFEu;
 constexpr uint32_t OW_SPILL_CAP = 16384;      // spill entries per CTA
 constexpr uint32_t EMPTY32 = 0xFFFFFFFFu;
@@ -56,6 +57,7 @@ struct OwnSmem {
   uint4 stage[OW_STAGES][OW_STAGE];
   uint32_t key[OW_TAB];
   uint32_t cnt[OW_TAB];
+  uint32_t pend[OW_CONS_WARPS][OW_PEND];
   unsigned long long full[OW_STAGES], empty[OW_STAGES];
   OwMeta meta[OW_STAGES];
   uint32_t distinct;
@@ -285,8 +287,10 @@ __device__ __forceinline__ uint32_t bucket_slot(const uint4 v, uint32_t key, uin
   const uint32_t j = (v.y == key ? 1u : 0u) | (v.z == key ? 2u : 0u) | (v.w == key ? 3u : 0u);
   return (v.x == key) | (j != 0u) ? 4 * b + j : (uint32_t)OW_MISS;
 }
-__device__ __forceinline__ void red_shared_inc(uint32_t* p) {
-  asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(smem_u32(p)) : "memory");
+__device__ __forceinline__ void red_shared_inc_if(uint32_t* p, bool pred) {  // predicated, no branch
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.u32 p, %1, 0;\n@p red.shared.add.u32 [%0], 1;\n}\n" ::"r"(smem_u32(p)), "r"((uint32_t)pred)
+      : "memory");
 }
 
 // slow path: the key is not in its home bucket (new key, or displaced). Returns the slot, or
@@ -384,6 +388,7 @@ __device__ __noinline__ void own_cold(const uint4 q, uint32_t seg_launch, const 
   k.fallback |= r == 3;
 }
 
+template <int MODE>  // 0 = the product; 1, 2, 3, 9 = measurement variants (DC_OWN_MODE)
 __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   OwnSmem& sm = *reinterpret_cast<OwnSmem*>(smem_raw);
@@ -416,7 +421,7 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
     const uint32_t lane = tid;
     uint32_t st = 0, ph = 0, prev_ctx = OW_DONE;
     volatile uint32_t* freq = &sm.flush_req;
-    const bool prof = a.probe_mode == 2 || a.probe_mode == 9;  // measurement only
+    const bool prof = MODE == 2 || MODE == 9;  // measurement only
     long long p_wait = 0, p_comp = 0, p_stages = 0, p_pieces = 0;
     const long long p_t0 = prof ? clock64() : 0;
     // stage batches: cb = stages [bs, bs + 32), nb = [bs + 32, bs + 64)
@@ -547,25 +552,46 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
   uint32_t cur_ctx = OW_DONE, st = 0, ph = 0;
   OwCounters k{0, 0, 0, 0};
   uint32_t sinkv = 0;
-  long long t_wait = 0, t_flush = 0, t_work = 0, n_stage = 0, t_key = 0, t_bucket = 0, t_add = 0, n_miss = 0;  // probe_mode 9 only
+  long long t_wait = 0, t_flush = 0, t_work = 0, n_stage = 0, t_key = 0, t_bucket = 0, t_add = 0, n_miss = 0;  // MODE 9 only
+  uint32_t np = 0;        // queued misses of this warp (warp-uniform)
+  uint32_t inserted = 0;  // keys this lane inserted since the last publish
+  auto probe_one = [&](uint32_t key) {
+    const uint32_t r = own_probe(sm, key, own_bucket(key));
+    inserted += r >> 31;
+    own_add(sm, a, key, r & 0x7FFFFFFFu, 1u, cur_ctx);
+  };
+  // one `distinct` update per warp round (flush request when it crosses OW_FLUSH_REQ)
+  auto publish = [&]() {
+    const uint32_t ins = __reduce_add_sync(0xffffffffu, inserted);
+    inserted = 0;
+    if (lane == 0 && ins) {
+      const uint32_t before = atomicAdd(&sm.distinct, ins);
+      if (before < OW_FLUSH_REQ && before + ins >= OW_FLUSH_REQ) *(volatile uint32_t*)&sm.flush_req = 1u;
+    }
+  };
   while (true) {
-    const long long c_0 = a.probe_mode == 9 ? clock64() : 0;
+    const long long c_0 = MODE == 9 ? clock64() : 0;
     mbar_wait(&sm.full[st], ph);
-    const long long c_1 = a.probe_mode == 9 ? clock64() : 0;
+    const long long c_1 = MODE == 9 ? clock64() : 0;
     const uint32_t flush = sm.meta[st].flush, mctx = sm.meta[st].ctx;
     if (flush) {  // uniform: every consumer sees the same meta
+      if (np) {  // this warp's queued misses belong to the table being flushed
+        if (lane < np) probe_one(sm.pend[w][lane]);
+        np = 0;
+        publish();
+      }
       cons_sync();  // every consumer finished all previous stages
       // always entered by every consumer (its barriers are uniform); empty tables emit nothing.
       own_flush(sm, a, cur_ctx, ctid);
     }
-    if (a.probe_mode == 9) {
+    if (MODE == 9) {
       t_wait += c_1 - c_0;
       t_flush += clock64() - c_1;
     }
     if (mctx == OW_DONE) break;
     cur_ctx = mctx;
     const bool ctx_ok = mctx < a.N;
-    if (a.probe_mode == 2) {  // measurement only: the TMA pipeline alone (stage released unread)
+    if (MODE == 2) {  // measurement only: the TMA pipeline alone (stage released unread)
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[st]);
       if (++st == OW_STAGES) {
@@ -584,8 +610,6 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
       vld[i] = lane < sm.meta[st].row_valid[row];
       q[i] = vld[i] ? sm.stage[st][32 * row + lane] : make_uint4(0, 0, 0, 0);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.empty[st]);  // the stage is in registers: release it early
     uint32_t t[OW_PER_LANE], b[OW_PER_LANE];
     bool cold = false;
 #pragma unroll
@@ -599,72 +623,47 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
       for (int i = 0; i < OW_PER_LANE; ++i)
         if (vld[i] && t[i] == EMPTY32) own_cold(q[i], lch[i], a, ctx_ok, k, sm);
     }
-    const long long c_2 = a.probe_mode == 9 ? clock64() : 0;
-    if (a.probe_mode == 9) t_key += c_2 - c_1;
-    if (a.probe_mode == 1) {  // measurement: data movement + classification only
+    const long long c_2 = MODE == 9 ? clock64() : 0;
+    if (MODE == 9) t_key += c_2 - c_1;
+    if (MODE == 1) {  // measurement: data movement + classification only
 #pragma unroll
       for (int i = 0; i < OW_PER_LANE; ++i) sinkv ^= t[i] * (2 * i + 1);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.empty[st]);
     } else {
-      uint32_t slot[OW_PER_LANE], inserted = 0;
+      uint32_t slot[OW_PER_LANE];
 #pragma unroll
-      for (int i = 0; i < OW_PER_LANE; ++i) {
-        b[i] = own_bucket(t[i]);
-      }
+      for (int i = 0; i < OW_PER_LANE; ++i) b[i] = own_bucket(t[i]);
 #pragma unroll
       for (int i = 0; i < OW_PER_LANE; ++i) {
         const uint4 v = *reinterpret_cast<const uint4*>(&sm.key[4 * b[i]]);  // home bucket
         slot[i] = bucket_slot(v, t[i], b[i]);
       }
-      const long long c_3 = a.probe_mode == 9 ? clock64() : 0;
-      if (a.probe_mode == 9) t_bucket += c_3 - c_2;
-      // hits: add directly. Misses (new or displaced keys, ~3 % of samples) are compacted
-      // across the warp and probed together, so the slow path runs once per round with the
-      // missing keys spread over the lanes instead of once per sample slot with 1-2 lanes active.
-      uint32_t mm[OW_PER_LANE], cum[OW_PER_LANE + 1];
-      cum[0] = 0;
+      const long long c_3 = MODE == 9 ? clock64() : 0;
+      if (MODE == 9) t_bucket += c_3 - c_2;
+      // Hits are added directly. Misses (new or displaced keys, a few % of the samples) are
+      // queued per warp and probed 32 at a time, so the slow path runs with all lanes busy.
 #pragma unroll
       for (int i = 0; i < OW_PER_LANE; ++i) {
         const bool miss = t[i] != EMPTY32 && slot[i] == OW_MISS;
-        if (t[i] != EMPTY32 && !miss) red_shared_inc(&sm.cnt[slot[i]]);  // hit: never the spill slot
-        mm[i] = __ballot_sync(0xffffffffu, miss);
-        cum[i + 1] = cum[i] + __popc(mm[i]);
+        red_shared_inc_if(&sm.cnt[slot[i] & 0x7FFFFFFFu], t[i] != EMPTY32 && !miss);  // hit: never the spill slot
+        const uint32_t mm = __ballot_sync(0xffffffffu, miss);
+        if (miss) sm.pend[w][np + __popc(mm & lanemask_lt())] = t[i];
+        np += __popc(mm);
       }
-      const uint32_t nmiss = a.probe_mode == 3 ? 0u : cum[OW_PER_LANE];  // mode 3: measurement only (misses dropped)
-      if (a.probe_mode == 9 && lane == 0) n_miss += nmiss;
-      for (uint32_t base = 0; base < nmiss; base += 32) {
-        const uint32_t d = base + lane;
-        const bool active = d < cum[OW_PER_LANE];
-        int ii = 0;
-        uint32_t mi = mm[0], ci = 0;
-#pragma unroll
-        for (int i = 1; i < OW_PER_LANE; ++i)
-          if (d >= cum[i]) {
-            ii = i;
-            mi = mm[i];
-            ci = cum[i];
-          }
-        const uint32_t src = active ? __fns(mi, 0, (int)(d - ci) + 1) : 0u;
-        uint32_t key = EMPTY32;
-#pragma unroll
-        for (int i = 0; i < OW_PER_LANE; ++i) {
-          const uint32_t ki = __shfl_sync(0xffffffffu, t[i], src);
-          if (i == ii) key = ki;
-        }
-        if (active) {
-          const uint32_t r = own_probe(sm, key, own_bucket(key));
-          inserted += r >> 31;
-          own_add(sm, a, key, r & 0x7FFFFFFFu, 1u, mctx);
-        }
+      if (MODE == 3) np = 0;  // measurement only: misses dropped
+      if (MODE == 9 && lane == 0) n_miss += np;
+      __syncwarp();
+      while (np >= 32) {
+        np -= 32;
+        probe_one(sm.pend[w][np + lane]);
       }
-      if (a.probe_mode == 9) t_add += clock64() - c_3;
-      // one `distinct` update per warp round (flush request when it crosses OW_FLUSH_REQ)
-      const uint32_t ins = __reduce_add_sync(0xffffffffu, inserted);
-      if (lane == 0 && ins) {
-        const uint32_t before = atomicAdd(&sm.distinct, ins);
-        if (before < OW_FLUSH_REQ && before + ins >= OW_FLUSH_REQ) *(volatile uint32_t*)&sm.flush_req = 1u;
-      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.empty[st]);
+      publish();
+      if (MODE == 9) t_add += clock64() - c_3;
     }
-    if (a.probe_mode == 9) {
+    if (MODE == 9) {
       t_work += clock64() - c_1;
       ++n_stage;
     }
@@ -673,7 +672,7 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
       ph ^= 1u;
     }
   }
-  if (a.probe_mode == 9 && lane == 0) {  // measurement: per-warp cycle split (wait / flush / work)
+  if (MODE == 9 && lane == 0) {  // measurement: per-warp cycle split (wait / flush / work)
     unsigned long long* dbg = reinterpret_cast<unsigned long long*>(a.sink) + 8 * (blockIdx.x * OW_CONS_WARPS + w);
     dbg[0] = t_wait;
     dbg[1] = t_flush;
@@ -697,7 +696,7 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
     if (bad_s) atomicAdd(a.ldiag + DG_BAD_STALL, (unsigned long long)bad_s);
     if (zero) atomicAdd(a.ldiag + DG_ZERO, (unsigned long long)zero);
     if (fallback) atomicOr(a.g_flags, (uint32_t)OWF_FALLBACK);
-    if (a.probe_mode && sinkv == 0x12345678u) a.sink[0] = sinkv;
+    if (MODE && sinkv == 0x12345678u) a.sink[0] = sinkv;
   }
 }
 
@@ -1179,14 +1178,19 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
       a.sink = reinterpret_cast<uint32_t*>(dbg.p);
     }
     const size_t smem = sizeof(OwnSmem);
-    static bool attr_set = false;
-    if (!attr_set) {
-      DC_CUDA(c, cudaFuncSetAttribute(k_pc_owner, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr_set = true;
+    void (*kern)(OwnArgs) = k_pc_owner<0>;
+    switch (a.probe_mode) {  // measurement variants only
+      case 1: kern = k_pc_owner<1>; break;
+      case 2: kern = k_pc_owner<2>; break;
+      case 3: kern = k_pc_owner<3>; break;
+      case 4: kern = k_pc_owner<4>; break;
+      case 9: kern = k_pc_owner<9>; break;
+      default: a.probe_mode = 0;
     }
+    DC_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     {
       Region rk(c, "k:pc_owner");
-      k_pc_owner<<<G, OW_THREADS, smem, c->stream>>>(a);
+      kern<<<G, OW_THREADS, smem, c->stream>>>(a);
       DC_LAUNCHED(c);
     }
     if (a.probe_mode == 9 || a.probe_mode == 2) {  // measurement only: print the cycle splits
@@ -1213,6 +1217,9 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
     }
     DC_TRY(readback(c, ctr.p, 16, hc));
     DC_TRY(readback(c, flags.p, 8, hf));
+    if (a.probe_mode == 9)
+      fprintf(stderr, "{\"own_out\": {\"entries\": %llu, \"segments\": %llu}}\n", (unsigned long long)hc[0],
+              (unsigned long long)(hc[1] & 0xFFFFFFFFu));
   }
   if (hf[0]) return DC_OK;  // fallback / overflow -> generic schedule (diag of this pass discarded)
   const uint32_t n_segs = (uint32_t)(hc[1] & 0xFFFFFFFFu);
