@@ -700,6 +700,158 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
   }
 }
 
+// ---------------------------------------------------------------- global bitmap reduce
+// The data-parallel reduce used whenever every context's PC range is small enough (always for
+// real kernels). Per context c, with pc' = pc_off >> (common trailing zero bits of c's PCs),
+// key (pc', stall) is bit (pc' << 5 | stall) of c's slice of one global presence bitmap; one
+// 32-bit word per PC. Because contexts (then PCs, then stalls) are laid out in canonical order,
+// an exclusive scan over the words' popcounts is each bin's final index and a scan over
+// non-zero words each PC node's index: the partial entries are reduced by global atomics into
+// their final slots, without sorting.
+constexpr uint32_t BR_MAX_WORDS = 1u << 20;   // per context (larger PC ranges: per-group reduce)
+constexpr uint64_t BR_MAX_TOTAL = 1ull << 27;  // whole bitmap (512 MB)
+// segment kernels: one warp per (segment, chunk of BR_CH entries)
+constexpr uint32_t BR_CH = 256;
+constexpr uint32_t BR_MAXCH = ((OW_TAB > (int)OW_SPILL_CAP ? OW_TAB : OW_SPILL_CAP) + BR_CH - 1) / BR_CH;
+#define BR_FOR_CHUNKS(seg, n_segs, N)                                                                          \
+  for (uint64_t item = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; item < (uint64_t)n_segs * BR_MAXCH; \
+       item += ((uint64_t)gridDim.x * blockDim.x) >> 5)                                                        \
+    if (const uint4 sg = seg[item / BR_MAXCH]; sg.x < N && (item % BR_MAXCH) * BR_CH < sg.y)
+
+__global__ void k_br_range(const uint4* __restrict__ seg, uint32_t n_segs, const uint32_t* __restrict__ pkey, uint64_t N,
+                           uint32_t* __restrict__ cmax, uint32_t* __restrict__ cor) {
+  const uint32_t lane = threadIdx.x & 31;
+  BR_FOR_CHUNKS(seg, n_segs, N) {
+    const uint64_t base = (uint64_t)sg.z | ((uint64_t)sg.w << 32);
+    const uint32_t j0 = (uint32_t)(item % BR_MAXCH) * BR_CH, j1 = min(sg.y, j0 + BR_CH);
+    uint32_t mk = 0, orp = 0;
+#pragma unroll 4
+    for (uint32_t j = j0 + lane; j < j1; j += 32) {
+      const uint32_t kk = pkey[base + j];
+      mk = max(mk, kk + 1);  // 0 = no entry
+      orp |= kk >> 5;
+    }
+    mk = __reduce_max_sync(0xffffffffu, mk);
+    orp = __reduce_or_sync(0xffffffffu, orp);
+    if (lane == 0) {
+      atomicMax(cmax + sg.x, mk);
+      atomicOr(cor + sg.x, orp);
+    }
+  }
+}
+
+__global__ void k_br_words(const uint32_t* __restrict__ cmax, const uint32_t* __restrict__ cor, uint64_t N,
+                           uint64_t* __restrict__ cw, uint8_t* __restrict__ csh, uint32_t* too_wide) {
+  for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < N; c += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t m = cmax[c], o = cor[c];
+    const int sh = o ? __ffs(o) - 1 : 0;
+    const uint64_t words = m ? (uint64_t)(((m - 1) >> 5) >> sh) + 1 : 0;
+    if (words > BR_MAX_WORDS) atomicOr(too_wide, 1u);
+    cw[c] = words;
+    csh[c] = (uint8_t)sh;
+  }
+}
+
+__global__ void k_br_bits(const uint4* __restrict__ seg, uint32_t n_segs, const uint32_t* __restrict__ pkey, uint64_t N,
+                          const uint64_t* __restrict__ wbase, const uint8_t* __restrict__ csh, uint32_t* __restrict__ bm) {
+  BR_FOR_CHUNKS(seg, n_segs, N) {
+    const uint64_t base = (uint64_t)sg.z | ((uint64_t)sg.w << 32);
+    const uint32_t j0 = (uint32_t)(item % BR_MAXCH) * BR_CH, j1 = min(sg.y, j0 + BR_CH);
+    const uint64_t wb = wbase[sg.x];
+    const int sh = csh[sg.x];
+#pragma unroll 4
+    for (uint32_t j = j0 + (threadIdx.x & 31); j < j1; j += 32) {
+      const uint32_t kk = pkey[base + j];
+      atomicOr(bm + wb + ((kk >> 5) >> sh), 1u << (kk & 31u));
+    }
+  }
+}
+
+// packed per-word counts: bins (popcount) in the high half, PC nodes (word != 0) in the low half
+__global__ void k_br_pop(const uint32_t* __restrict__ bm, uint64_t W, uint64_t* __restrict__ pk) {
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < W; w += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t b = bm[w];
+    pk[w] = ((uint64_t)__popc(b) << 32) | (b != 0u ? 1u : 0u);
+  }
+}
+
+// one thread per bitmap word: its PC node and bins (counts are zeroed by the caller). The word's
+// context is found by binary search over the word bases (empty contexts share their base with
+// the next context, so the last base <= w is the owning, non-empty one).
+__global__ void k_br_emit(const uint32_t* __restrict__ bm, const uint64_t* __restrict__ pre, uint64_t W,
+                          const uint64_t* __restrict__ wbase, const uint8_t* __restrict__ csh, uint64_t N,
+                          uint32_t* __restrict__ pc_ctx, uint32_t* __restrict__ pc_off, uint32_t* __restrict__ bin_pcnode,
+                          uint16_t* __restrict__ bin_stall) {
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < W; w += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t bits = bm[w];
+    if (!bits) continue;
+    uint64_t lo = 0, hi = N - 1;  // last c with wbase[c] <= w
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi + 1) >> 1;
+      if (wbase[mid] <= w) lo = mid;
+      else hi = mid - 1;
+    }
+    const uint64_t c = lo;
+    const uint64_t pr = pre[w];
+    const uint32_t p = (uint32_t)pr;  // PC node rank
+    uint64_t r = pr >> 32;            // first bin
+    pc_ctx[p] = (uint32_t)c;
+    pc_off[p] = (uint32_t)((w - wbase[c]) << csh[c]);
+    while (bits) {
+      const uint32_t b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      bin_pcnode[r] = (uint32_t)(N + p);
+      bin_stall[r] = (uint16_t)b;
+      ++r;
+    }
+  }
+}
+
+// one warp per segment chunk: counts into their final bins; per-stall totals of the segment's
+// context summed in shared memory (exact: 32-bit halves with carry) and added once per chunk
+constexpr int BR_WARPS = 8;
+__global__ void __launch_bounds__(32 * BR_WARPS) k_br_count(
+    const uint4* __restrict__ seg, uint32_t n_segs, const uint32_t* __restrict__ pkey,
+    const unsigned long long* __restrict__ pcnt, uint64_t N, uint32_t S, const uint32_t* __restrict__ bm,
+    const uint64_t* __restrict__ pre, const uint64_t* __restrict__ wbase, const uint8_t* __restrict__ csh,
+    unsigned long long* __restrict__ bin_count, unsigned long long* __restrict__ xsamples,
+    unsigned long long* __restrict__ xstall) {
+  __shared__ uint32_t lo[BR_WARPS][32], hi[BR_WARPS][32];
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  lo[w][lane] = 0;
+  hi[w][lane] = 0;
+  __syncwarp();
+  BR_FOR_CHUNKS(seg, n_segs, N) {
+    const uint64_t base = (uint64_t)sg.z | ((uint64_t)sg.w << 32);
+    const uint32_t j0 = (uint32_t)(item % BR_MAXCH) * BR_CH, j1 = min(sg.y, j0 + BR_CH);
+    const uint64_t wb = wbase[sg.x];
+    const int sh = csh[sg.x];
+#pragma unroll 2
+    for (uint32_t j = j0 + lane; j < j1; j += 32) {
+      const uint32_t kk = pkey[base + j];
+      const unsigned long long cv = pcnt[base + j];
+      const uint64_t wd = wb + ((kk >> 5) >> sh);
+      const uint32_t b = kk & 31u;
+      const uint64_t r = (pre[wd] >> 32) + __popc(bm[wd] & ((1u << b) - 1u));
+      atomicAdd(bin_count + r, cv);
+      const uint32_t c32 = (uint32_t)cv;
+      const uint32_t old = atomicAdd(&lo[w][b], c32);
+      const uint32_t carry = old + c32 < old ? 1u : 0u;
+      if (carry + (uint32_t)(cv >> 32)) atomicAdd(&hi[w][b], carry + (uint32_t)(cv >> 32));
+    }
+    __syncwarp();
+    const unsigned long long t = ((unsigned long long)hi[w][lane] << 32) | lo[w][lane];
+    lo[w][lane] = 0;
+    hi[w][lane] = 0;
+    if (t && lane < S) atomicAdd(xstall + (uint64_t)lane * N + sg.x, t);
+    unsigned long long tot = lane < S ? t : 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    if (lane == 0 && tot) atomicAdd(xsamples + sg.x, tot);
+    __syncwarp();
+  }
+}
+
 // ---------------------------------------------------------------- per-context reduce
 // One CTA per context. Its partial entries (all segments of the context: several CTAs of the
 // main kernel and several flushes) are processed in key-range chunks of at most RD_CAP
@@ -1094,7 +1246,11 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
     k_own_keys<<<grid_for(c, n_launch, 256), 256, 0, c->stream>>>(launch_leaf, n_launch, N, k0.p, v0.p);
     DC_LAUNCHED(c);
     bool in1 = false;
-    DC_TRY(radix_sort_pairs(c, k0.p, v0.p, k1.p, v1.p, n_launch, 0, bits_for(N), &in1));
+    {
+      Region rs(c, "prep:sort");
+      DC_TRY(radix_sort_pairs(c, k0.p, v0.p, k1.p, v1.p, n_launch, 0, bits_for(N), &in1));
+    }
+    Region rpl(c, "prep:plan");
     const uint64_t* lkey = in1 ? k1.p : k0.p;
     const uint32_t* order = in1 ? v1.p : v0.p;
     DC_TRY(alloc(c, lrow, n_launch + 1));
@@ -1223,6 +1379,81 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
   }
   if (hf[0]) return DC_OK;  // fallback / overflow -> generic schedule (diag of this pass discarded)
   const uint32_t n_segs = (uint32_t)(hc[1] & 0xFFFFFFFFu);
+  {
+    // ------------------------------------------------ global bitmap reduce (see k_br_*)
+    HostRegion hr(c, "br");
+    Region rb(c, "pc:breduce");
+    Buf<uint32_t> cm, wide;
+    Buf<uint64_t> cw;
+    Buf<uint8_t> csh;
+    DC_TRY(alloc_zero(c, cm, 2 * N));  // cmax | cor
+    DC_TRY(alloc(c, cw, N + 1));
+    DC_TRY(alloc(c, csh, N));
+    DC_TRY(alloc_zero(c, wide, 1));
+    const int segs_grid = grid_for(c, (uint64_t)n_segs * BR_MAXCH * 32, 256);
+    {
+      Region rk(c, "k:br_range");
+      k_br_range<<<segs_grid, 256, 0, c->stream>>>(seg.p, n_segs, pkey.p, N, cm.p, cm.p + N);
+      DC_LAUNCHED(c);
+    }
+    {
+      Region rk(c, "k:br_words");
+      k_br_words<<<grid_for(c, N, 256), 256, 0, c->stream>>>(cm.p, cm.p + N, N, cw.p, csh.p, wide.p);
+      DC_LAUNCHED(c);
+    }
+    DC_TRY(excl_scan<uint64_t>(c, cw.p, cw.p, N, cw.p + N));  // word base per context, W at cw[N]
+    uint64_t hw[2] = {0, 0};
+    DC_TRY(readback(c, cw.p + N, 8, hw));
+    DC_TRY(readback(c, wide.p, 4, &hw[1]));
+    const uint64_t W = hw[0];
+    if (!(hw[1] & 0xFFFFFFFFu) && W <= BR_MAX_TOTAL) {
+      Buf<uint32_t> bm;
+      Buf<uint64_t> pk;
+      DC_TRY(alloc_zero(c, bm, W));
+      DC_TRY(alloc(c, pk, W + 1));
+      {
+        Region rk(c, "k:br_bits");
+        k_br_bits<<<segs_grid, 256, 0, c->stream>>>(seg.p, n_segs, pkey.p, N, cw.p, csh.p, bm.p);
+        DC_LAUNCHED(c);
+      }
+      {
+        Region rk(c, "k:br_pop");
+        k_br_pop<<<grid_for(c, W, 256), 256, 0, c->stream>>>(bm.p, W, pk.p);
+        DC_LAUNCHED(c);
+      }
+      DC_TRY(excl_scan<uint64_t>(c, pk.p, pk.p, W, pk.p + W));
+      uint64_t ht = 0;
+      DC_TRY(readback(c, pk.p + W, 8, &ht));
+      const uint64_t nb = ht >> 32, npc = ht & 0xFFFFFFFFu;
+      t->Npc = npc;
+      t->Nbins = nb;
+      DC_TRY(palloc(c, t->pc_ctx, npc));
+      DC_TRY(palloc(c, t->pc_off, npc));
+      DC_TRY(palloc(c, t->bin_pcnode, nb));
+      DC_TRY(palloc(c, t->bin_stall, nb));
+      DC_TRY(palloc(c, t->bin_count, nb));
+      DC_CUDA(c, cudaMemsetAsync(t->bin_count, 0, (nb ? nb : 1) * 8, c->stream));
+      if (nb) {
+        {
+          Region rk(c, "k:br_emit");
+          k_br_emit<<<grid_for(c, W, 256), 256, 0, c->stream>>>(bm.p, pk.p, W, cw.p, csh.p, N, t->pc_ctx, t->pc_off,
+                                                                t->bin_pcnode, t->bin_stall);
+          DC_LAUNCHED(c);
+        }
+        {
+          Region rk(c, "k:br_count");
+          k_br_count<<<grid_for(c, (uint64_t)n_segs * BR_MAXCH * 32, 32 * BR_WARPS), 32 * BR_WARPS, 0, c->stream>>>(
+              seg.p, n_segs, pkey.p, pcnt.p, N, S, bm.p, pk.p, cw.p, csh.p, (unsigned long long*)t->bin_count,
+              (unsigned long long*)t->xsamples, (unsigned long long*)t->xstall);
+          DC_LAUNCHED(c);
+        }
+      }
+      DC_TRY(add_diag(c, ldiag.p));
+      *n_bins_out = nb;
+      *handled = 1;
+      return DC_OK;
+    }
+  }
   Region rr(c, "pc:reduce");
   // group segments by context
   Buf<uint64_t> sk0, sk1;
