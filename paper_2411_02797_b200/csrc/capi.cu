@@ -165,6 +165,7 @@ void dc_ctx_destroy(dc_ctx* ctx) {
   cudaFree(ctx->d_flags);
   cudaFree(ctx->d_diag);
   cudaFreeHost(ctx->h_pinned);
+  for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -198,10 +199,9 @@ dc_status dc_ctx_timer_report(dc_ctx* ctx, char* buf, size_t len) {
     }
     tot[i] += ms;
     cnt[i] += 1;
-    cudaEventDestroy(t.a);
-    cudaEventDestroy(t.b);
   }
   ctx->timed.clear();
+  ctx->ev_next = 0;  // the events are reused by the next timed regions
   for (auto& h : ctx->htimed) {
     std::string nm = std::string("h:") + h.name;
     size_t i = 0;

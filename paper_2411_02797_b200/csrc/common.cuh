@@ -46,6 +46,16 @@ struct Ctx {
   std::vector<Timed> timed;
   struct HTimed { const char* name; double ms; };
   std::vector<HTimed> htimed;  // host-side durations ("h:<name>" in the report)
+  std::vector<cudaEvent_t> ev_pool;  // timing events, reused after each report
+  size_t ev_next = 0;
+  cudaEvent_t event() {
+    if (ev_next == ev_pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ev_pool.push_back(e);
+    }
+    return ev_pool[ev_next++];
+  }
 };
 
 // RAII host wall-clock timer (no-op unless timing is on): finds host stalls between kernels
@@ -69,14 +79,13 @@ struct Region {
   cudaEvent_t a = nullptr;
   Region(Ctx* ctx, const char* n) : c(ctx), name(n) {
     if (c->timing) {
-      cudaEventCreate(&a);
+      a = c->event();
       cudaEventRecord(a, c->stream);
     }
   }
   ~Region() {
     if (c->timing && a) {
-      cudaEvent_t b;
-      cudaEventCreate(&b);
+      cudaEvent_t b = c->event();
       cudaEventRecord(b, c->stream);
       c->timed.push_back({name, a, b});
     }

@@ -59,20 +59,41 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_reduce(const T* __restric
   if (threadIdx.x == 0) sums[blockIdx.x] = tot;
 }
 
-// single-block scan of a (short) array, in place; optionally stores the total
+// single-block scan of a medium array (out may equal in): tiles of 4096 staged through shared
+// memory (coalesced), 4 consecutive elements per thread, carry across tiles
+constexpr int SCAN1_THREADS = 1024, SCAN1_ITEMS = 4, SCAN1_TILE = SCAN1_THREADS * SCAN1_ITEMS;
+constexpr uint64_t SCAN1_MAX = 16 * SCAN1_TILE;
 template <class T>
-__global__ void __launch_bounds__(1024) k_scan_single(T* a, uint64_t n, T* total) {
-  __shared__ T carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (uint64_t base = 0; base < n; base += 1024) {
-    uint64_t j = base + threadIdx.x;
-    T v = j < n ? a[j] : T(0);
-    T tot;
-    T ex = block_excl_scan<T, 1024>(v, &tot);
-    if (j < n) a[j] = carry + ex;
+__global__ void __launch_bounds__(SCAN1_THREADS) k_scan_one(const T* in, T* out, uint64_t n, T* total) {
+  __shared__ T tile[SCAN1_TILE];
+  T carry = 0;
+  for (uint64_t base = 0; base < n; base += SCAN1_TILE) {
+#pragma unroll
+    for (int i = 0; i < SCAN1_ITEMS; ++i) {
+      const uint64_t j = base + (uint64_t)i * SCAN1_THREADS + threadIdx.x;
+      tile[i * SCAN1_THREADS + threadIdx.x] = j < n ? in[j] : T(0);
+    }
     __syncthreads();
-    if (threadIdx.x == 0) carry += tot;
+    T v[SCAN1_ITEMS], s = 0;
+#pragma unroll
+    for (int i = 0; i < SCAN1_ITEMS; ++i) {
+      v[i] = tile[threadIdx.x * SCAN1_ITEMS + i];
+      s += v[i];
+    }
+    T tot;
+    T ex = block_excl_scan<T, SCAN1_THREADS>(s, &tot) + carry;
+#pragma unroll
+    for (int i = 0; i < SCAN1_ITEMS; ++i) {
+      tile[threadIdx.x * SCAN1_ITEMS + i] = ex;
+      ex += v[i];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < SCAN1_ITEMS; ++i) {
+      const uint64_t j = base + (uint64_t)i * SCAN1_THREADS + threadIdx.x;
+      if (j < n) out[j] = tile[i * SCAN1_THREADS + threadIdx.x];
+    }
+    carry += tot;
     __syncthreads();
   }
   if (total && threadIdx.x == 0) *total = carry;
@@ -108,9 +129,8 @@ dc_status excl_scan(Ctx* c, const T* in, T* out, uint64_t n, T* total_dev) {
     return DC_OK;
   }
   uint64_t nt = (n + SCAN_TILE - 1) / SCAN_TILE;
-  if (nt == 1) {
-    if (in != out) DC_CUDA(c, cudaMemcpyAsync(out, in, n * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
-    k_scan_single<T><<<1, 1024, 0, c->stream>>>(out, n, total_dev);
+  if (n <= SCAN1_MAX) {  // one launch
+    k_scan_one<T><<<1, SCAN1_THREADS, 0, c->stream>>>(in, out, n, total_dev);
     DC_LAUNCHED(c);
     return DC_OK;
   }
