@@ -46,7 +46,8 @@ def traffic_for(kernel: str):
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
-            return json.load(f).get(kernel)
+            t = json.load(f)
+        return t.get("k_" + kernel, t.get(kernel))
     except Exception:
         return None
 
@@ -117,9 +118,12 @@ def make_workload(cfg: int, rank: int, device: str, n_records: int | None = None
     return p, tr
 
 
-def run_step(dc, ctx, tr, cfg: int, want_views: bool = True):
-    """One pass of the hot path; returns (cct, views)."""
+def run_step(dc, ctx, tr, cfg: int, want_views: bool = True, comm=None):
+    """One pass of the hot path; returns (cct, views). With a communicator (N > 1) the step is
+    the local rows a1-a6 + a5 followed by the cross-rank merge a9 (NCCL exchange), and returns
+    this rank's partition of the merged CCT; the views run on a single GPU's complete CCT."""
     if cfg == 4:
+        d = tr.dict
         cct, leaf = dc.dc_cct_build(ctx, tr.offsets, tr.ids, tr.n_frames, tr.dict)
     else:
         ids, d = dc.dc_intern_frames(ctx, tr.keys, tr.ids_buf)
@@ -129,6 +133,12 @@ def run_step(dc, ctx, tr, cfg: int, want_views: bool = True):
         dc.dc_pc_sample_attribute(ctx, cct, tr.samples, leaf, tr.launch_off, n_stall=tr.n_stall)
     dc.dc_cct_rollup(ctx, cct)
     views = {}
+    if comm is not None:
+        lv = cct.view()
+        views["local"] = (int(lv.n_nodes), int(lv.n_bins))
+        part, _gd = dc.dc_cct_merge_ranks(ctx, comm, cct, d)
+        cct.free()
+        return part, views
     if want_views:
         hot = dc.dc_hotspots_topk(ctx, cct, dc.DC_VIEW_INCLUSIVE, 0, 1 << dc.DC_KIND_KERNEL, 0.01, 10)
         views["hotspots"] = hot
@@ -241,6 +251,10 @@ def main():
     if args.config == 4:
         keys = torch.from_numpy(np.ascontiguousarray(p.pool_keys).view(np.int32).reshape(-1, 4).copy()).to(dev)
     ctx = dc.Context(local)
+    comm = None
+    if world > 1:
+        from paper_2411_02797_b200 import dist as dcdist
+        comm = dcdist.make_comm(ctx, world, rank)
     if args.config == 4:
         tr.dict = dc.dc_dict_from_sorted(ctx, keys)
     F = int(tr.offsets[-1].item())
@@ -255,7 +269,7 @@ def main():
             dist.barrier()
 
     for _ in range(args.warmup):
-        cct, _ = run_step(dc, ctx, tr, args.config)
+        cct, _ = run_step(dc, ctx, tr, args.config, comm=comm)
         cct.free()
     ctx.sync()
     # ---------------- timed region (device time, CUDA events on the library stream; the
@@ -270,7 +284,7 @@ def main():
         e0.record(stream)
         last = None
         for _ in range(args.steps):
-            cct, views = run_step(dc, ctx, tr, args.config)
+            cct, views = run_step(dc, ctx, tr, args.config, comm=comm)
             if last is not None:
                 last.free()
             last = cct
@@ -280,14 +294,17 @@ def main():
     launches = (ctx.launches - l0) // args.steps
     step_bytes = (ctx.diag()["bytes_moved_est"] - b0) / args.steps
     ms = e0.elapsed_time(e1) / args.steps
-    nv = last.view()
-    n_bins, n_nodes = int(nv.n_bins), int(nv.n_nodes)
+    if "local" in views:
+        n_nodes, n_bins = views["local"]
+    else:
+        nv = last.view()
+        n_bins, n_nodes = int(nv.n_bins), int(nv.n_nodes)
     last.free()
     # ---------------- instrumented pass: per-stage / per-kernel CUDA-event timers
     ctx.set_timing(True)
     ctx.timer_report()
     for _ in range(max(2, min(args.steps, 5))):
-        cct, _ = run_step(dc, ctx, tr, args.config)
+        cct, _ = run_step(dc, ctx, tr, args.config, comm=comm)
         cct.free()
     timers = ctx.timer_report()
     ctx.set_timing(False)
@@ -339,7 +356,7 @@ def main():
             for _ in range(args.e2e_steps):
                 for k in host:
                     devb[k].copy_(host[k], non_blocking=True)
-                cct, views = run_step(dc, ctx, t2, args.config)
+                cct, views = run_step(dc, ctx, t2, args.config, comm=comm)
                 # results read back to the host every step: the top-k entries (24 B each)
                 d2h = 24 * (len(views.get("hotspots", [])) + len(views.get("stall", [])))
                 cct.free()
@@ -370,7 +387,8 @@ def main():
                            "pc_samples": int(tr.samples.shape[0]) if args.config == 3 else 0,
                            "launch_records": tr.n_records, "nodes": n_nodes, "bins": n_bins,
                            "l2": "inputs larger than L2 (1.6 GB of samples per step); no flush",
-                           "parallelism": f"dp{world} (independent shards, weak scaling)"},
+                           "parallelism": (f"dp{world}: per-rank shard, local CCT + NCCL cross-rank merge "
+                                           "(dc_cct_merge_ranks), weak scaling") if world > 1 else "dp1"},
                 "roofline": roof, "stages_ms": stages, "gpu_launches": int(launches),
                 "step_hbm": {"alg_bytes_per_step": int(step_bytes), "gbs": round(step_bytes / (ms / 1e3) / 1e9, 1),
                              "frac_of_peak": round(step_bytes / (ms / 1e3) / 1e9 / peak, 4)},

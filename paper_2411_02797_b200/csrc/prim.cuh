@@ -59,44 +59,38 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_reduce(const T* __restric
   if (threadIdx.x == 0) sums[blockIdx.x] = tot;
 }
 
-// single-block scan of a medium array (out may equal in): tiles of 4096 staged through shared
-// memory (coalesced), 4 consecutive elements per thread, carry across tiles
-constexpr int SCAN1_THREADS = 1024, SCAN1_ITEMS = 4, SCAN1_TILE = SCAN1_THREADS * SCAN1_ITEMS;
-constexpr uint64_t SCAN1_MAX = 16 * SCAN1_TILE;
+// single-block scan of a medium array (out may equal in): warp w owns the contiguous chunk
+// [w*C, (w+1)*C); pass 1 sums the chunks, one warp scans the 32 chunk sums, pass 2 re-reads each
+// chunk (L1/L2-resident) and scans it 32 elements at a time with a running carry.
+constexpr int SCAN1_THREADS = 1024;
+constexpr uint64_t SCAN1_MAX = 1ull << 16;
 template <class T>
 __global__ void __launch_bounds__(SCAN1_THREADS) k_scan_one(const T* in, T* out, uint64_t n, T* total) {
-  __shared__ T tile[SCAN1_TILE];
-  T carry = 0;
-  for (uint64_t base = 0; base < n; base += SCAN1_TILE) {
+  __shared__ T wsum[32];
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint64_t C = (n + 31) / 32;
+  const uint64_t lo = w * C, hi = lo + C < n ? lo + C : n;
+  T s = 0;
+  for (uint64_t j = lo + lane; j < hi; j += 32) s += in[j];
 #pragma unroll
-    for (int i = 0; i < SCAN1_ITEMS; ++i) {
-      const uint64_t j = base + (uint64_t)i * SCAN1_THREADS + threadIdx.x;
-      tile[i * SCAN1_THREADS + threadIdx.x] = j < n ? in[j] : T(0);
-    }
-    __syncthreads();
-    T v[SCAN1_ITEMS], s = 0;
-#pragma unroll
-    for (int i = 0; i < SCAN1_ITEMS; ++i) {
-      v[i] = tile[threadIdx.x * SCAN1_ITEMS + i];
-      s += v[i];
-    }
-    T tot;
-    T ex = block_excl_scan<T, SCAN1_THREADS>(s, &tot) + carry;
-#pragma unroll
-    for (int i = 0; i < SCAN1_ITEMS; ++i) {
-      tile[threadIdx.x * SCAN1_ITEMS + i] = ex;
-      ex += v[i];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < SCAN1_ITEMS; ++i) {
-      const uint64_t j = base + (uint64_t)i * SCAN1_THREADS + threadIdx.x;
-      if (j < n) out[j] = tile[i * SCAN1_THREADS + threadIdx.x];
-    }
-    carry += tot;
-    __syncthreads();
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) wsum[w] = s;
+  __syncthreads();
+  if (w == 0) {
+    const T v = wsum[lane];
+    const T inc = warp_incl_scan(v);
+    wsum[lane] = inc - v;
+    if (lane == 31 && total) *total = inc;
   }
-  if (total && threadIdx.x == 0) *total = carry;
+  __syncthreads();
+  T carry = wsum[w];
+  for (uint64_t b = lo; b < hi; b += 32) {
+    const uint64_t j = b + lane;
+    const T v = j < hi ? in[j] : T(0);
+    const T inc = warp_incl_scan(v);
+    if (j < hi) out[j] = carry + inc - v;
+    carry += __shfl_sync(0xffffffffu, inc, 31);
+  }
 }
 
 template <class T>
