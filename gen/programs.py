@@ -138,7 +138,7 @@ def config1(seed: int = 1, n_templates: int = 400) -> Program:
 # ------------------------------------------------------------------------------------------
 # Config 2: PyTorch ResNet-50 training-shaped (SURVEY §8(d) cfg 2)
 # ------------------------------------------------------------------------------------------
-def _resnet_sites(pool: Pool, rng, local_tag: str | None = None):
+def _resnet_sites(pool: Pool, rng, local_tag: int | None = None):
     """Returns a list of (path, kind-of-op) for one training iteration, program order."""
     prefix = [pool.py("train.py", 212, "main"), pool.py("train.py", 150, "train_epoch"),
               pool.py("train.py", 97, "train_step")]
@@ -239,7 +239,9 @@ def _resnet_sites(pool: Pool, rng, local_tag: str | None = None):
     if local_tag is not None:
         # rank-local frames (data loader / logging): prepended to 5% of the sites
         n_local = max(1, len(sites) // 20)
-        dl = [pool.py(f"dataloader_{local_tag}.py", 31, "fetch"), pool.py(f"logging_{local_tag}.py", 7, "log")]
+        # same file names on every rank (string ids stay consistent across shards), rank-specific
+        # lines: these keys differ between the per-shard dictionaries
+        dl = [pool.py("dataloader.py", 1000 + local_tag, "fetch"), pool.py("logging.py", 2000 + local_tag, "log")]
         for i in range(n_local):
             j = (i * 20 + 3) % len(sites)
             sites[j] = sites[j][:3] + dl + sites[j][3:]
@@ -412,7 +414,7 @@ def config5(shard: int, seed_base: int = 50) -> Program:
     seed = seed_base + shard
     rng = np.random.default_rng(2)  # same program on every rank ...
     pool = Pool()
-    sites = _resnet_sites(pool, rng, local_tag=f"rank{shard}")  # ... plus 5 % rank-local frames
+    sites = _resnet_sites(pool, rng, local_tag=shard)  # ... plus 5 % rank-local frames
     keys, labels, paths = pool.finalize(sites)
     off, frames = _pack_sites(paths)
     n = len(paths)
