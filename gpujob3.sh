@@ -1,7 +1,10 @@
-set -x
-timeout 300 python -u tools/own_modes.py 0 > gpurun_out/modes.log 2>&1
-cat gpurun_out/modes.log | tail -8
-timeout 900 python -u -m pytest tests -m gpu -q -x --timeout 200 --timeout-method thread -p no:cacheprovider --tb=short > gpurun_out/gpu_tests.log 2>&1
-tail -15 gpurun_out/gpu_tests.log
-timeout 900 python -u bench.py --steps 10 --warmup 3 > gpurun_out/bench.log 2>&1
-tail -c 3000 gpurun_out/bench.log
+# new build path: gpu tests + config-4/2/3 bench lines
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/gpu_tests.log
+tail -25 gpurun_out/gpu_tests.log
+timeout 600 python -u bench.py --config 4 --steps 5 --no-cpu --e2e-steps 0 > gpurun_out/bench_cfg4.log 2>&1
+tail -c 1800 gpurun_out/bench_cfg4.log
+timeout 600 python -u bench.py --config 2 --steps 10 --no-cpu --e2e-steps 0 > gpurun_out/bench_cfg2.log 2>&1
+tail -c 1500 gpurun_out/bench_cfg2.log
+timeout 600 python -u bench.py --steps 10 --no-cpu --e2e-steps 0 > gpurun_out/bench_cfg3.log 2>&1
+tail -c 1500 gpurun_out/bench_cfg3.log

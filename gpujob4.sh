@@ -1,2 +1,3 @@
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_modes.csv python -u tools/own_modes.py 0 > gpurun_out/ncu_modes.log 2>&1
-tail -3 gpurun_out/ncu_modes.log
+mkdir -p gpurun_out
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/cfg4_launches.csv python -u bench.py --config 4 --steps 1 --warmup 3 --e2e-steps 0 --no-cpu > gpurun_out/cfg4_launches.log 2>&1
+tail -c 300 gpurun_out/cfg4_launches.log

@@ -11,6 +11,10 @@
 //    keys and a run-length encoding assign node ids base_{d+1} + run, which is exactly the
 //    canonical (depth, lexicographic) order (reading R2). P <= SMALL_P runs entirely inside
 //    one CTA (shared memory, no host round trips); larger P runs one kernel sequence per level.
+#include <stdlib.h>
+
+#include <algorithm>
+
 #include "prim.cuh"
 
 namespace dc {
@@ -20,129 +24,337 @@ constexpr int SB_THREADS = 1024;
 
 __device__ __forceinline__ int bits_for_dev(uint32_t v) { return v ? 32 - __clz(v) : 0; }
 
-// ------------------------------------------------------------------ a2: hash + dedup
-__device__ __forceinline__ uint64_t frame_hash(uint32_t f, uint32_t j) {
-  return mix64(((uint64_t)j << 32 | f) * 0x9E3779B97F4A7C15ull + 0x632BE59BD9B4E019ull);
+// ------------------------------------------------------------------ a2: fused path streaming + exact dedup
+// One pass over the records, in tiles of PT_T consecutive records. A tile's frames are one
+// contiguous range of the frames array; it is staged into shared memory with a TMA bulk copy
+// (cp.async.bulk + mbarrier, double-buffered, the copy of tile k+1 in flight while tile k is
+// processed) together with the tile's offsets. Per tile:
+//   * records are cut into chunks of PT_CH frames (balanced across threads whatever the path
+//     lengths); each chunk adds sum (f+1)*pos[j] into its record's 64-bit path hash
+//     (position-keyed, additive, so chunks combine in any order);
+//   * one thread per record inserts/looks up the finalized hash in an L2-resident table whose
+//     slot carries the representative record (the first inserter) with its offset and length;
+//   * every record whose representative is another record is compared with it frame by frame
+//     (the representative's frames are read through L2; the record's own frames are still in
+//     shared memory), so the dedup is exact: a mismatch (hash collision) makes the record a
+//     representative of its own.
+// The frames are read from HBM exactly once. Tiles whose frames do not fit the stage (very deep
+// paths) or that cannot be staged (unaligned inputs, the array tail) are read from global
+// memory by the same code.
+constexpr int PT_T = 128;           // records per tile
+constexpr int PT_THREADS = 256;
+constexpr uint32_t PT_FW = 8192;    // staged frame window per stage (32 KB)
+constexpr uint32_t PT_CH = 16;      // chunk length (staged tiles)
+constexpr uint32_t PT_CH_G = 128;   // chunk length (global tiles): <= PT_T * 1024 / 128 chunks
+constexpr uint32_t PT_LIST = 1024;  // chunk list capacity (>= PT_FW / PT_CH + PT_T and >= PT_T * 8)
+constexpr uint32_t PT_NONE = 0xFFFFFFFFu;
+
+struct __align__(32) PathSlot {
+  unsigned long long key;  // finalized path hash, ~0 = empty
+  unsigned long long off;  // representative: first frame, length, record index (rep written last)
+  uint32_t len, rep;
+  unsigned long long pad;
+};
+
+struct PathSmem {
+  uint32_t fr[2][PT_FW];
+  unsigned long long offs[2][PT_T + 2];
+  unsigned long long pos[DC_MAX_DEPTH];
+  unsigned long long full[2];
+  unsigned long long meta_f0[2], meta_f1[2];
+  uint32_t meta_mode[2];
+  unsigned long long h[PT_T];
+  unsigned long long rec_o[PT_T];
+  unsigned long long rep_o[PT_T];
+  uint32_t rec_L[PT_T];
+  uint32_t slot[PT_T];
+  uint32_t need[PT_T];  // 0 nothing to compare, 1 compare with the representative, 2 differs
+  uint32_t list[PT_LIST];
+};
+
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 
-__global__ void k_path_hash(const uint64_t* __restrict__ off, const uint32_t* __restrict__ frames, uint64_t R,
-                            uint32_t n_frames, uint64_t* __restrict__ hash, uint32_t* __restrict__ len, uint32_t* d_flags,
-                            unsigned long long* d_diag, uint64_t hash_mask) {
-  const uint32_t lane = lane_id();
-  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  uint32_t maxd = 0, empties = 0, flags = 0;
-  for (uint64_t r = warp; r < R; r += nw) {
-    uint64_t o0 = off[r], o1 = off[r + 1];
-    uint64_t L = o1 >= o0 ? o1 - o0 : 0;
-    if (o1 < o0) flags |= FLAG_BAD_OFFSETS;
-    if (L > DC_MAX_DEPTH) {
-      flags |= FLAG_TOO_DEEP;
-      L = DC_MAX_DEPTH;
-    }
-    uint64_t h = 0;
-    for (uint32_t j = lane; j < L; j += 32) {
-      uint32_t f = frames[o0 + j];
-      if (f >= n_frames) flags |= FLAG_BAD_FRAME;
-      h += frame_hash(f, j);
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
-    if (lane == 0) {
-      h = mix64(h ^ (L * 0xC2B2AE3D27D4EB4Full)) & hash_mask;
-      if (h == ~0ull) h = ~1ull;
-      hash[r] = h;
-      len[r] = (uint32_t)L;
-    }
-    maxd = max(maxd, (uint32_t)L);
-    empties += (L == 0);
+// chunk loop over frames held at src (shared stage or the global array); OP(i, j0, j1, p) gets
+// the record, the position range and the index of the record's first frame in src
+template <class F>
+__device__ __forceinline__ void pt_chunks(const PathSmem& sm, uint32_t n_chunks, uint32_t ch, F op) {
+  for (uint32_t ci = threadIdx.x; ci < n_chunks; ci += PT_THREADS) {
+    const uint32_t e = sm.list[ci];
+    const uint32_t i = e >> 16, j0 = (e & 0xFFFFu) * ch;
+    const uint32_t j1 = min(j0 + ch, sm.rec_L[i]);
+    op(i, j0, j1);
   }
-  flags = __reduce_or_sync(0xffffffffu, flags);  // a bad frame may be seen by any lane
-  if (lane == 0) {
+}
+
+__global__ void __launch_bounds__(PT_THREADS) k_paths(const uint64_t* __restrict__ off, const uint32_t* __restrict__ frames,
+                                                      uint64_t R, uint32_t n_frames, PathSlot* __restrict__ tab, uint64_t mask,
+                                                      uint32_t* __restrict__ slot_of_rec, uint32_t* __restrict__ extra_rec,
+                                                      unsigned int* __restrict__ d_cnt, uint32_t* d_flags,
+                                                      unsigned long long* d_diag, uint64_t hash_mask, int tma_ok) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PathSmem& sm = *reinterpret_cast<PathSmem*>(smem_raw);
+  const uint32_t tid = threadIdx.x;
+  const uint64_t n_tiles = (R + PT_T - 1) / PT_T, G = gridDim.x;
+  for (uint32_t j = tid; j < DC_MAX_DEPTH; j += PT_THREADS) sm.pos[j] = mix64(0x9E3779B97F4A7C15ull * (j + 1)) | 1ull;
+  if (tid == 0) {
+    mbar_init(&sm.full[0], 1);
+    mbar_init(&sm.full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t flags = 0, maxd = 0, empties = 0;
+  // ---- producer (thread 0): stage tile t into buffer s; F0/F1 = first/end frame of the tile
+  const uint64_t Ftot = tid == 0 ? off[R] : 0;
+  auto issue = [&](uint64_t t, int s, uint64_t F0, uint64_t F1) {
+    const uint64_t r0 = t * PT_T;
+    uint32_t mode = 0, bytes = 0;
+    const uint64_t a = F0 & ~3ull, b = (F1 + 3) & ~3ull;
+    if (tma_ok && F1 >= F0 && b - a <= PT_FW && b <= Ftot) {
+      mode |= 1;
+      bytes += (uint32_t)(b - a) * 4u;
+    }
+    if (tma_ok && r0 + PT_T + 2 <= R + 1) {
+      mode |= 2;
+      bytes += (PT_T + 2) * 8u;
+    }
+    sm.meta_f0[s] = F0;
+    sm.meta_f1[s] = F1;
+    sm.meta_mode[s] = mode;
+    if (bytes) {
+      mbar_expect_tx(&sm.full[s], bytes);
+      if ((mode & 1) && b > a) tma_bulk_g2s(sm.fr[s], frames + a, (uint32_t)(b - a) * 4u, &sm.full[s]);
+      if (mode & 2) tma_bulk_g2s(sm.offs[s], off + r0, (PT_T + 2) * 8u, &sm.full[s]);
+    } else {
+      mbar_arrive(&sm.full[s]);
+    }
+  };
+  uint64_t t = blockIdx.x, nf0 = 0, nf1 = 0;
+  if (tid == 0) {
+    if (t < n_tiles) issue(t, 0, off[t * PT_T], off[min(R, t * PT_T + PT_T)]);
+    if (t + G < n_tiles) {
+      nf0 = off[(t + G) * PT_T];
+      nf1 = off[min(R, (t + G) * PT_T + PT_T)];
+    }
+  }
+  for (uint32_t k = 0; t < n_tiles; ++k, t += G) {
+    const int s = k & 1;
+    if (tid == 0) {
+      if (t + G < n_tiles) issue(t + G, s ^ 1, nf0, nf1);  // offsets loaded one tile ago
+      const uint64_t t2 = t + 2 * G;
+      if (t2 < n_tiles) {
+        nf0 = off[t2 * PT_T];
+        nf1 = off[min(R, t2 * PT_T + PT_T)];
+      }
+    }
+    mbar_wait(&sm.full[s], (k >> 1) & 1u);
+    const uint64_t r0 = t * PT_T;
+    const uint32_t n = (uint32_t)min((uint64_t)PT_T, R - r0);
+    const uint32_t mode = sm.meta_mode[s];
+    const bool staged = mode & 1;
+    const uint64_t F0 = sm.meta_f0[s], F1 = sm.meta_f1[s], a = F0 & ~3ull;
+    const uint32_t ch = staged ? PT_CH : PT_CH_G;
+    // ---- per record: bounds, length, chunk list
+    uint32_t c = 0, L = 0;
+    uint64_t o = 0;
+    if (tid < n) {
+      uint64_t o0, o1;
+      if (mode & 2) {
+        o0 = sm.offs[s][tid];
+        o1 = sm.offs[s][tid + 1];
+      } else {
+        o0 = off[r0 + tid];
+        o1 = off[r0 + tid + 1];
+      }
+      uint64_t LL = o1 >= o0 ? o1 - o0 : 0;
+      if (o1 < o0) flags |= FLAG_BAD_OFFSETS;
+      if (LL > DC_MAX_DEPTH) {
+        flags |= FLAG_TOO_DEEP;
+        LL = DC_MAX_DEPTH;
+      }
+      // frames outside the staged window / the array: malformed offsets (never read)
+      if (LL && (staged ? (o0 < F0 || o0 + LL > F1) : (o0 + LL > off[R]))) {
+        flags |= FLAG_BAD_OFFSETS;
+        LL = 0;
+      }
+      o = o0;
+      L = (uint32_t)LL;
+      c = (L + ch - 1) / ch;
+      maxd = max(maxd, L);
+      empties += L == 0;
+    }
+    uint32_t n_chunks;
+    const uint32_t cs = block_excl_scan<uint32_t, PT_THREADS>(c, &n_chunks);
+    if (tid < n) {
+      sm.h[tid] = 0;
+      sm.rec_o[tid] = o;
+      sm.rec_L[tid] = L;
+      for (uint32_t j = 0; j < c; ++j) sm.list[cs + j] = tid << 16 | j;
+    }
+    __syncthreads();
+    // ---- path hashes (and frame-id validation)
+    uint32_t bad = 0;
+    if (staged) {
+      pt_chunks(sm, n_chunks, ch, [&](uint32_t i, uint32_t j0, uint32_t j1) {
+        const uint32_t* src = sm.fr[s] + (sm.rec_o[i] - a);
+        unsigned long long acc = 0;
+        for (uint32_t j = j0; j < j1; ++j) {
+          const uint32_t f = src[j];
+          bad |= f >= n_frames;
+          acc += ((unsigned long long)f + 1ull) * sm.pos[j];
+        }
+        atomicAdd(&sm.h[i], acc);
+      });
+    } else {
+      pt_chunks(sm, n_chunks, ch, [&](uint32_t i, uint32_t j0, uint32_t j1) {
+        const uint32_t* src = frames + sm.rec_o[i];
+        unsigned long long acc = 0;
+        for (uint32_t j = j0; j < j1; ++j) {
+          const uint32_t f = __ldg(src + j);
+          bad |= f >= n_frames;
+          acc += ((unsigned long long)f + 1ull) * sm.pos[j];
+        }
+        atomicAdd(&sm.h[i], acc);
+      });
+    }
+    if (bad) flags |= FLAG_BAD_FRAME;
+    __syncthreads();
+    // ---- table: insert or find; the inserter publishes its record as the representative
+    uint32_t sl = PT_NONE;
+    bool mine = false;
+    if (tid < n) {
+      uint64_t H = mix64(sm.h[tid] ^ ((uint64_t)L * 0xC2B2AE3D27D4EB4Full)) & hash_mask;
+      if (H == ~0ull) H = ~1ull;
+      uint64_t q = (H * 0x9E3779B97F4A7C15ull >> 17) & mask;
+      for (uint64_t probe = 0; probe <= mask; ++probe, q = (q + 1) & mask) {
+        const unsigned long long cur = ld_relaxed_u64(&tab[q].key);
+        if (cur == H) {
+          sl = (uint32_t)q;
+          break;
+        }
+        if (cur == ~0ull) {
+          const unsigned long long old = atomicCAS(&tab[q].key, ~0ull, (unsigned long long)H);
+          if (old == ~0ull) {
+            sl = (uint32_t)q;
+            mine = true;
+            break;
+          }
+          if (old == H) {
+            sl = (uint32_t)q;
+            break;
+          }
+        }
+      }
+      if (mine) {
+        tab[sl].off = o;
+        tab[sl].len = L;
+        st_release_u32(&tab[sl].rep, (uint32_t)(r0 + tid));
+        const unsigned ins = atomicAdd(d_cnt, 1u);
+        if ((uint64_t)ins * 2 >= mask) atomicOr(d_cnt + 3, 1u);  // past half load: retry larger
+      }
+      if (sl == PT_NONE) atomicOr(d_cnt + 3, 1u);  // table full
+    }
+    __syncthreads();  // this CTA's representatives are published
+    if (tid < n) {
+      uint32_t need = 0;
+      if (sl != PT_NONE && !mine) {
+        while (ld_acquire_u32(&tab[sl].rep) == PT_NONE) {
+        }
+        const uint64_t ro = tab[sl].off;
+        const uint32_t rl = tab[sl].len;
+        need = rl != L ? 2u : (L ? 1u : 0u);
+        sm.rep_o[tid] = ro;
+      }
+      sm.need[tid] = need;
+      sm.slot[tid] = sl;
+    }
+    __syncthreads();
+    // ---- exact verification against the representative
+    if (staged) {
+      pt_chunks(sm, n_chunks, ch, [&](uint32_t i, uint32_t j0, uint32_t j1) {
+        if (sm.need[i] != 1u) return;
+        const uint32_t* src = sm.fr[s] + (sm.rec_o[i] - a);
+        const uint32_t* rep = frames + sm.rep_o[i];
+        bool diff = false;
+        for (uint32_t j = j0; j < j1; ++j) diff |= src[j] != __ldg(rep + j);
+        if (diff) sm.need[i] = 2u;
+      });
+    } else {
+      pt_chunks(sm, n_chunks, ch, [&](uint32_t i, uint32_t j0, uint32_t j1) {
+        if (sm.need[i] != 1u) return;
+        const uint32_t* src = frames + sm.rec_o[i];
+        const uint32_t* rep = frames + sm.rep_o[i];
+        bool diff = false;
+        for (uint32_t j = j0; j < j1; ++j) diff |= __ldg(src + j) != __ldg(rep + j);
+        if (diff) sm.need[i] = 2u;
+      });
+    }
+    __syncthreads();
+    if (tid < n) {
+      uint32_t out = sm.slot[tid];
+      if (sm.need[tid] == 2u) {  // collision: a representative of its own
+        const unsigned e = atomicAdd(d_cnt + 1, 1u);
+        extra_rec[e] = (uint32_t)(r0 + tid);
+        const uint64_t v = mask + 1 + (uint64_t)e;
+        if (v >= PT_NONE) atomicOr(d_cnt + 3, 2u);
+        out = (uint32_t)v;
+      }
+      if (out == PT_NONE) out = 0;  // overflow: the host retries
+      slot_of_rec[r0 + tid] = out;
+    }
+    __syncthreads();  // stage s and the per-record arrays are free
+  }
+  // ---- diag / flags, one atomic per warp
+  flags = __reduce_or_sync(0xffffffffu, flags);
+  maxd = __reduce_max_sync(0xffffffffu, maxd);
+  empties = __reduce_add_sync(0xffffffffu, empties);
+  if (lane_id() == 0) {
     if (maxd) atomicMax(&d_diag[DG_MAXDEPTH], (unsigned long long)maxd);
-    if (empties) atomicAdd(&d_diag[DG_EMPTY], (unsigned long long)empties);
+    if (empties) atomicAdd(d_cnt + 4, empties);  // added to the diag once (k_items_finish), not per retry
     if (flags) atomicOr(d_flags, flags);
   }
 }
 
-__global__ void k_path_insert(const uint64_t* __restrict__ hash, uint64_t R, unsigned long long* htab, uint32_t* rtab,
-                              uint64_t mask, uint32_t* __restrict__ slot_of_rec, unsigned int* d_count) {
-  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < R; r += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t h = hash[r];
-    uint64_t s = (h * 0x9E3779B97F4A7C15ull >> 17) & mask;
-    bool found = false;
-    for (uint64_t probe = 0; probe <= mask; ++probe, s = (s + 1) & mask) {
-      unsigned long long cur = ld_relaxed_u64(htab + s);
-      if (cur == h) { found = true; break; }
-      if (cur == ~0ull) {
-        unsigned long long old = atomicCAS(htab + s, ~0ull, (unsigned long long)h);
-        if (old == ~0ull) {
-          atomicAdd(d_count, 1u);
-          found = true;
-          break;
-        }
-        if (old == h) { found = true; break; }
-      }
-    }
-    if (!found) {  // table full: the host retries with a larger table
-      atomicOr(d_count + 3, 1u);
-      slot_of_rec[r] = 0;
-      continue;
-    }
-    atomicMin(rtab + s, (uint32_t)r);
-    slot_of_rec[r] = (uint32_t)s;
-  }
-}
-
-// exact verification: warp per record against its representative
-__global__ void k_path_verify(const uint64_t* __restrict__ off, const uint32_t* __restrict__ frames,
-                              const uint32_t* __restrict__ len, uint64_t R, const uint32_t* __restrict__ rtab,
-                              uint32_t* __restrict__ slot_of_rec, uint32_t* __restrict__ extra_rec, unsigned int* d_extra,
-                              uint64_t cap) {
-  const uint32_t lane = lane_id();
-  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t r = warp; r < R; r += nw) {
-    uint32_t s = slot_of_rec[r];
-    uint32_t rep = rtab[s];
-    if (rep == (uint32_t)r) continue;
-    uint32_t L = len[r];
-    bool diff = len[rep] != L;
-    if (!diff) {
-      const uint32_t* a = frames + off[r];
-      const uint32_t* b = frames + off[rep];
-      for (uint32_t j = lane; j < L; j += 32)
-        if (a[j] != b[j]) diff = true;
-      diff = __any_sync(0xffffffffu, diff);
-    }
-    if (diff && lane == 0) {  // collision: r becomes a representative of its own
-      unsigned e = atomicAdd(d_extra, 1u);
-      extra_rec[e] = (uint32_t)r;
-      slot_of_rec[r] = (uint32_t)(cap + e);
-    }
-  }
-}
-
-__global__ void k_path_compact(const unsigned long long* __restrict__ htab, const uint32_t* __restrict__ rtab, uint64_t cap,
-                               uint32_t* __restrict__ pid_of_slot, uint32_t* __restrict__ item_rec, unsigned int* d_pos) {
+// representatives in table-slot order: item ids, their record and path length
+__global__ void k_path_compact(const PathSlot* __restrict__ tab, uint64_t cap, uint32_t* __restrict__ pid_of_slot,
+                               uint32_t* __restrict__ item_rec, uint32_t* __restrict__ item_len, unsigned int* d_pos) {
   for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < cap; s += (uint64_t)gridDim.x * blockDim.x) {
-    if (htab[s] == ~0ull) continue;
+    if (tab[s].key == ~0ull) continue;
     unsigned p = atomicAdd(d_pos, 1u);
     pid_of_slot[s] = p;
-    item_rec[p] = rtab[s];
+    item_rec[p] = tab[s].rep;
+    item_len[p] = tab[s].len;
   }
 }
 
 __global__ void k_items_finish(uint32_t* __restrict__ item_rec, const uint32_t* __restrict__ extra_rec, uint32_t P0,
-                               uint32_t n_extra, const uint32_t* __restrict__ len, uint32_t* __restrict__ item_len,
-                               unsigned long long* d_sumlen) {
+                               uint32_t n_extra, const uint64_t* __restrict__ off, uint32_t* __restrict__ item_len,
+                               unsigned long long* d_sumlen, const unsigned int* d_cnt, unsigned long long* d_diag) {
   uint32_t P = P0 + n_extra;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && d_cnt[4]) atomicAdd(&d_diag[DG_EMPTY], (unsigned long long)d_cnt[4]);
   unsigned long long acc = 0;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += gridDim.x * blockDim.x) {
-    if (i >= P0) item_rec[i] = extra_rec[i - P0];
-    uint32_t L = len[item_rec[i]];
-    item_len[i] = L;
-    acc += L;
+    if (i >= P0) {  // collision extras: length from the offsets (validated by k_paths)
+      const uint32_t r = extra_rec[i - P0];
+      item_rec[i] = r;
+      const uint64_t o0 = off[r], o1 = off[r + 1];
+      item_len[i] = (uint32_t)(o1 >= o0 ? min(o1 - o0, (uint64_t)DC_MAX_DEPTH) : 0);
+    }
+    acc += item_len[i];
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -442,6 +654,314 @@ static dc_status build_large(Ctx* c, const dc_paths* p, const uint32_t* item_rec
   return DC_OK;
 }
 
+// ------------------------------------------------------------------ a3: large P, Euler tour
+// Canonical numbering without a per-level loop (depth up to DC_MAX_DEPTH):
+//  1. every prefix of every distinct path is inserted into a node hash table keyed by a
+//     position-keyed prefix hash (warp per path, warp scan of the frame terms); a slot carries
+//     (parent slot, frame). An existing key must carry the same (parent slot, frame): a
+//     mismatch is a hash collision and is detected exactly (by induction from the root, equal
+//     keys with equal (parent, frame) are equal prefixes) — the caller then falls back to the
+//     level-wise build;
+//  2. nodes are sorted by (parent, frame): siblings contiguous in frame order;
+//  3. an Euler tour over first-child / next-sibling links is ranked by pointer jumping: the
+//     number of "down" steps before a node is its DFS preorder with children in frame order,
+//     i.e. its rank in the lexicographic order of paths;
+//  4. sorting by (depth, preorder) gives the canonical (depth, lexicographic) ids (reading R2).
+struct __align__(16) NodeSlot {
+  unsigned long long key;  // prefix hash, ~0 = empty
+  unsigned long long pay;  // parent slot << 32 | frame; ~0 until published
+};
+constexpr uint32_t NS_ROOT = 0xFFFFFFFEu;  // parent slot of depth-1 nodes
+
+__device__ __forceinline__ unsigned long long node_pos(uint32_t j) { return mix64(0xD1B54A32D192ED03ull * (j + 1)) | 1ull; }
+
+__global__ void k_prefix_nodes(const uint64_t* __restrict__ off, const uint32_t* __restrict__ frames,
+                               const uint32_t* __restrict__ item_rec, const uint32_t* __restrict__ item_len, uint32_t P,
+                               NodeSlot* __restrict__ tab, uint64_t mask, uint16_t* __restrict__ sdepth,
+                               uint32_t* __restrict__ leaf_slot, unsigned int* d_cnt, uint64_t hmask) {
+  const uint32_t lane = lane_id();
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t p = warp; p < P; p += nw) {
+    const uint32_t L = item_len[p];
+    if (L == 0) {
+      if (lane == 0) leaf_slot[p] = PT_NONE;  // empty path: the root
+      continue;
+    }
+    const uint64_t base = off[item_rec[p]];
+    unsigned long long carry = 0;
+    uint32_t parent = NS_ROOT, last = PT_NONE;
+    for (uint32_t j0 = 0; j0 < L; j0 += 32) {
+      const uint32_t j = j0 + lane;
+      const bool act = j < L;
+      const uint32_t f = act ? frames[base + j] : 0u;
+      const unsigned long long g = act ? ((unsigned long long)f + 1ull) * node_pos(j) : 0ull;
+      const unsigned long long incl = warp_incl_scan<unsigned long long>(g) + carry;
+      uint64_t H = mix64(incl ^ ((uint64_t)(j + 1) * 0xC2B2AE3D27D4EB4Full)) & hmask;
+      if (H == ~0ull) H = ~1ull;
+      uint32_t sl = PT_NONE;
+      bool mine = false;
+      if (act) {
+        uint64_t q = (H * 0x9E3779B97F4A7C15ull >> 17) & mask;
+        for (uint64_t probe = 0; probe <= mask; ++probe, q = (q + 1) & mask) {
+          const unsigned long long cur = ld_relaxed_u64(&tab[q].key);
+          if (cur == H) {
+            sl = (uint32_t)q;
+            break;
+          }
+          if (cur == ~0ull) {
+            const unsigned long long old = atomicCAS(&tab[q].key, ~0ull, (unsigned long long)H);
+            if (old == ~0ull) {
+              sl = (uint32_t)q;
+              mine = true;
+              break;
+            }
+            if (old == H) {
+              sl = (uint32_t)q;
+              break;
+            }
+          }
+        }
+      }
+      uint32_t ps = __shfl_up_sync(0xffffffffu, sl, 1);
+      if (lane == 0) ps = parent;
+      const unsigned long long pay = (unsigned long long)ps << 32 | f;
+      if (act && mine) {
+        sdepth[sl] = (uint16_t)(j + 1);
+        st_release_u64(&tab[sl].pay, pay);
+        const unsigned ins = atomicAdd(d_cnt, 1u);
+        if ((uint64_t)ins * 2 >= mask) atomicOr(d_cnt + 1, 1u);  // past half load: retry larger
+      }
+      if (act && sl == PT_NONE) atomicOr(d_cnt + 1, 1u);
+      __syncwarp();
+      if (act && !mine && sl != PT_NONE) {
+        unsigned long long pp;
+        while ((pp = ld_acquire_u64(&tab[sl].pay)) == ~0ull) {
+        }
+        if (pp != pay) atomicOr(d_cnt + 2, 1u);  // same key, different (parent, frame): collision
+      }
+      carry = __shfl_sync(0xffffffffu, incl, 31);
+      parent = __shfl_sync(0xffffffffu, sl, 31);
+      last = __shfl_sync(0xffffffffu, sl, (L - 1 - j0) & 31u);
+    }
+    if (lane == 0) leaf_slot[p] = last;
+  }
+}
+
+__global__ void k_node_compact(const NodeSlot* __restrict__ tab, uint64_t cap, uint32_t* __restrict__ nslot,
+                               uint32_t* __restrict__ nidx, unsigned int* d_pos) {
+  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < cap; s += (uint64_t)gridDim.x * blockDim.x) {
+    if (tab[s].key == ~0ull) continue;
+    const unsigned n = atomicAdd(d_pos, 1u);
+    nslot[n] = (uint32_t)s;
+    nidx[s] = n;
+  }
+}
+
+// node fields (root = index Nn) and the sibling sort key (parent + 1, frame)
+__global__ void k_node_fields(uint32_t Nn, const uint32_t* __restrict__ nslot, const uint32_t* __restrict__ nidx,
+                              const NodeSlot* __restrict__ tab, const uint16_t* __restrict__ sdepth, int fbits,
+                              uint32_t* __restrict__ par, uint32_t* __restrict__ frm, uint16_t* __restrict__ dep,
+                              uint64_t* __restrict__ skey, uint32_t* __restrict__ sval) {
+  for (uint32_t n = blockIdx.x * blockDim.x + threadIdx.x; n < Nn; n += gridDim.x * blockDim.x) {
+    const uint32_t s = nslot[n];
+    const unsigned long long pay = tab[s].pay;
+    const uint32_t ps = (uint32_t)(pay >> 32), f = (uint32_t)pay;
+    const uint32_t pn = ps == NS_ROOT ? Nn : nidx[ps];
+    par[n] = pn;
+    frm[n] = f;
+    dep[n] = sdepth[s];
+    skey[n] = ((uint64_t)(ps == NS_ROOT ? 0u : pn + 1u) << fbits) | f;
+    sval[n] = n;
+  }
+}
+
+__global__ void k_euler_links(uint32_t Nn, const uint64_t* __restrict__ ks, const uint32_t* __restrict__ vs, int fbits,
+                              uint32_t* __restrict__ first_child, uint32_t* __restrict__ next_sib) {
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < Nn; k += gridDim.x * blockDim.x) {
+    const uint32_t n = vs[k];
+    const uint64_t g = ks[k] >> fbits;
+    if (k == 0 || (ks[k - 1] >> fbits) != g) first_child[g == 0 ? Nn : (uint32_t)(g - 1)] = n;
+    next_sib[n] = (k + 1 < Nn && (ks[k + 1] >> fbits) == g) ? vs[k + 1] : PT_NONE;
+  }
+}
+
+// tour elements: down(n) = n, up(n) = Nn + 1 + n (n <= Nn, root = Nn); packed (next << 32 | weight)
+__global__ void k_euler_init(uint32_t Nn, const uint32_t* __restrict__ par, const uint32_t* __restrict__ first_child,
+                             const uint32_t* __restrict__ next_sib, unsigned long long* __restrict__ tour) {
+  const uint64_t M = 2ull * (Nn + 1);
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < M; x += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t nx, w;
+    if (x <= Nn) {
+      const uint32_t fc = first_child[x];
+      nx = fc != PT_NONE ? fc : (uint32_t)(Nn + 1 + x);
+      w = 1;
+    } else {
+      const uint32_t n = (uint32_t)(x - (Nn + 1));
+      if (n == Nn) {
+        nx = PT_NONE;
+      } else {
+        const uint32_t ns = next_sib[n];
+        nx = ns != PT_NONE ? ns : Nn + 1 + par[n];
+      }
+      w = 0;
+    }
+    tour[x] = (unsigned long long)nx << 32 | w;
+  }
+}
+
+// one pointer-jumping round: suffix weight sums along the tour
+__global__ void k_wyllie(uint64_t M, const unsigned long long* __restrict__ in, unsigned long long* __restrict__ out) {
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < M; x += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long e = in[x];
+    const uint32_t nx = (uint32_t)(e >> 32);
+    if (nx == PT_NONE) {
+      out[x] = e;
+    } else {
+      const unsigned long long f = in[nx];
+      out[x] = (f & 0xFFFFFFFF00000000ull) | (uint32_t)((uint32_t)e + (uint32_t)f);
+    }
+  }
+}
+
+__global__ void k_canon_keys(uint32_t Nn, const uint16_t* __restrict__ dep, const unsigned long long* __restrict__ tour,
+                             int pbits, uint64_t* __restrict__ ck, uint32_t* __restrict__ cv) {
+  for (uint32_t n = blockIdx.x * blockDim.x + threadIdx.x; n < Nn; n += gridDim.x * blockDim.x) {
+    const uint32_t pre = (Nn + 1) - (uint32_t)tour[n];  // down steps before down(n)
+    ck[n] = ((uint64_t)dep[n] << pbits) | pre;
+    cv[n] = n;
+  }
+}
+
+__global__ void k_canon_ids(uint32_t Nn, const uint32_t* __restrict__ cv, uint32_t* __restrict__ canon) {
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < Nn; k += gridDim.x * blockDim.x) canon[cv[k]] = k + 1;
+}
+
+__global__ void k_canon_write(uint32_t Nn, const uint64_t* __restrict__ ck, const uint32_t* __restrict__ cv, int pbits,
+                              const uint32_t* __restrict__ par, const uint32_t* __restrict__ frm,
+                              const uint32_t* __restrict__ canon, uint32_t* __restrict__ parent, uint32_t* __restrict__ frame_out,
+                              uint16_t* __restrict__ depth, uint32_t* __restrict__ level_off, uint32_t Lmax) {
+  const uint64_t gid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (gid == 0) {
+    parent[0] = DC_NO_NODE;
+    frame_out[0] = DC_NO_NODE;
+    depth[0] = 0;
+    level_off[0] = 0;
+    if (Nn == 0)
+      for (uint32_t d = 1; d <= Lmax + 1; ++d) level_off[d] = 1;
+  }
+  for (uint32_t k = (uint32_t)gid; k < Nn; k += gridDim.x * blockDim.x) {
+    const uint32_t n = cv[k], id = k + 1;
+    const uint32_t pn = par[n];
+    parent[id] = pn == Nn ? 0u : canon[pn];
+    frame_out[id] = frm[n];
+    const uint32_t d = (uint32_t)(ck[k] >> pbits);
+    depth[id] = (uint16_t)d;
+    if (k == 0 || (uint32_t)(ck[k - 1] >> pbits) != d) level_off[d] = id;
+    if (k == Nn - 1)
+      for (uint32_t dd = d + 1; dd <= Lmax + 1; ++dd) level_off[dd] = Nn + 1;
+  }
+}
+
+__global__ void k_item_leaf(uint32_t P, const uint32_t* __restrict__ leaf_slot, const uint32_t* __restrict__ nidx,
+                            const uint32_t* __restrict__ canon, uint32_t* __restrict__ leaf_of_item) {
+  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < P; p += gridDim.x * blockDim.x) {
+    const uint32_t ls = leaf_slot[p];
+    leaf_of_item[p] = ls == PT_NONE ? 0u : canon[nidx[ls]];
+  }
+}
+
+// returns *collided = true (and builds nothing) when a prefix-hash collision was detected
+static dc_status build_euler(Ctx* c, const dc_paths* p, const uint32_t* item_rec, const uint32_t* item_len, uint32_t P,
+                             uint64_t sumlen, uint32_t Lmax, int fbits, dc_cct* t, uint32_t* leaf_of_item, uint64_t* h_N,
+                             bool* collided) {
+  *collided = false;
+  Buf<NodeSlot> tab;
+  Buf<uint16_t> sdepth;
+  Buf<uint32_t> leaf_slot;
+  Buf<unsigned int> cnt;
+  DC_TRY(alloc(c, leaf_slot, P));
+  const uint64_t want = std::min<uint64_t>(sumlen + 1, 8ull * P + 1024);
+  uint64_t cap = 1024;
+  while (cap < 2 * want) cap <<= 1;
+  uint32_t hc[4];
+  for (int attempt = 0;; ++attempt) {
+    DC_TRY(alloc(c, tab, cap));
+    DC_TRY(alloc(c, sdepth, cap));
+    DC_CUDA(c, cudaMemsetAsync(tab.p, 0xFF, cap * sizeof(NodeSlot), c->stream));
+    DC_TRY(alloc_zero(c, cnt, 4));  // [0] nodes, [1] overflow, [2] collision, [3] compact pos
+    k_prefix_nodes<<<grid_for(c, (uint64_t)P * 32, 256), 256, 0, c->stream>>>(p->offsets, p->frames, item_rec, item_len, P, tab.p,
+                                                                              cap - 1, sdepth.p, leaf_slot.p, cnt.p,
+                                                                              c->node_mask);
+    DC_LAUNCHED(c);
+    DC_TRY(readback(c, cnt.p, 16, hc));
+    if (hc[2]) {
+      *collided = true;
+      return DC_OK;
+    }
+    if (!hc[1]) break;
+    uint64_t big = 1024;
+    while (big < 2 * (sumlen + 1)) big <<= 1;
+    if (attempt || big <= cap || big > (1ull << 31)) return fail(c, DC_ERR_CAPACITY, "dc_cct_build: node table overflow");
+    cap = big;
+  }
+  const uint32_t Nn = hc[0];  // nodes without the root
+  Buf<uint32_t> nslot, nidx, par, frm, sv0, sv1, first_child, next_sib, canon;
+  Buf<uint16_t> dep;
+  Buf<uint64_t> sk0, sk1;
+  Buf<unsigned long long> tour0, tour1;
+  DC_TRY(alloc(c, nslot, Nn));
+  DC_TRY(alloc(c, nidx, cap));
+  DC_TRY(alloc(c, par, Nn));
+  DC_TRY(alloc(c, frm, Nn));
+  DC_TRY(alloc(c, dep, Nn));
+  DC_TRY(alloc(c, sk0, Nn));
+  DC_TRY(alloc(c, sk1, Nn));
+  DC_TRY(alloc(c, sv0, Nn));
+  DC_TRY(alloc(c, sv1, Nn));
+  DC_TRY(alloc(c, first_child, (uint64_t)Nn + 1));
+  DC_TRY(alloc(c, next_sib, Nn));
+  DC_TRY(alloc(c, canon, Nn));
+  const uint64_t M = 2ull * (Nn + 1);
+  DC_TRY(alloc(c, tour0, M));
+  DC_TRY(alloc(c, tour1, M));
+  k_node_compact<<<grid_for(c, cap, 256), 256, 0, c->stream>>>(tab.p, cap, nslot.p, nidx.p, cnt.p + 3);
+  DC_LAUNCHED(c);
+  k_node_fields<<<grid_for(c, Nn, 256), 256, 0, c->stream>>>(Nn, nslot.p, nidx.p, tab.p, sdepth.p, fbits, par.p, frm.p, dep.p,
+                                                            sk0.p, sv0.p);
+  DC_LAUNCHED(c);
+  bool in1 = false;
+  DC_TRY(radix_sort_pairs(c, sk0.p, sv0.p, sk1.p, sv1.p, Nn, 0, fbits + bits_for((uint64_t)Nn + 1), &in1));
+  const uint64_t* ks = in1 ? sk1.p : sk0.p;
+  const uint32_t* vs = in1 ? sv1.p : sv0.p;
+  DC_CUDA(c, cudaMemsetAsync(first_child.p, 0xFF, ((uint64_t)Nn + 1) * 4, c->stream));
+  k_euler_links<<<grid_for(c, Nn, 256), 256, 0, c->stream>>>(Nn, ks, vs, fbits, first_child.p, next_sib.p);
+  DC_LAUNCHED(c);
+  k_euler_init<<<grid_for(c, M, 256), 256, 0, c->stream>>>(Nn, par.p, first_child.p, next_sib.p, tour0.p);
+  DC_LAUNCHED(c);
+  unsigned long long *tin = tour0.p, *tout = tour1.p;
+  for (uint64_t span = 1; span < M; span <<= 1) {
+    k_wyllie<<<grid_for(c, M, 256), 256, 0, c->stream>>>(M, tin, tout);
+    DC_LAUNCHED(c);
+    std::swap(tin, tout);
+  }
+  const int pbits = bits_for((uint64_t)Nn + 1);
+  k_canon_keys<<<grid_for(c, Nn, 256), 256, 0, c->stream>>>(Nn, dep.p, tin, pbits, sk0.p, sv0.p);
+  DC_LAUNCHED(c);
+  DC_TRY(radix_sort_pairs(c, sk0.p, sv0.p, sk1.p, sv1.p, Nn, 0, pbits + bits_for(Lmax), &in1));
+  const uint64_t* cks = in1 ? sk1.p : sk0.p;
+  const uint32_t* cvs = in1 ? sv1.p : sv0.p;
+  k_canon_ids<<<grid_for(c, Nn, 256), 256, 0, c->stream>>>(Nn, cvs, canon.p);
+  DC_LAUNCHED(c);
+  k_canon_write<<<grid_for(c, Nn ? Nn : 1, 256), 256, 0, c->stream>>>(Nn, cks, cvs, pbits, par.p, frm.p, canon.p, t->parent,
+                                                                    t->frame, t->depth, t->level_off, Lmax);
+  DC_LAUNCHED(c);
+  k_item_leaf<<<grid_for(c, P, 256), 256, 0, c->stream>>>(P, leaf_slot.p, nidx.p, canon.p, leaf_of_item);
+  DC_LAUNCHED(c);
+  *h_N = (uint64_t)Nn + 1;
+  return DC_OK;
+}
+
 dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_frames, uint32_t* out_leaf, dc_cct** out) {
   *out = nullptr;
   const uint64_t R = p->n_records;
@@ -455,52 +975,53 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
     DC_TRY(palloc(c, t->frame_kind, n_frames));
     DC_CUDA(c, cudaMemcpyAsync(t->frame_kind, dict->kinds, n_frames, cudaMemcpyDeviceToDevice, c->stream));
   }
-  // ---- a2: hash, group, verify
-  Buf<uint64_t> hash;
-  Buf<uint32_t> len, slot_of_rec, rtab, extra_rec, pid_of_slot, item_rec, item_len, leaf_of_item, leafbuf;
-  Buf<unsigned long long> htab, sumlen;
+  // ---- a2: one fused pass: hash, group, verify exactly (k_paths)
+  Buf<uint32_t> slot_of_rec, extra_rec, pid_of_slot, item_rec, item_len, leaf_of_item, leafbuf;
+  Buf<PathSlot> tab;
+  Buf<unsigned long long> sumlen;
   Buf<unsigned int> cnt;
-  DC_TRY(alloc(c, hash, R));
-  DC_TRY(alloc(c, len, R));
   DC_TRY(alloc(c, slot_of_rec, R));
-  k_path_hash<<<grid_for(c, R * 32, 256), 256, 0, c->stream>>>(p->offsets, p->frames, R, n_frames, hash.p, len.p,
-                                                                c->d_flags, (unsigned long long*)c->d_diag, c->hash_mask);
-  DC_LAUNCHED(c);
-  // path table sized for the distinct paths, not the records (retry once if it fills up)
-  uint64_t cap = 1024;
-  while (cap < 2 * (R < (1ull << 20) ? R : (1ull << 20))) cap <<= 1;
-  for (int attempt = 0;; ++attempt) {
-    DC_TRY(alloc(c, htab, cap));
-    DC_TRY(alloc(c, rtab, cap));
-    DC_CUDA(c, cudaMemsetAsync(htab.p, 0xFF, cap * 8, c->stream));
-    DC_CUDA(c, cudaMemsetAsync(rtab.p, 0xFF, cap * 4, c->stream));
-    DC_TRY(alloc_zero(c, cnt, 4));  // [0] distinct, [1] extra, [2] compact pos, [3] overflow
-    k_path_insert<<<grid_for(c, R, 256), 256, 0, c->stream>>>(hash.p, R, htab.p, rtab.p, cap - 1, slot_of_rec.p, cnt.p);
-    DC_LAUNCHED(c);
-    uint32_t hcnt[4];
-    DC_TRY(readback(c, cnt.p, 16, hcnt));
-    if (!hcnt[3] && (uint64_t)hcnt[0] * 2 <= cap) break;
-    if (attempt || cap >= (1ull << 31)) return fail(c, DC_ERR_CAPACITY, "dc_cct_build: path table overflow");
-    cap = 1024;
-    while (cap < 2 * R) cap <<= 1;
-    if (cap > (1ull << 31)) cap = 1ull << 31;
-  }
   DC_TRY(alloc(c, extra_rec, R));
-  k_path_verify<<<grid_for(c, R * 32, 256), 256, 0, c->stream>>>(p->offsets, p->frames, len.p, R, rtab.p, slot_of_rec.p,
-                                                                  extra_rec.p, cnt.p + 1, cap);
-  DC_LAUNCHED(c);
+  const int tma_ok = ((uintptr_t)p->offsets % 16 == 0) && ((uintptr_t)p->frames % 16 == 0) && !getenv("DC_TEST_NO_TMA");
+  static bool attr = false;
+  if (!attr) {
+    DC_CUDA(c, cudaFuncSetAttribute(k_paths, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PathSmem)));
+    attr = true;
+  }
+  int per_sm = 1;
+  DC_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_paths, PT_THREADS, sizeof(PathSmem)));
+  const uint64_t n_tiles = (R + PT_T - 1) / PT_T;
+  const int pgrid = (int)std::min<uint64_t>(std::max<uint64_t>(n_tiles, 1), (uint64_t)c->num_sms * std::max(per_sm, 1));
+  // path table sized for the distinct paths, not the records (retry if it passes half load)
+  uint64_t cap = 1024;
+  while (cap < 2 * (R < (1ull << 19) ? R : (1ull << 19))) cap <<= 1;
+  uint32_t hc[8];
+  for (int attempt = 0;; ++attempt) {
+    DC_TRY(alloc(c, tab, cap));
+    DC_CUDA(c, cudaMemsetAsync(tab.p, 0xFF, cap * sizeof(PathSlot), c->stream));
+    DC_TRY(alloc_zero(c, cnt, 8));  // [0] distinct, [1] extra, [2] compact pos, [3] overflow, [4] empty paths
+    if (R) {
+      k_paths<<<pgrid, PT_THREADS, sizeof(PathSmem), c->stream>>>(p->offsets, p->frames, R, n_frames, tab.p, cap - 1,
+                                                                  slot_of_rec.p, extra_rec.p, cnt.p, c->d_flags,
+                                                                  (unsigned long long*)c->d_diag, c->hash_mask, tma_ok);
+      DC_LAUNCHED(c);
+    }
+    DC_TRY(readback(c, cnt.p, 32, hc));
+    if (!hc[3]) break;
+    if ((hc[3] & 2) || attempt > 2 || cap >= (1ull << 31))
+      return fail(c, DC_ERR_CAPACITY, "dc_cct_build: path table overflow");
+    cap = cap * 8 < (1ull << 31) ? cap * 8 : (1ull << 31);
+  }
   DC_TRY(alloc(c, pid_of_slot, cap));
-  uint32_t hc[4];
-  DC_TRY(readback(c, cnt.p, 8, hc));
   const uint32_t P0 = hc[0], n_extra = hc[1], P = P0 + n_extra;
   DC_TRY(alloc(c, item_rec, P));
   DC_TRY(alloc(c, item_len, P));
   DC_TRY(alloc(c, leaf_of_item, P));
   DC_TRY(alloc_zero(c, sumlen, 1));
-  k_path_compact<<<grid_for(c, cap, 256), 256, 0, c->stream>>>(htab.p, rtab.p, cap, pid_of_slot.p, item_rec.p, cnt.p + 2);
+  k_path_compact<<<grid_for(c, cap, 256), 256, 0, c->stream>>>(tab.p, cap, pid_of_slot.p, item_rec.p, item_len.p, cnt.p + 2);
   DC_LAUNCHED(c);
-  k_items_finish<<<grid_for(c, P, 256), 256, 0, c->stream>>>(item_rec.p, extra_rec.p, P0, n_extra, len.p, item_len.p,
-                                                             sumlen.p);
+  k_items_finish<<<grid_for(c, P, 256), 256, 0, c->stream>>>(item_rec.p, extra_rec.p, P0, n_extra, p->offsets, item_len.p,
+                                                             sumlen.p, cnt.p, (unsigned long long*)c->d_diag);
   DC_LAUNCHED(c);
   uint64_t hsum = 0, hmaxd = 0;
   DC_TRY(readback(c, sumlen.p, 8, &hsum));
@@ -528,7 +1049,13 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
     DC_TRY(readback(c, dN.p, 4, &hN));
     N = hN;
   } else {
-    DC_TRY(build_large(c, p, item_rec.p, item_len.p, P, Lmax, fbits, t, leaf_of_item.p, &levels, &N));
+    bool collided = true;
+    if (!getenv("DC_TEST_LEVELWISE"))
+      DC_TRY(build_euler(c, p, item_rec.p, item_len.p, P, hsum, Lmax, fbits, t, leaf_of_item.p, &N, &collided));
+    if (collided) {  // prefix-hash collision (or forced): exact level-wise construction
+      if (!getenv("DC_TEST_LEVELWISE")) c->host_collisions += 1;
+      DC_TRY(build_large(c, p, item_rec.p, item_len.p, P, Lmax, fbits, t, leaf_of_item.p, &levels, &N));
+    }
   }
   // max depth of this tree
   t->N = N;

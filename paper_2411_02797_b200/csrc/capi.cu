@@ -110,6 +110,10 @@ dc_status dc_ctx_create(int device, void* cuda_stream, dc_ctx** out) {
     int b = atoi(w);
     if (b > 0 && b < 64) ctx->hash_mask = (1ull << b) - 1ull;
   }
+  if (const char* w = getenv("DC_TEST_WEAK_NODE_HASH")) {
+    int b = atoi(w);
+    if (b > 0 && b < 64) ctx->node_mask = (1ull << b) - 1ull;
+  }
   if (const char* w = getenv("DC_TEST_WEAK_MERGE_HASH")) {
     int b = atoi(w);
     if (b > 0 && b < 64) ctx->merge_mask = (1ull << b) - 1ull;

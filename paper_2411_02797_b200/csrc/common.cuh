@@ -39,7 +39,8 @@ struct Ctx {
   uint64_t host_levels = 0;      // tree levels built
   uint64_t host_collisions = 0;  // path-hash collisions resolved exactly
   uint64_t hash_mask = ~0ull;    // fault injection: DC_TEST_WEAK_HASH=bits shortens path hashes
-  uint64_t merge_mask = ~0ull;   // fault injection: DC_TEST_WEAK_MERGE_HASH=bits shortens merge hashes
+  uint64_t merge_mask = ~0ull;
+  uint64_t node_mask = ~0ull;    // fault injection: DC_TEST_WEAK_NODE_HASH=bits shortens prefix-node hashes   // fault injection: DC_TEST_WEAK_MERGE_HASH=bits shortens merge hashes
   // optional CUDA-event timers (dc_ctx_set_timing): (name, start, stop) per timed region
   bool timing = false;
   struct Timed { const char* name; cudaEvent_t a, b; };
@@ -273,4 +274,33 @@ __device__ __forceinline__ void atomic_add_u128(unsigned long long* lo, unsigned
   if (add_hi + carry) atomicAdd(hi, (unsigned long long)(add_hi + carry));
 }
 
+// ---------------------------------------------------------------- mbarrier / TMA bulk-copy helpers (sm_90+)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 }  // namespace dc

@@ -297,3 +297,35 @@ def test_full_size_config3_sampled_contexts():
         assert np.array_equal(a["bin_count"][bsel], r["bin_count"])
         assert a["xsamples"][cnode] == r["xsamples"][1]
     del torch
+
+
+@pytest.mark.parametrize("env", [{}, {"DC_TEST_LEVELWISE": "1"}, {"DC_TEST_WEAK_NODE_HASH": "7"}, {"DC_TEST_NO_TMA": "1"}])
+def test_large_P_build_variants(monkeypatch, env):
+    """> 4096 distinct paths, deep recursion and shared prefixes: the Euler-tour build, the
+    level-wise build (forced), the Euler build with prefix-node hashes cut to 7 bits (its
+    collision check must detect it and fall back to the exact level-wise build), and the record
+    pass without TMA staging — all equal to the oracle."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    import paper_2411_02797_b200 as dc
+    ctx = dc.Context(0)
+    rng = np.random.default_rng(11)
+    paths = []
+    for _ in range(12_000):
+        pre = [0, 1, 2][: int(rng.integers(0, 4))]
+        rec = [5, 6] * int(rng.integers(0, 120)) if rng.random() < 0.1 else []
+        tail = [int(x) for x in rng.integers(0, 40, size=int(rng.integers(0, 14)))]
+        paths.append(tuple(pre + rec + tail))
+    paths += paths[:3000] + [()] * 5
+    order = rng.permutation(len(paths))
+    paths = [paths[i] for i in order]
+    off, fr = _csr(paths)
+    X = rng.integers(0, 10**9, size=(2, len(paths)), dtype=np.uint64)
+    a = gpu_run(off, fr, X, n_frames=40, ctx=ctx)
+    ref = oracle_run(off, fr, X, 2).arrays()
+    assert_same(a, ref, ctx=f"largeP {env}")
+    dep = a["depth"].astype(np.int64)
+    lo = [int(np.searchsorted(dep, d, side="left")) for d in range(int(a["max_depth"]) + 2)]
+    assert a["level_off"].tolist() == lo
+    if "DC_TEST_WEAK_NODE_HASH" in env:
+        assert ctx.diag()["collisions_detected"] > 0
