@@ -24,52 +24,52 @@ constexpr int SB_THREADS = 1024;
 
 __device__ __forceinline__ int bits_for_dev(uint32_t v) { return v ? 32 - __clz(v) : 0; }
 
-// ------------------------------------------------------------------ a2: fused path streaming + exact dedup
-// One pass over the records, in tiles of PT_T consecutive records. A tile's frames are one
-// contiguous range of the frames array; it is staged into shared memory with a TMA bulk copy
-// (cp.async.bulk + mbarrier, double-buffered, the copy of tile k+1 in flight while tile k is
-// processed) together with the tile's offsets. Per tile:
-//   * records are cut into chunks of PT_CH frames (balanced across threads whatever the path
-//     lengths); each chunk adds sum (f+1)*pos[j] into its record's 64-bit path hash
-//     (position-keyed, additive, so chunks combine in any order);
-//   * one thread per record inserts/looks up the finalized hash in an L2-resident table whose
-//     slot carries the representative record (the first inserter) with its offset and length;
-//   * every record whose representative is another record is compared with it frame by frame
-//     (the representative's frames are read through L2; the record's own frames are still in
-//     shared memory), so the dedup is exact: a mismatch (hash collision) makes the record a
-//     representative of its own.
-// The frames are read from HBM exactly once. Tiles whose frames do not fit the stage (very deep
-// paths) or that cannot be staged (unaligned inputs, the array tail) are read from global
-// memory by the same code.
+// ------------------------------------------------------------------ a2: path streaming + exact dedup
+// Two passes over the records:
+//  1. k_path_hash streams the frames once: tiles of PT_T consecutive records, whose frames are
+//     one contiguous range, are staged in shared memory with TMA bulk copies (cp.async.bulk +
+//     mbarrier, double-buffered: the copy of the next tile is in flight while this one is
+//     hashed) together with the tile's offsets. Each record is cut into chunks of PT_CH frames
+//     (odd, so the chunks a warp works on start in different shared-memory banks); a thread per
+//     chunk accumulates two 32-bit position-keyed sums f*A[j] and (f^K)*B[j] and adds them to
+//     its record with native shared atomics. Output: one 64-bit hash per record (its length
+//     mixed in); frame ids and offsets are validated on the way.
+//  2. k_path_group: lane i of a warp inserts / finds record r0+i's hash in an L2-resident table
+//     whose slot names a representative record (the first inserter) with its frame offset and
+//     length; then the warp compares each record with its representative, 32 frames at a time
+//     (coalesced on both sides). A mismatch (a hash collision) makes the record a
+//     representative of its own, so the dedup is exact whatever the hash.
 constexpr int PT_T = 128;           // records per tile
 constexpr int PT_THREADS = 256;
-constexpr uint32_t PT_FW = 8192;    // staged frame window per stage (32 KB)
-constexpr uint32_t PT_CH = 16;      // chunk length (staged tiles)
-constexpr uint32_t PT_CH_G = 128;   // chunk length (global tiles): <= PT_T * 1024 / 128 chunks
-constexpr uint32_t PT_LIST = 1024;  // chunk list capacity (>= PT_FW / PT_CH + PT_T and >= PT_T * 8)
+constexpr int PT_WARPS = PT_THREADS / 32;
+constexpr int PT_RPW = PT_T / PT_WARPS;  // records per warp (16)
+constexpr uint32_t PT_FW = 8192;    // staged frame window per stage (32 KB): 2 CTAs per SM
+constexpr uint32_t PT_CH = 17;      // chunk length (staged tiles; odd: bank spread)
+constexpr uint32_t PT_CH_G = 129;   // chunk length (global tiles)
 constexpr uint32_t PT_NONE = 0xFFFFFFFFu;
 
 struct __align__(32) PathSlot {
-  unsigned long long key;  // finalized path hash, ~0 = empty
+  unsigned long long key;  // record hash, ~0 = empty
   unsigned long long off;  // representative: first frame, length, record index (rep written last)
   uint32_t len, rep;
   unsigned long long pad;
 };
 
+struct PathWarp {  // per warp: its 16 records of the tile
+  unsigned long long o[PT_RPW];
+  uint32_t L[PT_RPW];
+  uint32_t cs[PT_RPW + 1];  // chunk starts (exclusive scan), cs[16] = chunks
+  uint32_t h1[PT_RPW], h2[PT_RPW];
+};
+
 struct PathSmem {
   uint32_t fr[2][PT_FW];
   unsigned long long offs[2][PT_T + 2];
-  unsigned long long pos[DC_MAX_DEPTH];
+  uint2 pos[DC_MAX_DEPTH];
   unsigned long long full[2];
   unsigned long long meta_f0[2], meta_f1[2];
   uint32_t meta_mode[2];
-  unsigned long long h[PT_T];
-  unsigned long long rec_o[PT_T];
-  unsigned long long rep_o[PT_T];
-  uint32_t rec_L[PT_T];
-  uint32_t slot[PT_T];
-  uint32_t need[PT_T];  // 0 nothing to compare, 1 compare with the representative, 2 differs
-  uint32_t list[PT_LIST];
+  PathWarp wp[PT_WARPS];
 };
 
 __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
@@ -88,29 +88,54 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {  // read-once data: no L1 allocation
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
 
-// chunk loop over frames held at src (shared stage or the global array); OP(i, j0, j1, p) gets
-// the record, the position range and the index of the record's first frame in src
-template <class F>
-__device__ __forceinline__ void pt_chunks(const PathSmem& sm, uint32_t n_chunks, uint32_t ch, F op) {
-  for (uint32_t ci = threadIdx.x; ci < n_chunks; ci += PT_THREADS) {
-    const uint32_t e = sm.list[ci];
-    const uint32_t i = e >> 16, j0 = (e & 0xFFFFu) * ch;
-    const uint32_t j1 = min(j0 + ch, sm.rec_L[i]);
-    op(i, j0, j1);
+// one warp's chunks: lane takes chunks lane, lane+32, ...; its record by a 4-step search of the
+// warp's chunk starts
+template <bool STAGED>
+__device__ __forceinline__ void pt_hash_chunks(PathWarp& W, const uint2* __restrict__ pos, const uint32_t* __restrict__ src,
+                                               uint64_t base, uint32_t n_chunks, uint32_t n_frames, uint32_t& bad) {
+  constexpr uint32_t CH = STAGED ? PT_CH : PT_CH_G;
+  for (uint32_t ci = lane_id(); ci < n_chunks; ci += 32) {
+    uint32_t k = 0;
+#pragma unroll
+    for (uint32_t step = PT_RPW / 2; step; step >>= 1)
+      if (W.cs[k + step] <= ci) k += step;
+    const uint32_t j0 = (ci - W.cs[k]) * CH;
+    const uint32_t j1 = min(j0 + CH, W.L[k]);
+    const uint32_t* q = src + (W.o[k] - base);
+    uint32_t a1 = 0, a2 = 0, mx = 0;
+#pragma unroll 4
+    for (uint32_t j = j0; j < j1; ++j) {
+      const uint32_t f = STAGED ? q[j] : ld_stream_u32(q + j);
+      const uint2 w = pos[j];
+      a1 += f * w.x;
+      a2 += (f ^ 0x9E3779B9u) * w.y;
+      mx = max(mx, f);
+    }
+    if (j1 > j0 && mx >= n_frames) bad = 1;
+    atomicAdd(&W.h1[k], a1);
+    atomicAdd(&W.h2[k], a2);
   }
 }
 
-__global__ void __launch_bounds__(PT_THREADS) k_paths(const uint64_t* __restrict__ off, const uint32_t* __restrict__ frames,
-                                                      uint64_t R, uint32_t n_frames, PathSlot* __restrict__ tab, uint64_t mask,
-                                                      uint32_t* __restrict__ slot_of_rec, uint32_t* __restrict__ extra_rec,
-                                                      unsigned int* __restrict__ d_cnt, uint32_t* d_flags,
-                                                      unsigned long long* d_diag, uint64_t hash_mask, int tma_ok) {
+__global__ void __launch_bounds__(PT_THREADS) k_path_hash(const uint64_t* __restrict__ off, const uint32_t* __restrict__ frames,
+                                                          uint64_t R, uint32_t n_frames, uint64_t* __restrict__ hash,
+                                                          unsigned int* __restrict__ d_cnt, uint32_t* d_flags,
+                                                          unsigned long long* d_diag, uint64_t hash_mask, int tma_ok) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PathSmem& sm = *reinterpret_cast<PathSmem*>(smem_raw);
-  const uint32_t tid = threadIdx.x;
+  const uint32_t tid = threadIdx.x, lane = lane_id(), w = tid >> 5;
+  PathWarp& W = sm.wp[w];
   const uint64_t n_tiles = (R + PT_T - 1) / PT_T, G = gridDim.x;
-  for (uint32_t j = tid; j < DC_MAX_DEPTH; j += PT_THREADS) sm.pos[j] = mix64(0x9E3779B97F4A7C15ull * (j + 1)) | 1ull;
+  for (uint32_t j = tid; j < DC_MAX_DEPTH; j += PT_THREADS) {
+    const uint64_t m = mix64(0x9E3779B97F4A7C15ull * (j + 1));
+    sm.pos[j] = make_uint2((uint32_t)m | 1u, (uint32_t)(m >> 32) | 1u);
+  }
   if (tid == 0) {
     mbar_init(&sm.full[0], 1);
     mbar_init(&sm.full[1], 1);
@@ -118,8 +143,8 @@ __global__ void __launch_bounds__(PT_THREADS) k_paths(const uint64_t* __restrict
   }
   __syncthreads();
   uint32_t flags = 0, maxd = 0, empties = 0;
+  const uint64_t Ftot = off[R];
   // ---- producer (thread 0): stage tile t into buffer s; F0/F1 = first/end frame of the tile
-  const uint64_t Ftot = tid == 0 ? off[R] : 0;
   auto issue = [&](uint64_t t, int s, uint64_t F0, uint64_t F1) {
     const uint64_t r0 = t * PT_T;
     uint32_t mode = 0, bytes = 0;
@@ -166,19 +191,21 @@ __global__ void __launch_bounds__(PT_THREADS) k_paths(const uint64_t* __restrict
     const uint32_t n = (uint32_t)min((uint64_t)PT_T, R - r0);
     const uint32_t mode = sm.meta_mode[s];
     const bool staged = mode & 1;
-    const uint64_t F0 = sm.meta_f0[s], F1 = sm.meta_f1[s], a = F0 & ~3ull;
+    const uint64_t F0 = sm.meta_f0[s], F1 = sm.meta_f1[s];
     const uint32_t ch = staged ? PT_CH : PT_CH_G;
-    // ---- per record: bounds, length, chunk list
+    // ---- this warp's records: bounds, length, chunk starts (warp scan); no block barrier
+    const uint32_t i = w * PT_RPW + lane;  // tile-local record of lanes 0..15
+    const bool mine = lane < PT_RPW && i < n;
     uint32_t c = 0, L = 0;
     uint64_t o = 0;
-    if (tid < n) {
+    if (mine) {
       uint64_t o0, o1;
       if (mode & 2) {
-        o0 = sm.offs[s][tid];
-        o1 = sm.offs[s][tid + 1];
+        o0 = sm.offs[s][i];
+        o1 = sm.offs[s][i + 1];
       } else {
-        o0 = off[r0 + tid];
-        o1 = off[r0 + tid + 1];
+        o0 = off[r0 + i];
+        o1 = off[r0 + i + 1];
       }
       uint64_t LL = o1 >= o0 ? o1 - o0 : 0;
       if (o1 < o0) flags |= FLAG_BAD_OFFSETS;
@@ -187,7 +214,7 @@ __global__ void __launch_bounds__(PT_THREADS) k_paths(const uint64_t* __restrict
         LL = DC_MAX_DEPTH;
       }
       // frames outside the staged window / the array: malformed offsets (never read)
-      if (LL && (staged ? (o0 < F0 || o0 + LL > F1) : (o0 + LL > off[R]))) {
+      if (LL && (staged ? (o0 < F0 || o0 + LL > F1) : (o0 + LL > Ftot))) {
         flags |= FLAG_BAD_OFFSETS;
         LL = 0;
       }
@@ -197,48 +224,60 @@ __global__ void __launch_bounds__(PT_THREADS) k_paths(const uint64_t* __restrict
       maxd = max(maxd, L);
       empties += L == 0;
     }
-    uint32_t n_chunks;
-    const uint32_t cs = block_excl_scan<uint32_t, PT_THREADS>(c, &n_chunks);
-    if (tid < n) {
-      sm.h[tid] = 0;
-      sm.rec_o[tid] = o;
-      sm.rec_L[tid] = L;
-      for (uint32_t j = 0; j < c; ++j) sm.list[cs + j] = tid << 16 | j;
+    const uint32_t incl = warp_incl_scan<uint32_t>(c);
+    const uint32_t n_chunks = __shfl_sync(0xffffffffu, incl, 31);
+    if (lane < PT_RPW) {
+      W.o[lane] = o;
+      W.L[lane] = L;
+      W.cs[lane] = incl - c;
+      W.h1[lane] = 0;
+      W.h2[lane] = 0;
+      if (lane == PT_RPW - 1) W.cs[PT_RPW] = incl;
     }
-    __syncthreads();
-    // ---- path hashes (and frame-id validation)
+    __syncwarp();
     uint32_t bad = 0;
-    if (staged) {
-      pt_chunks(sm, n_chunks, ch, [&](uint32_t i, uint32_t j0, uint32_t j1) {
-        const uint32_t* src = sm.fr[s] + (sm.rec_o[i] - a);
-        unsigned long long acc = 0;
-        for (uint32_t j = j0; j < j1; ++j) {
-          const uint32_t f = src[j];
-          bad |= f >= n_frames;
-          acc += ((unsigned long long)f + 1ull) * sm.pos[j];
-        }
-        atomicAdd(&sm.h[i], acc);
-      });
-    } else {
-      pt_chunks(sm, n_chunks, ch, [&](uint32_t i, uint32_t j0, uint32_t j1) {
-        const uint32_t* src = frames + sm.rec_o[i];
-        unsigned long long acc = 0;
-        for (uint32_t j = j0; j < j1; ++j) {
-          const uint32_t f = __ldg(src + j);
-          bad |= f >= n_frames;
-          acc += ((unsigned long long)f + 1ull) * sm.pos[j];
-        }
-        atomicAdd(&sm.h[i], acc);
-      });
-    }
+    if (staged) pt_hash_chunks<true>(W, sm.pos, sm.fr[s], F0 & ~3ull, n_chunks, n_frames, bad);
+    else pt_hash_chunks<false>(W, sm.pos, frames, 0, n_chunks, n_frames, bad);
     if (bad) flags |= FLAG_BAD_FRAME;
-    __syncthreads();
-    // ---- table: insert or find; the inserter publishes its record as the representative
-    uint32_t sl = PT_NONE;
-    bool mine = false;
-    if (tid < n) {
-      uint64_t H = mix64(sm.h[tid] ^ ((uint64_t)L * 0xC2B2AE3D27D4EB4Full)) & hash_mask;
+    __syncwarp();
+    if (mine) {
+      uint64_t H = mix64(((uint64_t)W.h1[lane] << 32 | W.h2[lane]) ^ ((uint64_t)L * 0xC2B2AE3D27D4EB4Full)) & hash_mask;
       if (H == ~0ull) H = ~1ull;
+      hash[r0 + i] = H;
+    }
+    __syncthreads();  // stage s is free for the copy issued next iteration
+  }
+  // ---- diag / flags, one atomic per warp
+  flags = __reduce_or_sync(0xffffffffu, flags);
+  maxd = __reduce_max_sync(0xffffffffu, maxd);
+  empties = __reduce_add_sync(0xffffffffu, empties);
+  if (lane == 0) {
+    if (maxd) atomicMax(&d_diag[DG_MAXDEPTH], (unsigned long long)maxd);
+    if (empties) atomicAdd(d_cnt + 4, empties);  // added to the diag once (k_items_finish)
+    if (flags) atomicOr(d_flags, flags);
+  }
+}
+
+// lane i: record r0 + i into the table; then the warp verifies each record against its
+// representative frame by frame
+__global__ void __launch_bounds__(256) k_path_group(const uint64_t* __restrict__ off, const uint32_t* __restrict__ frames,
+                                                    const uint64_t* __restrict__ hash, uint64_t R, PathSlot* __restrict__ tab,
+                                                    uint64_t mask, uint32_t* __restrict__ slot_of_rec,
+                                                    uint32_t* __restrict__ extra_rec, unsigned int* __restrict__ d_cnt) {
+  const uint32_t lane = lane_id();
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t r0 = warp * 32; r0 < R; r0 += nw * 32) {
+    const uint64_t r = r0 + lane;
+    const bool act = r < R;
+    uint64_t o = 0, ro = 0;
+    uint32_t L = 0, sl = PT_NONE, need = 0;
+    bool mine = false;
+    if (act) {
+      o = off[r];
+      const uint64_t o1 = off[r + 1];
+      L = (uint32_t)(o1 >= o ? min(o1 - o, (uint64_t)DC_MAX_DEPTH) : 0);  // validated by k_path_hash
+      const uint64_t H = hash[r];
       uint64_t q = (H * 0x9E3779B97F4A7C15ull >> 17) & mask;
       for (uint64_t probe = 0; probe <= mask; ++probe, q = (q + 1) & mask) {
         const unsigned long long cur = ld_relaxed_u64(&tab[q].key);
@@ -262,70 +301,65 @@ __global__ void __launch_bounds__(PT_THREADS) k_paths(const uint64_t* __restrict
       if (mine) {
         tab[sl].off = o;
         tab[sl].len = L;
-        st_release_u32(&tab[sl].rep, (uint32_t)(r0 + tid));
+        st_release_u32(&tab[sl].rep, (uint32_t)r);
         const unsigned ins = atomicAdd(d_cnt, 1u);
         if ((uint64_t)ins * 2 >= mask) atomicOr(d_cnt + 3, 1u);  // past half load: retry larger
       }
       if (sl == PT_NONE) atomicOr(d_cnt + 3, 1u);  // table full
     }
-    __syncthreads();  // this CTA's representatives are published
-    if (tid < n) {
-      uint32_t need = 0;
-      if (sl != PT_NONE && !mine) {
-        while (ld_acquire_u32(&tab[sl].rep) == PT_NONE) {
-        }
-        const uint64_t ro = tab[sl].off;
-        const uint32_t rl = tab[sl].len;
-        need = rl != L ? 2u : (L ? 1u : 0u);
-        sm.rep_o[tid] = ro;
+    __syncwarp();  // this warp's representatives are published
+    if (act && sl != PT_NONE && !mine) {
+      for (uint64_t spin = 0; ld_acquire_u32(&tab[sl].rep) == PT_NONE; ++spin)
+        if (spin > DC_SPIN_LIMIT) __trap();
+      ro = tab[sl].off;
+      const uint32_t rl = tab[sl].len;
+      need = rl != L ? 2u : (L ? 1u : 0u);
+    }
+    // verify, 8 records at a time: their first 64 frames on both sides are loaded before any
+    // compare, so the DRAM latency of the own frames is paid once per group
+    uint32_t todo = __ballot_sync(0xffffffffu, need == 1u);
+    while (todo) {
+      int idx[8];
+      uint64_t oo[8], rr[8];
+      uint32_t ll[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        idx[u] = todo ? __ffs(todo) - 1 : -1;
+        if (todo) todo &= todo - 1;
+        const int i = idx[u] < 0 ? 0 : idx[u];
+        oo[u] = __shfl_sync(0xffffffffu, o, i);
+        rr[u] = __shfl_sync(0xffffffffu, ro, i);
+        const uint32_t li = __shfl_sync(0xffffffffu, L, i);
+        ll[u] = idx[u] < 0 ? 0u : li;
       }
-      sm.need[tid] = need;
-      sm.slot[tid] = sl;
+      uint32_t a0[8], b0[8], a1[8], b1[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const bool p0 = lane < ll[u], p1 = lane + 32 < ll[u];
+        a0[u] = p0 ? ld_stream_u32(frames + oo[u] + lane) : 0u;
+        b0[u] = p0 ? __ldg(frames + rr[u] + lane) : 0u;
+        a1[u] = p1 ? ld_stream_u32(frames + oo[u] + lane + 32) : 0u;
+        b1[u] = p1 ? __ldg(frames + rr[u] + lane + 32) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        bool diff = (a0[u] != b0[u]) | (a1[u] != b1[u]);
+        for (uint32_t j = lane + 64; j < ll[u]; j += 32) diff |= ld_stream_u32(frames + oo[u] + j) != __ldg(frames + rr[u] + j);
+        if (__any_sync(0xffffffffu, diff) && lane == (uint32_t)idx[u]) need = 2u;
+      }
     }
-    __syncthreads();
-    // ---- exact verification against the representative
-    if (staged) {
-      pt_chunks(sm, n_chunks, ch, [&](uint32_t i, uint32_t j0, uint32_t j1) {
-        if (sm.need[i] != 1u) return;
-        const uint32_t* src = sm.fr[s] + (sm.rec_o[i] - a);
-        const uint32_t* rep = frames + sm.rep_o[i];
-        bool diff = false;
-        for (uint32_t j = j0; j < j1; ++j) diff |= src[j] != __ldg(rep + j);
-        if (diff) sm.need[i] = 2u;
-      });
-    } else {
-      pt_chunks(sm, n_chunks, ch, [&](uint32_t i, uint32_t j0, uint32_t j1) {
-        if (sm.need[i] != 1u) return;
-        const uint32_t* src = frames + sm.rec_o[i];
-        const uint32_t* rep = frames + sm.rep_o[i];
-        bool diff = false;
-        for (uint32_t j = j0; j < j1; ++j) diff |= __ldg(src + j) != __ldg(rep + j);
-        if (diff) sm.need[i] = 2u;
-      });
-    }
-    __syncthreads();
-    if (tid < n) {
-      uint32_t out = sm.slot[tid];
-      if (sm.need[tid] == 2u) {  // collision: a representative of its own
+    if (act) {
+      uint32_t out = sl;
+      if (need == 2u) {  // collision: a representative of its own
         const unsigned e = atomicAdd(d_cnt + 1, 1u);
-        extra_rec[e] = (uint32_t)(r0 + tid);
+        extra_rec[e] = (uint32_t)r;
         const uint64_t v = mask + 1 + (uint64_t)e;
         if (v >= PT_NONE) atomicOr(d_cnt + 3, 2u);
         out = (uint32_t)v;
       }
       if (out == PT_NONE) out = 0;  // overflow: the host retries
-      slot_of_rec[r0 + tid] = out;
+      slot_of_rec[r] = out;
     }
-    __syncthreads();  // stage s and the per-record arrays are free
-  }
-  // ---- diag / flags, one atomic per warp
-  flags = __reduce_or_sync(0xffffffffu, flags);
-  maxd = __reduce_max_sync(0xffffffffu, maxd);
-  empties = __reduce_add_sync(0xffffffffu, empties);
-  if (lane_id() == 0) {
-    if (maxd) atomicMax(&d_diag[DG_MAXDEPTH], (unsigned long long)maxd);
-    if (empties) atomicAdd(d_cnt + 4, empties);  // added to the diag once (k_items_finish), not per retry
-    if (flags) atomicOr(d_flags, flags);
   }
 }
 
@@ -361,12 +395,23 @@ __global__ void k_items_finish(uint32_t* __restrict__ item_rec, const uint32_t* 
   if (lane_id() == 0 && acc) atomicAdd(d_sumlen, acc);
 }
 
-__global__ void k_rec_leaf(const uint32_t* __restrict__ slot_of_rec, const uint32_t* __restrict__ pid_of_slot, uint64_t cap,
+// slot -> leaf node (one L2-resident map), then one gather per record, 4 records per thread
+__global__ void k_slot_leaf(const PathSlot* __restrict__ tab, uint64_t cap, const uint32_t* __restrict__ pid_of_slot,
+                            const uint32_t* __restrict__ leaf_of_item, uint32_t* __restrict__ leaf_of_slot) {
+  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < cap; s += (uint64_t)gridDim.x * blockDim.x)
+    leaf_of_slot[s] = tab[s].key == ~0ull ? 0u : leaf_of_item[pid_of_slot[s]];
+}
+
+__global__ void k_rec_leaf(const uint32_t* __restrict__ slot_of_rec, const uint32_t* __restrict__ leaf_of_slot, uint64_t cap,
                            uint32_t P0, const uint32_t* __restrict__ leaf_of_item, uint64_t R, uint32_t* __restrict__ leaf) {
-  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < R; r += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t s = slot_of_rec[r];
-    uint32_t item = s < cap ? pid_of_slot[s] : P0 + (uint32_t)(s - cap);
-    leaf[r] = leaf_of_item[item];
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < R; r += 4 * stride) {
+    uint32_t s[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) s[u] = r + u * stride < R ? slot_of_rec[r + u * stride] : 0u;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (r + u * stride < R) leaf[r + u * stride] = s[u] < cap ? leaf_of_slot[s[u]] : leaf_of_item[P0 + (uint32_t)(s[u] - cap)];
   }
 }
 
@@ -475,8 +520,8 @@ __global__ void __launch_bounds__(SB_THREADS, 1) k_build_small(const uint64_t* _
     n_active += tot;
   }
   __syncthreads();
-  uint32_t lvl_start = 0, width = 1, next = 1;
-  for (uint32_t d = 0; n_active > 0; ++d) {
+  uint32_t lvl_start = 0, width = 1, next = 1, d = 0;
+  for (; n_active > 0; ++d) {
     const int pbits = bits_for_dev(width - 1);
     for (uint32_t i = threadIdx.x; i < n_active; i += SB_THREADS) {
       const uint32_t it = sm.val[act][i];
@@ -521,7 +566,10 @@ __global__ void __launch_bounds__(SB_THREADS, 1) k_build_small(const uint64_t* _
     if (threadIdx.x == 0) level_off[d + 2] = next;
     n_active = n_keep;
   }
-  if (threadIdx.x == 0) *d_N = next;
+  if (threadIdx.x == 0) {
+    d_N[0] = next;
+    d_N[1] = d;  // levels built = depth of the tree
+  }
 }
 
 // ------------------------------------------------------------------ a3: large P, per level
@@ -736,8 +784,8 @@ __global__ void k_prefix_nodes(const uint64_t* __restrict__ off, const uint32_t*
       __syncwarp();
       if (act && !mine && sl != PT_NONE) {
         unsigned long long pp;
-        while ((pp = ld_acquire_u64(&tab[sl].pay)) == ~0ull) {
-        }
+        for (uint64_t spin = 0; (pp = ld_acquire_u64(&tab[sl].pay)) == ~0ull; ++spin)
+          if (spin > DC_SPIN_LIMIT) __trap();
         if (pp != pay) atomicOr(d_cnt + 2, 1u);  // same key, different (parent, frame): collision
       }
       carry = __shfl_sync(0xffffffffu, incl, 31);
@@ -975,23 +1023,32 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
     DC_TRY(palloc(c, t->frame_kind, n_frames));
     DC_CUDA(c, cudaMemcpyAsync(t->frame_kind, dict->kinds, n_frames, cudaMemcpyDeviceToDevice, c->stream));
   }
-  // ---- a2: one fused pass: hash, group, verify exactly (k_paths)
+  // ---- a2: hash pass (frames streamed once), then group + exact verification
   Buf<uint32_t> slot_of_rec, extra_rec, pid_of_slot, item_rec, item_len, leaf_of_item, leafbuf;
+  Buf<uint64_t> hash;
   Buf<PathSlot> tab;
   Buf<unsigned long long> sumlen;
   Buf<unsigned int> cnt;
+  DC_TRY(alloc(c, hash, R));
   DC_TRY(alloc(c, slot_of_rec, R));
   DC_TRY(alloc(c, extra_rec, R));
+  DC_TRY(alloc_zero(c, cnt, 8));  // [0] distinct, [1] extra, [2] compact pos, [3] overflow, [4] empty paths
   const int tma_ok = ((uintptr_t)p->offsets % 16 == 0) && ((uintptr_t)p->frames % 16 == 0) && !getenv("DC_TEST_NO_TMA");
   static bool attr = false;
   if (!attr) {
-    DC_CUDA(c, cudaFuncSetAttribute(k_paths, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PathSmem)));
+    DC_CUDA(c, cudaFuncSetAttribute(k_path_hash, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PathSmem)));
     attr = true;
   }
-  int per_sm = 1;
-  DC_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_paths, PT_THREADS, sizeof(PathSmem)));
-  const uint64_t n_tiles = (R + PT_T - 1) / PT_T;
-  const int pgrid = (int)std::min<uint64_t>(std::max<uint64_t>(n_tiles, 1), (uint64_t)c->num_sms * std::max(per_sm, 1));
+  if (R) {
+    int per_sm = 1;
+    DC_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_path_hash, PT_THREADS, sizeof(PathSmem)));
+    const uint64_t n_tiles = (R + PT_T - 1) / PT_T;
+    const int hgrid = (int)std::min<uint64_t>(n_tiles, (uint64_t)c->num_sms * std::max(per_sm, 1));
+    k_path_hash<<<hgrid, PT_THREADS, sizeof(PathSmem), c->stream>>>(p->offsets, p->frames, R, n_frames, hash.p, cnt.p,
+                                                                     c->d_flags, (unsigned long long*)c->d_diag,
+                                                                     c->hash_mask, tma_ok);
+    DC_LAUNCHED(c);
+  }
   // path table sized for the distinct paths, not the records (retry if it passes half load)
   uint64_t cap = 1024;
   while (cap < 2 * (R < (1ull << 19) ? R : (1ull << 19))) cap <<= 1;
@@ -999,11 +1056,10 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
   for (int attempt = 0;; ++attempt) {
     DC_TRY(alloc(c, tab, cap));
     DC_CUDA(c, cudaMemsetAsync(tab.p, 0xFF, cap * sizeof(PathSlot), c->stream));
-    DC_TRY(alloc_zero(c, cnt, 8));  // [0] distinct, [1] extra, [2] compact pos, [3] overflow, [4] empty paths
+    DC_CUDA(c, cudaMemsetAsync(cnt.p, 0, 16, c->stream));  // [0..3]; [4] (empty paths) kept
     if (R) {
-      k_paths<<<pgrid, PT_THREADS, sizeof(PathSmem), c->stream>>>(p->offsets, p->frames, R, n_frames, tab.p, cap - 1,
-                                                                  slot_of_rec.p, extra_rec.p, cnt.p, c->d_flags,
-                                                                  (unsigned long long*)c->d_diag, c->hash_mask, tma_ok);
+      k_path_group<<<grid_for(c, (R + 31) / 32 * 32, 256), 256, 0, c->stream>>>(p->offsets, p->frames, hash.p, R, tab.p,
+                                                                                cap - 1, slot_of_rec.p, extra_rec.p, cnt.p);
       DC_LAUNCHED(c);
     }
     DC_TRY(readback(c, cnt.p, 32, hc));
@@ -1023,10 +1079,11 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
   k_items_finish<<<grid_for(c, P, 256), 256, 0, c->stream>>>(item_rec.p, extra_rec.p, P0, n_extra, p->offsets, item_len.p,
                                                              sumlen.p, cnt.p, (unsigned long long*)c->d_diag);
   DC_LAUNCHED(c);
-  uint64_t hsum = 0, hmaxd = 0;
-  DC_TRY(readback(c, sumlen.p, 8, &hsum));
-  DC_TRY(readback(c, c->d_diag + DG_MAXDEPTH, 8, &hmaxd));
-  DC_TRY(check_flags(c));
+  uint64_t hsum = 0, hmaxd = 0, F = 0;
+  uint32_t hflags = 0;
+  DC_TRY(readback_multi(c, {{sumlen.p, 8, &hsum}, {c->d_diag + DG_MAXDEPTH, 8, &hmaxd}, {c->d_flags, 4, &hflags},
+                            {p->offsets + R, 8, &F}}));
+  DC_TRY(flags_status(c, hflags));
   const uint64_t Nbound = 1 + hsum;
   if (Nbound >= (1ull << 32)) return fail(c, DC_ERR_CAPACITY, "dc_cct_build: more than 2^32 nodes");
   // hmaxd is the deepest path seen on this context so far (>= this trace's): sizes level_off
@@ -1039,15 +1096,16 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
   uint32_t levels = 0;
   if (P <= SMALL_P) {
     Buf<uint32_t> dN;
-    DC_TRY(alloc(c, dN, 1));
+    DC_TRY(alloc(c, dN, 2));
     size_t smem = sizeof(SmallSmem);
     DC_CUDA(c, cudaFuncSetAttribute(k_build_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_build_small<<<1, SB_THREADS, smem, c->stream>>>(p->offsets, p->frames, item_rec.p, item_len.p, P, fbits, t->parent,
                                                       t->frame, t->depth, t->level_off, leaf_of_item.p, dN.p);
     DC_LAUNCHED(c);
-    uint32_t hN = 0;
-    DC_TRY(readback(c, dN.p, 4, &hN));
-    N = hN;
+    uint32_t hN[2] = {0, 0};
+    DC_TRY(readback(c, dN.p, 8, hN));
+    N = hN[0];
+    t->max_depth = hN[1];
   } else {
     bool collided = true;
     if (!getenv("DC_TEST_LEVELWISE"))
@@ -1064,10 +1122,17 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
     DC_TRY(alloc(c, leafbuf, R));
     leaf = leafbuf.p;
   }
-  k_rec_leaf<<<grid_for(c, R, 256), 256, 0, c->stream>>>(slot_of_rec.p, pid_of_slot.p, cap, P0, leaf_of_item.p, R, leaf);
-  DC_LAUNCHED(c);
-  // depth of the tree = largest d with a node
   {
+    Buf<uint32_t> leaf_of_slot;
+    DC_TRY(alloc(c, leaf_of_slot, cap));
+    k_slot_leaf<<<grid_for(c, cap, 256), 256, 0, c->stream>>>(tab.p, cap, pid_of_slot.p, leaf_of_item.p, leaf_of_slot.p);
+    DC_LAUNCHED(c);
+    k_rec_leaf<<<grid_for(c, (R + 3) / 4, 256), 256, 0, c->stream>>>(slot_of_rec.p, leaf_of_slot.p, cap, P0, leaf_of_item.p, R,
+                                                                     leaf);
+    DC_LAUNCHED(c);
+  }
+  // depth of the tree = largest d with a node
+  if (P > SMALL_P) {
     uint16_t md = 0;
     if (N > 1) DC_TRY(readback(c, t->depth + (N - 1), 2, &md));
     t->max_depth = md;
@@ -1078,8 +1143,6 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
   DC_CUDA(c, cudaMemsetAsync(t->xcnt, 0, N * 8, c->stream));
   DC_CUDA(c, cudaMemsetAsync(t->icnt, 0, N * 8, c->stream));
   // algorithmic bytes: offsets + frames of every record once, leaf, node table
-  uint64_t F = 0;
-  DC_TRY(readback(c, p->offsets + R, 8, &F));
   c->bytes_host += 8 * (R + 1) + 4 * F + 4 * R + 10 * N;
   c->host_levels += t->max_depth;
   c->host_collisions += n_extra;

@@ -46,6 +46,36 @@ dc_status readback(Ctx* c, const void* dev, size_t bytes, void* host) {
   return DC_OK;
 }
 
+dc_status readback_multi(Ctx* c, std::initializer_list<RB> items) {
+  HostRegion hr(c, "readback");
+  size_t o = 0;
+  for (const RB& it : items) {
+    if (o + it.bytes > 4096) return fail(c, DC_ERR_ARG, "readback_multi: more than 4 KB");
+    if (it.bytes) DC_CUDA(c, cudaMemcpyAsync((char*)c->h_pinned + o, it.dev, it.bytes, cudaMemcpyDeviceToHost, c->stream));
+    o += (it.bytes + 7) & ~(size_t)7;
+  }
+  DC_CUDA(c, cudaStreamSynchronize(c->stream));
+  o = 0;
+  for (const RB& it : items) {
+    memcpy(it.host, (char*)c->h_pinned + o, it.bytes);
+    o += (it.bytes + 7) & ~(size_t)7;
+  }
+  return DC_OK;
+}
+
+dc_status flags_status(Ctx* c, uint32_t f) {
+  if (f) {
+    const char* why = (f & FLAG_BAD_FRAME)    ? "frame id >= n_frames"
+                      : (f & FLAG_BAD_KEY)    ? "raw frame key with reserved kind 0xFFFFFFFF"
+                      : (f & FLAG_TOO_DEEP)   ? "call path deeper than DC_MAX_DEPTH"
+                      : (f & FLAG_BAD_LEAF)   ? "leaf / launch_leaf entry is not a node of the tree"
+                      : (f & FLAG_BAD_OFFSETS)? "record offsets are not non-decreasing"
+                                              : "internal error";
+    return fail(c, DC_ERR_TRACE, "malformed trace (flags 0x%x): %s", f, why);
+  }
+  return DC_OK;
+}
+
 dc_status check_flags(Ctx* c) {
   uint32_t f = 0;
   DC_TRY(readback(c, c->d_flags, 4, &f));

@@ -7,6 +7,10 @@
 //    its path to the root (one thread per (node, column group); integer atomics), which
 //    needs no per-level barrier — depth-256 trees cost one launch.
 // a8: mean/std from the exact integers with single roundings (reading R18).
+#include <stdlib.h>
+
+#include <algorithm>
+
 #include "prim.cuh"
 
 namespace dc {
@@ -120,6 +124,111 @@ __global__ void k_push(const uint32_t* __restrict__ parent, uint64_t N, uint32_t
   }
 }
 
+// Level-synchronous rollup for deep / large trees: one persistent cooperative kernel walks the
+// levels bottom-up; every node of level d adds its (final) inclusive values into its parent,
+// with a software grid barrier between levels. Siblings are contiguous (canonical order), so a
+// warp whose 32 nodes share one parent reduces in registers and issues one update.
+struct RollArgs {
+  const uint32_t* parent;
+  const uint32_t* level_off;
+  uint32_t maxd;
+  uint64_t N;
+  uint32_t M, S, G;
+  unsigned long long *icnt, *mcols, *isamples, *istall;
+  unsigned int* bar;  // [0] arrivals, [1] generation
+};
+
+__device__ __forceinline__ void grid_barrier(unsigned int* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int* gen = bar + 1;
+    const unsigned int g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      for (uint64_t spin = 0; *gen == g; ++spin)
+        if (spin > DC_SPIN_LIMIT) __trap();
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = min(v, (uint64_t)__shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ void warp_sum_u128(uint64_t& lo, uint64_t& hi) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const uint64_t l2 = __shfl_xor_sync(0xffffffffu, lo, o), h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+    const uint64_t t = lo + l2;
+    hi += h2 + (t < lo);
+    lo = t;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_rollup_levels(RollArgs a) {
+  const uint64_t N = a.N;
+  const uint32_t M = a.M, lane = lane_id();
+  const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
+  for (uint32_t d = a.maxd; d >= 1; --d) {
+    const uint64_t lo = a.level_off[d], width = a.level_off[d + 1] - lo;
+    const uint64_t items = width * a.G;
+    const uint64_t rounds = (items + nthreads - 1) / nthreads;
+    for (uint64_t k = 0; k < rounds; ++k) {  // warp-uniform trip count (shuffles below)
+      const uint64_t t = k * nthreads + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+      const bool act = t < items;
+      const uint32_t g = act ? (uint32_t)(t / width) : 0xFFFFFFFFu;
+      const uint64_t m = act ? lo + t % width : 0;
+      const uint32_t p = act ? a.parent[m] : 0xFFFFFFFFu;
+      // every lane takes part in these shuffles (none inside a short-circuit)
+      const uint32_t p0 = __shfl_sync(0xffffffffu, p, 0), g0 = __shfl_sync(0xffffffffu, g, 0);
+      const bool uni = __all_sync(0xffffffffu, act && p == p0 && g == g0);
+      if (g == 0 || (uni && g0 == 0)) {
+        uint64_t v = act ? a.icnt[m] : 0;
+        if (uni) v = warp_sum_u64(v);
+        if (v && (!uni || lane == 0)) atomicAdd(a.icnt + p, (unsigned long long)v);
+      } else if (g <= M) {
+        const uint32_t mm = g - 1;
+        const uint64_t cnt = a.icnt[m];
+        uint64_t sum = a.mcols[((uint64_t)C_ISUM * M + mm) * N + m];
+        uint64_t mn = a.mcols[((uint64_t)C_IMIN * M + mm) * N + m];
+        uint64_t qlo = a.mcols[((uint64_t)C_ISQLO * M + mm) * N + m];
+        uint64_t qhi = a.mcols[((uint64_t)C_ISQHI * M + mm) * N + m];
+        if (uni) {
+          sum = warp_sum_u64(sum);
+          mn = warp_min_u64(mn);
+          warp_sum_u128(qlo, qhi);
+        }
+        const bool any = uni ? __any_sync(0xffffffffu, cnt != 0) : cnt != 0;
+        if (any && (!uni || lane == 0)) {
+          if (sum) atomicAdd(a.mcols + ((uint64_t)C_ISUM * M + mm) * N + p, (unsigned long long)sum);
+          atomicMin(a.mcols + ((uint64_t)C_IMIN * M + mm) * N + p, (unsigned long long)mn);
+          if (qlo | qhi)
+            atomic_add_u128(a.mcols + ((uint64_t)C_ISQLO * M + mm) * N + p, a.mcols + ((uint64_t)C_ISQHI * M + mm) * N + p, qlo,
+                            qhi);
+        }
+      } else if (act || uni) {
+        unsigned long long* col = g == M + 1 ? a.isamples : a.istall + (uint64_t)(g - M - 2) * N;
+        uint64_t v = act ? col[m] : 0;
+        if (uni) v = warp_sum_u64(v);
+        if (v && (!uni || lane == 0)) atomicAdd(col + p, (unsigned long long)v);
+      }
+    }
+    grid_barrier(a.bar);
+  }
+}
+
 dc_status rollup(Ctx* c, dc_cct* t) {
   const uint64_t N = t->N;
   const uint32_t M = t->M, S = t->S;
@@ -135,8 +244,21 @@ dc_status rollup(Ctx* c, dc_cct* t) {
     DC_CUDA(c, cudaMemcpyAsync(t->isamples, t->xsamples, N * 8, cudaMemcpyDeviceToDevice, s));
     DC_CUDA(c, cudaMemcpyAsync(t->istall, t->xstall, (uint64_t)S * N * 8, cudaMemcpyDeviceToDevice, s));
   }
-  if (N > 1) {
-    const uint32_t G = 1 + M + (t->xsamples ? 1 + S : 0);
+  const uint32_t G = 1 + M + (t->xsamples ? 1 + S : 0);
+  // walk cost of the per-node ancestor push ~ N * depth; deep / large trees go level by level
+  const bool levels = ((uint64_t)N * t->max_depth > (16ull << 20) || getenv("DC_TEST_ROLLUP_LEVELS")) && !getenv("DC_TEST_ROLLUP_PUSH");
+  if (N > 1 && levels) {
+    static int per_sm = 0;
+    if (!per_sm) DC_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rollup_levels, 256, 0));
+    Buf<unsigned int> bar;
+    DC_TRY(alloc_zero(c, bar, 2));
+    RollArgs ra{t->parent, t->level_off, t->max_depth, N, M, S, G, (unsigned long long*)t->icnt, (unsigned long long*)t->mcols,
+                (unsigned long long*)t->isamples, (unsigned long long*)t->istall, bar.p};
+    void* args[] = {&ra};
+    const int grid = c->num_sms * std::max(1, std::min(per_sm, 4));
+    DC_CUDA(c, cudaLaunchCooperativeKernel((void*)k_rollup_levels, grid, 256, args, 0, s));
+    DC_LAUNCHED(c);
+  } else if (N > 1) {
     k_push<<<grid_for(c, (N - 1) * G, 256, 16), 256, 0, s>>>(t->parent, N, M, S, G, t->xcnt, (unsigned long long*)t->icnt,
                                                              (unsigned long long*)t->mcols, t->xsamples,
                                                              (unsigned long long*)t->isamples, t->xstall,

@@ -4,6 +4,7 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <chrono>
+#include <initializer_list>
 #include <string>
 #include <vector>
 
@@ -224,6 +225,14 @@ dc_status palloc(Ctx* c, T*& p, size_t n) {
 // synchronous small readback through the pinned buffer
 dc_status readback(Ctx* c, const void* dev, size_t bytes, void* host);
 dc_status check_flags(Ctx* c);  // synchronizes; DC_ERR_TRACE if a flag is set
+// several small readbacks behind one stream synchronisation (<= 4 KB in total)
+struct RB {
+  const void* dev;
+  size_t bytes;
+  void* host;
+};
+dc_status readback_multi(Ctx* c, std::initializer_list<RB> items);
+dc_status flags_status(Ctx* c, uint32_t flags);  // DC_ERR_TRACE if any flag bit is set
 dc_status add_diag(Ctx* c, const unsigned long long* src_dev);  // d_diag[i] += src[i], i < DG_N
 
 inline int grid_for(Ctx* c, uint64_t work, int per_block, int waves = 8) {
@@ -285,18 +294,25 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, uint32_t b
 __device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity) {
+// Every device-side wait is bounded: a wait that outlives DC_SPIN_LIMIT polls is a bug (a lost
+// arrival), and the kernel traps (a launch error the host reports) instead of hanging the GPU.
+constexpr uint64_t DC_SPIN_LIMIT = 1ull << 28;
+__device__ __forceinline__ bool mbar_try_wait(unsigned long long* b, uint32_t parity) {
+  uint32_t ok;
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
-      "LAB_WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@P1 bra DONE;\n"
-      "bra LAB_WAIT;\n"
-      "DONE:\n"
-      "}\n" ::"r"(smem_u32(b)),
-      "r"(parity)
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
       : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity) {
+  for (uint64_t i = 0; !mbar_try_wait(b, parity); ++i)
+    if (i > DC_SPIN_LIMIT) __trap();
 }
 __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),

@@ -17,7 +17,8 @@ __device__ __forceinline__ uint64_t key_lo(const dc_frame_key& k) { return (uint
 
 __global__ void k_intern_insert(const dc_frame_key* __restrict__ keys, uint64_t n, ulonglong2* table, uint64_t mask,
                                 uint32_t* __restrict__ out_slot, unsigned long long* d_count, uint32_t* d_overflow,
-                                uint32_t* d_flags) {
+                                uint32_t* d_flags, unsigned long long* d_max) {
+  uint64_t mx_addr = 0, mx_ks = 0;  // radix widths of the canonical sort (max addr, max kind<<32|str)
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
     ulonglong2 kv = __ldg(reinterpret_cast<const ulonglong2*>(keys) + j);  // 16-B coalesced load
     const uint64_t lo = kv.x, hi = kv.y;                                    // lo = kind | str<<32, hi = addr
@@ -26,6 +27,8 @@ __global__ void k_intern_insert(const dc_frame_key* __restrict__ keys, uint64_t 
       out_slot[j] = 0;
       continue;
     }
+    mx_addr = max(mx_addr, hi);
+    mx_ks = max(mx_ks, (lo << 32) | (lo >> 32));
     uint64_t h = mix64(lo ^ mix64(hi + 0x9E3779B97F4A7C15ull));
     uint64_t s = h & mask;
     uint32_t found = 0xFFFFFFFFu;
@@ -50,11 +53,19 @@ __global__ void k_intern_insert(const dc_frame_key* __restrict__ keys, uint64_t 
     }
     out_slot[j] = found;
   }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    mx_addr = max(mx_addr, (uint64_t)__shfl_xor_sync(0xffffffffu, mx_addr, o));
+    mx_ks = max(mx_ks, (uint64_t)__shfl_xor_sync(0xffffffffu, mx_ks, o));
+  }
+  if (lane_id() == 0) {
+    if (mx_addr) atomicMax(&d_max[0], (unsigned long long)mx_addr);
+    if (mx_ks) atomicMax(&d_max[1], (unsigned long long)mx_ks);
+  }
 }
 
 __global__ void k_intern_compact(const ulonglong2* __restrict__ table, uint64_t cap, uint64_t* __restrict__ addr_key,
-                                 uint64_t* __restrict__ ks_key, uint32_t* __restrict__ slot_of, unsigned int* d_pos,
-                                 unsigned long long* d_max) {
+                                 uint64_t* __restrict__ ks_key, uint32_t* __restrict__ slot_of, unsigned int* d_pos) {
   for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < cap; s += (uint64_t)gridDim.x * blockDim.x) {
     ulonglong2 cur = table[s];
     if ((uint32_t)cur.x == 0xFFFFFFFFu) continue;
@@ -63,8 +74,6 @@ __global__ void k_intern_compact(const ulonglong2* __restrict__ table, uint64_t 
     uint32_t kind = (uint32_t)cur.x, str = (uint32_t)(cur.x >> 32);
     ks_key[p] = ((uint64_t)kind << 32) | str;
     slot_of[p] = (uint32_t)s;
-    atomicMax(&d_max[0], (unsigned long long)cur.y);
-    atomicMax(&d_max[1], (unsigned long long)ks_key[p]);
   }
 }
 
@@ -128,8 +137,9 @@ dc_status intern_frames(Ctx* c, const dc_frame_key* keys, uint64_t n, uint32_t* 
     return fail(c, DC_ERR_CAPACITY, "dc_intern_frames: n >= 2^32 keys");
   }
   Buf<ulonglong2> table;
-  Buf<unsigned long long> cnt;
+  Buf<unsigned long long> cnt, mx;
   Buf<uint32_t> ovf;
+  uint64_t mxh[2] = {0, 0};
   uint64_t cap = next_pow2(2 * (n < (1ull << 20) ? n : (1ull << 20)));
   if (cap < 1024) cap = 1024;
   uint64_t D = 0;
@@ -138,12 +148,12 @@ dc_status intern_frames(Ctx* c, const dc_frame_key* keys, uint64_t n, uint32_t* 
     DC_CUDA(c, cudaMemsetAsync(table.p, 0xFF, cap * sizeof(ulonglong2), c->stream));
     DC_TRY(alloc_zero(c, cnt, 1));
     DC_TRY(alloc_zero(c, ovf, 1));
+    DC_TRY(alloc_zero(c, mx, 2));
     k_intern_insert<<<grid_for(c, n, 256), 256, 0, c->stream>>>(keys, n, table.p, cap - 1, out_ids, cnt.p, ovf.p,
-                                                                 c->d_flags);
+                                                                 c->d_flags, mx.p);
     DC_LAUNCHED(c);
-    uint64_t h[2];
-    DC_TRY(readback(c, cnt.p, 8, &h[0]));
-    DC_TRY(readback(c, ovf.p, 4, &h[1]));
+    uint64_t h[2] = {0, 0};
+    DC_TRY(readback_multi(c, {{cnt.p, 8, &h[0]}, {ovf.p, 4, &h[1]}, {mx.p, 16, mxh}}));
     D = h[0];
     bool overflow = (uint32_t)h[1] != 0;
     if (!overflow && D * 2 <= cap) break;
@@ -157,7 +167,6 @@ dc_status intern_frames(Ctx* c, const dc_frame_key* keys, uint64_t n, uint32_t* 
   d->D = D;
   Buf<uint64_t> ka, kb, ka2;
   Buf<uint32_t> slot_of, ord0, ord1, rank_of_slot;
-  Buf<unsigned long long> mx;
   Buf<unsigned int> pos;
   DC_TRY(alloc(c, ka, D));
   DC_TRY(alloc(c, kb, D));
@@ -166,12 +175,9 @@ dc_status intern_frames(Ctx* c, const dc_frame_key* keys, uint64_t n, uint32_t* 
   DC_TRY(alloc(c, ord0, D));
   DC_TRY(alloc(c, ord1, D));
   DC_TRY(alloc(c, rank_of_slot, cap));
-  DC_TRY(alloc_zero(c, mx, 2));
   DC_TRY(alloc_zero(c, pos, 1));
-  k_intern_compact<<<grid_for(c, cap, 256), 256, 0, c->stream>>>(table.p, cap, ka.p, kb.p, slot_of.p, pos.p, mx.p);
+  k_intern_compact<<<grid_for(c, cap, 256), 256, 0, c->stream>>>(table.p, cap, ka.p, kb.p, slot_of.p, pos.p);
   DC_LAUNCHED(c);
-  uint64_t mxh[2];
-  DC_TRY(readback(c, mx.p, 16, mxh));
   k_iota<<<grid_for(c, D, 256), 256, 0, c->stream>>>(ord0.p, D);
   DC_LAUNCHED(c);
   // LSD: by addr, then (stable) by kind<<32|str  ==> lexicographic (kind, str_id, addr)

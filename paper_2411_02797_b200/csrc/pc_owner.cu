@@ -182,6 +182,7 @@ struct OwnArgs {
   uint64_t spill_base0;        // CTA b spills into pkey/pcnt[spill_base0 + b * OW_SPILL_CAP ...]
   uint32_t probe_mode;         // measurement only (DC_OWN_MODE): 1 = stream + keys, no table
   uint32_t* sink;
+  const uint32_t* bad;         // launch_sample_off inconsistent (k_own_check): do nothing, generic schedule
 };
 
 // all consumer threads; the caller has synchronised the consumers (every insert is done)
@@ -253,7 +254,7 @@ __device__ __forceinline__ uint4 ld_shared_v4_volatile(const uint32_t* p) {
   return v;
 }
 
-// branch-free home-bucket lookup: keys are unique in the table, so at most one compare holds
+// branch-free bucket lookup: keys are unique in the table, so at most one compare holds
 __device__ __forceinline__ uint32_t bucket_slot(const uint4 v, uint32_t key, uint32_t b) {
   const uint32_t j = (v.y == key ? 1u : 0u) | (v.z == key ? 2u : 0u) | (v.w == key ? 3u : 0u);
   return (v.x == key) | (j != 0u) ? 4 * b + j : (uint32_t)OW_MISS;
@@ -270,7 +271,8 @@ __device__ __forceinline__ void red_shared_inc_if(uint32_t* p, bool pred) {  // 
 __device__ __noinline__ uint32_t own_probe(OwnSmem& sm, uint32_t key, uint32_t b) {
   // `distinct` is refreshed once per warp round (not per insert), hence the margin in OW_SPILL_AT
   const bool full = *(volatile uint32_t*)&sm.distinct >= OW_SPILL_AT;
-  while (true) {
+  for (uint32_t walked = 0;; ++walked) {
+    if (walked > 2 * OW_NB) return OW_TAB;  // cannot happen below OW_SPILL_AT; spill rather than spin
     const uint4 v = ld_shared_v4_volatile(&sm.key[4 * b]);
     const int j = bucket_match(v, key);
     if (j >= 0) return 4 * b + j;
@@ -364,6 +366,7 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   OwnSmem& sm = *reinterpret_cast<OwnSmem*>(smem_raw);
   const uint32_t tid = threadIdx.x;
+  if (*a.bad) return;  // the stage plan is meaningless; the host reruns the generic schedule
   // range of this CTA: stages [s0, s1) of the plan
   const uint64_t G = gridDim.x, ST = *a.st_total;
   const uint64_t s0 = ST * blockIdx.x / G, s1 = ST * (blockIdx.x + 1) / G;
@@ -526,11 +529,12 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
   long long t_wait = 0, t_flush = 0, t_work = 0, n_stage = 0, t_key = 0, t_bucket = 0, t_add = 0, n_miss = 0;  // MODE 9 only
   uint32_t np = 0;        // queued misses of this warp (warp-uniform)
   uint32_t inserted = 0;  // keys this lane inserted since the last publish
-  auto probe_one = [&](uint32_t key) {
+  auto probe_add = [&](uint32_t key, uint32_t add) {
     const uint32_t r = own_probe(sm, key, own_bucket(key));
     inserted += r >> 31;
-    own_add(sm, a, key, r & 0x7FFFFFFFu, 1u, cur_ctx);
+    own_add(sm, a, key, r & 0x7FFFFFFFu, add, cur_ctx);
   };
+  auto probe_one = [&](uint32_t key) { probe_add(key, 1u); };
   // one `distinct` update per warp round (flush request when it crosses OW_FLUSH_REQ)
   auto publish = [&]() {
     const uint32_t ins = __reduce_add_sync(0xffffffffu, inserted);
@@ -596,11 +600,13 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
     }
     const long long c_2 = MODE == 9 ? clock64() : 0;
     if (MODE == 9) t_key += c_2 - c_1;
+    // the stage's samples and row meta are in registers: release the slot to the producer now,
+    // before the table work (one more stage of prefetch in flight)
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[st]);
     if (MODE == 1) {  // measurement: data movement + classification only
 #pragma unroll
       for (int i = 0; i < OW_PER_LANE; ++i) sinkv ^= t[i] * (2 * i + 1);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.empty[st]);
     } else {
       uint32_t slot[OW_PER_LANE];
 #pragma unroll
@@ -630,7 +636,6 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
         probe_one(sm.pend[w][np + lane]);
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.empty[st]);
       publish();
       if (MODE == 9) t_add += clock64() - c_3;
     }
@@ -689,9 +694,11 @@ constexpr uint32_t BR_MAXCH = ((OW_TAB > (int)OW_SPILL_CAP ? OW_TAB : OW_SPILL_C
        item += ((uint64_t)gridDim.x * blockDim.x) >> 5)                                                        \
     if (const uint4 sg = seg[item / BR_MAXCH]; sg.x < N && (item % BR_MAXCH) * BR_CH < sg.y)
 
-__global__ void k_br_range(const uint4* __restrict__ seg, uint32_t n_segs, const uint32_t* __restrict__ pkey, uint64_t N,
-                           uint32_t* __restrict__ cmax, uint32_t* __restrict__ cor) {
+// runs before the host has read the segment count: it takes the device counter (clamped)
+__global__ void k_br_range(const uint4* __restrict__ seg, const unsigned int* __restrict__ d_nsegs, uint32_t cap_segs,
+                           const uint32_t* __restrict__ pkey, uint64_t N, uint32_t* __restrict__ cmax, uint32_t* __restrict__ cor) {
   const uint32_t lane = threadIdx.x & 31;
+  const uint32_t n_segs = min(*d_nsegs, cap_segs);
   BR_FOR_CHUNKS(seg, n_segs, N) {
     const uint64_t base = (uint64_t)sg.z | ((uint64_t)sg.w << 32);
     const uint32_t j0 = (uint32_t)(item % BR_MAXCH) * BR_CH, j1 = min(sg.y, j0 + BR_CH);
@@ -1251,15 +1258,15 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
                                                                        n_launch, row_cap, rowpos.p, row_launch.p,
                                                                        row_valid.p, st_first.p, st_ctx.p);
     DC_LAUNCHED(c);
-    uint32_t hbad = 0;
-    DC_TRY(readback(c, bad.p, 4, &hbad));
-    if (hbad) return DC_OK;  // offsets inconsistent: generic schedule
   }
   // partial outputs
   const uint32_t G = (uint32_t)c->num_sms;
   const uint64_t cap_entries = n + 1;
   const uint32_t cap_segs = (uint32_t)(n_launch + 4ull * G + n / 4096 + 1024);
-  Buf<uint32_t> pkey, flags;
+  Buf<uint32_t> pkey, flags, cm, wide;
+  Buf<uint64_t> cw;
+  Buf<uint8_t> csh;
+  uint64_t hw[2] = {0, 0};
   Buf<unsigned long long> pcnt, ctr, ldiag;
   Buf<uint4> seg;
   uint64_t hc[2];
@@ -1298,6 +1305,7 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
     a.spill_base0 = cap_entries;
     a.probe_mode = 0;
     a.sink = flags.p;
+    a.bad = bad.p;
     if (const char* pm = getenv("DC_OWN_MODE")) a.probe_mode = (uint32_t)atoi(pm);  // measurement only
     Buf<unsigned long long> dbg;
     if (a.probe_mode == 9 || a.probe_mode == 2) {
@@ -1342,8 +1350,27 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
               "\"key_cyc\": %.0f, \"bucket_cyc\": %.0f, \"add_cyc\": %.0f, \"misses\": %.0f}}\n",
               s[0] / nw, s[1] / nw, s[2] / nw, s[3] / nw, s[4] / nw, s[5] / nw, s[6] / nw, s[7]);
     }
-    DC_TRY(readback(c, ctr.p, 16, hc));
-    DC_TRY(readback(c, flags.p, 8, hf));
+    // the reduce's first kernels run on the device counts, before the one host round trip
+    DC_TRY(alloc_zero(c, cm, 2 * N));  // cmax | cor
+    DC_TRY(alloc(c, cw, N + 1));
+    DC_TRY(alloc(c, csh, N));
+    DC_TRY(alloc_zero(c, wide, 1));
+    {
+      Region rk(c, "k:br_range");
+      k_br_range<<<grid_for(c, (uint64_t)cap_segs * BR_MAXCH * 32, 256), 256, 0, c->stream>>>(seg.p, a.g_segs, cap_segs, pkey.p,
+                                                                                            N, cm.p, cm.p + N);
+      DC_LAUNCHED(c);
+    }
+    {
+      Region rk(c, "k:br_words");
+      k_br_words<<<grid_for(c, N, 256), 256, 0, c->stream>>>(cm.p, cm.p + N, N, cw.p, csh.p, wide.p);
+      DC_LAUNCHED(c);
+    }
+    DC_TRY(excl_scan<uint64_t>(c, cw.p, cw.p, N, cw.p + N));  // word base per context, W at cw[N]
+    uint32_t hbad = 0;
+    DC_TRY(readback_multi(c, {{ctr.p, 16, hc}, {flags.p, 8, hf}, {bad.p, 4, &hbad}, {cw.p + N, 8, &hw[0]},
+                              {wide.p, 4, &hw[1]}}));
+    if (hbad) return DC_OK;  // offsets inconsistent: generic schedule
     if (a.probe_mode == 9)
       fprintf(stderr, "{\"own_out\": {\"entries\": %llu, \"segments\": %llu}}\n", (unsigned long long)hc[0],
               (unsigned long long)(hc[1] & 0xFFFFFFFFu));
@@ -1354,28 +1381,7 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
     // ------------------------------------------------ global bitmap reduce (see k_br_*)
     HostRegion hr(c, "br");
     Region rb(c, "pc:breduce");
-    Buf<uint32_t> cm, wide;
-    Buf<uint64_t> cw;
-    Buf<uint8_t> csh;
-    DC_TRY(alloc_zero(c, cm, 2 * N));  // cmax | cor
-    DC_TRY(alloc(c, cw, N + 1));
-    DC_TRY(alloc(c, csh, N));
-    DC_TRY(alloc_zero(c, wide, 1));
     const int segs_grid = grid_for(c, (uint64_t)n_segs * BR_MAXCH * 32, 256);
-    {
-      Region rk(c, "k:br_range");
-      k_br_range<<<segs_grid, 256, 0, c->stream>>>(seg.p, n_segs, pkey.p, N, cm.p, cm.p + N);
-      DC_LAUNCHED(c);
-    }
-    {
-      Region rk(c, "k:br_words");
-      k_br_words<<<grid_for(c, N, 256), 256, 0, c->stream>>>(cm.p, cm.p + N, N, cw.p, csh.p, wide.p);
-      DC_LAUNCHED(c);
-    }
-    DC_TRY(excl_scan<uint64_t>(c, cw.p, cw.p, N, cw.p + N));  // word base per context, W at cw[N]
-    uint64_t hw[2] = {0, 0};
-    DC_TRY(readback(c, cw.p + N, 8, hw));
-    DC_TRY(readback(c, wide.p, 4, &hw[1]));
     const uint64_t W = hw[0];
     if (!(hw[1] & 0xFFFFFFFFu) && W <= BR_MAX_TOTAL) {
       Buf<uint32_t> bm;

@@ -23,7 +23,10 @@ pytestmark = pytest.mark.gpu
 NOPC = [k for k in CMP_KEYS if "samples" not in k and "stall" not in k and "pc" not in k and "bin" not in k]
 
 
-def test_config4_prefix_vs_oracle():
+@pytest.mark.parametrize("rollup", ["levels", "push"])
+def test_config4_prefix_vs_oracle(rollup, monkeypatch):
+    if rollup == "push":
+        monkeypatch.setenv("DC_TEST_ROLLUP_PUSH", "1")
     p = gen.programs.config4()
     tr = gen.make_trace(p, n_records=2_000_000, raw_keys=False)
     off = tr.offsets.numpy().view(np.uint64)
