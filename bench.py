@@ -268,9 +268,15 @@ def main():
         if dist is not None:
             dist.barrier()
 
+    # warm-up exactly like the timed loop (the previous step's CCT stays alive while the next one
+    # is built), so the memory pool has grown to its steady-state size before timing
+    last = None
     for _ in range(args.warmup):
         cct, _ = run_step(dc, ctx, tr, args.config, comm=comm)
-        cct.free()
+        if last is not None:
+            last.free()
+        last = cct
+    last.free()
     ctx.sync()
     # ---------------- timed region (device time, CUDA events on the library stream; the
     # library's own per-stage timers are off here and measured in a separate pass below)

@@ -1016,6 +1016,7 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
   if (R >= (1ull << 32)) return fail(c, DC_ERR_CAPACITY, "dc_cct_build: n_records >= 2^32");
   dc_cct* t = new dc_cct();
   t->device = c->device;
+  t->owner_uid = c->uid;
   t->R = R;
   t->n_frames = n_frames;
   const int fbits = bits_for(n_frames > 0 ? n_frames - 1 : 0) > 0 ? bits_for(n_frames - 1) : 1;

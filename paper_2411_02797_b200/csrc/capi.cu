@@ -1,5 +1,7 @@
 // capi.cu — the exported C ABI of libdc (include/dc.h): argument checks, handle state
 // machine, context plumbing. Every compute step runs in the kernels of the other files.
+#include <mutex>
+#include <unordered_map>
 #include <stdarg.h>
 #include <stdlib.h>
 #include <string.h>
@@ -74,6 +76,33 @@ dc_status flags_status(Ctx* c, uint32_t f) {
     return fail(c, DC_ERR_TRACE, "malformed trace (flags 0x%x): %s", f, why);
   }
   return DC_OK;
+}
+
+static std::mutex g_ctx_mu;
+static std::unordered_map<uint64_t, cudaStream_t> g_live_ctx;  // context uid -> its stream
+static uint64_t g_next_uid = 1;
+void register_ctx(Ctx* c, bool live) {
+  std::lock_guard<std::mutex> g(g_ctx_mu);
+  if (live) {
+    c->uid = g_next_uid++;
+    g_live_ctx[c->uid] = c->stream;
+  } else {
+    g_live_ctx.erase(c->uid);
+  }
+}
+void free_handle_ptrs(uint64_t owner_uid, void* const* ps, size_t n) {
+  {
+    std::lock_guard<std::mutex> g(g_ctx_mu);
+    auto it = g_live_ctx.find(owner_uid);
+    if (it != g_live_ctx.end()) {  // stream-ordered: after every queued use on the context stream
+      for (size_t i = 0; i < n; ++i)
+        if (ps[i]) cudaFreeAsync(ps[i], it->second);
+      return;
+    }
+  }
+  cudaDeviceSynchronize();
+  for (size_t i = 0; i < n; ++i)
+    if (ps[i]) cudaFree(ps[i]);
 }
 
 dc_status check_flags(Ctx* c) {
@@ -164,6 +193,7 @@ dc_status dc_ctx_create(int device, void* cuda_stream, dc_ctx** out) {
   cudaMemsetAsync(ctx->d_flags, 0, 4, ctx->stream);
   cudaMemsetAsync(ctx->d_diag, 0, DG_N * 8, ctx->stream);
   cudaStreamSynchronize(ctx->stream);
+  dc::register_ctx(ctx, true);
   *out = ctx;
   return DC_OK;
 }
@@ -195,6 +225,7 @@ dc_status dc_ctx_diag(dc_ctx* ctx, dc_diag* out_h) {
 void dc_ctx_destroy(dc_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
+  dc::register_ctx(ctx, false);  // handles outliving the context free synchronously from now on
   cudaStreamSynchronize(ctx->stream);
   cudaFree(ctx->d_flags);
   cudaFree(ctx->d_diag);
@@ -288,8 +319,8 @@ dc_status dc_dict_arrays(const dc_dict* d, const dc_frame_key** keys_dev, const 
 void dc_dict_free(dc_dict* d) {
   if (!d) return;
   cudaSetDevice(d->device);
-  cudaFree(d->keys);
-  cudaFree(d->kinds);
+  void* ps[] = {d->keys, d->kinds};
+  dc::free_handle_ptrs(d->owner_uid, ps, 2);
   delete d;
 }
 
@@ -402,9 +433,7 @@ void dc_cct_free(dc_cct* t) {
   void* ps[] = {t->parent, t->frame, t->level_off, t->depth, t->frame_kind, t->xcnt, t->icnt, t->mcols, t->xsamples,
                 t->isamples, t->xstall, t->istall, t->pc_ctx, t->pc_off, t->bin_pcnode, t->bin_stall, t->bin_count,
                 t->part_nodes, t->part_bins};
-  cudaDeviceSynchronize();
-  for (void* p : ps)
-    if (p) cudaFree(p);
+  dc::free_handle_ptrs(t->owner_uid, ps, sizeof ps / sizeof ps[0]);
   delete t;
 }
 

@@ -39,6 +39,15 @@ __global__ void k_attribute(const uint32_t* __restrict__ leaf, uint64_t R, const
   }
 }
 
+// all metric columns in one pass: min columns start at UINT64_MAX (reading R11), the rest at 0
+__global__ void k_init_cols(uint64_t* __restrict__ mcols, uint32_t M, uint64_t N) {
+  const uint64_t total = 8ull * M * N;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t which = i / ((uint64_t)M * N);
+    mcols[i] = (which == C_XMIN || which == C_IMIN) ? ~0ull : 0ull;
+  }
+}
+
 dc_status ensure_metric_cols(Ctx* c, dc_cct* t, uint32_t M) {
   if (t->mcols) {
     if (t->M != M) return fail(c, DC_ERR_ARG, "metric count %u differs from the first call's %u", M, t->M);
@@ -47,11 +56,8 @@ dc_status ensure_metric_cols(Ctx* c, dc_cct* t, uint32_t M) {
   t->M = M;
   const uint64_t N = t->N;
   DC_TRY(palloc(c, t->mcols, (uint64_t)8 * M * N));
-  DC_CUDA(c, cudaMemsetAsync(t->mcols, 0, (uint64_t)8 * M * N * 8, c->stream));
-  for (uint32_t m = 0; m < M; ++m) {
-    k_fill_u64<<<grid_for(c, N, 256), 256, 0, c->stream>>>(t->col(C_XMIN, m), N, ~0ull);
-    DC_LAUNCHED(c);
-    k_fill_u64<<<grid_for(c, N, 256), 256, 0, c->stream>>>(t->col(C_IMIN, m), N, ~0ull);
+  if (M) {
+    k_init_cols<<<grid_for(c, 8ull * M * N, 256), 256, 0, c->stream>>>(t->mcols, M, N);
     DC_LAUNCHED(c);
   }
   return DC_OK;
@@ -234,12 +240,8 @@ dc_status rollup(Ctx* c, dc_cct* t) {
   const uint32_t M = t->M, S = t->S;
   cudaStream_t s = c->stream;
   DC_CUDA(c, cudaMemcpyAsync(t->icnt, t->xcnt, N * 8, cudaMemcpyDeviceToDevice, s));
-  for (uint32_t m = 0; m < M; ++m) {
-    DC_CUDA(c, cudaMemcpyAsync(t->col(C_ISUM, m), t->col(C_XSUM, m), N * 8, cudaMemcpyDeviceToDevice, s));
-    DC_CUDA(c, cudaMemcpyAsync(t->col(C_IMIN, m), t->col(C_XMIN, m), N * 8, cudaMemcpyDeviceToDevice, s));
-    DC_CUDA(c, cudaMemcpyAsync(t->col(C_ISQLO, m), t->col(C_XSQLO, m), N * 8, cudaMemcpyDeviceToDevice, s));
-    DC_CUDA(c, cudaMemcpyAsync(t->col(C_ISQHI, m), t->col(C_XSQHI, m), N * 8, cudaMemcpyDeviceToDevice, s));
-  }
+  // the exclusive block [xsum, xmin, xsq_lo, xsq_hi][M][N] is contiguous, and so is the inclusive one
+  if (M) DC_CUDA(c, cudaMemcpyAsync(t->col(C_ISUM, 0), t->col(C_XSUM, 0), 4ull * M * N * 8, cudaMemcpyDeviceToDevice, s));
   if (t->xsamples) {
     DC_CUDA(c, cudaMemcpyAsync(t->isamples, t->xsamples, N * 8, cudaMemcpyDeviceToDevice, s));
     DC_CUDA(c, cudaMemcpyAsync(t->istall, t->xstall, (uint64_t)S * N * 8, cudaMemcpyDeviceToDevice, s));

@@ -27,6 +27,7 @@ enum { DG_EMPTY = 0, DG_BAD_LAUNCH, DG_BAD_STALL, DG_ZERO, DG_COLL, DG_LEVELS, D
 
 struct Ctx {
   int device = 0;
+  uint64_t uid = 0;  // unique per context (handle frees look it up)
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   std::string err;
@@ -98,8 +99,17 @@ struct Region {
 
 struct dc_ctx : dc::Ctx {};
 
+// Handles remember the context that made them: while that context is alive they are freed
+// stream-ordered on its stream (cudaFreeAsync, no device synchronisation); otherwise with a
+// device synchronisation and cudaFree.
+namespace dc {
+void register_ctx(Ctx* c, bool live);
+void free_handle_ptrs(uint64_t owner_uid, void* const* ps, size_t n);
+}  // namespace dc
+
 struct dc_dict {
   int device = 0;
+  uint64_t owner_uid = 0;  // context that allocated the arrays (0: none)
   uint64_t D = 0;
   dc_frame_key* keys = nullptr;  // dev [D]
   uint8_t* kinds = nullptr;      // dev [D]
@@ -107,6 +117,7 @@ struct dc_dict {
 
 struct dc_cct {
   int device = 0;
+  uint64_t owner_uid = 0;  // context that allocated the arrays (0: none)
   uint64_t N = 0, Npc = 0, Nbins = 0, R = 0;
   uint32_t M = 0, S = 0, max_depth = 0, n_frames = 0;
   int state = 0;  // 0 BUILT, 1 DIRTY, 2 ROLLED

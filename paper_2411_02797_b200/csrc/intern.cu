@@ -124,6 +124,7 @@ static uint64_t next_pow2(uint64_t v) {
 dc_status intern_frames(Ctx* c, const dc_frame_key* keys, uint64_t n, uint32_t* out_ids, dc_dict** out) {
   dc_dict* d = new dc_dict();
   d->device = c->device;
+  d->owner_uid = c->uid;
   *out = nullptr;
   if (n == 0) {
     d->D = 0;
@@ -205,6 +206,7 @@ dc_status intern_frames(Ctx* c, const dc_frame_key* keys, uint64_t n, uint32_t* 
 dc_status dict_from_sorted(Ctx* c, const dc_frame_key* keys, uint64_t D, dc_dict** out) {
   dc_dict* d = new dc_dict();
   d->device = c->device;
+  d->owner_uid = c->uid;
   d->D = D;
   DC_TRY(palloc(c, d->keys, D));
   DC_TRY(palloc(c, d->kinds, D));

@@ -374,6 +374,7 @@ static dc_cct* make_partition(Ctx* c, const RecFmt& f, uint64_t n_nodes, Buf<uin
                               Buf<uint64_t>& bins, uint32_t n_frames) {
   dc_cct* t = new dc_cct();
   t->device = c->device;
+  t->owner_uid = c->uid;
   t->M = f.M;
   t->S = f.has_pc ? f.S : 0;
   t->N = n_nodes;
@@ -542,6 +543,7 @@ static dc_status canonicalize(Ctx* c, const uint64_t* rec, uint64_t n, const uin
   if (lvl[1] != 1) return fail(c, DC_ERR_COLLISION, "merge: %u root records", lvl[1]);
   dc_cct* t = new dc_cct();
   t->device = c->device;
+  t->owner_uid = c->uid;
   t->N = n;
   t->n_frames = n_frames;
   t->max_depth = L - 1;
