@@ -422,6 +422,7 @@ struct SmallSmem {
   uint32_t node_of_item[SMALL_P];
   uint64_t off_of_item[SMALL_P];
   uint16_t len_of_item[SMALL_P];
+  uint32_t next_frame[SMALL_P];  // frame d of each active item, prefetched during level d-1
   uint32_t wcnt[32][256];
 };
 
@@ -521,12 +522,30 @@ __global__ void __launch_bounds__(SB_THREADS, 1) k_build_small(const uint64_t* _
   }
   __syncthreads();
   uint32_t lvl_start = 0, width = 1, next = 1, d = 0;
+  for (uint32_t i = threadIdx.x; i < n_active; i += SB_THREADS) {
+    const uint32_t it = sm.val[0][i];
+    sm.next_frame[it] = frames[sm.off_of_item[it]];
+  }
+  __syncthreads();
   for (; n_active > 0; ++d) {
     const int pbits = bits_for_dev(width - 1);
-    for (uint32_t i = threadIdx.x; i < n_active; i += SB_THREADS) {
-      const uint32_t it = sm.val[act][i];
-      const uint32_t f = frames[sm.off_of_item[it] + d];
-      sm.key[act][i] = ((uint64_t)(sm.node_of_item[it] - lvl_start) << fbits) | f;
+    // this level's frames come from shared memory; the next level's are loaded now and land
+    // while the level is sorted and numbered (the global-load latency leaves the level loop)
+    constexpr int PF = SMALL_P / SB_THREADS;
+    uint32_t pf_it[PF], pf_f[PF];
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      const uint32_t i = threadIdx.x + u * SB_THREADS;
+      pf_it[u] = DC_NO_NODE;
+      if (i < n_active) {
+        const uint32_t it = sm.val[act][i];
+        const uint32_t f = sm.next_frame[it];
+        sm.key[act][i] = ((uint64_t)(sm.node_of_item[it] - lvl_start) << fbits) | f;
+        if (sm.len_of_item[it] > d + 1) {
+          pf_it[u] = it;
+          pf_f[u] = frames[sm.off_of_item[it] + d + 1];
+        }
+      }
     }
     __syncthreads();
     bool in_order = true;
@@ -565,6 +584,10 @@ __global__ void __launch_bounds__(SB_THREADS, 1) k_build_small(const uint64_t* _
     next += n_runs;
     if (threadIdx.x == 0) level_off[d + 2] = next;
     n_active = n_keep;
+#pragma unroll
+    for (int u = 0; u < PF; ++u)
+      if (pf_it[u] != DC_NO_NODE) sm.next_frame[pf_it[u]] = pf_f[u];
+    __syncthreads();
   }
   if (threadIdx.x == 0) {
     d_N[0] = next;
