@@ -215,6 +215,48 @@ dc_status dc_hotspots_topk(dc_ctx* ctx, const dc_cct* cct, dc_view view, uint32_
 dc_status dc_cct_derived(dc_ctx* ctx, const dc_cct* cct, uint32_t metric, int incl, double* out_mean,
                          double* out_std);
 
+/* ------------------------------------------------------------- analyzer rules (NEXT-2)
+   The example analyses of §4.3 as device predicates over a complete, rolled-up tree.
+   Ratios are binary64 with single roundings; thresholds are the caller's (the paper fixes
+   none except the ratio 2 of ③). */
+typedef enum {
+  DC_RULE_SMALL_KERNELS = 2, /* ② kernel fusion: node n (not the root)
+                                qualifies if launches(n) > 0 and
+                                (double)isum[metric_a](n) / (double)launches(n) < threshold,
+                                launches(n) = xcnt summed over the nodes of n's subtree whose
+                                frame kind is in kind_mask (records ending at kernel frames) */
+  DC_RULE_CPU_LATENCY = 5    /* ⑤ CPU latency: n qualifies if
+                                isum[metric_a](n) > floor and
+                                (double)isum[metric_a] / (double)max(isum[metric_b], 1) > threshold
+                                (SPEC.md analyze_cpu_latency: max(.,1) guard, absolute floor) */
+} dc_rule;
+typedef struct {
+  uint32_t metric_a, metric_b, kind_mask, _pad;
+  double threshold;
+  uint64_t floor;
+} dc_rule_params;
+
+/* dc_analyze_flags — ids of the flagged nodes in breadth-first (= ascending id) order: a node
+   is flagged if it qualifies and no ancestor (the root excluded) qualifies — children of a
+   flagged frame are not re-flagged (SPEC.md analyze_kernel_fusion / analyze_cpu_latency,
+   reading R22). Writes the first min(total, cap) ids to out_ids_h (host) and *n_out_h = total.
+   Requires state ROLLED and a complete (not partitioned) tree. Synchronizes. */
+dc_status dc_analyze_flags(dc_ctx* ctx, const dc_cct* cct, dc_rule rule, const dc_rule_params* params,
+                           uint32_t* out_ids_h, uint32_t cap, uint32_t* n_out_h);
+
+typedef struct { uint32_t node, stall; uint64_t count; } dc_stall_issue;
+
+/* dc_analyze_stalls — analysis ④ (SPEC.md analyze_stalls): hotspots =
+   dc_hotspots_topk(INCLUSIVE, metric, kind_mask, hot_threshold, all); for each hotspot n in
+   that order, its instruction (PC) children c with (double)samples(c) / (double)isamples(n) >
+   stall_threshold; per stall reason s, the sum of bin(c, s) over those children; the non-zero
+   reasons ordered by (count desc, s asc), first k (<= 32) per hotspot, as {n, s, count}
+   entries. Writes the first min(total, cap) entries to out_h; *n_out_h = total. Requires
+   ROLLED. Synchronizes. */
+dc_status dc_analyze_stalls(dc_ctx* ctx, const dc_cct* cct, uint32_t metric, uint32_t kind_mask, double hot_threshold,
+                            double stall_threshold, uint32_t k, dc_stall_issue* out_h, uint32_t cap,
+                            uint32_t* n_out_h);
+
 /* ------------------------------------------------------------- borrowed view */
 typedef struct {
   uint64_t n_nodes, n_pc_nodes, n_bins, n_records;

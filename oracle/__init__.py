@@ -50,6 +50,8 @@ def lib():
         L.or_diag.argtypes = [P, P]
         L.or_get.argtypes = [P, P]
         L.or_topk.argtypes = [P, ctypes.c_int, u32, u32, P, u32, ctypes.c_double, u32, u32, P, P]
+        L.or_rule_flags.argtypes = [P, ctypes.c_int, u32, u32, u32, P, u32, ctypes.c_double, ctypes.c_uint64, P, u32, P]
+        L.or_stall_issues.argtypes = [P, u32, u32, P, u32, ctypes.c_double, ctypes.c_double, u32, P, u32, P]
         L.or_derived.argtypes = [P, u32, ctypes.c_int, P, P]
         L.or_u256_to_double.argtypes = [P]
         L.or_u256_to_double.restype = ctypes.c_double
@@ -64,6 +66,8 @@ def _p(a):
 KEY_DTYPE = np.dtype([("kind", "<u4"), ("str_id", "<u4"), ("addr", "<u8")])
 SAMPLE_DTYPE = np.dtype([("launch", "<u4"), ("pc_off", "<u4"), ("stall", "<u2"), ("flags", "<u2"), ("count", "<u4")])
 TOPK_DTYPE = np.dtype([("id", "<u4"), ("pad", "<u4"), ("value", "<u8"), ("fraction", "<f8")])
+STALL_ISSUE_DTYPE = np.dtype([("node", "<u4"), ("stall", "<u4"), ("count", "<u8")])
+RULE_SMALL_KERNELS, RULE_CPU_LATENCY = 2, 5
 
 
 def as_keys(keys) -> np.ndarray:
@@ -177,6 +181,32 @@ class OracleCCT:
                            0 if fk is None else len(fk), float(threshold), k, stall_node, _p(out), ctypes.byref(n))
         assert rc == 0, rc
         return out[: n.value]
+
+    def rule_flags(self, rule: int, metric_a: int, metric_b: int = 0, kind_mask: int = 0xFFFFFFFF, frame_kind=None,
+                   threshold: float = 0.0, floor: int = 0, cap: int = 1 << 20):
+        """Analyses ② (rule 2) / ⑤ (rule 5): flagged canonical node ids in BFS order."""
+        if not self._final:
+            self.finalize()
+        out = np.zeros(max(cap, 1), np.uint32)
+        n = ctypes.c_uint32(0)
+        fk = None if frame_kind is None else np.ascontiguousarray(frame_kind, np.uint8)
+        rc = lib().or_rule_flags(self.h, rule, metric_a, metric_b, kind_mask & 0xFFFFFFFF, _p(fk), 0 if fk is None else len(fk),
+                                 float(threshold), int(floor), _p(out), cap, ctypes.byref(n))
+        assert rc == 0, rc
+        return out[: min(n.value, cap)].tolist()
+
+    def stall_issues(self, metric: int = 0, kind_mask: int = 0xFFFFFFFF, frame_kind=None, hot_threshold: float = 0.0,
+                     stall_threshold: float = 0.0, k: int = 3, cap: int = 1 << 16):
+        """Analysis ④: (hotspot node, stall, count) entries."""
+        if not self._final:
+            self.finalize()
+        out = np.zeros(max(cap, 1), STALL_ISSUE_DTYPE)
+        n = ctypes.c_uint32(0)
+        fk = None if frame_kind is None else np.ascontiguousarray(frame_kind, np.uint8)
+        rc = lib().or_stall_issues(self.h, metric & 0xFFFFFFFF, kind_mask & 0xFFFFFFFF, _p(fk), 0 if fk is None else len(fk),
+                                   float(hot_threshold), float(stall_threshold), k, _p(out), cap, ctypes.byref(n))
+        assert rc == 0, rc
+        return [(int(e["node"]), int(e["stall"]), int(e["count"])) for e in out[: min(n.value, cap)]]
 
     def derived(self, metric: int, incl: bool = True):
         if not self._final:

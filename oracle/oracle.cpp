@@ -35,6 +35,14 @@
 //                     hotspot_threshold` with total = root; bottom-up
 //                     aggregation of the same frame across call paths; stall
 //                     top-k of analysis ④.
+//  * or_rule_flags  — example analyses ② "Small GPU kernels" and ⑤ "CPU
+//                     time abnormality" over `bfs(call_tree.nodes)`, with
+//                     SPEC.md's readings (launch count of the frame's kernels, max(gpu, 1)
+//                     guard, absolute floor, children of a flagged frame not re-flagged;
+//                     DESIGN.md reading R22). Literal BFS over the canonical tree.
+//  * or_stall_issues — analysis ④: for n in hotspots, its children c with
+//                     c.stalls > stall_threshold, topk(stall reasons) (SPEC.md analyze_stalls:
+//                     the threshold is a fraction of the kernel's samples; reading R23).
 //  * or_derived     — average and (population) standard deviation (reading
 //                     R7): mean = sum/count, std = sqrt(count*sumsq - sum^2)/count with the
 //                     radicand formed exactly in a hand-rolled 256-bit integer and rounded
@@ -316,6 +324,93 @@ int or_topk(const OrCct* c, int view, uint32_t metric, uint32_t kind_mask, const
   uint32_t m = (uint32_t)std::min<size_t>(k, keep.size());
   for (uint32_t j = 0; j < m; ++j) out[j] = keep[j];
   *n_out = m;
+  return 0;
+}
+
+// ---------------------------------------------------------------- analyzer rules
+enum { OR_RULE_SMALL_KERNELS = 2, OR_RULE_CPU_LATENCY = 5 };
+
+int or_rule_flags(const OrCct* c, int rule, uint32_t metric_a, uint32_t metric_b, uint32_t kind_mask, const uint8_t* frame_kind,
+                  uint32_t n_frames, double threshold, uint64_t floor_v, uint32_t* out, uint32_t cap, uint32_t* n_out) {
+  *n_out = 0;
+  if (!c->final_) return 1;
+  if (metric_a >= c->M || (rule == OR_RULE_CPU_LATENCY && metric_b >= c->M)) return 2;
+  if (rule != OR_RULE_SMALL_KERNELS && rule != OR_RULE_CPU_LATENCY) return 2;
+  const size_t N = c->order.size();
+  // launches(n): kernel launches in n's subtree = xcnt of every kernel-kind node, propagated
+  // to each ancestor one node at a time (the root is not a frame and is not considered)
+  std::vector<uint64_t> launches(N, 0);
+  for (size_t id = 1; id < N; ++id) {
+    const TNode& n = c->t[c->order[id]];
+    if (!kind_ok(frame_kind, n_frames, n.frame, kind_mask) || n.xcnt == 0) continue;
+    for (uint32_t tn = c->order[id]; tn != 0; tn = c->t[tn].parent) launches[c->canon[tn]] += n.xcnt;
+  }
+  auto qualifies = [&](size_t id) -> bool {
+    const TNode& n = c->t[c->order[id]];
+    if (rule == OR_RULE_SMALL_KERNELS)  // n.gpu_time / n.count < gpu_threshold
+      return launches[id] > 0 && (double)n.i[metric_a].sum / (double)launches[id] < threshold;
+    const uint64_t cpu = n.i[metric_a].sum, gpu = n.i[metric_b].sum;  // n.cpu_time / n.gpu_time > cpu_threshold
+    return cpu > floor_v && (double)cpu / (double)(gpu > 0 ? gpu : 1) > threshold;
+  };
+  // for n in bfs(call_tree.nodes): canonical ids are breadth-first (reading R2), so ascending
+  // id order is the BFS; a node below a flagged frame is not re-flagged
+  std::vector<char> flagged(N, 0), below(N, 0);
+  std::vector<uint32_t> res;
+  for (size_t id = 1; id < N; ++id) {
+    const uint32_t p = c->canon[c->t[c->order[id]].parent];
+    below[id] = p != 0 && (below[p] || flagged[p]);
+    if (!below[id] && qualifies(id)) {
+      flagged[id] = 1;
+      res.push_back((uint32_t)id);
+    }
+  }
+  for (size_t j = 0; j < res.size() && j < cap; ++j) out[j] = res[j];
+  *n_out = (uint32_t)res.size();
+  return 0;
+}
+
+struct OrStallIssue { uint32_t node, stall; uint64_t count; };
+
+int or_stall_issues(const OrCct* c, uint32_t metric, uint32_t kind_mask, const uint8_t* frame_kind, uint32_t n_frames,
+                    double hot_threshold, double stall_threshold, uint32_t k, OrStallIssue* out, uint32_t cap,
+                    uint32_t* n_out) {
+  *n_out = 0;
+  if (!c->final_) return 1;
+  if (k > 32) k = 32;
+  // hotspots = hotspot_analysis(call_tree)
+  std::vector<OrTopk> hot(c->order.size());
+  uint32_t nh = 0;
+  int rc = or_topk(c, OR_VIEW_INCLUSIVE, metric, kind_mask, frame_kind, n_frames, hot_threshold, (uint32_t)c->order.size(),
+                   0, hot.data(), &nh);
+  if (rc) return rc;
+  uint32_t w = 0, total = 0;
+  const uint32_t Nn = (uint32_t)c->order.size();
+  for (uint32_t h = 0; h < nh; ++h) {
+    const uint32_t node = hot[h].id;
+    const uint64_t ksamples = c->t[c->order[node]].isamples;
+    // for c in n.children (the instruction children): c.stalls = its samples
+    std::map<uint32_t, uint64_t> pc_total;                 // pc node id -> samples
+    for (const auto& b : c->cbins) {
+      const uint32_t pn = std::get<0>(b);
+      if (c->pcs[pn - Nn].first == node) pc_total[pn] += std::get<2>(b);
+    }
+    std::map<uint16_t, uint64_t> reasons;                  // stall -> count over the kept children
+    for (const auto& b : c->cbins) {
+      const uint32_t pn = std::get<0>(b);
+      if (c->pcs[pn - Nn].first != node) continue;
+      if (ksamples > 0 && (double)pc_total[pn] / (double)ksamples > stall_threshold) reasons[std::get<1>(b)] += std::get<2>(b);
+    }
+    std::vector<std::pair<uint64_t, uint16_t>> r;          // stall_reasons = topk(stalls)
+    for (auto& kv : reasons)
+      if (kv.second) r.push_back({kv.second, kv.first});
+    std::sort(r.begin(), r.end(), [](const std::pair<uint64_t, uint16_t>& a, const std::pair<uint64_t, uint16_t>& b) {
+      if (a.first != b.first) return a.first > b.first;
+      return a.second < b.second;
+    });
+    for (size_t j = 0; j < r.size() && j < k; ++j, ++total)
+      if (w < cap) out[w++] = OrStallIssue{node, r[j].second, r[j].first};
+  }
+  *n_out = total;
   return 0;
 }
 

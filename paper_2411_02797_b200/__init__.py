@@ -19,6 +19,8 @@ import ctypes
 import numpy as np
 import torch
 
+from . import _lib
+
 from ._lib import (DC_KIND_API, DC_KIND_INSTR, DC_KIND_KERNEL, DC_KIND_NATIVE, DC_KIND_OP, DC_KIND_PY,  # noqa: F401
                    DC_METRIC_SAMPLES, DC_NO_NODE, DC_VIEW_BOTTOM_UP, DC_VIEW_EXCLUSIVE, DC_VIEW_INCLUSIVE, DC_VIEW_STALL,
                    DcError, dc_cct_view, dc_diag, dc_paths, dc_topk_entry, lib)
@@ -248,6 +250,34 @@ def dc_hotspots_topk(ctx: Context, cct: CCT, view: int, metric: int = 0, kind_ma
                                      int(k), int(stall_node), ctypes.cast(out, ctypes.c_void_p), ctypes.byref(n)),
               "dc_hotspots_topk")
     return [(int(out[i].id), int(out[i].value), float(out[i].fraction)) for i in range(n.value)]
+
+
+DC_RULE_SMALL_KERNELS = 2
+DC_RULE_CPU_LATENCY = 5
+
+
+def dc_analyze_flags(ctx: Context, cct: CCT, rule: int, metric_a: int, metric_b: int = 0, kind_mask: int = 0xFFFFFFFF,
+                     threshold: float = 0.0, floor: int = 0, cap: int = 1 << 16) -> list[int]:
+    """Analyzer rules ② (small kernels) / ⑤ (CPU latency) as device predicates: flagged node ids,
+    breadth-first order (include/dc.h dc_analyze_flags)."""
+    prm = _lib.dc_rule_params(metric_a=metric_a, metric_b=metric_b, kind_mask=kind_mask & 0xFFFFFFFF,
+                              threshold=float(threshold), floor=int(floor))
+    out = (ctypes.c_uint32 * max(cap, 1))()
+    n = ctypes.c_uint32(0)
+    ctx.check(lib().dc_analyze_flags(ctx.h, cct.h, int(rule), ctypes.byref(prm), ctypes.cast(out, ctypes.c_void_p), int(cap),
+                                     ctypes.byref(n)), "dc_analyze_flags")
+    return [int(out[i]) for i in range(min(n.value, cap))]
+
+
+def dc_analyze_stalls(ctx: Context, cct: CCT, metric: int = 0, kind_mask: int = 0xFFFFFFFF, hot_threshold: float = 0.0,
+                      stall_threshold: float = 0.0, k: int = 3, cap: int = 1 << 16) -> list[tuple[int, int, int]]:
+    """Analysis ④: (hotspot node, stall reason, count) entries (include/dc.h dc_analyze_stalls)."""
+    out = (_lib.dc_stall_issue * max(cap, 1))()
+    n = ctypes.c_uint32(0)
+    ctx.check(lib().dc_analyze_stalls(ctx.h, cct.h, int(metric), kind_mask & 0xFFFFFFFF, float(hot_threshold),
+                                      float(stall_threshold), int(k), ctypes.cast(out, ctypes.c_void_p), int(cap),
+                                      ctypes.byref(n)), "dc_analyze_stalls")
+    return [(int(out[i].node), int(out[i].stall), int(out[i].count)) for i in range(min(n.value, cap))]
 
 
 def dc_cct_derived(ctx: Context, cct: CCT, metric: int, incl: bool = True):

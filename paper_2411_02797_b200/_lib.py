@@ -38,6 +38,14 @@ class dc_topk_entry(ctypes.Structure):
     _fields_ = [("id", u32), ("_pad", u32), ("value", u64), ("fraction", f64)]
 
 
+class dc_rule_params(ctypes.Structure):
+    _fields_ = [("metric_a", u32), ("metric_b", u32), ("kind_mask", u32), ("_pad", u32), ("threshold", f64), ("floor", u64)]
+
+
+class dc_stall_issue(ctypes.Structure):
+    _fields_ = [("node", u32), ("stall", u32), ("count", u64)]
+
+
 class dc_diag(ctypes.Structure):
     _fields_ = [(n, u64) for n in ["empty_paths", "samples_bad_launch", "samples_bad_stall", "samples_zero_count",
                                    "collisions_detected", "levels_built", "max_depth_seen", "bytes_moved_est"]]
@@ -80,6 +88,8 @@ def lib():
             "dc_pc_sample_attribute": (i32, [P, P, P, u64, P, u64, P, u32]),
             "dc_hotspots_topk": (i32, [P, P, i32, u32, u32, f64, u32, u32, P, ctypes.POINTER(u32)]),
             "dc_cct_derived": (i32, [P, P, u32, i32, P, P]),
+            "dc_analyze_flags": (i32, [P, P, i32, ctypes.POINTER(dc_rule_params), P, u32, ctypes.POINTER(u32)]),
+            "dc_analyze_stalls": (i32, [P, P, u32, u32, f64, f64, u32, P, u32, ctypes.POINTER(u32)]),
             "dc_cct_view_get": (i32, [P, ctypes.POINTER(dc_cct_view)]),
             "dc_cct_free": (None, [P]),
             "dc_nccl_unique_id": (i32, [P]),

@@ -7,7 +7,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libdc.so")
-SOURCES = ["capi.cu", "intern.cu", "build.cu", "columns.cu", "pc.cu", "pc_owner.cu", "views.cu", "merge.cu"]
+SOURCES = ["capi.cu", "intern.cu", "build.cu", "columns.cu", "pc.cu", "pc_owner.cu", "views.cu", "merge.cu", "rules.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -16,6 +16,10 @@ dc_status attribute_metrics(Ctx* c, dc_cct* t, const uint32_t* leaf, uint64_t R,
 dc_status rollup(Ctx* c, dc_cct* t);
 dc_status pc_attribute(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, const uint32_t* launch_leaf, uint64_t n_launch,
                        const uint64_t* launch_off, uint32_t S);
+dc_status analyze_flags(Ctx* c, const dc_cct* t, dc_rule rule, const dc_rule_params* p, uint32_t* out_h, uint32_t cap,
+                        uint32_t* n_out_h);
+dc_status analyze_stalls(Ctx* c, const dc_cct* t, uint32_t metric, uint32_t kind_mask, double hot_threshold,
+                         double stall_threshold, uint32_t k, dc_stall_issue* out_h, uint32_t cap, uint32_t* n_out_h);
 dc_status hotspots_topk(Ctx* c, const dc_cct* t, dc_view view, uint32_t metric, uint32_t kind_mask, double threshold,
                         uint32_t k, uint32_t stall_node, dc_topk_entry* out_h, uint32_t* n_out_h);
 dc_status derived(Ctx* c, const dc_cct* t, uint32_t metric, int incl, double* mean, double* stdv);
@@ -378,6 +382,24 @@ dc_status dc_hotspots_topk(dc_ctx* ctx, const dc_cct* cct, dc_view view, uint32_
   ON_DEVICE(ctx);
   Region rg(ctx, "topk");
   return hotspots_topk(ctx, cct, view, metric, kind_mask, threshold, k, stall_node, out_h, n_out_h);
+}
+
+dc_status dc_analyze_flags(dc_ctx* ctx, const dc_cct* cct, dc_rule rule, const dc_rule_params* params, uint32_t* out_ids_h,
+                           uint32_t cap, uint32_t* n_out_h) {
+  CHECK_CTX(ctx);
+  ARG(cct && params && n_out_h && (cap == 0 || out_ids_h), "bad arguments");
+  ON_DEVICE(ctx);
+  Region rg(ctx, "rules");
+  return analyze_flags(ctx, cct, rule, params, out_ids_h, cap, n_out_h);
+}
+
+dc_status dc_analyze_stalls(dc_ctx* ctx, const dc_cct* cct, uint32_t metric, uint32_t kind_mask, double hot_threshold,
+                            double stall_threshold, uint32_t k, dc_stall_issue* out_h, uint32_t cap, uint32_t* n_out_h) {
+  CHECK_CTX(ctx);
+  ARG(cct && n_out_h && (cap == 0 || out_h), "bad arguments");
+  ON_DEVICE(ctx);
+  Region rg(ctx, "rules");
+  return analyze_stalls(ctx, cct, metric, kind_mask, hot_threshold, stall_threshold, k, out_h, cap, n_out_h);
 }
 
 dc_status dc_cct_derived(dc_ctx* ctx, const dc_cct* cct, uint32_t metric, int incl, double* out_mean, double* out_std) {

@@ -1,0 +1,214 @@
+// rules.cu — SURVEY §8(f) NEXT-2: the analyzer's rule predicates as device kernels over the
+// rolled-up CCT (readings R22-R24).
+//   ② small kernels (SPEC.md analyze_kernel_fusion): breadth-first over the
+//      frame nodes, n qualifies if launches(n) > 0 and gpu_time(n) / launches(n) < threshold,
+//      launches(n) = records in n's subtree that end at a frame of the kernel kind mask,
+//      gpu_time(n) = inclusive sum of the time metric; a qualifying node is flagged unless an
+//      ancestor qualifies ("children of a flagged node are not re-flagged").
+//   ⑤ CPU latency (SPEC.md analyze_cpu_latency): n qualifies if
+//      cpu(n) / max(gpu(n), 1) > threshold and cpu(n) > floor; same ancestor suppression.
+//   ④ stalls (SPEC.md analyze_stalls): for every hotspot (view ①), its
+//      instruction (PC) children whose samples / the hotspot's samples > stall_threshold; their
+//      stall counts summed per reason; top-k reasons by (count desc, reason asc).
+// Ratios are formed in binary64 with single roundings (__ddiv_rn), as in the oracle.
+#include "prim.cuh"
+
+namespace dc {
+
+dc_status hotspots_topk(Ctx* c, const dc_cct* t, dc_view view, uint32_t metric, uint32_t kind_mask, double threshold, uint32_t k,
+                        uint32_t stall_node, dc_topk_entry* out_h, uint32_t* n_out_h);
+
+__device__ __forceinline__ bool rule_kind_ok(const uint8_t* fk, uint32_t n_frames, uint32_t f, uint32_t mask) {
+  if (!fk) return true;
+  if (f >= n_frames) return false;
+  const uint32_t k = fk[f];
+  return k < 32 && ((mask >> k) & 1u);
+}
+__device__ __forceinline__ double rdiv(uint64_t a, uint64_t b) { return __ddiv_rn(__ull2double_rn(a), __ull2double_rn(b)); }
+
+// launches(n) = sum of xcnt over masked-kind nodes of n's subtree: own value + push to ancestors
+__global__ void k_rule_launches(const uint32_t* __restrict__ parent, const uint32_t* __restrict__ frame,
+                                const uint8_t* __restrict__ fk, uint32_t n_frames, uint32_t mask,
+                                const uint64_t* __restrict__ xcnt, uint64_t N, unsigned long long* __restrict__ il) {
+  for (uint64_t n = 1 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; n < N; n += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t v = rule_kind_ok(fk, n_frames, frame[n], mask) ? xcnt[n] : 0;
+    if (!v) continue;
+    atomicAdd(il + n, (unsigned long long)v);
+    for (uint32_t a = parent[n], prev = (uint32_t)n; a < prev && a != 0; prev = a, a = parent[a]) atomicAdd(il + a, (unsigned long long)v);
+  }
+}
+
+__global__ void k_rule_qualify(int rule, uint64_t N, const uint64_t* __restrict__ a, const uint64_t* __restrict__ b,
+                               const uint64_t* __restrict__ il, double threshold, uint64_t floor, uint8_t* __restrict__ q) {
+  for (uint64_t n = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; n < N; n += (uint64_t)gridDim.x * blockDim.x) {
+    bool ok = false;
+    if (n > 0) {
+      if (rule == DC_RULE_SMALL_KERNELS) {
+        const uint64_t l = il[n];
+        ok = l > 0 && rdiv(a[n], l) < threshold;
+      } else {
+        const uint64_t cpu = a[n], gpu = b[n];
+        ok = cpu > floor && rdiv(cpu, gpu > 0 ? gpu : 1) > threshold;
+      }
+    }
+    q[n] = ok ? 1 : 0;
+  }
+}
+
+// flagged = qualifies and no proper (non-root) ancestor qualifies
+__global__ void k_rule_suppress(const uint32_t* __restrict__ parent, uint64_t N, const uint8_t* __restrict__ q,
+                                uint32_t* __restrict__ flag) {
+  for (uint64_t n = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; n < N; n += (uint64_t)gridDim.x * blockDim.x) {
+    bool f = q[n] != 0;
+    if (f)
+      for (uint32_t a = parent[n], prev = (uint32_t)n; a < prev && a != 0; prev = a, a = parent[a])
+        if (q[a]) {
+          f = false;
+          break;
+        }
+    flag[n] = f ? 1u : 0u;
+  }
+}
+
+__global__ void k_rule_emit(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos, uint64_t N, uint32_t cap,
+                            uint32_t* __restrict__ out) {
+  for (uint64_t n = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; n < N; n += (uint64_t)gridDim.x * blockDim.x)
+    if (flag[n] && pos[n] < cap) out[pos[n]] = (uint32_t)n;
+}
+
+dc_status analyze_flags(Ctx* c, const dc_cct* t, dc_rule rule, const dc_rule_params* p, uint32_t* out_h, uint32_t cap,
+                        uint32_t* n_out_h) {
+  *n_out_h = 0;
+  if (t->state != 2) return fail(c, DC_ERR_STATE, "dc_analyze_flags needs a rolled-up tree (call dc_cct_rollup)");
+  if (t->partition) return fail(c, DC_ERR_STATE, "dc_analyze_flags needs a complete tree (gather the partitions first)");
+  if (rule != DC_RULE_SMALL_KERNELS && rule != DC_RULE_CPU_LATENCY) return fail(c, DC_ERR_ARG, "unknown rule %d", (int)rule);
+  if (p->metric_a >= t->M || (rule == DC_RULE_CPU_LATENCY && p->metric_b >= t->M))
+    return fail(c, DC_ERR_ARG, "metric out of range (M = %u)", t->M);
+  const uint64_t N = t->N;
+  Buf<unsigned long long> il;
+  Buf<uint8_t> q;
+  Buf<uint32_t> flag, pos, cnt, out;
+  if (rule == DC_RULE_SMALL_KERNELS) {
+    DC_TRY(alloc_zero(c, il, N));
+    k_rule_launches<<<grid_for(c, N, 256), 256, 0, c->stream>>>(t->parent, t->frame, t->frame_kind, t->n_frames, p->kind_mask,
+                                                               t->xcnt, N, il.p);
+    DC_LAUNCHED(c);
+  }
+  DC_TRY(alloc(c, q, N));
+  DC_TRY(alloc(c, flag, N));
+  DC_TRY(alloc(c, pos, N));
+  DC_TRY(alloc(c, cnt, 1));
+  DC_TRY(alloc(c, out, cap ? cap : 1));
+  k_rule_qualify<<<grid_for(c, N, 256), 256, 0, c->stream>>>((int)rule, N, t->col(C_ISUM, p->metric_a),
+                                                             rule == DC_RULE_CPU_LATENCY ? t->col(C_ISUM, p->metric_b) : nullptr,
+                                                             (const uint64_t*)il.p, p->threshold, p->floor, q.p);
+  DC_LAUNCHED(c);
+  k_rule_suppress<<<grid_for(c, N, 256), 256, 0, c->stream>>>(t->parent, N, q.p, flag.p);
+  DC_LAUNCHED(c);
+  DC_TRY(excl_scan<uint32_t>(c, flag.p, pos.p, N, cnt.p));
+  k_rule_emit<<<grid_for(c, N, 256), 256, 0, c->stream>>>(flag.p, pos.p, N, cap, out.p);
+  DC_LAUNCHED(c);
+  uint32_t nf = 0;
+  DC_TRY(readback(c, cnt.p, 4, &nf));
+  const uint32_t m = nf < cap ? nf : cap;
+  if (m) DC_TRY(readback(c, out.p, (size_t)m * 4, out_h));
+  *n_out_h = nf;  // total flagged; the first min(nf, cap) ids (ascending = breadth-first) are written
+  return DC_OK;
+}
+
+// ---- ④: one block per hotspot node
+constexpr int ST_THREADS = 256;
+__device__ __forceinline__ uint64_t lower_bound_u32(const uint32_t* a, uint64_t n, uint64_t v) {
+  uint64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) / 2;
+    if (a[mid] < v) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(ST_THREADS) k_stall_issues(const uint32_t* __restrict__ hot, uint64_t N, uint64_t Npc,
+                                                             uint64_t Nb, uint32_t S, const uint32_t* __restrict__ pc_ctx,
+                                                             const uint32_t* __restrict__ bin_pcnode,
+                                                             const uint16_t* __restrict__ bin_stall,
+                                                             const uint64_t* __restrict__ bin_count,
+                                                             const uint64_t* __restrict__ isamples, double stall_threshold,
+                                                             uint32_t k, unsigned long long* __restrict__ pc_tot,
+                                                             dc_stall_issue* __restrict__ out, uint32_t* __restrict__ n_out) {
+  __shared__ unsigned long long ss[32];
+  const uint32_t node = hot[blockIdx.x];
+  if (threadIdx.x < 32) ss[threadIdx.x] = 0;
+  const uint64_t plo = lower_bound_u32(pc_ctx, Npc, node), phi = lower_bound_u32(pc_ctx, Npc, (uint64_t)node + 1);
+  const uint64_t blo = lower_bound_u32(bin_pcnode, Nb, N + plo), bhi = lower_bound_u32(bin_pcnode, Nb, N + phi);
+  const uint64_t total = isamples[node];
+  __syncthreads();
+  // per-instruction sample totals (this block's PC nodes are its own: disjoint slices of pc_tot)
+  for (uint64_t b = blo + threadIdx.x; b < bhi; b += ST_THREADS)
+    atomicAdd(pc_tot + (bin_pcnode[b] - N), (unsigned long long)bin_count[b]);
+  __syncthreads();
+  for (uint64_t b = blo + threadIdx.x; b < bhi; b += ST_THREADS) {
+    const uint64_t pt = pc_tot[bin_pcnode[b] - N];
+    if (total > 0 && rdiv(pt, total) > stall_threshold && bin_stall[b] < 32)
+      atomicAdd(&ss[bin_stall[b]], (unsigned long long)bin_count[b]);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {  // rank the reasons: (count desc, reason asc), non-zero only
+    const uint32_t s = threadIdx.x;
+    const uint64_t v = s < S ? ss[s] : 0;
+    const bool ok = v > 0;
+    const uint32_t okm = __ballot_sync(0xffffffffu, ok);
+    uint32_t rank = 0;
+    for (uint32_t o = 0; o < 32; ++o) {
+      const uint64_t vo = __shfl_sync(0xffffffffu, v, o);
+      if (((okm >> o) & 1u) && (vo > v || (vo == v && o < s))) ++rank;
+    }
+    if (ok && rank < k) {
+      dc_stall_issue e;
+      e.node = node;
+      e.stall = s;
+      e.count = v;
+      out[(uint64_t)blockIdx.x * k + rank] = e;
+    }
+    if (s == 0) n_out[blockIdx.x] = min((uint32_t)__popc(okm), k);
+  }
+}
+
+dc_status analyze_stalls(Ctx* c, const dc_cct* t, uint32_t metric, uint32_t kind_mask, double hot_threshold,
+                         double stall_threshold, uint32_t k, dc_stall_issue* out_h, uint32_t cap, uint32_t* n_out_h) {
+  *n_out_h = 0;
+  if (t->state != 2) return fail(c, DC_ERR_STATE, "dc_analyze_stalls needs a rolled-up tree (call dc_cct_rollup)");
+  if (t->partition) return fail(c, DC_ERR_STATE, "dc_analyze_stalls needs a complete tree (gather the partitions first)");
+  if (k > 32) k = 32;
+  if (k == 0 || !t->xsamples || t->Nbins == 0) return DC_OK;
+  // hotspots (analysis ①), every one above the threshold, in (value desc, id asc) order
+  std::vector<dc_topk_entry> hs((size_t)t->N);
+  uint32_t nh = 0;
+  DC_TRY(hotspots_topk(c, t, DC_VIEW_INCLUSIVE, metric, kind_mask, hot_threshold, (uint32_t)t->N, 0, hs.data(), &nh));
+  if (nh == 0) return DC_OK;
+  std::vector<uint32_t> hid(nh);
+  for (uint32_t i = 0; i < nh; ++i) hid[i] = hs[i].id;
+  Buf<uint32_t> dhot, dn;
+  Buf<unsigned long long> pc_tot;
+  Buf<dc_stall_issue> dout;
+  DC_TRY(alloc(c, dhot, nh));
+  DC_TRY(alloc(c, dn, nh));
+  DC_TRY(alloc_zero(c, pc_tot, t->Npc));
+  DC_TRY(alloc(c, dout, (uint64_t)nh * k));
+  DC_CUDA(c, cudaMemcpyAsync(dhot.p, hid.data(), nh * 4, cudaMemcpyHostToDevice, c->stream));
+  k_stall_issues<<<nh, ST_THREADS, 0, c->stream>>>(dhot.p, t->N, t->Npc, t->Nbins, t->S, t->pc_ctx, t->bin_pcnode, t->bin_stall,
+                                                   t->bin_count, t->isamples, stall_threshold, k, pc_tot.p, dout.p, dn.p);
+  DC_LAUNCHED(c);
+  std::vector<uint32_t> hn(nh);
+  std::vector<dc_stall_issue> ho((size_t)nh * k);
+  DC_TRY(readback(c, dn.p, nh * 4, hn.data()));
+  DC_TRY(readback(c, dout.p, ho.size() * sizeof(dc_stall_issue), ho.data()));
+  uint32_t w = 0, total = 0;
+  for (uint32_t i = 0; i < nh; ++i)
+    for (uint32_t r = 0; r < hn[i]; ++r, ++total)
+      if (w < cap) out_h[w++] = ho[(size_t)i * k + r];
+  *n_out_h = total;
+  return DC_OK;
+}
+
+}  // namespace dc

@@ -1,0 +1,95 @@
+"""GPU parity of the analyzer rules (include/dc.h dc_analyze_flags /
+dc_analyze_stalls) against the oracle, element by element: random tiny traces (every frame
+counts as a kernel: no dictionary), config 2 (ResNet-50-shaped, kinds from the interned
+dictionary) and config 3 (PC samples: analysis ④)."""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from pipeline import gpu_run, oracle_run
+from test_oracle_pins import _rand_trace
+
+pytestmark = pytest.mark.gpu
+
+
+def _csr(paths):
+    off = np.zeros(len(paths) + 1, np.uint64)
+    off[1:] = np.cumsum([len(p) for p in paths])
+    fr = np.asarray([f for p in paths for f in p], np.uint32)
+    return off, fr
+
+
+def _samples(lst):
+    s = np.zeros(len(lst), oracle.SAMPLE_DTYPE)
+    for i, (l, pc, st, c) in enumerate(lst):
+        s[i] = (l, pc, st, 0, c)
+    return s
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_rules_random_vs_oracle(seed):
+    import paper_2411_02797_b200 as dc
+    rng = np.random.default_rng(9100 + seed)
+    ctx = dc.Context(0)
+    for _ in range(20):
+        paths, X, samples, S = _rand_trace(rng)
+        off, fr = _csr(paths)
+        A = 1 + max([f for p in paths for f in p] + [0])
+        Xa = np.asarray(X, np.uint64).reshape(len(X), -1)
+        smp = _samples(samples)
+        a = gpu_run(off, fr, Xa, n_frames=A, samples=smp, n_stall=S, ctx=ctx)
+        o = oracle_run(off, fr, Xa, len(X), smp, len(paths), S)
+        M = len(X)
+        vals = [v for row in X for v in row] or [1]
+        for rule in (dc.DC_RULE_SMALL_KERNELS, dc.DC_RULE_CPU_LATENCY):
+            ma, mb = int(rng.integers(0, M)), int(rng.integers(0, M))
+            thr = float(rng.choice([0.5, 2.0, float(np.median(vals)) + 0.5]))
+            floor = int(rng.choice([0, int(np.median(vals))]))
+            got = dc.dc_analyze_flags(ctx, a["_cct"], rule, ma, mb, 1 << 4, thr, floor)
+            exp = o.rule_flags(rule, ma, mb, kind_mask=1 << 4, threshold=thr, floor=floor)
+            assert got == exp, (rule, thr, floor)
+        for hot_thr, st_thr, k in [(0.0, 0.0, 3), (0.1, 0.2, 2), (0.3, 0.05, 5)]:
+            got = dc.dc_analyze_stalls(ctx, a["_cct"], 0, 0xFFFFFFFF, hot_thr, st_thr, k)
+            exp = o.stall_issues(0, hot_threshold=hot_thr, stall_threshold=st_thr, k=k)
+            assert got == exp, (hot_thr, st_thr, k)
+
+
+def test_rules_config2_vs_oracle():
+    """ResNet-50-shaped trace (raw keys, kinds from the dictionary): ② on gpu_time (metric 0)
+    over kernel launches; ⑤ with metric 2 (blocks) as the 'cpu' column against gpu_time."""
+    import paper_2411_02797_b200 as dc
+    p = gen.programs.program(2)
+    tr = gen.make_trace(p, n_records=120_000)
+    a = gpu_run(tr.offsets.numpy(), keys=tr.keys.numpy(), metrics=tr.metrics.numpy())
+    ctx = a["_ctx"]
+    oids, od = oracle.intern(tr.keys.numpy())
+    o = oracle_run(tr.offsets.numpy(), oids, tr.metrics.numpy(), p.n_metrics)
+    fk = np.asarray(od["kind"], np.uint8)
+    for thr in (5_000.0, 20_000.0, 60_000.0):
+        got = dc.dc_analyze_flags(ctx, a["_cct"], dc.DC_RULE_SMALL_KERNELS, 0, 0, 1 << dc.DC_KIND_KERNEL, thr)
+        exp = o.rule_flags(oracle.RULE_SMALL_KERNELS, 0, kind_mask=1 << dc.DC_KIND_KERNEL, frame_kind=fk, threshold=thr)
+        assert got == exp and (thr < 10_000 or got), thr
+    for thr in (0.01, 0.5):
+        got = dc.dc_analyze_flags(ctx, a["_cct"], dc.DC_RULE_CPU_LATENCY, 2, 0, 0, thr, 1000)
+        exp = o.rule_flags(oracle.RULE_CPU_LATENCY, 2, 0, threshold=thr, floor=1000)
+        assert got == exp, thr
+
+
+def test_stalls_config3_vs_oracle():
+    """Analysis ④ on an LLM-decode-shaped PC-sampling trace (kinds from the dictionary)."""
+    import paper_2411_02797_b200 as dc
+    p = gen.programs.config3(n_samples=3_000_000)
+    tr = gen.make_trace(p, pc=True, bad_per_million=200)
+    a = gpu_run(tr.offsets.numpy(), keys=tr.keys.numpy(), metrics=tr.metrics.numpy(), samples=tr.samples.numpy(),
+                launch_off=tr.launch_off.numpy(), n_launch=tr.n_launch)
+    ctx = a["_ctx"]
+    oids, od = oracle.intern(tr.keys.numpy())
+    o = oracle_run(tr.offsets.numpy(), oids, tr.metrics.numpy(), p.n_metrics, tr.samples.numpy(), tr.n_launch)
+    fk = np.asarray(od["kind"], np.uint8)
+    for hot_thr, st_thr, k in [(0.01, 0.02, 3), (0.0, 0.0, 5), (0.05, 0.1, 1)]:
+        got = dc.dc_analyze_stalls(ctx, a["_cct"], 0, 1 << dc.DC_KIND_KERNEL, hot_thr, st_thr, k)
+        exp = o.stall_issues(0, kind_mask=1 << dc.DC_KIND_KERNEL, frame_kind=fk, hot_threshold=hot_thr,
+                             stall_threshold=st_thr, k=k)
+        assert got == exp, (hot_thr, st_thr, k)
+        assert got or hot_thr > 0.0

@@ -1,0 +1,149 @@
+"""Pins of the oracle's analyzer rules against the paper / SPEC worked
+examples and a brute-force definition on random trees (independent of oracle/: the CCT is
+rebuilt from distinct prefixes by tests/bruteforce.py).
+
+② small kernels, PAPER.md:398-404 `n.gpu_time / n.count < gpu_threshold` over bfs(nodes);
+⑤ CPU latency, PAPER.md:428-434 `n.cpu_time / n.gpu_time > cpu_threshold`;
+④ fine-grained stalls; readings R22-R23 from SPEC.md
+analyze_kernel_fusion / analyze_cpu_latency / analyze_stalls.
+"""
+import numpy as np
+import pytest
+
+import bruteforce as bf
+import oracle
+from test_oracle_pins import _rand_trace, run
+
+KERNEL = 4
+PY = 0
+
+
+def test_spec_kernel_fusion_transformer_fixture():
+    """SPEC.md analyze_kernel_fusion: loss_fn launches softmax, copy and
+    nll_loss with equal counts and short kernels -> flagged at loss_fn, its kernels not
+    re-flagged; a frame with 1 ms kernels is not flagged (threshold 20 us)."""
+    # frames: 0 train.py:10, 1 loss_fn, 2 model_fwd (PY); 3 softmax, 4 copy, 5 nll_loss, 6 gemm (KERNEL)
+    fk = np.array([PY, PY, PY, KERNEL, KERNEL, KERNEL, KERNEL], np.uint8)
+    paths, ns = [], []
+    for k in (3, 4, 5):
+        paths += [(0, 1, k)] * 100
+        ns += [5_000] * 100
+    paths += [(0, 2, 6)] * 100
+    ns += [1_000_000] * 100
+    o = run(paths, [ns])
+    ids = {tuple(q): i for i, q in enumerate(bf.cct(paths, [ns])["order"])}
+    got = o.rule_flags(oracle.RULE_SMALL_KERNELS, 0, kind_mask=1 << KERNEL, frame_kind=fk, threshold=20_000.0)
+    assert got == [ids[(0, 1)]]
+    # one kernel of 1 ms, threshold 20 us -> nothing (SPEC.md: TRIVIAL)
+    o2 = run([(0, 6)], [[1_000_000]])
+    assert o2.rule_flags(oracle.RULE_SMALL_KERNELS, 0, kind_mask=1 << KERNEL, frame_kind=fk, threshold=20_000.0) == []
+
+
+def test_spec_cpu_latency_fixtures():
+    """SPEC.md analyze_cpu_latency: U-Net data_selection (69 % of CPU time, 1.3 s GPU) flagged;
+    zero GPU time with 50 ms CPU and threshold 5 flagged through max(gpu, 1); a balanced frame
+    not flagged; the 1 ms floor."""
+    # metric 0 = cpu ns, metric 1 = gpu ns; frames 0 main, 1 data_selection, 2 train_step, 3 idle, 4 balanced
+    paths = [(0, 1), (0, 2), (0, 3), (0, 4), (0, 4)]
+    cpu = [69_000_000_000, 31_000_000_000, 50_000_000, 2_000_000, 2_000_000]
+    gpu = [1_300_000_000, 40_000_000_000, 0, 2_000_000, 2_000_000]
+    o = run(paths, [cpu, gpu])
+    ids = {tuple(q): i for i, q in enumerate(bf.cct(paths, [cpu, gpu])["order"])}
+    got = o.rule_flags(oracle.RULE_CPU_LATENCY, 0, 1, threshold=5.0, floor=1_000_000)
+    assert got == [ids[(0, 1)], ids[(0, 3)]]
+    # the floor: 50 ms of CPU below a 100 ms floor is not flagged
+    assert o.rule_flags(oracle.RULE_CPU_LATENCY, 0, 1, threshold=5.0, floor=100_000_000) == [ids[(0, 1)]]
+
+
+def test_spec_stall_issue_fixture():
+    """SPEC.md analyze_stalls: hotspot kernel with {math_dep: 60, const_mem_miss: 30, other: 10}
+    of 100 samples on three instructions, threshold 0.2, k = 2 -> [math_dep, const_mem_miss]
+    (PAPER.md:699-702 names both reasons for the Llama3 RMSNorm kernel)."""
+    MATH, CONST, OTHER = 3, 7, 19
+    paths = [(0, 1)]
+    samples = [(0, 0xA0, MATH, 60), (0, 0xB0, CONST, 30), (0, 0xC0, OTHER, 10)]
+    o = run(paths, [[100]], samples, n_stall=24)
+    got = o.stall_issues(0, hot_threshold=0.5, stall_threshold=0.2, k=2)
+    assert got == [(2, MATH, 60), (2, CONST, 30)]
+    # an instruction mixing reasons counts all of its reasons once it passes the threshold
+    samples = [(0, 0xA0, MATH, 50), (0, 0xA0, OTHER, 5), (0, 0xB0, CONST, 10), (0, 0xC0, OTHER, 35)]
+    o = run(paths, [[100]], samples, n_stall=24)
+    assert o.stall_issues(0, hot_threshold=0.5, stall_threshold=0.2, k=3) == [(2, MATH, 50), (2, OTHER, 40)]
+    # a kernel with no instruction samples -> no issue (SPEC.md: TRIVIAL)
+    o = run(paths, [[100]], [], n_stall=24)
+    assert o.stall_issues(0, hot_threshold=0.5, stall_threshold=0.2, k=3) == []
+
+
+def _bf_flags(b, paths, X, rule, ma, mb, fk, mask, thr, floor):
+    """Flagged ids by the plain definition: BFS (= (depth, lex) order), ancestor suppression."""
+    N = b["n_nodes"]
+    order = b["order"]
+    launches = [0] * N
+    for r, p in enumerate(paths):
+        if p and (fk is None or (int(fk[p[-1]]) < 32 and (mask >> int(fk[p[-1]])) & 1)):
+            for d in range(1, len(p) + 1):
+                launches[b["ids"][tuple(p[:d])]] += 1
+
+    def q(i):
+        if rule == 2:
+            return launches[i] > 0 and b["isum"][ma][i] / launches[i] < thr
+        cpu, gpu = b["isum"][ma][i], b["isum"][mb][i]
+        return cpu > floor and cpu / max(gpu, 1) > thr
+
+    flagged = []
+    for i in range(1, N):
+        anc = [b["ids"][order[i][:d]] for d in range(1, len(order[i]))]
+        if q(i) and not any(q(a) for a in anc):
+            flagged.append(i)
+    return flagged
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_rules_bruteforce_random(seed):
+    rng = np.random.default_rng(7000 + seed)
+    for _ in range(60):
+        paths, X, samples, S = _rand_trace(rng)
+        A = 1 + max([f for p in paths for f in p] + [0])
+        fk = rng.integers(0, 6, size=A).astype(np.uint8)
+        b = bf.cct(paths, X)
+        o = run(paths, X)
+        M = len(X)
+        for rule in (2, 5):
+            ma, mb = int(rng.integers(0, M)), int(rng.integers(0, M))
+            vals = [v for row in X for v in row] or [1]
+            thr = float(rng.choice([0.5, 1.0, 2.0, float(np.median(vals)) + 0.5]))
+            floor = int(rng.choice([0, int(np.median(vals))]))
+            mask = int(rng.choice([1 << KERNEL, 0b110000, 0xFFFFFFFF]))
+            exp = _bf_flags(b, paths, X, rule, ma, mb, fk, mask, thr, floor)
+            got = o.rule_flags(rule, ma, mb, kind_mask=mask, frame_kind=fk, threshold=thr, floor=floor)
+            assert got == exp, (rule, thr, floor, mask)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_stall_issues_bruteforce_random(seed):
+    rng = np.random.default_rng(8100 + seed)
+    for _ in range(60):
+        paths, X, samples, S = _rand_trace(rng)
+        b = bf.cct(paths, X)
+        pcb = bf.pc_bins(b, paths, samples, len(paths), S)
+        o = run(paths, X, samples, n_stall=S)
+        hot_thr = float(rng.choice([0.0, 0.05, 0.2]))
+        st_thr = float(rng.choice([0.0, 0.1, 0.3]))
+        k = int(rng.integers(1, 5))
+        # hotspots by definition: all non-root nodes, inclusive metric 0, (value desc, id asc)
+        hot = bf.topk_nodes(b["isum"][0], b["isum"][0][0], list(range(1, b["n_nodes"])), hot_thr, b["n_nodes"])
+        exp = []
+        for (n, _, _) in hot:
+            kids = {pid: 0 for pid, (ctx, pc) in enumerate(pcb["pcs"], start=b["n_nodes"]) if ctx == n}
+            for (pid, s, c) in pcb["bins"]:
+                if pid in kids:
+                    kids[pid] += c
+            tot = pcb["isamples"][n]
+            reasons = {}
+            for (pid, s, c) in pcb["bins"]:
+                if pid in kids and tot > 0 and kids[pid] / tot > st_thr:
+                    reasons[s] = reasons.get(s, 0) + c
+            r = sorted(((c, s) for s, c in reasons.items() if c), key=lambda e: (-e[0], e[1]))[:k]
+            exp += [(n, s, c) for c, s in r]
+        got = o.stall_issues(0, hot_threshold=hot_thr, stall_threshold=st_thr, k=k)
+        assert got == exp
