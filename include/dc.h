@@ -301,7 +301,9 @@ dc_status dc_cct_merge_ranks(dc_ctx* ctx, dc_comm* comm, const dc_cct* local, co
 dc_status dc_cct_gather(dc_ctx* ctx, dc_comm* comm, const dc_cct* part, int root, dc_cct** out_canonical);
 /* Single-GPU emulation of merge_ranks + gather for P logical ranks (loopback exchange through
    device copies instead of NCCL; same partition/reduce/verify/canonicalise kernels).
-   locals[p] (ROLLED) with dicts[p]; returns the canonical merged tree and global dictionary. */
+   locals[p] (ROLLED) with dicts[p]; returns the canonical merged tree and global dictionary.
+   With P = 2 it is also the fold step of chunked / online aggregation:
+   merge(CCT of chunks 0..k-1, CCT of chunk k) = CCT of chunks 0..k (reading R19). */
 dc_status dc_cct_merge_local(dc_ctx* ctx, uint32_t P, dc_cct* const* locals, dc_dict* const* dicts, dc_cct** out_canonical,
                              dc_dict** out_global_dict);
 

@@ -338,6 +338,24 @@ def dc_cct_merge_local(ctx: Context, locals_: list, dicts: list):
     return CCT(out, ctx), Dict(gd)
 
 
+def aggregate_chunks(ctx: Context, chunks):
+    """SURVEY §8(f) NEXT-1, chunked / online aggregation: fold an iterable of (rolled-up CCT,
+    dictionary) pairs — each built from one chunk of the trace with the dc_* calls — into one
+    canonical CCT with dc_cct_merge_local (the cross-rank merge's partition / reduce / verify /
+    canonicalise kernels with a loopback exchange). The result equals the CCT of the
+    concatenated chunks (reading R19); inputs are freed as they are folded."""
+    acc = accd = None
+    for cct, d in chunks:
+        if acc is None:
+            acc, accd = cct, d
+            continue
+        merged, md = dc_cct_merge_local(ctx, [acc, cct], [accd, d])
+        acc.free()
+        cct.free()
+        acc, accd = merged, md
+    return acc, accd
+
+
 def dc_cct_gather(ctx: Context, comm: Comm, part: CCT, root: int = 0):
     h = ctypes.c_void_p()
     ctx.check(lib().dc_cct_gather(ctx.h, comm.h, part.h, int(root), ctypes.byref(h)), "dc_cct_gather")

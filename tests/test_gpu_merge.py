@@ -103,3 +103,17 @@ def test_merge_collision_is_detected(monkeypatch):
     with pytest.raises(dc.DcError) as e:
         dc.dc_cct_merge_local(ctx, [c for c, _ in parts], [d for _, d in parts])
     assert e.value.status == 7
+
+
+def test_chunked_online_aggregation_config3():
+    """NEXT-1: a config-3-shaped trace ingested in 4 chunks (records + their PC samples), each
+    built into its own CCT, folded with aggregate_chunks == the oracle's CCT of the whole trace."""
+    import paper_2411_02797_b200 as dc
+    ctx = dc.Context(0)
+    p = gen.programs.config3(n_samples=2_000_000)
+    tr = gen.make_trace(p, pc=True, bad_per_million=300)
+    chunks = (_shard_run(dc, ctx, **sh) for sh in _split(tr, 4, with_pc=True))
+    acc, d = dc.aggregate_chunks(ctx, chunks)
+    o, od = _oracle_concat(tr, p.n_metrics, with_pc=True)
+    assert np.array_equal(d.keys(), od)
+    assert_same(acc.to_numpy(), o.arrays(), ctx="chunked")
