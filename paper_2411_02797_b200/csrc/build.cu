@@ -31,9 +31,9 @@ __device__ __forceinline__ int bits_for_dev(uint32_t v) { return v ? 32 - __clz(
 //     mbarrier, double-buffered: the copy of the next tile is in flight while this one is
 //     hashed) together with the tile's offsets. Each record is cut into chunks of PT_CH frames
 //     (odd, so the chunks a warp works on start in different shared-memory banks); a thread per
-//     chunk accumulates two 32-bit position-keyed sums f*A[j] and (f^K)*B[j] and adds them to
-//     its record with native shared atomics. Output: one 64-bit hash per record (its length
-//     mixed in); frame ids and offsets are validated on the way.
+//     chunk accumulates the position-keyed sum f*A[j] (one 32x32+64-bit multiply-add per frame)
+//     and adds its two 32-bit halves to its record with native shared atomics. Output: one
+//     64-bit hash per record (its length mixed in); frame ids and offsets are validated.
 //  2. k_path_group: lane i of a warp inserts / finds record r0+i's hash in an L2-resident table
 //     whose slot names a representative record (the first inserter) with its frame offset and
 //     length; then the warp compares each record with its representative, 32 frames at a time
@@ -65,7 +65,7 @@ struct PathWarp {  // per warp: its 16 records of the tile
 struct PathSmem {
   uint32_t fr[2][PT_FW];
   unsigned long long offs[2][PT_T + 2];
-  uint2 pos[DC_MAX_DEPTH];
+  uint32_t pos[DC_MAX_DEPTH];
   unsigned long long full[2];
   unsigned long long meta_f0[2], meta_f1[2];
   uint32_t meta_mode[2];
@@ -97,7 +97,7 @@ __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {  // read-
 // one warp's chunks: lane takes chunks lane, lane+32, ...; its record by a 4-step search of the
 // warp's chunk starts
 template <bool STAGED>
-__device__ __forceinline__ void pt_hash_chunks(PathWarp& W, const uint2* __restrict__ pos, const uint32_t* __restrict__ src,
+__device__ __forceinline__ void pt_hash_chunks(PathWarp& W, const uint32_t* __restrict__ pos, const uint32_t* __restrict__ src,
                                                uint64_t base, uint32_t n_chunks, uint32_t n_frames, uint32_t& bad) {
   constexpr uint32_t CH = STAGED ? PT_CH : PT_CH_G;
   for (uint32_t ci = lane_id(); ci < n_chunks; ci += 32) {
@@ -108,18 +108,17 @@ __device__ __forceinline__ void pt_hash_chunks(PathWarp& W, const uint2* __restr
     const uint32_t j0 = (ci - W.cs[k]) * CH;
     const uint32_t j1 = min(j0 + CH, W.L[k]);
     const uint32_t* q = src + (W.o[k] - base);
-    uint32_t a1 = 0, a2 = 0, mx = 0;
+    unsigned long long acc = 0;  // sum of f * A[j]: one 32x32+64 multiply-add per frame
+    uint32_t mx = 0;
 #pragma unroll 4
     for (uint32_t j = j0; j < j1; ++j) {
       const uint32_t f = STAGED ? q[j] : ld_stream_u32(q + j);
-      const uint2 w = pos[j];
-      a1 += f * w.x;
-      a2 += (f ^ 0x9E3779B9u) * w.y;
+      acc += (unsigned long long)f * pos[j];
       mx = max(mx, f);
     }
     if (j1 > j0 && mx >= n_frames) bad = 1;
-    atomicAdd(&W.h1[k], a1);
-    atomicAdd(&W.h2[k], a2);
+    atomicAdd(&W.h1[k], (uint32_t)acc);  // two native 32-bit adds (a deterministic function of
+    atomicAdd(&W.h2[k], (uint32_t)(acc >> 32));  // the path: chunking depends only on positions)
   }
 }
 
@@ -134,7 +133,7 @@ __global__ void __launch_bounds__(PT_THREADS) k_path_hash(const uint64_t* __rest
   const uint64_t n_tiles = (R + PT_T - 1) / PT_T, G = gridDim.x;
   for (uint32_t j = tid; j < DC_MAX_DEPTH; j += PT_THREADS) {
     const uint64_t m = mix64(0x9E3779B97F4A7C15ull * (j + 1));
-    sm.pos[j] = make_uint2((uint32_t)m | 1u, (uint32_t)(m >> 32) | 1u);
+    sm.pos[j] = (uint32_t)(m >> 32) | 0x80000001u;
   }
   if (tid == 0) {
     mbar_init(&sm.full[0], 1);
@@ -318,6 +317,7 @@ __global__ void __launch_bounds__(256) k_path_group(const uint64_t* __restrict__
     // verify, 8 records at a time: their first 64 frames on both sides are loaded before any
     // compare, so the DRAM latency of the own frames is paid once per group
     uint32_t todo = __ballot_sync(0xffffffffu, need == 1u);
+    const uint32_t* fl = frames + lane;
     while (todo) {
       int idx[8];
       uint64_t oo[8], rr[8];
@@ -334,19 +334,26 @@ __global__ void __launch_bounds__(256) k_path_group(const uint64_t* __restrict__
       }
       uint32_t a0[8], b0[8], a1[8], b1[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < 8; ++u) {  // lane-relative pointers: the second step is an immediate offset
+        const uint32_t* po = fl + oo[u];
+        const uint32_t* pr = fl + rr[u];
         const bool p0 = lane < ll[u], p1 = lane + 32 < ll[u];
-        a0[u] = p0 ? ld_stream_u32(frames + oo[u] + lane) : 0u;
-        b0[u] = p0 ? __ldg(frames + rr[u] + lane) : 0u;
-        a1[u] = p1 ? ld_stream_u32(frames + oo[u] + lane + 32) : 0u;
-        b1[u] = p1 ? __ldg(frames + rr[u] + lane + 32) : 0u;
+        a0[u] = p0 ? ld_stream_u32(po) : 0u;
+        b0[u] = p0 ? __ldg(pr) : 0u;
+        a1[u] = p1 ? ld_stream_u32(po + 32) : 0u;
+        b1[u] = p1 ? __ldg(pr + 32) : 0u;
       }
+      uint32_t dmask = 0;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         bool diff = (a0[u] != b0[u]) | (a1[u] != b1[u]);
-        for (uint32_t j = lane + 64; j < ll[u]; j += 32) diff |= ld_stream_u32(frames + oo[u] + j) != __ldg(frames + rr[u] + j);
-        if (__any_sync(0xffffffffu, diff) && lane == (uint32_t)idx[u]) need = 2u;
+        for (uint32_t j = 64; lane + j < ll[u]; j += 32) diff |= ld_stream_u32(fl + oo[u] + j) != __ldg(fl + rr[u] + j);
+        dmask |= diff ? 1u << u : 0u;
       }
+      dmask = __reduce_or_sync(0xffffffffu, dmask);  // one vote for the 8 records
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (((dmask >> u) & 1u) && lane == (uint32_t)idx[u]) need = 2u;
     }
     if (act) {
       uint32_t out = sl;
