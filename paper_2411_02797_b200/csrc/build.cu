@@ -317,7 +317,6 @@ __global__ void __launch_bounds__(256) k_path_group(const uint64_t* __restrict__
     // verify, 8 records at a time: their first 64 frames on both sides are loaded before any
     // compare, so the DRAM latency of the own frames is paid once per group
     uint32_t todo = __ballot_sync(0xffffffffu, need == 1u);
-    const uint32_t* fl = frames + lane;
     while (todo) {
       int idx[8];
       uint64_t oo[8], rr[8];
@@ -334,26 +333,19 @@ __global__ void __launch_bounds__(256) k_path_group(const uint64_t* __restrict__
       }
       uint32_t a0[8], b0[8], a1[8], b1[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {  // lane-relative pointers: the second step is an immediate offset
-        const uint32_t* po = fl + oo[u];
-        const uint32_t* pr = fl + rr[u];
+      for (int u = 0; u < 8; ++u) {
         const bool p0 = lane < ll[u], p1 = lane + 32 < ll[u];
-        a0[u] = p0 ? ld_stream_u32(po) : 0u;
-        b0[u] = p0 ? __ldg(pr) : 0u;
-        a1[u] = p1 ? ld_stream_u32(po + 32) : 0u;
-        b1[u] = p1 ? __ldg(pr + 32) : 0u;
+        a0[u] = p0 ? ld_stream_u32(frames + oo[u] + lane) : 0u;
+        b0[u] = p0 ? __ldg(frames + rr[u] + lane) : 0u;
+        a1[u] = p1 ? ld_stream_u32(frames + oo[u] + lane + 32) : 0u;
+        b1[u] = p1 ? __ldg(frames + rr[u] + lane + 32) : 0u;
       }
-      uint32_t dmask = 0;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         bool diff = (a0[u] != b0[u]) | (a1[u] != b1[u]);
-        for (uint32_t j = 64; lane + j < ll[u]; j += 32) diff |= ld_stream_u32(fl + oo[u] + j) != __ldg(fl + rr[u] + j);
-        dmask |= diff ? 1u << u : 0u;
+        for (uint32_t j = lane + 64; j < ll[u]; j += 32) diff |= ld_stream_u32(frames + oo[u] + j) != __ldg(frames + rr[u] + j);
+        if (__any_sync(0xffffffffu, diff) && lane == (uint32_t)idx[u]) need = 2u;
       }
-      dmask = __reduce_or_sync(0xffffffffu, dmask);  // one vote for the 8 records
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (((dmask >> u) & 1u) && lane == (uint32_t)idx[u]) need = 2u;
     }
     if (act) {
       uint32_t out = sl;
