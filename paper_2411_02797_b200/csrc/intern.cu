@@ -1,9 +1,10 @@
 // intern.cu — a1: frame interning (§4.2 frame identity/unification).
 //
-// K1 insert: one raw 16-B key per thread (vector load), open-addressing table of 16-B slots
-//    in L2, read-first probing so repeated keys (the common case: a few hundred distinct
-//    frames among tens of millions of entries) cost one L2 read, 128-bit atomicCAS only to
-//    claim an empty slot. Emits the slot of each key into out_ids (reused as scratch).
+// K1 insert: one raw 16-B key per thread (vector load); a per-CTA shared-memory cache of
+//    (key -> slot) answers repeated keys (the common case: a few hundred to a few thousand
+//    distinct frames among millions of entries); a cache miss probes the open-addressing table
+//    of 16-B slots in L2 (read-first, 128-bit atomicCAS only to claim an empty slot). Emits the
+//    slot of each key into out_ids (reused as scratch).
 // K2 canon: compact the D occupied slots, stable LSD radix sort by (addr) then
 //    (kind<<32|str_id) -> lexicographic rank; slot -> rank table.
 // K3 remap: out_ids[j] = rank[slot[j]].
@@ -15,9 +16,22 @@ static constexpr uint64_t EMPTY = ~0ull;
 
 __device__ __forceinline__ uint64_t key_lo(const dc_frame_key& k) { return (uint64_t)k.kind | ((uint64_t)k.str_id << 32); }
 
-__global__ void k_intern_insert(const dc_frame_key* __restrict__ keys, uint64_t n, ulonglong2* table, uint64_t mask,
-                                uint32_t* __restrict__ out_slot, unsigned long long* d_count, uint32_t* d_overflow,
-                                uint32_t* d_flags, unsigned long long* d_max) {
+// Per-CTA shared-memory cache of (key -> table slot): traces repeat a few thousand distinct
+// frames across millions of entries, so after warm-up almost every key is resolved in shared
+// memory and the L2 table is probed only on a cache miss. Entries are claimed with a CAS on
+// their slot word (EMPTY -> BUSY), written, then published; they are never evicted.
+constexpr int IC_SLOTS = 2048;        // cache entries per CTA (40 KB)
+constexpr int IC_PROBE = 8;           // linear probe window
+constexpr uint32_t IC_EMPTY = 0xFFFFFFFFu, IC_BUSY = 0xFFFFFFFEu;
+
+__global__ void __launch_bounds__(256) k_intern_insert(const dc_frame_key* __restrict__ keys, uint64_t n, ulonglong2* table,
+                                                       uint64_t mask, uint32_t* __restrict__ out_slot,
+                                                       unsigned long long* d_count, uint32_t* d_overflow, uint32_t* d_flags,
+                                                       unsigned long long* d_max) {
+  __shared__ unsigned long long c_lo[IC_SLOTS], c_hi[IC_SLOTS];
+  __shared__ uint32_t c_slot[IC_SLOTS];
+  for (int i = threadIdx.x; i < IC_SLOTS; i += blockDim.x) c_slot[i] = IC_EMPTY;
+  __syncthreads();
   uint64_t mx_addr = 0, mx_ks = 0;  // radix widths of the canonical sort (max addr, max kind<<32|str)
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
     ulonglong2 kv = __ldg(reinterpret_cast<const ulonglong2*>(keys) + j);  // 16-B coalesced load
@@ -29,27 +43,51 @@ __global__ void k_intern_insert(const dc_frame_key* __restrict__ keys, uint64_t 
     }
     mx_addr = max(mx_addr, hi);
     mx_ks = max(mx_ks, (lo << 32) | (lo >> 32));
-    uint64_t h = mix64(lo ^ mix64(hi + 0x9E3779B97F4A7C15ull));
-    uint64_t s = h & mask;
-    uint32_t found = 0xFFFFFFFFu;
-    for (uint64_t probe = 0; probe <= mask; ++probe, s = (s + 1) & mask) {
-      ulonglong2 cur = ld_relaxed_v2(table + s);
-      if (cur.x == lo && cur.y == hi && hi != EMPTY) { found = (uint32_t)s; break; }
-      bool maybe_partial = ((uint32_t)cur.x == 0xFFFFFFFFu) || cur.y == EMPTY;  // empty, or a torn read of a claim
-      if (!maybe_partial) continue;                                          // a different, fully written key
-      unsigned __int128 expect = ((unsigned __int128)EMPTY << 64) | EMPTY;
-      unsigned __int128 want = ((unsigned __int128)hi << 64) | lo;
-      unsigned __int128 old = atomicCAS(reinterpret_cast<unsigned __int128*>(table + s), expect, want);
-      if (old == expect) {
-        atomicAdd(d_count, 1ull);
-        found = (uint32_t)s;
+    const uint64_t h = mix64(lo ^ mix64(hi + 0x9E3779B97F4A7C15ull));
+    // ---- shared cache
+    const uint32_t c0 = (uint32_t)(h >> 40) & (IC_SLOTS - 1);
+    uint32_t found = 0xFFFFFFFFu, claim = IC_EMPTY;
+    for (int k = 0; k < IC_PROBE; ++k) {
+      const uint32_t e = (c0 + k) & (IC_SLOTS - 1);
+      const uint32_t v = *(volatile uint32_t*)&c_slot[e];
+      if (v == IC_EMPTY) {  // the key is not cached: claim this entry for it (best effort)
+        if (atomicCAS(&c_slot[e], IC_EMPTY, IC_BUSY) == IC_EMPTY) claim = e;
         break;
       }
-      if ((uint64_t)old == lo && (uint64_t)(old >> 64) == hi) { found = (uint32_t)s; break; }
+      if (v == IC_BUSY) continue;
+      __threadfence_block();
+      if (*(volatile unsigned long long*)&c_lo[e] == lo && *(volatile unsigned long long*)&c_hi[e] == hi) {
+        found = v;
+        break;
+      }
     }
-    if (found == 0xFFFFFFFFu) {
-      atomicOr(d_overflow, 1u);
-      found = 0;
+    if (found == 0xFFFFFFFFu) {  // ---- L2 table
+      uint64_t s = h & mask;
+      for (uint64_t probe = 0; probe <= mask; ++probe, s = (s + 1) & mask) {
+        ulonglong2 cur = ld_relaxed_v2(table + s);
+        if (cur.x == lo && cur.y == hi && hi != EMPTY) { found = (uint32_t)s; break; }
+        bool maybe_partial = ((uint32_t)cur.x == 0xFFFFFFFFu) || cur.y == EMPTY;  // empty, or a torn read of a claim
+        if (!maybe_partial) continue;                                          // a different, fully written key
+        unsigned __int128 expect = ((unsigned __int128)EMPTY << 64) | EMPTY;
+        unsigned __int128 want = ((unsigned __int128)hi << 64) | lo;
+        unsigned __int128 old = atomicCAS(reinterpret_cast<unsigned __int128*>(table + s), expect, want);
+        if (old == expect) {
+          atomicAdd(d_count, 1ull);
+          found = (uint32_t)s;
+          break;
+        }
+        if ((uint64_t)old == lo && (uint64_t)(old >> 64) == hi) { found = (uint32_t)s; break; }
+      }
+      if (found == 0xFFFFFFFFu) {
+        atomicOr(d_overflow, 1u);
+        found = 0;
+      }
+    }
+    if (claim != IC_EMPTY) {  // publish the cache entry (key first, slot word last)
+      c_lo[claim] = lo;
+      c_hi[claim] = hi;
+      __threadfence_block();
+      atomicExch(&c_slot[claim], found);
     }
     out_slot[j] = found;
   }
