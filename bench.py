@@ -101,6 +101,20 @@ class Clocks:
                 "n_samples": len(self.samples)}
 
 
+def spin_waits(device: int):
+    """The hot path's few host round trips (sizes read back between kernels) wait on the stream;
+    spin-waiting (CU_CTX_SCHED_SPIN on the primary context, set before it is created) wakes the
+    host within microseconds instead of after a yield/blocking wake-up, which otherwise adds
+    box-dependent idle gaps to every step. Best effort: ignored if the context already exists."""
+    try:
+        from cuda.bindings import driver as cu
+        cu.cuInit(0)
+        _, dev = cu.cuDeviceGet(device)
+        cu.cuDevicePrimaryCtxSetFlags(dev, cu.CUctx_flags.CU_CTX_SCHED_SPIN)
+    except Exception:
+        pass
+
+
 # --------------------------------------------------------------------------- workloads
 def make_workload(cfg: int, rank: int, device: str, n_records: int | None = None):
     import gen
@@ -239,6 +253,7 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    spin_waits(local)
     torch.cuda.set_device(local)
     dist = None
     if world > 1:

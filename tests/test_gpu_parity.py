@@ -149,14 +149,18 @@ def test_configs_vs_oracle(cfg, R):
     assert_same(a, ref, ctx=f"cfg{cfg}")
 
 
-def test_generic_schedule_equals_owner_schedule():
-    """launch_sample_off given vs NULL: identical results (and oracle)."""
+def test_generic_schedule_equals_owner_schedule(monkeypatch):
+    """launch_sample_off given vs NULL: identical results (and oracle); the owner schedule's
+    launch ordering by the one-CTA counting sort and by the multi-pass radix sort."""
     p = gen.programs.config3(n_samples=2_000_000)
     tr = gen.make_trace(p, pc=True, bad_per_million=1000)
     kw = dict(keys=tr.keys.numpy(), metrics=tr.metrics.numpy(), samples=tr.samples.numpy(), n_launch=tr.n_launch)
     a = gpu_run(tr.offsets.numpy(), launch_off=tr.launch_off.numpy(), **kw)
     b = gpu_run(tr.offsets.numpy(), launch_off=None, **kw)
     assert_same(a, b, ctx="owner vs generic")
+    monkeypatch.setenv("DC_TEST_OWN_RADIX", "1")
+    c = gpu_run(tr.offsets.numpy(), launch_off=tr.launch_off.numpy(), **kw)
+    assert_same(a, c, ctx="owner (radix-sorted launches)")
 
 
 @pytest.mark.parametrize("n,npc,big", [(3_000_000, 2000, False), (400_000, 20_000, False), (200_000, 300, True)])
