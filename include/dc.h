@@ -257,6 +257,17 @@ dc_status dc_analyze_stalls(dc_ctx* ctx, const dc_cct* cct, uint32_t metric, uin
                             double stall_threshold, uint32_t k, dc_stall_issue* out_h, uint32_t cap,
                             uint32_t* n_out_h);
 
+/* dc_export_folded — flame-graph folded stacks (SPEC.md export_folded;
+   PAPER.md:444-447): one line per non-root node whose exclusive sum of `metric` is non-zero, in
+   canonical (breadth-first) order: node_h[i], value_h[i] (the exclusive value), and its path =
+   frames_h[off_h[i] .. off_h[i] + depth) (frame ids, outermost first; labels are the caller's).
+   *n_lines_h / *n_frames_h receive the totals; when they exceed cap_lines / cap_frames nothing
+   else is written (call again with room). Host buffers. The root's exclusive value (empty
+   paths) has no stack and no line (reading R24). Requires metrics. Synchronizes. */
+dc_status dc_export_folded(dc_ctx* ctx, const dc_cct* cct, uint32_t metric, uint32_t* node_h, uint64_t* value_h,
+                           uint64_t* off_h, uint32_t* frames_h, uint64_t cap_lines, uint64_t cap_frames,
+                           uint64_t* n_lines_h, uint64_t* n_frames_h);
+
 /* ------------------------------------------------------------- borrowed view */
 typedef struct {
   uint64_t n_nodes, n_pc_nodes, n_bins, n_records;

@@ -228,3 +228,24 @@ def run(offsets, frames, metrics, n_metrics, samples=None, n_launch=0, n_stall=0
 def u256_to_double(limbs) -> float:
     w = np.ascontiguousarray(limbs, np.uint64)
     return lib().or_u256_to_double(_p(w))
+
+
+def folded(arrays: dict, metric: int, labels) -> str:
+    """SURVEY §8(f) NEXT-3 / SPEC.md export_folded, plain Python over the oracle's canonical
+    arrays: one line per non-root node with a non-zero exclusive value, in node order; the
+    path from the root (walking parent links) joined by ';' (';' in a label -> ','), a space,
+    the integer exclusive value (reading R24: the root has no stack and no line)."""
+    parent, frame = arrays["parent"], arrays["frame"]
+    xsum = arrays["xsum"][metric]
+    out = []
+    for n in range(1, int(arrays["n_nodes"])):
+        v = int(xsum[n])
+        if v == 0:
+            continue
+        path, a = [], n
+        while a != 0:
+            path.append(str(labels[int(frame[a])]).replace(";", ","))
+            a = int(parent[a])
+        out.append(";".join(reversed(path)) + f" {v}\n")
+    return "".join(out)
+

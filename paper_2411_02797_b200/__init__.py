@@ -280,6 +280,30 @@ def dc_analyze_stalls(ctx: Context, cct: CCT, metric: int = 0, kind_mask: int = 
     return [(int(out[i].node), int(out[i].stall), int(out[i].count)) for i in range(min(n.value, cap))]
 
 
+def dc_export_folded(ctx: Context, cct: CCT, metric: int = 0):
+    """Folded flame-graph stacks as arrays: (node ids, exclusive values, list of frame-id paths)
+    (include/dc.h dc_export_folded)."""
+    nl, nf = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    ctx.check(lib().dc_export_folded(ctx.h, cct.h, int(metric), None, None, None, None, 0, 0, ctypes.byref(nl),
+                                     ctypes.byref(nf)), "dc_export_folded")
+    L, F = nl.value, nf.value
+    nodes, vals, offs = np.zeros(max(L, 1), np.uint32), np.zeros(max(L, 1), np.uint64), np.zeros(max(L, 1), np.uint64)
+    frames = np.zeros(max(F, 1), np.uint32)
+    p = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    ctx.check(lib().dc_export_folded(ctx.h, cct.h, int(metric), p(nodes), p(vals), p(offs), p(frames), L, F, ctypes.byref(nl),
+                                     ctypes.byref(nf)), "dc_export_folded")
+    ends = list(offs[1:L].tolist()) + [F]
+    paths = [frames[int(o):int(e)].tolist() for o, e in zip(offs[:L].tolist(), ends)]
+    return nodes[:L].tolist(), vals[:L].tolist(), paths
+
+
+def folded_text(ctx: Context, cct: CCT, labels, metric: int = 0) -> str:
+    """SPEC.md export_folded text: frames joined by ';' (';' inside labels replaced by ','), one
+    space, the integer exclusive value; LF line endings. labels[frame id] -> str."""
+    _, vals, paths = dc_export_folded(ctx, cct, metric)
+    return "".join(";".join(str(labels[f]).replace(";", ",") for f in path) + f" {v}\n" for path, v in zip(paths, vals))
+
+
 def dc_cct_derived(ctx: Context, cct: CCT, metric: int, incl: bool = True):
     N = cct.n_nodes
     mean = torch.empty(max(N, 1), dtype=torch.float64, device=f"cuda:{ctx.device}")

@@ -20,6 +20,8 @@ dc_status analyze_flags(Ctx* c, const dc_cct* t, dc_rule rule, const dc_rule_par
                         uint32_t* n_out_h);
 dc_status analyze_stalls(Ctx* c, const dc_cct* t, uint32_t metric, uint32_t kind_mask, double hot_threshold,
                          double stall_threshold, uint32_t k, dc_stall_issue* out_h, uint32_t cap, uint32_t* n_out_h);
+dc_status export_folded(Ctx* c, const dc_cct* t, uint32_t metric, uint32_t* node_h, uint64_t* value_h, uint64_t* off_h,
+                        uint32_t* frames_h, uint64_t cap_lines, uint64_t cap_frames, uint64_t* n_lines_h, uint64_t* n_frames_h);
 dc_status hotspots_topk(Ctx* c, const dc_cct* t, dc_view view, uint32_t metric, uint32_t kind_mask, double threshold,
                         uint32_t k, uint32_t stall_node, dc_topk_entry* out_h, uint32_t* n_out_h);
 dc_status derived(Ctx* c, const dc_cct* t, uint32_t metric, int incl, double* mean, double* stdv);
@@ -400,6 +402,17 @@ dc_status dc_analyze_stalls(dc_ctx* ctx, const dc_cct* cct, uint32_t metric, uin
   ON_DEVICE(ctx);
   Region rg(ctx, "rules");
   return analyze_stalls(ctx, cct, metric, kind_mask, hot_threshold, stall_threshold, k, out_h, cap, n_out_h);
+}
+
+dc_status dc_export_folded(dc_ctx* ctx, const dc_cct* cct, uint32_t metric, uint32_t* node_h, uint64_t* value_h,
+                           uint64_t* off_h, uint32_t* frames_h, uint64_t cap_lines, uint64_t cap_frames, uint64_t* n_lines_h,
+                           uint64_t* n_frames_h) {
+  CHECK_CTX(ctx);
+  ARG(cct && n_lines_h && n_frames_h, "bad arguments");
+  ARG((cap_lines == 0 || (node_h && value_h && off_h)) && (cap_frames == 0 || frames_h), "bad arguments");
+  ON_DEVICE(ctx);
+  Region rg(ctx, "export");
+  return export_folded(ctx, cct, metric, node_h, value_h, off_h, frames_h, cap_lines, cap_frames, n_lines_h, n_frames_h);
 }
 
 dc_status dc_cct_derived(dc_ctx* ctx, const dc_cct* cct, uint32_t metric, int incl, double* out_mean, double* out_std) {

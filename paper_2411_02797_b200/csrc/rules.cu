@@ -212,3 +212,79 @@ dc_status analyze_stalls(Ctx* c, const dc_cct* t, uint32_t metric, uint32_t kind
 }
 
 }  // namespace dc
+
+// ---------------------------------------------------------------- NEXT-3: folded flame-graph stacks
+// One line per non-root node with a non-zero exclusive value of the metric (SPEC.md
+// export_folded, PAPER.md:444-447 flame graphs): the node's path (frame ids, root excluded,
+// outermost first) and its exclusive value, in canonical (breadth-first) node order. Labels are
+// the caller's (strings are not part of the device data).
+namespace dc {
+__global__ void k_fold_flags(const uint64_t* __restrict__ x, const uint16_t* __restrict__ depth, uint64_t N,
+                             uint32_t* __restrict__ flag, uint64_t* __restrict__ dep) {
+  for (uint64_t n = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; n < N; n += (uint64_t)gridDim.x * blockDim.x) {
+    const bool f = n > 0 && x[n] != 0;
+    flag[n] = f ? 1u : 0u;
+    dep[n] = f ? depth[n] : 0;
+  }
+}
+__global__ void k_fold_emit(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos, const uint64_t* __restrict__ poff,
+                            const uint32_t* __restrict__ parent, const uint32_t* __restrict__ frame, const uint16_t* __restrict__ depth,
+                            const uint64_t* __restrict__ x, uint64_t N, uint32_t* __restrict__ node_out, uint64_t* __restrict__ val_out,
+                            uint64_t* __restrict__ off_out, uint32_t* __restrict__ frames_out) {
+  for (uint64_t n = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; n < N; n += (uint64_t)gridDim.x * blockDim.x) {
+    if (!flag[n]) continue;
+    const uint32_t i = pos[n];
+    const uint64_t o = poff[n];
+    node_out[i] = (uint32_t)n;
+    val_out[i] = x[n];
+    off_out[i] = o;
+    uint64_t k = depth[n];
+    for (uint32_t a = (uint32_t)n; a != 0 && k > 0; a = parent[a]) frames_out[o + --k] = frame[a];
+  }
+}
+}  // namespace dc
+
+namespace dc {
+dc_status export_folded(Ctx* c, const dc_cct* t, uint32_t metric, uint32_t* node_h, uint64_t* value_h, uint64_t* off_h,
+                        uint32_t* frames_h, uint64_t cap_lines, uint64_t cap_frames, uint64_t* n_lines_h, uint64_t* n_frames_h) {
+  *n_lines_h = *n_frames_h = 0;
+  if (t->state == 0) return fail(c, DC_ERR_STATE, "dc_export_folded needs metrics (call dc_cct_attribute_metrics)");
+  if (t->partition) return fail(c, DC_ERR_STATE, "dc_export_folded needs a complete tree (gather the partitions first)");
+  if (metric >= t->M) return fail(c, DC_ERR_ARG, "metric %u >= M = %u", metric, t->M);
+  const uint64_t N = t->N;
+  Buf<uint32_t> flag, pos, tot32;
+  Buf<uint64_t> dep, poff, tot64;
+  DC_TRY(alloc(c, flag, N));
+  DC_TRY(alloc(c, pos, N));
+  DC_TRY(alloc(c, dep, N));
+  DC_TRY(alloc(c, poff, N));
+  DC_TRY(alloc(c, tot32, 1));
+  DC_TRY(alloc(c, tot64, 1));
+  k_fold_flags<<<grid_for(c, N, 256), 256, 0, c->stream>>>(t->col(C_XSUM, metric), t->depth, N, flag.p, dep.p);
+  DC_LAUNCHED(c);
+  DC_TRY(excl_scan<uint32_t>(c, flag.p, pos.p, N, tot32.p));
+  DC_TRY(excl_scan<uint64_t>(c, dep.p, poff.p, N, tot64.p));
+  uint32_t nl = 0;
+  uint64_t nf = 0;
+  DC_TRY(readback_multi(c, {{tot32.p, 4, &nl}, {tot64.p, 8, &nf}}));
+  *n_lines_h = nl;
+  *n_frames_h = nf;
+  if (nl > cap_lines || nf > cap_frames) return DC_OK;  // sizes only: the caller retries with room
+  Buf<uint32_t> nodes, frames;
+  Buf<uint64_t> vals, offs;
+  DC_TRY(alloc(c, nodes, nl));
+  DC_TRY(alloc(c, vals, nl));
+  DC_TRY(alloc(c, offs, nl));
+  DC_TRY(alloc(c, frames, nf));
+  k_fold_emit<<<grid_for(c, N, 256), 256, 0, c->stream>>>(flag.p, pos.p, poff.p, t->parent, t->frame, t->depth,
+                                                          t->col(C_XSUM, metric), N, nodes.p, vals.p, offs.p, frames.p);
+  DC_LAUNCHED(c);
+  if (nl) {
+    DC_TRY(readback(c, nodes.p, (size_t)nl * 4, node_h));
+    DC_TRY(readback(c, vals.p, (size_t)nl * 8, value_h));
+    DC_TRY(readback(c, offs.p, (size_t)nl * 8, off_h));
+  }
+  if (nf) DC_TRY(readback(c, frames.p, (size_t)nf * 4, frames_h));
+  return DC_OK;
+}
+}  // namespace dc

@@ -93,3 +93,29 @@ def test_stalls_config3_vs_oracle():
                              stall_threshold=st_thr, k=k)
         assert got == exp, (hot_thr, st_thr, k)
         assert got or hot_thr > 0.0
+
+
+def test_folded_export_vs_oracle():
+    """NEXT-3: folded flame-graph text of the CUDA path == the oracle's, byte for byte, on random
+    traces and on a config-2 trace (labels = frame ids)."""
+    import paper_2411_02797_b200 as dc
+    rng = np.random.default_rng(9300)
+    ctx = dc.Context(0)
+    for _ in range(15):
+        paths, X, samples, S = _rand_trace(rng)
+        off, fr = _csr(paths)
+        A = 1 + max([f for p in paths for f in p] + [0])
+        Xa = np.asarray(X, np.uint64).reshape(len(X), -1)
+        a = gpu_run(off, fr, Xa, n_frames=A, ctx=ctx)
+        o = oracle_run(off, fr, Xa, len(X)).arrays()
+        labels = [f"f{i};x" if i % 5 == 0 else f"f{i}" for i in range(A)]
+        for m in range(len(X)):
+            assert dc.folded_text(ctx, a["_cct"], labels, m) == oracle.folded(o, m, labels)
+    p = gen.programs.program(2)
+    tr = gen.make_trace(p, n_records=50_000)
+    a = gpu_run(tr.offsets.numpy(), keys=tr.keys.numpy(), metrics=tr.metrics.numpy())
+    oids, od = oracle.intern(tr.keys.numpy())
+    o = oracle_run(tr.offsets.numpy(), oids, tr.metrics.numpy(), p.n_metrics).arrays()
+    labels = [str(i) for i in range(len(od))]
+    text = dc.folded_text(a["_ctx"], a["_cct"], labels, 0)
+    assert text == oracle.folded(o, 0, labels) and text.count("\n") > 100

@@ -147,3 +147,32 @@ def test_stall_issues_bruteforce_random(seed):
             exp += [(n, s, c) for c, s in r]
         got = o.stall_issues(0, hot_threshold=hot_thr, stall_threshold=st_thr, k=k)
         assert got == exp
+
+
+# ------------------------------------------------------------------ NEXT-3: folded stacks
+def test_spec_folded_example():
+    """SPEC.md export_folded: main -> train -> kernel with exclusive 3050 at the kernel ->
+    "main;train.py:10;conv_kern 3050"; an empty tree gives an empty text; ';' in labels -> ','."""
+    labels = ["main", "train.py:10", "conv_kern"]
+    o = run([(0, 1, 2)], [[3050]])
+    assert oracle.folded(o.arrays(), 0, labels) == "main;train.py:10;conv_kern 3050\n"
+    assert oracle.folded(run([], [[]]).arrays(), 0, labels) == ""
+    assert oracle.folded(run([(0,)], [[5]]).arrays(), 0, ["a;b"]) == "a,b 5\n"
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_folded_bruteforce_and_conservation(seed):
+    rng = np.random.default_rng(8500 + seed)
+    for _ in range(60):
+        paths, X, samples, S = _rand_trace(rng)
+        A = 1 + max([f for p in paths for f in p] + [0])
+        labels = [f"f{i}" for i in range(A)]
+        b = bf.cct(paths, X)
+        o = run(paths, X)
+        text = oracle.folded(o.arrays(), 0, labels)
+        exp = "".join(";".join(labels[f] for f in q) + f" {b['xsum'][0][i]}\n"
+                      for i, q in enumerate(b["order"]) if i > 0 and b["xsum"][0][i])
+        assert text == exp
+        # conservation: lines + the root's own (empty-path) value == the root inclusive value
+        total = sum(int(line.rsplit(" ", 1)[1]) for line in text.splitlines())
+        assert total + b["xsum"][0][0] == b["isum"][0][0]
