@@ -268,6 +268,18 @@ dc_status dc_export_folded(dc_ctx* ctx, const dc_cct* cct, uint32_t metric, uint
                            uint64_t* off_h, uint32_t* frames_h, uint64_t cap_lines, uint64_t cap_frames,
                            uint64_t* n_lines_h, uint64_t* n_frames_h);
 
+/* dc_cpu_intervals — CPU-sample interval attribution (PAPER.md:359-363
+   "subtract the previous timestamp from it, and use the result as the interval between two
+   samples"; SPEC.md attribute_cpu_sample). Samples in trace order: thread[n] (u32), kind[n]
+   (u8: CPU_TIME / REAL_TIME / ...), ts[n] (u64, ns). For each (thread, kind) stream the first
+   sample is the baseline (out_valid 0, out_interval 0); every later one gets ts - ts of the
+   previous sample of its stream (out_valid 1). The intervals of the valid samples are then
+   attributed to their call paths with dc_cct_attribute_metrics. Timestamps decreasing inside a
+   stream are a trace error (DC_ERR_TRACE at the next synchronisation). Device pointers;
+   asynchronous. */
+dc_status dc_cpu_intervals(dc_ctx* ctx, const uint32_t* thread, const uint8_t* kind, const uint64_t* ts, uint64_t n,
+                           uint64_t* out_interval, uint8_t* out_valid);
+
 /* ------------------------------------------------------------- borrowed view */
 typedef struct {
   uint64_t n_nodes, n_pc_nodes, n_bins, n_records;

@@ -249,3 +249,23 @@ def folded(arrays: dict, metric: int, labels) -> str:
         out.append(";".join(reversed(path)) + f" {v}\n")
     return "".join(out)
 
+
+def cpu_intervals(thread, kind, ts):
+    """SURVEY §8(f) NEXT-4, PAPER.md:359-363 / SPEC.md attribute_cpu_sample, replayed one sample
+    at a time in trace order with the previous timestamp of each (thread, kind) stream: the
+    first sample of a stream is the baseline (interval 0, valid False); later ones get
+    ts - previous ts. Returns (intervals, valid) as Python lists."""
+    prev = {}
+    iv, ok = [], []
+    for t, k, x in zip(list(map(int, thread)), list(map(int, kind)), list(map(int, ts))):
+        key = (t, k)
+        if key in prev:
+            assert x >= prev[key], "timestamps must not decrease within a stream"
+            iv.append(x - prev[key])
+            ok.append(True)
+        else:
+            iv.append(0)
+            ok.append(False)
+        prev[key] = x
+    return iv, ok
+

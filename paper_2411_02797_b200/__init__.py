@@ -280,6 +280,17 @@ def dc_analyze_stalls(ctx: Context, cct: CCT, metric: int = 0, kind_mask: int = 
     return [(int(out[i].node), int(out[i].stall), int(out[i].count)) for i in range(min(n.value, cap))]
 
 
+def dc_cpu_intervals(ctx: Context, thread: torch.Tensor, kind: torch.Tensor, ts: torch.Tensor):
+    """NEXT-4 CPU-sample intervals (include/dc.h dc_cpu_intervals): (interval u64 as int64 tensor,
+    valid u8 tensor), trace order. thread int32, kind uint8, ts int64 (device tensors)."""
+    n = int(ts.numel())
+    iv = torch.empty(max(n, 1), dtype=torch.int64, device=ts.device)
+    ok = torch.empty(max(n, 1), dtype=torch.uint8, device=ts.device)
+    ctx.check(lib().dc_cpu_intervals(ctx.h, _ptr(thread) if n else None, _ptr(kind) if n else None, _ptr(ts) if n else None, n,
+                                     _ptr(iv), _ptr(ok)), "dc_cpu_intervals")
+    return iv[:n], ok[:n]
+
+
 def dc_export_folded(ctx: Context, cct: CCT, metric: int = 0):
     """Folded flame-graph stacks as arrays: (node ids, exclusive values, list of frame-id paths)
     (include/dc.h dc_export_folded)."""

@@ -22,6 +22,8 @@ dc_status analyze_stalls(Ctx* c, const dc_cct* t, uint32_t metric, uint32_t kind
                          double stall_threshold, uint32_t k, dc_stall_issue* out_h, uint32_t cap, uint32_t* n_out_h);
 dc_status export_folded(Ctx* c, const dc_cct* t, uint32_t metric, uint32_t* node_h, uint64_t* value_h, uint64_t* off_h,
                         uint32_t* frames_h, uint64_t cap_lines, uint64_t cap_frames, uint64_t* n_lines_h, uint64_t* n_frames_h);
+dc_status cpu_intervals(Ctx* c, const uint32_t* thread, const uint8_t* kind, const uint64_t* ts, uint64_t n,
+                        uint64_t* out_interval, uint8_t* out_valid);
 dc_status hotspots_topk(Ctx* c, const dc_cct* t, dc_view view, uint32_t metric, uint32_t kind_mask, double threshold,
                         uint32_t k, uint32_t stall_node, dc_topk_entry* out_h, uint32_t* n_out_h);
 dc_status derived(Ctx* c, const dc_cct* t, uint32_t metric, int incl, double* mean, double* stdv);
@@ -413,6 +415,15 @@ dc_status dc_export_folded(dc_ctx* ctx, const dc_cct* cct, uint32_t metric, uint
   ON_DEVICE(ctx);
   Region rg(ctx, "export");
   return export_folded(ctx, cct, metric, node_h, value_h, off_h, frames_h, cap_lines, cap_frames, n_lines_h, n_frames_h);
+}
+
+dc_status dc_cpu_intervals(dc_ctx* ctx, const uint32_t* thread, const uint8_t* kind, const uint64_t* ts, uint64_t n,
+                           uint64_t* out_interval, uint8_t* out_valid) {
+  CHECK_CTX(ctx);
+  ARG(n == 0 || (thread && kind && ts && out_interval && out_valid), "bad arguments");
+  ON_DEVICE(ctx);
+  Region rg(ctx, "intervals");
+  return cpu_intervals(ctx, thread, kind, ts, n, out_interval, out_valid);
 }
 
 dc_status dc_cct_derived(dc_ctx* ctx, const dc_cct* cct, uint32_t metric, int incl, double* out_mean, double* out_std) {

@@ -288,3 +288,58 @@ dc_status export_folded(Ctx* c, const dc_cct* t, uint32_t metric, uint32_t* node
   return DC_OK;
 }
 }  // namespace dc
+
+// ---------------------------------------------------------------- NEXT-4: CPU-sample intervals
+// on each CPU_TIME / REAL_TIME sample the profiler "subtract[s] the previous
+// timestamp from it, and use[s] the result as the interval between two samples"; SPEC.md
+// attribute_cpu_sample: per (thread, kind), the first sample is the baseline and attributes
+// nothing. In bulk: a stable radix sort of the samples by (thread, kind) keeps trace order inside
+// each stream, then a segmented adjacent difference, scattered back to trace order.
+namespace dc {
+__global__ void k_iv_keys(const uint32_t* __restrict__ thread, const uint8_t* __restrict__ kind, uint64_t n,
+                          uint64_t* __restrict__ key, uint32_t* __restrict__ val) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    key[i] = (uint64_t)thread[i] << 8 | kind[i];
+    val[i] = (uint32_t)i;
+  }
+}
+__global__ void k_iv_diff(const uint64_t* __restrict__ key, const uint32_t* __restrict__ val, const uint64_t* __restrict__ ts,
+                          uint64_t n, uint64_t* __restrict__ interval, uint8_t* __restrict__ valid, uint32_t* d_flags) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t i = val[j];
+    uint64_t iv = 0;
+    uint8_t ok = 0;
+    if (j > 0 && key[j - 1] == key[j]) {
+      const uint64_t t0 = ts[val[j - 1]], t1 = ts[i];
+      if (t1 >= t0) {
+        iv = t1 - t0;
+        ok = 1;
+      } else {
+        atomicOr(d_flags, FLAG_BAD_OFFSETS);  // timestamps not monotone within a (thread, kind) stream
+      }
+    }
+    interval[i] = iv;
+    valid[i] = ok;
+  }
+}
+
+dc_status cpu_intervals(Ctx* c, const uint32_t* thread, const uint8_t* kind, const uint64_t* ts, uint64_t n,
+                        uint64_t* out_interval, uint8_t* out_valid) {
+  if (n == 0) return DC_OK;
+  if (n >= (1ull << 31)) return fail(c, DC_ERR_CAPACITY, "dc_cpu_intervals: n >= 2^31 samples");
+  Buf<uint64_t> k0, k1;
+  Buf<uint32_t> v0, v1;
+  DC_TRY(alloc(c, k0, n));
+  DC_TRY(alloc(c, k1, n));
+  DC_TRY(alloc(c, v0, n));
+  DC_TRY(alloc(c, v1, n));
+  k_iv_keys<<<grid_for(c, n, 256), 256, 0, c->stream>>>(thread, kind, n, k0.p, v0.p);
+  DC_LAUNCHED(c);
+  bool in1 = false;
+  DC_TRY(radix_sort_pairs(c, k0.p, v0.p, k1.p, v1.p, n, 0, 40, &in1));
+  k_iv_diff<<<grid_for(c, n, 256), 256, 0, c->stream>>>(in1 ? k1.p : k0.p, in1 ? v1.p : v0.p, ts, n, out_interval, out_valid,
+                                                         c->d_flags);
+  DC_LAUNCHED(c);
+  return DC_OK;
+}
+}  // namespace dc

@@ -119,3 +119,35 @@ def test_folded_export_vs_oracle():
     labels = [str(i) for i in range(len(od))]
     text = dc.folded_text(a["_ctx"], a["_cct"], labels, 0)
     assert text == oracle.folded(o, 0, labels) and text.count("\n") > 100
+
+
+def test_cpu_intervals_vs_oracle_and_attribution():
+    """NEXT-4: intervals of the CUDA path == the oracle's replay; the valid intervals attributed to
+    their samples' call paths give the oracle's CCT of the same (filtered) records."""
+    import torch
+    import paper_2411_02797_b200 as dc
+    rng = np.random.default_rng(9400)
+    ctx = dc.Context(0)
+    for n in (1, 17, 3000, 250_000):
+        th = rng.integers(0, 33, n).astype(np.int32)
+        kd = rng.integers(0, 2, n).astype(np.uint8)
+        ts = np.cumsum(rng.integers(0, 10**6, n)).astype(np.int64)
+        iv, ok = dc.dc_cpu_intervals(ctx, torch.from_numpy(th).cuda(), torch.from_numpy(kd).cuda(), torch.from_numpy(ts).cuda())
+        eiv, eok = oracle.cpu_intervals(th, kd, ts)
+        assert iv.cpu().numpy().tolist() == eiv and ok.cpu().numpy().astype(bool).tolist() == eok
+    # attribution: each sample has a call path; valid samples' intervals are the metric
+    n = 20_000
+    paths = [tuple(int(x) for x in rng.integers(0, 12, size=int(rng.integers(1, 8)))) for _ in range(n)]
+    th = rng.integers(0, 4, n).astype(np.int32)
+    kd = np.zeros(n, np.uint8)
+    ts = np.cumsum(rng.integers(1, 5000, n)).astype(np.int64)
+    iv, ok = dc.dc_cpu_intervals(ctx, torch.from_numpy(th).cuda(), torch.from_numpy(kd).cuda(), torch.from_numpy(ts).cuda())
+    keep = ok.cpu().numpy().astype(bool)
+    kp = [p for p, k in zip(paths, keep) if k]
+    off, fr = _csr(kp)
+    X = iv.cpu().numpy()[keep].astype(np.uint64)[None]
+    a = gpu_run(off, fr, X, n_frames=12, ctx=ctx)
+    eiv, eok = oracle.cpu_intervals(th, kd, ts)
+    ref = oracle_run(off, fr, np.asarray([[v for v, o in zip(eiv, eok) if o]], np.uint64), 1).arrays()
+    for key in ("parent", "frame", "xcnt", "xsum", "isum", "imin"):
+        assert np.array_equal(np.asarray(a[key]), np.asarray(ref[key])), key

@@ -176,3 +176,35 @@ def test_folded_bruteforce_and_conservation(seed):
         # conservation: lines + the root's own (empty-path) value == the root inclusive value
         total = sum(int(line.rsplit(" ", 1)[1]) for line in text.splitlines())
         assert total + b["xsum"][0][0] == b["isum"][0][0]
+
+
+# ------------------------------------------------------------------ NEXT-4: CPU-sample intervals
+def test_spec_cpu_sample_intervals():
+    """SPEC.md attribute_cpu_sample: samples at t=100, 350 on one stream -> one interval 250; a
+    single sample -> none; alternating paths A, B at t=0, 10, 30 on one thread -> A baseline,
+    B 10, A 20 (the interval goes to the sample's own path); streams are per (thread, kind)."""
+    assert oracle.cpu_intervals([1, 1], [0, 0], [100, 350]) == ([0, 250], [False, True])
+    assert oracle.cpu_intervals([1], [0], [100]) == ([0], [False])
+    iv, ok = oracle.cpu_intervals([7, 7, 7], [0, 0, 0], [0, 10, 30])
+    paths = ["A", "B", "A"]
+    attributed = [(p, v) for p, v, o in zip(paths, iv, ok) if o]
+    assert attributed == [("B", 10), ("A", 20)]
+    # two threads and two kinds interleaved: four independent streams
+    iv, ok = oracle.cpu_intervals([1, 2, 1, 1, 2, 1], [0, 0, 1, 0, 0, 1], [5, 6, 7, 15, 26, 27])
+    assert iv == [0, 0, 0, 10, 20, 20] and ok == [False, False, False, True, True, True]
+
+
+def test_cpu_intervals_sum_law():
+    """Per stream the intervals telescope: their sum == last ts - first ts."""
+    rng = np.random.default_rng(8800)
+    n = 5000
+    th = rng.integers(0, 7, n)
+    kd = rng.integers(0, 2, n)
+    ts = np.cumsum(rng.integers(0, 1000, n))
+    iv, ok = oracle.cpu_intervals(th, kd, ts)
+    for t in range(7):
+        for k in range(2):
+            sel = [i for i in range(n) if th[i] == t and kd[i] == k]
+            if sel:
+                assert sum(iv[i] for i in sel) == int(ts[sel[-1]] - ts[sel[0]])
+                assert [ok[i] for i in sel] == [False] + [True] * (len(sel) - 1)
