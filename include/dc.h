@@ -225,6 +225,13 @@ typedef enum {
                                 (double)isum[metric_a](n) / (double)launches(n) < threshold,
                                 launches(n) = xcnt summed over the nodes of n's subtree whose
                                 frame kind is in kind_mask (records ending at kernel frames) */
+  DC_RULE_BWD_FWD = 3,       /* ③ forward/backward: n (frame kind in kind_mask,
+                                normally operators) qualifies if fwd = isum[metric_b](n) > 0, fwd >=
+                                floor (the epsilon guard) and (double)isum[metric_a] / (double)fwd >
+                                threshold (the paper's ratio 2); per node, no ancestor suppression
+                                (SPEC.md analyze_fwd_bwd, reading R25). metric_a / metric_b are the
+                                backward / forward time columns (a record's time goes to the column of
+                                its direction; paths integrated with dc_seq_associate) */
   DC_RULE_CPU_LATENCY = 5    /* ⑤ CPU latency: n qualifies if
                                 isum[metric_a](n) > floor and
                                 (double)isum[metric_a] / (double)max(isum[metric_b], 1) > threshold
@@ -236,10 +243,10 @@ typedef struct {
   uint64_t floor;
 } dc_rule_params;
 
-/* dc_analyze_flags — ids of the flagged nodes in breadth-first (= ascending id) order: a node
-   is flagged if it qualifies and no ancestor (the root excluded) qualifies — children of a
-   flagged frame are not re-flagged (SPEC.md analyze_kernel_fusion / analyze_cpu_latency,
-   reading R22). Writes the first min(total, cap) ids to out_ids_h (host) and *n_out_h = total.
+/* dc_analyze_flags — ids of the flagged nodes in breadth-first (= ascending id) order. For ② and
+   ⑤ a node is flagged if it qualifies and no ancestor (the root excluded) qualifies — children
+   of a flagged frame are not re-flagged (SPEC.md analyze_kernel_fusion / analyze_cpu_latency,
+   reading R22); for ③ every qualifying node is flagged. Writes the first min(total, cap) ids to out_ids_h (host) and *n_out_h = total.
    Requires state ROLLED and a complete (not partitioned) tree. Synchronizes. */
 dc_status dc_analyze_flags(dc_ctx* ctx, const dc_cct* cct, dc_rule rule, const dc_rule_params* params,
                            uint32_t* out_ids_h, uint32_t cap, uint32_t* n_out_h);
@@ -279,6 +286,21 @@ dc_status dc_export_folded(dc_ctx* ctx, const dc_cct* cct, uint32_t metric, uint
    asynchronous. */
 dc_status dc_cpu_intervals(dc_ctx* ctx, const uint32_t* thread, const uint8_t* kind, const uint64_t* ts, uint64_t n,
                            uint64_t* out_interval, uint8_t* out_valid);
+
+/* dc_seq_associate — forward/backward operator association (
+   SPEC.md associate_backward): the forward registry is fwd_seq[nf] (sequence ids; < 0 = none,
+   not registered) with the forward ops' Python + framework path prefixes (CSR fwd_off[nf+1],
+   fwd_frames); it is a map, so a later entry with the same id replaces an earlier one. Each
+   backward record r (bwd_seq[r], its own native/kernel path CSR bwd_off / bwd_frames) gets the
+   integrated path = the registered forward prefix of its sequence id followed by its own
+   frames; a record without a sequence id (< 0) keeps its path; an id missing from the registry
+   keeps its path and is counted in *n_unmatched_h. out_off (device, [nb+1]) receives the
+   integrated offsets; out_frames (device, cap_frames) the frames when *n_frames_h <= cap_frames
+   (otherwise only the offsets: call again with room). Synchronizes. */
+dc_status dc_seq_associate(dc_ctx* ctx, const int64_t* fwd_seq, const uint64_t* fwd_off, const uint32_t* fwd_frames,
+                           uint64_t nf, const int64_t* bwd_seq, const uint64_t* bwd_off, const uint32_t* bwd_frames,
+                           uint64_t nb, uint64_t* out_off, uint32_t* out_frames, uint64_t cap_frames, uint64_t* n_frames_h,
+                           uint64_t* n_unmatched_h);
 
 /* ------------------------------------------------------------- borrowed view */
 typedef struct {

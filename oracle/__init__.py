@@ -67,7 +67,7 @@ KEY_DTYPE = np.dtype([("kind", "<u4"), ("str_id", "<u4"), ("addr", "<u8")])
 SAMPLE_DTYPE = np.dtype([("launch", "<u4"), ("pc_off", "<u4"), ("stall", "<u2"), ("flags", "<u2"), ("count", "<u4")])
 TOPK_DTYPE = np.dtype([("id", "<u4"), ("pad", "<u4"), ("value", "<u8"), ("fraction", "<f8")])
 STALL_ISSUE_DTYPE = np.dtype([("node", "<u4"), ("stall", "<u4"), ("count", "<u8")])
-RULE_SMALL_KERNELS, RULE_CPU_LATENCY = 2, 5
+RULE_SMALL_KERNELS, RULE_BWD_FWD, RULE_CPU_LATENCY = 2, 3, 5
 
 
 def as_keys(keys) -> np.ndarray:
@@ -268,4 +268,25 @@ def cpu_intervals(thread, kind, ts):
             ok.append(False)
         prev[key] = x
     return iv, ok
+
+
+def seq_associate(fwd_seq, fwd_paths, bwd_seq, bwd_paths):
+    """SURVEY §8(f) NEXT-4, PAPER.md:314-321 / SPEC.md associate_backward, replayed in order: the
+    forward registry is a dict sequence id -> the forward op's Python + framework prefix (entries
+    with id < 0 are not registered; a later entry replaces an earlier one); a backward record
+    with a registered id gets prefix + its own frames, otherwise its own frames (an unknown id is
+    counted). Returns (paths, unmatched)."""
+    reg = {}
+    for s, p in zip(list(map(int, fwd_seq)), fwd_paths):
+        if s >= 0:
+            reg[s] = list(p)
+    out, unmatched = [], 0
+    for s, p in zip(list(map(int, bwd_seq)), bwd_paths):
+        if s >= 0 and s in reg:
+            out.append(reg[s] + list(p))
+        else:
+            if s >= 0:
+                unmatched += 1
+            out.append(list(p))
+    return out, unmatched
 

@@ -40,6 +40,8 @@
 //                     SPEC.md's readings (launch count of the frame's kernels, max(gpu, 1)
 //                     guard, absolute floor, children of a flagged frame not re-flagged;
 //                     DESIGN.md reading R22). Literal BFS over the canonical tree.
+//                     ③ "Backward abnormality" per operator node, with
+//                     SPEC.md's forward-time epsilon guard (reading R25).
 //  * or_stall_issues — analysis ④: for n in hotspots, its children c with
 //                     c.stalls > stall_threshold, topk(stall reasons) (SPEC.md analyze_stalls:
 //                     the threshold is a fraction of the kernel's samples; reading R23).
@@ -328,14 +330,14 @@ int or_topk(const OrCct* c, int view, uint32_t metric, uint32_t kind_mask, const
 }
 
 // ---------------------------------------------------------------- analyzer rules
-enum { OR_RULE_SMALL_KERNELS = 2, OR_RULE_CPU_LATENCY = 5 };
+enum { OR_RULE_SMALL_KERNELS = 2, OR_RULE_BWD_FWD = 3, OR_RULE_CPU_LATENCY = 5 };
 
 int or_rule_flags(const OrCct* c, int rule, uint32_t metric_a, uint32_t metric_b, uint32_t kind_mask, const uint8_t* frame_kind,
                   uint32_t n_frames, double threshold, uint64_t floor_v, uint32_t* out, uint32_t cap, uint32_t* n_out) {
   *n_out = 0;
   if (!c->final_) return 1;
-  if (metric_a >= c->M || (rule == OR_RULE_CPU_LATENCY && metric_b >= c->M)) return 2;
-  if (rule != OR_RULE_SMALL_KERNELS && rule != OR_RULE_CPU_LATENCY) return 2;
+  if (metric_a >= c->M || (rule != OR_RULE_SMALL_KERNELS && metric_b >= c->M)) return 2;
+  if (rule != OR_RULE_SMALL_KERNELS && rule != OR_RULE_CPU_LATENCY && rule != OR_RULE_BWD_FWD) return 2;
   const size_t N = c->order.size();
   // launches(n): kernel launches in n's subtree = xcnt of every kernel-kind node, propagated
   // to each ancestor one node at a time (the root is not a frame and is not considered)
@@ -349,6 +351,11 @@ int or_rule_flags(const OrCct* c, int rule, uint32_t metric_a, uint32_t metric_b
     const TNode& n = c->t[c->order[id]];
     if (rule == OR_RULE_SMALL_KERNELS)  // n.gpu_time / n.count < gpu_threshold
       return launches[id] > 0 && (double)n.i[metric_a].sum / (double)launches[id] < threshold;
+    if (rule == OR_RULE_BWD_FWD) {  // for n in call_tree.operators: n.backward.time / n.forward.time > 2
+      const uint64_t bwd = n.i[metric_a].sum, fwd = n.i[metric_b].sum;
+      return kind_ok(frame_kind, n_frames, n.frame, kind_mask) && fwd > 0 && fwd >= floor_v &&
+             (double)bwd / (double)fwd > threshold;
+    }
     const uint64_t cpu = n.i[metric_a].sum, gpu = n.i[metric_b].sum;  // n.cpu_time / n.gpu_time > cpu_threshold
     return cpu > floor_v && (double)cpu / (double)(gpu > 0 ? gpu : 1) > threshold;
   };
@@ -358,7 +365,7 @@ int or_rule_flags(const OrCct* c, int rule, uint32_t metric_a, uint32_t metric_b
   std::vector<uint32_t> res;
   for (size_t id = 1; id < N; ++id) {
     const uint32_t p = c->canon[c->t[c->order[id]].parent];
-    below[id] = p != 0 && (below[p] || flagged[p]);
+    below[id] = rule != OR_RULE_BWD_FWD && p != 0 && (below[p] || flagged[p]);  // ③: every operator node
     if (!below[id] && qualifies(id)) {
       flagged[id] = 1;
       res.push_back((uint32_t)id);

@@ -252,6 +252,7 @@ def dc_hotspots_topk(ctx: Context, cct: CCT, view: int, metric: int = 0, kind_ma
     return [(int(out[i].id), int(out[i].value), float(out[i].fraction)) for i in range(n.value)]
 
 
+DC_RULE_BWD_FWD = 3
 DC_RULE_SMALL_KERNELS = 2
 DC_RULE_CPU_LATENCY = 5
 
@@ -289,6 +290,21 @@ def dc_cpu_intervals(ctx: Context, thread: torch.Tensor, kind: torch.Tensor, ts:
     ctx.check(lib().dc_cpu_intervals(ctx.h, _ptr(thread) if n else None, _ptr(kind) if n else None, _ptr(ts) if n else None, n,
                                      _ptr(iv), _ptr(ok)), "dc_cpu_intervals")
     return iv[:n], ok[:n]
+
+
+def dc_seq_associate(ctx: Context, fwd_seq: torch.Tensor, fwd_off: torch.Tensor, fwd_frames: torch.Tensor,
+                     bwd_seq: torch.Tensor, bwd_off: torch.Tensor, bwd_frames: torch.Tensor):
+    """NEXT-4 forward/backward association (include/dc.h dc_seq_associate): integrated backward
+    paths as (offsets int64 [nb+1], frames int32) device tensors, and the unmatched count."""
+    nf, nb = int(fwd_seq.numel()), int(bwd_seq.numel())
+    out_off = torch.empty(nb + 1, dtype=torch.int64, device=bwd_off.device)
+    nfr, nun = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    q = lambda t: _ptr(t) if t.numel() else None  # noqa: E731
+    args = (ctx.h, q(fwd_seq), q(fwd_off), q(fwd_frames), nf, q(bwd_seq), q(bwd_off), q(bwd_frames), nb, _ptr(out_off))
+    ctx.check(lib().dc_seq_associate(*args, None, 0, ctypes.byref(nfr), ctypes.byref(nun)), "dc_seq_associate")
+    out = torch.empty(max(nfr.value, 1), dtype=torch.int32, device=bwd_off.device)
+    ctx.check(lib().dc_seq_associate(*args, _ptr(out), nfr.value, ctypes.byref(nfr), ctypes.byref(nun)), "dc_seq_associate")
+    return out_off, out[: nfr.value], int(nun.value)
 
 
 def dc_export_folded(ctx: Context, cct: CCT, metric: int = 0):

@@ -91,6 +91,7 @@ def lib():
             "dc_analyze_flags": (i32, [P, P, i32, ctypes.POINTER(dc_rule_params), P, u32, ctypes.POINTER(u32)]),
             "dc_analyze_stalls": (i32, [P, P, u32, u32, f64, f64, u32, P, u32, ctypes.POINTER(u32)]),
             "dc_cpu_intervals": (i32, [P, P, P, P, u64, P, P]),
+            "dc_seq_associate": (i32, [P, P, P, P, u64, P, P, P, u64, P, P, u64, ctypes.POINTER(u64), ctypes.POINTER(u64)]),
             "dc_export_folded": (i32, [P, P, u32, P, P, P, P, u64, u64, ctypes.POINTER(u64), ctypes.POINTER(u64)]),
             "dc_cct_view_get": (i32, [P, ctypes.POINTER(dc_cct_view)]),
             "dc_cct_free": (None, [P]),

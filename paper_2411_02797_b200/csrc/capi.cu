@@ -24,6 +24,9 @@ dc_status export_folded(Ctx* c, const dc_cct* t, uint32_t metric, uint32_t* node
                         uint32_t* frames_h, uint64_t cap_lines, uint64_t cap_frames, uint64_t* n_lines_h, uint64_t* n_frames_h);
 dc_status cpu_intervals(Ctx* c, const uint32_t* thread, const uint8_t* kind, const uint64_t* ts, uint64_t n,
                         uint64_t* out_interval, uint8_t* out_valid);
+dc_status seq_associate(Ctx* c, const int64_t* fseq, const uint64_t* foff, const uint32_t* ffr, uint64_t nf, const int64_t* bseq,
+                        const uint64_t* boff, const uint32_t* bfr, uint64_t nb, uint64_t* out_off, uint32_t* out_frames,
+                        uint64_t cap_frames, uint64_t* n_frames_h, uint64_t* n_unmatched_h);
 dc_status hotspots_topk(Ctx* c, const dc_cct* t, dc_view view, uint32_t metric, uint32_t kind_mask, double threshold,
                         uint32_t k, uint32_t stall_node, dc_topk_entry* out_h, uint32_t* n_out_h);
 dc_status derived(Ctx* c, const dc_cct* t, uint32_t metric, int incl, double* mean, double* stdv);
@@ -424,6 +427,20 @@ dc_status dc_cpu_intervals(dc_ctx* ctx, const uint32_t* thread, const uint8_t* k
   ON_DEVICE(ctx);
   Region rg(ctx, "intervals");
   return cpu_intervals(ctx, thread, kind, ts, n, out_interval, out_valid);
+}
+
+dc_status dc_seq_associate(dc_ctx* ctx, const int64_t* fwd_seq, const uint64_t* fwd_off, const uint32_t* fwd_frames,
+                           uint64_t nf, const int64_t* bwd_seq, const uint64_t* bwd_off, const uint32_t* bwd_frames,
+                           uint64_t nb, uint64_t* out_off, uint32_t* out_frames, uint64_t cap_frames, uint64_t* n_frames_h,
+                           uint64_t* n_unmatched_h) {
+  CHECK_CTX(ctx);
+  ARG(n_frames_h && n_unmatched_h && out_off, "bad arguments");
+  ARG(nf == 0 || (fwd_seq && fwd_off), "bad forward registry");
+  ARG(nb == 0 || (bwd_seq && bwd_off), "bad backward records");
+  ON_DEVICE(ctx);
+  Region rg(ctx, "associate");
+  return seq_associate(ctx, fwd_seq, fwd_off, fwd_frames, nf, bwd_seq, bwd_off, bwd_frames, nb, out_off, out_frames, cap_frames,
+                       n_frames_h, n_unmatched_h);
 }
 
 dc_status dc_cct_derived(dc_ctx* ctx, const dc_cct* cct, uint32_t metric, int incl, double* out_mean, double* out_std) {

@@ -38,6 +38,12 @@ __global__ void k_rule_launches(const uint32_t* __restrict__ parent, const uint3
   }
 }
 
+__global__ void k_rule_kind_gate(const uint32_t* __restrict__ frame, const uint8_t* __restrict__ fk, uint32_t n_frames,
+                                 uint32_t mask, uint64_t N, unsigned long long* __restrict__ gate) {
+  for (uint64_t n = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; n < N; n += (uint64_t)gridDim.x * blockDim.x)
+    gate[n] = (n > 0 && rule_kind_ok(fk, n_frames, frame[n], mask)) ? 1ull : 0ull;
+}
+
 __global__ void k_rule_qualify(int rule, uint64_t N, const uint64_t* __restrict__ a, const uint64_t* __restrict__ b,
                                const uint64_t* __restrict__ il, double threshold, uint64_t floor, uint8_t* __restrict__ q) {
   for (uint64_t n = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; n < N; n += (uint64_t)gridDim.x * blockDim.x) {
@@ -46,6 +52,9 @@ __global__ void k_rule_qualify(int rule, uint64_t N, const uint64_t* __restrict_
       if (rule == DC_RULE_SMALL_KERNELS) {
         const uint64_t l = il[n];
         ok = l > 0 && rdiv(a[n], l) < threshold;
+      } else if (rule == DC_RULE_BWD_FWD) {  // kind gate applied by the caller through il (0/1)
+        const uint64_t bwd = a[n], fwd = b[n];
+        ok = il[n] != 0 && fwd > 0 && fwd >= floor && rdiv(bwd, fwd) > threshold;
       } else {
         const uint64_t cpu = a[n], gpu = b[n];
         ok = cpu > floor && rdiv(cpu, gpu > 0 ? gpu : 1) > threshold;
@@ -57,10 +66,10 @@ __global__ void k_rule_qualify(int rule, uint64_t N, const uint64_t* __restrict_
 
 // flagged = qualifies and no proper (non-root) ancestor qualifies
 __global__ void k_rule_suppress(const uint32_t* __restrict__ parent, uint64_t N, const uint8_t* __restrict__ q,
-                                uint32_t* __restrict__ flag) {
+                                uint32_t* __restrict__ flag, int suppress) {
   for (uint64_t n = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; n < N; n += (uint64_t)gridDim.x * blockDim.x) {
     bool f = q[n] != 0;
-    if (f)
+    if (f && suppress)
       for (uint32_t a = parent[n], prev = (uint32_t)n; a < prev && a != 0; prev = a, a = parent[a])
         if (q[a]) {
           f = false;
@@ -81,8 +90,9 @@ dc_status analyze_flags(Ctx* c, const dc_cct* t, dc_rule rule, const dc_rule_par
   *n_out_h = 0;
   if (t->state != 2) return fail(c, DC_ERR_STATE, "dc_analyze_flags needs a rolled-up tree (call dc_cct_rollup)");
   if (t->partition) return fail(c, DC_ERR_STATE, "dc_analyze_flags needs a complete tree (gather the partitions first)");
-  if (rule != DC_RULE_SMALL_KERNELS && rule != DC_RULE_CPU_LATENCY) return fail(c, DC_ERR_ARG, "unknown rule %d", (int)rule);
-  if (p->metric_a >= t->M || (rule == DC_RULE_CPU_LATENCY && p->metric_b >= t->M))
+  if (rule != DC_RULE_SMALL_KERNELS && rule != DC_RULE_CPU_LATENCY && rule != DC_RULE_BWD_FWD)
+    return fail(c, DC_ERR_ARG, "unknown rule %d", (int)rule);
+  if (p->metric_a >= t->M || (rule != DC_RULE_SMALL_KERNELS && p->metric_b >= t->M))
     return fail(c, DC_ERR_ARG, "metric out of range (M = %u)", t->M);
   const uint64_t N = t->N;
   Buf<unsigned long long> il;
@@ -93,6 +103,10 @@ dc_status analyze_flags(Ctx* c, const dc_cct* t, dc_rule rule, const dc_rule_par
     k_rule_launches<<<grid_for(c, N, 256), 256, 0, c->stream>>>(t->parent, t->frame, t->frame_kind, t->n_frames, p->kind_mask,
                                                                t->xcnt, N, il.p);
     DC_LAUNCHED(c);
+  } else if (rule == DC_RULE_BWD_FWD) {  // operator nodes: the kind gate as a 0/1 column
+    DC_TRY(alloc(c, il, N));
+    k_rule_kind_gate<<<grid_for(c, N, 256), 256, 0, c->stream>>>(t->frame, t->frame_kind, t->n_frames, p->kind_mask, N, il.p);
+    DC_LAUNCHED(c);
   }
   DC_TRY(alloc(c, q, N));
   DC_TRY(alloc(c, flag, N));
@@ -100,10 +114,11 @@ dc_status analyze_flags(Ctx* c, const dc_cct* t, dc_rule rule, const dc_rule_par
   DC_TRY(alloc(c, cnt, 1));
   DC_TRY(alloc(c, out, cap ? cap : 1));
   k_rule_qualify<<<grid_for(c, N, 256), 256, 0, c->stream>>>((int)rule, N, t->col(C_ISUM, p->metric_a),
-                                                             rule == DC_RULE_CPU_LATENCY ? t->col(C_ISUM, p->metric_b) : nullptr,
+                                                             rule != DC_RULE_SMALL_KERNELS ? t->col(C_ISUM, p->metric_b) : nullptr,
                                                              (const uint64_t*)il.p, p->threshold, p->floor, q.p);
   DC_LAUNCHED(c);
-  k_rule_suppress<<<grid_for(c, N, 256), 256, 0, c->stream>>>(t->parent, N, q.p, flag.p);
+  // ② and ⑤ report the highest qualifying frame; ③ is per operator node (no suppression)
+  k_rule_suppress<<<grid_for(c, N, 256), 256, 0, c->stream>>>(t->parent, N, q.p, flag.p, rule == DC_RULE_BWD_FWD ? 0 : 1);
   DC_LAUNCHED(c);
   DC_TRY(excl_scan<uint32_t>(c, flag.p, pos.p, N, cnt.p));
   k_rule_emit<<<grid_for(c, N, 256), 256, 0, c->stream>>>(flag.p, pos.p, N, cap, out.p);
@@ -339,6 +354,121 @@ dc_status cpu_intervals(Ctx* c, const uint32_t* thread, const uint8_t* kind, con
   DC_TRY(radix_sort_pairs(c, k0.p, v0.p, k1.p, v1.p, n, 0, 40, &in1));
   k_iv_diff<<<grid_for(c, n, 256), 256, 0, c->stream>>>(in1 ? k1.p : k0.p, in1 ? v1.p : v0.p, ts, n, out_interval, out_valid,
                                                          c->d_flags);
+  DC_LAUNCHED(c);
+  return DC_OK;
+}
+}  // namespace dc
+
+// ---------------------------------------------------------------- NEXT-4: forward/backward association
+// backward threads lose the Python / framework context; "the backward thread
+// looks up the forward CPU thread, fetches the Python and framework call path of the
+// corresponding forward operator [same sequence ID], and integrates it with the native call path
+// of the backward operator". SPEC.md associate_backward: forward prefix root-ward of the backward
+// frames; an unknown sequence id keeps the backward path (and is counted); the registry is a map
+// (a later forward entry with the same id replaces an earlier one).
+namespace dc {
+constexpr uint64_t SQ_EMPTY = ~0ull;
+__device__ __forceinline__ uint64_t sq_slot(uint64_t seq, uint64_t mask) { return (mix64(seq) >> 7) & mask; }
+
+__global__ void k_seq_insert(const int64_t* __restrict__ fseq, uint64_t nf, unsigned long long* key, unsigned long long* idx,
+                             uint64_t mask, unsigned int* overflow) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nf; i += (uint64_t)gridDim.x * blockDim.x) {
+    const int64_t s = fseq[i];
+    if (s < 0) continue;  // only forward ops carrying a sequence id are registered
+    uint64_t q = sq_slot((uint64_t)s, mask);
+    bool done = false;
+    for (uint64_t p = 0; p <= mask && !done; ++p, q = (q + 1) & mask) {
+      const unsigned long long old = atomicCAS(key + q, SQ_EMPTY, (unsigned long long)s);
+      if (old == SQ_EMPTY || old == (unsigned long long)s) {
+        atomicMax(idx + q, (unsigned long long)i);  // the map keeps the last entry
+        done = true;
+      }
+    }
+    if (!done) atomicOr(overflow, 1u);
+  }
+}
+
+// per backward record: its forward entry (or none) and integrated length
+__global__ void k_seq_lookup(const int64_t* __restrict__ bseq, uint64_t nb, const uint64_t* __restrict__ boff,
+                             const uint64_t* __restrict__ foff, const unsigned long long* __restrict__ key,
+                             const unsigned long long* __restrict__ idx, uint64_t mask, uint64_t* __restrict__ fwd_of,
+                             uint64_t* __restrict__ len, unsigned long long* unmatched) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < nb; r += (uint64_t)gridDim.x * blockDim.x) {
+    const int64_t s = bseq[r];
+    uint64_t f = SQ_EMPTY;
+    if (s >= 0) {
+      uint64_t q = sq_slot((uint64_t)s, mask);
+      for (uint64_t p = 0; p <= mask; ++p, q = (q + 1) & mask) {
+        const unsigned long long k = key[q];
+        if (k == (unsigned long long)s) {
+          f = idx[q];
+          break;
+        }
+        if (k == SQ_EMPTY) break;
+      }
+      if (f == SQ_EMPTY) atomicAdd(unmatched, 1ull);
+    }
+    fwd_of[r] = f;
+    len[r] = (f == SQ_EMPTY ? 0 : foff[f + 1] - foff[f]) + (boff[r + 1] - boff[r]);
+  }
+}
+
+// warp per backward record: forward prefix then the record's own frames
+__global__ void k_seq_copy(uint64_t nb, const uint64_t* __restrict__ fwd_of, const uint64_t* __restrict__ foff,
+                           const uint32_t* __restrict__ ffr, const uint64_t* __restrict__ boff, const uint32_t* __restrict__ bfr,
+                           const uint64_t* __restrict__ ooff, uint32_t* __restrict__ ofr) {
+  const uint32_t lane = lane_id();
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t r = warp; r < nb; r += nw) {
+    const uint64_t f = fwd_of[r], o = ooff[r];
+    uint64_t pl = 0;
+    if (f != SQ_EMPTY) {
+      const uint64_t a = foff[f];
+      pl = foff[f + 1] - a;
+      for (uint64_t j = lane; j < pl; j += 32) ofr[o + j] = ffr[a + j];
+    }
+    const uint64_t b = boff[r], bl = boff[r + 1] - b;
+    for (uint64_t j = lane; j < bl; j += 32) ofr[o + pl + j] = bfr[b + j];
+  }
+}
+
+dc_status seq_associate(Ctx* c, const int64_t* fseq, const uint64_t* foff, const uint32_t* ffr, uint64_t nf, const int64_t* bseq,
+                        const uint64_t* boff, const uint32_t* bfr, uint64_t nb, uint64_t* out_off, uint32_t* out_frames,
+                        uint64_t cap_frames, uint64_t* n_frames_h, uint64_t* n_unmatched_h) {
+  *n_frames_h = 0;
+  *n_unmatched_h = 0;
+  if (nb == 0) {
+    DC_CUDA(c, cudaMemsetAsync(out_off, 0, 8, c->stream));
+    return DC_OK;
+  }
+  uint64_t cap = 1024;
+  while (cap < 2 * nf) cap <<= 1;
+  Buf<unsigned long long> key, idx, unm;
+  Buf<unsigned int> ovf;
+  Buf<uint64_t> fwd_of, len;
+  DC_TRY(alloc(c, key, cap));
+  DC_TRY(alloc_zero(c, idx, cap));
+  DC_TRY(alloc_zero(c, unm, 1));
+  DC_TRY(alloc_zero(c, ovf, 1));
+  DC_TRY(alloc(c, fwd_of, nb));
+  DC_TRY(alloc(c, len, nb));
+  DC_CUDA(c, cudaMemsetAsync(key.p, 0xFF, cap * 8, c->stream));
+  if (nf) {
+    k_seq_insert<<<grid_for(c, nf, 256), 256, 0, c->stream>>>(fseq, nf, key.p, idx.p, cap - 1, ovf.p);
+    DC_LAUNCHED(c);
+  }
+  k_seq_lookup<<<grid_for(c, nb, 256), 256, 0, c->stream>>>(bseq, nb, boff, foff, key.p, idx.p, cap - 1, fwd_of.p, len.p, unm.p);
+  DC_LAUNCHED(c);
+  DC_TRY(excl_scan<uint64_t>(c, len.p, out_off, nb, out_off + nb));
+  uint64_t tot = 0, un = 0;
+  uint32_t of = 0;
+  DC_TRY(readback_multi(c, {{out_off + nb, 8, &tot}, {unm.p, 8, &un}, {ovf.p, 4, &of}}));
+  if (of) return fail(c, DC_ERR_CAPACITY, "dc_seq_associate: registry table overflow");
+  *n_frames_h = tot;
+  *n_unmatched_h = un;
+  if (tot > cap_frames) return DC_OK;  // offsets only: the caller retries with room
+  k_seq_copy<<<grid_for(c, nb * 32, 256), 256, 0, c->stream>>>(nb, fwd_of.p, foff, ffr, boff, bfr, out_off, out_frames);
   DC_LAUNCHED(c);
   return DC_OK;
 }

@@ -151,3 +151,37 @@ def test_cpu_intervals_vs_oracle_and_attribution():
     ref = oracle_run(off, fr, np.asarray([[v for v, o in zip(eiv, eok) if o]], np.uint64), 1).arrays()
     for key in ("parent", "frame", "xcnt", "xsum", "isum", "imin"):
         assert np.array_equal(np.asarray(a[key]), np.asarray(ref[key])), key
+
+
+def test_seq_associate_and_bwd_fwd_rule_vs_oracle():
+    """NEXT-4: forward/backward association (registry with repeated and negative ids, unknown ids)
+    == the oracle's replay; then ③ on the CCT of the integrated paths == the oracle's."""
+    import torch
+    import paper_2411_02797_b200 as dc
+    rng = np.random.default_rng(9500)
+    ctx = dc.Context(0)
+    nf, nb = 3000, 20_000
+    fwd_seq = rng.integers(-1, 2500, nf).astype(np.int64)
+    fwd_paths = [[int(x) for x in rng.integers(0, 40, size=int(rng.integers(0, 6)))] for _ in range(nf)]
+    bwd_seq = rng.integers(-1, 2700, nb).astype(np.int64)
+    bwd_paths = [[int(x) for x in rng.integers(40, 60, size=int(rng.integers(0, 5)))] for _ in range(nb)]
+    foff, ffr = _csr(fwd_paths)
+    boff, bfr = _csr(bwd_paths)
+    cu = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a).view(dt)).cuda()  # noqa: E731
+    off, fr, unm = dc.dc_seq_associate(ctx, cu(fwd_seq, np.int64), cu(foff, np.int64), cu(ffr, np.int32),
+                                       cu(bwd_seq, np.int64), cu(boff, np.int64), cu(bfr, np.int32))
+    exp, eunm = oracle.seq_associate(fwd_seq, fwd_paths, bwd_seq, bwd_paths)
+    o_np, f_np = off.cpu().numpy().view(np.uint64), fr.cpu().numpy().view(np.uint32)
+    got = [f_np[o_np[r]:o_np[r + 1]].tolist() for r in range(nb)]
+    assert got == exp and unm == eunm and unm > 0
+    # ③ over the integrated paths: metric 0 = backward time, 1 = forward time
+    X = np.zeros((2, nb), np.uint64)
+    t = rng.integers(1, 10**6, nb).astype(np.uint64)
+    back = rng.random(nb) < 0.5
+    X[0, back] = t[back]
+    X[1, ~back] = t[~back]
+    a = gpu_run(o_np, f_np, X, n_frames=60, ctx=ctx)
+    ref = oracle_run(o_np, f_np, X, 2)
+    for thr, floor in [(2.0, 1), (1.0, 10**5), (0.5, 0)]:
+        got = dc.dc_analyze_flags(ctx, a["_cct"], dc.DC_RULE_BWD_FWD, 0, 1, 0xFFFFFFFF, thr, floor)
+        assert got == ref.rule_flags(oracle.RULE_BWD_FWD, 0, 1, threshold=thr, floor=floor), (thr, floor)

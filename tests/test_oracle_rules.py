@@ -87,13 +87,18 @@ def _bf_flags(b, paths, X, rule, ma, mb, fk, mask, thr, floor):
     def q(i):
         if rule == 2:
             return launches[i] > 0 and b["isum"][ma][i] / launches[i] < thr
+        if rule == 3:
+            f = order[i][-1]
+            kind_ok = fk is None or (int(fk[f]) < 32 and (mask >> int(fk[f])) & 1)
+            bwd, fwd = b["isum"][ma][i], b["isum"][mb][i]
+            return bool(kind_ok) and fwd > 0 and fwd >= floor and bwd / fwd > thr
         cpu, gpu = b["isum"][ma][i], b["isum"][mb][i]
         return cpu > floor and cpu / max(gpu, 1) > thr
 
     flagged = []
     for i in range(1, N):
         anc = [b["ids"][order[i][:d]] for d in range(1, len(order[i]))]
-        if q(i) and not any(q(a) for a in anc):
+        if q(i) and (rule == 3 or not any(q(a) for a in anc)):
             flagged.append(i)
     return flagged
 
@@ -108,7 +113,7 @@ def test_rules_bruteforce_random(seed):
         b = bf.cct(paths, X)
         o = run(paths, X)
         M = len(X)
-        for rule in (2, 5):
+        for rule in (2, 3, 5):
             ma, mb = int(rng.integers(0, M)), int(rng.integers(0, M))
             vals = [v for row in X for v in row] or [1]
             thr = float(rng.choice([0.5, 1.0, 2.0, float(np.median(vals)) + 0.5]))
@@ -208,3 +213,36 @@ def test_cpu_intervals_sum_law():
             if sel:
                 assert sum(iv[i] for i in sel) == int(ts[sel[-1]] - ts[sel[0]])
                 assert [ok[i] for i in sel] == [False] + [True] * (len(sel) - 1)
+
+
+# ------------------------------------------------------------------ NEXT-4: forward/backward
+def test_spec_associate_backward():
+    """SPEC.md associate_backward: registry has seq 7 -> the output's root section is the forward
+    prefix of seq 7; an absent id -> the backward path unchanged + 1 diagnostic; two backward ops
+    with seq 7 get identical prefixes; a later registry entry replaces an earlier one."""
+    fwd_seq = [7, 3, 7]
+    fwd = [[0, 1, 5], [0, 2], [0, 1, 6]]          # the second seq-7 entry replaces the first
+    bwd_seq = [7, 9, 7, -1]
+    bwd = [[20, 21], [22], [23], [24]]
+    paths, unmatched = oracle.seq_associate(fwd_seq, fwd, bwd_seq, bwd)
+    assert paths == [[0, 1, 6, 20, 21], [22], [0, 1, 6, 23], [24]] and unmatched == 1
+
+
+def test_spec_fwd_bwd_rule_dlrm_fixture():
+    """③ (PAPER.md:406-412, SPEC.md analyze_fwd_bwd): DLRM aten::index forward 0.8 % vs backward
+    39.9 % of the time -> ratio 49.9 > 2 -> flagged; forward == backward -> not
+    flagged; forward below the epsilon -> skipped."""
+    OP, KERNEL = 1, 4
+    # frames: 0 train.py (PY), 1 aten::index (OP), 2 aten::mm (OP), 3 fwd kernel, 4 bwd kernel (KERNEL)
+    fk = np.array([0, OP, OP, KERNEL, KERNEL], np.uint8)
+    # metric 0 = backward time, metric 1 = forward time (a record's time in its direction's column)
+    paths = [(0, 1, 3), (0, 1, 4), (0, 2, 3), (0, 2, 4)]
+    bwd = [0, 39_900, 0, 500]
+    fwd = [800, 0, 500, 0]
+    o = run(paths, [bwd, fwd])
+    ids = {tuple(q): i for i, q in enumerate(bf.cct(paths, [bwd, fwd])["order"])}
+    got = o.rule_flags(oracle.RULE_BWD_FWD, 0, 1, kind_mask=1 << OP, frame_kind=fk, threshold=2.0, floor=1)
+    assert got == [ids[(0, 1)]]
+    assert abs(39_900 / 800 - 49.875) < 1e-12
+    # epsilon: a forward time below the floor is skipped
+    assert o.rule_flags(oracle.RULE_BWD_FWD, 0, 1, kind_mask=1 << OP, frame_kind=fk, threshold=2.0, floor=1000) == []

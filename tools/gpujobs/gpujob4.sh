@@ -1,5 +1,3 @@
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_parity.py -x -q --timeout 300 -k "owner or config or f1 or random" > gpurun_out/gpu_tests.log 2>&1; echo "rc=$?" >> gpurun_out/gpu_tests.log
-tail -3 gpurun_out/gpu_tests.log
-timeout 300 python -u tools/own_modes.py 9 0 > gpurun_out/own_modes.log 2>&1
-grep -v "^$" gpurun_out/own_modes.log | tail -6
+timeout 600 python -m pytest tests/test_gpu_rules.py -x -q --timeout 300 > gpurun_out/gpu_rules.log 2>&1; echo "rc=$?" >> gpurun_out/gpu_rules.log
+tail -8 gpurun_out/gpu_rules.log
