@@ -85,44 +85,28 @@ __global__ void k_own_keys(const uint32_t* __restrict__ leaf, uint64_t n_launch,
   }
 }
 
-// Launches ordered by context in one CTA (counting sort over the context ids, shared-memory
-// histogram; the order inside a context is irrelevant to the result) with the offsets check
-// fused in: replaces check + keys + a multi-pass radix sort when the launch count and the node
-// count are small (config 3: 20k launches, 18k nodes).
-constexpr int OS_THREADS = 1024;
-constexpr uint32_t OS_MAX_BINS = 36864;  // 144 KB of u32 counters
-__global__ void __launch_bounds__(OS_THREADS) k_own_sort_small(const uint32_t* __restrict__ leaf, const uint64_t* __restrict__ off,
-                                                               uint64_t n_launch, uint64_t n, uint64_t N,
-                                                               uint64_t* __restrict__ key, uint32_t* __restrict__ val,
-                                                               uint32_t* bad) {
-  extern __shared__ uint32_t hist[];  // [N + 1]
-  const uint32_t NB = (uint32_t)N + 1;
-  for (uint32_t i = threadIdx.x; i < NB; i += OS_THREADS) hist[i] = 0;
-  __syncthreads();
+// Launches ordered by context with a counting sort over the context ids (the order inside a
+// context is irrelevant to the result): histogram with the offsets check fused in, a scan of the
+// N + 1 counters, a scatter through atomic cursors. Three launches instead of check + keys + a
+// multi-pass radix sort.
+__global__ void k_own_hist(const uint32_t* __restrict__ leaf, const uint64_t* __restrict__ off, uint64_t n_launch, uint64_t n,
+                           uint64_t N, uint32_t* __restrict__ hist, uint32_t* bad) {
   bool b = false;
-  for (uint32_t l = threadIdx.x; l < n_launch; l += OS_THREADS) {
+  for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < n_launch; l += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t c = leaf[l];
     atomicAdd(&hist[c < N ? c : (uint32_t)N], 1u);
     b |= off[l + 1] < off[l];
   }
-  if (threadIdx.x == 0 && (off[0] != 0 || off[n_launch] != n)) b = true;
-  if (__syncthreads_or(b) && threadIdx.x == 0) atomicOr(bad, 1u);
-  // exclusive scan of the histogram: contiguous chunk per thread, then a block scan of the chunk sums
-  const uint32_t per = (NB + OS_THREADS - 1) / OS_THREADS, lo = threadIdx.x * per, hi = min(NB, lo + per);
-  uint32_t sum = 0;
-  for (uint32_t i = lo; i < hi; ++i) sum += hist[i];
-  uint32_t run = block_excl_scan<uint32_t, OS_THREADS>(sum, nullptr);
-  for (uint32_t i = lo; i < hi; ++i) {
-    const uint32_t v = hist[i];
-    hist[i] = run;
-    run += v;
-  }
-  __syncthreads();
-  for (uint32_t l = threadIdx.x; l < n_launch; l += OS_THREADS) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (off[0] != 0 || off[n_launch] != n)) b = true;
+  if (b) atomicOr(bad, 1u);
+}
+__global__ void k_own_scatter(const uint32_t* __restrict__ leaf, uint64_t n_launch, uint64_t N, uint32_t* __restrict__ cursor,
+                              uint64_t* __restrict__ key, uint32_t* __restrict__ val) {
+  for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < n_launch; l += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t c0 = leaf[l], c = c0 < N ? c0 : (uint32_t)N;
-    const uint32_t pos = atomicAdd(&hist[c], 1u);
+    const uint32_t pos = atomicAdd(&cursor[c], 1u);
     key[pos] = c;
-    val[pos] = l;
+    val[pos] = (uint32_t)l;
   }
 }
 
@@ -1263,14 +1247,14 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
     DC_TRY(alloc(c, v0, n_launch));
     DC_TRY(alloc(c, v1, n_launch));
     bool in1 = false;
-    if (n_launch <= 65536 && N + 1 <= OS_MAX_BINS && !getenv("DC_TEST_OWN_RADIX")) {
+    if (N < (1ull << 31) && !getenv("DC_TEST_OWN_RADIX")) {
       Region rs(c, "prep:sort");
-      static bool attr = false;
-      if (!attr) {
-        DC_CUDA(c, cudaFuncSetAttribute(k_own_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(OS_MAX_BINS * 4)));
-        attr = true;
-      }
-      k_own_sort_small<<<1, OS_THREADS, (N + 1) * 4, c->stream>>>(launch_leaf, launch_off, n_launch, n, N, k0.p, v0.p, bad.p);
+      Buf<uint32_t> hist;
+      DC_TRY(alloc_zero(c, hist, N + 1));
+      k_own_hist<<<grid_for(c, n_launch, 256), 256, 0, c->stream>>>(launch_leaf, launch_off, n_launch, n, N, hist.p, bad.p);
+      DC_LAUNCHED(c);
+      DC_TRY(excl_scan<uint32_t>(c, hist.p, hist.p, N + 1, nullptr));
+      k_own_scatter<<<grid_for(c, n_launch, 256), 256, 0, c->stream>>>(launch_leaf, n_launch, N, hist.p, k0.p, v0.p);
       DC_LAUNCHED(c);
     } else {
       k_own_check<<<grid_for(c, n_launch, 256), 256, 0, c->stream>>>(launch_off, n_launch, n, bad.p);
