@@ -301,16 +301,19 @@ def main():
     l0 = ctx.launches
     b0 = ctx.diag()["bytes_moved_est"]
     clk = Clocks(local)
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     with clk:
         e0.record(stream)
         last = None
-        for _ in range(args.steps):
+        for i in range(args.steps):
             cct, views = run_step(dc, ctx, tr, args.config, comm=comm)
             if last is not None:
                 last.free()
             last = cct
+            step_ev[i].record(stream)  # per-step boundaries (distribution of step times)
         e1.record(stream)
         torch.cuda.synchronize()
+    per_step = [e0.elapsed_time(step_ev[0])] + [step_ev[i - 1].elapsed_time(step_ev[i]) for i in range(1, args.steps)]
     barrier()
     launches = (ctx.launches - l0) // args.steps
     step_bytes = (ctx.diag()["bytes_moved_est"] - b0) / args.steps
@@ -413,7 +416,9 @@ def main():
                 "roofline": roof, "stages_ms": stages, "gpu_launches": int(launches),
                 "step_hbm": {"alg_bytes_per_step": int(step_bytes), "gbs": round(step_bytes / (ms / 1e3) / 1e9, 1),
                              "frac_of_peak": round(step_bytes / (ms / 1e3) / 1e9 / peak, 4)},
-                "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu}
+                "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
+                "step_ms_dist": {"min": round(min(per_step), 4), "median": round(statistics.median(per_step), 4),
+                                 "max": round(max(per_step), 4)}}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

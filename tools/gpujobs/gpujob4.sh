@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_merge.py -x -q --timeout 300 > gpurun_out/gpu_tests.log 2>&1; echo "rc=$?" >> gpurun_out/gpu_tests.log
-tail -2 gpurun_out/gpu_tests.log
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/l.csv python -u bench.py --steps 1 --warmup 3 --e2e-steps 0 --no-cpu > gpurun_out/l.log 2>&1
+timeout 300 python -u tools/host_overhead.py > gpurun_out/host.log 2>&1; head -60 gpurun_out/host.log
+nproc; cat /proc/cpuinfo | grep "model name" | head -1

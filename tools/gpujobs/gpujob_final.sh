@@ -1,0 +1,6 @@
+# full check of the tree on a fresh box: all GPU tests, smoke(), default bench line
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests -m gpu -q --timeout 300 > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/gpu_tests.log
+tail -4 gpurun_out/gpu_tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log; tail -2 gpurun_out/smoke.log
+timeout 600 python -u bench.py > gpurun_out/bench.log 2>&1; tail -c 2600 gpurun_out/bench.log
