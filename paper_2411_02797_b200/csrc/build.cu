@@ -48,6 +48,7 @@ constexpr uint32_t PT_FW = 8192;    // staged frame window per stage (32 KB): 2 
 constexpr uint32_t PT_CH = 17;      // chunk length (staged tiles; odd: bank spread)
 constexpr uint32_t PT_CH_G = 129;   // chunk length (global tiles)
 constexpr uint32_t PT_NONE = 0xFFFFFFFFu;
+constexpr int PG_U = 4;             // k_path_group: records verified per round
 
 struct __align__(32) PathSlot {
   unsigned long long key;  // record hash, ~0 = empty
@@ -319,11 +320,11 @@ __global__ void __launch_bounds__(256) k_path_group(const uint64_t* __restrict__
     // compare, so the DRAM latency of the own frames is paid once per group
     uint32_t todo = __ballot_sync(0xffffffffu, need == 1u);
     while (todo) {
-      int idx[8];
-      uint64_t oo[8], rr[8];
-      uint32_t ll[8];
+      int idx[PG_U];
+      uint64_t oo[PG_U], rr[PG_U];
+      uint32_t ll[PG_U];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < PG_U; ++u) {
         idx[u] = todo ? __ffs(todo) - 1 : -1;
         if (todo) todo &= todo - 1;
         const int i = idx[u] < 0 ? 0 : idx[u];
@@ -332,9 +333,9 @@ __global__ void __launch_bounds__(256) k_path_group(const uint64_t* __restrict__
         const uint32_t li = __shfl_sync(0xffffffffu, L, i);
         ll[u] = idx[u] < 0 ? 0u : li;
       }
-      uint32_t a0[8], b0[8], a1[8], b1[8];
+      uint32_t a0[PG_U], b0[PG_U], a1[PG_U], b1[PG_U];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < PG_U; ++u) {
         const bool p0 = lane < ll[u], p1 = lane + 32 < ll[u];
         a0[u] = p0 ? ld_stream_u32(frames + oo[u] + lane) : 0u;
         b0[u] = p0 ? __ldg(frames + rr[u] + lane) : 0u;
@@ -342,7 +343,7 @@ __global__ void __launch_bounds__(256) k_path_group(const uint64_t* __restrict__
         b1[u] = p1 ? __ldg(frames + rr[u] + lane + 32) : 0u;
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < PG_U; ++u) {
         bool diff = (a0[u] != b0[u]) | (a1[u] != b1[u]);
         for (uint32_t j = lane + 64; j < ll[u]; j += 32) diff |= ld_stream_u32(frames + oo[u] + j) != __ldg(frames + rr[u] + j);
         if (__any_sync(0xffffffffu, diff) && lane == (uint32_t)idx[u]) need = 2u;

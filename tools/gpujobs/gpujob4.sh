@@ -1,5 +1,4 @@
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_parity.py -x -q --timeout 300 -k "owner or config or f1 or random or generic" > gpurun_out/gpu_tests.log 2>&1; echo "rc=$?" >> gpurun_out/gpu_tests.log
+timeout 600 python -m pytest tests/test_gpu_configs45.py tests/test_gpu_parity.py -x -q --timeout 300 -k "config or random or largeP or collision" > gpurun_out/gpu_tests.log 2>&1; echo "rc=$?" >> gpurun_out/gpu_tests.log
 tail -2 gpurun_out/gpu_tests.log
-timeout 300 python -u tools/own_modes.py 9 0 > gpurun_out/own_modes.log 2>&1
-grep -v "^$" gpurun_out/own_modes.log | tail -6
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/cfg4_launches.csv python -u bench.py --config 4 --steps 1 --warmup 3 --e2e-steps 0 --no-cpu > gpurun_out/cfg4_launches.log 2>&1
