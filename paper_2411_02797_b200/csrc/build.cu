@@ -40,7 +40,7 @@ __device__ __forceinline__ int bits_for_dev(uint32_t v) { return v ? 32 - __clz(
 //     length; then the warp compares each record with its representative, 32 frames at a time
 //     (coalesced on both sides). A mismatch (a hash collision) makes the record a
 //     representative of its own, so the dedup is exact whatever the hash.
-constexpr int PT_T = 128;           // records per tile
+constexpr int PT_T = 128;           // records per tile (96 with a 24 KB window: 13.4 ms vs 11.0 on config 4)
 constexpr int PT_THREADS = 256;
 constexpr int PT_WARPS = PT_THREADS / 32;
 constexpr int PT_RPW = PT_T / PT_WARPS;  // records per warp (16)
@@ -105,8 +105,8 @@ __device__ __forceinline__ void pt_hash_chunks(PathWarp& W, const uint32_t* __re
   for (uint32_t ci = lane_id(); ci < n_chunks; ci += 32) {
     uint32_t k = 0;
 #pragma unroll
-    for (uint32_t step = PT_RPW / 2; step; step >>= 1)
-      if (W.cs[k + step] <= ci) k += step;
+    for (uint32_t step = 16; step; step >>= 1)  // largest record whose chunk start <= ci (PT_RPW <= 32)
+      if (k + step < PT_RPW && W.cs[k + step] <= ci) k += step;
     const uint32_t j0 = (ci - W.cs[k]) * CH;
     const uint32_t j1 = min(j0 + CH, W.L[k]);
     const uint32_t* q = src + (W.o[k] - base);
