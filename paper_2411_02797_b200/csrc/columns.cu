@@ -32,7 +32,10 @@ __global__ void k_attribute(const uint32_t* __restrict__ leaf, uint64_t R, const
     for (uint32_t m = 0; m < M; ++m) {
       uint64_t x = X[m * ld + r];
       atomicAdd(mcols + ((uint64_t)C_XSUM * M + m) * N + n, (unsigned long long)x);
-      atomicMin(mcols + ((uint64_t)C_XMIN * M + m) * N + n, (unsigned long long)x);
+      // min only when x can lower it: after the first few records of a node the plain read
+      // (an L2 hit) settles almost every record without an atomic
+      unsigned long long* mn = mcols + ((uint64_t)C_XMIN * M + m) * N + n;
+      if (x < ld_relaxed_u64(mn)) atomicMin(mn, (unsigned long long)x);
       uint64_t sq_lo = x * x, sq_hi = __umul64hi(x, x);
       atomic_add_u128(mcols + ((uint64_t)C_XSQLO * M + m) * N + n, mcols + ((uint64_t)C_XSQHI * M + m) * N + n, sq_lo, sq_hi);
     }
