@@ -33,13 +33,12 @@ __global__ void __launch_bounds__(256) k_intern_insert(const dc_frame_key* __res
   for (int i = threadIdx.x; i < IC_SLOTS; i += blockDim.x) c_slot[i] = IC_EMPTY;
   __syncthreads();
   uint64_t mx_addr = 0, mx_ks = 0;  // radix widths of the canonical sort (max addr, max kind<<32|str)
-  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
-    ulonglong2 kv = __ldg(reinterpret_cast<const ulonglong2*>(keys) + j);  // 16-B coalesced load
+  auto process = [&](uint64_t j, ulonglong2 kv) {
     const uint64_t lo = kv.x, hi = kv.y;                                    // lo = kind | str<<32, hi = addr
     if ((uint32_t)lo == 0xFFFFFFFFu) {
       atomicOr(d_flags, FLAG_BAD_KEY);
       out_slot[j] = 0;
-      continue;
+      return;
     }
     mx_addr = max(mx_addr, hi);
     mx_ks = max(mx_ks, (lo << 32) | (lo >> 32));
@@ -49,14 +48,14 @@ __global__ void __launch_bounds__(256) k_intern_insert(const dc_frame_key* __res
     uint32_t found = 0xFFFFFFFFu, claim = IC_EMPTY;
     for (int k = 0; k < IC_PROBE; ++k) {
       const uint32_t e = (c0 + k) & (IC_SLOTS - 1);
-      const uint32_t v = *(volatile uint32_t*)&c_slot[e];
+      uint32_t v;  // acquire: a published slot word orders the entry's key before it
+      asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(&c_slot[e])) : "memory");
       if (v == IC_EMPTY) {  // the key is not cached: claim this entry for it (best effort)
         if (atomicCAS(&c_slot[e], IC_EMPTY, IC_BUSY) == IC_EMPTY) claim = e;
         break;
       }
       if (v == IC_BUSY) continue;
-      __threadfence_block();
-      if (*(volatile unsigned long long*)&c_lo[e] == lo && *(volatile unsigned long long*)&c_hi[e] == hi) {
+      if (c_lo[e] == lo && c_hi[e] == hi) {
         found = v;
         break;
       }
@@ -90,6 +89,17 @@ __global__ void __launch_bounds__(256) k_intern_insert(const dc_frame_key* __res
       atomicExch(&c_slot[claim], found);
     }
     out_slot[j] = found;
+  };
+  // four keys per thread in flight: their 16-B loads are issued before any of them is resolved
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j0 < n; j0 += 4 * stride) {
+    ulonglong2 kv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      kv[u] = j0 + u * stride < n ? __ldg(reinterpret_cast<const ulonglong2*>(keys) + j0 + u * stride) : make_ulonglong2(0, 0);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (j0 + u * stride < n) process(j0 + u * stride, kv[u]);
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
@@ -188,7 +198,7 @@ dc_status intern_frames(Ctx* c, const dc_frame_key* keys, uint64_t n, uint32_t* 
     DC_TRY(alloc_zero(c, cnt, 1));
     DC_TRY(alloc_zero(c, ovf, 1));
     DC_TRY(alloc_zero(c, mx, 2));
-    k_intern_insert<<<grid_for(c, n, 256), 256, 0, c->stream>>>(keys, n, table.p, cap - 1, out_ids, cnt.p, ovf.p,
+    k_intern_insert<<<grid_for(c, (n + 3) / 4, 256), 256, 0, c->stream>>>(keys, n, table.p, cap - 1, out_ids, cnt.p, ovf.p,
                                                                  c->d_flags, mx.p);
     DC_LAUNCHED(c);
     uint64_t h[2] = {0, 0};
