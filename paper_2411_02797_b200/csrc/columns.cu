@@ -19,9 +19,14 @@ __global__ void k_fill_u64(uint64_t* a, uint64_t n, uint64_t v) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) a[i] = v;
 }
 
+// K > 1 (small trees with many records per node): CTA b updates copy b % K of the columns
+// (strides cs / ms), so K times fewer updates meet on one address; k_attr_fold adds the copies
+// into the node columns. K = 1 updates the node columns directly.
 __global__ void k_attribute(const uint32_t* __restrict__ leaf, uint64_t R, const uint64_t* __restrict__ X, uint32_t M,
-                            uint64_t ld, uint64_t N, unsigned long long* __restrict__ xcnt, unsigned long long* __restrict__ mcols,
-                            uint32_t* d_flags) {
+                            uint64_t ld, uint64_t N, unsigned long long* __restrict__ xcnt0, unsigned long long* __restrict__ mcols0,
+                            uint32_t* d_flags, uint32_t K, uint64_t cs, uint64_t ms) {
+  unsigned long long* xcnt = xcnt0 + (uint64_t)(blockIdx.x % K) * cs;
+  unsigned long long* mcols = mcols0 + (uint64_t)(blockIdx.x % K) * ms;
   for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < R; r += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t n = leaf[r];
     if (n >= N) {
@@ -39,6 +44,52 @@ __global__ void k_attribute(const uint32_t* __restrict__ leaf, uint64_t R, const
       uint64_t sq_lo = x * x, sq_hi = __umul64hi(x, x);
       atomic_add_u128(mcols + ((uint64_t)C_XSQLO * M + m) * N + n, mcols + ((uint64_t)C_XSQHI * M + m) * N + n, sq_lo, sq_hi);
     }
+  }
+}
+
+// the K copies: count, then per metric (sum, min, sq_lo, sq_hi); min starts at UINT64_MAX
+__global__ void k_attr_init_copies(uint64_t* __restrict__ cnt, uint64_t* __restrict__ cols, uint32_t K, uint32_t M, uint64_t N) {
+  const uint64_t MN = (uint64_t)M * N, tot_c = (uint64_t)K * N, tot_m = (uint64_t)K * 4 * MN;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < tot_c + tot_m; i += (uint64_t)gridDim.x * blockDim.x) {
+    if (i < tot_c) {
+      cnt[i] = 0;
+    } else {
+      const uint64_t j = i - tot_c;
+      cols[j] = ((j / MN) % 4 == C_XMIN) ? ~0ull : 0ull;
+    }
+  }
+}
+// node columns += the K copies (exact: u64 count / sum, min, 128-bit sum of squares)
+__global__ void k_attr_fold(const uint64_t* __restrict__ cnt, const uint64_t* __restrict__ cols, uint32_t K, uint32_t M, uint64_t N,
+                            uint64_t* __restrict__ xcnt, uint64_t* __restrict__ mcols) {
+  const uint64_t MN = (uint64_t)M * N;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < N * (1 + M); i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t g = i / N, n = i - g * N;
+    if (g == 0) {
+      uint64_t c = 0;
+      for (uint32_t k = 0; k < K; ++k) c += cnt[(uint64_t)k * N + n];
+      xcnt[n] += c;
+      continue;
+    }
+    const uint64_t m = g - 1;
+    uint64_t sum = 0, mn = ~0ull, lo = 0, hi = 0;
+    for (uint32_t k = 0; k < K; ++k) {
+      const uint64_t* b = cols + (uint64_t)k * 4 * MN;
+      sum += b[(uint64_t)C_XSUM * MN + m * N + n];
+      mn = min(mn, b[(uint64_t)C_XMIN * MN + m * N + n]);
+      const uint64_t l = b[(uint64_t)C_XSQLO * MN + m * N + n];
+      const uint64_t t = lo + l;
+      hi += b[(uint64_t)C_XSQHI * MN + m * N + n] + (t < lo);
+      lo = t;
+    }
+    mcols[(uint64_t)C_XSUM * MN + m * N + n] += sum;
+    uint64_t& xm = mcols[(uint64_t)C_XMIN * MN + m * N + n];
+    xm = min(xm, mn);
+    uint64_t& ql = mcols[(uint64_t)C_XSQLO * MN + m * N + n];
+    uint64_t& qh = mcols[(uint64_t)C_XSQHI * MN + m * N + n];
+    const uint64_t nl = ql + lo;
+    qh = qh + hi + (nl < lo);
+    ql = nl;
   }
 }
 
@@ -68,9 +119,24 @@ dc_status ensure_metric_cols(Ctx* c, dc_cct* t, uint32_t M) {
 
 dc_status attribute_metrics(Ctx* c, dc_cct* t, const uint32_t* leaf, uint64_t R, const uint64_t* X, uint32_t M, uint64_t ld) {
   DC_TRY(ensure_metric_cols(c, t, M));
-  if (R) {
-    k_attribute<<<grid_for(c, R, 256), 256, 0, c->stream>>>(leaf, R, X, M, ld, t->N, (unsigned long long*)t->xcnt,
-                                                            (unsigned long long*)t->mcols, c->d_flags);
+  const uint64_t N = t->N;
+  // contention: with many records per node, same-address atomics serialise; spread them over K
+  // copies of the columns (a few MB at most) and fold the copies afterwards
+  const uint32_t K = (N <= (1u << 16) && R >= 64 * N && !getenv("DC_TEST_ATTR_DIRECT")) ? 16u : 1u;
+  if (R && K == 1) {
+    k_attribute<<<grid_for(c, R, 256), 256, 0, c->stream>>>(leaf, R, X, M, ld, N, (unsigned long long*)t->xcnt,
+                                                            (unsigned long long*)t->mcols, c->d_flags, 1, 0, 0);
+    DC_LAUNCHED(c);
+  } else if (R) {
+    Buf<uint64_t> ccnt, ccols;
+    DC_TRY(alloc(c, ccnt, (uint64_t)K * N));
+    DC_TRY(alloc(c, ccols, (uint64_t)K * 4 * M * N + 1));
+    k_attr_init_copies<<<grid_for(c, (uint64_t)K * N * (1 + 4 * M), 256), 256, 0, c->stream>>>(ccnt.p, ccols.p, K, M, N);
+    DC_LAUNCHED(c);
+    k_attribute<<<grid_for(c, R, 256), 256, 0, c->stream>>>(leaf, R, X, M, ld, N, (unsigned long long*)ccnt.p,
+                                                            (unsigned long long*)ccols.p, c->d_flags, K, N, 4ull * M * N);
+    DC_LAUNCHED(c);
+    k_attr_fold<<<grid_for(c, N * (1 + M), 256), 256, 0, c->stream>>>(ccnt.p, ccols.p, K, M, N, t->xcnt, t->mcols);
     DC_LAUNCHED(c);
   }
   t->state = 1;

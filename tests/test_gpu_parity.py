@@ -133,7 +133,7 @@ def test_kind_mask_and_bottom_up_with_dict():
                 assert got == [(int(e["id"]), int(e["value"]), float(e["fraction"])) for e in exp]
 
 
-@pytest.mark.parametrize("cfg,R", [(1, None), (2, 200_000), (3, None)])
+@pytest.mark.parametrize("cfg,R", [(1, None), (2, 200_000), (2, 1_000_000), (3, None)])
 def test_configs_vs_oracle(cfg, R):
     p = gen.programs.program(cfg) if cfg != 3 else gen.programs.config3(n_samples=4_000_000)
     tr = gen.make_trace(p, n_records=R, pc=(cfg == 3), bad_per_million=500 if cfg == 3 else 0)
@@ -335,3 +335,20 @@ def test_large_P_build_variants(monkeypatch, env):
     assert a["level_off"].tolist() == lo
     if "DC_TEST_WEAK_NODE_HASH" in env:
         assert ctx.diag()["collisions_detected"] > 0
+
+
+@pytest.mark.parametrize("direct", [False, True])
+def test_attribute_contended_columns(monkeypatch, direct):
+    """Many records on few nodes (the replicated-column attribution path, K copies folded) and the
+    direct path: identical to the oracle, with values up to 2^40 (128-bit squares)."""
+    if direct:
+        monkeypatch.setenv("DC_TEST_ATTR_DIRECT", "1")
+    rng = np.random.default_rng(77)
+    base = [tuple(int(x) for x in rng.integers(0, 20, size=int(rng.integers(1, 7)))) for _ in range(60)]
+    paths = [base[i] for i in rng.integers(0, len(base), size=300_000)]
+    off, fr = _csr(paths)
+    X = np.stack([rng.integers(0, 2**40, size=len(paths), dtype=np.uint64),
+                  rng.integers(0, 1000, size=len(paths), dtype=np.uint64)])
+    a = gpu_run(off, fr, X, n_frames=20)
+    ref = oracle_run(off, fr, X, 2).arrays()
+    assert_same(a, ref, ctx=f"contended direct={direct}")
