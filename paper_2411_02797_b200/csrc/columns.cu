@@ -173,7 +173,8 @@ __global__ void k_push(const uint32_t* __restrict__ parent, uint64_t N, uint32_t
       // ids strictly decrease towards the root (parent[n] < n), which also bounds the walk
       for (uint32_t a = parent[n], prev = (uint32_t)n; a < prev; prev = a, a = parent[a]) {
         if (s) atomicAdd(mcols + ((uint64_t)C_ISUM * M + m) * N + a, (unsigned long long)s);
-        atomicMin(mcols + ((uint64_t)C_IMIN * M + m) * N + a, (unsigned long long)mn);
+        unsigned long long* pm = mcols + ((uint64_t)C_IMIN * M + m) * N + a;
+        if (mn < ld_relaxed_u64(pm)) atomicMin(pm, (unsigned long long)mn);
         if (qlo | qhi)
           atomic_add_u128(mcols + ((uint64_t)C_ISQLO * M + m) * N + a, mcols + ((uint64_t)C_ISQHI * M + m) * N + a, qlo, qhi);
         if (a == 0) break;
