@@ -112,7 +112,7 @@ __global__ void k_own_scatter(const uint32_t* __restrict__ leaf, uint64_t n_laun
 
 // ---- stage plan. The ctx-ordered launches are laid out as a stream of 32-sample rows: launch i
 // takes rows_i = ceil(cnt_i / 32) rows (its last row partial), the launches of one context are
-// contiguous and every context starts on a stage boundary (64 rows), so a stage holds one
+// contiguous and every context starts on a stage boundary (OW_ROWS rows), so a stage holds one
 // context and every row one launch. Per row the plan stores the launch id and the number of
 // valid samples (0 for padding); per stage, its first launch and context.
 __global__ void k_plan_launch(const uint64_t* __restrict__ off, const uint32_t* __restrict__ order,
@@ -143,7 +143,7 @@ __global__ void k_plan_gstages(const uint64_t* __restrict__ E, const uint32_t* _
                                uint64_t n_launch, uint64_t* __restrict__ gst) {
   const uint32_t NG = *ng;
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < n_launch; g += (uint64_t)gridDim.x * blockDim.x)
-    gst[g] = g < NG ? (E[gfirst[g + 1]] - E[gfirst[g]] + 63) / 64 : 0;
+    gst[g] = g < NG ? (E[gfirst[g + 1]] - E[gfirst[g]] + OW_ROWS - 1) / OW_ROWS : 0;
 }
 
 // one warp per launch: row position, row meta, stage starts
@@ -158,7 +158,7 @@ __global__ void k_plan_rows(const uint64_t* __restrict__ E, const uint32_t* __re
   for (uint64_t i = wid; i < n_launch; i += nw) {
     const uint32_t flag = (i == 0 || lkey[i] != lkey[i - 1]) ? 1u : 0u;
     const uint32_t g = gx[i] + flag - 1;
-    const uint64_t rp = 64 * SB[g] + E[i] - E[gfirst[g]];
+    const uint64_t rp = OW_ROWS * SB[g] + E[i] - E[gfirst[g]];
     const uint64_t rows = E[i + 1] - E[i], c = lcnt[i];
     const uint32_t l = order[i], ctx = (uint32_t)lkey[i];
     if (lane == 0) rowpos[i] = rp;
@@ -170,9 +170,9 @@ __global__ void k_plan_rows(const uint64_t* __restrict__ E, const uint32_t* __re
       }
     }
     if (rows > 0) {  // stages whose first row lies in this launch
-      const uint64_t s_lo = (rp + 63) / 64, s_hi = (rp + rows - 1) / 64;
+      const uint64_t s_lo = (rp + OW_ROWS - 1) / OW_ROWS, s_hi = (rp + rows - 1) / OW_ROWS;
       for (uint64_t st = s_lo + lane; st <= s_hi; st += 32)
-        if (64 * st < row_cap) {
+        if (OW_ROWS * st < row_cap) {
           st_first[st] = (uint32_t)i;
           st_ctx[st] = ctx;
         }
@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
   if (tid < 32) {
     // ------------------------------------------------ producer warp
     // Per stage s the plan gives the first launch f; lane j cuts launch f + j to the stage's rows
-    // [64 s, 64 s + 64) and issues its own TMA bulk copy, lane 0 copies the stage's row meta.
+    // [OW_ROWS s, OW_ROWS (s + 1)) and issues its own TMA bulk copy, lane 0 copies the row meta.
     // The launch fields of stage s + 1 are loaded while stage s is issued (and the per-stage
     // first-launch / context words 32 stages at a time, one batch ahead).
     const uint32_t lane = tid;
@@ -465,7 +465,7 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
       if (lane == 0) mbar_wait(&sm.empty[st], ph ^ 1u);  // the slot (and its meta) is free
       __syncwarp();
       const long long pc1 = prof ? clock64() : 0;
-      const uint64_t R0 = 64 * s, R1 = R0 + 64;
+      const uint64_t R0 = OW_ROWS * s, R1 = R0 + OW_ROWS;
       if (lane == 0) {
         uint32_t flush = ctx != prev_ctx ? 1u : 0u;
         if (*freq) {
@@ -1235,9 +1235,9 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
   Buf<uint64_t> lrow, lsrc, lcnt, gst, rowpos, tot;
   Buf<uint32_t> lflag, gx, gfirst, row_launch, st_first, st_ctx;
   Buf<uint8_t> row_valid;
-  // rows: sum ceil(cnt/32) <= n/32 + n_launch; context padding < 64 rows per context (<= n_launch)
-  const uint64_t st_cap = (n / 32 + n_launch + 63) / 64 + n_launch + 1;
-  const uint64_t row_cap = 64 * st_cap;
+  // rows: sum ceil(cnt/32) <= n/32 + n_launch; context padding < OW_ROWS rows per context (<= n_launch)
+  const uint64_t st_cap = (n / 32 + n_launch + OW_ROWS - 1) / OW_ROWS + n_launch + 1;
+  const uint64_t row_cap = OW_ROWS * st_cap;
   {
     Region rp(c, "pc:prep");
     DC_TRY(alloc_zero(c, bad, 1));
