@@ -125,9 +125,12 @@ def make_workload(cfg: int, rank: int, device: str, n_records: int | None = None
         p = programs.config2()
     elif cfg == 4:
         p = programs.config4()
+    elif cfg == 5:
+        p = programs.config5(shard=rank)  # rank p builds shard p (its own seed and rank-local frames)
     else:
         p = programs.config1()
-    p.seed = p.seed + 7919 * rank  # weak scaling: each rank its own draws of the same program
+    if cfg != 5:
+        p.seed = p.seed + 7919 * rank  # weak scaling: each rank its own draws of the same program
     tr = gen.make_trace(p, n_records=n_records, device=device, raw_keys=(cfg != 4), ids=(cfg == 4), pc=(cfg == 3))
     return p, tr
 
@@ -238,7 +241,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="dc", choices=["dc", "reference"])
-    ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4])
+    ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--records", type=int, default=None, help="override record count (configs 2/4)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-launches", type=int, default=1000, help="bounded oracle sample (launch records)")
@@ -355,7 +358,7 @@ def main():
 
     # ---------------- e2e through the public API with host buffers
     e2e = None
-    if args.e2e_steps > 0 and args.config in (1, 2, 3):
+    if args.e2e_steps > 0 and args.config in (1, 2, 3, 5):
         host = {"keys": tr.keys.cpu().pin_memory(), "offsets": tr.offsets.cpu().pin_memory(),
                 "metrics": tr.metrics.cpu().pin_memory()}
         if args.config == 3:
@@ -403,14 +406,16 @@ def main():
         wl = {3: "config3: LLM-inference PC-sampling trace, 20k launch records (raw 16-B frame keys, mean depth ~42) "
                  "+ 100M PC samples (16 B each), 24 stall reasons",
               2: "config2: ResNet-50-training-shaped trace, 1M launch records, 5 metrics, raw frame keys",
-              1: "config1: tiny 10k-record trace", 4: "config4: JAX-shaped pre-interned trace, depth <= 256"}[args.config]
+              1: "config1: tiny 10k-record trace", 4: "config4: JAX-shaped pre-interned trace, depth <= 256",
+              5: "config5: one DDP shard per rank (config-2 program, rank-local frames, own raw-key dictionary), "
+                 "125M records per rank; merged across ranks at N > 1"}[args.config]
         line = {"metric": METRIC, "value": value, "unit": "records/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "u64", "data": "synthetic (counter-based generator, gen/)",
                 "config": {"workload": wl, "config_id": args.config, "records_per_gpu_step": recs,
                            "pc_samples": int(tr.samples.shape[0]) if args.config == 3 else 0,
                            "launch_records": tr.n_records, "nodes": n_nodes, "bins": n_bins,
-                           "l2": "inputs larger than L2 (1.6 GB of samples per step); no flush",
+                           "l2": f"inputs larger than L2 ({step_bytes / 1e9:.2f} GB read per step); no flush",
                            "parallelism": (f"dp{world}: per-rank shard, local CCT + NCCL cross-rank merge "
                                            "(dc_cct_merge_ranks), weak scaling") if world > 1 else "dp1"},
                 "roofline": roof, "stages_ms": stages, "gpu_launches": int(launches),

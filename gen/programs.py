@@ -429,4 +429,6 @@ def config5(shard: int, seed_base: int = 50) -> Program:
 
 
 def program(cfg: int, **kw) -> Program:
+    if cfg == 5:
+        return config5(**({"shard": 0} | kw))
     return {1: config1, 2: config2, 3: config3, 4: config4}[cfg](**kw)

@@ -1,5 +1,3 @@
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_parity.py -x -q --timeout 300 -k "owner or config or f1 or random or generic" > gpurun_out/gpu_tests.log 2>&1; echo "rc=$?" >> gpurun_out/gpu_tests.log
-tail -2 gpurun_out/gpu_tests.log
-timeout 300 python -u tools/own_modes.py 9 0 > gpurun_out/own_modes.log 2>&1
-grep -v "^$" gpurun_out/own_modes.log | tail -6
+timeout 600 python -u bench.py --config 5 --steps 5 --e2e-steps 1 --cpu-launches 20000 > gpurun_out/bench_cfg5.log 2>&1
+tail -c 2500 gpurun_out/bench_cfg5.log
