@@ -15,10 +15,6 @@
 
 namespace dc {
 
-__global__ void k_fill_u64(uint64_t* a, uint64_t n, uint64_t v) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) a[i] = v;
-}
-
 // K > 1 (small trees with many records per node): CTA b updates copy b % K of the columns
 // (strides cs / ms), so K times fewer updates meet on one address; k_attr_fold adds the copies
 // into the node columns. K = 1 updates the node columns directly.
