@@ -127,7 +127,7 @@ __device__ __forceinline__ void pt_hash_chunks(PathWarp& W, const uint32_t* __re
 __global__ void __launch_bounds__(PT_THREADS) k_path_hash(const uint64_t* __restrict__ off, const uint32_t* __restrict__ frames,
                                                           uint64_t R, uint32_t n_frames, uint64_t* __restrict__ hash,
                                                           unsigned int* __restrict__ d_cnt, uint32_t* d_flags,
-                                                          unsigned long long* d_diag, uint64_t hash_mask, int tma_ok) {
+                                                          unsigned long long* d_diag, uint64_t hash_mask, int tma_ok) { DC_PDL_ENTER();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PathSmem& sm = *reinterpret_cast<PathSmem*>(smem_raw);
   const uint32_t tid = threadIdx.x, lane = lane_id(), w = tid >> 5;
@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(PT_THREADS) k_path_hash(const uint64_t* __rest
 __global__ void __launch_bounds__(256) k_path_group(const uint64_t* __restrict__ off, const uint32_t* __restrict__ frames,
                                                     const uint64_t* __restrict__ hash, uint64_t R, PathSlot* __restrict__ tab,
                                                     uint64_t mask, uint32_t* __restrict__ slot_of_rec,
-                                                    uint32_t* __restrict__ extra_rec, unsigned int* __restrict__ d_cnt) {
+                                                    uint32_t* __restrict__ extra_rec, unsigned int* __restrict__ d_cnt) { DC_PDL_ENTER();
   const uint32_t lane = lane_id();
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -366,7 +366,7 @@ __global__ void __launch_bounds__(256) k_path_group(const uint64_t* __restrict__
 
 // representatives in table-slot order: item ids, their record and path length
 __global__ void k_path_compact(const PathSlot* __restrict__ tab, uint64_t cap, uint32_t* __restrict__ pid_of_slot,
-                               uint32_t* __restrict__ item_rec, uint32_t* __restrict__ item_len, unsigned int* d_pos) {
+                               uint32_t* __restrict__ item_rec, uint32_t* __restrict__ item_len, unsigned int* d_pos) { DC_PDL_ENTER();
   for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < cap; s += (uint64_t)gridDim.x * blockDim.x) {
     if (tab[s].key == ~0ull) continue;
     unsigned p = atomicAdd(d_pos, 1u);
@@ -378,7 +378,7 @@ __global__ void k_path_compact(const PathSlot* __restrict__ tab, uint64_t cap, u
 
 __global__ void k_items_finish(uint32_t* __restrict__ item_rec, const uint32_t* __restrict__ extra_rec, uint32_t P0,
                                uint32_t n_extra, const uint64_t* __restrict__ off, uint32_t* __restrict__ item_len,
-                               unsigned long long* d_sumlen, const unsigned int* d_cnt, unsigned long long* d_diag) {
+                               unsigned long long* d_sumlen, const unsigned int* d_cnt, unsigned long long* d_diag) { DC_PDL_ENTER();
   uint32_t P = P0 + n_extra;
   if (blockIdx.x == 0 && threadIdx.x == 0 && d_cnt[4]) atomicAdd(&d_diag[DG_EMPTY], (unsigned long long)d_cnt[4]);
   unsigned long long acc = 0;
@@ -398,13 +398,13 @@ __global__ void k_items_finish(uint32_t* __restrict__ item_rec, const uint32_t* 
 
 // slot -> leaf node (one L2-resident map), then one gather per record, 4 records per thread
 __global__ void k_slot_leaf(const PathSlot* __restrict__ tab, uint64_t cap, const uint32_t* __restrict__ pid_of_slot,
-                            const uint32_t* __restrict__ leaf_of_item, uint32_t* __restrict__ leaf_of_slot) {
+                            const uint32_t* __restrict__ leaf_of_item, uint32_t* __restrict__ leaf_of_slot) { DC_PDL_ENTER();
   for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < cap; s += (uint64_t)gridDim.x * blockDim.x)
     leaf_of_slot[s] = tab[s].key == ~0ull ? 0u : leaf_of_item[pid_of_slot[s]];
 }
 
 __global__ void k_rec_leaf(const uint32_t* __restrict__ slot_of_rec, const uint32_t* __restrict__ leaf_of_slot, uint64_t cap,
-                           uint32_t P0, const uint32_t* __restrict__ leaf_of_item, uint64_t R, uint32_t* __restrict__ leaf) {
+                           uint32_t P0, const uint32_t* __restrict__ leaf_of_item, uint64_t R, uint32_t* __restrict__ leaf) { DC_PDL_ENTER();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < R; r += 4 * stride) {
     uint32_t s[4];
@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(SB_THREADS, 1) k_build_small(const uint64_t* _
                                                                uint32_t P, int fbits, uint32_t* __restrict__ parent,
                                                                uint32_t* __restrict__ frame_out, uint16_t* __restrict__ depth,
                                                                uint32_t* __restrict__ level_off, uint32_t* __restrict__ leaf_of_item,
-                                                               uint32_t* d_N) {
+                                                               uint32_t* d_N) { DC_PDL_ENTER();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SmallSmem& sm = *reinterpret_cast<SmallSmem*>(smem_raw);
   const uint64_t fmask = (1ull << fbits) - 1ull;
@@ -600,7 +600,7 @@ __global__ void __launch_bounds__(SB_THREADS, 1) k_build_small(const uint64_t* _
 __global__ void k_lvl_keys(const uint64_t* __restrict__ off, const uint32_t* __restrict__ frames,
                            const uint32_t* __restrict__ item_rec, const uint32_t* __restrict__ active, uint32_t n_active,
                            const uint32_t* __restrict__ node_of_item, uint32_t lvl_start, uint32_t d, int fbits,
-                           uint64_t* __restrict__ key, uint32_t* __restrict__ val) {
+                           uint64_t* __restrict__ key, uint32_t* __restrict__ val) { DC_PDL_ENTER();
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_active; i += gridDim.x * blockDim.x) {
     uint32_t it = active[i];
     uint32_t f = frames[off[item_rec[it]] + d];
@@ -609,7 +609,7 @@ __global__ void k_lvl_keys(const uint64_t* __restrict__ off, const uint32_t* __r
   }
 }
 
-__global__ void k_lvl_heads(const uint64_t* __restrict__ key, uint32_t n, uint32_t* __restrict__ head) {
+__global__ void k_lvl_heads(const uint64_t* __restrict__ key, uint32_t n, uint32_t* __restrict__ head) { DC_PDL_ENTER();
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     head[i] = (i == 0 || key[i - 1] != key[i]) ? 1u : 0u;
 }
@@ -618,7 +618,7 @@ __global__ void k_lvl_assign(const uint64_t* __restrict__ key, const uint32_t* _
                              const uint32_t* __restrict__ run_excl, uint32_t lvl_start, uint32_t next, uint32_t d, int fbits,
                              const uint32_t* __restrict__ item_len, uint32_t* __restrict__ parent, uint32_t* __restrict__ frame_out,
                              uint16_t* __restrict__ depth, uint32_t* __restrict__ node_of_item, uint32_t* __restrict__ leaf_of_item,
-                             uint32_t* __restrict__ keep) {
+                             uint32_t* __restrict__ keep) { DC_PDL_ENTER();
   const uint64_t fmask = (1ull << fbits) - 1ull;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     uint64_t k = key[i];
@@ -639,13 +639,13 @@ __global__ void k_lvl_assign(const uint64_t* __restrict__ key, const uint32_t* _
 }
 
 __global__ void k_lvl_compact(const uint32_t* __restrict__ val, const uint32_t* __restrict__ keep,
-                              const uint32_t* __restrict__ keep_excl, uint32_t n, uint32_t* __restrict__ active) {
+                              const uint32_t* __restrict__ keep_excl, uint32_t n, uint32_t* __restrict__ active) { DC_PDL_ENTER();
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     if (keep[i]) active[keep_excl[i]] = val[i];
 }
 
 __global__ void k_lvl_init(const uint32_t* __restrict__ item_len, uint32_t P, uint32_t* __restrict__ keep,
-                           uint32_t* __restrict__ node_of_item, uint32_t* __restrict__ leaf_of_item, uint32_t* __restrict__ idx) {
+                           uint32_t* __restrict__ node_of_item, uint32_t* __restrict__ leaf_of_item, uint32_t* __restrict__ idx) { DC_PDL_ENTER();
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += gridDim.x * blockDim.x) {
     keep[i] = item_len[i] > 0;
     node_of_item[i] = 0;
@@ -654,7 +654,7 @@ __global__ void k_lvl_init(const uint32_t* __restrict__ item_len, uint32_t P, ui
   }
 }
 
-__global__ void k_root(uint32_t* parent, uint32_t* frame_out, uint16_t* depth, uint32_t* level_off) {
+__global__ void k_root(uint32_t* parent, uint32_t* frame_out, uint16_t* depth, uint32_t* level_off) { DC_PDL_ENTER();
   parent[0] = DC_NO_NODE;
   frame_out[0] = DC_NO_NODE;
   depth[0] = 0;
@@ -679,12 +679,12 @@ static dc_status build_large(Ctx* c, const dc_paths* p, const uint32_t* item_rec
   DC_TRY(alloc(c, k1, P));
   Buf<uint32_t> tot;
   DC_TRY(alloc(c, tot, 2));
-  k_root<<<1, 1, 0, c->stream>>>(t->parent, t->frame, t->depth, t->level_off);
+  dc_launch(k_root, 1, 1, 0, c->stream, t->parent, t->frame, t->depth, t->level_off);
   DC_LAUNCHED(c);
-  k_lvl_init<<<grid_for(c, P, 256), 256, 0, c->stream>>>(item_len, P, keep.p, node_of_item.p, leaf_of_item, idx.p);
+  dc_launch(k_lvl_init, grid_for(c, P, 256), 256, 0, c->stream, item_len, P, keep.p, node_of_item.p, leaf_of_item, idx.p);
   DC_LAUNCHED(c);
   DC_TRY(excl_scan<uint32_t>(c, keep.p, keep_ex.p, P, tot.p));
-  k_lvl_compact<<<grid_for(c, P, 256), 256, 0, c->stream>>>(idx.p, keep.p, keep_ex.p, P, active.p);
+  dc_launch(k_lvl_compact, grid_for(c, P, 256), 256, 0, c->stream, idx.p, keep.p, keep_ex.p, P, active.p);
   DC_LAUNCHED(c);
   uint32_t hn[2];
   DC_TRY(readback(c, tot.p, 4, hn));
@@ -694,22 +694,22 @@ static dc_status build_large(Ctx* c, const dc_paths* p, const uint32_t* item_rec
   uint32_t d = 0;
   for (; n_active > 0; ++d) {
     int pbits = bits_for(width - 1);
-    k_lvl_keys<<<grid_for(c, n_active, 256), 256, 0, c->stream>>>(p->offsets, p->frames, item_rec, active.p, n_active,
+    dc_launch(k_lvl_keys, grid_for(c, n_active, 256), 256, 0, c->stream, p->offsets, p->frames, item_rec, active.p, n_active,
                                                                   node_of_item.p, lvl_start, d, fbits, k0.p, v0.p);
     DC_LAUNCHED(c);
     bool in1 = false;
     DC_TRY(radix_sort_pairs(c, k0.p, v0.p, k1.p, v1.p, n_active, 0, pbits + fbits, &in1));
     uint64_t* ks = in1 ? k1.p : k0.p;
     uint32_t* vs = in1 ? v1.p : v0.p;
-    k_lvl_heads<<<grid_for(c, n_active, 256), 256, 0, c->stream>>>(ks, n_active, keep.p);
+    dc_launch(k_lvl_heads, grid_for(c, n_active, 256), 256, 0, c->stream, ks, n_active, keep.p);
     DC_LAUNCHED(c);
     DC_TRY(excl_scan<uint32_t>(c, keep.p, runs.p, n_active, tot.p));
-    k_lvl_assign<<<grid_for(c, n_active, 256), 256, 0, c->stream>>>(ks, vs, n_active, runs.p, lvl_start, next, d, fbits,
+    dc_launch(k_lvl_assign, grid_for(c, n_active, 256), 256, 0, c->stream, ks, vs, n_active, runs.p, lvl_start, next, d, fbits,
                                                                     item_len, t->parent, t->frame, t->depth,
                                                                     node_of_item.p, leaf_of_item, keep.p);
     DC_LAUNCHED(c);
     DC_TRY(excl_scan<uint32_t>(c, keep.p, keep_ex.p, n_active, tot.p + 1));
-    k_lvl_compact<<<grid_for(c, n_active, 256), 256, 0, c->stream>>>(vs, keep.p, keep_ex.p, n_active, active.p);
+    dc_launch(k_lvl_compact, grid_for(c, n_active, 256), 256, 0, c->stream, vs, keep.p, keep_ex.p, n_active, active.p);
     DC_LAUNCHED(c);
     DC_TRY(readback(c, tot.p, 8, hn));
     uint32_t n_runs = hn[0];
@@ -750,7 +750,7 @@ __device__ __forceinline__ unsigned long long node_pos(uint32_t j) { return mix6
 __global__ void k_prefix_nodes(const uint64_t* __restrict__ off, const uint32_t* __restrict__ frames,
                                const uint32_t* __restrict__ item_rec, const uint32_t* __restrict__ item_len, uint32_t P,
                                NodeSlot* __restrict__ tab, uint64_t mask, uint16_t* __restrict__ sdepth,
-                               uint32_t* __restrict__ leaf_slot, unsigned int* d_cnt, uint64_t hmask) {
+                               uint32_t* __restrict__ leaf_slot, unsigned int* d_cnt, uint64_t hmask) { DC_PDL_ENTER();
   const uint32_t lane = lane_id();
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -821,7 +821,7 @@ __global__ void k_prefix_nodes(const uint64_t* __restrict__ off, const uint32_t*
 }
 
 __global__ void k_node_compact(const NodeSlot* __restrict__ tab, uint64_t cap, uint32_t* __restrict__ nslot,
-                               uint32_t* __restrict__ nidx, unsigned int* d_pos) {
+                               uint32_t* __restrict__ nidx, unsigned int* d_pos) { DC_PDL_ENTER();
   for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < cap; s += (uint64_t)gridDim.x * blockDim.x) {
     if (tab[s].key == ~0ull) continue;
     const unsigned n = atomicAdd(d_pos, 1u);
@@ -834,7 +834,7 @@ __global__ void k_node_compact(const NodeSlot* __restrict__ tab, uint64_t cap, u
 __global__ void k_node_fields(uint32_t Nn, const uint32_t* __restrict__ nslot, const uint32_t* __restrict__ nidx,
                               const NodeSlot* __restrict__ tab, const uint16_t* __restrict__ sdepth, int fbits,
                               uint32_t* __restrict__ par, uint32_t* __restrict__ frm, uint16_t* __restrict__ dep,
-                              uint64_t* __restrict__ skey, uint32_t* __restrict__ sval) {
+                              uint64_t* __restrict__ skey, uint32_t* __restrict__ sval) { DC_PDL_ENTER();
   for (uint32_t n = blockIdx.x * blockDim.x + threadIdx.x; n < Nn; n += gridDim.x * blockDim.x) {
     const uint32_t s = nslot[n];
     const unsigned long long pay = tab[s].pay;
@@ -849,7 +849,7 @@ __global__ void k_node_fields(uint32_t Nn, const uint32_t* __restrict__ nslot, c
 }
 
 __global__ void k_euler_links(uint32_t Nn, const uint64_t* __restrict__ ks, const uint32_t* __restrict__ vs, int fbits,
-                              uint32_t* __restrict__ first_child, uint32_t* __restrict__ next_sib) {
+                              uint32_t* __restrict__ first_child, uint32_t* __restrict__ next_sib) { DC_PDL_ENTER();
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < Nn; k += gridDim.x * blockDim.x) {
     const uint32_t n = vs[k];
     const uint64_t g = ks[k] >> fbits;
@@ -860,7 +860,7 @@ __global__ void k_euler_links(uint32_t Nn, const uint64_t* __restrict__ ks, cons
 
 // tour elements: down(n) = n, up(n) = Nn + 1 + n (n <= Nn, root = Nn); packed (next << 32 | weight)
 __global__ void k_euler_init(uint32_t Nn, const uint32_t* __restrict__ par, const uint32_t* __restrict__ first_child,
-                             const uint32_t* __restrict__ next_sib, unsigned long long* __restrict__ tour) {
+                             const uint32_t* __restrict__ next_sib, unsigned long long* __restrict__ tour) { DC_PDL_ENTER();
   const uint64_t M = 2ull * (Nn + 1);
   for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < M; x += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t nx, w;
@@ -883,7 +883,7 @@ __global__ void k_euler_init(uint32_t Nn, const uint32_t* __restrict__ par, cons
 }
 
 // one pointer-jumping round: suffix weight sums along the tour
-__global__ void k_wyllie(uint64_t M, const unsigned long long* __restrict__ in, unsigned long long* __restrict__ out) {
+__global__ void k_wyllie(uint64_t M, const unsigned long long* __restrict__ in, unsigned long long* __restrict__ out) { DC_PDL_ENTER();
   for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < M; x += (uint64_t)gridDim.x * blockDim.x) {
     const unsigned long long e = in[x];
     const uint32_t nx = (uint32_t)(e >> 32);
@@ -897,7 +897,7 @@ __global__ void k_wyllie(uint64_t M, const unsigned long long* __restrict__ in, 
 }
 
 __global__ void k_canon_keys(uint32_t Nn, const uint16_t* __restrict__ dep, const unsigned long long* __restrict__ tour,
-                             int pbits, uint64_t* __restrict__ ck, uint32_t* __restrict__ cv) {
+                             int pbits, uint64_t* __restrict__ ck, uint32_t* __restrict__ cv) { DC_PDL_ENTER();
   for (uint32_t n = blockIdx.x * blockDim.x + threadIdx.x; n < Nn; n += gridDim.x * blockDim.x) {
     const uint32_t pre = (Nn + 1) - (uint32_t)tour[n];  // down steps before down(n)
     ck[n] = ((uint64_t)dep[n] << pbits) | pre;
@@ -905,14 +905,14 @@ __global__ void k_canon_keys(uint32_t Nn, const uint16_t* __restrict__ dep, cons
   }
 }
 
-__global__ void k_canon_ids(uint32_t Nn, const uint32_t* __restrict__ cv, uint32_t* __restrict__ canon) {
+__global__ void k_canon_ids(uint32_t Nn, const uint32_t* __restrict__ cv, uint32_t* __restrict__ canon) { DC_PDL_ENTER();
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < Nn; k += gridDim.x * blockDim.x) canon[cv[k]] = k + 1;
 }
 
 __global__ void k_canon_write(uint32_t Nn, const uint64_t* __restrict__ ck, const uint32_t* __restrict__ cv, int pbits,
                               const uint32_t* __restrict__ par, const uint32_t* __restrict__ frm,
                               const uint32_t* __restrict__ canon, uint32_t* __restrict__ parent, uint32_t* __restrict__ frame_out,
-                              uint16_t* __restrict__ depth, uint32_t* __restrict__ level_off, uint32_t Lmax) {
+                              uint16_t* __restrict__ depth, uint32_t* __restrict__ level_off, uint32_t Lmax) { DC_PDL_ENTER();
   const uint64_t gid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (gid == 0) {
     parent[0] = DC_NO_NODE;
@@ -936,7 +936,7 @@ __global__ void k_canon_write(uint32_t Nn, const uint64_t* __restrict__ ck, cons
 }
 
 __global__ void k_item_leaf(uint32_t P, const uint32_t* __restrict__ leaf_slot, const uint32_t* __restrict__ nidx,
-                            const uint32_t* __restrict__ canon, uint32_t* __restrict__ leaf_of_item) {
+                            const uint32_t* __restrict__ canon, uint32_t* __restrict__ leaf_of_item) { DC_PDL_ENTER();
   for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < P; p += gridDim.x * blockDim.x) {
     const uint32_t ls = leaf_slot[p];
     leaf_of_item[p] = ls == PT_NONE ? 0u : canon[nidx[ls]];
@@ -962,7 +962,7 @@ static dc_status build_euler(Ctx* c, const dc_paths* p, const uint32_t* item_rec
     DC_TRY(alloc(c, sdepth, cap));
     DC_CUDA(c, cudaMemsetAsync(tab.p, 0xFF, cap * sizeof(NodeSlot), c->stream));
     DC_TRY(alloc_zero(c, cnt, 4));  // [0] nodes, [1] overflow, [2] collision, [3] compact pos
-    k_prefix_nodes<<<grid_for(c, (uint64_t)P * 32, 256), 256, 0, c->stream>>>(p->offsets, p->frames, item_rec, item_len, P, tab.p,
+    dc_launch(k_prefix_nodes, grid_for(c, (uint64_t)P * 32, 256), 256, 0, c->stream, p->offsets, p->frames, item_rec, item_len, P, tab.p,
                                                                               cap - 1, sdepth.p, leaf_slot.p, cnt.p,
                                                                               c->node_mask);
     DC_LAUNCHED(c);
@@ -997,9 +997,9 @@ static dc_status build_euler(Ctx* c, const dc_paths* p, const uint32_t* item_rec
   const uint64_t M = 2ull * (Nn + 1);
   DC_TRY(alloc(c, tour0, M));
   DC_TRY(alloc(c, tour1, M));
-  k_node_compact<<<grid_for(c, cap, 256), 256, 0, c->stream>>>(tab.p, cap, nslot.p, nidx.p, cnt.p + 3);
+  dc_launch(k_node_compact, grid_for(c, cap, 256), 256, 0, c->stream, tab.p, cap, nslot.p, nidx.p, cnt.p + 3);
   DC_LAUNCHED(c);
-  k_node_fields<<<grid_for(c, Nn, 256), 256, 0, c->stream>>>(Nn, nslot.p, nidx.p, tab.p, sdepth.p, fbits, par.p, frm.p, dep.p,
+  dc_launch(k_node_fields, grid_for(c, Nn, 256), 256, 0, c->stream, Nn, nslot.p, nidx.p, tab.p, sdepth.p, fbits, par.p, frm.p, dep.p,
                                                             sk0.p, sv0.p);
   DC_LAUNCHED(c);
   bool in1 = false;
@@ -1007,28 +1007,28 @@ static dc_status build_euler(Ctx* c, const dc_paths* p, const uint32_t* item_rec
   const uint64_t* ks = in1 ? sk1.p : sk0.p;
   const uint32_t* vs = in1 ? sv1.p : sv0.p;
   DC_CUDA(c, cudaMemsetAsync(first_child.p, 0xFF, ((uint64_t)Nn + 1) * 4, c->stream));
-  k_euler_links<<<grid_for(c, Nn, 256), 256, 0, c->stream>>>(Nn, ks, vs, fbits, first_child.p, next_sib.p);
+  dc_launch(k_euler_links, grid_for(c, Nn, 256), 256, 0, c->stream, Nn, ks, vs, fbits, first_child.p, next_sib.p);
   DC_LAUNCHED(c);
-  k_euler_init<<<grid_for(c, M, 256), 256, 0, c->stream>>>(Nn, par.p, first_child.p, next_sib.p, tour0.p);
+  dc_launch(k_euler_init, grid_for(c, M, 256), 256, 0, c->stream, Nn, par.p, first_child.p, next_sib.p, tour0.p);
   DC_LAUNCHED(c);
   unsigned long long *tin = tour0.p, *tout = tour1.p;
   for (uint64_t span = 1; span < M; span <<= 1) {
-    k_wyllie<<<grid_for(c, M, 256), 256, 0, c->stream>>>(M, tin, tout);
+    dc_launch(k_wyllie, grid_for(c, M, 256), 256, 0, c->stream, M, tin, tout);
     DC_LAUNCHED(c);
     std::swap(tin, tout);
   }
   const int pbits = bits_for((uint64_t)Nn + 1);
-  k_canon_keys<<<grid_for(c, Nn, 256), 256, 0, c->stream>>>(Nn, dep.p, tin, pbits, sk0.p, sv0.p);
+  dc_launch(k_canon_keys, grid_for(c, Nn, 256), 256, 0, c->stream, Nn, dep.p, tin, pbits, sk0.p, sv0.p);
   DC_LAUNCHED(c);
   DC_TRY(radix_sort_pairs(c, sk0.p, sv0.p, sk1.p, sv1.p, Nn, 0, pbits + bits_for(Lmax), &in1));
   const uint64_t* cks = in1 ? sk1.p : sk0.p;
   const uint32_t* cvs = in1 ? sv1.p : sv0.p;
-  k_canon_ids<<<grid_for(c, Nn, 256), 256, 0, c->stream>>>(Nn, cvs, canon.p);
+  dc_launch(k_canon_ids, grid_for(c, Nn, 256), 256, 0, c->stream, Nn, cvs, canon.p);
   DC_LAUNCHED(c);
-  k_canon_write<<<grid_for(c, Nn ? Nn : 1, 256), 256, 0, c->stream>>>(Nn, cks, cvs, pbits, par.p, frm.p, canon.p, t->parent,
+  dc_launch(k_canon_write, grid_for(c, Nn ? Nn : 1, 256), 256, 0, c->stream, Nn, cks, cvs, pbits, par.p, frm.p, canon.p, t->parent,
                                                                     t->frame, t->depth, t->level_off, Lmax);
   DC_LAUNCHED(c);
-  k_item_leaf<<<grid_for(c, P, 256), 256, 0, c->stream>>>(P, leaf_slot.p, nidx.p, canon.p, leaf_of_item);
+  dc_launch(k_item_leaf, grid_for(c, P, 256), 256, 0, c->stream, P, leaf_slot.p, nidx.p, canon.p, leaf_of_item);
   DC_LAUNCHED(c);
   *h_N = (uint64_t)Nn + 1;
   return DC_OK;
@@ -1069,7 +1069,7 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
     DC_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_path_hash, PT_THREADS, sizeof(PathSmem)));
     const uint64_t n_tiles = (R + PT_T - 1) / PT_T;
     const int hgrid = (int)std::min<uint64_t>(n_tiles, (uint64_t)c->num_sms * std::max(per_sm, 1));
-    k_path_hash<<<hgrid, PT_THREADS, sizeof(PathSmem), c->stream>>>(p->offsets, p->frames, R, n_frames, hash.p, cnt.p,
+    dc_launch(k_path_hash, hgrid, PT_THREADS, sizeof(PathSmem), c->stream, p->offsets, p->frames, R, n_frames, hash.p, cnt.p,
                                                                      c->d_flags, (unsigned long long*)c->d_diag,
                                                                      c->hash_mask, tma_ok);
     DC_LAUNCHED(c);
@@ -1083,7 +1083,7 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
     DC_CUDA(c, cudaMemsetAsync(tab.p, 0xFF, cap * sizeof(PathSlot), c->stream));
     DC_CUDA(c, cudaMemsetAsync(cnt.p, 0, 16, c->stream));  // [0..3]; [4] (empty paths) kept
     if (R) {
-      k_path_group<<<grid_for(c, (R + 31) / 32 * 32, 256), 256, 0, c->stream>>>(p->offsets, p->frames, hash.p, R, tab.p,
+      dc_launch(k_path_group, grid_for(c, (R + 31) / 32 * 32, 256), 256, 0, c->stream, p->offsets, p->frames, hash.p, R, tab.p,
                                                                                 cap - 1, slot_of_rec.p, extra_rec.p, cnt.p);
       DC_LAUNCHED(c);
     }
@@ -1099,9 +1099,9 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
   DC_TRY(alloc(c, item_len, P));
   DC_TRY(alloc(c, leaf_of_item, P));
   DC_TRY(alloc_zero(c, sumlen, 1));
-  k_path_compact<<<grid_for(c, cap, 256), 256, 0, c->stream>>>(tab.p, cap, pid_of_slot.p, item_rec.p, item_len.p, cnt.p + 2);
+  dc_launch(k_path_compact, grid_for(c, cap, 256), 256, 0, c->stream, tab.p, cap, pid_of_slot.p, item_rec.p, item_len.p, cnt.p + 2);
   DC_LAUNCHED(c);
-  k_items_finish<<<grid_for(c, P, 256), 256, 0, c->stream>>>(item_rec.p, extra_rec.p, P0, n_extra, p->offsets, item_len.p,
+  dc_launch(k_items_finish, grid_for(c, P, 256), 256, 0, c->stream, item_rec.p, extra_rec.p, P0, n_extra, p->offsets, item_len.p,
                                                              sumlen.p, cnt.p, (unsigned long long*)c->d_diag);
   DC_LAUNCHED(c);
   uint64_t hsum = 0, hmaxd = 0, F = 0;
@@ -1124,7 +1124,7 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
     DC_TRY(alloc(c, dN, 2));
     size_t smem = sizeof(SmallSmem);
     DC_CUDA(c, cudaFuncSetAttribute(k_build_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_build_small<<<1, SB_THREADS, smem, c->stream>>>(p->offsets, p->frames, item_rec.p, item_len.p, P, fbits, t->parent,
+    dc_launch(k_build_small, 1, SB_THREADS, smem, c->stream, p->offsets, p->frames, item_rec.p, item_len.p, P, fbits, t->parent,
                                                       t->frame, t->depth, t->level_off, leaf_of_item.p, dN.p);
     DC_LAUNCHED(c);
     uint32_t hN[2] = {0, 0};
@@ -1150,9 +1150,9 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
   {
     Buf<uint32_t> leaf_of_slot;
     DC_TRY(alloc(c, leaf_of_slot, cap));
-    k_slot_leaf<<<grid_for(c, cap, 256), 256, 0, c->stream>>>(tab.p, cap, pid_of_slot.p, leaf_of_item.p, leaf_of_slot.p);
+    dc_launch(k_slot_leaf, grid_for(c, cap, 256), 256, 0, c->stream, tab.p, cap, pid_of_slot.p, leaf_of_item.p, leaf_of_slot.p);
     DC_LAUNCHED(c);
-    k_rec_leaf<<<grid_for(c, (R + 3) / 4, 256), 256, 0, c->stream>>>(slot_of_rec.p, leaf_of_slot.p, cap, P0, leaf_of_item.p, R,
+    dc_launch(k_rec_leaf, grid_for(c, (R + 3) / 4, 256), 256, 0, c->stream, slot_of_rec.p, leaf_of_slot.p, cap, P0, leaf_of_item.p, R,
                                                                      leaf);
     DC_LAUNCHED(c);
   }

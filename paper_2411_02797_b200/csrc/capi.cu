@@ -9,6 +9,14 @@
 #include "prim.cuh"
 
 namespace dc {
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("DC_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
 dc_status intern_frames(Ctx* c, const dc_frame_key* keys, uint64_t n, uint32_t* out_ids, dc_dict** out);
 dc_status dict_from_sorted(Ctx* c, const dc_frame_key* keys, uint64_t D, dc_dict** out);
 dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_frames, uint32_t* out_leaf, dc_cct** out);
@@ -131,12 +139,12 @@ dc_status check_flags(Ctx* c) {
   return DC_OK;
 }
 
-__global__ void k_add_diag(unsigned long long* dst, const unsigned long long* src) {
+__global__ void k_add_diag(unsigned long long* dst, const unsigned long long* src) { DC_PDL_ENTER();
   if (threadIdx.x < DG_N) dst[threadIdx.x] += src[threadIdx.x];
 }
 
 dc_status add_diag(Ctx* c, const unsigned long long* src_dev) {
-  k_add_diag<<<1, 32, 0, c->stream>>>((unsigned long long*)c->d_diag, src_dev);
+  dc_launch(k_add_diag, 1, 32, 0, c->stream, (unsigned long long*)c->d_diag, src_dev);
   DC_LAUNCHED(c);
   return DC_OK;
 }

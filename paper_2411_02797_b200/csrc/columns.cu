@@ -20,7 +20,7 @@ namespace dc {
 // into the node columns. K = 1 updates the node columns directly.
 __global__ void k_attribute(const uint32_t* __restrict__ leaf, uint64_t R, const uint64_t* __restrict__ X, uint32_t M,
                             uint64_t ld, uint64_t N, unsigned long long* __restrict__ xcnt0, unsigned long long* __restrict__ mcols0,
-                            uint32_t* d_flags, uint32_t K, uint64_t cs, uint64_t ms) {
+                            uint32_t* d_flags, uint32_t K, uint64_t cs, uint64_t ms) { DC_PDL_ENTER();
   unsigned long long* xcnt = xcnt0 + (uint64_t)(blockIdx.x % K) * cs;
   unsigned long long* mcols = mcols0 + (uint64_t)(blockIdx.x % K) * ms;
   for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < R; r += (uint64_t)gridDim.x * blockDim.x) {
@@ -44,7 +44,7 @@ __global__ void k_attribute(const uint32_t* __restrict__ leaf, uint64_t R, const
 }
 
 // the K copies: count, then per metric (sum, min, sq_lo, sq_hi); min starts at UINT64_MAX
-__global__ void k_attr_init_copies(uint64_t* __restrict__ cnt, uint64_t* __restrict__ cols, uint32_t K, uint32_t M, uint64_t N) {
+__global__ void k_attr_init_copies(uint64_t* __restrict__ cnt, uint64_t* __restrict__ cols, uint32_t K, uint32_t M, uint64_t N) { DC_PDL_ENTER();
   const uint64_t MN = (uint64_t)M * N, tot_c = (uint64_t)K * N, tot_m = (uint64_t)K * 4 * MN;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < tot_c + tot_m; i += (uint64_t)gridDim.x * blockDim.x) {
     if (i < tot_c) {
@@ -57,7 +57,7 @@ __global__ void k_attr_init_copies(uint64_t* __restrict__ cnt, uint64_t* __restr
 }
 // node columns += the K copies (exact: u64 count / sum, min, 128-bit sum of squares)
 __global__ void k_attr_fold(const uint64_t* __restrict__ cnt, const uint64_t* __restrict__ cols, uint32_t K, uint32_t M, uint64_t N,
-                            uint64_t* __restrict__ xcnt, uint64_t* __restrict__ mcols) {
+                            uint64_t* __restrict__ xcnt, uint64_t* __restrict__ mcols) { DC_PDL_ENTER();
   const uint64_t MN = (uint64_t)M * N;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < N * (1 + M); i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t g = i / N, n = i - g * N;
@@ -90,7 +90,7 @@ __global__ void k_attr_fold(const uint64_t* __restrict__ cnt, const uint64_t* __
 }
 
 // all metric columns in one pass: min columns start at UINT64_MAX (reading R11), the rest at 0
-__global__ void k_init_cols(uint64_t* __restrict__ mcols, uint32_t M, uint64_t N) {
+__global__ void k_init_cols(uint64_t* __restrict__ mcols, uint32_t M, uint64_t N) { DC_PDL_ENTER();
   const uint64_t total = 8ull * M * N;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t which = i / ((uint64_t)M * N);
@@ -107,7 +107,7 @@ dc_status ensure_metric_cols(Ctx* c, dc_cct* t, uint32_t M) {
   const uint64_t N = t->N;
   DC_TRY(palloc(c, t->mcols, (uint64_t)8 * M * N));
   if (M) {
-    k_init_cols<<<grid_for(c, 8ull * M * N, 256), 256, 0, c->stream>>>(t->mcols, M, N);
+    dc_launch(k_init_cols, grid_for(c, 8ull * M * N, 256), 256, 0, c->stream, t->mcols, M, N);
     DC_LAUNCHED(c);
   }
   return DC_OK;
@@ -120,19 +120,19 @@ dc_status attribute_metrics(Ctx* c, dc_cct* t, const uint32_t* leaf, uint64_t R,
   // copies of the columns (a few MB at most) and fold the copies afterwards
   const uint32_t K = (N <= (1u << 16) && R >= 64 * N && !getenv("DC_TEST_ATTR_DIRECT")) ? 16u : 1u;
   if (R && K == 1) {
-    k_attribute<<<grid_for(c, R, 256), 256, 0, c->stream>>>(leaf, R, X, M, ld, N, (unsigned long long*)t->xcnt,
+    dc_launch(k_attribute, grid_for(c, R, 256), 256, 0, c->stream, leaf, R, X, M, ld, N, (unsigned long long*)t->xcnt,
                                                             (unsigned long long*)t->mcols, c->d_flags, 1, 0, 0);
     DC_LAUNCHED(c);
   } else if (R) {
     Buf<uint64_t> ccnt, ccols;
     DC_TRY(alloc(c, ccnt, (uint64_t)K * N));
     DC_TRY(alloc(c, ccols, (uint64_t)K * 4 * M * N + 1));
-    k_attr_init_copies<<<grid_for(c, (uint64_t)K * N * (1 + 4 * M), 256), 256, 0, c->stream>>>(ccnt.p, ccols.p, K, M, N);
+    dc_launch(k_attr_init_copies, grid_for(c, (uint64_t)K * N * (1 + 4 * M), 256), 256, 0, c->stream, ccnt.p, ccols.p, K, M, N);
     DC_LAUNCHED(c);
-    k_attribute<<<grid_for(c, R, 256), 256, 0, c->stream>>>(leaf, R, X, M, ld, N, (unsigned long long*)ccnt.p,
+    dc_launch(k_attribute, grid_for(c, R, 256), 256, 0, c->stream, leaf, R, X, M, ld, N, (unsigned long long*)ccnt.p,
                                                             (unsigned long long*)ccols.p, c->d_flags, K, N, 4ull * M * N);
     DC_LAUNCHED(c);
-    k_attr_fold<<<grid_for(c, N * (1 + M), 256), 256, 0, c->stream>>>(ccnt.p, ccols.p, K, M, N, t->xcnt, t->mcols);
+    dc_launch(k_attr_fold, grid_for(c, N * (1 + M), 256), 256, 0, c->stream, ccnt.p, ccols.p, K, M, N, t->xcnt, t->mcols);
     DC_LAUNCHED(c);
   }
   t->state = 1;
@@ -146,7 +146,7 @@ __global__ void k_push(const uint32_t* __restrict__ parent, uint64_t N, uint32_t
                        const uint64_t* __restrict__ xcnt, unsigned long long* __restrict__ icnt,
                        unsigned long long* __restrict__ mcols, const uint64_t* __restrict__ xsamples,
                        unsigned long long* __restrict__ isamples, const uint64_t* __restrict__ xstall,
-                       unsigned long long* __restrict__ istall) {
+                       unsigned long long* __restrict__ istall) { DC_PDL_ENTER();
   const uint64_t total = (N - 1) * (uint64_t)G;
   for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t n = 1 + t / G;
@@ -249,7 +249,7 @@ __device__ __forceinline__ void warp_sum_u128(uint64_t& lo, uint64_t& hi) {
   }
 }
 
-__global__ void __launch_bounds__(256) k_rollup_levels(RollArgs a) {
+__global__ void __launch_bounds__(256) k_rollup_levels(RollArgs a) { DC_PDL_ENTER();
   const uint64_t N = a.N;
   const uint32_t M = a.M, lane = lane_id();
   const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
@@ -327,7 +327,7 @@ dc_status rollup(Ctx* c, dc_cct* t) {
     DC_CUDA(c, cudaLaunchCooperativeKernel((void*)k_rollup_levels, grid, 256, args, 0, s));
     DC_LAUNCHED(c);
   } else if (N > 1) {
-    k_push<<<grid_for(c, (N - 1) * G, 256, 16), 256, 0, s>>>(t->parent, N, M, S, G, t->xcnt, (unsigned long long*)t->icnt,
+    dc_launch(k_push, grid_for(c, (N - 1) * G, 256, 16), 256, 0, s, t->parent, N, M, S, G, t->xcnt, (unsigned long long*)t->icnt,
                                                              (unsigned long long*)t->mcols, t->xsamples,
                                                              (unsigned long long*)t->isamples, t->xstall,
                                                              (unsigned long long*)t->istall);
@@ -359,7 +359,7 @@ __device__ double u192_to_double_rn(uint64_t w2, uint64_t w1, uint64_t w0) {
 }
 
 __global__ void k_derived(const uint64_t* __restrict__ cnt, const uint64_t* __restrict__ sum, const uint64_t* __restrict__ sq_lo,
-                          const uint64_t* __restrict__ sq_hi, uint64_t N, double* __restrict__ mean, double* __restrict__ stdv) {
+                          const uint64_t* __restrict__ sq_hi, uint64_t N, double* __restrict__ mean, double* __restrict__ stdv) { DC_PDL_ENTER();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < N; i += (uint64_t)gridDim.x * blockDim.x) {
     uint64_t n = cnt[i];
     if (!n) {
@@ -393,7 +393,7 @@ dc_status derived(Ctx* c, const dc_cct* t, uint32_t metric, int incl, double* me
   if (metric >= t->M) return fail(c, DC_ERR_ARG, "metric %u >= M = %u", metric, t->M);
   if (incl && t->state != 2) return fail(c, DC_ERR_STATE, "inclusive derived values need dc_cct_rollup first");
   const uint64_t* cnt = incl ? t->icnt : t->xcnt;
-  k_derived<<<grid_for(c, t->N, 256), 256, 0, c->stream>>>(cnt, t->col(incl ? C_ISUM : C_XSUM, metric),
+  dc_launch(k_derived, grid_for(c, t->N, 256), 256, 0, c->stream, cnt, t->col(incl ? C_ISUM : C_XSUM, metric),
                                                            t->col(incl ? C_ISQLO : C_XSQLO, metric),
                                                            t->col(incl ? C_ISQHI : C_XSQHI, metric), t->N, mean, stdv);
   DC_LAUNCHED(c);

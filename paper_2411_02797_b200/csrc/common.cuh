@@ -6,6 +6,7 @@
 #include <chrono>
 #include <initializer_list>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/dc.h"
@@ -170,6 +171,36 @@ dc_status fail(Ctx* c, dc_status s, const char* fmt, ...);
     cudaError_t _e = cudaGetLastError();                                                              \
     if (_e != cudaSuccess) return ::dc::cuda_fail((ctx), _e, "kernel launch at " __FILE__ ":" DC_STR(__LINE__)); \
   } while (0)
+
+// Programmatic dependent launch. Every kernel of the library starts with DC_PDL_ENTER():
+// griddepcontrol.wait blocks until the preceding grid on the stream has completed and its
+// memory is visible (so the stream-order semantics are unchanged), then launch_dependents lets
+// the NEXT grid's CTAs be scheduled while this one runs — they park at their own wait. This
+// hides the launch latency of the ~45 short kernels of one step. When the
+// previous stream operation is not a kernel (memset, memcpy, event) the attribute has no effect.
+#define DC_PDL_ENTER()                                 \
+  do {                                                 \
+    asm volatile("griddepcontrol.wait;" ::: "memory"); \
+    asm volatile("griddepcontrol.launch_dependents;"); \
+  } while (0)
+
+bool pdl_enabled();  // env DC_NO_PDL=1 launches without the attribute (A/B measurement)
+
+template <typename... KArgs, typename... Args>
+inline void dc_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  // errors surface through cudaGetLastError in DC_LAUNCHED
+  (void)cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // stream-ordered device allocation (memory pool); RAII buffer
 template <class T>

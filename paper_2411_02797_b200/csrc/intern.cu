@@ -27,7 +27,7 @@ constexpr uint32_t IC_EMPTY = 0xFFFFFFFFu, IC_BUSY = 0xFFFFFFFEu;
 __global__ void __launch_bounds__(256) k_intern_insert(const dc_frame_key* __restrict__ keys, uint64_t n, ulonglong2* table,
                                                        uint64_t mask, uint32_t* __restrict__ out_slot,
                                                        unsigned long long* d_count, uint32_t* d_overflow, uint32_t* d_flags,
-                                                       unsigned long long* d_max) {
+                                                       unsigned long long* d_max) { DC_PDL_ENTER();
   __shared__ unsigned long long c_lo[IC_SLOTS], c_hi[IC_SLOTS];
   __shared__ uint32_t c_slot[IC_SLOTS];
   for (int i = threadIdx.x; i < IC_SLOTS; i += blockDim.x) c_slot[i] = IC_EMPTY;
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(256) k_intern_insert(const dc_frame_key* __res
 }
 
 __global__ void k_intern_compact(const ulonglong2* __restrict__ table, uint64_t cap, uint64_t* __restrict__ addr_key,
-                                 uint64_t* __restrict__ ks_key, uint32_t* __restrict__ slot_of, unsigned int* d_pos) {
+                                 uint64_t* __restrict__ ks_key, uint32_t* __restrict__ slot_of, unsigned int* d_pos) { DC_PDL_ENTER();
   for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < cap; s += (uint64_t)gridDim.x * blockDim.x) {
     ulonglong2 cur = table[s];
     if ((uint32_t)cur.x == 0xFFFFFFFFu) continue;
@@ -126,7 +126,7 @@ __global__ void k_intern_compact(const ulonglong2* __restrict__ table, uint64_t 
 }
 
 __global__ void k_gather_u64(const uint64_t* __restrict__ src, const uint32_t* __restrict__ idx, uint64_t* __restrict__ dst,
-                             uint64_t n) {
+                             uint64_t n) { DC_PDL_ENTER();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
     dst[i] = src[idx[i]];
 }
@@ -134,7 +134,7 @@ __global__ void k_gather_u64(const uint64_t* __restrict__ src, const uint32_t* _
 // rank r -> dictionary key; slot -> rank
 __global__ void k_intern_rank(const uint32_t* __restrict__ order, const uint32_t* __restrict__ slot_of,
                               const ulonglong2* __restrict__ table, uint32_t* __restrict__ rank_of_slot,
-                              dc_frame_key* __restrict__ dict, uint8_t* __restrict__ kinds, uint64_t D) {
+                              dc_frame_key* __restrict__ dict, uint8_t* __restrict__ kinds, uint64_t D) { DC_PDL_ENTER();
   for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < D; r += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t s = slot_of[order[r]];
     rank_of_slot[s] = (uint32_t)r;
@@ -148,17 +148,17 @@ __global__ void k_intern_rank(const uint32_t* __restrict__ order, const uint32_t
   }
 }
 
-__global__ void k_intern_remap(uint32_t* ids, uint64_t n, const uint32_t* __restrict__ rank_of_slot) {
+__global__ void k_intern_remap(uint32_t* ids, uint64_t n, const uint32_t* __restrict__ rank_of_slot) { DC_PDL_ENTER();
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x)
     ids[j] = rank_of_slot[ids[j]];
 }
 
-__global__ void k_iota(uint32_t* a, uint64_t n) {
+__global__ void k_iota(uint32_t* a, uint64_t n) { DC_PDL_ENTER();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
     a[i] = (uint32_t)i;
 }
 
-__global__ void k_kinds_of(const dc_frame_key* __restrict__ dict, uint8_t* kinds, uint64_t D) {
+__global__ void k_kinds_of(const dc_frame_key* __restrict__ dict, uint8_t* kinds, uint64_t D) { DC_PDL_ENTER();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < D; i += (uint64_t)gridDim.x * blockDim.x)
     kinds[i] = (uint8_t)(dict[i].kind < 255 ? dict[i].kind : 255);
 }
@@ -198,7 +198,7 @@ dc_status intern_frames(Ctx* c, const dc_frame_key* keys, uint64_t n, uint32_t* 
     DC_TRY(alloc_zero(c, cnt, 1));
     DC_TRY(alloc_zero(c, ovf, 1));
     DC_TRY(alloc_zero(c, mx, 2));
-    k_intern_insert<<<grid_for(c, (n + 3) / 4, 256), 256, 0, c->stream>>>(keys, n, table.p, cap - 1, out_ids, cnt.p, ovf.p,
+    dc_launch(k_intern_insert, grid_for(c, (n + 3) / 4, 256), 256, 0, c->stream, keys, n, table.p, cap - 1, out_ids, cnt.p, ovf.p,
                                                                  c->d_flags, mx.p);
     DC_LAUNCHED(c);
     uint64_t h[2] = {0, 0};
@@ -225,26 +225,26 @@ dc_status intern_frames(Ctx* c, const dc_frame_key* keys, uint64_t n, uint32_t* 
   DC_TRY(alloc(c, ord1, D));
   DC_TRY(alloc(c, rank_of_slot, cap));
   DC_TRY(alloc_zero(c, pos, 1));
-  k_intern_compact<<<grid_for(c, cap, 256), 256, 0, c->stream>>>(table.p, cap, ka.p, kb.p, slot_of.p, pos.p);
+  dc_launch(k_intern_compact, grid_for(c, cap, 256), 256, 0, c->stream, table.p, cap, ka.p, kb.p, slot_of.p, pos.p);
   DC_LAUNCHED(c);
-  k_iota<<<grid_for(c, D, 256), 256, 0, c->stream>>>(ord0.p, D);
+  dc_launch(k_iota, grid_for(c, D, 256), 256, 0, c->stream, ord0.p, D);
   DC_LAUNCHED(c);
   // LSD: by addr, then (stable) by kind<<32|str  ==> lexicographic (kind, str_id, addr)
   bool in1 = false;
   DC_TRY(radix_sort_pairs(c, ka.p, ord0.p, ka2.p, ord1.p, D, 0, bits_for(mxh[0]), &in1));
   uint32_t* ord = in1 ? ord1.p : ord0.p;
   uint32_t* ord_alt = in1 ? ord0.p : ord1.p;
-  k_gather_u64<<<grid_for(c, D, 256), 256, 0, c->stream>>>(kb.p, ord, ka.p, D);  // ka <- kb[ord]
+  dc_launch(k_gather_u64, grid_for(c, D, 256), 256, 0, c->stream, kb.p, ord, ka.p, D);  // ka <- kb[ord]
   DC_LAUNCHED(c);
   bool in1b = false;
   DC_TRY(radix_sort_pairs(c, ka.p, ord, ka2.p, ord_alt, D, 0, bits_for(mxh[1]), &in1b));
   uint32_t* final_ord = in1b ? ord_alt : ord;
   DC_TRY(palloc(c, d->keys, D));
   DC_TRY(palloc(c, d->kinds, D));
-  k_intern_rank<<<grid_for(c, D, 256), 256, 0, c->stream>>>(final_ord, slot_of.p, table.p, rank_of_slot.p, d->keys,
+  dc_launch(k_intern_rank, grid_for(c, D, 256), 256, 0, c->stream, final_ord, slot_of.p, table.p, rank_of_slot.p, d->keys,
                                                             d->kinds, D);
   DC_LAUNCHED(c);
-  k_intern_remap<<<grid_for(c, n, 256), 256, 0, c->stream>>>(out_ids, n, rank_of_slot.p);
+  dc_launch(k_intern_remap, grid_for(c, n, 256), 256, 0, c->stream, out_ids, n, rank_of_slot.p);
   DC_LAUNCHED(c);
   c->bytes_host += 20 * n + 16 * D;
   *out = d;
@@ -260,7 +260,7 @@ dc_status dict_from_sorted(Ctx* c, const dc_frame_key* keys, uint64_t D, dc_dict
   DC_TRY(palloc(c, d->kinds, D));
   if (D) {
     DC_CUDA(c, cudaMemcpyAsync(d->keys, keys, D * sizeof(dc_frame_key), cudaMemcpyDeviceToDevice, c->stream));
-    k_kinds_of<<<grid_for(c, D, 256), 256, 0, c->stream>>>(d->keys, d->kinds, D);
+    dc_launch(k_kinds_of, grid_for(c, D, 256), 256, 0, c->stream, d->keys, d->kinds, D);
     DC_LAUNCHED(c);
   }
   *out = d;

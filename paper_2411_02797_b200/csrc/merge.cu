@@ -50,14 +50,14 @@ __device__ __forceinline__ void mix128(uint64_t& lo, uint64_t& hi, uint32_t f) {
 }
 constexpr uint64_t H0_LO = 0x6A09E667F3BCC908ull, H0_HI = 0xBB67AE8584CAA73Bull;
 
-__global__ void k_hash_root(uint64_t* h) {
+__global__ void k_hash_root(uint64_t* h) { DC_PDL_ENTER();
   h[0] = H0_LO;
   h[1] = H0_HI;
 }
 // nodes [a, b): h[2n..2n+1] from the parent's
 __global__ void k_hash_level(const uint32_t* __restrict__ parent, const uint32_t* __restrict__ frame,
                              const uint32_t* __restrict__ l2g, uint32_t a, uint32_t b, uint64_t* __restrict__ h,
-                             uint64_t mask) {
+                             uint64_t mask) { DC_PDL_ENTER();
   for (uint32_t n = a + blockIdx.x * blockDim.x + threadIdx.x; n < b; n += gridDim.x * blockDim.x) {
     uint32_t p = parent[n];
     uint64_t lo = h[2ull * p], hi = h[2ull * p + 1];
@@ -71,7 +71,7 @@ __global__ void k_hash_level(const uint32_t* __restrict__ parent, const uint32_t
 
 __device__ __forceinline__ uint32_t owner_of(uint64_t hi, uint32_t P) { return (uint32_t)__umul64hi(hi, (uint64_t)P); }
 
-__global__ void k_part_count(const uint64_t* __restrict__ h, uint64_t N, uint32_t P, unsigned long long* cnt) {
+__global__ void k_part_count(const uint64_t* __restrict__ h, uint64_t N, uint32_t P, unsigned long long* cnt) { DC_PDL_ENTER();
   for (uint64_t n = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; n < N; n += (uint64_t)gridDim.x * blockDim.x)
     atomicAdd(cnt + owner_of(h[2 * n + 1], P), 1ull);
 }
@@ -81,7 +81,7 @@ __global__ void k_part_nodes(const uint64_t* __restrict__ h, const uint32_t* __r
                              const uint16_t* __restrict__ depth, const uint32_t* __restrict__ l2g, const uint64_t* __restrict__ xcnt,
                              const uint64_t* __restrict__ icnt, const uint64_t* __restrict__ mcols, const uint64_t* __restrict__ xs,
                              const uint64_t* __restrict__ is, const uint64_t* __restrict__ xst, const uint64_t* __restrict__ ist,
-                             uint64_t N, RecFmt f, uint32_t P, unsigned long long* cursor, uint64_t* __restrict__ out) {
+                             uint64_t N, RecFmt f, uint32_t P, unsigned long long* cursor, uint64_t* __restrict__ out) { DC_PDL_ENTER();
   for (uint64_t n = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; n < N; n += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t o = owner_of(h[2 * n + 1], P);
     const unsigned long long slot = atomicAdd(cursor + o, 1ull);
@@ -117,7 +117,7 @@ __device__ __forceinline__ uint32_t bin_owner(uint64_t hlo, uint64_t hi, uint32_
 __global__ void k_part_bins(const uint64_t* __restrict__ h, const uint32_t* __restrict__ bin_pcnode, const uint16_t* __restrict__ bin_stall,
                             const uint64_t* __restrict__ bin_count, const uint32_t* __restrict__ pc_ctx,
                             const uint32_t* __restrict__ pc_off, uint64_t N, uint64_t nb, uint32_t P, int count_only,
-                            unsigned long long* cnt_or_cursor, uint64_t* __restrict__ out) {
+                            unsigned long long* cnt_or_cursor, uint64_t* __restrict__ out) { DC_PDL_ENTER();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nb; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t pn = bin_pcnode[i] - (uint32_t)N;
     const uint32_t ctx = pc_ctx[pn], pc = pc_off[pn];
@@ -135,7 +135,7 @@ __global__ void k_part_bins(const uint64_t* __restrict__ h, const uint32_t* __re
 
 // ---------------------------------------------------------------- reduce received records
 __global__ void k_rec_key(const uint64_t* __restrict__ rec, uint32_t W, uint64_t n, int word, const uint32_t* __restrict__ order,
-                          uint64_t* __restrict__ key, uint32_t* __restrict__ val) {
+                          uint64_t* __restrict__ key, uint32_t* __restrict__ val) { DC_PDL_ENTER();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t src = order ? order[i] : (uint32_t)i;
     key[i] = rec[(uint64_t)src * W + word];
@@ -151,13 +151,13 @@ static dc_status sort_recs128(Ctx* c, const uint64_t* rec, uint32_t W, uint64_t 
   DC_TRY(alloc(c, k1, n));
   DC_TRY(alloc(c, v0, n));
   DC_TRY(alloc(c, v1, n));
-  k_rec_key<<<grid_for(c, n, 256), 256, 0, c->stream>>>(rec, W, n, wlo, nullptr, k0.p, v0.p);
+  dc_launch(k_rec_key, grid_for(c, n, 256), 256, 0, c->stream, rec, W, n, wlo, nullptr, k0.p, v0.p);
   DC_LAUNCHED(c);
   bool in1 = false;
   DC_TRY(radix_sort_pairs(c, k0.p, v0.p, k1.p, v1.p, n, 0, 64, &in1));
   uint32_t* ord = in1 ? v1.p : v0.p;
   // second key in the current order
-  k_rec_key<<<grid_for(c, n, 256), 256, 0, c->stream>>>(rec, W, n, whi, ord, in1 ? k0.p : k1.p, in1 ? v0.p : v1.p);
+  dc_launch(k_rec_key, grid_for(c, n, 256), 256, 0, c->stream, rec, W, n, whi, ord, in1 ? k0.p : k1.p, in1 ? v0.p : v1.p);
   DC_LAUNCHED(c);
   // the gather above wrote (key_hi, idx) into the "other" buffers; sort them stably
   uint64_t* ka = in1 ? k0.p : k1.p;
@@ -172,7 +172,7 @@ static dc_status sort_recs128(Ctx* c, const uint64_t* rec, uint32_t W, uint64_t 
 }
 
 __global__ void k_run_heads(const uint64_t* __restrict__ rec, uint32_t W, const uint32_t* __restrict__ order, uint64_t n, int w0,
-                            int w1, uint32_t* __restrict__ head) {
+                            int w1, uint32_t* __restrict__ head) { DC_PDL_ENTER();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     bool hd = i == 0;
     if (!hd) {
@@ -187,7 +187,7 @@ __global__ void k_run_heads(const uint64_t* __restrict__ rec, uint32_t W, const 
 // combine a run of node records (run heads only): sums, mins; verify parent hash, frame, depth
 __global__ void k_combine_nodes(const uint64_t* __restrict__ rec, const uint32_t* __restrict__ order, const uint32_t* __restrict__ head,
                                 const uint32_t* __restrict__ run_ix, uint64_t n, RecFmt f, uint64_t* __restrict__ out,
-                                uint32_t* d_collision) {
+                                uint32_t* d_collision) { DC_PDL_ENTER();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     if (!head[i]) continue;
     uint64_t* o = out + (uint64_t)run_ix[i] * f.W;
@@ -219,7 +219,7 @@ __global__ void k_combine_nodes(const uint64_t* __restrict__ rec, const uint32_t
 }
 
 __global__ void k_combine_bins(const uint64_t* __restrict__ rec, const uint32_t* __restrict__ order, const uint32_t* __restrict__ head,
-                               const uint32_t* __restrict__ run_ix, uint64_t n, uint64_t* __restrict__ out) {
+                               const uint32_t* __restrict__ run_ix, uint64_t n, uint64_t* __restrict__ out) { DC_PDL_ENTER();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     if (!head[i]) continue;
     uint64_t* o = out + (uint64_t)run_ix[i] * BIN_W;
@@ -248,20 +248,20 @@ static dc_status reduce_records(Ctx* c, const uint64_t* rec, uint64_t n, uint32_
   DC_TRY(alloc(c, head, n));
   DC_TRY(alloc(c, run, n));
   DC_TRY(alloc(c, tot, 1));
-  k_run_heads<<<grid_for(c, n, 256), 256, 0, c->stream>>>(rec, W, order.p, n, 0, 1, head.p);
+  dc_launch(k_run_heads, grid_for(c, n, 256), 256, 0, c->stream, rec, W, order.p, n, 0, 1, head.p);
   DC_LAUNCHED(c);
   DC_TRY(excl_scan<uint32_t>(c, head.p, run.p, n, tot.p));
   uint32_t hn = 0;
   DC_TRY(readback(c, tot.p, 4, &hn));
   DC_TRY(alloc(c, out, (uint64_t)hn * W));
-  k_combine_nodes<<<grid_for(c, n, 256), 256, 0, c->stream>>>(rec, order.p, head.p, run.p, n, f, out.p, d_collision);
+  dc_launch(k_combine_nodes, grid_for(c, n, 256), 256, 0, c->stream, rec, order.p, head.p, run.p, n, f, out.p, d_collision);
   DC_LAUNCHED(c);
   *n_out = hn;
   return DC_OK;
 }
 
 __global__ void k_gather_recs(const uint64_t* __restrict__ rec, uint32_t W, const uint32_t* __restrict__ order, uint64_t n,
-                              uint64_t* __restrict__ out) {
+                              uint64_t* __restrict__ out) { DC_PDL_ENTER();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n * W; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t r = i / W, w = i % W;
     out[i] = rec[(uint64_t)order[r] * W + w];
@@ -288,7 +288,7 @@ static dc_status reduce_bins(Ctx* c, const uint64_t* rec, uint64_t n, Buf<uint64
     uint32_t* vin = in1 ? v1.p : v0.p;
     uint64_t* kout = in1 ? k0.p : k1.p;
     uint32_t* vout = in1 ? v0.p : v1.p;
-    k_rec_key<<<grid_for(c, n, 256), 256, 0, c->stream>>>(rec, BIN_W, n, word, ord, kin, vin);
+    dc_launch(k_rec_key, grid_for(c, n, 256), 256, 0, c->stream, rec, BIN_W, n, word, ord, kin, vin);
     DC_LAUNCHED(c);
     bool r1 = false;
     DC_TRY(radix_sort_pairs(c, kin, vin, kout, vout, n, 0, 64, &r1));
@@ -298,13 +298,13 @@ static dc_status reduce_bins(Ctx* c, const uint64_t* rec, uint64_t n, Buf<uint64
   DC_TRY(alloc(c, head, n));
   DC_TRY(alloc(c, run, n));
   DC_TRY(alloc(c, tot, 1));
-  k_run_heads<<<grid_for(c, n, 256), 256, 0, c->stream>>>(rec, BIN_W, ord, n, 0, 2, head.p);
+  dc_launch(k_run_heads, grid_for(c, n, 256), 256, 0, c->stream, rec, BIN_W, ord, n, 0, 2, head.p);
   DC_LAUNCHED(c);
   DC_TRY(excl_scan<uint32_t>(c, head.p, run.p, n, tot.p));
   uint32_t hn = 0;
   DC_TRY(readback(c, tot.p, 4, &hn));
   DC_TRY(alloc(c, out, (uint64_t)hn * BIN_W));
-  k_combine_bins<<<grid_for(c, n, 256), 256, 0, c->stream>>>(rec, ord, head.p, run.p, n, out.p);
+  dc_launch(k_combine_bins, grid_for(c, n, 256), 256, 0, c->stream, rec, ord, head.p, run.p, n, out.p);
   DC_LAUNCHED(c);
   *n_out = hn;
   return DC_OK;
@@ -320,24 +320,24 @@ static dc_status partition(Ctx* c, const dc_cct* t, const uint32_t* l2g, uint32_
   const uint64_t N = t->N;
   Buf<uint64_t> h;
   DC_TRY(alloc(c, h, 2 * N));
-  k_hash_root<<<1, 1, 0, c->stream>>>(h.p);
+  dc_launch(k_hash_root, 1, 1, 0, c->stream, h.p);
   DC_LAUNCHED(c);
   std::vector<uint32_t> lo(t->max_depth + 2);
   DC_TRY(readback(c, t->level_off, lo.size() * 4, lo.data()));
   for (uint32_t d = 1; d <= t->max_depth; ++d) {
     const uint32_t a = lo[d], b = lo[d + 1];
     if (b > a) {
-      k_hash_level<<<grid_for(c, b - a, 256), 256, 0, c->stream>>>(t->parent, t->frame, l2g, a, b, h.p, c->merge_mask);
+      dc_launch(k_hash_level, grid_for(c, b - a, 256), 256, 0, c->stream, t->parent, t->frame, l2g, a, b, h.p, c->merge_mask);
       DC_LAUNCHED(c);
     }
   }
   Buf<unsigned long long> cnt, cur;
   DC_TRY(alloc_zero(c, cnt, 2 * P));
   DC_TRY(alloc(c, cur, 2 * P));
-  k_part_count<<<grid_for(c, N, 256), 256, 0, c->stream>>>(h.p, N, P, cnt.p);
+  dc_launch(k_part_count, grid_for(c, N, 256), 256, 0, c->stream, h.p, N, P, cnt.p);
   DC_LAUNCHED(c);
   if (t->Nbins)
-    k_part_bins<<<grid_for(c, t->Nbins, 256), 256, 0, c->stream>>>(h.p, t->bin_pcnode, t->bin_stall, t->bin_count, t->pc_ctx,
+    dc_launch(k_part_bins, grid_for(c, t->Nbins, 256), 256, 0, c->stream, h.p, t->bin_pcnode, t->bin_stall, t->bin_count, t->pc_ctx,
                                                                    t->pc_off, N, t->Nbins, P, 1, cnt.p + P, nullptr);
   DC_LAUNCHED(c);
   std::vector<uint64_t> hc(2 * P);
@@ -356,12 +356,12 @@ static dc_status partition(Ctx* c, const dc_cct* t, const uint32_t* l2g, uint32_
   DC_TRY(alloc(c, s.nodes, an * f.W));
   DC_TRY(alloc(c, s.bins, ab * BIN_W));
   const uint64_t* mc = t->mcols;
-  k_part_nodes<<<grid_for(c, N, 256), 256, 0, c->stream>>>(h.p, t->parent, t->frame, t->depth, l2g, t->xcnt, t->icnt, mc,
+  dc_launch(k_part_nodes, grid_for(c, N, 256), 256, 0, c->stream, h.p, t->parent, t->frame, t->depth, l2g, t->xcnt, t->icnt, mc,
                                                            t->xsamples, t->isamples, t->xstall, t->istall, N, f, P, cur.p,
                                                            s.nodes.p);
   DC_LAUNCHED(c);
   if (t->Nbins) {
-    k_part_bins<<<grid_for(c, t->Nbins, 256), 256, 0, c->stream>>>(h.p, t->bin_pcnode, t->bin_stall, t->bin_count, t->pc_ctx,
+    dc_launch(k_part_bins, grid_for(c, t->Nbins, 256), 256, 0, c->stream, h.p, t->bin_pcnode, t->bin_stall, t->bin_count, t->pc_ctx,
                                                                    t->pc_off, N, t->Nbins, P, 0, cur.p + P, s.bins.p);
     DC_LAUNCHED(c);
   }
@@ -392,7 +392,7 @@ static dc_cct* make_partition(Ctx* c, const RecFmt& f, uint64_t n_nodes, Buf<uin
 // ---------------------------------------------------------------- canonicalisation (gather)
 // all unique node records (any order) -> canonical CCT
 __global__ void k_canon_depthkey(const uint64_t* __restrict__ rec, uint32_t W, uint64_t n, uint64_t* __restrict__ key,
-                                 uint32_t* __restrict__ val) {
+                                 uint32_t* __restrict__ val) { DC_PDL_ENTER();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     key[i] = rec[i * W + 4] >> 32;  // depth
     val[i] = (uint32_t)i;
@@ -402,7 +402,7 @@ __global__ void k_canon_depthkey(const uint64_t* __restrict__ rec, uint32_t W, u
 // hash table h(128) -> canonical id
 __device__ __forceinline__ uint64_t htab_slot(uint64_t lo, uint64_t hi, uint64_t mask) { return mix64(lo ^ (hi * 3)) & mask; }
 __global__ void k_htab_insert(const uint64_t* __restrict__ rec, uint32_t W, const uint32_t* __restrict__ order, uint32_t a, uint32_t b,
-                              const uint32_t* __restrict__ canon_of_pos, ulonglong2* tab, uint32_t* tid, uint64_t mask) {
+                              const uint32_t* __restrict__ canon_of_pos, ulonglong2* tab, uint32_t* tid, uint64_t mask) { DC_PDL_ENTER();
   for (uint32_t i = a + blockIdx.x * blockDim.x + threadIdx.x; i < b; i += gridDim.x * blockDim.x) {
     const uint64_t* r = rec + (uint64_t)order[i] * W;
     const uint64_t lo = r[0], hi = r[1];
@@ -430,7 +430,7 @@ __device__ __forceinline__ uint32_t htab_find(const ulonglong2* tab, const uint3
 // level d: key = (parent canonical id - level_start(d-1)) << fbits | gframe for records order[a..b)
 __global__ void k_canon_keys(const uint64_t* __restrict__ rec, uint32_t W, const uint32_t* __restrict__ order, uint32_t a, uint32_t b,
                              const ulonglong2* __restrict__ tab, const uint32_t* __restrict__ tid, uint64_t mask, uint32_t prev_start,
-                             int fbits, uint64_t* __restrict__ key, uint32_t* __restrict__ val, uint32_t* d_err) {
+                             int fbits, uint64_t* __restrict__ key, uint32_t* __restrict__ val, uint32_t* d_err) { DC_PDL_ENTER();
   for (uint32_t i = a + blockIdx.x * blockDim.x + threadIdx.x; i < b; i += gridDim.x * blockDim.x) {
     const uint64_t* r = rec + (uint64_t)order[i] * W;
     const uint32_t p = htab_find(tab, tid, mask, r[2], r[3]);
@@ -445,7 +445,7 @@ __global__ void k_canon_emit(const uint64_t* __restrict__ rec, RecFmt f, const u
                              uint32_t* __restrict__ parent, uint32_t* __restrict__ frame, uint16_t* __restrict__ depth,
                              uint64_t* __restrict__ xcnt, uint64_t* __restrict__ icnt, uint64_t* __restrict__ mcols,
                              uint64_t* __restrict__ xs, uint64_t* __restrict__ is, uint64_t* __restrict__ xst,
-                             uint64_t* __restrict__ ist, uint32_t* __restrict__ canon_of_pos, uint32_t dpt) {
+                             uint64_t* __restrict__ ist, uint32_t* __restrict__ canon_of_pos, uint32_t dpt) { DC_PDL_ENTER();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n_level; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t id = start + (uint32_t)i;
     const uint64_t* r = rec + (uint64_t)src[i] * f.W;
@@ -472,7 +472,7 @@ __global__ void k_canon_emit(const uint64_t* __restrict__ rec, RecFmt f, const u
 // bins -> (ctx canonical, pc, stall) sort keys
 __global__ void k_canon_binkeys(const uint64_t* __restrict__ bins, uint64_t nb, const ulonglong2* __restrict__ tab,
                                 const uint32_t* __restrict__ tid, uint64_t mask, int pcb, uint64_t* __restrict__ key,
-                                uint32_t* __restrict__ val, uint32_t* d_err) {
+                                uint32_t* __restrict__ val, uint32_t* d_err) { DC_PDL_ENTER();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nb; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t* r = bins + i * BIN_W;
     const uint32_t ctx = htab_find(tab, tid, mask, r[0], r[1]);
@@ -482,21 +482,21 @@ __global__ void k_canon_binkeys(const uint64_t* __restrict__ bins, uint64_t nb, 
     val[i] = (uint32_t)i;
   }
 }
-__global__ void k_canon_binmax(const uint64_t* __restrict__ bins, uint64_t nb, unsigned int* mx) {
+__global__ void k_canon_binmax(const uint64_t* __restrict__ bins, uint64_t nb, unsigned int* mx) { DC_PDL_ENTER();
   uint32_t m = 0;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nb; i += (uint64_t)gridDim.x * blockDim.x)
     m = max(m, (uint32_t)bins[i * BIN_W + 2]);
   for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
   if (lane_id() == 0 && m) atomicMax(mx, m);
 }
-__global__ void k_canon_binheads(const uint64_t* __restrict__ key, uint64_t nb, uint32_t* __restrict__ head) {
+__global__ void k_canon_binheads(const uint64_t* __restrict__ key, uint64_t nb, uint32_t* __restrict__ head) { DC_PDL_ENTER();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nb; i += (uint64_t)gridDim.x * blockDim.x)
     head[i] = (i == 0 || (key[i - 1] >> 5) != (key[i] >> 5)) ? 1u : 0u;
 }
 __global__ void k_canon_binemit(const uint64_t* __restrict__ key, const uint32_t* __restrict__ val, const uint64_t* __restrict__ bins,
                                 uint64_t nb, int pcb, const uint32_t* __restrict__ head, const uint32_t* __restrict__ run, uint64_t N,
                                 uint32_t* __restrict__ pc_ctx, uint32_t* __restrict__ pc_off, uint32_t* __restrict__ bin_pcnode,
-                                uint16_t* __restrict__ bin_stall, uint64_t* __restrict__ bin_count) {
+                                uint16_t* __restrict__ bin_stall, uint64_t* __restrict__ bin_count) { DC_PDL_ENTER();
   const uint64_t pm = (1ull << pcb) - 1ull;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nb; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t k = key[i];
@@ -522,7 +522,7 @@ static dc_status canonicalize(Ctx* c, const uint64_t* rec, uint64_t n, const uin
   DC_TRY(alloc(c, k1, n));
   DC_TRY(alloc(c, v0, n));
   DC_TRY(alloc(c, v1, n));
-  k_canon_depthkey<<<grid_for(c, n, 256), 256, 0, c->stream>>>(rec, f.W, n, k0.p, v0.p);
+  dc_launch(k_canon_depthkey, grid_for(c, n, 256), 256, 0, c->stream, rec, f.W, n, k0.p, v0.p);
   DC_LAUNCHED(c);
   bool in1 = false;
   DC_TRY(radix_sort_pairs(c, k0.p, v0.p, k1.p, v1.p, n, 0, 16, &in1));
@@ -585,7 +585,7 @@ static dc_status canonicalize(Ctx* c, const uint64_t* rec, uint64_t n, const uin
       DC_CUDA(c, cudaMemsetAsync(k0.p, 0, 8, c->stream));
     } else {
       const int pbits = bits_for(lvl[d] - lvl[d - 1] > 1 ? lvl[d] - lvl[d - 1] - 1 : 1);
-      k_canon_keys<<<grid_for(c, m, 256), 256, 0, c->stream>>>(rec, f.W, byd.p, a, b, tab.p, tid.p, cap - 1, prev_start, fbits,
+      dc_launch(k_canon_keys, grid_for(c, m, 256), 256, 0, c->stream, rec, f.W, byd.p, a, b, tab.p, tid.p, cap - 1, prev_start, fbits,
                                                                k0.p, v0.p, err.p);
       DC_LAUNCHED(c);
       bool r1 = false;
@@ -593,13 +593,13 @@ static dc_status canonicalize(Ctx* c, const uint64_t* rec, uint64_t n, const uin
       keys = r1 ? k1.p : k0.p;
       src = r1 ? v1.p : v0.p;
     }
-    k_canon_emit<<<grid_for(c, m, 256), 256, 0, c->stream>>>(rec, f, src, m, keys, fbits, prev_start, a, n, t->parent, t->frame,
+    dc_launch(k_canon_emit, grid_for(c, m, 256), 256, 0, c->stream, rec, f, src, m, keys, fbits, prev_start, a, n, t->parent, t->frame,
                                                              t->depth, t->xcnt, t->icnt, t->mcols, t->xsamples, t->isamples,
                                                              t->xstall, t->istall, canon.p, d);
     DC_LAUNCHED(c);
     // register this level's hashes: position i (in emit order) -> canonical id a + i
     // (emit order == src order; insert needs the record index per position)
-    k_htab_insert<<<grid_for(c, m, 256), 256, 0, c->stream>>>(rec, f.W, src, 0, m, canon.p, tab.p, tid.p, cap - 1);
+    dc_launch(k_htab_insert, grid_for(c, m, 256), 256, 0, c->stream, rec, f.W, src, 0, m, canon.p, tab.p, tid.p, cap - 1);
     DC_LAUNCHED(c);
     prev_start = a;
   }
@@ -616,12 +616,12 @@ static dc_status canonicalize(Ctx* c, const uint64_t* rec, uint64_t n, const uin
     DC_TRY(alloc(c, bv0, nb));
     DC_TRY(alloc(c, bv1, nb));
     DC_TRY(alloc_zero(c, mx, 1));
-    k_canon_binmax<<<grid_for(c, nb, 256), 256, 0, c->stream>>>(bins, nb, mx.p);
+    dc_launch(k_canon_binmax, grid_for(c, nb, 256), 256, 0, c->stream, bins, nb, mx.p);
     DC_LAUNCHED(c);
     uint32_t hm = 0;
     DC_TRY(readback(c, mx.p, 4, &hm));
     const int pcb = bits_for(hm) ? bits_for(hm) : 1;
-    k_canon_binkeys<<<grid_for(c, nb, 256), 256, 0, c->stream>>>(bins, nb, tab.p, tid.p, cap - 1, pcb, bk0.p, bv0.p, err.p);
+    dc_launch(k_canon_binkeys, grid_for(c, nb, 256), 256, 0, c->stream, bins, nb, tab.p, tid.p, cap - 1, pcb, bk0.p, bv0.p, err.p);
     DC_LAUNCHED(c);
     bool r1 = false;
     DC_TRY(radix_sort_pairs(c, bk0.p, bv0.p, bk1.p, bv1.p, nb, 0, bits_for(n) + pcb + 5, &r1));
@@ -630,7 +630,7 @@ static dc_status canonicalize(Ctx* c, const uint64_t* rec, uint64_t n, const uin
     DC_TRY(alloc(c, head, nb));
     DC_TRY(alloc(c, run, nb));
     DC_TRY(alloc(c, tot, 1));
-    k_canon_binheads<<<grid_for(c, nb, 256), 256, 0, c->stream>>>(sk, nb, head.p);
+    dc_launch(k_canon_binheads, grid_for(c, nb, 256), 256, 0, c->stream, sk, nb, head.p);
     DC_LAUNCHED(c);
     DC_TRY(excl_scan<uint32_t>(c, head.p, run.p, nb, tot.p));
     uint32_t npc = 0;
@@ -642,7 +642,7 @@ static dc_status canonicalize(Ctx* c, const uint64_t* rec, uint64_t n, const uin
     DC_TRY(palloc(c, t->bin_pcnode, nb));
     DC_TRY(palloc(c, t->bin_stall, nb));
     DC_TRY(palloc(c, t->bin_count, nb));
-    k_canon_binemit<<<grid_for(c, nb, 256), 256, 0, c->stream>>>(sk, sv, bins, nb, pcb, head.p, run.p, n, t->pc_ctx, t->pc_off,
+    dc_launch(k_canon_binemit, grid_for(c, nb, 256), 256, 0, c->stream, sk, sv, bins, nb, pcb, head.p, run.p, n, t->pc_ctx, t->pc_off,
                                                                  t->bin_pcnode, t->bin_stall, t->bin_count);
     DC_LAUNCHED(c);
   }
@@ -653,7 +653,7 @@ static dc_status canonicalize(Ctx* c, const uint64_t* rec, uint64_t n, const uin
 }
 
 // ---------------------------------------------------------------- dictionary unify
-__global__ void k_l2g(const uint32_t* __restrict__ ids, uint64_t base, uint64_t D, uint32_t* __restrict__ l2g) {
+__global__ void k_l2g(const uint32_t* __restrict__ ids, uint64_t base, uint64_t D, uint32_t* __restrict__ l2g) { DC_PDL_ENTER();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < D; i += (uint64_t)gridDim.x * blockDim.x)
     l2g[i] = ids[base + i];
 }
@@ -670,7 +670,7 @@ static dc_status unify_dicts(Ctx* c, const dc_frame_key* all_keys, const std::ve
     const uint64_t D = key_off[p + 1] - key_off[p];
     DC_TRY(alloc(c, l2g[p], D));
     if (D) {
-      k_l2g<<<grid_for(c, D, 256), 256, 0, c->stream>>>(ids.p, key_off[p], D, l2g[p].p);
+      dc_launch(k_l2g, grid_for(c, D, 256), 256, 0, c->stream, ids.p, key_off[p], D, l2g[p].p);
       DC_LAUNCHED(c);
     }
   }

@@ -35,7 +35,7 @@ __device__ __forceinline__ void block_diag_add(unsigned long long* d_diag, uint3
 __global__ void k_pc_table(const dc_pc_sample* __restrict__ smp, uint64_t n, const uint32_t* __restrict__ launch_leaf,
                            uint64_t n_launch, uint32_t S, uint64_t N, ulonglong2* table, unsigned long long* tcnt,
                            uint64_t mask, unsigned int* d_distinct, unsigned int* d_overflow, unsigned long long* d_diag,
-                           uint32_t* d_flags) {
+                           uint32_t* d_flags) { DC_PDL_ENTER();
   uint32_t bad_l = 0, bad_s = 0, zero = 0;
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
     uint4 q = __ldg(reinterpret_cast<const uint4*>(smp) + j);  // {launch, pc_off, stall|flags<<16, count}
@@ -66,7 +66,7 @@ __global__ void k_pc_table(const dc_pc_sample* __restrict__ smp, uint64_t n, con
 
 // compact the table into (sort key, count) with key = ((ctx << pcb | pc) << 5) | stall
 __global__ void k_pc_compact(const ulonglong2* __restrict__ table, const unsigned long long* __restrict__ tcnt, uint64_t cap,
-                             int pcb, uint64_t* __restrict__ keys, uint64_t* __restrict__ cnts, unsigned int* d_pos) {
+                             int pcb, uint64_t* __restrict__ keys, uint64_t* __restrict__ cnts, unsigned int* d_pos) { DC_PDL_ENTER();
   for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < cap; s += (uint64_t)gridDim.x * blockDim.x) {
     ulonglong2 cur = table[s];
     if (cur.x == ~0ull) continue;
@@ -77,7 +77,7 @@ __global__ void k_pc_compact(const ulonglong2* __restrict__ table, const unsigne
   }
 }
 
-__global__ void k_pc_maxpc(const ulonglong2* __restrict__ table, uint64_t cap, unsigned int* d_max) {
+__global__ void k_pc_maxpc(const ulonglong2* __restrict__ table, uint64_t cap, unsigned int* d_max) { DC_PDL_ENTER();
   uint32_t m = 0;
   for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < cap; s += (uint64_t)gridDim.x * blockDim.x) {
     ulonglong2 cur = table[s];
@@ -88,12 +88,12 @@ __global__ void k_pc_maxpc(const ulonglong2* __restrict__ table, uint64_t cap, u
   if (lane_id() == 0 && m) atomicMax(d_max, m);
 }
 
-__global__ void k_iota32(uint32_t* a, uint64_t n) {
+__global__ void k_iota32(uint32_t* a, uint64_t n) { DC_PDL_ENTER();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) a[i] = (uint32_t)i;
 }
 
 // heads of (ctx, pc) runs among sorted bins
-__global__ void k_pc_heads(const uint64_t* __restrict__ keys, uint64_t nb, uint32_t* __restrict__ head) {
+__global__ void k_pc_heads(const uint64_t* __restrict__ keys, uint64_t nb, uint32_t* __restrict__ head) { DC_PDL_ENTER();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nb; i += (uint64_t)gridDim.x * blockDim.x)
     head[i] = (i == 0 || (keys[i - 1] >> 5) != (keys[i] >> 5)) ? 1u : 0u;
 }
@@ -102,7 +102,7 @@ __global__ void k_pc_emit(const uint64_t* __restrict__ keys, const uint32_t* __r
                           uint64_t nb, int pcb, const uint32_t* __restrict__ head, const uint32_t* __restrict__ run_excl,
                           uint64_t N, uint64_t S, uint32_t* __restrict__ pc_ctx, uint32_t* __restrict__ pc_off,
                           uint32_t* __restrict__ bin_pcnode, uint16_t* __restrict__ bin_stall, uint64_t* __restrict__ bin_count,
-                          unsigned long long* __restrict__ xsamples, unsigned long long* __restrict__ xstall) {
+                          unsigned long long* __restrict__ xsamples, unsigned long long* __restrict__ xstall) { DC_PDL_ENTER();
   const uint64_t pcmask = (1ull << pcb) - 1ull;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nb; i += (uint64_t)gridDim.x * blockDim.x) {
     uint64_t k = keys[i];
@@ -171,7 +171,7 @@ dc_status pc_attribute(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, con
       DC_CUDA(c, cudaMemsetAsync(table.p, 0xFF, cap * 16, c->stream));
       {
         Region rk(c, "k:pc_table");
-        k_pc_table<<<grid_for(c, n, 256, 16), 256, 0, c->stream>>>(s, n, launch_leaf, n_launch, S, N, table.p, tcnt.p,
+        dc_launch(k_pc_table, grid_for(c, n, 256, 16), 256, 0, c->stream, s, n, launch_leaf, n_launch, S, N, table.p, tcnt.p,
                                                                     cap - 1, ctr.p, ctr.p + 1, ldiag.p, c->d_flags);
       DC_LAUNCHED(c);
       }
@@ -188,7 +188,7 @@ dc_status pc_attribute(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, con
     DC_TRY(add_diag(c, ldiag.p));
     Buf<unsigned int> mx;
     DC_TRY(alloc_zero(c, mx, 2));
-    k_pc_maxpc<<<grid_for(c, cap, 256), 256, 0, c->stream>>>(table.p, cap, mx.p);
+    dc_launch(k_pc_maxpc, grid_for(c, cap, 256), 256, 0, c->stream, table.p, cap, mx.p);
     DC_LAUNCHED(c);
     uint32_t hm[2];
     DC_TRY(readback(c, mx.p, 8, hm));
@@ -198,7 +198,7 @@ dc_status pc_attribute(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, con
       return fail(c, DC_ERR_CAPACITY, "PC bin sort key exceeds 64 bits");
     DC_TRY(alloc(c, keys, nb));
     DC_TRY(alloc(c, cnts, nb));
-    k_pc_compact<<<grid_for(c, cap, 256), 256, 0, c->stream>>>(table.p, tcnt.p, cap, pcb, keys.p, cnts.p, mx.p + 1);
+    dc_launch(k_pc_compact, grid_for(c, cap, 256), 256, 0, c->stream, table.p, tcnt.p, cap, pcb, keys.p, cnts.p, mx.p + 1);
     DC_LAUNCHED(c);
     table.release();
     tcnt.release();
@@ -210,7 +210,7 @@ dc_status pc_attribute(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, con
   DC_TRY(alloc(c, keys2, nb));
   DC_TRY(alloc(c, ord0, nb));
   DC_TRY(alloc(c, ord1, nb));
-  k_iota32<<<grid_for(c, nb, 256), 256, 0, c->stream>>>(ord0.p, nb);
+  dc_launch(k_iota32, grid_for(c, nb, 256), 256, 0, c->stream, ord0.p, nb);
   DC_LAUNCHED(c);
   bool in1 = false;
   const int kbits = bits_for(N > 1 ? N - 1 : 1) + pcb + 5;
@@ -219,7 +219,7 @@ dc_status pc_attribute(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, con
   uint32_t* so = in1 ? ord1.p : ord0.p;
   DC_TRY(alloc(c, head, nb));
   DC_TRY(alloc(c, runs, nb));
-  k_pc_heads<<<grid_for(c, nb, 256), 256, 0, c->stream>>>(sk, nb, head.p);
+  dc_launch(k_pc_heads, grid_for(c, nb, 256), 256, 0, c->stream, sk, nb, head.p);
   DC_LAUNCHED(c);
   Buf<uint32_t> npc;
   DC_TRY(alloc(c, npc, 1));
@@ -234,7 +234,7 @@ dc_status pc_attribute(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, con
   DC_TRY(palloc(c, t->bin_stall, nb));
   DC_TRY(palloc(c, t->bin_count, nb));
   if (nb) {
-    k_pc_emit<<<grid_for(c, nb, 256), 256, 0, c->stream>>>(sk, so, cnts.p, nb, pcb, head.p, runs.p, N, S, t->pc_ctx,
+    dc_launch(k_pc_emit, grid_for(c, nb, 256), 256, 0, c->stream, sk, so, cnts.p, nb, pcb, head.p, runs.p, N, S, t->pc_ctx,
                                                            t->pc_off, t->bin_pcnode, t->bin_stall, t->bin_count,
                                                            (unsigned long long*)t->xsamples, (unsigned long long*)t->xstall);
     DC_LAUNCHED(c);

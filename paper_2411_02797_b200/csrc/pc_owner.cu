@@ -70,14 +70,14 @@ struct OwnSmem {
 __device__ __forceinline__ void cons_sync() { asm volatile("bar.sync 1, %0;" ::"n"(OW_CONS) : "memory"); }
 
 // ---------------------------------------------------------------- prep kernels
-__global__ void k_own_check(const uint64_t* __restrict__ off, uint64_t n_launch, uint64_t n, uint32_t* bad) {
+__global__ void k_own_check(const uint64_t* __restrict__ off, uint64_t n_launch, uint64_t n, uint32_t* bad) { DC_PDL_ENTER();
   for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < n_launch; l += (uint64_t)gridDim.x * blockDim.x)
     if (off[l + 1] < off[l]) atomicOr(bad, 1u);
   if (blockIdx.x == 0 && threadIdx.x == 0 && (off[0] != 0 || off[n_launch] != n)) atomicOr(bad, 1u);
 }
 
 __global__ void k_own_keys(const uint32_t* __restrict__ leaf, uint64_t n_launch, uint64_t N, uint64_t* __restrict__ key,
-                           uint32_t* __restrict__ val) {
+                           uint32_t* __restrict__ val) { DC_PDL_ENTER();
   for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < n_launch; l += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t c = leaf[l];
     key[l] = c < N ? c : N;
@@ -90,7 +90,7 @@ __global__ void k_own_keys(const uint32_t* __restrict__ leaf, uint64_t n_launch,
 // N + 1 counters, a scatter through atomic cursors. Three launches instead of check + keys + a
 // multi-pass radix sort.
 __global__ void k_own_hist(const uint32_t* __restrict__ leaf, const uint64_t* __restrict__ off, uint64_t n_launch, uint64_t n,
-                           uint64_t N, uint32_t* __restrict__ hist, uint32_t* bad) {
+                           uint64_t N, uint32_t* __restrict__ hist, uint32_t* bad) { DC_PDL_ENTER();
   bool b = false;
   for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < n_launch; l += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t c = leaf[l];
@@ -101,7 +101,7 @@ __global__ void k_own_hist(const uint32_t* __restrict__ leaf, const uint64_t* __
   if (b) atomicOr(bad, 1u);
 }
 __global__ void k_own_scatter(const uint32_t* __restrict__ leaf, uint64_t n_launch, uint64_t N, uint32_t* __restrict__ cursor,
-                              uint64_t* __restrict__ key, uint32_t* __restrict__ val) {
+                              uint64_t* __restrict__ key, uint32_t* __restrict__ val) { DC_PDL_ENTER();
   for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < n_launch; l += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t c0 = leaf[l], c = c0 < N ? c0 : (uint32_t)N;
     const uint32_t pos = atomicAdd(&cursor[c], 1u);
@@ -117,7 +117,7 @@ __global__ void k_own_scatter(const uint32_t* __restrict__ leaf, uint64_t n_laun
 // valid samples (0 for padding); per stage, its first launch and context.
 __global__ void k_plan_launch(const uint64_t* __restrict__ off, const uint32_t* __restrict__ order,
                               const uint64_t* __restrict__ lkey, uint64_t n_launch, uint64_t* __restrict__ lrow,
-                              uint32_t* __restrict__ lflag, uint64_t* __restrict__ lsrc, uint64_t* __restrict__ lcnt) {
+                              uint32_t* __restrict__ lflag, uint64_t* __restrict__ lsrc, uint64_t* __restrict__ lcnt) { DC_PDL_ENTER();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n_launch; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t l = order[i];
     const uint64_t b = off[l], e = off[l + 1];
@@ -131,7 +131,7 @@ __global__ void k_plan_launch(const uint64_t* __restrict__ off, const uint32_t* 
 
 // gfirst[g] = first sorted launch of context group g; gfirst[NG] = n_launch
 __global__ void k_plan_gfirst(const uint64_t* __restrict__ lkey, const uint32_t* __restrict__ gx, const uint32_t* ng,
-                              uint64_t n_launch, uint32_t* __restrict__ gfirst) {
+                              uint64_t n_launch, uint32_t* __restrict__ gfirst) { DC_PDL_ENTER();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n_launch; i += (uint64_t)gridDim.x * blockDim.x) {
     if (i == 0 || lkey[i] != lkey[i - 1]) gfirst[gx[i]] = (uint32_t)i;
     if (i == n_launch - 1) gfirst[*ng] = (uint32_t)n_launch;
@@ -140,7 +140,7 @@ __global__ void k_plan_gfirst(const uint64_t* __restrict__ lkey, const uint32_t*
 
 // stages per group (0 past the last group, so the scan can run over the n_launch bound)
 __global__ void k_plan_gstages(const uint64_t* __restrict__ E, const uint32_t* __restrict__ gfirst, const uint32_t* ng,
-                               uint64_t n_launch, uint64_t* __restrict__ gst) {
+                               uint64_t n_launch, uint64_t* __restrict__ gst) { DC_PDL_ENTER();
   const uint32_t NG = *ng;
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < n_launch; g += (uint64_t)gridDim.x * blockDim.x)
     gst[g] = g < NG ? (E[gfirst[g + 1]] - E[gfirst[g]] + OW_ROWS - 1) / OW_ROWS : 0;
@@ -152,7 +152,7 @@ __global__ void k_plan_rows(const uint64_t* __restrict__ E, const uint32_t* __re
                             const uint64_t* __restrict__ lkey, const uint32_t* __restrict__ order,
                             const uint64_t* __restrict__ lcnt, uint64_t n_launch, uint64_t row_cap,
                             uint64_t* __restrict__ rowpos, uint32_t* __restrict__ row_launch, uint8_t* __restrict__ row_valid,
-                            uint32_t* __restrict__ st_first, uint32_t* __restrict__ st_ctx) {
+                            uint32_t* __restrict__ st_first, uint32_t* __restrict__ st_ctx) { DC_PDL_ENTER();
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5, nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t i = wid; i < n_launch; i += nw) {
@@ -387,7 +387,7 @@ __device__ __noinline__ void own_cold(const uint4 q, uint32_t seg_launch, const 
 }
 
 template <int MODE>  // 0 = the product; 1, 2, 3, 9 = measurement variants (DC_OWN_MODE)
-__global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) {
+__global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) { DC_PDL_ENTER();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   OwnSmem& sm = *reinterpret_cast<OwnSmem*>(smem_raw);
   const uint32_t tid = threadIdx.x;
@@ -723,7 +723,7 @@ constexpr uint32_t BR_MAXCH = ((OW_TAB > (int)OW_SPILL_CAP ? OW_TAB : OW_SPILL_C
 
 // runs before the host has read the segment count: it takes the device counter (clamped)
 __global__ void k_br_range(const uint4* __restrict__ seg, const unsigned int* __restrict__ d_nsegs, uint32_t cap_segs,
-                           const uint32_t* __restrict__ pkey, uint64_t N, uint32_t* __restrict__ cmax, uint32_t* __restrict__ cor) {
+                           const uint32_t* __restrict__ pkey, uint64_t N, uint32_t* __restrict__ cmax, uint32_t* __restrict__ cor) { DC_PDL_ENTER();
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t n_segs = min(*d_nsegs, cap_segs);
   BR_FOR_CHUNKS(seg, n_segs, N) {
@@ -746,7 +746,7 @@ __global__ void k_br_range(const uint4* __restrict__ seg, const unsigned int* __
 }
 
 __global__ void k_br_words(const uint32_t* __restrict__ cmax, const uint32_t* __restrict__ cor, uint64_t N,
-                           uint64_t* __restrict__ cw, uint8_t* __restrict__ csh, uint32_t* too_wide) {
+                           uint64_t* __restrict__ cw, uint8_t* __restrict__ csh, uint32_t* too_wide) { DC_PDL_ENTER();
   for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < N; c += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t m = cmax[c], o = cor[c];
     const int sh = o ? __ffs(o) - 1 : 0;
@@ -758,7 +758,7 @@ __global__ void k_br_words(const uint32_t* __restrict__ cmax, const uint32_t* __
 }
 
 __global__ void k_br_bits(const uint4* __restrict__ seg, uint32_t n_segs, const uint32_t* __restrict__ pkey, uint64_t N,
-                          const uint64_t* __restrict__ wbase, const uint8_t* __restrict__ csh, uint32_t* __restrict__ bm) {
+                          const uint64_t* __restrict__ wbase, const uint8_t* __restrict__ csh, uint32_t* __restrict__ bm) { DC_PDL_ENTER();
   BR_FOR_CHUNKS(seg, n_segs, N) {
     const uint64_t base = (uint64_t)sg.z | ((uint64_t)sg.w << 32);
     const uint32_t j0 = (uint32_t)(item % BR_MAXCH) * BR_CH, j1 = min(sg.y, j0 + BR_CH);
@@ -773,7 +773,7 @@ __global__ void k_br_bits(const uint4* __restrict__ seg, uint32_t n_segs, const 
 }
 
 // packed per-word counts: bins (popcount) in the high half, PC nodes (word != 0) in the low half
-__global__ void k_br_pop(const uint32_t* __restrict__ bm, uint64_t W, uint64_t* __restrict__ pk) {
+__global__ void k_br_pop(const uint32_t* __restrict__ bm, uint64_t W, uint64_t* __restrict__ pk) { DC_PDL_ENTER();
   for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < W; w += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t b = bm[w];
     pk[w] = ((uint64_t)__popc(b) << 32) | (b != 0u ? 1u : 0u);
@@ -786,7 +786,7 @@ __global__ void k_br_pop(const uint32_t* __restrict__ bm, uint64_t W, uint64_t* 
 __global__ void k_br_emit(const uint32_t* __restrict__ bm, const uint64_t* __restrict__ pre, uint64_t W,
                           const uint64_t* __restrict__ wbase, const uint8_t* __restrict__ csh, uint64_t N,
                           uint32_t* __restrict__ pc_ctx, uint32_t* __restrict__ pc_off, uint32_t* __restrict__ bin_pcnode,
-                          uint16_t* __restrict__ bin_stall) {
+                          uint16_t* __restrict__ bin_stall) { DC_PDL_ENTER();
   for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < W; w += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t bits = bm[w];
     if (!bits) continue;
@@ -820,7 +820,7 @@ __global__ void __launch_bounds__(32 * BR_WARPS) k_br_count(
     const unsigned long long* __restrict__ pcnt, uint64_t N, uint32_t S, const uint32_t* __restrict__ bm,
     const uint64_t* __restrict__ pre, const uint64_t* __restrict__ wbase, const uint8_t* __restrict__ csh,
     unsigned long long* __restrict__ bin_count, unsigned long long* __restrict__ xsamples,
-    unsigned long long* __restrict__ xstall) {
+    unsigned long long* __restrict__ xstall) { DC_PDL_ENTER();
   __shared__ uint32_t lo[BR_WARPS][32], hi[BR_WARPS][32];
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   lo[w][lane] = 0;
@@ -895,7 +895,7 @@ __global__ void __launch_bounds__(RD_THREADS, 1) k_own_reduce(
     const unsigned long long* __restrict__ pcnt, uint64_t N, uint32_t* __restrict__ okey,
     unsigned long long* __restrict__ ocnt, uint32_t* __restrict__ g_nbins, uint32_t* __restrict__ g_npcs,
     uint32_t* __restrict__ g_ctx, unsigned long long* __restrict__ xsamples, unsigned long long* __restrict__ xstall,
-    uint32_t S, uint32_t* g_flags) {
+    uint32_t S, uint32_t* g_flags) { DC_PDL_ENTER();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   RedSmem& sm = *reinterpret_cast<RedSmem*>(smem_raw);
   const uint32_t tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
@@ -1170,7 +1170,7 @@ __global__ void k_own_place(const uint64_t* __restrict__ grp_out, const uint32_t
                             const uint32_t* __restrict__ g_ctx, uint32_t n_groups, const uint32_t* __restrict__ okey,
                             const unsigned long long* __restrict__ ocnt, uint64_t N, uint32_t* __restrict__ pc_ctx,
                             uint32_t* __restrict__ pc_off, uint32_t* __restrict__ bin_pcnode, uint16_t* __restrict__ bin_stall,
-                            uint64_t* __restrict__ bin_count) {
+                            uint64_t* __restrict__ bin_count) { DC_PDL_ENTER();
   for (uint32_t g = blockIdx.x; g < n_groups; g += gridDim.x) {
     const uint64_t ib = grp_out[g];
     const uint32_t nb = g_nbins[g], ob = bin_base[g], pb = pc_base[g], ctx = g_ctx[g];
@@ -1197,24 +1197,24 @@ __global__ void k_own_place(const uint64_t* __restrict__ grp_out, const uint32_t
   }
 }
 
-__global__ void k_own_groups(const uint64_t* __restrict__ skey, uint32_t n, uint32_t* __restrict__ head) {
+__global__ void k_own_groups(const uint64_t* __restrict__ skey, uint32_t n, uint32_t* __restrict__ head) { DC_PDL_ENTER();
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     head[i] = (i == 0 || skey[i - 1] != skey[i]) ? 1u : 0u;
 }
 __global__ void k_own_gstart(const uint32_t* __restrict__ head, const uint32_t* __restrict__ hex, uint32_t n,
-                             uint32_t* __restrict__ grp_start, uint32_t n_groups) {
+                             uint32_t* __restrict__ grp_start, uint32_t n_groups) { DC_PDL_ENTER();
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     if (head[i]) grp_start[hex[i]] = i;
   if (blockIdx.x == 0 && threadIdx.x == 0) grp_start[n_groups] = n;
 }
-__global__ void k_own_segkeys(const uint4* __restrict__ seg, uint32_t n, uint64_t* __restrict__ key, uint32_t* __restrict__ val) {
+__global__ void k_own_segkeys(const uint4* __restrict__ seg, uint32_t n, uint64_t* __restrict__ key, uint32_t* __restrict__ val) { DC_PDL_ENTER();
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     key[i] = seg[i].x;
     val[i] = i;
   }
 }
 __global__ void k_own_gsize(const uint4* __restrict__ seg, const uint32_t* __restrict__ order, const uint32_t* __restrict__ grp_start,
-                            uint32_t n_groups, uint64_t* __restrict__ gsz) {
+                            uint32_t n_groups, uint64_t* __restrict__ gsz) { DC_PDL_ENTER();
   for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < n_groups; g += gridDim.x * blockDim.x) {
     uint64_t s = 0;
     for (uint32_t i = grp_start[g]; i < grp_start[g + 1]; ++i) s += seg[order[i]].y;
@@ -1251,15 +1251,15 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
       Region rs(c, "prep:sort");
       Buf<uint32_t> hist;
       DC_TRY(alloc_zero(c, hist, N + 1));
-      k_own_hist<<<grid_for(c, n_launch, 256), 256, 0, c->stream>>>(launch_leaf, launch_off, n_launch, n, N, hist.p, bad.p);
+      dc_launch(k_own_hist, grid_for(c, n_launch, 256), 256, 0, c->stream, launch_leaf, launch_off, n_launch, n, N, hist.p, bad.p);
       DC_LAUNCHED(c);
       DC_TRY(excl_scan<uint32_t>(c, hist.p, hist.p, N + 1, nullptr));
-      k_own_scatter<<<grid_for(c, n_launch, 256), 256, 0, c->stream>>>(launch_leaf, n_launch, N, hist.p, k0.p, v0.p);
+      dc_launch(k_own_scatter, grid_for(c, n_launch, 256), 256, 0, c->stream, launch_leaf, n_launch, N, hist.p, k0.p, v0.p);
       DC_LAUNCHED(c);
     } else {
-      k_own_check<<<grid_for(c, n_launch, 256), 256, 0, c->stream>>>(launch_off, n_launch, n, bad.p);
+      dc_launch(k_own_check, grid_for(c, n_launch, 256), 256, 0, c->stream, launch_off, n_launch, n, bad.p);
       DC_LAUNCHED(c);
-      k_own_keys<<<grid_for(c, n_launch, 256), 256, 0, c->stream>>>(launch_leaf, n_launch, N, k0.p, v0.p);
+      dc_launch(k_own_keys, grid_for(c, n_launch, 256), 256, 0, c->stream, launch_leaf, n_launch, N, k0.p, v0.p);
       DC_LAUNCHED(c);
       Region rs(c, "prep:sort");
       DC_TRY(radix_sort_pairs(c, k0.p, v0.p, k1.p, v1.p, n_launch, 0, bits_for(N), &in1));
@@ -1280,17 +1280,17 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
     DC_TRY(alloc_zero(c, row_valid, row_cap));
     DC_TRY(alloc(c, st_first, st_cap));
     DC_TRY(alloc(c, st_ctx, st_cap));
-    k_plan_launch<<<grid_for(c, n_launch, 256), 256, 0, c->stream>>>(launch_off, order, lkey, n_launch, lrow.p, lflag.p,
+    dc_launch(k_plan_launch, grid_for(c, n_launch, 256), 256, 0, c->stream, launch_off, order, lkey, n_launch, lrow.p, lflag.p,
                                                                     lsrc.p, lcnt.p);
     DC_LAUNCHED(c);
     DC_TRY(excl_scan<uint64_t>(c, lrow.p, lrow.p, n_launch, lrow.p + n_launch));  // E: first row within the stream
     DC_TRY(excl_scan<uint32_t>(c, lflag.p, gx.p, n_launch, gx.p + n_launch));      // group index, NG at gx[n]
-    k_plan_gfirst<<<grid_for(c, n_launch, 256), 256, 0, c->stream>>>(lkey, gx.p, gx.p + n_launch, n_launch, gfirst.p);
+    dc_launch(k_plan_gfirst, grid_for(c, n_launch, 256), 256, 0, c->stream, lkey, gx.p, gx.p + n_launch, n_launch, gfirst.p);
     DC_LAUNCHED(c);
-    k_plan_gstages<<<grid_for(c, n_launch, 256), 256, 0, c->stream>>>(lrow.p, gfirst.p, gx.p + n_launch, n_launch, gst.p);
+    dc_launch(k_plan_gstages, grid_for(c, n_launch, 256), 256, 0, c->stream, lrow.p, gfirst.p, gx.p + n_launch, n_launch, gst.p);
     DC_LAUNCHED(c);
     DC_TRY(excl_scan<uint64_t>(c, gst.p, gst.p, n_launch, tot.p));  // first stage per group, total stages
-    k_plan_rows<<<grid_for(c, n_launch * 32, 256), 256, 0, c->stream>>>(lrow.p, gx.p, gfirst.p, gst.p, lkey, order, lcnt.p,
+    dc_launch(k_plan_rows, grid_for(c, n_launch * 32, 256), 256, 0, c->stream, lrow.p, gx.p, gfirst.p, gst.p, lkey, order, lcnt.p,
                                                                        n_launch, row_cap, rowpos.p, row_launch.p,
                                                                        row_valid.p, st_first.p, st_ctx.p);
     DC_LAUNCHED(c);
@@ -1361,7 +1361,7 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
     DC_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     {
       Region rk(c, "k:pc_owner");
-      kern<<<G, OW_THREADS, smem, c->stream>>>(a);
+      dc_launch(kern, G, OW_THREADS, smem, c->stream, a);
       DC_LAUNCHED(c);
     }
     if (a.probe_mode == 9 || a.probe_mode == 2) {  // measurement only: print the cycle splits
@@ -1393,13 +1393,13 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
     DC_TRY(alloc_zero(c, wide, 1));
     {
       Region rk(c, "k:br_range");
-      k_br_range<<<grid_for(c, (uint64_t)cap_segs * BR_MAXCH * 32, 256), 256, 0, c->stream>>>(seg.p, a.g_segs, cap_segs, pkey.p,
+      dc_launch(k_br_range, grid_for(c, (uint64_t)cap_segs * BR_MAXCH * 32, 256), 256, 0, c->stream, seg.p, a.g_segs, cap_segs, pkey.p,
                                                                                             N, cm.p, cm.p + N);
       DC_LAUNCHED(c);
     }
     {
       Region rk(c, "k:br_words");
-      k_br_words<<<grid_for(c, N, 256), 256, 0, c->stream>>>(cm.p, cm.p + N, N, cw.p, csh.p, wide.p);
+      dc_launch(k_br_words, grid_for(c, N, 256), 256, 0, c->stream, cm.p, cm.p + N, N, cw.p, csh.p, wide.p);
       DC_LAUNCHED(c);
     }
     DC_TRY(excl_scan<uint64_t>(c, cw.p, cw.p, N, cw.p + N));  // word base per context, W at cw[N]
@@ -1426,12 +1426,12 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
       DC_TRY(alloc(c, pk, W + 1));
       {
         Region rk(c, "k:br_bits");
-        k_br_bits<<<segs_grid, 256, 0, c->stream>>>(seg.p, n_segs, pkey.p, N, cw.p, csh.p, bm.p);
+        dc_launch(k_br_bits, segs_grid, 256, 0, c->stream, seg.p, n_segs, pkey.p, N, cw.p, csh.p, bm.p);
         DC_LAUNCHED(c);
       }
       {
         Region rk(c, "k:br_pop");
-        k_br_pop<<<grid_for(c, W, 256), 256, 0, c->stream>>>(bm.p, W, pk.p);
+        dc_launch(k_br_pop, grid_for(c, W, 256), 256, 0, c->stream, bm.p, W, pk.p);
         DC_LAUNCHED(c);
       }
       DC_TRY(excl_scan<uint64_t>(c, pk.p, pk.p, W, pk.p + W));
@@ -1449,14 +1449,13 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
       if (nb) {
         {
           Region rk(c, "k:br_emit");
-          k_br_emit<<<grid_for(c, W, 256), 256, 0, c->stream>>>(bm.p, pk.p, W, cw.p, csh.p, N, t->pc_ctx, t->pc_off,
+          dc_launch(k_br_emit, grid_for(c, W, 256), 256, 0, c->stream, bm.p, pk.p, W, cw.p, csh.p, N, t->pc_ctx, t->pc_off,
                                                                 t->bin_pcnode, t->bin_stall);
           DC_LAUNCHED(c);
         }
         {
           Region rk(c, "k:br_count");
-          k_br_count<<<grid_for(c, (uint64_t)n_segs * BR_MAXCH * 32, 32 * BR_WARPS), 32 * BR_WARPS, 0, c->stream>>>(
-              seg.p, n_segs, pkey.p, pcnt.p, N, S, bm.p, pk.p, cw.p, csh.p, (unsigned long long*)t->bin_count,
+          dc_launch(k_br_count, grid_for(c, (uint64_t)n_segs * BR_MAXCH * 32, 32 * BR_WARPS), 32 * BR_WARPS, 0, c->stream, seg.p, n_segs, pkey.p, pcnt.p, N, S, bm.p, pk.p, cw.p, csh.p, (unsigned long long*)t->bin_count,
               (unsigned long long*)t->xsamples, (unsigned long long*)t->xstall);
           DC_LAUNCHED(c);
         }
@@ -1477,13 +1476,13 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
   DC_TRY(alloc(c, sv1, n_segs));
   DC_TRY(alloc(c, head, n_segs));
   DC_TRY(alloc(c, hex, n_segs));
-  k_own_segkeys<<<grid_for(c, n_segs, 256), 256, 0, c->stream>>>(seg.p, n_segs, sk0.p, sv0.p);
+  dc_launch(k_own_segkeys, grid_for(c, n_segs, 256), 256, 0, c->stream, seg.p, n_segs, sk0.p, sv0.p);
   DC_LAUNCHED(c);
   bool sin1 = false;
   DC_TRY(radix_sort_pairs(c, sk0.p, sv0.p, sk1.p, sv1.p, n_segs, 0, bits_for(N), &sin1));
   uint64_t* ssk = sin1 ? sk1.p : sk0.p;
   uint32_t* sso = sin1 ? sv1.p : sv0.p;
-  k_own_groups<<<grid_for(c, n_segs, 256), 256, 0, c->stream>>>(ssk, n_segs, head.p);
+  dc_launch(k_own_groups, grid_for(c, n_segs, 256), 256, 0, c->stream, ssk, n_segs, head.p);
   DC_LAUNCHED(c);
   Buf<uint32_t> ng;
   DC_TRY(alloc(c, ng, 1));
@@ -1503,12 +1502,12 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
     return DC_OK;
   }
   DC_TRY(alloc(c, grp_start, n_groups + 1));
-  k_own_gstart<<<grid_for(c, n_segs, 256), 256, 0, c->stream>>>(head.p, hex.p, n_segs, grp_start.p, n_groups);
+  dc_launch(k_own_gstart, grid_for(c, n_segs, 256), 256, 0, c->stream, head.p, hex.p, n_segs, grp_start.p, n_groups);
   DC_LAUNCHED(c);
   Buf<uint64_t> gsz, gout;
   DC_TRY(alloc(c, gsz, n_groups));
   DC_TRY(alloc(c, gout, n_groups + 1));
-  k_own_gsize<<<grid_for(c, n_groups, 128), 128, 0, c->stream>>>(seg.p, sso, grp_start.p, n_groups, gsz.p);
+  dc_launch(k_own_gsize, grid_for(c, n_groups, 128), 128, 0, c->stream, seg.p, sso, grp_start.p, n_groups, gsz.p);
   DC_LAUNCHED(c);
   DC_TRY(excl_scan<uint64_t>(c, gsz.p, gout.p, n_groups, gout.p + n_groups));
   // per-context reduce
@@ -1531,8 +1530,7 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
   }
   {
     Region rk(c, "k:own_reduce");
-    k_own_reduce<<<n_groups < (uint32_t)G ? n_groups : G, RD_THREADS, rsmem, c->stream>>>(
-        seg.p, sso, grp_start.p, n_groups, gout.p, pkey.p, pcnt.p, N, okey.p, ocnt.p, gnb.p, gnp.p, gctx.p,
+    dc_launch(k_own_reduce, n_groups < (uint32_t)G ? n_groups : G, RD_THREADS, rsmem, c->stream, seg.p, sso, grp_start.p, n_groups, gout.p, pkey.p, pcnt.p, N, okey.p, ocnt.p, gnb.p, gnp.p, gctx.p,
         (unsigned long long*)t->xsamples, (unsigned long long*)t->xstall, S, flags.p);
     DC_LAUNCHED(c);
   }
@@ -1554,8 +1552,7 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
   DC_TRY(palloc(c, t->bin_pcnode, nb));
   DC_TRY(palloc(c, t->bin_stall, nb));
   DC_TRY(palloc(c, t->bin_count, nb));
-  k_own_place<<<n_groups < 4u * G ? (n_groups ? n_groups : 1) : 4 * G, 256, 0, c->stream>>>(
-      gout.p, gnb.p, bbase.p, pbase.p, gctx.p, n_groups, okey.p, ocnt.p, N, t->pc_ctx, t->pc_off, t->bin_pcnode,
+  dc_launch(k_own_place, n_groups < 4u * G ? (n_groups ? n_groups : 1) : 4 * G, 256, 0, c->stream, gout.p, gnb.p, bbase.p, pbase.p, gctx.p, n_groups, okey.p, ocnt.p, N, t->pc_ctx, t->pc_off, t->bin_pcnode,
       t->bin_stall, t->bin_count);
   DC_LAUNCHED(c);
   DC_TRY(add_diag(c, ldiag.p));

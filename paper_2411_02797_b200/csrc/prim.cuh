@@ -46,7 +46,7 @@ __device__ __forceinline__ T block_excl_scan(T v, T* total) {
 }
 
 template <class T>
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan_reduce(const T* __restrict__ in, uint64_t n, T* __restrict__ sums) {
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_reduce(const T* __restrict__ in, uint64_t n, T* __restrict__ sums) { DC_PDL_ENTER();
   const uint64_t base = (uint64_t)blockIdx.x * SCAN_TILE;
   T s = 0;
 #pragma unroll
@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_reduce(const T* __restric
 constexpr int SCAN1_THREADS = 1024;
 constexpr uint64_t SCAN1_MAX = 1ull << 16;
 template <class T>
-__global__ void __launch_bounds__(SCAN1_THREADS) k_scan_one(const T* in, T* out, uint64_t n, T* total) {
+__global__ void __launch_bounds__(SCAN1_THREADS) k_scan_one(const T* in, T* out, uint64_t n, T* total) { DC_PDL_ENTER();
   __shared__ T wsum[32];
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint64_t C = (n + 31) / 32;
@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(SCAN1_THREADS) k_scan_one(const T* in, T* out,
 
 template <class T>
 __global__ void __launch_bounds__(SCAN_THREADS) k_scan_down(const T* __restrict__ in, T* out, uint64_t n,
-                                                            const T* __restrict__ offs) {
+                                                            const T* __restrict__ offs) { DC_PDL_ENTER();
   // each thread owns SCAN_ITEMS consecutive elements of the tile
   const uint64_t base = (uint64_t)blockIdx.x * SCAN_TILE + (uint64_t)threadIdx.x * SCAN_ITEMS;
   T v[SCAN_ITEMS];
@@ -124,16 +124,16 @@ dc_status excl_scan(Ctx* c, const T* in, T* out, uint64_t n, T* total_dev) {
   }
   uint64_t nt = (n + SCAN_TILE - 1) / SCAN_TILE;
   if (n <= SCAN1_MAX) {  // one launch
-    k_scan_one<T><<<1, SCAN1_THREADS, 0, c->stream>>>(in, out, n, total_dev);
+    dc_launch(k_scan_one<T>, 1, SCAN1_THREADS, 0, c->stream, in, out, n, total_dev);
     DC_LAUNCHED(c);
     return DC_OK;
   }
   Buf<T> sums;
   DC_TRY(alloc(c, sums, nt));
-  k_scan_reduce<T><<<(unsigned)nt, SCAN_THREADS, 0, c->stream>>>(in, n, sums.p);
+  dc_launch(k_scan_reduce<T>, (unsigned)nt, SCAN_THREADS, 0, c->stream, in, n, sums.p);
   DC_LAUNCHED(c);
   DC_TRY(excl_scan<T>(c, sums.p, sums.p, nt, total_dev));
-  k_scan_down<T><<<(unsigned)nt, SCAN_THREADS, 0, c->stream>>>(in, out, n, sums.p);
+  dc_launch(k_scan_down<T>, (unsigned)nt, SCAN_THREADS, 0, c->stream, in, out, n, sums.p);
   DC_LAUNCHED(c);
   return DC_OK;
 }
@@ -151,7 +151,7 @@ __device__ __forceinline__ uint32_t rs_digit(uint64_t k, int shift, uint32_t mas
 
 // per-tile digit histogram, digit-major: hist[d * n_tiles + tile]
 static __global__ void __launch_bounds__(RS_THREADS) k_rs_count(const uint64_t* __restrict__ keys, uint32_t n, int shift,
-                                                         uint32_t mask, uint32_t* __restrict__ hist, uint32_t n_tiles) {
+                                                         uint32_t mask, uint32_t* __restrict__ hist, uint32_t n_tiles) { DC_PDL_ENTER();
   __shared__ uint32_t cnt[256];
   cnt[threadIdx.x] = 0;
   __syncthreads();
@@ -172,7 +172,7 @@ static __global__ void __launch_bounds__(RS_THREADS) k_rs_count(const uint64_t* 
 static __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals,
                                                            uint64_t* __restrict__ okeys, uint32_t* __restrict__ ovals, uint32_t n,
                                                            int shift, uint32_t mask, const uint32_t* __restrict__ offs,
-                                                           uint32_t n_tiles) {
+                                                           uint32_t n_tiles) { DC_PDL_ENTER();
   __shared__ uint32_t wcnt[RS_WARPS][256];
   for (int i = threadIdx.x; i < RS_WARPS * 256; i += RS_THREADS) (&wcnt[0][0])[i] = 0;
   __syncthreads();
@@ -231,7 +231,7 @@ struct SmallSortSmem {
 
 static __global__ void __launch_bounds__(SS_THREADS, 1) k_sort_small(const uint64_t* __restrict__ ik, const uint32_t* __restrict__ iv,
                                                                   uint64_t* __restrict__ ok, uint32_t* __restrict__ ov, uint32_t n,
-                                                                  int begin_bit, int end_bit) {
+                                                                  int begin_bit, int end_bit) { DC_PDL_ENTER();
   extern __shared__ __align__(128) unsigned char ss_raw[];
   SmallSortSmem& sm = *reinterpret_cast<SmallSortSmem*>(ss_raw);
   const uint32_t tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
@@ -307,7 +307,7 @@ static inline dc_status radix_sort_pairs(Ctx* c, uint64_t* k0, uint32_t* v0, uin
       DC_CUDA(c, cudaFuncSetAttribute(k_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SmallSortSmem)));
       attr = true;
     }
-    k_sort_small<<<1, SS_THREADS, sizeof(SmallSortSmem), c->stream>>>(k0, v0, k1, v1, (uint32_t)n, begin_bit, end_bit);
+    dc_launch(k_sort_small, 1, SS_THREADS, sizeof(SmallSortSmem), c->stream, k0, v0, k1, v1, (uint32_t)n, begin_bit, end_bit);
     DC_LAUNCHED(c);
     *result_in_1 = true;
     return DC_OK;
@@ -324,10 +324,10 @@ static inline dc_status radix_sort_pairs(Ctx* c, uint64_t* k0, uint32_t* v0, uin
     const uint32_t* iv = in1 ? v1 : v0;
     uint64_t* ok = in1 ? k0 : k1;
     uint32_t* ov = in1 ? v0 : v1;
-    k_rs_count<<<nt, RS_THREADS, 0, c->stream>>>(ik, (uint32_t)n, shift, mask, hist.p, nt);
+    dc_launch(k_rs_count, nt, RS_THREADS, 0, c->stream, ik, (uint32_t)n, shift, mask, hist.p, nt);
     DC_LAUNCHED(c);
     DC_TRY(excl_scan<uint32_t>(c, hist.p, hist.p, (uint64_t)256 * nt, nullptr));
-    k_rs_scatter<<<nt, RS_THREADS, 0, c->stream>>>(ik, iv, ok, ov, (uint32_t)n, shift, mask, hist.p, nt);
+    dc_launch(k_rs_scatter, nt, RS_THREADS, 0, c->stream, ik, iv, ok, ov, (uint32_t)n, shift, mask, hist.p, nt);
     DC_LAUNCHED(c);
     in1 = !in1;
   }

@@ -29,7 +29,7 @@ __device__ __forceinline__ double rdiv(uint64_t a, uint64_t b) { return __ddiv_r
 // launches(n) = sum of xcnt over masked-kind nodes of n's subtree: own value + push to ancestors
 __global__ void k_rule_launches(const uint32_t* __restrict__ parent, const uint32_t* __restrict__ frame,
                                 const uint8_t* __restrict__ fk, uint32_t n_frames, uint32_t mask,
-                                const uint64_t* __restrict__ xcnt, uint64_t N, unsigned long long* __restrict__ il) {
+                                const uint64_t* __restrict__ xcnt, uint64_t N, unsigned long long* __restrict__ il) { DC_PDL_ENTER();
   for (uint64_t n = 1 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; n < N; n += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t v = rule_kind_ok(fk, n_frames, frame[n], mask) ? xcnt[n] : 0;
     if (!v) continue;
@@ -39,13 +39,13 @@ __global__ void k_rule_launches(const uint32_t* __restrict__ parent, const uint3
 }
 
 __global__ void k_rule_kind_gate(const uint32_t* __restrict__ frame, const uint8_t* __restrict__ fk, uint32_t n_frames,
-                                 uint32_t mask, uint64_t N, unsigned long long* __restrict__ gate) {
+                                 uint32_t mask, uint64_t N, unsigned long long* __restrict__ gate) { DC_PDL_ENTER();
   for (uint64_t n = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; n < N; n += (uint64_t)gridDim.x * blockDim.x)
     gate[n] = (n > 0 && rule_kind_ok(fk, n_frames, frame[n], mask)) ? 1ull : 0ull;
 }
 
 __global__ void k_rule_qualify(int rule, uint64_t N, const uint64_t* __restrict__ a, const uint64_t* __restrict__ b,
-                               const uint64_t* __restrict__ il, double threshold, uint64_t floor, uint8_t* __restrict__ q) {
+                               const uint64_t* __restrict__ il, double threshold, uint64_t floor, uint8_t* __restrict__ q) { DC_PDL_ENTER();
   for (uint64_t n = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; n < N; n += (uint64_t)gridDim.x * blockDim.x) {
     bool ok = false;
     if (n > 0) {
@@ -66,7 +66,7 @@ __global__ void k_rule_qualify(int rule, uint64_t N, const uint64_t* __restrict_
 
 // flagged = qualifies and no proper (non-root) ancestor qualifies
 __global__ void k_rule_suppress(const uint32_t* __restrict__ parent, uint64_t N, const uint8_t* __restrict__ q,
-                                uint32_t* __restrict__ flag, int suppress) {
+                                uint32_t* __restrict__ flag, int suppress) { DC_PDL_ENTER();
   for (uint64_t n = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; n < N; n += (uint64_t)gridDim.x * blockDim.x) {
     bool f = q[n] != 0;
     if (f && suppress)
@@ -80,7 +80,7 @@ __global__ void k_rule_suppress(const uint32_t* __restrict__ parent, uint64_t N,
 }
 
 __global__ void k_rule_emit(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos, uint64_t N, uint32_t cap,
-                            uint32_t* __restrict__ out) {
+                            uint32_t* __restrict__ out) { DC_PDL_ENTER();
   for (uint64_t n = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; n < N; n += (uint64_t)gridDim.x * blockDim.x)
     if (flag[n] && pos[n] < cap) out[pos[n]] = (uint32_t)n;
 }
@@ -100,12 +100,12 @@ dc_status analyze_flags(Ctx* c, const dc_cct* t, dc_rule rule, const dc_rule_par
   Buf<uint32_t> flag, pos, cnt, out;
   if (rule == DC_RULE_SMALL_KERNELS) {
     DC_TRY(alloc_zero(c, il, N));
-    k_rule_launches<<<grid_for(c, N, 256), 256, 0, c->stream>>>(t->parent, t->frame, t->frame_kind, t->n_frames, p->kind_mask,
+    dc_launch(k_rule_launches, grid_for(c, N, 256), 256, 0, c->stream, t->parent, t->frame, t->frame_kind, t->n_frames, p->kind_mask,
                                                                t->xcnt, N, il.p);
     DC_LAUNCHED(c);
   } else if (rule == DC_RULE_BWD_FWD) {  // operator nodes: the kind gate as a 0/1 column
     DC_TRY(alloc(c, il, N));
-    k_rule_kind_gate<<<grid_for(c, N, 256), 256, 0, c->stream>>>(t->frame, t->frame_kind, t->n_frames, p->kind_mask, N, il.p);
+    dc_launch(k_rule_kind_gate, grid_for(c, N, 256), 256, 0, c->stream, t->frame, t->frame_kind, t->n_frames, p->kind_mask, N, il.p);
     DC_LAUNCHED(c);
   }
   DC_TRY(alloc(c, q, N));
@@ -113,15 +113,15 @@ dc_status analyze_flags(Ctx* c, const dc_cct* t, dc_rule rule, const dc_rule_par
   DC_TRY(alloc(c, pos, N));
   DC_TRY(alloc(c, cnt, 1));
   DC_TRY(alloc(c, out, cap ? cap : 1));
-  k_rule_qualify<<<grid_for(c, N, 256), 256, 0, c->stream>>>((int)rule, N, t->col(C_ISUM, p->metric_a),
+  dc_launch(k_rule_qualify, grid_for(c, N, 256), 256, 0, c->stream, (int)rule, N, t->col(C_ISUM, p->metric_a),
                                                              rule != DC_RULE_SMALL_KERNELS ? t->col(C_ISUM, p->metric_b) : nullptr,
                                                              (const uint64_t*)il.p, p->threshold, p->floor, q.p);
   DC_LAUNCHED(c);
   // ② and ⑤ report the highest qualifying frame; ③ is per operator node (no suppression)
-  k_rule_suppress<<<grid_for(c, N, 256), 256, 0, c->stream>>>(t->parent, N, q.p, flag.p, rule == DC_RULE_BWD_FWD ? 0 : 1);
+  dc_launch(k_rule_suppress, grid_for(c, N, 256), 256, 0, c->stream, t->parent, N, q.p, flag.p, rule == DC_RULE_BWD_FWD ? 0 : 1);
   DC_LAUNCHED(c);
   DC_TRY(excl_scan<uint32_t>(c, flag.p, pos.p, N, cnt.p));
-  k_rule_emit<<<grid_for(c, N, 256), 256, 0, c->stream>>>(flag.p, pos.p, N, cap, out.p);
+  dc_launch(k_rule_emit, grid_for(c, N, 256), 256, 0, c->stream, flag.p, pos.p, N, cap, out.p);
   DC_LAUNCHED(c);
   uint32_t nf = 0;
   DC_TRY(readback(c, cnt.p, 4, &nf));
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(ST_THREADS) k_stall_issues(const uint32_t* __r
                                                              const uint64_t* __restrict__ bin_count,
                                                              const uint64_t* __restrict__ isamples, double stall_threshold,
                                                              uint32_t k, unsigned long long* __restrict__ pc_tot,
-                                                             dc_stall_issue* __restrict__ out, uint32_t* __restrict__ n_out) {
+                                                             dc_stall_issue* __restrict__ out, uint32_t* __restrict__ n_out) { DC_PDL_ENTER();
   __shared__ unsigned long long ss[32];
   const uint32_t node = hot[blockIdx.x];
   if (threadIdx.x < 32) ss[threadIdx.x] = 0;
@@ -211,7 +211,7 @@ dc_status analyze_stalls(Ctx* c, const dc_cct* t, uint32_t metric, uint32_t kind
   DC_TRY(alloc_zero(c, pc_tot, t->Npc));
   DC_TRY(alloc(c, dout, (uint64_t)nh * k));
   DC_CUDA(c, cudaMemcpyAsync(dhot.p, hid.data(), nh * 4, cudaMemcpyHostToDevice, c->stream));
-  k_stall_issues<<<nh, ST_THREADS, 0, c->stream>>>(dhot.p, t->N, t->Npc, t->Nbins, t->S, t->pc_ctx, t->bin_pcnode, t->bin_stall,
+  dc_launch(k_stall_issues, nh, ST_THREADS, 0, c->stream, dhot.p, t->N, t->Npc, t->Nbins, t->S, t->pc_ctx, t->bin_pcnode, t->bin_stall,
                                                    t->bin_count, t->isamples, stall_threshold, k, pc_tot.p, dout.p, dn.p);
   DC_LAUNCHED(c);
   std::vector<uint32_t> hn(nh);
@@ -235,7 +235,7 @@ dc_status analyze_stalls(Ctx* c, const dc_cct* t, uint32_t metric, uint32_t kind
 // the caller's (strings are not part of the device data).
 namespace dc {
 __global__ void k_fold_flags(const uint64_t* __restrict__ x, const uint16_t* __restrict__ depth, uint64_t N,
-                             uint32_t* __restrict__ flag, uint64_t* __restrict__ dep) {
+                             uint32_t* __restrict__ flag, uint64_t* __restrict__ dep) { DC_PDL_ENTER();
   for (uint64_t n = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; n < N; n += (uint64_t)gridDim.x * blockDim.x) {
     const bool f = n > 0 && x[n] != 0;
     flag[n] = f ? 1u : 0u;
@@ -245,7 +245,7 @@ __global__ void k_fold_flags(const uint64_t* __restrict__ x, const uint16_t* __r
 __global__ void k_fold_emit(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos, const uint64_t* __restrict__ poff,
                             const uint32_t* __restrict__ parent, const uint32_t* __restrict__ frame, const uint16_t* __restrict__ depth,
                             const uint64_t* __restrict__ x, uint64_t N, uint32_t* __restrict__ node_out, uint64_t* __restrict__ val_out,
-                            uint64_t* __restrict__ off_out, uint32_t* __restrict__ frames_out) {
+                            uint64_t* __restrict__ off_out, uint32_t* __restrict__ frames_out) { DC_PDL_ENTER();
   for (uint64_t n = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; n < N; n += (uint64_t)gridDim.x * blockDim.x) {
     if (!flag[n]) continue;
     const uint32_t i = pos[n];
@@ -275,7 +275,7 @@ dc_status export_folded(Ctx* c, const dc_cct* t, uint32_t metric, uint32_t* node
   DC_TRY(alloc(c, poff, N));
   DC_TRY(alloc(c, tot32, 1));
   DC_TRY(alloc(c, tot64, 1));
-  k_fold_flags<<<grid_for(c, N, 256), 256, 0, c->stream>>>(t->col(C_XSUM, metric), t->depth, N, flag.p, dep.p);
+  dc_launch(k_fold_flags, grid_for(c, N, 256), 256, 0, c->stream, t->col(C_XSUM, metric), t->depth, N, flag.p, dep.p);
   DC_LAUNCHED(c);
   DC_TRY(excl_scan<uint32_t>(c, flag.p, pos.p, N, tot32.p));
   DC_TRY(excl_scan<uint64_t>(c, dep.p, poff.p, N, tot64.p));
@@ -291,7 +291,7 @@ dc_status export_folded(Ctx* c, const dc_cct* t, uint32_t metric, uint32_t* node
   DC_TRY(alloc(c, vals, nl));
   DC_TRY(alloc(c, offs, nl));
   DC_TRY(alloc(c, frames, nf));
-  k_fold_emit<<<grid_for(c, N, 256), 256, 0, c->stream>>>(flag.p, pos.p, poff.p, t->parent, t->frame, t->depth,
+  dc_launch(k_fold_emit, grid_for(c, N, 256), 256, 0, c->stream, flag.p, pos.p, poff.p, t->parent, t->frame, t->depth,
                                                           t->col(C_XSUM, metric), N, nodes.p, vals.p, offs.p, frames.p);
   DC_LAUNCHED(c);
   if (nl) {
@@ -312,14 +312,14 @@ dc_status export_folded(Ctx* c, const dc_cct* t, uint32_t metric, uint32_t* node
 // each stream, then a segmented adjacent difference, scattered back to trace order.
 namespace dc {
 __global__ void k_iv_keys(const uint32_t* __restrict__ thread, const uint8_t* __restrict__ kind, uint64_t n,
-                          uint64_t* __restrict__ key, uint32_t* __restrict__ val) {
+                          uint64_t* __restrict__ key, uint32_t* __restrict__ val) { DC_PDL_ENTER();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     key[i] = (uint64_t)thread[i] << 8 | kind[i];
     val[i] = (uint32_t)i;
   }
 }
 __global__ void k_iv_diff(const uint64_t* __restrict__ key, const uint32_t* __restrict__ val, const uint64_t* __restrict__ ts,
-                          uint64_t n, uint64_t* __restrict__ interval, uint8_t* __restrict__ valid, uint32_t* d_flags) {
+                          uint64_t n, uint64_t* __restrict__ interval, uint8_t* __restrict__ valid, uint32_t* d_flags) { DC_PDL_ENTER();
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t i = val[j];
     uint64_t iv = 0;
@@ -348,11 +348,11 @@ dc_status cpu_intervals(Ctx* c, const uint32_t* thread, const uint8_t* kind, con
   DC_TRY(alloc(c, k1, n));
   DC_TRY(alloc(c, v0, n));
   DC_TRY(alloc(c, v1, n));
-  k_iv_keys<<<grid_for(c, n, 256), 256, 0, c->stream>>>(thread, kind, n, k0.p, v0.p);
+  dc_launch(k_iv_keys, grid_for(c, n, 256), 256, 0, c->stream, thread, kind, n, k0.p, v0.p);
   DC_LAUNCHED(c);
   bool in1 = false;
   DC_TRY(radix_sort_pairs(c, k0.p, v0.p, k1.p, v1.p, n, 0, 40, &in1));
-  k_iv_diff<<<grid_for(c, n, 256), 256, 0, c->stream>>>(in1 ? k1.p : k0.p, in1 ? v1.p : v0.p, ts, n, out_interval, out_valid,
+  dc_launch(k_iv_diff, grid_for(c, n, 256), 256, 0, c->stream, in1 ? k1.p : k0.p, in1 ? v1.p : v0.p, ts, n, out_interval, out_valid,
                                                          c->d_flags);
   DC_LAUNCHED(c);
   return DC_OK;
@@ -371,7 +371,7 @@ constexpr uint64_t SQ_EMPTY = ~0ull;
 __device__ __forceinline__ uint64_t sq_slot(uint64_t seq, uint64_t mask) { return (mix64(seq) >> 7) & mask; }
 
 __global__ void k_seq_insert(const int64_t* __restrict__ fseq, uint64_t nf, unsigned long long* key, unsigned long long* idx,
-                             uint64_t mask, unsigned int* overflow) {
+                             uint64_t mask, unsigned int* overflow) { DC_PDL_ENTER();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nf; i += (uint64_t)gridDim.x * blockDim.x) {
     const int64_t s = fseq[i];
     if (s < 0) continue;  // only forward ops carrying a sequence id are registered
@@ -392,7 +392,7 @@ __global__ void k_seq_insert(const int64_t* __restrict__ fseq, uint64_t nf, unsi
 __global__ void k_seq_lookup(const int64_t* __restrict__ bseq, uint64_t nb, const uint64_t* __restrict__ boff,
                              const uint64_t* __restrict__ foff, const unsigned long long* __restrict__ key,
                              const unsigned long long* __restrict__ idx, uint64_t mask, uint64_t* __restrict__ fwd_of,
-                             uint64_t* __restrict__ len, unsigned long long* unmatched) {
+                             uint64_t* __restrict__ len, unsigned long long* unmatched) { DC_PDL_ENTER();
   for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < nb; r += (uint64_t)gridDim.x * blockDim.x) {
     const int64_t s = bseq[r];
     uint64_t f = SQ_EMPTY;
@@ -416,7 +416,7 @@ __global__ void k_seq_lookup(const int64_t* __restrict__ bseq, uint64_t nb, cons
 // warp per backward record: forward prefix then the record's own frames
 __global__ void k_seq_copy(uint64_t nb, const uint64_t* __restrict__ fwd_of, const uint64_t* __restrict__ foff,
                            const uint32_t* __restrict__ ffr, const uint64_t* __restrict__ boff, const uint32_t* __restrict__ bfr,
-                           const uint64_t* __restrict__ ooff, uint32_t* __restrict__ ofr) {
+                           const uint64_t* __restrict__ ooff, uint32_t* __restrict__ ofr) { DC_PDL_ENTER();
   const uint32_t lane = lane_id();
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -455,10 +455,10 @@ dc_status seq_associate(Ctx* c, const int64_t* fseq, const uint64_t* foff, const
   DC_TRY(alloc(c, len, nb));
   DC_CUDA(c, cudaMemsetAsync(key.p, 0xFF, cap * 8, c->stream));
   if (nf) {
-    k_seq_insert<<<grid_for(c, nf, 256), 256, 0, c->stream>>>(fseq, nf, key.p, idx.p, cap - 1, ovf.p);
+    dc_launch(k_seq_insert, grid_for(c, nf, 256), 256, 0, c->stream, fseq, nf, key.p, idx.p, cap - 1, ovf.p);
     DC_LAUNCHED(c);
   }
-  k_seq_lookup<<<grid_for(c, nb, 256), 256, 0, c->stream>>>(bseq, nb, boff, foff, key.p, idx.p, cap - 1, fwd_of.p, len.p, unm.p);
+  dc_launch(k_seq_lookup, grid_for(c, nb, 256), 256, 0, c->stream, bseq, nb, boff, foff, key.p, idx.p, cap - 1, fwd_of.p, len.p, unm.p);
   DC_LAUNCHED(c);
   DC_TRY(excl_scan<uint64_t>(c, len.p, out_off, nb, out_off + nb));
   uint64_t tot = 0, un = 0;
@@ -468,7 +468,7 @@ dc_status seq_associate(Ctx* c, const int64_t* fseq, const uint64_t* foff, const
   *n_frames_h = tot;
   *n_unmatched_h = un;
   if (tot > cap_frames) return DC_OK;  // offsets only: the caller retries with room
-  k_seq_copy<<<grid_for(c, nb * 32, 256), 256, 0, c->stream>>>(nb, fwd_of.p, foff, ffr, boff, bfr, out_off, out_frames);
+  dc_launch(k_seq_copy, grid_for(c, nb * 32, 256), 256, 0, c->stream, nb, fwd_of.p, foff, ffr, boff, bfr, out_off, out_frames);
   DC_LAUNCHED(c);
   return DC_OK;
 }

@@ -24,7 +24,7 @@ __device__ __forceinline__ double frac_of(uint64_t v, uint64_t total) {
 // flag[i] for candidates i in [0, n) of the view; value[i]
 __global__ void k_view_nodes(const uint64_t* __restrict__ val, const uint32_t* __restrict__ frame, const uint8_t* __restrict__ fk,
                              uint32_t n_frames, uint32_t mask, uint64_t N, const uint64_t* __restrict__ total_p, double threshold,
-                             uint32_t* __restrict__ flag) {
+                             uint32_t* __restrict__ flag) { DC_PDL_ENTER();
   const uint64_t total = *total_p;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < N; i += (uint64_t)gridDim.x * blockDim.x) {
     bool ok = i > 0 && total > 0 && kind_ok(fk, n_frames, frame[i], mask) && frac_of(val[i], total) > threshold;
@@ -34,7 +34,7 @@ __global__ void k_view_nodes(const uint64_t* __restrict__ val, const uint32_t* _
 
 __global__ void k_bu_accum(const uint64_t* __restrict__ xval, const uint32_t* __restrict__ frame, const uint8_t* __restrict__ fk,
                            uint32_t n_frames, uint32_t mask, uint64_t N, unsigned long long* __restrict__ byf,
-                           uint32_t* __restrict__ seen) {
+                           uint32_t* __restrict__ seen) { DC_PDL_ENTER();
   for (uint64_t i = 1 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < N; i += (uint64_t)gridDim.x * blockDim.x) {
     uint32_t f = frame[i];
     if (f >= n_frames || !kind_ok(fk, n_frames, f, mask)) continue;
@@ -45,14 +45,14 @@ __global__ void k_bu_accum(const uint64_t* __restrict__ xval, const uint32_t* __
 }
 
 __global__ void k_view_frames(const uint64_t* __restrict__ byf, const uint32_t* __restrict__ seen, uint32_t n_frames,
-                              const uint64_t* __restrict__ total_p, double threshold, uint32_t* __restrict__ flag) {
+                              const uint64_t* __restrict__ total_p, double threshold, uint32_t* __restrict__ flag) { DC_PDL_ENTER();
   const uint64_t total = *total_p;
   for (uint32_t f = blockIdx.x * blockDim.x + threadIdx.x; f < n_frames; f += gridDim.x * blockDim.x)
     flag[f] = (seen[f] && total > 0 && frac_of(byf[f], total) > threshold) ? 1u : 0u;
 }
 
 __global__ void k_view_compact(const uint64_t* __restrict__ val, const uint32_t* __restrict__ flag,
-                               const uint32_t* __restrict__ pos, uint64_t n, uint64_t* __restrict__ key, uint32_t* __restrict__ id) {
+                               const uint32_t* __restrict__ pos, uint64_t n, uint64_t* __restrict__ key, uint32_t* __restrict__ id) { DC_PDL_ENTER();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
     if (flag[i]) {
       key[pos[i]] = ~val[i];  // ascending ~value == descending value; stable keeps id order
@@ -61,7 +61,7 @@ __global__ void k_view_compact(const uint64_t* __restrict__ val, const uint32_t*
 }
 
 __global__ void k_view_emit(const uint64_t* __restrict__ key, const uint32_t* __restrict__ id, uint32_t k,
-                            const uint64_t* __restrict__ total_p, dc_topk_entry* __restrict__ out) {
+                            const uint64_t* __restrict__ total_p, dc_topk_entry* __restrict__ out) { DC_PDL_ENTER();
   const uint64_t total = *total_p;
   for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) {
     uint64_t v = ~key[i];
@@ -77,7 +77,7 @@ __global__ void k_view_emit(const uint64_t* __restrict__ key, const uint32_t* __
 // one warp: rank S <= 32 stall counts by (count desc, stall asc), keep fraction > threshold
 __global__ void k_view_stall(const uint64_t* __restrict__ istall, const uint64_t* __restrict__ isamples, uint64_t N,
                              uint32_t S, uint32_t node, double threshold, uint32_t k, dc_topk_entry* __restrict__ out,
-                             uint32_t* __restrict__ n_out) {
+                             uint32_t* __restrict__ n_out) { DC_PDL_ENTER();
   const uint32_t s = lane_id();
   const uint64_t total = isamples[node];
   uint64_t v = s < S ? istall[(uint64_t)s * N + node] : 0;
@@ -111,7 +111,7 @@ dc_status hotspots_topk(Ctx* c, const dc_cct* t, dc_view view, uint32_t metric, 
     if (!t->xsamples) return DC_OK;
     Buf<uint32_t> nout;
     DC_TRY(alloc(c, nout, 1));
-    k_view_stall<<<1, 32, 0, c->stream>>>(t->istall, t->isamples, t->N, t->S, stall_node, threshold, k, out.p, nout.p);
+    dc_launch(k_view_stall, 1, 32, 0, c->stream, t->istall, t->isamples, t->N, t->S, stall_node, threshold, k, out.p, nout.p);
     DC_LAUNCHED(c);
     uint32_t h = 0;
     DC_TRY(readback(c, nout.p, 4, &h));
@@ -140,7 +140,7 @@ dc_status hotspots_topk(Ctx* c, const dc_cct* t, dc_view view, uint32_t metric, 
     n = t->N;
     val = view == DC_VIEW_INCLUSIVE ? ival : xval;
     DC_TRY(alloc(c, flag, n));
-    k_view_nodes<<<grid_for(c, n, 256), 256, 0, c->stream>>>(val, t->frame, t->frame_kind, t->n_frames, kind_mask, n, total_p,
+    dc_launch(k_view_nodes, grid_for(c, n, 256), 256, 0, c->stream, val, t->frame, t->frame_kind, t->n_frames, kind_mask, n, total_p,
                                                              threshold, flag.p);
     DC_LAUNCHED(c);
   } else if (view == DC_VIEW_BOTTOM_UP) {
@@ -148,10 +148,10 @@ dc_status hotspots_topk(Ctx* c, const dc_cct* t, dc_view view, uint32_t metric, 
     DC_TRY(alloc_zero(c, byf, n));
     DC_TRY(alloc_zero(c, seen, n));
     DC_TRY(alloc(c, flag, n));
-    k_bu_accum<<<grid_for(c, t->N, 256), 256, 0, c->stream>>>(xval, t->frame, t->frame_kind, t->n_frames, kind_mask, t->N,
+    dc_launch(k_bu_accum, grid_for(c, t->N, 256), 256, 0, c->stream, xval, t->frame, t->frame_kind, t->n_frames, kind_mask, t->N,
                                                               byf.p, seen.p);
     DC_LAUNCHED(c);
-    k_view_frames<<<grid_for(c, n, 256), 256, 0, c->stream>>>((const uint64_t*)byf.p, seen.p, (uint32_t)n, total_p, threshold,
+    dc_launch(k_view_frames, grid_for(c, n, 256), 256, 0, c->stream, (const uint64_t*)byf.p, seen.p, (uint32_t)n, total_p, threshold,
                                                               flag.p);
     DC_LAUNCHED(c);
     val = (const uint64_t*)byf.p;
@@ -169,12 +169,12 @@ dc_status hotspots_topk(Ctx* c, const dc_cct* t, dc_view view, uint32_t metric, 
   DC_TRY(alloc(c, k1, nc));
   DC_TRY(alloc(c, i0, nc));
   DC_TRY(alloc(c, i1, nc));
-  k_view_compact<<<grid_for(c, n, 256), 256, 0, c->stream>>>(val, flag.p, pos.p, n, k0.p, i0.p);
+  dc_launch(k_view_compact, grid_for(c, n, 256), 256, 0, c->stream, val, flag.p, pos.p, n, k0.p, i0.p);
   DC_LAUNCHED(c);
   bool in1 = false;
   DC_TRY(radix_sort_pairs(c, k0.p, i0.p, k1.p, i1.p, nc, 0, 64, &in1));
   uint32_t kk = nc < k ? nc : k;
-  k_view_emit<<<1, 256, 0, c->stream>>>(in1 ? k1.p : k0.p, in1 ? i1.p : i0.p, kk, total_p, out.p);
+  dc_launch(k_view_emit, 1, 256, 0, c->stream, in1 ? k1.p : k0.p, in1 ? i1.p : i0.p, kk, total_p, out.p);
   DC_LAUNCHED(c);
   DC_TRY(readback(c, out.p, kk * sizeof(dc_topk_entry), out_h));
   *n_out_h = kk;
