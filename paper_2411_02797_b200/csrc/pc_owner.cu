@@ -2,20 +2,23 @@
 //
 // When samples arrive contiguous per launch (launch_sample_off given, "flushes the metrics"
 // per activity buffer), launches are ordered by their context node and the
-// resulting ctx-ordered virtual sample stream is cut into num_SMs equal ranges, one
-// persistent 1024-thread CTA per SM:
-//   * warp 0 (one lane) streams the range's launch segments into shared memory with TMA bulk
-//     copies (cp.async.bulk + mbarrier, 3 x 31 KB stages) and decides the flush points;
-//   * 31 consumer warps aggregate (pc_off, stall) -> count in a 16384-slot shared-memory hash
-//     table (32-bit keys/counts, native shared atomics), deduplicating equal keys inside each
-//     warp (__match_any_sync) first, so a hot PC costs one atomic per warp; warps run free
+// resulting ctx-ordered virtual sample stream is cut into num_SMs equal ranges of stages, one
+// persistent CTA per SM; a CTA that finishes its range steals stages from the back of the
+// range with the most unclaimed stages (per-CTA claim words), so the slowest range does not
+// set the kernel time:
+//   * the producer warp streams each stage's launch segments (32-sample rows, see the stage
+//     plan below) into shared memory with TMA bulk copies (cp.async.bulk + mbarrier, 4 x 32 KB
+//     stages) and decides the flush points;
+//   * 16 consumer warps aggregate (pc_off, stall) -> count in an 11,136-slot shared-memory
+//     hash table probed in 4-slot buckets (one 16-B load settles a hit; predicated
+//     red.shared.add); misses are queued per warp and probed 32 at a time; warps run free
 //     (no per-stage CTA barrier) and only meet at flushes;
-//   * on a context change (or when the table passes half load) the table is flushed once to
-//     a partial list in HBM: each bin is written once per (CTA, context) segment — no global
-//     atomics on bins, no L2 hash table.
-// k_own_reduce then merges each context's segments in shared memory (stable radix sort +
-// reduce), producing canonical (pc, stall) order, PC node counts and the context's exclusive
-// samples / stall[s] totals; k_own_place writes the final SoA arrays.
+//   * on a context change (or at 2/3 table load) the table is flushed once to a partial list
+//     in HBM: each bin is written once per (CTA, context) segment — no global atomics on
+//     bins, no L2 hash table.
+// The global-bitmap reduce (k_br_*) then adds the partial entries into their final, canonical
+// (pc, stall) slots (the per-context shared-memory sort reduce, k_own_reduce, takes contexts
+// whose PC range is too wide for the bitmap).
 // Any sample this schedule cannot take (a valid launch that disagrees with its segment,
 // pc_off >= 2^27, a context whose partial list cannot be chunked into shared memory) makes
 // the call fall back to the generic schedule (pc.cu) for the whole input — same result.
@@ -41,6 +44,8 @@ constexpr uint32_t OW_FLUSH_REQ = OW_TAB * 2 / 3;
 constexpr uint32_t OW_SPILL_AT = OW_TAB - OW_CONS_WARPS * OW_PEND - 1;
 constexpr uint32_t OW_MISS = 0xFFFFFFFEu;
 constexpr uint32_t OW_SPILL_CAP = 16384;      // spill entries per CTA
+constexpr uint32_t OW_CLAIM = 4;              // stages claimed from the own range at a time
+constexpr uint32_t OW_STEAL = 8;              // at most this many stages stolen at a time
 constexpr uint32_t EMPTY32 = 0xFFFFFFFFu;
 constexpr uint32_t OW_DONE = 0xFFFFFFFFu;
 
@@ -208,6 +213,7 @@ struct OwnArgs {
   uint32_t probe_mode;         // measurement only (DC_OWN_MODE): 1 = stream + keys, no table
   uint32_t* sink;
   const uint32_t* bad;         // launch_sample_off inconsistent (k_own_check): do nothing, generic schedule
+  unsigned long long* claim;   // [gridDim.x] stage claim words, zeroed by the host
 };
 
 // all consumer threads; the caller has synchronised the consumers (every insert is done)
@@ -423,21 +429,83 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) { DC_PDL_
     const bool prof = MODE == 2 || MODE == 9;  // measurement only
     long long p_wait = 0, p_comp = 0, p_stages = 0, p_pieces = 0;
     const long long p_t0 = prof ? clock64() : 0;
-    // stage batches: cb = stages [bs, bs + 32), nb = [bs + 32, bs + 64)
-    uint64_t bs = s0;
-    uint32_t cb_first = 0, cb_ctx = 0, nb_first = 0, nb_ctx = 0;
-    if (s0 + lane < s1) {
-      cb_first = a.st_first[s0 + lane];
-      cb_ctx = a.st_ctx[s0 + lane];
+    // ---- stage source. The CTA's own range [s0, s1) is claimed from the front, OW_CLAIM stages
+    // at a time (claim word: stages taken from the front | from the back << 32). When it is
+    // exhausted the CTA steals from the back of the range with the most unclaimed stages (at
+    // most OW_STEAL at a time), so CTAs whose contexts cost more per sample (more distinct keys,
+    // more flushes) do not set the kernel time. Any stage is processed by exactly one CTA.
+    unsigned long long* const claim = a.claim;
+    uint64_t c_lo = 0, c_hi = 0;    // claimed, not yet handed out
+    unsigned long long w_pend = 0;  // lane 0: result of the outstanding front claim
+    bool own = true;
+    if (lane == 0) w_pend = atomicAdd(claim + blockIdx.x, (unsigned long long)OW_CLAIM);
+    auto next_stage = [&]() -> uint64_t {
+      if (c_lo < c_hi) return c_lo++;
+      if (own) {
+        const unsigned long long w = __shfl_sync(0xffffffffu, w_pend, 0);
+        const uint64_t lo = s0 + (uint32_t)w, hi_all = s1 - (w >> 32);
+        const uint64_t hi = lo + OW_CLAIM < hi_all ? lo + OW_CLAIM : hi_all;
+        if (lo < hi) {
+          c_lo = lo + 1;
+          c_hi = hi;
+          if (lane == 0) w_pend = atomicAdd(claim + blockIdx.x, (unsigned long long)OW_CLAIM);  // used at the next call
+          return lo;
+        }
+        own = false;
+      }
+      for (uint32_t tries = 0;; ++tries) {
+        if (tries > (1u << 20)) __trap();  // bounded: every failed CAS means another CTA progressed
+        uint64_t best = 0;
+        uint32_t bv = 0;
+        unsigned long long bw = 0;
+        for (uint32_t v = lane; v < G; v += 32) {
+          const unsigned long long w = ld_relaxed_u64(claim + v);
+          const uint64_t lo = ST * v / G + (uint32_t)w, hi = ST * (v + 1) / G - (w >> 32);
+          const uint64_t rem = hi > lo ? hi - lo : 0;
+          if (rem > best) {
+            best = rem;
+            bv = v;
+            bw = w;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          const uint64_t ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const uint32_t ov = __shfl_xor_sync(0xffffffffu, bv, o);
+          const unsigned long long ow = __shfl_xor_sync(0xffffffffu, bw, o);
+          if (ob > best || (ob == best && ov < bv)) {
+            best = ob;
+            bv = ov;
+            bw = ow;
+          }
+        }
+        if (best == 0) return ~0ull;  // nothing left anywhere
+        uint64_t t = (best + 1) / 2;
+        if (t > OW_STEAL) t = OW_STEAL;
+        uint32_t got = 0;
+        if (lane == 0) got = atomicCAS(claim + bv, bw, bw + (t << 32)) == bw;
+        if (__shfl_sync(0xffffffffu, got, 0)) {
+          const uint64_t hi = ST * (bv + 1) / G - (bw >> 32);
+          c_lo = hi - t + 1;
+          c_hi = hi;
+          return hi - t;
+        }
+      }
+    };
+    // software pipeline over the stage stream: stage A is issued now, B's launch fields and C's
+    // first-launch / context words are in flight (one iteration of latency hidden each)
+    uint64_t sA = next_stage(), sB = sA != ~0ull ? next_stage() : ~0ull;
+    uint32_t fA = 0, cA = 0, fB = 0, cB = 0;
+    if (sA != ~0ull) {
+      fA = a.st_first[sA];
+      cA = a.st_ctx[sA];
     }
-    if (s0 + 32 + lane < s1) {
-      nb_first = a.st_first[s0 + 32 + lane];
-      nb_ctx = a.st_ctx[s0 + 32 + lane];
+    if (sB != ~0ull) {
+      fB = a.st_first[sB];
+      cB = a.st_ctx[sB];
     }
-    // launch fields of the next stage to issue
     uint64_t x_rp = ~0ull, x_src = 0, x_cnt = 0;
-    auto load_launch = [&](uint64_t s) {
-      const uint32_t f = __shfl_sync(0xffffffffu, s - bs < 32 ? cb_first : nb_first, (uint32_t)(s - bs) & 31);
+    auto load_launch = [&](uint32_t f) {
       const uint64_t li = (uint64_t)f + lane;
       x_rp = ~0ull;
       if (li < a.n_launch) {
@@ -446,22 +514,25 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) { DC_PDL_
         x_cnt = a.lcnt[li];
       }
     };
-    if (s0 < s1) load_launch(s0);
-    for (uint64_t s = s0; s < s1; ++s) {
+    if (sA != ~0ull) load_launch(fA);
+    while (sA != ~0ull) {
       const long long pc0 = prof ? clock64() : 0;
-      const uint32_t ctx = __shfl_sync(0xffffffffu, s - bs < 32 ? cb_ctx : nb_ctx, (uint32_t)(s - bs) & 31);
-      const uint32_t f = __shfl_sync(0xffffffffu, s - bs < 32 ? cb_first : nb_first, (uint32_t)(s - bs) & 31);
+      const uint64_t s = sA;
+      const uint32_t ctx = cA, f = fA;
       uint64_t rp = x_rp, src = x_src, cnt = x_cnt;
-      if (s + 1 - bs == 32) {  // advance the stage batches (the next one is loaded ahead)
-        bs += 32;
-        cb_first = nb_first;
-        cb_ctx = nb_ctx;
-        if (bs + 32 + lane < s1) {
-          nb_first = a.st_first[bs + 32 + lane];
-          nb_ctx = a.st_ctx[bs + 32 + lane];
-        }
+      const uint64_t sC = sB != ~0ull ? next_stage() : ~0ull;
+      uint32_t fC = 0, cC = 0;
+      if (sC != ~0ull) {
+        fC = a.st_first[sC];
+        cC = a.st_ctx[sC];
       }
-      if (s + 1 < s1) load_launch(s + 1);
+      if (sB != ~0ull) load_launch(fB);
+      sA = sB;
+      fA = fB;
+      cA = cB;
+      sB = sC;
+      fB = fC;
+      cB = cC;
       if (lane == 0) mbar_wait(&sm.empty[st], ph ^ 1u);  // the slot (and its meta) is free
       __syncwarp();
       const long long pc1 = prof ? clock64() : 0;
@@ -1238,6 +1309,7 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
   // rows: sum ceil(cnt/32) <= n/32 + n_launch; context padding < OW_ROWS rows per context (<= n_launch)
   const uint64_t st_cap = (n / 32 + n_launch + OW_ROWS - 1) / OW_ROWS + n_launch + 1;
   const uint64_t row_cap = OW_ROWS * st_cap;
+  if (st_cap >= (1ull << 32)) return DC_OK;  // stage claims count in 32 bits
   {
     Region rp(c, "pc:prep");
     DC_TRY(alloc_zero(c, bad, 1));
@@ -1312,7 +1384,7 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
     DC_TRY(alloc(c, pkey, cap_entries + (uint64_t)G * OW_SPILL_CAP));
     DC_TRY(alloc(c, pcnt, cap_entries + (uint64_t)G * OW_SPILL_CAP));
     DC_TRY(alloc(c, seg, cap_segs));
-    DC_TRY(alloc_zero(c, ctr, 2));
+    DC_TRY(alloc_zero(c, ctr, 2 + (uint64_t)G));  // entry / segment counters + per-CTA stage claims
     DC_TRY(alloc_zero(c, flags, 2));
     DC_TRY(alloc_zero(c, ldiag, DG_N));
     OwnArgs a;
@@ -1342,6 +1414,7 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
     a.probe_mode = 0;
     a.sink = flags.p;
     a.bad = bad.p;
+    a.claim = ctr.p + 2;
     if (const char* pm = getenv("DC_OWN_MODE")) a.probe_mode = (uint32_t)atoi(pm);  // measurement only
     Buf<unsigned long long> dbg;
     if (a.probe_mode == 9 || a.probe_mode == 2) {
