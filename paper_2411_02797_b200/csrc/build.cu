@@ -45,8 +45,10 @@ constexpr int PT_THREADS = 256;
 constexpr int PT_WARPS = PT_THREADS / 32;
 constexpr int PT_RPW = PT_T / PT_WARPS;  // records per warp (16)
 constexpr uint32_t PT_FW = 8192;    // staged frame window per stage (32 KB): 2 CTAs per SM
-constexpr uint32_t PT_CH = 17;      // chunk length (staged tiles; odd: bank spread)
-constexpr uint32_t PT_CH_G = 129;   // chunk length (global tiles)
+// chunk length (odd: bank spread). The same for staged and global tiles: the high half of the
+// hash sums each chunk's high word, so the hash of a path is a function of its frames and of
+// the chunk boundaries — different chunkings would give one path two hashes (two items).
+constexpr uint32_t PT_CH = 17;
 constexpr uint32_t PT_NONE = 0xFFFFFFFFu;
 constexpr int PG_U = 4;             // k_path_group: records verified per round
 
@@ -101,7 +103,7 @@ __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {  // read-
 template <bool STAGED>
 __device__ __forceinline__ void pt_hash_chunks(PathWarp& W, const uint32_t* __restrict__ pos, const uint32_t* __restrict__ src,
                                                uint64_t base, uint32_t n_chunks, uint32_t n_frames, uint32_t& bad) {
-  constexpr uint32_t CH = STAGED ? PT_CH : PT_CH_G;
+  constexpr uint32_t CH = PT_CH;
   for (uint32_t ci = lane_id(); ci < n_chunks; ci += 32) {
     uint32_t k = 0;
 #pragma unroll
@@ -193,7 +195,7 @@ __global__ void __launch_bounds__(PT_THREADS) k_path_hash(const uint64_t* __rest
     const uint32_t mode = sm.meta_mode[s];
     const bool staged = mode & 1;
     const uint64_t F0 = sm.meta_f0[s], F1 = sm.meta_f1[s];
-    const uint32_t ch = staged ? PT_CH : PT_CH_G;
+    const uint32_t ch = PT_CH;
     // ---- this warp's records: bounds, length, chunk starts (warp scan); no block barrier
     const uint32_t i = w * PT_RPW + lane;  // tile-local record of lanes 0..15
     const bool mine = lane < PT_RPW && i < n;
@@ -593,6 +595,172 @@ __global__ void __launch_bounds__(SB_THREADS, 1) k_build_small(const uint64_t* _
   if (threadIdx.x == 0) {
     d_N[0] = next;
     d_N[1] = d;  // levels built = depth of the tree
+  }
+}
+
+// ------------------------------------------------------------------ a3: small P, no level loop
+// The canonical order is the lexicographic order of the prefixes: node (depth d) ids follow
+// (parent id, frame), so by induction the depth-d nodes are the distinct d-prefixes in lex
+// order. Sorting the P distinct paths lexicographically therefore orders every level at once:
+// with the paths sorted and LCP[k] = lcp(path[k-1], path[k]), sorted path k creates exactly the
+// nodes of depths LCP[k]+1 .. len[k] (a shorter path cannot sit between two paths sharing a
+// d-prefix, because the paths with a given prefix are contiguous in lex order), so
+//   level_off[d] = 1 + sum_k max(0, min(len_k, d-1) - LCP_k),
+//   id(k, d)     = level_off[d] + #{k' <= k : LCP_k' < d <= len_k'} - 1,
+// and the parent of (k, d) is (k, d-1) by the same count at depth d-1. Two launches replace
+// the one-CTA level loop (k_build_small): a rank kernel (all pairwise path comparisons, the
+// paths staged in shared memory in 16-B chunks; LCP with the predecessor = the largest LCP over
+// the smaller paths) and one CTA per depth that numbers and writes that level.
+constexpr int SR_THREADS = 512;
+__device__ __forceinline__ void sr_block_sum_max(uint32_t& sum, uint32_t& mx) {
+  __shared__ uint32_t s_sum[SR_THREADS / 32], s_max[SR_THREADS / 32];
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  sum = __reduce_add_sync(0xffffffffu, sum);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if (lane == 0) {
+    s_sum[w] = sum;
+    s_max[w] = mx;
+  }
+  __syncthreads();
+  sum = 0;
+  mx = 0;
+  for (int i = 0; i < SR_THREADS / 32; ++i) {
+    sum += s_sum[i];
+    mx = max(mx, s_max[i]);
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(SR_THREADS, 1) k_small_rank(const uint64_t* __restrict__ off, const uint32_t* __restrict__ frames,
+                                                               const uint32_t* __restrict__ item_rec, const uint32_t* __restrict__ item_len,
+                                                               uint32_t P, uint32_t* __restrict__ sorted_item, uint32_t* __restrict__ lcp_s,
+                                                               uint32_t* __restrict__ len_s, uint32_t* __restrict__ leaf_of_item) { DC_PDL_ENTER();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* sstart = reinterpret_cast<uint32_t*>(smem_raw);  // [P] first 16-B chunk of path i
+  uint32_t* slen = sstart + P;                               // [P]
+  uint4* chunks = reinterpret_cast<uint4*>(smem_raw + ((8ull * P + 15) & ~15ull));
+  uint32_t* fr = reinterpret_cast<uint32_t*>(chunks);
+  // chunk starts: exclusive scan of ceil(len / 4)
+  uint32_t run = 0;
+  for (uint32_t base = 0; base < P; base += SR_THREADS) {
+    const uint32_t i = base + threadIdx.x;
+    const uint32_t L = i < P ? item_len[i] : 0u;
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan<uint32_t, SR_THREADS>((L + 3) / 4, &tot);
+    if (i < P) {
+      sstart[i] = run + ex;
+      slen[i] = L;
+    }
+    run += tot;
+  }
+  __syncthreads();
+  // stage the frames (warp per path; the pad of the last chunk is never compared)
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (uint32_t i = w; i < P; i += SR_THREADS / 32) {
+    const uint32_t L = slen[i];
+    const uint64_t o = off[item_rec[i]];
+    uint32_t* dst = fr + 4ull * sstart[i];
+    for (uint32_t m = lane; m < L; m += 32) dst[m] = frames[o + m];
+  }
+  __syncthreads();
+  for (uint32_t i = blockIdx.x; i < P; i += gridDim.x) {
+    const uint32_t Li = slen[i];
+    const uint4* A = chunks + sstart[i];
+    const uint32_t* a = fr + 4ull * sstart[i];
+    uint32_t rank = 0, mlcp = 0;
+    for (uint32_t j = threadIdx.x; j < P; j += SR_THREADS) {
+      const uint32_t Lj = slen[j];
+      const uint4* B = chunks + sstart[j];
+      const uint32_t* b = fr + 4ull * sstart[j];
+      const uint32_t lim = min(Li, Lj);
+      uint32_t c = 0;
+      while (4 * c + 4 <= lim) {
+        const uint4 x = A[c], y = B[c];
+        if ((x.x != y.x) | (x.y != y.y) | (x.z != y.z) | (x.w != y.w)) break;
+        ++c;
+      }
+      uint32_t m = 4 * c;
+      while (m < lim && a[m] == b[m]) ++m;
+      // path j < path i; equal paths (possible among collision extras) are ordered by index
+      const bool less = m < lim ? b[m] < a[m] : (Lj < Li || (Lj == Li && j < i));
+      if (less) {
+        ++rank;
+        mlcp = max(mlcp, m);
+      }
+    }
+    sr_block_sum_max(rank, mlcp);
+    if (threadIdx.x == 0) {
+      sorted_item[rank] = i;
+      lcp_s[rank] = mlcp;  // the predecessor in lex order shares the longest prefix
+      len_s[rank] = Li;
+      if (Li == 0) leaf_of_item[i] = 0;  // empty path -> root
+    }
+  }
+}
+
+// one CTA per depth d = blockIdx.x + 1 (d = Lmax + 1 only writes level_off[Lmax + 1] = N)
+__global__ void __launch_bounds__(SR_THREADS) k_small_emit(const uint64_t* __restrict__ off, const uint32_t* __restrict__ frames,
+                                                            const uint32_t* __restrict__ item_rec, uint32_t P,
+                                                            const uint32_t* __restrict__ sorted_item, const uint32_t* __restrict__ lcp_s,
+                                                            const uint32_t* __restrict__ len_s, uint32_t Lmax, uint32_t* __restrict__ parent,
+                                                            uint32_t* __restrict__ frame_out, uint16_t* __restrict__ depth,
+                                                            uint32_t* __restrict__ level_off, uint32_t* __restrict__ leaf_of_item,
+                                                            uint32_t* d_N) { DC_PDL_ENTER();
+  const uint32_t d = blockIdx.x + 1;
+  // nodes above depth d and above depth d - 1 (level_off[d] - 1, level_off[d-1] - 1)
+  uint32_t above = 0, above_p = 0, maxlen = 0, dups = 0;
+  for (uint32_t k = threadIdx.x; k < P; k += SR_THREADS) {
+    const uint32_t L = len_s[k], g = lcp_s[k];
+    dups += (L > 0 && g >= L) ? 1u : 0u;
+    const uint32_t t1 = min(L, d - 1), t2 = d >= 2 ? min(L, d - 2) : 0u;
+    above += t1 > g ? t1 - g : 0u;
+    above_p += t2 > g ? t2 - g : 0u;
+    maxlen = max(maxlen, L);
+  }
+  uint32_t dummy = 0;
+  sr_block_sum_max(above, maxlen);
+  sr_block_sum_max(above_p, dummy);
+  sr_block_sum_max(dups, dummy);
+  const uint32_t lo = 1 + above, lo_p = 1 + above_p;
+  if (threadIdx.x == 0) {
+    level_off[d] = lo;
+    if (d == 1) {
+      level_off[0] = 0;
+      parent[0] = DC_NO_NODE;
+      frame_out[0] = DC_NO_NODE;
+      depth[0] = 0;
+    }
+    if (d == Lmax + 1) {
+      d_N[0] = lo;       // N
+      d_N[1] = maxlen;   // depth of the tree
+      d_N[2] = dups;     // items repeating another item's path (0 unless the dedup split a path)
+    }
+  }
+  if (d > Lmax) return;
+  uint32_t run = 0;  // (count at d << 16 | count at d - 1) before this chunk; P <= 4096 < 2^16
+  for (uint32_t base = 0; base < P; base += SR_THREADS) {
+    const uint32_t k = base + threadIdx.x;
+    uint32_t fd = 0, fp = 0;
+    uint32_t L = 0;
+    if (k < P) {
+      L = len_s[k];
+      const uint32_t g = lcp_s[k];
+      fd = (g < d && d <= L) ? 1u : 0u;
+      fp = (d >= 2 && g < d - 1 && d - 1 <= L) ? 1u : 0u;
+    }
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan<uint32_t, SR_THREADS>((fd << 16) | fp, &tot);
+    const uint32_t inc = run + ex + (fd << 16) + fp;
+    const uint32_t id = lo + (inc >> 16) - 1;  // the depth-d node on path k (created by k or before)
+    if (fd) {
+      parent[id] = d == 1 ? 0u : lo_p + (inc & 0xFFFFu) - 1;
+      frame_out[id] = frames[off[item_rec[sorted_item[k]]] + d - 1];
+      depth[id] = (uint16_t)d;
+    }
+    // a path equal to its predecessor (an item the exact dedup split off after a hash collision
+    // may repeat another item's path) creates no node; its leaf is the predecessor's
+    if (k < P && L == d) leaf_of_item[sorted_item[k]] = id;
+    run += tot;
   }
 }
 
@@ -1119,7 +1287,32 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
   DC_TRY(palloc(c, t->level_off, (uint64_t)Lmax + 2));
   uint64_t N = 0;
   uint32_t levels = 0;
-  if (P <= SMALL_P) {
+  const uint64_t rank_smem = ((8ull * P + 15) & ~15ull) + 4ull * (hsum + 3ull * P);
+  if (P <= SMALL_P && rank_smem + 1024 <= c->smem_optin && !getenv("DC_TEST_BUILD_LEVELS")) {
+    // lexicographic rank of the distinct paths + one CTA per depth (no level loop)
+    Buf<uint32_t> dN, srt, lcp, len;
+    DC_TRY(alloc(c, dN, 3));
+    DC_TRY(alloc(c, srt, P));
+    DC_TRY(alloc(c, lcp, P));
+    DC_TRY(alloc(c, len, P));
+    DC_CUDA(c, cudaFuncSetAttribute(k_small_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rank_smem));
+    const uint32_t G = P == 0 ? 1u : P < (uint32_t)c->num_sms ? P : (uint32_t)c->num_sms;
+    dc_launch(k_small_rank, G, SR_THREADS, rank_smem, c->stream, p->offsets, p->frames, item_rec.p, item_len.p, P, srt.p, lcp.p,
+              len.p, leaf_of_item.p);
+    DC_LAUNCHED(c);
+    dc_launch(k_small_emit, Lmax + 1, SR_THREADS, 0, c->stream, p->offsets, p->frames, item_rec.p, P, srt.p, lcp.p, len.p, Lmax,
+              t->parent, t->frame, t->depth, t->level_off, leaf_of_item.p, dN.p);
+    DC_LAUNCHED(c);
+    uint32_t hN[3] = {0, 0, 0};
+    DC_TRY(readback(c, dN.p, 12, hN));
+    N = hN[0];
+    t->max_depth = hN[1];
+    // distinct table slots must hold distinct paths (the tree is right either way: equal paths
+    // share their nodes); DC_STRICT=1 (the test suite) turns a lost dedup into an error;
+    // collision extras may repeat each other's path, table items never do
+    if (hN[2] > n_extra && getenv("DC_STRICT"))
+      return fail(c, DC_ERR_STATE, "internal: %u of %u path items repeat a path (%u collision extras)", hN[2], P, n_extra);
+  } else if (P <= SMALL_P) {
     Buf<uint32_t> dN;
     DC_TRY(alloc(c, dN, 2));
     size_t smem = sizeof(SmallSmem);

@@ -7,6 +7,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 TESTS = os.path.dirname(os.path.abspath(__file__))
+# library self-checks of internal invariants (e.g. the path dedup) are errors under test
+os.environ.setdefault("DC_STRICT", "1")
 if TESTS not in sys.path:
     sys.path.insert(0, TESTS)
 

@@ -73,5 +73,8 @@ def assert_same(got: dict, ref: dict, keys=CMP_KEYS, ctx=""):
         if not np.array_equal(g, r):
             bad = np.argwhere(g != r)[:5]
             raise AssertionError(f"{ctx}: {k} differs at {bad.tolist()}: got {g[tuple(bad[0])]} ref {r[tuple(bad[0])]}")
+    if "level_off" in got:  # level_off[d] = first node of depth >= d (depth is non-decreasing)
+        dep, lo = np.asarray(got["depth"]), np.asarray(got["level_off"])
+        assert np.array_equal(lo, np.searchsorted(dep, np.arange(len(lo)), side="left")), f"{ctx}: level_off"
     if "leaf" in ref and ref["leaf"] is not None and "leaf" in got:
         assert np.array_equal(got["leaf"], ref["leaf"]), f"{ctx}: leaf differs"

@@ -86,6 +86,8 @@ def _rand_trace(rng, R_max=300, A_max=40):
 def test_random_traces_vs_oracle(seed, monkeypatch):
     if seed % 2:  # odd seeds: the level-synchronous rollup (cooperative kernel) on small trees
         monkeypatch.setenv("DC_TEST_ROLLUP_LEVELS", "1")
+    if seed >= 4:  # the one-CTA level loop instead of the lexicographic-rank build
+        monkeypatch.setenv("DC_TEST_BUILD_LEVELS", "1")
     rng = np.random.default_rng(500 + seed)
     import paper_2411_02797_b200 as dc
     ctx = dc.Context(0)
@@ -179,6 +181,67 @@ def test_owner_high_cardinality_flush_spill_and_wrap(n, npc, big):
     a = gpu_run(off, fr, X, n_frames=2, samples=s, launch_off=lo, n_stall=24)
     ref = oracle_run(off, fr, X, 1, s, 1, 24).arrays()
     assert_same(a, ref, ctx=f"owner n={n} npc={npc}")
+
+
+@pytest.mark.parametrize("n_launch,heavy", [(3, 1), (300, 40), (2000, 5)])
+def test_owner_work_stealing_skewed_contexts(n_launch, heavy):
+    """Stage ranges of very unequal cost: a few launches carry most samples with many distinct
+    keys (flushes), the rest are light; with 3 launches most CTAs start with an empty range and
+    only steal. Every stage must be aggregated exactly once: oracle and generic schedule agree."""
+    rng = np.random.default_rng(n_launch)
+    paths = [(0, 1), (0, 2), (1, 3), (1, 2, 4), (3,), (0, 1, 2, 3)]
+    off, fr = _csr([paths[i % len(paths)] for i in range(n_launch)])  # launch i = record i
+    X = np.ones((1, n_launch), np.uint64)
+    cnt = rng.integers(1, 300, n_launch)
+    cnt[:heavy] = rng.integers(100_000, 400_000, heavy)
+    lo = np.zeros(n_launch + 1, np.uint64)
+    lo[1:] = np.cumsum(cnt)
+    n = int(lo[-1])
+    s = np.zeros(n, oracle.SAMPLE_DTYPE)
+    s["launch"] = np.repeat(np.arange(n_launch, dtype=np.uint32), cnt)
+    heavy_s = s["launch"] < heavy
+    s["pc_off"] = np.where(heavy_s, 16 * rng.integers(0, 30_000, n), 16 * rng.integers(0, 50, n))
+    s["stall"] = rng.integers(0, 24, n)
+    s["count"] = 1
+    kw = dict(n_frames=5, samples=s, n_stall=24)
+    a = gpu_run(off, fr, X, launch_off=lo, **kw)
+    b = gpu_run(off, fr, X, launch_off=None, **kw)
+    assert_same(a, b, ctx="owner vs generic (skewed)")
+    ref = oracle_run(off, fr, X, 1, s, n_launch, 24).arrays()
+    assert_same(a, ref, ctx=f"owner skewed n_launch={n_launch}")
+
+
+@pytest.mark.parametrize("levels", [False, True])
+def test_small_build_deep_and_prefix_paths(levels, monkeypatch):
+    """Small-P build at the depth limit: chains up to 1000 frames, paths that are prefixes of
+    other paths, shared deep prefixes that branch late, an empty path; both small-P builders."""
+    if levels:
+        monkeypatch.setenv("DC_TEST_BUILD_LEVELS", "1")
+    rng = np.random.default_rng(77)
+    base = [int(x) for x in rng.integers(0, 40, 1000)]
+    paths = [tuple(base), tuple(base[:500]), tuple(base[:499] + [41]), tuple(base[:999] + [0]), (), tuple(base[:1]),
+             tuple(base[:3] + [7, 7, 7]), (5,), (5, 5), tuple(base[:700] + [3] * 50)]
+    paths += [tuple(base[: int(rng.integers(1, 1000))]) + tuple(int(x) for x in rng.integers(0, 42, 3)) for _ in range(60)]
+    off, fr = _csr(paths)
+    X = rng.integers(0, 1000, size=(1, len(paths)), dtype=np.uint64)
+    a = gpu_run(off, fr, X, n_frames=42)
+    ref = oracle_run(off, fr, X, 1).arrays()
+    assert_same(a, ref, ctx=f"deep small build levels={levels}")
+
+
+def test_dedup_independent_of_tile_staging():
+    """One path hashed in a tile whose frames are staged in shared memory and in a tile read from
+    global memory (frames > the staging window) must give one item: with DC_STRICT=1 (conftest)
+    a repeated table item is an error, and the tree must equal the oracle's."""
+    rng = np.random.default_rng(3)
+    X = tuple(int(x) for x in rng.integers(0, 50, 40))
+    deep = [tuple(int(x) for x in rng.integers(0, 50, 100)) for _ in range(127)]
+    paths = deep + [X] + [X] * 128 + [X[:20], X] * 100  # tile 0: 12,740 frames (global), tile 1: staged
+    off, fr = _csr(paths)
+    M = np.ones((1, len(paths)), np.uint64)
+    a = gpu_run(off, fr, M, n_frames=50)
+    ref = oracle_run(off, fr, M, 1).arrays()
+    assert_same(a, ref, ctx="dedup across staged / global tiles")
 
 
 def test_edge_cases():
