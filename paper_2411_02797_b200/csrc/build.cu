@@ -634,17 +634,20 @@ __device__ __forceinline__ void sr_block_sum_max(uint32_t& sum, uint32_t& mx) {
 __global__ void __launch_bounds__(SR_THREADS, 1) k_small_rank(const uint64_t* __restrict__ off, const uint32_t* __restrict__ frames,
                                                                const uint32_t* __restrict__ item_rec, const uint32_t* __restrict__ item_len,
                                                                uint32_t P, uint32_t* __restrict__ sorted_item, uint32_t* __restrict__ lcp_s,
-                                                               uint32_t* __restrict__ len_s, uint32_t* __restrict__ leaf_of_item) { DC_PDL_ENTER();
+                                                               uint32_t* __restrict__ len_s, uint64_t* __restrict__ po_s,
+                                                               uint32_t* __restrict__ leaf_of_item) { DC_PDL_ENTER();
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint32_t* sstart = reinterpret_cast<uint32_t*>(smem_raw);  // [P] first 16-B chunk of path i
+  uint64_t* spo = reinterpret_cast<uint64_t*>(smem_raw);     // [P] first frame of path i (global)
+  uint32_t* sstart = reinterpret_cast<uint32_t*>(spo + P);   // [P] first 16-B chunk of path i
   uint32_t* slen = sstart + P;                               // [P]
-  uint4* chunks = reinterpret_cast<uint4*>(smem_raw + ((8ull * P + 15) & ~15ull));
+  uint4* chunks = reinterpret_cast<uint4*>(smem_raw + ((16ull * P + 15) & ~15ull));
   uint32_t* fr = reinterpret_cast<uint32_t*>(chunks);
-  // chunk starts: exclusive scan of ceil(len / 4)
+  // chunk starts: exclusive scan of ceil(len / 4); path offsets (loads of all items in flight)
   uint32_t run = 0;
   for (uint32_t base = 0; base < P; base += SR_THREADS) {
     const uint32_t i = base + threadIdx.x;
     const uint32_t L = i < P ? item_len[i] : 0u;
+    if (i < P) spo[i] = off[item_rec[i]];
     uint32_t tot;
     const uint32_t ex = block_excl_scan<uint32_t, SR_THREADS>((L + 3) / 4, &tot);
     if (i < P) {
@@ -654,13 +657,35 @@ __global__ void __launch_bounds__(SR_THREADS, 1) k_small_rank(const uint64_t* __
     run += tot;
   }
   __syncthreads();
-  // stage the frames (warp per path; the pad of the last chunk is never compared)
-  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (uint32_t i = w; i < P; i += SR_THREADS / 32) {
-    const uint32_t L = slen[i];
-    const uint64_t o = off[item_rec[i]];
-    uint32_t* dst = fr + 4ull * sstart[i];
-    for (uint32_t m = lane; m < L; m += 32) dst[m] = frames[o + m];
+  // stage the frames, one 16-B chunk per thread and step (the path found by binary search over
+  // the chunk starts); 4 chunks per thread in flight. The pad of a last chunk is never compared.
+  const uint32_t C = run;
+  for (uint32_t q0 = threadIdx.x; q0 < C; q0 += 4 * SR_THREADS) {
+    uint4 v[4];
+    uint32_t qq[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t q = q0 + u * SR_THREADS;
+      qq[u] = q;
+      v[u] = make_uint4(0, 0, 0, 0);
+      if (q < C) {
+        uint32_t lo = 0, hi = P;  // last i with sstart[i] <= q (an empty path shares its start)
+        while (hi - lo > 1) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (sstart[mid] <= q) lo = mid;
+          else hi = mid;
+        }
+        const uint32_t m = 4 * (q - sstart[lo]), L = slen[lo];
+        const uint32_t* src = frames + spo[lo] + m;
+        v[u].x = src[0];
+        if (m + 1 < L) v[u].y = src[1];
+        if (m + 2 < L) v[u].z = src[2];
+        if (m + 3 < L) v[u].w = src[3];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (qq[u] < C) chunks[qq[u]] = v[u];
   }
   __syncthreads();
   for (uint32_t i = blockIdx.x; i < P; i += gridDim.x) {
@@ -693,14 +718,15 @@ __global__ void __launch_bounds__(SR_THREADS, 1) k_small_rank(const uint64_t* __
       sorted_item[rank] = i;
       lcp_s[rank] = mlcp;  // the predecessor in lex order shares the longest prefix
       len_s[rank] = Li;
+      po_s[rank] = spo[i];
       if (Li == 0) leaf_of_item[i] = 0;  // empty path -> root
     }
   }
 }
 
 // one CTA per depth d = blockIdx.x + 1 (d = Lmax + 1 only writes level_off[Lmax + 1] = N)
-__global__ void __launch_bounds__(SR_THREADS) k_small_emit(const uint64_t* __restrict__ off, const uint32_t* __restrict__ frames,
-                                                            const uint32_t* __restrict__ item_rec, uint32_t P,
+__global__ void __launch_bounds__(SR_THREADS) k_small_emit(const uint64_t* __restrict__ po_s, const uint32_t* __restrict__ frames,
+                                                            uint32_t P,
                                                             const uint32_t* __restrict__ sorted_item, const uint32_t* __restrict__ lcp_s,
                                                             const uint32_t* __restrict__ len_s, uint32_t Lmax, uint32_t* __restrict__ parent,
                                                             uint32_t* __restrict__ frame_out, uint16_t* __restrict__ depth,
@@ -754,7 +780,7 @@ __global__ void __launch_bounds__(SR_THREADS) k_small_emit(const uint64_t* __res
     const uint32_t id = lo + (inc >> 16) - 1;  // the depth-d node on path k (created by k or before)
     if (fd) {
       parent[id] = d == 1 ? 0u : lo_p + (inc & 0xFFFFu) - 1;
-      frame_out[id] = frames[off[item_rec[sorted_item[k]]] + d - 1];
+      frame_out[id] = frames[po_s[k] + d - 1];
       depth[id] = (uint16_t)d;
     }
     // a path equal to its predecessor (an item the exact dedup split off after a hash collision
@@ -1287,20 +1313,22 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
   DC_TRY(palloc(c, t->level_off, (uint64_t)Lmax + 2));
   uint64_t N = 0;
   uint32_t levels = 0;
-  const uint64_t rank_smem = ((8ull * P + 15) & ~15ull) + 4ull * (hsum + 3ull * P);
+  const uint64_t rank_smem = ((16ull * P + 15) & ~15ull) + 4ull * (hsum + 3ull * P);
   if (P <= SMALL_P && rank_smem + 1024 <= c->smem_optin && !getenv("DC_TEST_BUILD_LEVELS")) {
     // lexicographic rank of the distinct paths + one CTA per depth (no level loop)
     Buf<uint32_t> dN, srt, lcp, len;
+    Buf<uint64_t> pos;
     DC_TRY(alloc(c, dN, 3));
+    DC_TRY(alloc(c, pos, P));
     DC_TRY(alloc(c, srt, P));
     DC_TRY(alloc(c, lcp, P));
     DC_TRY(alloc(c, len, P));
     DC_CUDA(c, cudaFuncSetAttribute(k_small_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rank_smem));
     const uint32_t G = P == 0 ? 1u : P < (uint32_t)c->num_sms ? P : (uint32_t)c->num_sms;
     dc_launch(k_small_rank, G, SR_THREADS, rank_smem, c->stream, p->offsets, p->frames, item_rec.p, item_len.p, P, srt.p, lcp.p,
-              len.p, leaf_of_item.p);
+              len.p, pos.p, leaf_of_item.p);
     DC_LAUNCHED(c);
-    dc_launch(k_small_emit, Lmax + 1, SR_THREADS, 0, c->stream, p->offsets, p->frames, item_rec.p, P, srt.p, lcp.p, len.p, Lmax,
+    dc_launch(k_small_emit, Lmax + 1, SR_THREADS, 0, c->stream, pos.p, p->frames, P, srt.p, lcp.p, len.p, Lmax,
               t->parent, t->frame, t->depth, t->level_off, leaf_of_item.p, dN.p);
     DC_LAUNCHED(c);
     uint32_t hN[3] = {0, 0, 0};
