@@ -233,13 +233,16 @@ __device__ __forceinline__ void own_flush(OwnSmem& sm, const OwnArgs& a, uint32_
       }
     }
     sm.seg_base = base;
-    if (sm.spill_n > sm.spill_seg) {  // spilled entries of this context form their own segment
-      const uint32_t ns = min(sm.spill_n, OW_SPILL_CAP) - sm.spill_seg;
+    // spilled entries of this context form their own segment; spill_n keeps counting past the
+    // region (overflow: flagged, generic schedule) but a segment never reaches beyond it
+    const uint32_t sp_hi = min(sm.spill_n, OW_SPILL_CAP);
+    if (sp_hi > sm.spill_seg) {
+      const uint32_t ns = sp_hi - sm.spill_seg;
       const uint64_t sb = a.spill_base0 + (uint64_t)blockIdx.x * OW_SPILL_CAP + sm.spill_seg;
       const unsigned si2 = atomicAdd(a.g_segs, 1u);
       if (si2 < a.cap_segs) a.seg[si2] = make_uint4(ctx, ns, (uint32_t)sb, (uint32_t)(sb >> 32));
       else atomicOr(a.g_flags, (uint32_t)OWF_OVERFLOW);
-      sm.spill_seg = sm.spill_n;
+      sm.spill_seg = sp_hi;
     }
   }
   constexpr uint32_t PER_WARP = (OW_TAB / 32 + OW_CONS_WARPS - 1) / OW_CONS_WARPS * 32;  // 416 slots, multiple of 32
@@ -794,8 +797,10 @@ constexpr uint32_t BR_MAXCH = ((OW_TAB > (int)OW_SPILL_CAP ? OW_TAB : OW_SPILL_C
 
 // runs before the host has read the segment count: it takes the device counter (clamped)
 __global__ void k_br_range(const uint4* __restrict__ seg, const unsigned int* __restrict__ d_nsegs, uint32_t cap_segs,
-                           const uint32_t* __restrict__ pkey, uint64_t N, uint32_t* __restrict__ cmax, uint32_t* __restrict__ cor) { DC_PDL_ENTER();
+                           const uint32_t* __restrict__ pkey, uint64_t N, uint32_t* __restrict__ cmax, uint32_t* __restrict__ cor,
+                           const uint32_t* __restrict__ g_flags) { DC_PDL_ENTER();
   const uint32_t lane = threadIdx.x & 31;
+  if (*g_flags) return;  // fallback / overflow: the host reruns the generic schedule
   const uint32_t n_segs = min(*d_nsegs, cap_segs);
   BR_FOR_CHUNKS(seg, n_segs, N) {
     const uint64_t base = (uint64_t)sg.z | ((uint64_t)sg.w << 32);
@@ -1467,7 +1472,7 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
     {
       Region rk(c, "k:br_range");
       dc_launch(k_br_range, grid_for(c, (uint64_t)cap_segs * BR_MAXCH * 32, 256), 256, 0, c->stream, seg.p, a.g_segs, cap_segs, pkey.p,
-                                                                                            N, cm.p, cm.p + N);
+                N, cm.p, cm.p + N, flags.p);
       DC_LAUNCHED(c);
     }
     {
