@@ -43,7 +43,8 @@ constexpr int OW_PEND = OW_ROUND + 32;        // per-warp queue of missed keys (
 constexpr uint32_t OW_FLUSH_REQ = OW_TAB * 2 / 3;
 constexpr uint32_t OW_SPILL_AT = OW_TAB - OW_CONS_WARPS * OW_PEND - 1;
 constexpr uint32_t OW_MISS = 0xFFFFFFFEu;
-constexpr uint32_t OW_SPILL_CAP = 16384;      // spill entries per CTA
+constexpr uint32_t OW_SPILL_CAP = 4096;       // spill chunk (entries); the first per CTA is preallocated
+constexpr uint32_t OW_SP_RING = 8;            // spill chunk bases kept (by generation)
 constexpr uint32_t OW_CLAIM = 4;              // stages claimed from the own range at a time
 constexpr uint32_t OW_STEAL = 8;              // at most this many stages stolen at a time
 constexpr uint32_t EMPTY32 = 0xFFFFFFFFu;
@@ -67,7 +68,10 @@ struct OwnSmem {
   OwMeta meta[OW_STAGES];
   uint32_t distinct;
   uint32_t flush_req;
-  uint32_t spill_n, spill_seg;  // spill entries written / already covered by a segment
+  // spill allocator: word = generation << 20 | entries taken in the generation's chunk; a full
+  // chunk is closed as a segment and replaced by one from the global entry pool (sp_lock)
+  uint32_t sp_word, sp_seg, sp_lock;  // sp_seg: entries of the current chunk already in a segment
+  unsigned long long sp_base[OW_SP_RING];
   uint32_t warp_cnt[OW_CONS_WARPS];
   unsigned long long seg_base;
 };
@@ -233,16 +237,15 @@ __device__ __forceinline__ void own_flush(OwnSmem& sm, const OwnArgs& a, uint32_
       }
     }
     sm.seg_base = base;
-    // spilled entries of this context form their own segment; spill_n keeps counting past the
-    // region (overflow: flagged, generic schedule) but a segment never reaches beyond it
-    const uint32_t sp_hi = min(sm.spill_n, OW_SPILL_CAP);
-    if (sp_hi > sm.spill_seg) {
-      const uint32_t ns = sp_hi - sm.spill_seg;
-      const uint64_t sb = a.spill_base0 + (uint64_t)blockIdx.x * OW_SPILL_CAP + sm.spill_seg;
+    // this context's entries of the current spill chunk form their own segment
+    const uint32_t wv = *(volatile uint32_t*)&sm.sp_word;
+    const uint32_t sp_hi = min(wv & 0xFFFFFu, OW_SPILL_CAP);
+    if (sp_hi > sm.sp_seg) {
+      const uint64_t sb = sm.sp_base[(wv >> 20) % OW_SP_RING] + sm.sp_seg;
       const unsigned si2 = atomicAdd(a.g_segs, 1u);
-      if (si2 < a.cap_segs) a.seg[si2] = make_uint4(ctx, ns, (uint32_t)sb, (uint32_t)(sb >> 32));
+      if (si2 < a.cap_segs) a.seg[si2] = make_uint4(ctx, sp_hi - sm.sp_seg, (uint32_t)sb, (uint32_t)(sb >> 32));
       else atomicOr(a.g_flags, (uint32_t)OWF_OVERFLOW);
-      sm.spill_seg = sp_hi;
+      sm.sp_seg = sp_hi;
     }
   }
   constexpr uint32_t PER_WARP = (OW_TAB / 32 + OW_CONS_WARPS - 1) / OW_CONS_WARPS * 32;  // 416 slots, multiple of 32
@@ -324,34 +327,58 @@ __device__ __noinline__ uint32_t own_probe(OwnSmem& sm, uint32_t key, uint32_t b
   }
 }
 
-__device__ __forceinline__ void own_add(OwnSmem& sm, const OwnArgs& a, uint32_t key, uint32_t h, uint32_t add, uint32_t ctx) {
-  if (h == (uint32_t)OW_TAB) {  // spill: one partial entry in this CTA's region
-    const uint32_t i = atomicAdd(&sm.spill_n, 1u);
+// One exact partial entry outside the table (table full, or a sample whose count is not 1).
+// Entries go to the CTA's current spill chunk; the thread that finds the chunk full (and wins
+// sp_lock) closes it as a segment of the current context (all consumers are in one context
+// between flushes), takes a fresh chunk from the global entry pool and opens the next
+// generation; the others wait for it and retry. Entries never exceed the samples, so the pool
+// (n + 1 + one chunk per CTA) cannot run out.
+__device__ __noinline__ void own_spill(OwnSmem& sm, const OwnArgs& a, uint32_t key, uint32_t count, uint32_t ctx) {
+  for (uint32_t spin = 0;; ++spin) {
+    if (spin > DC_SPIN_LIMIT) __trap();
+    const uint32_t wv = atomicAdd(&sm.sp_word, 1u);
+    const uint32_t gen = wv >> 20, i = wv & 0xFFFFFu;
     if (i < OW_SPILL_CAP) {
-      const uint64_t o = a.spill_base0 + (uint64_t)blockIdx.x * OW_SPILL_CAP + i;
+      const uint64_t o = *(volatile unsigned long long*)&sm.sp_base[gen % OW_SP_RING] + i;
       a.pkey[o] = key;
-      a.pcnt[o] = add;
-    } else {
-      atomicOr(a.g_flags, (uint32_t)OWF_OVERFLOW);
+      a.pcnt[o] = count;
+      return;
     }
+    if (atomicCAS(&sm.sp_lock, 0u, 1u) == 0u) {
+      if ((*(volatile uint32_t*)&sm.sp_word >> 20) == gen) {  // nobody replaced the chunk yet
+        const uint64_t cb = sm.sp_base[gen % OW_SP_RING];
+        if (OW_SPILL_CAP > sm.sp_seg) {
+          const uint64_t sb = cb + sm.sp_seg;
+          const unsigned si = atomicAdd(a.g_segs, 1u);
+          if (si < a.cap_segs) a.seg[si] = make_uint4(ctx, OW_SPILL_CAP - sm.sp_seg, (uint32_t)sb, (uint32_t)(sb >> 32));
+          else atomicOr(a.g_flags, (uint32_t)OWF_OVERFLOW);
+        }
+        const unsigned long long nb = atomicAdd(a.g_entries, (unsigned long long)OW_SPILL_CAP);
+        if (nb + OW_SPILL_CAP > a.cap_entries) atomicOr(a.g_flags, (uint32_t)OWF_OVERFLOW);  // cannot happen
+        *(volatile unsigned long long*)&sm.sp_base[(gen + 1) % OW_SP_RING] =
+            nb + OW_SPILL_CAP > a.cap_entries ? a.spill_base0 + (uint64_t)blockIdx.x * OW_SPILL_CAP : nb;
+        *(volatile uint32_t*)&sm.sp_seg = 0;
+        __threadfence_block();
+        atomicExch(&sm.sp_word, ((gen + 1) & 0xFFFu) << 20);
+      }
+      __threadfence_block();
+      atomicExch(&sm.sp_lock, 0u);
+    } else {
+      while ((*(volatile uint32_t*)&sm.sp_word >> 20) == gen && (*(volatile uint32_t*)&sm.sp_word & 0xFFFFFu) >= OW_SPILL_CAP) {
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void own_add(OwnSmem& sm, const OwnArgs& a, uint32_t key, uint32_t h, uint32_t add, uint32_t ctx) {
+  if (h == (uint32_t)OW_TAB) {  // table full: one exact partial entry in the spill chunk
+    own_spill(sm, a, key, add, ctx);
     return;
   }
   // Fire-and-forget shared reduction. Only samples with count == 1 reach the table (others
-  // go to the spill region), so a counter gains at most one per sample of the CTA's range
-  // between flushes and can never wrap: the range is < 2^32 samples.
+  // go to the spill region), so a counter gains at most one per sample of the CTA between
+  // flushes and cannot wrap below 2^32 samples per CTA.
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(smem_u32(&sm.cnt[h])), "r"(add) : "memory");
-}
-
-// a sample whose count is not 1 is kept exactly as its own partial entry (HBM), not in the table
-__device__ __forceinline__ void own_spill(OwnSmem& sm, const OwnArgs& a, uint32_t key, uint32_t count) {
-  const uint32_t i = atomicAdd(&sm.spill_n, 1u);
-  if (i < OW_SPILL_CAP) {
-    const uint64_t o = a.spill_base0 + (uint64_t)blockIdx.x * OW_SPILL_CAP + i;
-    a.pkey[o] = key;
-    a.pcnt[o] = count;
-  } else {
-    atomicOr(a.g_flags, (uint32_t)OWF_OVERFLOW);
-  }
 }
 
 struct OwCounters {
@@ -381,11 +408,11 @@ __device__ __forceinline__ bool own_hot(const uint4 q, uint32_t row_launch, uint
   return (q.x == row_launch) & ((q.z & 0xFFFFu) < S) & (q.w == 1u) & (q.y < (1u << 27) - 1u);
 }
 __device__ __noinline__ void own_cold(const uint4 q, uint32_t seg_launch, const OwnArgs& a, bool ctx_ok, OwCounters& k,
-                                      OwnSmem& sm) {
+                                      OwnSmem& sm, uint32_t ctx) {
   const uint32_t stall = q.z & 0xFFFFu;
   const bool ok = (q.x == seg_launch) & (stall < a.S) & (q.w != 0) & (q.y < (1u << 27) - 1u) & ctx_ok & (q.x < a.n_launch);
   if (ok) {  // valid sample with count > 1
-    own_spill(sm, a, (q.y << 5) | stall, q.w);
+    own_spill(sm, a, (q.y << 5) | stall, q.w, ctx);
     return;
   }
   const uint32_t r = own_reject(q.x, stall, q.w, seg_launch, a.n_launch, a.S, ctx_ok, a.trace_flags);
@@ -415,8 +442,10 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) { DC_PDL_
     }
     sm.distinct = 0;
     sm.flush_req = 0;
-    sm.spill_n = 0;
-    sm.spill_seg = 0;
+    sm.sp_word = 0;
+    sm.sp_seg = 0;
+    sm.sp_lock = 0;
+    sm.sp_base[0] = a.spill_base0 + (uint64_t)blockIdx.x * OW_SPILL_CAP;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -695,7 +724,7 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) { DC_PDL_
     if (__any_sync(0xffffffffu, cold)) {  // rare: spills and invalid samples
 #pragma unroll
       for (int i = 0; i < OW_PER_LANE; ++i)
-        if (vld[i] && t[i] == EMPTY32) own_cold(q[i], lch[i], a, ctx_ok, k, sm);
+        if (vld[i] && t[i] == EMPTY32) own_cold(q[i], lch[i], a, ctx_ok, k, sm, mctx);
     }
     const long long c_2 = MODE == 9 ? clock64() : 0;
     if (MODE == 9) t_key += c_2 - c_1;
@@ -1374,8 +1403,10 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
   }
   // partial outputs
   const uint32_t G = (uint32_t)c->num_sms;
-  const uint64_t cap_entries = n + 1;
-  const uint32_t cap_segs = (uint32_t)(n_launch + 4ull * G + n / 4096 + 1024);
+  // entry pool: table flushes + spill chunks after each CTA's first (at most n entries, plus a
+  // partly used last chunk per CTA); the first chunks sit after the pool
+  const uint64_t cap_entries = n + 1 + (uint64_t)G * OW_SPILL_CAP;
+  const uint32_t cap_segs = (uint32_t)(n_launch + 4ull * G + n / 4096 + n / OW_SPILL_CAP + 1024);
   Buf<uint32_t> pkey, flags, cm, wide;
   Buf<uint64_t> cw;
   Buf<uint8_t> csh;
@@ -1489,7 +1520,10 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
       fprintf(stderr, "{\"own_out\": {\"entries\": %llu, \"segments\": %llu}}\n", (unsigned long long)hc[0],
               (unsigned long long)(hc[1] & 0xFFFFFFFFu));
   }
-  if (hf[0]) return DC_OK;  // fallback / overflow -> generic schedule (diag of this pass discarded)
+  if (hf[0]) {  // fallback / overflow -> generic schedule (diag of this pass discarded)
+    if (getenv("DC_TEST_OWNER_STRICT")) return fail(c, DC_ERR_STATE, "test: owner schedule fell back (flags 0x%x)", hf[0]);
+    return DC_OK;
+  }
   const uint32_t n_segs = (uint32_t)(hc[1] & 0xFFFFFFFFu);
   {
     // ------------------------------------------------ global bitmap reduce (see k_br_*)

@@ -166,9 +166,11 @@ def test_generic_schedule_equals_owner_schedule(monkeypatch):
 
 
 @pytest.mark.parametrize("n,npc,big", [(3_000_000, 2000, False), (400_000, 20_000, False), (200_000, 300, True)])
-def test_owner_high_cardinality_flush_spill_and_wrap(n, npc, big):
+def test_owner_high_cardinality_flush_spill_and_wrap(n, npc, big, monkeypatch):
     """One context with up to 480k (pc, stall) keys: mid-context flushes and spills in the
-    context-owner schedule; big=True uses counts up to 2^31 (32-bit shared-counter carries)."""
+    context-owner schedule; big=True uses counts up to 2^31 (32-bit shared-counter carries),
+    so every sample is spilled (many spill-chunk switches). The schedule must not fall back."""
+    monkeypatch.setenv("DC_TEST_OWNER_STRICT", "1")
     rng = np.random.default_rng(n)
     s = np.zeros(n, oracle.SAMPLE_DTYPE)
     s["launch"] = 0
@@ -184,10 +186,12 @@ def test_owner_high_cardinality_flush_spill_and_wrap(n, npc, big):
 
 
 @pytest.mark.parametrize("n_launch,heavy", [(3, 1), (300, 40), (2000, 5)])
-def test_owner_work_stealing_skewed_contexts(n_launch, heavy):
+def test_owner_work_stealing_skewed_contexts(n_launch, heavy, monkeypatch):
     """Stage ranges of very unequal cost: a few launches carry most samples with many distinct
-    keys (flushes), the rest are light; with 3 launches most CTAs start with an empty range and
-    only steal. Every stage must be aggregated exactly once: oracle and generic schedule agree."""
+    keys (flushes, spill chunks), the rest are light; with 3 launches most CTAs start with an
+    empty range and only steal. Every stage must be aggregated exactly once: oracle and generic
+    schedule agree, and the owner schedule must not fall back."""
+    monkeypatch.setenv("DC_TEST_OWNER_STRICT", "1")
     rng = np.random.default_rng(n_launch)
     paths = [(0, 1), (0, 2), (1, 3), (1, 2, 4), (3,), (0, 1, 2, 3)]
     off, fr = _csr([paths[i % len(paths)] for i in range(n_launch)])  # launch i = record i
