@@ -60,6 +60,7 @@ class Clocks:
 
     def __init__(self, device: int):
         self.samples, self.reasons, self.ok = [], set(), False
+        self.period = float(os.environ.get("DC_BENCH_CLOCK_MS", "5")) / 1000.0  # measurement experiments only
         try:
             import pynvml
             pynvml.nvmlInit()
@@ -80,7 +81,7 @@ class Clocks:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.005)
+            time.sleep(self.period)
 
     def __enter__(self):
         self.stop = False
@@ -238,7 +239,7 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="dc", choices=["dc", "reference"])
     ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5])
@@ -317,6 +318,8 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
     per_step = [e0.elapsed_time(step_ev[0])] + [step_ev[i - 1].elapsed_time(step_ev[i]) for i in range(1, args.steps)]
+    if os.environ.get("DC_BENCH_DUMP_STEPS"):
+        print(json.dumps({"per_step_ms": [round(x, 3) for x in per_step]}), file=sys.stderr)
     barrier()
     launches = (ctx.launches - l0) // args.steps
     step_bytes = (ctx.diag()["bytes_moved_est"] - b0) / args.steps

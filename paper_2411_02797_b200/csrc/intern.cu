@@ -148,6 +148,46 @@ __global__ void k_intern_rank(const uint32_t* __restrict__ order, const uint32_t
   }
 }
 
+// Small dictionaries (D <= IR_MAX_D, every config with raw keys): the rank of each distinct key
+// is the number of smaller keys, counted directly — one launch instead of two radix sorts, a
+// gather and the rank kernel. CTA: 32 keys (one per lane), its warps split the comparison
+// range (broadcast loads), partial counts summed in shared memory. Keys are distinct.
+constexpr uint32_t IR_MAX_D = 8192;
+constexpr int IR_WARPS = 8;
+__global__ void __launch_bounds__(32 * IR_WARPS) k_intern_rank_small(const uint64_t* __restrict__ ka, const uint64_t* __restrict__ kb,
+                                                                     const uint32_t* __restrict__ slot_of, const ulonglong2* __restrict__ table,
+                                                                     uint32_t* __restrict__ rank_of_slot, dc_frame_key* __restrict__ dict,
+                                                                     uint8_t* __restrict__ kinds, uint32_t D) { DC_PDL_ENTER();
+  __shared__ uint32_t part[IR_WARPS][32];
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t i = blockIdx.x * 32 + lane;
+  const bool ok = i < D;
+  const uint64_t a = ok ? ka[i] : 0, b = ok ? kb[i] : 0;  // (kind << 32 | str_id, addr) order
+  const uint32_t per = (D + IR_WARPS - 1) / IR_WARPS, j0 = w * per, j1 = min(D, j0 + per);
+  uint32_t r = 0;
+#pragma unroll 4
+  for (uint32_t j = j0; j < j1; ++j) {
+    const uint64_t bj = kb[j], aj = ka[j];
+    r += (bj < b) | ((bj == b) & (aj < a));
+  }
+  part[w][lane] = r;
+  __syncthreads();
+  if (w == 0 && ok) {
+    uint32_t rank = 0;
+#pragma unroll
+    for (int ww = 0; ww < IR_WARPS; ++ww) rank += part[ww][lane];
+    const uint32_t s = slot_of[i];
+    rank_of_slot[s] = rank;
+    const ulonglong2 cur = table[s];
+    dc_frame_key k;
+    k.kind = (uint32_t)cur.x;
+    k.str_id = (uint32_t)(cur.x >> 32);
+    k.addr = cur.y;
+    dict[rank] = k;
+    kinds[rank] = (uint8_t)(k.kind < 255 ? k.kind : 255);
+  }
+}
+
 __global__ void k_intern_remap(uint32_t* ids, uint64_t n, const uint32_t* __restrict__ rank_of_slot) { DC_PDL_ENTER();
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x)
     ids[j] = rank_of_slot[ids[j]];
@@ -227,6 +267,18 @@ dc_status intern_frames(Ctx* c, const dc_frame_key* keys, uint64_t n, uint32_t* 
   DC_TRY(alloc_zero(c, pos, 1));
   dc_launch(k_intern_compact, grid_for(c, cap, 256), 256, 0, c->stream, table.p, cap, ka.p, kb.p, slot_of.p, pos.p);
   DC_LAUNCHED(c);
+  if (D <= IR_MAX_D && !getenv("DC_TEST_INTERN_RADIX")) {
+    DC_TRY(palloc(c, d->keys, D));
+    DC_TRY(palloc(c, d->kinds, D));
+    dc_launch(k_intern_rank_small, (uint32_t)((D + 31) / 32), 32 * IR_WARPS, 0, c->stream, ka.p, kb.p, slot_of.p, table.p,
+              rank_of_slot.p, d->keys, d->kinds, (uint32_t)D);
+    DC_LAUNCHED(c);
+    dc_launch(k_intern_remap, grid_for(c, n, 256), 256, 0, c->stream, out_ids, n, rank_of_slot.p);
+    DC_LAUNCHED(c);
+    c->bytes_host += 20 * n + 16 * D;
+    *out = d;
+    return DC_OK;
+  }
   dc_launch(k_iota, grid_for(c, D, 256), 256, 0, c->stream, ord0.p, D);
   DC_LAUNCHED(c);
   // LSD: by addr, then (stable) by kind<<32|str  ==> lexicographic (kind, str_id, addr)

@@ -6,6 +6,7 @@ import os
 
 import numpy as np
 import pytest
+import torch
 
 import gen
 import oracle
@@ -419,3 +420,27 @@ def test_attribute_contended_columns(monkeypatch, direct):
     a = gpu_run(off, fr, X, n_frames=20)
     ref = oracle_run(off, fr, X, 2).arrays()
     assert_same(a, ref, ctx=f"contended direct={direct}")
+
+
+@pytest.mark.parametrize("D,radix", [(3000, False), (3000, True), (20000, False), (1, False)])
+def test_intern_rank_paths(D, radix, monkeypatch):
+    """Frame interning: the direct-count rank (D <= 8192) and the two-pass radix sort (forced, or
+    D > 8192) give the oracle's ids and sorted dictionary; keys share kinds / strings / addresses
+    so every field of the (kind, str_id, addr) order decides some pairs."""
+    if radix:
+        monkeypatch.setenv("DC_TEST_INTERN_RADIX", "1")
+    import paper_2411_02797_b200 as dc
+    rng = np.random.default_rng(D)
+    base = np.zeros(D, oracle.KEY_DTYPE)
+    base["kind"] = rng.integers(0, 6, D)
+    base["str_id"] = rng.integers(0, max(2, D // 50), D)
+    base["addr"] = rng.integers(0, 2**40, D, dtype=np.uint64)
+    base["addr"][: D // 3] = rng.integers(0, 8, D // 3)  # small addresses: ties on the high words
+    keys = base[rng.integers(0, D, 400_000)]
+    ctx = dc.Context(0)
+    kk = torch.from_numpy(np.ascontiguousarray(keys).view(np.int32).reshape(-1, 4)).to("cuda:0")
+    ids, d = dc.dc_intern_frames(ctx, kk)
+    oids, od = oracle.intern(keys)
+    assert np.array_equal(ids.cpu().numpy().view(np.uint32), oids)
+    assert np.array_equal(d.keys(), od)
+    assert np.array_equal(d.kinds(), np.minimum(od["kind"], 255).astype(np.uint8))
