@@ -196,6 +196,93 @@ __global__ void k_push(const uint32_t* __restrict__ parent, uint64_t N, uint32_t
   }
 }
 
+// Push without any returned atomic (the variant used for trees that fit the shared-memory
+// parent array, N <= PL_MAX_N): the parent array is staged in shared memory, so the ancestor
+// walk costs a shared load per step; count / sum / samples / stall are fire-and-forget adds,
+// min a fire-and-forget atomicMin, and the u128 square sum is pushed as four 32-bit limbs into
+// limb accumulators L[m][k][a] (each < 2^64: at most N < 2^32 contributions of < 2^32), folded
+// exactly into the inclusive (sq_lo, sq_hi) by k_push_fold. Every walk step issues and moves on.
+constexpr uint32_t PL_MAX_N = 48u << 10;
+__global__ void __launch_bounds__(1024) k_push_limbs(const uint32_t* __restrict__ parent, uint64_t N, uint32_t M, uint32_t G,
+                                                     const uint64_t* __restrict__ xcnt, unsigned long long* __restrict__ icnt,
+                                                     unsigned long long* __restrict__ mcols, unsigned long long* __restrict__ limbs,
+                                                     const uint64_t* __restrict__ xsamples, unsigned long long* __restrict__ isamples,
+                                                     const uint64_t* __restrict__ xstall, unsigned long long* __restrict__ istall) { DC_PDL_ENTER();
+  extern __shared__ uint32_t spar[];
+  for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) spar[i] = parent[i];
+  __syncthreads();
+  const uint64_t total = (N - 1) * (uint64_t)G;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t n = (uint32_t)(1 + t / G);
+    const uint32_t g = (uint32_t)(t % G);
+    if (g >= 1 && g <= M) {
+      if (!xcnt[n]) continue;
+      const uint32_t m = g - 1;
+      const uint64_t sm = mcols[((uint64_t)C_XSUM * M + m) * N + n];
+      const uint64_t mn = mcols[((uint64_t)C_XMIN * M + m) * N + n];
+      const uint64_t qlo = mcols[((uint64_t)C_XSQLO * M + m) * N + n];
+      const uint64_t qhi = mcols[((uint64_t)C_XSQHI * M + m) * N + n];
+      const uint64_t q0 = qlo & 0xFFFFFFFFull, q1 = qlo >> 32, q2 = qhi & 0xFFFFFFFFull, q3 = qhi >> 32;
+      unsigned long long* isum = mcols + ((uint64_t)C_ISUM * M + m) * N;
+      unsigned long long* imin = mcols + ((uint64_t)C_IMIN * M + m) * N;
+      unsigned long long* L = limbs + (uint64_t)m * 4 * N;
+      // ids strictly decrease towards the root (parent[n] < n), which also bounds the walk
+      for (uint32_t a = spar[n], prev = n; a < prev; prev = a, a = spar[a]) {
+        if (sm) atomicAdd(isum + a, (unsigned long long)sm);
+        atomicMin(imin + a, (unsigned long long)mn);
+        if (q0) atomicAdd(L + a, (unsigned long long)q0);
+        if (q1) atomicAdd(L + N + a, (unsigned long long)q1);
+        if (q2) atomicAdd(L + 2 * N + a, (unsigned long long)q2);
+        if (q3) atomicAdd(L + 3 * N + a, (unsigned long long)q3);
+        if (a == 0) break;
+      }
+      continue;
+    }
+    unsigned long long* col;
+    uint64_t v;
+    if (g == 0) {
+      col = icnt;
+      v = xcnt[n];
+    } else if (g == M + 1) {
+      col = isamples;
+      v = xsamples[n];
+    } else {
+      const uint32_t st = g - M - 2;
+      col = istall + (uint64_t)st * N;
+      v = xstall[(uint64_t)st * N + n];
+    }
+    if (!v) continue;
+    for (uint32_t a = spar[n], prev = n; a < prev; prev = a, a = spar[a]) {
+      atomicAdd(col + a, (unsigned long long)v);
+      if (a == 0) break;
+    }
+  }
+}
+
+// incl sq (u128) += L0 + L1 * 2^32 + L2 * 2^64 + L3 * 2^96, exactly (u192 intermediate)
+__global__ void k_push_fold(uint64_t N, uint32_t M, const unsigned long long* __restrict__ limbs,
+                            unsigned long long* __restrict__ mcols) { DC_PDL_ENTER();
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < (uint64_t)M * N; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t m = i / N, n = i % N;
+    const unsigned long long* L = limbs + m * 4 * N;
+    const uint64_t l0 = L[n], l1 = L[N + n], l2 = L[2 * N + n], l3 = L[3 * N + n];
+    if ((l0 | l1 | l2 | l3) == 0) continue;
+    uint64_t* plo = (uint64_t*)mcols + ((uint64_t)C_ISQLO * M + m) * N + n;
+    uint64_t* phi = (uint64_t*)mcols + ((uint64_t)C_ISQHI * M + m) * N + n;
+    // lo word: existing lo + l0 + (l1 << 32); hi word: existing hi + (l1 >> 32) + l2 + (l3 << 32) + carries
+    uint64_t lo = *plo, hi = *phi;
+    uint64_t t = lo + l0;
+    hi += t < lo ? 1u : 0u;
+    lo = t;
+    t = lo + (l1 << 32);
+    hi += t < lo ? 1u : 0u;
+    lo = t;
+    hi += (l1 >> 32) + l2 + (l3 << 32);  // the u128 total fits by definition (exact square sums)
+    *plo = lo;
+    *phi = hi;
+  }
+}
+
 // Level-synchronous rollup for deep / large trees: one persistent cooperative kernel walks the
 // levels bottom-up; every node of level d adds its (final) inclusive values into its parent,
 // with a software grid barrier between levels. Siblings are contiguous (canonical order), so a
@@ -326,6 +413,22 @@ dc_status rollup(Ctx* c, dc_cct* t) {
     const int grid = c->num_sms * std::max(1, std::min(per_sm, 4));
     DC_CUDA(c, cudaLaunchCooperativeKernel((void*)k_rollup_levels, grid, 256, args, 0, s));
     DC_LAUNCHED(c);
+  } else if (N > 1 && N <= PL_MAX_N && !getenv("DC_TEST_ROLLUP_PUSH_RETURNED")) {
+    Buf<unsigned long long> limbs;
+    if (M) DC_TRY(alloc_zero(c, limbs, 4ull * M * N));
+    const size_t smem = N * 4;
+    DC_CUDA(c, cudaFuncSetAttribute(k_push_limbs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const uint64_t work = (N - 1) * G;
+    uint64_t grid = (work + 1023) / 1024;
+    if (grid > (uint64_t)c->num_sms) grid = c->num_sms;
+    dc_launch(k_push_limbs, (uint32_t)grid, 1024, smem, s, t->parent, N, M, G, t->xcnt, (unsigned long long*)t->icnt,
+              (unsigned long long*)t->mcols, limbs.p, t->xsamples, (unsigned long long*)t->isamples, t->xstall,
+              (unsigned long long*)t->istall);
+    DC_LAUNCHED(c);
+    if (M) {
+      dc_launch(k_push_fold, grid_for(c, (uint64_t)M * N, 256), 256, 0, s, N, M, limbs.p, (unsigned long long*)t->mcols);
+      DC_LAUNCHED(c);
+    }
   } else if (N > 1) {
     dc_launch(k_push, grid_for(c, (N - 1) * G, 256, 16), 256, 0, s, t->parent, N, M, S, G, t->xcnt, (unsigned long long*)t->icnt,
                                                              (unsigned long long*)t->mcols, t->xsamples,

@@ -89,6 +89,8 @@ def test_random_traces_vs_oracle(seed, monkeypatch):
         monkeypatch.setenv("DC_TEST_ROLLUP_LEVELS", "1")
     if seed >= 4:  # the one-CTA level loop instead of the lexicographic-rank build
         monkeypatch.setenv("DC_TEST_BUILD_LEVELS", "1")
+    if seed in (0, 4):  # the ancestor push with returned u128 atomics instead of 32-bit limbs
+        monkeypatch.setenv("DC_TEST_ROLLUP_PUSH_RETURNED", "1")
     rng = np.random.default_rng(500 + seed)
     import paper_2411_02797_b200 as dc
     ctx = dc.Context(0)
