@@ -936,18 +936,37 @@ __global__ void __launch_bounds__(32 * BR_WARPS) k_br_count(
     const uint32_t j0 = (uint32_t)(item % BR_MAXCH) * BR_CH, j1 = min(sg.y, j0 + BR_CH);
     const uint64_t wb = wbase[sg.x];
     const int sh = csh[sg.x];
-#pragma unroll 2
-    for (uint32_t j = j0 + lane; j < j1; j += 32) {
-      const uint32_t kk = pkey[base + j];
-      const unsigned long long cv = pcnt[base + j];
-      const uint64_t wd = wb + ((kk >> 5) >> sh);
-      const uint32_t b = kk & 31u;
-      const uint64_t r = (pre[wd] >> 32) + __popc(bm[wd] & ((1u << b) - 1u));
-      atomicAdd(bin_count + r, cv);
-      const uint32_t c32 = (uint32_t)cv;
+    // all BR_CH / 32 entries of the lane in flight at once: entry loads, then the bitmap word /
+    // prefix loads, then the updates (one latency round each instead of one per entry pair)
+    constexpr int U = BR_CH / 32;
+    uint32_t kk[U];
+    unsigned long long cv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t j = j0 + lane + 32 * u;
+      kk[u] = j < j1 ? pkey[base + j] : 0u;
+      cv[u] = j < j1 ? pcnt[base + j] : 0ull;
+    }
+    uint64_t pr[U];
+    uint32_t bw[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t j = j0 + lane + 32 * u;
+      const uint64_t wd = wb + ((kk[u] >> 5) >> sh);
+      pr[u] = j < j1 ? pre[wd] : 0ull;
+      bw[u] = j < j1 ? bm[wd] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t j = j0 + lane + 32 * u;
+      if (j >= j1) continue;
+      const uint32_t b = kk[u] & 31u;
+      const uint64_t r = (pr[u] >> 32) + __popc(bw[u] & ((1u << b) - 1u));
+      atomicAdd(bin_count + r, cv[u]);
+      const uint32_t c32 = (uint32_t)cv[u];
       const uint32_t old = atomicAdd(&lo[w][b], c32);
       const uint32_t carry = old + c32 < old ? 1u : 0u;
-      if (carry + (uint32_t)(cv >> 32)) atomicAdd(&hi[w][b], carry + (uint32_t)(cv >> 32));
+      if (carry + (uint32_t)(cv[u] >> 32)) atomicAdd(&hi[w][b], carry + (uint32_t)(cv[u] >> 32));
     }
     __syncwarp();
     const unsigned long long t = ((unsigned long long)hi[w][lane] << 32) | lo[w][lane];
