@@ -117,3 +117,20 @@ def test_chunked_online_aggregation_config3():
     o, od = _oracle_concat(tr, p.n_metrics, with_pc=True)
     assert np.array_equal(d.keys(), od)
     assert_same(acc.to_numpy(), o.arrays(), ctx="chunked")
+
+
+def test_merge_ranks_nccl_single_rank():
+    """The NCCL path of dc_cct_merge_ranks / dc_cct_gather on a one-rank communicator (every
+    collective and send/recv runs, to self): the gathered canonical CCT equals the oracle's."""
+    import paper_2411_02797_b200 as dc
+    ctx = dc.Context(0)
+    p = gen.programs.config3(n_samples=1_000_000)
+    tr = gen.make_trace(p, pc=True, bad_per_million=200)
+    sh = _split(tr, 1, with_pc=True)[0]
+    cct, d = _shard_run(dc, ctx, **sh)
+    comm = dc.dc_comm_create(ctx, dc.dc_nccl_unique_id(), 1, 0)
+    part, gd = dc.dc_cct_merge_ranks(ctx, comm, cct, d)
+    canon = dc.dc_cct_gather(ctx, comm, part, 0)
+    o, od = _oracle_concat(tr, p.n_metrics, with_pc=True)
+    assert np.array_equal(gd.keys(), od)
+    assert_same(canon.to_numpy(), o.arrays(), ctx="nccl merge, 1 rank")
