@@ -16,6 +16,7 @@ Prints ONE JSON line on rank 0.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -287,6 +288,11 @@ def main():
         if dist is not None:
             dist.barrier()
 
+    # setup: grow the library's stream-ordered pool past one step's peak (scratch of the PC
+    # histogram ~12 B/sample, records and frames ~64 B/record, plus the live previous tree) so
+    # no timed step maps new memory (dc_ctx_reserve; measured: a 5th-step stall of up to 30 ms)
+    n_smp = int(tr.samples.shape[0]) if args.config == 3 else 0
+    ctx.reserve(2 * (16 * n_smp + 64 * tr.n_records + 4 * F) + (256 << 20))
     # warm-up exactly like the timed loop (the previous step's CCT stays alive while the next one
     # is built), so the memory pool has grown to its steady-state size before timing
     last = None
@@ -300,6 +306,10 @@ def main():
     # ---------------- timed region (device time, CUDA events on the library stream; the
     # library's own per-stage timers are off here and measured in a separate pass below)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # no Python garbage collection inside the timed region: a full collection over torch's heap
+    # takes milliseconds and stalls the host between the step's launches
+    gc.collect()
+    gc.disable()
     barrier()
     torch.cuda.synchronize()
     l0 = ctx.launches
@@ -317,6 +327,7 @@ def main():
             step_ev[i].record(stream)  # per-step boundaries (distribution of step times)
         e1.record(stream)
         torch.cuda.synchronize()
+    gc.enable()
     per_step = [e0.elapsed_time(step_ev[0])] + [step_ev[i - 1].elapsed_time(step_ev[i]) for i in range(1, args.steps)]
     if os.environ.get("DC_BENCH_DUMP_STEPS"):
         print(json.dumps({"per_step_ms": [round(x, 3) for x in per_step]}), file=sys.stderr)
@@ -378,6 +389,8 @@ def main():
         t2.n_records = tr.n_records
         for k, v in devb.items():
             setattr(t2, k, v)
+        gc.collect()
+        gc.disable()
         barrier()
         torch.cuda.synchronize()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -392,6 +405,7 @@ def main():
                 cct.free()
             f1.record(stream)
         torch.cuda.synchronize()
+        gc.enable()
         barrier()
         ems = f0.elapsed_time(f1) / args.e2e_steps
         if dist is not None:

@@ -93,6 +93,13 @@ uint64_t dc_ctx_launch_count(const dc_ctx* ctx);
    len bytes, NUL-terminated) and resets the timers. */
 dc_status dc_ctx_set_timing(dc_ctx* ctx, int on);
 dc_status dc_ctx_timer_report(dc_ctx* ctx, char* buf, size_t len);
+/* Grows the device's stream-ordered memory pool (the one every scratch and handle allocation of
+   the library comes from, release threshold = infinity) to hold at least `bytes` by allocating
+   and freeing one block on the context stream, then synchronizes. Later calls then carve their
+   buffers from memory that is already mapped, instead of mapping new physical memory (a
+   millisecond-scale stall) the first time a call needs more than any earlier one. Optional;
+   results never depend on it. DC_ERR_OOM if the pool cannot grow that far. */
+dc_status dc_ctx_reserve(dc_ctx* ctx, uint64_t bytes);
 
 /* ------------------------------------------------------------------- a1: interning */
 /* Raw frame key, 16 B. Identity: Python (PY, file string id, line);

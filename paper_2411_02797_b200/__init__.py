@@ -70,6 +70,10 @@ class Context:
     def launches(self) -> int:
         return int(lib().dc_ctx_launch_count(self.h))
 
+    def reserve(self, nbytes: int):
+        """Grow the stream-ordered pool to at least nbytes (dc_ctx_reserve)."""
+        self.check(lib().dc_ctx_reserve(self.h, int(nbytes)), "dc_ctx_reserve")
+
     def set_timing(self, on: bool):
         self.check(lib().dc_ctx_set_timing(self.h, int(bool(on))), "dc_ctx_set_timing")
 

@@ -263,6 +263,20 @@ dc_status dc_ctx_set_timing(dc_ctx* ctx, int on) {
   return DC_OK;
 }
 
+dc_status dc_ctx_reserve(dc_ctx* ctx, uint64_t bytes) {
+  CHECK_CTX(ctx);
+  ON_DEVICE(ctx);
+  if (!bytes) return DC_OK;
+  void* p = nullptr;
+  if (cudaMallocAsync(&p, bytes, ctx->stream) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(ctx, DC_ERR_OOM, "dc_ctx_reserve: cannot reserve %llu bytes", (unsigned long long)bytes);
+  }
+  DC_CUDA(ctx, cudaFreeAsync(p, ctx->stream));
+  DC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return DC_OK;
+}
+
 dc_status dc_ctx_timer_report(dc_ctx* ctx, char* buf, size_t len) {
   CHECK_CTX(ctx);
   ARG(buf && len, "buf is NULL");

@@ -446,3 +446,17 @@ def test_intern_rank_paths(D, radix, monkeypatch):
     assert np.array_equal(ids.cpu().numpy().view(np.uint32), oids)
     assert np.array_equal(d.keys(), od)
     assert np.array_equal(d.kinds(), np.minimum(od["kind"], 255).astype(np.uint8))
+
+
+def test_ctx_reserve():
+    """dc_ctx_reserve grows the pool (results unchanged); an impossible size is DC_ERR_OOM."""
+    import paper_2411_02797_b200 as dc
+    ctx = dc.Context(0)
+    ctx.reserve(1 << 30)
+    off, fr = _csr([(0, 1), (0, 2), (1,)])
+    X = np.array([[3, 4, 5]], np.uint64)
+    a = gpu_run(off, fr, X, n_frames=3, ctx=ctx)
+    assert_same(a, oracle_run(off, fr, X, 1).arrays(), ctx="after reserve")
+    with pytest.raises(dc.DcError) as e:
+        ctx.reserve(1 << 50)
+    assert e.value.status == 2  # DC_ERR_OOM
