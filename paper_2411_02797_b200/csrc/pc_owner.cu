@@ -1565,17 +1565,23 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
         dc_launch(k_br_pop, grid_for(c, W, 256), 256, 0, c->stream, bm.p, W, pk.p);
         DC_LAUNCHED(c);
       }
+      // output arrays sized by the partial-entry count (every bin has at least one entry, every
+      // PC node at least one bin) and allocated before the one round trip, so only the two
+      // launches follow it
+      const uint64_t nb_cap = hc[0] + (uint64_t)G * OW_SPILL_CAP;
+      DC_TRY(palloc(c, t->pc_ctx, nb_cap));
+      DC_TRY(palloc(c, t->pc_off, nb_cap));
+      DC_TRY(palloc(c, t->bin_pcnode, nb_cap));
+      DC_TRY(palloc(c, t->bin_stall, nb_cap));
+      DC_TRY(palloc(c, t->bin_count, nb_cap));
       DC_TRY(excl_scan<uint64_t>(c, pk.p, pk.p, W, pk.p + W));
       uint64_t ht = 0;
       DC_TRY(readback(c, pk.p + W, 8, &ht));
       const uint64_t nb = ht >> 32, npc = ht & 0xFFFFFFFFu;
+      if (nb > nb_cap) return fail(c, DC_ERR_STATE, "internal: %llu bins > %llu partial entries", (unsigned long long)nb,
+                                   (unsigned long long)nb_cap);
       t->Npc = npc;
       t->Nbins = nb;
-      DC_TRY(palloc(c, t->pc_ctx, npc));
-      DC_TRY(palloc(c, t->pc_off, npc));
-      DC_TRY(palloc(c, t->bin_pcnode, nb));
-      DC_TRY(palloc(c, t->bin_stall, nb));
-      DC_TRY(palloc(c, t->bin_count, nb));
       DC_CUDA(c, cudaMemsetAsync(t->bin_count, 0, (nb ? nb : 1) * 8, c->stream));
       if (nb) {
         {
