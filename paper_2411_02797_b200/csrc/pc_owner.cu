@@ -45,8 +45,8 @@ constexpr uint32_t OW_SPILL_AT = OW_TAB - OW_CONS_WARPS * OW_PEND - 1;
 constexpr uint32_t OW_MISS = 0xFFFFFFFEu;
 constexpr uint32_t OW_SPILL_CAP = 4096;       // spill chunk (entries); the first per CTA is preallocated
 constexpr uint32_t OW_SP_RING = 8;            // spill chunk bases kept (by generation)
-constexpr uint32_t OW_CLAIM = 4;              // stages claimed from the own range at a time
-constexpr uint32_t OW_STEAL = 8;              // at most this many stages stolen at a time
+constexpr uint32_t OW_CLAIM = 8;              // stages claimed from the own range at a time
+constexpr uint32_t OW_STEAL = 16;             // at most this many stages stolen at a time
 constexpr uint32_t EMPTY32 = 0xFFFFFFFFu;
 constexpr uint32_t OW_DONE = 0xFFFFFFFFu;
 
