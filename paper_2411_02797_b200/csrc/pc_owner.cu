@@ -1408,8 +1408,8 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
     dc_launch(k_plan_launch, grid_for(c, n_launch, 256), 256, 0, c->stream, launch_off, order, lkey, n_launch, lrow.p, lflag.p,
                                                                     lsrc.p, lcnt.p);
     DC_LAUNCHED(c);
-    DC_TRY(excl_scan<uint64_t>(c, lrow.p, lrow.p, n_launch, lrow.p + n_launch));  // E: first row within the stream
-    DC_TRY(excl_scan<uint32_t>(c, lflag.p, gx.p, n_launch, gx.p + n_launch));      // group index, NG at gx[n]
+    // E: first row within the stream; group index (NG at gx[n])
+    DC_TRY((excl_scan_pair<uint64_t, uint32_t>(c, lrow.p, lrow.p, lrow.p + n_launch, lflag.p, gx.p, gx.p + n_launch, n_launch)));
     dc_launch(k_plan_gfirst, grid_for(c, n_launch, 256), 256, 0, c->stream, lkey, gx.p, gx.p + n_launch, n_launch, gfirst.p);
     DC_LAUNCHED(c);
     dc_launch(k_plan_gstages, grid_for(c, n_launch, 256), 256, 0, c->stream, lrow.p, gfirst.p, gx.p + n_launch, n_launch, gst.p);

@@ -93,6 +93,61 @@ __global__ void __launch_bounds__(SCAN1_THREADS) k_scan_one(const T* in, T* out,
   }
 }
 
+// two independent exclusive scans of the same length in one launch (each pass of k_scan_one,
+// done for both arrays: their load latencies overlap)
+template <class A, class B>
+__global__ void __launch_bounds__(SCAN1_THREADS) k_scan_one_pair(const A* ia, A* oa, A* ta, const B* ib, B* ob, B* tb, uint64_t n) { DC_PDL_ENTER();
+  __shared__ A wa[32];
+  __shared__ B wb[32];
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint64_t C = (n + 31) / 32;
+  const uint64_t lo = w * C, hi = lo + C < n ? lo + C : n;
+  A sa = 0;
+  B sb = 0;
+  for (uint64_t j = lo + lane; j < hi; j += 32) {
+    sa += ia[j];
+    sb += ib[j];
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    sa += __shfl_xor_sync(0xffffffffu, sa, o);
+    sb += __shfl_xor_sync(0xffffffffu, sb, o);
+  }
+  if (lane == 0) {
+    wa[w] = sa;
+    wb[w] = sb;
+  }
+  __syncthreads();
+  if (w == 0) {
+    const A va = wa[lane];
+    const A inca = warp_incl_scan(va);
+    wa[lane] = inca - va;
+    const B vb = wb[lane];
+    const B incb = warp_incl_scan(vb);
+    wb[lane] = incb - vb;
+    if (lane == 31) {
+      if (ta) *ta = inca;
+      if (tb) *tb = incb;
+    }
+  }
+  __syncthreads();
+  A ca = wa[w];
+  B cb = wb[w];
+  for (uint64_t b = lo; b < hi; b += 32) {
+    const uint64_t j = b + lane;
+    const A va = j < hi ? ia[j] : A(0);
+    const B vb = j < hi ? ib[j] : B(0);
+    const A inca = warp_incl_scan(va);
+    const B incb = warp_incl_scan(vb);
+    if (j < hi) {
+      oa[j] = ca + inca - va;
+      ob[j] = cb + incb - vb;
+    }
+    ca += __shfl_sync(0xffffffffu, inca, 31);
+    cb += __shfl_sync(0xffffffffu, incb, 31);
+  }
+}
+
 template <class T>
 __global__ void __launch_bounds__(SCAN_THREADS) k_scan_down(const T* __restrict__ in, T* out, uint64_t n,
                                                             const T* __restrict__ offs) { DC_PDL_ENTER();
@@ -113,6 +168,20 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_down(const T* __restrict_
     if (j < n) out[j] = ex;
     ex += v[i];
   }
+}
+
+template <class T>
+dc_status excl_scan(Ctx* c, const T* in, T* out, uint64_t n, T* total_dev);
+// two exclusive scans of length n (one launch when n <= SCAN1_MAX)
+template <class A, class B>
+dc_status excl_scan_pair(Ctx* c, const A* ia, A* oa, A* ta, const B* ib, B* ob, B* tb, uint64_t n) {
+  if (n == 0 || n > SCAN1_MAX) {
+    DC_TRY(excl_scan<A>(c, ia, oa, n, ta));
+    return excl_scan<B>(c, ib, ob, n, tb);
+  }
+  dc_launch(k_scan_one_pair<A, B>, 1, SCAN1_THREADS, 0, c->stream, ia, oa, ta, ib, ob, tb, n);
+  DC_LAUNCHED(c);
+  return DC_OK;
 }
 
 // out[i] = sum(in[0..i)); total (device) optional. in may equal out.
