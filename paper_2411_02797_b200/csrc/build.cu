@@ -378,9 +378,14 @@ __global__ void k_path_compact(const PathSlot* __restrict__ tab, uint64_t cap, u
   }
 }
 
-__global__ void k_items_finish(uint32_t* __restrict__ item_rec, const uint32_t* __restrict__ extra_rec, uint32_t P0,
-                               uint32_t n_extra, const uint64_t* __restrict__ off, uint32_t* __restrict__ item_len,
+// P0 (table items) and n_extra (collision extras) are the device counters of k_path_group, so
+// this runs before the host has read them; after a table overflow (d_cnt[3]) the attempt is
+// discarded by the host and nothing is added to the diagnostics
+__global__ void k_items_finish(uint32_t* __restrict__ item_rec, const uint32_t* __restrict__ extra_rec,
+                               const uint64_t* __restrict__ off, uint32_t* __restrict__ item_len,
                                unsigned long long* d_sumlen, const unsigned int* d_cnt, unsigned long long* d_diag) { DC_PDL_ENTER();
+  if (d_cnt[3]) return;
+  const uint32_t P0 = d_cnt[0], n_extra = d_cnt[1];
   uint32_t P = P0 + n_extra;
   if (blockIdx.x == 0 && threadIdx.x == 0 && d_cnt[4]) atomicAdd(&d_diag[DG_EMPTY], (unsigned long long)d_cnt[4]);
   unsigned long long acc = 0;
@@ -1271,7 +1276,18 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
   // path table sized for the distinct paths, not the records (retry if it passes half load)
   uint64_t cap = 1024;
   while (cap < 2 * (R < (1ull << 19) ? R : (1ull << 19))) cap <<= 1;
+  if (getenv("DC_TEST_PATH_CAP")) cap = 1024;  // test only: force the table-overflow retry
+  // One round trip for the whole record pass: the item arrays are sized by the records (every
+  // item has its own representative record), compaction and item lengths run on the device
+  // counters, and the counters, length sum, deepest path, flags and frame count come back
+  // together. A table past half load (rare) repeats the attempt with a larger table.
   uint32_t hc[8];
+  uint64_t hsum = 0, hmaxd = 0, F = 0;
+  uint32_t hflags = 0;
+  const uint64_t ibound = R ? R : 1;
+  DC_TRY(alloc(c, item_rec, ibound));
+  DC_TRY(alloc(c, item_len, ibound));
+  DC_TRY(alloc(c, leaf_of_item, ibound));
   for (int attempt = 0;; ++attempt) {
     DC_TRY(alloc(c, tab, cap));
     DC_CUDA(c, cudaMemsetAsync(tab.p, 0xFF, cap * sizeof(PathSlot), c->stream));
@@ -1281,27 +1297,21 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
                                                                                 cap - 1, slot_of_rec.p, extra_rec.p, cnt.p);
       DC_LAUNCHED(c);
     }
-    DC_TRY(readback(c, cnt.p, 32, hc));
+    DC_TRY(alloc(c, pid_of_slot, cap));
+    DC_TRY(alloc_zero(c, sumlen, 1));
+    dc_launch(k_path_compact, grid_for(c, cap, 256), 256, 0, c->stream, tab.p, cap, pid_of_slot.p, item_rec.p, item_len.p, cnt.p + 2);
+    DC_LAUNCHED(c);
+    dc_launch(k_items_finish, grid_for(c, ibound, 256), 256, 0, c->stream, item_rec.p, extra_rec.p, p->offsets, item_len.p, sumlen.p,
+              cnt.p, (unsigned long long*)c->d_diag);
+    DC_LAUNCHED(c);
+    DC_TRY(readback_multi(c, {{cnt.p, 32, hc}, {sumlen.p, 8, &hsum}, {c->d_diag + DG_MAXDEPTH, 8, &hmaxd}, {c->d_flags, 4, &hflags},
+                              {p->offsets + R, 8, &F}}));
     if (!hc[3]) break;
     if ((hc[3] & 2) || attempt > 2 || cap >= (1ull << 31))
       return fail(c, DC_ERR_CAPACITY, "dc_cct_build: path table overflow");
     cap = cap * 8 < (1ull << 31) ? cap * 8 : (1ull << 31);
   }
-  DC_TRY(alloc(c, pid_of_slot, cap));
   const uint32_t P0 = hc[0], n_extra = hc[1], P = P0 + n_extra;
-  DC_TRY(alloc(c, item_rec, P));
-  DC_TRY(alloc(c, item_len, P));
-  DC_TRY(alloc(c, leaf_of_item, P));
-  DC_TRY(alloc_zero(c, sumlen, 1));
-  dc_launch(k_path_compact, grid_for(c, cap, 256), 256, 0, c->stream, tab.p, cap, pid_of_slot.p, item_rec.p, item_len.p, cnt.p + 2);
-  DC_LAUNCHED(c);
-  dc_launch(k_items_finish, grid_for(c, P, 256), 256, 0, c->stream, item_rec.p, extra_rec.p, P0, n_extra, p->offsets, item_len.p,
-                                                             sumlen.p, cnt.p, (unsigned long long*)c->d_diag);
-  DC_LAUNCHED(c);
-  uint64_t hsum = 0, hmaxd = 0, F = 0;
-  uint32_t hflags = 0;
-  DC_TRY(readback_multi(c, {{sumlen.p, 8, &hsum}, {c->d_diag + DG_MAXDEPTH, 8, &hmaxd}, {c->d_flags, 4, &hflags},
-                            {p->offsets + R, 8, &F}}));
   DC_TRY(flags_status(c, hflags));
   const uint64_t Nbound = 1 + hsum;
   if (Nbound >= (1ull << 32)) return fail(c, DC_ERR_CAPACITY, "dc_cct_build: more than 2^32 nodes");

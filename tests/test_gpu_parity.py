@@ -460,3 +460,16 @@ def test_ctx_reserve():
     with pytest.raises(dc.DcError) as e:
         ctx.reserve(1 << 50)
     assert e.value.status == 2  # DC_ERR_OOM
+
+
+def test_path_table_overflow_retry(monkeypatch):
+    """5,000 distinct paths into a 1,024-slot path table (DC_TEST_PATH_CAP): the record pass
+    detects the overflow, discards the attempt (diagnostics counted once) and retries larger."""
+    monkeypatch.setenv("DC_TEST_PATH_CAP", "1")
+    rng = np.random.default_rng(11)
+    paths = [tuple(int(x) for x in rng.integers(0, 60, int(rng.integers(1, 12)))) for _ in range(5000)] + [()] * 7
+    off, fr = _csr(paths)
+    X = rng.integers(0, 100, size=(1, len(paths)), dtype=np.uint64)
+    a = gpu_run(off, fr, X, n_frames=60)
+    assert_same(a, oracle_run(off, fr, X, 1).arrays(), ctx="path table retry")
+    assert a["_ctx"].diag()["empty_paths"] == 7
