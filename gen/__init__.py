@@ -189,3 +189,38 @@ def make_trace(p: Program, n_records: int | None = None, device: str = "cpu", ra
         torch.cuda.current_stream(dev).synchronize()
     tr._keep = keep
     return tr
+
+
+def make_chunk_host(p: Program, r0: int, n: int, raw_keys: bool = True, ids: bool = False):
+    """Records [r0, r0 + n) of program p on the host, as numpy arrays (offsets relative to the
+    chunk, starting at 0): (offsets u64 [n+1], ids u32 [F] or None, keys KEY-layout u8 [F, 16]
+    or None, metrics u64 [M, n]). Records are generated independently (counter-based), so the
+    concatenation of consecutive chunks is byte-identical to make_trace over [0, r0 + n) from r0
+    on — used to stream traces too large for host memory through the CPU oracle."""
+    L = lib()
+    keep: list = []
+    gp = _prog_struct(p, torch.device("cpu"), keep)
+    lens = np.zeros(max(n, 1), np.uint32)
+    L.dcgen_lengths_host(ctypes.byref(gp), u64(r0), u64(n), lens.ctypes.data_as(P))
+    off = np.zeros(n + 1, np.uint64)
+    off[1:] = np.cumsum(lens[:n], dtype=np.uint64)
+    F = int(off[-1])
+    ids_a = np.zeros(max(F, 1), np.uint32) if ids else None
+    keys_a = np.zeros((max(F, 1), 16), np.uint8) if raw_keys else None
+    pool = np.ascontiguousarray(p.pool_keys)
+    L.dcgen_frames_host(ctypes.byref(gp), u64(r0), u64(n), off.ctypes.data_as(P), pool.ctypes.data_as(P),
+                        ids_a.ctypes.data_as(P) if ids else None, keys_a.ctypes.data_as(P) if raw_keys else None)
+    met = np.zeros((p.n_metrics, max(n, 1)), np.uint64)
+    L.dcgen_metrics_host(ctypes.byref(gp), u64(r0), u64(n), met.ctypes.data_as(P), u64(max(n, 1)))
+    return off, (ids_a[:F] if ids else None), (keys_a[:F] if raw_keys else None), np.ascontiguousarray(met[:, :n])
+
+
+def generator_version() -> str:
+    """SHA-256 (first 16 hex digits) of the generator's sources: cached oracle results
+    (tests/golden/digest_*.json) are keyed by it and go stale when the generator changes."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in ["csrc/gen_core.h", "csrc/dcgen.cu", "programs.py", "rng.py"]:
+        with open(os.path.join(_HERE, f), "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]

@@ -290,3 +290,51 @@ def seq_associate(fwd_seq, fwd_paths, bwd_seq, bwd_paths):
             out.append(list(p))
     return out, unmatched
 
+
+
+def digest(a: dict, dict_keys) -> str:
+    """SURVEY.md §8(c) "Digest (large-config parity)": SHA-256 of the canonical little-endian
+    serialisation of the oracle's CCT (this is the oracle's own writer; the CUDA side has a
+    separate one). Layout: b"DCCCT1\\0\\0", u64 N, M, S, Npc, Nbins, D; parent u32[N], frame
+    u32[N], depth u16[N], xcnt u64[N], icnt u64[N]; per metric xsum, xmin, xsq_lo, xsq_hi, isum,
+    imin, isq_lo, isq_hi (u64[N] each); xsamples, isamples u64[N] (zeros without PC samples);
+    per stall xstall, istall u64[N]; pc_ctx, pc_off u32[Npc]; bin_pcnode u32[Nb], bin_stall
+    u16[Nb], bin_count u64[Nb]; the dictionary's 16-B keys (kind u32, str_id u32, addr u64)."""
+    import hashlib
+    import struct
+
+    N, M, S = int(a["n_nodes"]), int(a["n_metrics"]), int(a["n_stall"])
+    Np, Nb = int(a["n_pc_nodes"]), int(a["n_bins"])
+    k = as_keys(dict_keys) if len(dict_keys) else np.zeros(0, KEY_DTYPE)
+    h = hashlib.sha256()
+    h.update(b"DCCCT1\0\0" + struct.pack("<6Q", N, M, S, Np, Nb, len(k)))
+
+    def put(x, dt):
+        h.update(np.ascontiguousarray(np.asarray(x).astype(dt, copy=False)).tobytes())
+
+    put(a["parent"][:N], "<u4")
+    put(a["frame"][:N], "<u4")
+    put(a["depth"][:N], "<u2")
+    put(a["xcnt"][:N], "<u8")
+    put(a["icnt"][:N], "<u8")
+    for m in range(M):
+        for nm in ["xsum", "xmin", "xsq_lo", "xsq_hi", "isum", "imin", "isq_lo", "isq_hi"]:
+            put(a[nm][m][:N], "<u8")
+    put(a["xsamples"][:N] if S else np.zeros(N, np.uint64), "<u8")
+    put(a["isamples"][:N] if S else np.zeros(N, np.uint64), "<u8")
+    for s in range(S):
+        put(a["xstall"][s][:N], "<u8")
+        put(a["istall"][s][:N], "<u8")
+    put(a["pc_ctx"][:Np], "<u4")
+    put(a["pc_off"][:Np], "<u4")
+    put(a["bin_pcnode"][:Nb], "<u4")
+    put(a["bin_stall"][:Nb], "<u2")
+    put(a["bin_count"][:Nb], "<u8")
+    h.update(np.ascontiguousarray(k).tobytes())
+    return h.hexdigest()
+
+
+def leaf_digest(leaf) -> str:
+    """SHA-256 of the records' canonical leaf ids (u32 little-endian, trace order)."""
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(np.asarray(leaf).astype("<u4", copy=False)).tobytes()).hexdigest()
