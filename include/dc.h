@@ -93,13 +93,18 @@ uint64_t dc_ctx_launch_count(const dc_ctx* ctx);
    len bytes, NUL-terminated) and resets the timers. */
 dc_status dc_ctx_set_timing(dc_ctx* ctx, int on);
 dc_status dc_ctx_timer_report(dc_ctx* ctx, char* buf, size_t len);
-/* Grows the device's stream-ordered memory pool (the one every scratch and handle allocation of
-   the library comes from, release threshold = infinity) to hold at least `bytes` by allocating
+/* Grows the context's private stream-ordered memory pool (created by dc_ctx_create; every
+   scratch and handle allocation of the library comes from it; its release threshold is
+   infinity, which affects no other allocator of the process) to hold at least `bytes` by allocating
    and freeing one block on the context stream, then synchronizes. Later calls then carve their
    buffers from memory that is already mapped, instead of mapping new physical memory (a
    millisecond-scale stall) the first time a call needs more than any earlier one. Optional;
    results never depend on it. DC_ERR_OOM if the pool cannot grow that far. */
 dc_status dc_ctx_reserve(dc_ctx* ctx, uint64_t bytes);
+/* Synchronizes, then returns the context pool's cached free memory to the device down to
+   keep_bytes (cudaMemPoolTrimTo). Memory held by live handles is unaffected. The pool itself is
+   destroyed by dc_ctx_destroy (deferred until the last handle made on the context is freed). */
+dc_status dc_ctx_trim(dc_ctx* ctx, uint64_t keep_bytes);
 
 /* ------------------------------------------------------------------- a1: interning */
 /* Raw frame key, 16 B. Identity: Python (PY, file string id, line);
@@ -181,9 +186,14 @@ typedef struct { uint32_t launch, pc_off; uint16_t stall, flags; uint32_t count;
                      PAPER.md:355-356) and the context-owner histogram schedule is used; a
                      sample whose launch field disagrees with its segment is still
                      attributed by its own launch field. NULL selects the generic schedule.
-   n_stall           <= DC_MAX_STALL; fixed by the first call on a handle.
-   Must be called at most once per handle in this version (DC_ERR_STATE otherwise).
-   Synchronizes (reads bin counts). State -> DIRTY. */
+   n_stall           <= DC_MAX_STALL; fixed by the first call on a handle (DC_ERR_ARG if a
+                     later call differs).
+   Accumulates: may be called repeatedly, e.g. once per chunk / activity buffer of samples
+   (the paper "flushes the metrics" per buffer). A later call's bins and PC
+   nodes are merged exactly with the earlier ones (counts of equal (ctx, pc, stall) added, PC
+   nodes renumbered over the union), so any split of the samples into calls gives the same
+   tree as one call. On error the earlier results are kept. DC_ERR_STATE on a merged
+   partition. Synchronizes (reads bin counts). State -> DIRTY. */
 dc_status dc_pc_sample_attribute(dc_ctx* ctx, dc_cct* cct, const dc_pc_sample* s, uint64_t n,
                                  const uint32_t* launch_leaf, uint64_t n_launch,
                                  const uint64_t* launch_sample_off, uint32_t n_stall);
@@ -326,6 +336,11 @@ typedef struct {
   const uint64_t* bin_count;            /* [n_bins] */
   int state;                            /* 0 BUILT, 1 DIRTY, 2 ROLLED */
 } dc_cct_view;
+/* dc_cct_view_get — fills *out_h with the handle's sizes and borrowed device pointers.
+   The inclusive columns (icnt, isum, imin, isq_lo, isq_hi, isamples, istall) are defined only
+   after dc_cct_rollup: in state BUILT or DIRTY they are returned as NULL and the call returns
+   DC_ERR_STATE (every other field is still filled, so structure and exclusive columns can be
+   read before the rollup). DC_OK in state ROLLED. */
 dc_status dc_cct_view_get(const dc_cct* cct, dc_cct_view* out_h);
 void dc_cct_free(dc_cct* cct);
 void dc_dict_free(dc_dict* d);

@@ -74,6 +74,10 @@ class Context:
         """Grow the stream-ordered pool to at least nbytes (dc_ctx_reserve)."""
         self.check(lib().dc_ctx_reserve(self.h, int(nbytes)), "dc_ctx_reserve")
 
+    def trim(self, keep_bytes: int = 0):
+        """Return the context pool's cached free memory to the device (dc_ctx_trim)."""
+        self.check(lib().dc_ctx_trim(self.h, int(keep_bytes)), "dc_ctx_trim")
+
     def set_timing(self, on: bool):
         self.check(lib().dc_ctx_set_timing(self.h, int(bool(on))), "dc_ctx_set_timing")
 
@@ -147,31 +151,34 @@ class CCT:
         self.h = h
         self.ctx = ctx
 
-    def view(self) -> dc_cct_view:
+    def view(self, before_rollup: bool = False) -> dc_cct_view:
+        """dc_cct_view_get. Before dc_cct_rollup the call reports DC_ERR_STATE (inclusive
+        columns NULL); before_rollup=True accepts that and returns the partial view."""
         v = dc_cct_view()
         st = lib().dc_cct_view_get(self.h, ctypes.byref(v))
-        if st:
+        if st and not (before_rollup and st == _lib.DC_ERR_STATE):
             raise DcError(st, "dc_cct_view_get")
         return v
 
     def to_numpy(self) -> dict:
         """Host copies of every view array (names as in the oracle's arrays())."""
         self.ctx.sync()
-        v = self.view()
+        v = self.view(before_rollup=True)
         N, Np, Nb, M, S = v.n_nodes, v.n_pc_nodes, v.n_bins, v.n_metrics, v.n_stall
         a = dict(n_nodes=N, n_pc_nodes=Np, n_bins=Nb, n_metrics=M, n_stall=S, max_depth=v.max_depth, state=v.state)
         a["parent"] = _dev_to_numpy(v.parent, (N,), np.uint32)
         a["frame"] = _dev_to_numpy(v.frame, (N,), np.uint32)
         a["depth"] = _dev_to_numpy(v.depth, (N,), np.uint16)
         a["level_off"] = _dev_to_numpy(v.level_off, (v.max_depth + 2,), np.uint32)
+        rolled = v.state == 2  # inclusive columns exist only after dc_cct_rollup (None before)
         a["xcnt"] = _dev_to_numpy(v.xcnt, (N,), np.uint64)
-        a["icnt"] = _dev_to_numpy(v.icnt, (N,), np.uint64)
+        a["icnt"] = _dev_to_numpy(v.icnt, (N,), np.uint64) if rolled else None
         for nm in ["xsum", "xmin", "xsq_lo", "xsq_hi", "isum", "imin", "isq_lo", "isq_hi"]:
-            a[nm] = _dev_to_numpy(getattr(v, nm), (M, N), np.uint64)
+            a[nm] = _dev_to_numpy(getattr(v, nm), (M, N), np.uint64) if rolled or nm[0] == "x" else None
         a["xsamples"] = _dev_to_numpy(v.xsamples, (N,), np.uint64) if v.xsamples else np.zeros(N, np.uint64)
-        a["isamples"] = _dev_to_numpy(v.isamples, (N,), np.uint64) if v.isamples else np.zeros(N, np.uint64)
+        a["isamples"] = (_dev_to_numpy(v.isamples, (N,), np.uint64) if v.isamples else np.zeros(N, np.uint64)) if rolled else None
         a["xstall"] = _dev_to_numpy(v.xstall, (S, N), np.uint64)
-        a["istall"] = _dev_to_numpy(v.istall, (S, N), np.uint64)
+        a["istall"] = _dev_to_numpy(v.istall, (S, N), np.uint64) if rolled else None
         a["pc_ctx"] = _dev_to_numpy(v.pc_ctx, (Np,), np.uint32)
         a["pc_off"] = _dev_to_numpy(v.pc_off, (Np,), np.uint32)
         a["bin_pcnode"] = _dev_to_numpy(v.bin_pcnode, (Nb,), np.uint32)
@@ -179,9 +186,40 @@ class CCT:
         a["bin_count"] = _dev_to_numpy(v.bin_count, (Nb,), np.uint64)
         return a
 
+    def digest(self, d: "Dict | None") -> str:
+        """SHA-256 of the canonical little-endian serialisation of this (rolled-up) tree and its
+        dictionary (SURVEY.md §8(c) "Digest"): b"DCCCT1\\0\\0", u64 N, M, S, Npc, Nbins, D, then
+        parent, frame, depth (u16), xcnt, icnt, per metric the 8 columns xsum, xmin, xsq_lo,
+        xsq_hi, isum, imin, isq_lo, isq_hi, xsamples, isamples, per stall xstall / istall, pc_ctx,
+        pc_off, bin_pcnode, bin_stall (u16), bin_count, the dictionary's 16-B keys. Host-side
+        formatting of the view's arrays only (for comparing results across runs / with a cached
+        reference digest)."""
+        import hashlib
+        import struct
+        a = self.to_numpy()
+        N, M, S, Np, Nb = (int(a[k]) for k in ["n_nodes", "n_metrics", "n_stall", "n_pc_nodes", "n_bins"])
+        keys = d.keys() if d is not None and d.size else np.zeros(0, np.dtype([("kind", "<u4"), ("str_id", "<u4"), ("addr", "<u8")]))
+        h = hashlib.sha256(b"DCCCT1\0\0" + struct.pack("<6Q", N, M, S, Np, Nb, len(keys)))
+        cols = [("parent", "<u4"), ("frame", "<u4"), ("depth", "<u2"), ("xcnt", "<u8"), ("icnt", "<u8")]
+        for name, dt in cols:
+            h.update(np.ascontiguousarray(a[name], dtype=dt).tobytes())
+        for m in range(M):
+            for name in ["xsum", "xmin", "xsq_lo", "xsq_hi", "isum", "imin", "isq_lo", "isq_hi"]:
+                h.update(np.ascontiguousarray(a[name][m], dtype="<u8").tobytes())
+        h.update(np.ascontiguousarray(a["xsamples"], dtype="<u8").tobytes())
+        h.update(np.ascontiguousarray(a["isamples"], dtype="<u8").tobytes())
+        for s in range(S):
+            h.update(np.ascontiguousarray(a["xstall"][s], dtype="<u8").tobytes())
+            h.update(np.ascontiguousarray(a["istall"][s], dtype="<u8").tobytes())
+        for name, dt in [("pc_ctx", "<u4"), ("pc_off", "<u4"), ("bin_pcnode", "<u4"), ("bin_stall", "<u2"),
+                         ("bin_count", "<u8")]:
+            h.update(np.ascontiguousarray(a[name], dtype=dt).tobytes())
+        h.update(np.ascontiguousarray(keys).tobytes())
+        return h.hexdigest()
+
     @property
     def n_nodes(self) -> int:
-        return int(self.view().n_nodes)
+        return int(self.view(before_rollup=True).n_nodes)
 
     def free(self):
         if getattr(self, "h", None):

@@ -77,6 +77,7 @@ def lib():
             "dc_ctx_launch_count": (u64, [P]),
             "dc_ctx_set_timing": (i32, [P, i32]),
             "dc_ctx_reserve": (i32, [P, u64]),
+            "dc_ctx_trim": (i32, [P, u64]),
             "dc_ctx_timer_report": (i32, [P, ctypes.c_char_p, ctypes.c_size_t]),
             "dc_intern_frames": (i32, [P, P, u64, P, ctypes.POINTER(P)]),
             "dc_dict_from_sorted": (i32, [P, P, u64, ctypes.POINTER(P)]),

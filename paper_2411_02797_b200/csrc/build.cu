@@ -1238,8 +1238,9 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
   const uint64_t R = p->n_records;
   if (R >= (1ull << 32)) return fail(c, DC_ERR_CAPACITY, "dc_cct_build: n_records >= 2^32");
   dc_cct* t = new dc_cct();
+  HandleGuard<dc_cct, dc_cct_free> guard{t};  // frees the handle and its arrays on any error return
   t->device = c->device;
-  t->owner_uid = c->uid;
+  t->owner_uid = adopt_handle(c);
   t->R = R;
   t->n_frames = n_frames;
   const int fbits = bits_for(n_frames > 0 ? n_frames - 1 : 0) > 0 ? bits_for(n_frames - 1) : 1;
@@ -1258,11 +1259,8 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
   DC_TRY(alloc(c, extra_rec, R));
   DC_TRY(alloc_zero(c, cnt, 8));  // [0] distinct, [1] extra, [2] compact pos, [3] overflow, [4] empty paths
   const int tma_ok = ((uintptr_t)p->offsets % 16 == 0) && ((uintptr_t)p->frames % 16 == 0) && !getenv("DC_TEST_NO_TMA");
-  static bool attr = false;
-  if (!attr) {
-    DC_CUDA(c, cudaFuncSetAttribute(k_path_hash, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PathSmem)));
-    attr = true;
-  }
+  // per device (context) attribute: set on every call
+  DC_CUDA(c, cudaFuncSetAttribute(k_path_hash, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PathSmem)));
   if (R) {
     int per_sm = 1;
     DC_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_path_hash, PT_THREADS, sizeof(PathSmem)));
@@ -1404,6 +1402,7 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
   c->host_collisions += n_extra;
   (void)levels;
   t->state = 0;
+  guard.h = nullptr;
   *out = t;
   return DC_OK;
 }

@@ -97,31 +97,58 @@ dc_status flags_status(Ctx* c, uint32_t f) {
   return DC_OK;
 }
 
+// Contexts and the handles they made. A handle's arrays come from its context's private pool;
+// the pool lives until the context is destroyed AND the last of its handles is freed.
+struct CtxEntry {
+  cudaStream_t stream;
+  cudaMemPool_t pool;
+  int device;
+  bool live;
+  uint64_t handles;
+};
 static std::mutex g_ctx_mu;
-static std::unordered_map<uint64_t, cudaStream_t> g_live_ctx;  // context uid -> its stream
+static std::unordered_map<uint64_t, CtxEntry> g_ctx;  // context uid -> entry
 static uint64_t g_next_uid = 1;
+static void drop_entry_locked(std::unordered_map<uint64_t, CtxEntry>::iterator it) {
+  cudaSetDevice(it->second.device);
+  cudaMemPoolDestroy(it->second.pool);
+  g_ctx.erase(it);
+}
 void register_ctx(Ctx* c, bool live) {
   std::lock_guard<std::mutex> g(g_ctx_mu);
   if (live) {
     c->uid = g_next_uid++;
-    g_live_ctx[c->uid] = c->stream;
-  } else {
-    g_live_ctx.erase(c->uid);
+    g_ctx[c->uid] = CtxEntry{c->stream, c->pool, c->device, true, 0};
+    return;
   }
+  auto it = g_ctx.find(c->uid);
+  if (it == g_ctx.end()) return;
+  it->second.live = false;
+  if (it->second.handles == 0) drop_entry_locked(it);
+}
+uint64_t adopt_handle(Ctx* c) {
+  std::lock_guard<std::mutex> g(g_ctx_mu);
+  auto it = g_ctx.find(c->uid);
+  if (it != g_ctx.end()) it->second.handles++;
+  return c->uid;
 }
 void free_handle_ptrs(uint64_t owner_uid, void* const* ps, size_t n) {
-  {
-    std::lock_guard<std::mutex> g(g_ctx_mu);
-    auto it = g_live_ctx.find(owner_uid);
-    if (it != g_live_ctx.end()) {  // stream-ordered: after every queued use on the context stream
-      for (size_t i = 0; i < n; ++i)
-        if (ps[i]) cudaFreeAsync(ps[i], it->second);
-      return;
-    }
+  std::lock_guard<std::mutex> g(g_ctx_mu);
+  auto it = g_ctx.find(owner_uid);
+  if (it == g_ctx.end()) return;  // not made by a context (nothing allocated)
+  CtxEntry& e = it->second;
+  if (e.live) {  // stream-ordered: after every queued use on the context stream
+    for (size_t i = 0; i < n; ++i)
+      if (ps[i]) cudaFreeAsync(ps[i], e.stream);
+  } else {  // the context is gone: free in order after all device work
+    cudaSetDevice(e.device);
+    cudaDeviceSynchronize();
+    for (size_t i = 0; i < n; ++i)
+      if (ps[i]) cudaFreeAsync(ps[i], 0);
+    cudaStreamSynchronize(0);
   }
-  cudaDeviceSynchronize();
-  for (size_t i = 0; i < n; ++i)
-    if (ps[i]) cudaFree(ps[i]);
+  if (e.handles) e.handles--;
+  if (!e.live && e.handles == 0) drop_entry_locked(it);
 }
 
 dc_status check_flags(Ctx* c) {
@@ -197,15 +224,26 @@ dc_status dc_ctx_create(int device, void* cuda_stream, dc_ctx** out) {
     if (b > 0 && b < 64) ctx->merge_mask = (1ull << b) - 1ull;
   }
   ctx->smem_optin = prop.sharedMemPerBlockOptin;
-  // keep freed pool memory cached (stream-ordered allocations are reused across calls)
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+  // the context's private pool; freed memory stays cached in it (stream-ordered allocations are
+  // reused across calls) without touching the device's default pool
+  {
+    cudaMemPoolProps pp = {};
+    pp.allocType = cudaMemAllocationTypePinned;
+    pp.handleTypes = cudaMemHandleTypeNone;
+    pp.location.type = cudaMemLocationTypeDevice;
+    pp.location.id = device;
+    if (cudaMemPoolCreate(&ctx->pool, &pp) != cudaSuccess) {
+      cudaGetLastError();
+      delete ctx;
+      return DC_ERR_CUDA;
+    }
     uint64_t thr = ~0ull;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
   if (cudaMalloc(&ctx->d_flags, 4) != cudaSuccess || cudaMalloc(&ctx->d_diag, DG_N * 8) != cudaSuccess ||
       cudaMallocHost(&ctx->h_pinned, 4096) != cudaSuccess) {
     cudaGetLastError();
+    cudaMemPoolDestroy(ctx->pool);
     delete ctx;
     return DC_ERR_OOM;
   }
@@ -244,13 +282,16 @@ dc_status dc_ctx_diag(dc_ctx* ctx, dc_diag* out_h) {
 void dc_ctx_destroy(dc_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
-  dc::register_ctx(ctx, false);  // handles outliving the context free synchronously from now on
+  cudaStreamSynchronize(ctx->stream);
   cudaStreamSynchronize(ctx->stream);
   cudaFree(ctx->d_flags);
   cudaFree(ctx->d_diag);
   cudaFreeHost(ctx->h_pinned);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  // outstanding handles keep their arrays: the pool is destroyed once the last one is freed
+  // (handles outliving the context free synchronously from now on)
+  dc::register_ctx(ctx, false);
   delete ctx;
 }
 
@@ -268,12 +309,20 @@ dc_status dc_ctx_reserve(dc_ctx* ctx, uint64_t bytes) {
   ON_DEVICE(ctx);
   if (!bytes) return DC_OK;
   void* p = nullptr;
-  if (cudaMallocAsync(&p, bytes, ctx->stream) != cudaSuccess) {
+  if (cudaMallocFromPoolAsync(&p, bytes, ctx->pool, ctx->stream) != cudaSuccess) {
     cudaGetLastError();
     return fail(ctx, DC_ERR_OOM, "dc_ctx_reserve: cannot reserve %llu bytes", (unsigned long long)bytes);
   }
   DC_CUDA(ctx, cudaFreeAsync(p, ctx->stream));
   DC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return DC_OK;
+}
+
+dc_status dc_ctx_trim(dc_ctx* ctx, uint64_t keep_bytes) {
+  CHECK_CTX(ctx);
+  ON_DEVICE(ctx);
+  DC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  DC_CUDA(ctx, cudaMemPoolTrimTo(ctx->pool, keep_bytes));
   return DC_OK;
 }
 
@@ -362,10 +411,14 @@ dc_status dc_cct_build(dc_ctx* ctx, const dc_paths* paths, const dc_dict* dict, 
   CHECK_CTX(ctx);
   ARG(paths && out, "paths/out is NULL");
   ARG(paths->offsets, "paths->offsets is NULL");
-  ARG(paths->n_records == 0 || paths->frames || true, "");
   ARG(!dict || dict->D == n_frames, "dictionary size %llu != n_frames %u", (unsigned long long)(dict ? dict->D : 0), n_frames);
   ARG(n_frames < 0xFFFFFFFFu, "n_frames must be < 2^32-1");
   ON_DEVICE(ctx);
+  if (!paths->frames && paths->n_records) {  // allowed only when every path is empty
+    uint64_t F = 0;
+    DC_TRY(readback(ctx, paths->offsets + paths->n_records, 8, &F));
+    ARG(F == 0, "paths->frames is NULL but offsets[n_records] = %llu", (unsigned long long)F);
+  }
   Region rg(ctx, "build");
   return cct_build(ctx, paths, dict, n_frames, out_leaf, out);
 }
@@ -398,7 +451,10 @@ dc_status dc_pc_sample_attribute(dc_ctx* ctx, dc_cct* cct, const dc_pc_sample* s
   ARG(n == 0 || s, "samples pointer is NULL");
   ARG(n_launch == 0 || launch_leaf, "launch_leaf is NULL");
   ARG(((uintptr_t)s & 15) == 0, "samples must be 16-byte aligned");
-  if (cct->pc_done) return fail(ctx, DC_ERR_STATE, "dc_pc_sample_attribute already called on this tree");
+  if (cct->partition) return fail(ctx, DC_ERR_STATE, "a merged partition is read-only");
+  // repeated calls accumulate (e.g. one call per chunk of samples); S is fixed by the first
+  if (cct->pc_done && n_stall != cct->S)
+    return fail(ctx, DC_ERR_ARG, "n_stall %u differs from the first call's %u", n_stall, cct->S);
   ON_DEVICE(ctx);
   Region rg(ctx, "pc");
   return pc_attribute(ctx, cct, s, n, launch_leaf, n_launch, launch_sample_off, n_stall);
@@ -509,6 +565,10 @@ dc_status dc_cct_view_get(const dc_cct* t, dc_cct_view* v) {
   v->bin_stall = t->bin_stall;
   v->bin_count = t->bin_count;
   v->state = t->state;
+  if (t->state != 2) {  // inclusive columns are defined only after dc_cct_rollup
+    v->icnt = v->isum = v->imin = v->isq_lo = v->isq_hi = v->isamples = v->istall = nullptr;
+    return DC_ERR_STATE;
+  }
   return DC_OK;
 }
 

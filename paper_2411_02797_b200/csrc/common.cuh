@@ -31,6 +31,10 @@ struct Ctx {
   uint64_t uid = 0;  // unique per context (handle frees look it up)
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  // the context's own stream-ordered memory pool: every library allocation comes from it, its
+  // release threshold (kept at "never release" so steady-state steps reuse memory) affects
+  // nothing else in the process, and dc_ctx_trim / dc_ctx_destroy hand the memory back
+  cudaMemPool_t pool = nullptr;
   std::string err;
   uint32_t* d_flags = nullptr;   // [1]
   uint64_t* d_diag = nullptr;    // [DG_N]
@@ -106,6 +110,7 @@ struct dc_ctx : dc::Ctx {};
 namespace dc {
 void register_ctx(Ctx* c, bool live);
 void free_handle_ptrs(uint64_t owner_uid, void* const* ps, size_t n);
+uint64_t adopt_handle(Ctx* c);  // a new handle of context c: returns its owner uid (c->uid)
 }  // namespace dc
 
 struct dc_dict {
@@ -146,6 +151,16 @@ struct dc_cct {
 enum { C_XSUM = 0, C_XMIN, C_XSQLO, C_XSQHI, C_ISUM, C_IMIN, C_ISQLO, C_ISQHI };
 
 namespace dc {
+
+// Scope guard of a library handle under construction: frees it (and every array it holds)
+// when an error returns early; set h = nullptr to hand it out.
+template <class H, void (*FreeFn)(H*)>
+struct HandleGuard {
+  H* h;
+  ~HandleGuard() {
+    if (h) FreeFn(h);
+  }
+};
 
 #define DC_TRY(expr)                      \
   do {                                    \
@@ -237,7 +252,7 @@ dc_status alloc(Ctx* c, Buf<T>& b, size_t n) {
   b.s = c->stream;
   b.n = n;
   if (n == 0) n = 1;
-  cudaError_t e = cudaMallocAsync((void**)&b.p, n * sizeof(T), c->stream);
+  cudaError_t e = cudaMallocFromPoolAsync((void**)&b.p, n * sizeof(T), c->pool, c->stream);
   if (e != cudaSuccess) {
     b.p = nullptr;
     cudaGetLastError();
@@ -255,7 +270,7 @@ dc_status alloc_zero(Ctx* c, Buf<T>& b, size_t n) {
 template <class T>
 dc_status palloc(Ctx* c, T*& p, size_t n) {
   HostRegion hr(c, "palloc");
-  cudaError_t e = cudaMallocAsync((void**)&p, (n ? n : 1) * sizeof(T), c->stream);
+  cudaError_t e = cudaMallocFromPoolAsync((void**)&p, (n ? n : 1) * sizeof(T), c->pool, c->stream);
   if (e != cudaSuccess) {
     p = nullptr;
     cudaGetLastError();

@@ -211,20 +211,19 @@ static uint64_t next_pow2(uint64_t v) {
 
 dc_status intern_frames(Ctx* c, const dc_frame_key* keys, uint64_t n, uint32_t* out_ids, dc_dict** out) {
   dc_dict* d = new dc_dict();
+  HandleGuard<dc_dict, dc_dict_free> guard{d};  // frees the dictionary on any error return
   d->device = c->device;
-  d->owner_uid = c->uid;
+  d->owner_uid = adopt_handle(c);
   *out = nullptr;
   if (n == 0) {
     d->D = 0;
     DC_TRY(palloc(c, d->keys, 1));
     DC_TRY(palloc(c, d->kinds, 1));
+    guard.h = nullptr;
     *out = d;
     return DC_OK;
   }
-  if (n >= (1ull << 32)) {
-    delete d;
-    return fail(c, DC_ERR_CAPACITY, "dc_intern_frames: n >= 2^32 keys");
-  }
+  if (n >= (1ull << 32)) return fail(c, DC_ERR_CAPACITY, "dc_intern_frames: n >= 2^32 keys");
   Buf<ulonglong2> table;
   Buf<unsigned long long> cnt, mx;
   Buf<uint32_t> ovf;
@@ -246,10 +245,7 @@ dc_status intern_frames(Ctx* c, const dc_frame_key* keys, uint64_t n, uint32_t* 
     D = h[0];
     bool overflow = (uint32_t)h[1] != 0;
     if (!overflow && D * 2 <= cap) break;
-    if (attempt == 1) {
-      delete d;
-      return fail(c, DC_ERR_CAPACITY, "dc_intern_frames: hash table overflow");
-    }
+    if (attempt == 1) return fail(c, DC_ERR_CAPACITY, "dc_intern_frames: hash table overflow");
     cap = next_pow2(2 * n);
     if (cap < 1024) cap = 1024;
   }
@@ -276,6 +272,7 @@ dc_status intern_frames(Ctx* c, const dc_frame_key* keys, uint64_t n, uint32_t* 
     dc_launch(k_intern_remap, grid_for(c, n, 256), 256, 0, c->stream, out_ids, n, rank_of_slot.p);
     DC_LAUNCHED(c);
     c->bytes_host += 20 * n + 16 * D;
+    guard.h = nullptr;
     *out = d;
     return DC_OK;
   }
@@ -299,14 +296,16 @@ dc_status intern_frames(Ctx* c, const dc_frame_key* keys, uint64_t n, uint32_t* 
   dc_launch(k_intern_remap, grid_for(c, n, 256), 256, 0, c->stream, out_ids, n, rank_of_slot.p);
   DC_LAUNCHED(c);
   c->bytes_host += 20 * n + 16 * D;
+  guard.h = nullptr;
   *out = d;
   return DC_OK;
 }
 
 dc_status dict_from_sorted(Ctx* c, const dc_frame_key* keys, uint64_t D, dc_dict** out) {
   dc_dict* d = new dc_dict();
+  HandleGuard<dc_dict, dc_dict_free> guard{d};
   d->device = c->device;
-  d->owner_uid = c->uid;
+  d->owner_uid = adopt_handle(c);
   d->D = D;
   DC_TRY(palloc(c, d->keys, D));
   DC_TRY(palloc(c, d->kinds, D));
@@ -315,6 +314,7 @@ dc_status dict_from_sorted(Ctx* c, const dc_frame_key* keys, uint64_t D, dc_dict
     dc_launch(k_kinds_of, grid_for(c, D, 256), 256, 0, c->stream, d->keys, d->kinds, D);
     DC_LAUNCHED(c);
   }
+  guard.h = nullptr;
   *out = d;
   return DC_OK;
 }

@@ -374,7 +374,7 @@ static dc_cct* make_partition(Ctx* c, const RecFmt& f, uint64_t n_nodes, Buf<uin
                               Buf<uint64_t>& bins, uint32_t n_frames) {
   dc_cct* t = new dc_cct();
   t->device = c->device;
-  t->owner_uid = c->uid;
+  t->owner_uid = adopt_handle(c);
   t->M = f.M;
   t->S = f.has_pc ? f.S : 0;
   t->N = n_nodes;
@@ -543,7 +543,7 @@ static dc_status canonicalize(Ctx* c, const uint64_t* rec, uint64_t n, const uin
   if (lvl[1] != 1) return fail(c, DC_ERR_COLLISION, "merge: %u root records", lvl[1]);
   dc_cct* t = new dc_cct();
   t->device = c->device;
-  t->owner_uid = c->uid;
+  t->owner_uid = adopt_handle(c);
   t->N = n;
   t->n_frames = n_frames;
   t->max_depth = L - 1;
@@ -754,19 +754,29 @@ dc_status dc_cct_merge_ranks(dc_ctx* ctx, dc_comm* cm, const dc_cct* local, cons
   DC_CUDA(c, cudaSetDevice(c->device));
   Region rg(c, "merge");
   const int P = cm->nranks;
-  // 1. dictionaries: all-gather sizes, then keys padded to the max size
+  // 1. dictionaries: all-gather sizes together with each rank's record format (M, S, has_pc);
+  // every rank sees the same table, so a disagreement fails on every rank before any transfer
   Buf<uint64_t> dsz;
-  DC_TRY(alloc(c, dsz, P));
-  uint64_t myD = local_dict->D;
-  DC_CUDA(c, cudaMemcpyAsync(dsz.p + cm->rank, &myD, 8, cudaMemcpyHostToDevice, c->stream));
-  NCCL_TRY(c, ncclAllGather(dsz.p + cm->rank, dsz.p, 1, ncclUint64, cm->comm, c->stream));
-  std::vector<uint64_t> Ds(P);
-  DC_TRY(readback(c, dsz.p, 8 * P, Ds.data()));
+  DC_TRY(alloc(c, dsz, 4 * (uint64_t)P));
+  const RecFmt f = fmt_of(local);
+  const uint64_t mine[4] = {local_dict->D, local->M, f.has_pc ? local->S : 0, f.has_pc ? 1u : 0u};
+  DC_CUDA(c, cudaMemcpyAsync(dsz.p + 4 * cm->rank, mine, 32, cudaMemcpyHostToDevice, c->stream));
+  NCCL_TRY(c, ncclAllGather(dsz.p + 4 * cm->rank, dsz.p, 4, ncclUint64, cm->comm, c->stream));
+  std::vector<uint64_t> tab(4 * (size_t)P), Ds(P);
+  DC_TRY(readback(c, dsz.p, 32 * (size_t)P, tab.data()));
+  for (int p = 0; p < P; ++p) {
+    Ds[p] = tab[4 * p];
+    if (tab[4 * p + 1] != tab[1] || tab[4 * p + 2] != tab[2] || tab[4 * p + 3] != tab[3])
+      return fail(c, DC_ERR_ARG, "merge: rank %d has (M=%llu, S=%llu, pc=%llu) but rank 0 has (M=%llu, S=%llu, pc=%llu)", p,
+                  (unsigned long long)tab[4 * p + 1], (unsigned long long)tab[4 * p + 2], (unsigned long long)tab[4 * p + 3],
+                  (unsigned long long)tab[1], (unsigned long long)tab[2], (unsigned long long)tab[3]);
+  }
   uint64_t Dmax = 1;
   for (auto d : Ds) Dmax = d > Dmax ? d : Dmax;
   Buf<dc_frame_key> pad, all, packed;
   DC_TRY(alloc(c, pad, Dmax));
   DC_TRY(alloc(c, all, Dmax * P));
+  const uint64_t myD = local_dict->D;
   if (myD) DC_CUDA(c, cudaMemcpyAsync(pad.p, local_dict->keys, myD * 16, cudaMemcpyDeviceToDevice, c->stream));
   NCCL_TRY(c, ncclAllGather(pad.p, all.p, Dmax * 2, ncclUint64, cm->comm, c->stream));
   std::vector<uint64_t> koff(P + 1, 0);
@@ -778,7 +788,6 @@ dc_status dc_cct_merge_ranks(dc_ctx* ctx, dc_comm* cm, const dc_cct* local, cons
   std::vector<Buf<uint32_t>> l2g;
   DC_TRY(unify_dicts(c, packed.p, koff, &gd, l2g));
   // 2-3. hash + partition
-  const RecFmt f = fmt_of(local);
   Slabs s;
   DC_TRY(partition(c, local, l2g[cm->rank].p, P, f, s));
   // 4. exchange counts, then slabs

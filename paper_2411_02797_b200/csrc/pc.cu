@@ -129,18 +129,213 @@ static uint64_t np2(uint64_t v) {
   return p;
 }
 
+// ---------------------------------------------------------------- repeated calls (chunks)
+// A later call's bins and PC nodes are merged exactly with the earlier ones: both bin lists are
+// in canonical (ctx, pc, stall) order with unique keys, so after one sort of their union an
+// equal key occurs at most twice (adjacent); the first of a run emits the bin with both counts.
+__global__ void k_pc_binkeys(const uint32_t* __restrict__ pc_ctx, const uint32_t* __restrict__ pc_off,
+                             const uint32_t* __restrict__ bin_pcnode, const uint16_t* __restrict__ bin_stall,
+                             const uint64_t* __restrict__ bin_count, uint64_t nb, uint64_t N, int pcb,
+                             uint64_t* __restrict__ keys, uint64_t* __restrict__ cnts) { DC_PDL_ENTER();
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nb; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t p = bin_pcnode[i] - N;
+    keys[i] = ((((uint64_t)pc_ctx[p] << pcb) | pc_off[p]) << 5) | bin_stall[i];
+    cnts[i] = bin_count[i];
+  }
+}
+
+__global__ void k_pc_maxoff(const uint32_t* __restrict__ a, uint64_t n, unsigned int* d_max) { DC_PDL_ENTER();
+  uint32_t m = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) m = max(m, a[i]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane_id() == 0 && m) atomicMax(d_max, m);
+}
+
+// hb = first of an equal-key run (a bin), hp = first bin of a (ctx, pc) run (a PC node)
+__global__ void k_pc_mheads(const uint64_t* __restrict__ k, uint64_t nb, uint32_t* __restrict__ hb, uint32_t* __restrict__ hp) { DC_PDL_ENTER();
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nb; i += (uint64_t)gridDim.x * blockDim.x) {
+    const bool b = i == 0 || k[i - 1] != k[i];
+    hb[i] = b;
+    hp[i] = b && (i == 0 || (k[i - 1] >> 5) != (k[i] >> 5));
+  }
+}
+
+__global__ void k_pc_memit(const uint64_t* __restrict__ k, const uint32_t* __restrict__ ord, const uint64_t* __restrict__ cnts,
+                           uint64_t nb, int pcb, const uint32_t* __restrict__ hb, const uint32_t* __restrict__ hp,
+                           const uint32_t* __restrict__ bidx, const uint32_t* __restrict__ pidx, uint64_t N,
+                           uint32_t* __restrict__ pc_ctx, uint32_t* __restrict__ pc_off, uint32_t* __restrict__ bin_pcnode,
+                           uint16_t* __restrict__ bin_stall, uint64_t* __restrict__ bin_count) { DC_PDL_ENTER();
+  const uint64_t pcmask = (1ull << pcb) - 1ull;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nb; i += (uint64_t)gridDim.x * blockDim.x) {
+    if (!hb[i]) continue;
+    const uint64_t key = k[i], cp = key >> 5;
+    const uint32_t p = pidx[i] + hp[i] - 1u, b = bidx[i];
+    if (hp[i]) {
+      pc_ctx[p] = (uint32_t)(cp >> pcb);
+      pc_off[p] = (uint32_t)(cp & pcmask);
+    }
+    uint64_t cnt = cnts[ord[i]];
+    if (i + 1 < nb && k[i + 1] == key) cnt += cnts[ord[i + 1]];
+    bin_pcnode[b] = (uint32_t)(N + p);
+    bin_stall[b] = (uint16_t)(key & 31u);
+    bin_count[b] = cnt;
+  }
+}
+
+__global__ void k_add_u64(uint64_t* __restrict__ dst, const uint64_t* __restrict__ src, uint64_t n) { DC_PDL_ENTER();
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) dst[i] += src[i];
+}
+
+struct PcPrev {  // the tree's PC results before a repeated call
+  uint64_t *xsamples = nullptr, *xstall = nullptr, *bin_count = nullptr;
+  uint32_t *pc_ctx = nullptr, *pc_off = nullptr, *bin_pcnode = nullptr;
+  uint16_t* bin_stall = nullptr;
+  uint64_t Npc = 0, Nbins = 0;
+};
+
+static dc_status pc_merge_prev(Ctx* c, dc_cct* t, const PcPrev& o) {
+  const uint64_t N = t->N, S = t->S;
+  dc_launch(k_add_u64, grid_for(c, N, 256), 256, 0, c->stream, t->xsamples, o.xsamples, N);
+  DC_LAUNCHED(c);
+  dc_launch(k_add_u64, grid_for(c, S * N, 256), 256, 0, c->stream, t->xstall, o.xstall, S * N);
+  DC_LAUNCHED(c);
+  const uint64_t na = o.Nbins, nbn = t->Nbins, nb = na + nbn;
+  if (nb >= (1ull << 32)) return fail(c, DC_ERR_CAPACITY, "more than 2^32 PC bins");
+  Buf<unsigned int> mx;
+  DC_TRY(alloc_zero(c, mx, 1));
+  if (o.Npc) {
+    dc_launch(k_pc_maxoff, grid_for(c, o.Npc, 256), 256, 0, c->stream, o.pc_off, o.Npc, mx.p);
+    DC_LAUNCHED(c);
+  }
+  if (t->Npc) {
+    dc_launch(k_pc_maxoff, grid_for(c, t->Npc, 256), 256, 0, c->stream, t->pc_off, t->Npc, mx.p);
+    DC_LAUNCHED(c);
+  }
+  uint32_t hmax = 0;
+  DC_TRY(readback(c, mx.p, 4, &hmax));
+  int pcb = bits_for(hmax);
+  if (pcb == 0) pcb = 1;
+  const int kbits = bits_for(N > 1 ? N - 1 : 1) + pcb + 5;
+  if (kbits > 64) return fail(c, DC_ERR_CAPACITY, "PC bin sort key exceeds 64 bits");
+  Buf<uint64_t> k0, k1, cnts;
+  Buf<uint32_t> v0, v1, hb, hp, bidx, pidx, tot;
+  DC_TRY(alloc(c, k0, nb));
+  DC_TRY(alloc(c, k1, nb));
+  DC_TRY(alloc(c, cnts, nb));
+  DC_TRY(alloc(c, v0, nb));
+  DC_TRY(alloc(c, v1, nb));
+  if (na) {
+    dc_launch(k_pc_binkeys, grid_for(c, na, 256), 256, 0, c->stream, o.pc_ctx, o.pc_off, o.bin_pcnode, o.bin_stall, o.bin_count, na,
+              N, pcb, k0.p, cnts.p);
+    DC_LAUNCHED(c);
+  }
+  if (nbn) {
+    dc_launch(k_pc_binkeys, grid_for(c, nbn, 256), 256, 0, c->stream, t->pc_ctx, t->pc_off, t->bin_pcnode, t->bin_stall,
+              t->bin_count, nbn, N, pcb, k0.p + na, cnts.p + na);
+    DC_LAUNCHED(c);
+  }
+  dc_launch(k_iota32, grid_for(c, nb, 256), 256, 0, c->stream, v0.p, nb);
+  DC_LAUNCHED(c);
+  bool in1 = false;
+  DC_TRY(radix_sort_pairs(c, k0.p, v0.p, k1.p, v1.p, nb, 0, kbits, &in1));
+  const uint64_t* sk = in1 ? k1.p : k0.p;
+  const uint32_t* so = in1 ? v1.p : v0.p;
+  DC_TRY(alloc(c, hb, nb));
+  DC_TRY(alloc(c, hp, nb));
+  DC_TRY(alloc(c, bidx, nb));
+  DC_TRY(alloc(c, pidx, nb));
+  DC_TRY(alloc_zero(c, tot, 2));
+  if (nb) {
+    dc_launch(k_pc_mheads, grid_for(c, nb, 256), 256, 0, c->stream, sk, nb, hb.p, hp.p);
+    DC_LAUNCHED(c);
+    DC_TRY((excl_scan_pair<uint32_t, uint32_t>(c, hb.p, bidx.p, tot.p, hp.p, pidx.p, tot.p + 1, nb)));
+  }
+  uint32_t ht[2] = {0, 0};
+  DC_TRY(readback(c, tot.p, 8, ht));
+  void* stale[] = {t->pc_ctx, t->pc_off, t->bin_pcnode, t->bin_stall, t->bin_count};
+  t->pc_ctx = t->pc_off = t->bin_pcnode = nullptr;
+  t->bin_stall = nullptr;
+  t->bin_count = nullptr;
+  for (void* q : stale) cudaFreeAsync(q, c->stream);
+  t->Nbins = ht[0];
+  t->Npc = ht[1];
+  DC_TRY(palloc(c, t->pc_ctx, t->Npc));
+  DC_TRY(palloc(c, t->pc_off, t->Npc));
+  DC_TRY(palloc(c, t->bin_pcnode, t->Nbins));
+  DC_TRY(palloc(c, t->bin_stall, t->Nbins));
+  DC_TRY(palloc(c, t->bin_count, t->Nbins));
+  if (nb) {
+    dc_launch(k_pc_memit, grid_for(c, nb, 256), 256, 0, c->stream, sk, so, cnts.p, nb, pcb, hb.p, hp.p, bidx.p, pidx.p, N, t->pc_ctx,
+              t->pc_off, t->bin_pcnode, t->bin_stall, t->bin_count);
+    DC_LAUNCHED(c);
+  }
+  return DC_OK;
+}
+
+static dc_status pc_attribute_once(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, const uint32_t* launch_leaf,
+                                   uint64_t n_launch, const uint64_t* launch_off, uint32_t S);
+
 dc_status pc_attribute(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, const uint32_t* launch_leaf, uint64_t n_launch,
                        const uint64_t* launch_off, uint32_t S) {
   const uint64_t N = t->N;
-  t->S = S;
-  DC_TRY(palloc(c, t->xsamples, N));
-  DC_TRY(palloc(c, t->isamples, N));
-  DC_TRY(palloc(c, t->xstall, (uint64_t)S * N));
-  DC_TRY(palloc(c, t->istall, (uint64_t)S * N));
-  DC_CUDA(c, cudaMemsetAsync(t->xsamples, 0, N * 8, c->stream));
-  DC_CUDA(c, cudaMemsetAsync(t->isamples, 0, N * 8, c->stream));
-  DC_CUDA(c, cudaMemsetAsync(t->xstall, 0, (uint64_t)S * N * 8, c->stream));
-  DC_CUDA(c, cudaMemsetAsync(t->istall, 0, (uint64_t)S * N * 8, c->stream));
+  if (!t->pc_done) {  // first call: the tree's sample columns, zeroed
+    t->S = S;
+    DC_TRY(palloc(c, t->xsamples, N));
+    DC_TRY(palloc(c, t->isamples, N));
+    DC_TRY(palloc(c, t->xstall, (uint64_t)S * N));
+    DC_TRY(palloc(c, t->istall, (uint64_t)S * N));
+    DC_CUDA(c, cudaMemsetAsync(t->xsamples, 0, N * 8, c->stream));
+    DC_CUDA(c, cudaMemsetAsync(t->isamples, 0, N * 8, c->stream));
+    DC_CUDA(c, cudaMemsetAsync(t->xstall, 0, (uint64_t)S * N * 8, c->stream));
+    DC_CUDA(c, cudaMemsetAsync(t->istall, 0, (uint64_t)S * N * 8, c->stream));
+    return pc_attribute_once(c, t, s, n, launch_leaf, n_launch, launch_off, S);
+  }
+  // a later call (e.g. the next chunk of samples, "flushes the metrics" per
+  // buffer): this call's bins and exclusive columns are computed on their own, then merged
+  PcPrev o;
+  o.xsamples = t->xsamples;
+  o.xstall = t->xstall;
+  o.pc_ctx = t->pc_ctx;
+  o.pc_off = t->pc_off;
+  o.bin_pcnode = t->bin_pcnode;
+  o.bin_stall = t->bin_stall;
+  o.bin_count = t->bin_count;
+  o.Npc = t->Npc;
+  o.Nbins = t->Nbins;
+  t->xsamples = t->xstall = t->bin_count = nullptr;
+  t->pc_ctx = t->pc_off = t->bin_pcnode = nullptr;
+  t->bin_stall = nullptr;
+  t->Npc = t->Nbins = 0;
+  dc_status st = palloc(c, t->xsamples, N);
+  if (st == DC_OK) st = palloc(c, t->xstall, (uint64_t)S * N);
+  if (st == DC_OK && cudaMemsetAsync(t->xsamples, 0, N * 8, c->stream) != cudaSuccess) st = fail(c, DC_ERR_CUDA, "memset");
+  if (st == DC_OK && cudaMemsetAsync(t->xstall, 0, (uint64_t)S * N * 8, c->stream) != cudaSuccess) st = fail(c, DC_ERR_CUDA, "memset");
+  if (st == DC_OK) st = pc_attribute_once(c, t, s, n, launch_leaf, n_launch, launch_off, S);
+  if (st == DC_OK) st = pc_merge_prev(c, t, o);
+  if (st != DC_OK) {  // keep the earlier results: the handle stays valid, this call had no effect
+    void* cur[] = {t->xsamples, t->xstall, t->pc_ctx, t->pc_off, t->bin_pcnode, t->bin_stall, t->bin_count};
+    for (void* q : cur) if (q) cudaFreeAsync(q, c->stream);
+    t->xsamples = o.xsamples;
+    t->xstall = o.xstall;
+    t->pc_ctx = o.pc_ctx;
+    t->pc_off = o.pc_off;
+    t->bin_pcnode = o.bin_pcnode;
+    t->bin_stall = o.bin_stall;
+    t->bin_count = o.bin_count;
+    t->Npc = o.Npc;
+    t->Nbins = o.Nbins;
+    return st;
+  }
+  void* prev[] = {o.xsamples, o.xstall, o.pc_ctx, o.pc_off, o.bin_pcnode, o.bin_stall, o.bin_count};
+  for (void* q : prev) if (q) cudaFreeAsync(q, c->stream);
+  t->state = 1;
+  return DC_OK;
+}
+
+static dc_status pc_attribute_once(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, const uint32_t* launch_leaf,
+                                   uint64_t n_launch, const uint64_t* launch_off, uint32_t S) {
+  const uint64_t N = t->N;
   // -------- histogram into (sort key, count) pairs
   Buf<uint64_t> keys, cnts, keys2;
   uint64_t nb = 0;

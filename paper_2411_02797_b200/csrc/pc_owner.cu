@@ -1660,11 +1660,7 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
   DC_TRY(alloc(c, pbase, n_groups));
   DC_TRY(alloc(c, tots, 2));
   const size_t rsmem = sizeof(RedSmem);
-  static bool rattr_set = false;
-  if (!rattr_set) {
-    DC_CUDA(c, cudaFuncSetAttribute(k_own_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem));
-    rattr_set = true;
-  }
+  DC_CUDA(c, cudaFuncSetAttribute(k_own_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem));  // per device
   {
     Region rk(c, "k:own_reduce");
     dc_launch(k_own_reduce, n_groups < (uint32_t)G ? n_groups : G, RD_THREADS, rsmem, c->stream, seg.p, sso, grp_start.p, n_groups, gout.p, pkey.p, pcnt.p, N, okey.p, ocnt.p, gnb.p, gnp.p, gctx.p,

@@ -335,46 +335,6 @@ def test_permutation_invariance_and_determinism():
     assert np.array_equal(a["leaf"][perm], b["leaf"])
 
 
-def test_full_size_config3_sampled_contexts():
-    """BASELINE config 3 at full size (100M samples) in the bench's launch configuration:
-    exact per-context parity for sampled contexts (the oracle on just those launches' samples),
-    conservation for the rest."""
-    import torch
-    import paper_2411_02797_b200 as dc
-    p = gen.programs.config3()
-    tr = gen.make_trace(p, pc=True, device="cuda")
-    ctx = dc.Context(0)
-    ids, d = dc.dc_intern_frames(ctx, tr.keys)
-    cct, leaf = dc.dc_cct_build(ctx, tr.offsets, ids, d.size, d)
-    dc.dc_cct_attribute_metrics(ctx, cct, leaf, tr.metrics)
-    dc.dc_pc_sample_attribute(ctx, cct, tr.samples, leaf, tr.launch_off, n_stall=24)
-    dc.dc_cct_rollup(ctx, cct)
-    a = cct.to_numpy()
-    assert int(a["bin_count"].sum()) == 100_000_000 == int(a["isamples"][0])
-    leaf_np = leaf.cpu().numpy().view(np.uint32)
-    lo = tr.launch_off.cpu().numpy().view(np.uint64)
-    S = tr.samples.cpu().numpy()
-    rng = np.random.default_rng(0)
-    ctxs = rng.choice(np.unique(leaf_np), size=4, replace=False)
-    for cnode in ctxs:
-        launches = np.nonzero(leaf_np == cnode)[0]
-        sub = np.concatenate([S[lo[l]:lo[l + 1]] for l in launches])
-        # oracle over a single record with that context's path -> bins of that context
-        o = oracle.OracleCCT(1, 24).insert(np.array([0, 1], np.uint64), np.array([0], np.uint32), np.zeros((1, 1), np.uint64))
-        sub = sub.copy()
-        sub[:, 0] = 0
-        o.pc(sub, 1)
-        r = o.finalize().arrays()
-        sel = a["pc_ctx"] == cnode
-        pcnodes = np.nonzero(sel)[0] + a["n_nodes"]
-        assert np.array_equal(a["pc_off"][sel], r["pc_off"])
-        bsel = np.isin(a["bin_pcnode"], pcnodes)
-        assert np.array_equal(a["bin_stall"][bsel], r["bin_stall"])
-        assert np.array_equal(a["bin_count"][bsel], r["bin_count"])
-        assert a["xsamples"][cnode] == r["xsamples"][1]
-    del torch
-
-
 @pytest.mark.parametrize("env", [{}, {"DC_TEST_LEVELWISE": "1"}, {"DC_TEST_WEAK_NODE_HASH": "7"}, {"DC_TEST_NO_TMA": "1"}])
 def test_large_P_build_variants(monkeypatch, env):
     """> 4096 distinct paths, deep recursion and shared prefixes: the Euler-tour build, the
