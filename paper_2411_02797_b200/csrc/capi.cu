@@ -166,6 +166,32 @@ dc_status check_flags(Ctx* c) {
   return DC_OK;
 }
 
+dc_status scan_state(Ctx* c, uint64_t n_tiles, uint64_t** flag, uint64_t** val, uint64_t* seq, Buf<uint64_t>& tmp) {
+  constexpr uint64_t CAP = 1ull << 16;
+  if (!c->scan_ctr) {  // first use: persistent, zeroed once (flags carry a call sequence number)
+    if (cudaMalloc(&c->scan_flag, CAP * 8) != cudaSuccess || cudaMalloc(&c->scan_val, 4 * CAP * 8) != cudaSuccess ||
+        cudaMalloc(&c->scan_ctr, 8) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(c, DC_ERR_OOM, "scan state allocation failed");
+    }
+    DC_CUDA(c, cudaMemsetAsync(c->scan_flag, 0, CAP * 8, c->stream));
+    DC_CUDA(c, cudaMemsetAsync(c->scan_ctr, 0, 8, c->stream));
+    c->scan_cap = CAP;
+  }
+  if (n_tiles <= c->scan_cap) {
+    *flag = c->scan_flag;
+    *val = c->scan_val;
+    *seq = ++c->scan_seq;
+    return DC_OK;
+  }
+  // more tiles than the persistent state holds: fresh zeroed state for this call
+  DC_TRY(alloc_zero(c, tmp, 5 * n_tiles));
+  *flag = tmp.p;
+  *val = tmp.p + n_tiles;
+  *seq = 1;
+  return DC_OK;
+}
+
 __global__ void k_add_diag(unsigned long long* dst, const unsigned long long* src) { DC_PDL_ENTER();
   if (threadIdx.x < DG_N) dst[threadIdx.x] += src[threadIdx.x];
 }
@@ -286,6 +312,9 @@ void dc_ctx_destroy(dc_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   cudaFree(ctx->d_flags);
   cudaFree(ctx->d_diag);
+  cudaFree(ctx->scan_flag);
+  cudaFree(ctx->scan_val);
+  cudaFree(ctx->scan_ctr);
   cudaFreeHost(ctx->h_pinned);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);

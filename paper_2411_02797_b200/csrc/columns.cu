@@ -388,10 +388,109 @@ __global__ void __launch_bounds__(256) k_rollup_levels(RollArgs a) { DC_PDL_ENTE
   }
 }
 
+// Small trees (N <= RC_MAX_N, configs 1-3, 5): one CTA per inclusive column holds the whole
+// column in shared memory and walks the levels bottom-up (children contiguous, level_off gives
+// each level's range): every node of level d adds (or min-s) its final value into its parent's
+// slot with a shared-memory atomic, one barrier per level. The u128 square sums go as four
+// 32-bit limb columns (each sum < 2^32 * N < 2^64, exact), folded by k_roll_fold. Every
+// inclusive column is written whole (no copy of the exclusive block first): 2 launches.
+// Column c: 0 count; 1 + 6m + {0 sum, 1 min, 2..5 square limb 0..3}; 1 + 6M samples; 2 + 6M + s stall s.
+constexpr uint32_t RC_MAX_N = 26u << 10;
+constexpr int RC_THREADS = 1024;
+__global__ void __launch_bounds__(RC_THREADS, 1) k_roll_cols(const uint32_t* __restrict__ parent, const uint32_t* __restrict__ level_off,
+                                                            uint32_t maxd, uint32_t N, uint32_t M, const uint64_t* __restrict__ xcnt,
+                                                            uint64_t* __restrict__ icnt, uint64_t* __restrict__ mcols,
+                                                            uint64_t* __restrict__ limbs, const uint64_t* __restrict__ xsamples,
+                                                            uint64_t* __restrict__ isamples, const uint64_t* __restrict__ xstall,
+                                                            uint64_t* __restrict__ istall) { DC_PDL_ENTER();
+  extern __shared__ unsigned long long racc[];
+  const uint32_t col = blockIdx.x, tid = threadIdx.x;
+  const uint64_t* src;
+  uint64_t* dst;
+  bool is_min = false;
+  int limb = -1;
+  if (col == 0) {
+    src = xcnt;
+    dst = icnt;
+  } else if (col <= 6 * M) {
+    const uint32_t m = (col - 1) / 6, r = (col - 1) % 6;
+    if (r == 0) {
+      src = mcols + ((uint64_t)C_XSUM * M + m) * N;
+      dst = mcols + ((uint64_t)C_ISUM * M + m) * N;
+    } else if (r == 1) {
+      src = mcols + ((uint64_t)C_XMIN * M + m) * N;
+      dst = mcols + ((uint64_t)C_IMIN * M + m) * N;
+      is_min = true;
+    } else {
+      limb = (int)r - 2;
+      src = mcols + ((uint64_t)(limb < 2 ? C_XSQLO : C_XSQHI) * M + m) * N;
+      dst = limbs + ((uint64_t)m * 4 + limb) * N;
+    }
+  } else if (col == 6 * M + 1) {
+    src = xsamples;
+    dst = isamples;
+  } else {
+    const uint64_t st = col - 6 * M - 2;
+    src = xstall + st * N;
+    dst = istall + st * N;
+  }
+  for (uint32_t i = tid; i < N; i += RC_THREADS) {
+    uint64_t v = src[i];
+    if (limb >= 0) v = (limb & 1) ? v >> 32 : v & 0xFFFFFFFFull;
+    racc[i] = v;
+  }
+  __syncthreads();
+  for (uint32_t d = maxd; d >= 1; --d) {
+    const uint32_t lo = level_off[d], hi = level_off[d + 1];
+    for (uint32_t n = lo + tid; n < hi; n += RC_THREADS) {
+      const unsigned long long v = racc[n];
+      const uint32_t p = __ldg(parent + n);
+      if (is_min) {
+        if (v != ~0ull) atomicMin(&racc[p], v);
+      } else if (v) {
+        atomicAdd(&racc[p], v);
+      }
+    }
+    __syncthreads();
+  }
+  for (uint32_t i = tid; i < N; i += RC_THREADS) dst[i] = racc[i];
+}
+
+// inclusive (sq_lo, sq_hi) = L0 + L1 * 2^32 + L2 * 2^64 + L3 * 2^96 (the u128 total fits)
+__global__ void k_roll_fold(uint64_t N, uint32_t M, const uint64_t* __restrict__ limbs, uint64_t* __restrict__ mcols) { DC_PDL_ENTER();
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < (uint64_t)M * N; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t m = i / N, n = i % N;
+    const uint64_t* L = limbs + m * 4 * N;
+    const uint64_t l0 = L[n], l1 = L[N + n], l2 = L[2 * N + n], l3 = L[3 * N + n];
+    const uint64_t lo = l0 + (l1 << 32);
+    const uint64_t hi = (l1 >> 32) + l2 + (l3 << 32) + (lo < l0 ? 1u : 0u);
+    mcols[((uint64_t)C_ISQLO * M + m) * N + n] = lo;
+    mcols[((uint64_t)C_ISQHI * M + m) * N + n] = hi;
+  }
+}
+
 dc_status rollup(Ctx* c, dc_cct* t) {
   const uint64_t N = t->N;
   const uint32_t M = t->M, S = t->S;
   cudaStream_t s = c->stream;
+  if (N > 1 && N <= RC_MAX_N && !getenv("DC_TEST_ROLLUP_PUSH") && !getenv("DC_TEST_ROLLUP_LEVELS") &&
+      !getenv("DC_TEST_ROLLUP_PUSH_RETURNED")) {
+    Buf<uint64_t> limbs;
+    if (M) DC_TRY(alloc(c, limbs, 4ull * M * N));
+    const uint32_t cols = 1 + 6 * M + (t->xsamples ? 1 + S : 0);
+    const size_t smem = N * 8;
+    DC_CUDA(c, cudaFuncSetAttribute(k_roll_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dc_launch(k_roll_cols, cols, RC_THREADS, smem, s, t->parent, t->level_off, t->max_depth, (uint32_t)N, M, t->xcnt, t->icnt,
+              t->mcols, limbs.p, t->xsamples, t->isamples, t->xstall, t->istall);
+    DC_LAUNCHED(c);
+    if (M) {
+      dc_launch(k_roll_fold, grid_for(c, (uint64_t)M * N, 256), 256, 0, s, N, M, limbs.p, t->mcols);
+      DC_LAUNCHED(c);
+    }
+    t->state = 2;
+    c->bytes_host += (2 * (8 + 32ull * M) + 4) * N;
+    return DC_OK;
+  }
   DC_CUDA(c, cudaMemcpyAsync(t->icnt, t->xcnt, N * 8, cudaMemcpyDeviceToDevice, s));
   // the exclusive block [xsum, xmin, xsq_lo, xsq_hi][M][N] is contiguous, and so is the inclusive one
   if (M) DC_CUDA(c, cudaMemcpyAsync(t->col(C_ISUM, 0), t->col(C_XSUM, 0), 4ull * M * N * 8, cudaMemcpyDeviceToDevice, s));
@@ -403,8 +502,8 @@ dc_status rollup(Ctx* c, dc_cct* t) {
   // walk cost of the per-node ancestor push ~ N * depth; deep / large trees go level by level
   const bool levels = ((uint64_t)N * t->max_depth > (16ull << 20) || getenv("DC_TEST_ROLLUP_LEVELS")) && !getenv("DC_TEST_ROLLUP_PUSH");
   if (N > 1 && levels) {
-    static int per_sm = 0;
-    if (!per_sm) DC_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rollup_levels, 256, 0));
+    int per_sm = 0;
+    DC_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rollup_levels, 256, 0));
     Buf<unsigned int> bar;
     DC_TRY(alloc_zero(c, bar, 2));
     RollArgs ra{t->parent, t->level_off, t->max_depth, N, M, S, G, (unsigned long long*)t->icnt, (unsigned long long*)t->mcols,

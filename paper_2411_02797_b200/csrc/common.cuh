@@ -35,6 +35,11 @@ struct Ctx {
   // release threshold (kept at "never release" so steady-state steps reuse memory) affects
   // nothing else in the process, and dc_ctx_trim / dc_ctx_destroy hand the memory back
   cudaMemPool_t pool = nullptr;
+  // chained-scan tile state (prim.cuh): flags [scan_cap], values [4 * scan_cap], ticket counter
+  uint64_t* scan_flag = nullptr;
+  uint64_t* scan_val = nullptr;
+  unsigned long long* scan_ctr = nullptr;
+  uint64_t scan_cap = 0, scan_seq = 0, scan_tickets = 0;
   std::string err;
   uint32_t* d_flags = nullptr;   // [1]
   uint64_t* d_diag = nullptr;    // [DG_N]

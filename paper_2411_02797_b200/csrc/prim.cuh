@@ -1,14 +1,10 @@
 // prim.cuh — device-wide primitives of libdc (own implementations, no CUB on the hot path):
-// exclusive scan (reduce-then-scan, 3 phases) and a stable LSD radix sort of
+// exclusive scan (single pass, decoupled look-back) and a stable LSD radix sort of
 // (u64 key, u32 value) pairs over the significant bit range only.
 #pragma once
 #include "common.cuh"
 
 namespace dc {
-
-constexpr int SCAN_THREADS = 256;
-constexpr int SCAN_ITEMS = 16;
-constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
 
 template <class T>
 __device__ __forceinline__ T warp_incl_scan(T v) {
@@ -45,166 +41,159 @@ __device__ __forceinline__ T block_excl_scan(T v, T* total) {
   return excl;
 }
 
-template <class T>
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan_reduce(const T* __restrict__ in, uint64_t n, T* __restrict__ sums) { DC_PDL_ENTER();
-  const uint64_t base = (uint64_t)blockIdx.x * SCAN_TILE;
-  T s = 0;
-#pragma unroll
-  for (int i = 0; i < SCAN_ITEMS; ++i) {
-    uint64_t j = base + (uint64_t)i * SCAN_THREADS + threadIdx.x;
-    if (j < n) s += in[j];
-  }
-  T tot;
-  block_excl_scan<T, SCAN_THREADS>(s, &tot);
-  if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+// ------------------------------------------------------------------ single-pass chained scan
+// One launch for any length: tile ids come from a ticket counter (so every earlier tile is
+// already running), each tile publishes its aggregate, then one warp looks back over the
+// predecessors' (aggregate | inclusive prefix) flags 32 at a time (decoupled look-back). The
+// flags carry the call's sequence number, so the context's persistent tile state needs no
+// reset between calls. Up to two arrays are scanned by the same tiles (pair scans).
+constexpr int CS_THREADS = 256;
+
+__device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// single-block scan of a medium array (out may equal in): warp w owns the contiguous chunk
-// [w*C, (w+1)*C); pass 1 sums the chunks, one warp scans the 32 chunk sums, pass 2 re-reads each
-// chunk (L1/L2-resident) and scans it 32 elements at a time with a running carry.
-constexpr int SCAN1_THREADS = 1024;
-constexpr uint64_t SCAN1_MAX = 1ull << 16;
-template <class T>
-__global__ void __launch_bounds__(SCAN1_THREADS) k_scan_one(const T* in, T* out, uint64_t n, T* total) { DC_PDL_ENTER();
-  __shared__ T wsum[32];
-  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const uint64_t C = (n + 31) / 32;
-  const uint64_t lo = w * C, hi = lo + C < n ? lo + C : n;
-  T s = 0;
-  for (uint64_t j = lo + lane; j < hi; j += 32) s += in[j];
-#pragma unroll
-  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) wsum[w] = s;
+template <class A, class B, int ITEMS>
+__global__ void __launch_bounds__(CS_THREADS) k_scan_chained(const A* ia, A* oa, A* ta, const B* ib, B* ob, B* tb, uint64_t n,
+                                                             unsigned long long* ctr, uint64_t ticket_base, uint64_t* flag,
+                                                             uint64_t* val, uint64_t seq) { DC_PDL_ENTER();
+  __shared__ uint32_t s_tile;
+  __shared__ uint64_t s_pre[2];
+  if (threadIdx.x == 0) s_tile = (uint32_t)(atomicAdd(ctr, 1ull) - ticket_base);
   __syncthreads();
-  if (w == 0) {
-    const T v = wsum[lane];
-    const T inc = warp_incl_scan(v);
-    wsum[lane] = inc - v;
-    if (lane == 31 && total) *total = inc;
-  }
-  __syncthreads();
-  T carry = wsum[w];
-  for (uint64_t b = lo; b < hi; b += 32) {
-    const uint64_t j = b + lane;
-    const T v = j < hi ? in[j] : T(0);
-    const T inc = warp_incl_scan(v);
-    if (j < hi) out[j] = carry + inc - v;
-    carry += __shfl_sync(0xffffffffu, inc, 31);
-  }
-}
-
-// two independent exclusive scans of the same length in one launch (each pass of k_scan_one,
-// done for both arrays: their load latencies overlap)
-template <class A, class B>
-__global__ void __launch_bounds__(SCAN1_THREADS) k_scan_one_pair(const A* ia, A* oa, A* ta, const B* ib, B* ob, B* tb, uint64_t n) { DC_PDL_ENTER();
-  __shared__ A wa[32];
-  __shared__ B wb[32];
-  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const uint64_t C = (n + 31) / 32;
-  const uint64_t lo = w * C, hi = lo + C < n ? lo + C : n;
+  const uint32_t tile = s_tile;
+  const uint64_t base = (uint64_t)tile * (CS_THREADS * ITEMS) + (uint64_t)threadIdx.x * ITEMS;
+  const bool two = ib != nullptr;
+  A va[ITEMS];
+  B vb[ITEMS];
   A sa = 0;
   B sb = 0;
-  for (uint64_t j = lo + lane; j < hi; j += 32) {
-    sa += ia[j];
-    sb += ib[j];
-  }
 #pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    sa += __shfl_xor_sync(0xffffffffu, sa, o);
-    sb += __shfl_xor_sync(0xffffffffu, sb, o);
+  for (int i = 0; i < ITEMS; ++i) {
+    const uint64_t j = base + i;
+    va[i] = j < n ? ia[j] : A(0);
+    vb[i] = (two && j < n) ? ib[j] : B(0);
+    sa += va[i];
+    sb += vb[i];
   }
-  if (lane == 0) {
-    wa[w] = sa;
-    wb[w] = sb;
-  }
-  __syncthreads();
-  if (w == 0) {
-    const A va = wa[lane];
-    const A inca = warp_incl_scan(va);
-    wa[lane] = inca - va;
-    const B vb = wb[lane];
-    const B incb = warp_incl_scan(vb);
-    wb[lane] = incb - vb;
-    if (lane == 31) {
-      if (ta) *ta = inca;
-      if (tb) *tb = incb;
+  A tota;
+  B totb;
+  A exa = block_excl_scan<A, CS_THREADS>(sa, &tota);
+  B exb = two ? block_excl_scan<B, CS_THREADS>(sb, &totb) : B(0);
+  if (!two) totb = 0;
+  if (threadIdx.x < 32) {
+    const uint32_t lane = threadIdx.x;
+    uint64_t pa = 0, pb = 0;
+    if (tile == 0) {
+      if (lane == 0) {
+        val[2] = (uint64_t)tota;
+        val[3] = (uint64_t)totb;
+        st_release_u64(flag, (seq << 2) | 2u);
+      }
+    } else {
+      if (lane == 0) {
+        val[4ull * tile] = (uint64_t)tota;
+        val[4ull * tile + 1] = (uint64_t)totb;
+        st_release_u64(flag + tile, (seq << 2) | 1u);
+      }
+      int64_t j = (int64_t)tile - 1 - (int64_t)lane;
+      for (uint64_t spins = 0;;) {
+        uint32_t st = 2;  // lanes past tile 0 never matter (tile 0 is inclusive)
+        if (j >= 0) {
+          const uint64_t f = ld_acquire_u64(flag + j);
+          st = (f >> 2) == seq ? (uint32_t)(f & 3u) : 0u;
+        }
+        const uint32_t incl = __ballot_sync(0xffffffffu, st == 2);
+        const int first = incl ? __ffs(incl) - 1 : 31;  // nearest inclusive predecessor
+        const uint32_t need = first == 31 ? 0xffffffffu : ((2u << first) - 1u);
+        if (__ballot_sync(0xffffffffu, st == 0) & need) {  // a needed predecessor has not published
+          if (++spins > DC_SPIN_LIMIT) __trap();
+          continue;
+        }
+        uint64_t a = 0, b = 0;
+        if ((int)lane <= first && j >= 0) {
+          a = __ldcg(val + 4ull * j + (st == 2 ? 2 : 0));
+          b = __ldcg(val + 4ull * j + (st == 2 ? 3 : 1));
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          a += __shfl_xor_sync(0xffffffffu, a, o);
+          b += __shfl_xor_sync(0xffffffffu, b, o);
+        }
+        pa += a;
+        pb += b;
+        if (incl) break;
+        j -= 32;
+      }
+      if (lane == 0) {
+        val[4ull * tile + 2] = pa + (uint64_t)tota;
+        val[4ull * tile + 3] = pb + (uint64_t)totb;
+        st_release_u64(flag + tile, (seq << 2) | 2u);
+      }
+    }
+    if (lane == 0) {
+      s_pre[0] = pa;
+      s_pre[1] = pb;
     }
   }
   __syncthreads();
-  A ca = wa[w];
-  B cb = wb[w];
-  for (uint64_t b = lo; b < hi; b += 32) {
-    const uint64_t j = b + lane;
-    const A va = j < hi ? ia[j] : A(0);
-    const B vb = j < hi ? ib[j] : B(0);
-    const A inca = warp_incl_scan(va);
-    const B incb = warp_incl_scan(vb);
-    if (j < hi) {
-      oa[j] = ca + inca - va;
-      ob[j] = cb + incb - vb;
+  A ra = (A)s_pre[0] + exa;
+  B rb = (B)s_pre[1] + exb;
+  const uint64_t n_tiles = (n + CS_THREADS * ITEMS - 1) / (CS_THREADS * ITEMS);
+  if (tile == n_tiles - 1 && threadIdx.x == CS_THREADS - 1) {
+    if (ta) *ta = (A)s_pre[0] + exa + sa;
+    if (tb) *tb = (B)s_pre[1] + exb + sb;
+  }
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const uint64_t j = base + i;
+    if (j < n) {
+      oa[j] = ra;
+      if (two) ob[j] = rb;
     }
-    ca += __shfl_sync(0xffffffffu, inca, 31);
-    cb += __shfl_sync(0xffffffffu, incb, 31);
+    ra += va[i];
+    rb += vb[i];
   }
 }
 
-template <class T>
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan_down(const T* __restrict__ in, T* out, uint64_t n,
-                                                            const T* __restrict__ offs) { DC_PDL_ENTER();
-  // each thread owns SCAN_ITEMS consecutive elements of the tile
-  const uint64_t base = (uint64_t)blockIdx.x * SCAN_TILE + (uint64_t)threadIdx.x * SCAN_ITEMS;
-  T v[SCAN_ITEMS];
-  T s = 0;
-#pragma unroll
-  for (int i = 0; i < SCAN_ITEMS; ++i) {
-    uint64_t j = base + i;
-    v[i] = j < n ? in[j] : T(0);
-    s += v[i];
-  }
-  T ex = block_excl_scan<T, SCAN_THREADS>(s, nullptr) + offs[blockIdx.x];
-#pragma unroll
-  for (int i = 0; i < SCAN_ITEMS; ++i) {
-    uint64_t j = base + i;
-    if (j < n) out[j] = ex;
-    ex += v[i];
-  }
-}
+// the context's persistent chained-scan tile state (allocated on first use)
+dc_status scan_state(Ctx* c, uint64_t n_tiles, uint64_t** flag, uint64_t** val, uint64_t* seq, Buf<uint64_t>& tmp);
 
-template <class T>
-dc_status excl_scan(Ctx* c, const T* in, T* out, uint64_t n, T* total_dev);
-// two exclusive scans of length n (one launch when n <= SCAN1_MAX)
 template <class A, class B>
-dc_status excl_scan_pair(Ctx* c, const A* ia, A* oa, A* ta, const B* ib, B* ob, B* tb, uint64_t n) {
-  if (n == 0 || n > SCAN1_MAX) {
-    DC_TRY(excl_scan<A>(c, ia, oa, n, ta));
-    return excl_scan<B>(c, ib, ob, n, tb);
+dc_status scan_chained(Ctx* c, const A* ia, A* oa, A* ta, const B* ib, B* ob, B* tb, uint64_t n) {
+  if (n == 0) {
+    if (ta) DC_CUDA(c, cudaMemsetAsync(ta, 0, sizeof(A), c->stream));
+    if (tb) DC_CUDA(c, cudaMemsetAsync(tb, 0, sizeof(B), c->stream));
+    return DC_OK;
   }
-  dc_launch(k_scan_one_pair<A, B>, 1, SCAN1_THREADS, 0, c->stream, ia, oa, ta, ib, ob, tb, n);
+  constexpr int ITEMS = (sizeof(A) == 8 || sizeof(B) == 8) ? 8 : 16;
+  const uint64_t nt = (n + CS_THREADS * ITEMS - 1) / (CS_THREADS * ITEMS);
+  if (nt >= (1ull << 31)) return fail(c, DC_ERR_CAPACITY, "scan of %llu elements", (unsigned long long)n);
+  uint64_t *flag, *val, seq;
+  Buf<uint64_t> tmp;
+  DC_TRY(scan_state(c, nt, &flag, &val, &seq, tmp));
+  const uint64_t base = c->scan_tickets;
+  c->scan_tickets += nt;
+  dc_launch(k_scan_chained<A, B, ITEMS>, (unsigned)nt, CS_THREADS, 0, c->stream, ia, oa, ta, ib, ob, tb, n, c->scan_ctr, base, flag,
+            val, seq);
   DC_LAUNCHED(c);
   return DC_OK;
 }
 
-// out[i] = sum(in[0..i)); total (device) optional. in may equal out.
+// out[i] = sum(in[0..i)); total (device) optional. in may equal out. One launch.
 template <class T>
 dc_status excl_scan(Ctx* c, const T* in, T* out, uint64_t n, T* total_dev) {
-  if (n == 0) {
-    if (total_dev) DC_CUDA(c, cudaMemsetAsync(total_dev, 0, sizeof(T), c->stream));
-    return DC_OK;
-  }
-  uint64_t nt = (n + SCAN_TILE - 1) / SCAN_TILE;
-  if (n <= SCAN1_MAX) {  // one launch
-    dc_launch(k_scan_one<T>, 1, SCAN1_THREADS, 0, c->stream, in, out, n, total_dev);
-    DC_LAUNCHED(c);
-    return DC_OK;
-  }
-  Buf<T> sums;
-  DC_TRY(alloc(c, sums, nt));
-  dc_launch(k_scan_reduce<T>, (unsigned)nt, SCAN_THREADS, 0, c->stream, in, n, sums.p);
-  DC_LAUNCHED(c);
-  DC_TRY(excl_scan<T>(c, sums.p, sums.p, nt, total_dev));
-  dc_launch(k_scan_down<T>, (unsigned)nt, SCAN_THREADS, 0, c->stream, in, out, n, sums.p);
-  DC_LAUNCHED(c);
-  return DC_OK;
+  return scan_chained<T, T>(c, in, out, total_dev, (const T*)nullptr, (T*)nullptr, (T*)nullptr, n);
+}
+// two exclusive scans of length n in one launch
+template <class A, class B>
+dc_status excl_scan_pair(Ctx* c, const A* ia, A* oa, A* ta, const B* ib, B* ob, B* tb, uint64_t n) {
+  return scan_chained<A, B>(c, ia, oa, ta, ib, ob, tb, n);
 }
 
 // ------------------------------------------------------------------ radix sort (pairs)
@@ -371,11 +360,7 @@ static inline dc_status radix_sort_pairs(Ctx* c, uint64_t* k0, uint32_t* v0, uin
   *result_in_1 = false;
   if (n <= 1 || end_bit <= begin_bit) return DC_OK;
   if (n <= SS_MAX) {
-    static bool attr = false;
-    if (!attr) {
-      DC_CUDA(c, cudaFuncSetAttribute(k_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SmallSortSmem)));
-      attr = true;
-    }
+    DC_CUDA(c, cudaFuncSetAttribute(k_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SmallSortSmem)));
     dc_launch(k_sort_small, 1, SS_THREADS, sizeof(SmallSortSmem), c->stream, k0, v0, k1, v1, (uint32_t)n, begin_bit, end_bit);
     DC_LAUNCHED(c);
     *result_in_1 = true;

@@ -6,6 +6,9 @@
 //   STALL: stall-reason top-k of one node (analysis ④).
 // Candidates are compacted in id order and stably radix-sorted by ~value, which yields
 // (value desc, id asc) without a comparison sort.
+#include <stdlib.h>
+#include <vector>
+
 #include "prim.cuh"
 
 namespace dc {
@@ -99,6 +102,183 @@ __global__ void k_view_stall(const uint64_t* __restrict__ istall, const uint64_t
   if (s == 0) *n_out = min((uint32_t)__popc(okmask), k);
 }
 
+// ---------------------------------------------------------------- one-CTA top-k (small trees)
+// Candidates are compacted into shared memory; the k-th largest composite key (value, ~id) —
+// unique per candidate, so "larger" is exactly the (value desc, id asc) order — is found by a
+// 12-digit radix select (8-bit digits, most significant first), the k keys >= it are gathered
+// and placed by rank. The result count (or an overflow flag: more candidates than fit) is the
+// header entry out[0], so the host reads the whole answer with ONE copy.
+constexpr int TK_THREADS = 1024;
+constexpr uint32_t TK_CAP = 8192;        // candidates held in shared memory
+constexpr uint32_t TK_FRAMES = 8192;     // frames accumulated in shared memory (bottom-up)
+constexpr uint32_t TK_MAXK = 1024;
+constexpr uint64_t TK_MAX_NODES = 1ull << 18;
+struct TopkSmem {
+  uint64_t v[TK_CAP];
+  uint32_t id[TK_CAP];
+  unsigned long long byf[TK_FRAMES];
+  uint32_t seen[TK_FRAMES / 32];
+  uint32_t hist[256];
+  uint64_t sel_v[TK_MAXK];
+  uint32_t sel_id[TK_MAXK];
+  uint32_t cnt, nsel, digit, rem, overflow;
+  uint64_t total;
+};
+
+__device__ __forceinline__ uint32_t tk_digit(uint64_t v, uint32_t id, int p) {  // p = 0 (top) .. 11
+  return p < 8 ? (uint32_t)(v >> (56 - 8 * p)) & 0xFFu : (uint32_t)((~id) >> (24 - 8 * (p - 8))) & 0xFFu;
+}
+__device__ __forceinline__ bool tk_greater(uint64_t va, uint32_t ia, uint64_t vb, uint32_t ib) {
+  return va > vb || (va == vb && ia < ib);
+}
+
+__global__ void __launch_bounds__(TK_THREADS, 1) k_topk_one(const uint64_t* __restrict__ val, const uint32_t* __restrict__ frame,
+                                                           const uint8_t* __restrict__ fk, uint32_t n_frames, uint32_t mask,
+                                                           uint64_t N, const uint64_t* __restrict__ total_p, double threshold,
+                                                           uint32_t k, int bottom_up, dc_topk_entry* __restrict__ out) { DC_PDL_ENTER();
+  extern __shared__ __align__(16) unsigned char tk_raw[];
+  TopkSmem& sm = *reinterpret_cast<TopkSmem*>(tk_raw);
+  const uint32_t tid = threadIdx.x;
+  if (tid == 0) {
+    sm.cnt = 0;
+    sm.nsel = 0;
+    sm.overflow = 0;
+    sm.total = *total_p;
+  }
+  if (bottom_up) {
+    for (uint32_t f = tid; f < n_frames; f += TK_THREADS) sm.byf[f] = 0;
+    for (uint32_t w = tid; w < (n_frames + 31) / 32; w += TK_THREADS) sm.seen[w] = 0;
+  }
+  __syncthreads();
+  const uint64_t total = sm.total;
+  if (bottom_up) {  // same frame across call paths: exclusive values summed per frame
+    for (uint64_t i = 1 + tid; i < N; i += TK_THREADS) {
+      const uint32_t f = frame[i];
+      if (f >= n_frames || !kind_ok(fk, n_frames, f, mask)) continue;
+      const uint64_t v = val[i];
+      if (v) atomicAdd(&sm.byf[f], (unsigned long long)v);
+      atomicOr(&sm.seen[f >> 5], 1u << (f & 31));
+    }
+    __syncthreads();
+    if (total > 0)
+      for (uint32_t f = tid; f < n_frames; f += TK_THREADS) {
+        const uint64_t v = sm.byf[f];
+        if (((sm.seen[f >> 5] >> (f & 31)) & 1u) && frac_of(v, total) > threshold) {
+          const uint32_t q = atomicAdd(&sm.cnt, 1u);
+          if (q < TK_CAP) {
+            sm.v[q] = v;
+            sm.id[q] = f;
+          }
+        }
+      }
+  } else if (total > 0) {
+    for (uint64_t i = 1 + tid; i < N; i += TK_THREADS) {
+      if (!kind_ok(fk, n_frames, frame[i], mask)) continue;
+      const uint64_t v = val[i];
+      if (frac_of(v, total) > threshold) {
+        const uint32_t q = atomicAdd(&sm.cnt, 1u);
+        if (q < TK_CAP) {
+          sm.v[q] = v;
+          sm.id[q] = (uint32_t)i;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (sm.cnt > TK_CAP) {  // more candidates than shared memory holds: the host takes the general path
+    if (tid == 0) {
+      dc_topk_entry h = {};
+      h._pad = 1;
+      out[0] = h;
+    }
+    return;
+  }
+  const uint32_t c = sm.cnt, kk = min(k, c);
+  // radix select of the kk-th largest (value, ~id); every candidate key is distinct
+  uint64_t pv = 0;   // prefix of the value digits found so far
+  uint32_t pid = 0;  // prefix of the ~id digits
+  if (tid == 0) sm.rem = kk;
+  for (int p = 0; p < 12 && kk < c; ++p) {
+    if (tid < 256) sm.hist[tid] = 0;
+    __syncthreads();
+    for (uint32_t q = tid; q < c; q += TK_THREADS) {
+      const uint64_t v = sm.v[q];
+      const uint32_t ni = ~sm.id[q];
+      bool match;
+      if (p < 8) match = p == 0 || (v >> (64 - 8 * p)) == (pv >> (64 - 8 * p));
+      else match = v == pv && (p == 8 || (ni >> (32 - 8 * (p - 8))) == (pid >> (32 - 8 * (p - 8))));
+      if (match) atomicAdd(&sm.hist[tk_digit(v, sm.id[q], p)], 1u);
+    }
+    __syncthreads();
+    if (tid < 32) {  // largest digit d with (count of digits >= d) >= rem
+      const uint32_t rem = sm.rem;
+      uint32_t above = 0;
+      uint32_t d = 0, cnt_above = 0;
+      for (int g = 7; g >= 0; --g) {  // 8 groups of 32 digits, top down
+        const uint32_t dg = (uint32_t)g * 32 + tid;
+        const uint32_t h = sm.hist[dg];
+        // inclusive suffix sum within the group (digits >= dg)
+        uint32_t suf = h;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t u = __shfl_down_sync(0xffffffffu, suf, o);
+          if (tid + o < 32) suf += u;
+        }
+        const uint32_t hit = __ballot_sync(0xffffffffu, above + suf >= rem);
+        if (hit) {
+          const int l = 31 - __clz(hit);  // largest digit in the group reaching rem
+          d = (uint32_t)g * 32 + l;
+          const uint32_t suf_l = __shfl_sync(0xffffffffu, suf, l);
+          const uint32_t h_l = __shfl_sync(0xffffffffu, h, l);
+          cnt_above = above + suf_l - h_l;
+          break;
+        }
+        above += __shfl_sync(0xffffffffu, suf, 0);
+      }
+      if (tid == 0) {
+        sm.digit = d;
+        sm.rem = rem - cnt_above;
+      }
+    }
+    __syncthreads();
+    const uint32_t d = sm.digit;
+    if (p < 8) pv |= (uint64_t)d << (56 - 8 * p);
+    else pid |= d << (24 - 8 * (p - 8));
+  }
+  // gather the kk largest: key >= (pv, ~pid) (all candidates when kk == c)
+  const uint32_t kid = ~pid;
+  for (uint32_t q = tid; q < c; q += TK_THREADS) {
+    const uint64_t v = sm.v[q];
+    const uint32_t id = sm.id[q];
+    if (kk == c || v > pv || (v == pv && id <= kid)) {
+      const uint32_t s = atomicAdd(&sm.nsel, 1u);
+      if (s < TK_MAXK) {
+        sm.sel_v[s] = v;
+        sm.sel_id[s] = id;
+      }
+    }
+  }
+  __syncthreads();
+  const uint32_t ns = min(sm.nsel, kk);
+  for (uint32_t e = tid; e < ns; e += TK_THREADS) {
+    const uint64_t v = sm.sel_v[e];
+    const uint32_t id = sm.sel_id[e];
+    uint32_t rank = 0;
+    for (uint32_t o = 0; o < ns; ++o) rank += tk_greater(sm.sel_v[o], sm.sel_id[o], v, id) ? 1u : 0u;
+    dc_topk_entry en;
+    en.id = id;
+    en._pad = 0;
+    en.value = v;
+    en.fraction = frac_of(v, total);
+    out[1 + rank] = en;
+  }
+  if (tid == 0) {
+    dc_topk_entry h = {};
+    h.id = ns;
+    out[0] = h;
+  }
+}
+
 dc_status hotspots_topk(Ctx* c, const dc_cct* t, dc_view view, uint32_t metric, uint32_t kind_mask, double threshold, uint32_t k,
                         uint32_t stall_node, dc_topk_entry* out_h, uint32_t* n_out_h) {
   *n_out_h = 0;
@@ -109,14 +289,16 @@ dc_status hotspots_topk(Ctx* c, const dc_cct* t, dc_view view, uint32_t metric, 
   if (view == DC_VIEW_STALL) {
     if (stall_node >= t->N) return fail(c, DC_ERR_ARG, "stall_node %u >= n_nodes", stall_node);
     if (!t->xsamples) return DC_OK;
-    Buf<uint32_t> nout;
-    DC_TRY(alloc(c, nout, 1));
-    dc_launch(k_view_stall, 1, 32, 0, c->stream, t->istall, t->isamples, t->N, t->S, stall_node, threshold, k, out.p, nout.p);
+    const uint32_t ks = k < 32 ? k : 32;  // at most 32 stall reasons
+    DC_TRY(alloc(c, out, ks + 1));
+    dc_launch(k_view_stall, 1, 32, 0, c->stream, t->istall, t->isamples, t->N, t->S, stall_node, threshold, ks, out.p + 1,
+              (uint32_t*)out.p);
     DC_LAUNCHED(c);
-    uint32_t h = 0;
-    DC_TRY(readback(c, nout.p, 4, &h));
-    if (h) DC_TRY(readback(c, out.p, h * sizeof(dc_topk_entry), out_h));
-    *n_out_h = h;
+    std::vector<dc_topk_entry> h(ks + 1);
+    DC_TRY(readback(c, out.p, (ks + 1) * sizeof(dc_topk_entry), h.data()));
+    const uint32_t nh = h[0].id;
+    for (uint32_t i = 0; i < nh; ++i) out_h[i] = h[1 + i];
+    *n_out_h = nh;
     return DC_OK;
   }
   const uint64_t *ival, *xval;
@@ -130,6 +312,25 @@ dc_status hotspots_topk(Ctx* c, const dc_cct* t, dc_view view, uint32_t metric, 
     xval = t->col(C_XSUM, metric);
   }
   const uint64_t* total_p = ival;  // root = node 0
+  const bool bu = view == DC_VIEW_BOTTOM_UP;
+  if ((view == DC_VIEW_INCLUSIVE || view == DC_VIEW_EXCLUSIVE || bu) && t->N <= TK_MAX_NODES && k <= TK_MAXK &&
+      (!bu || t->n_frames <= TK_FRAMES) && !getenv("DC_TEST_TOPK_GENERAL")) {
+    Buf<dc_topk_entry> o1;
+    DC_TRY(alloc(c, o1, k + 1));
+    DC_CUDA(c, cudaFuncSetAttribute(k_topk_one, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TopkSmem)));
+    dc_launch(k_topk_one, 1, TK_THREADS, sizeof(TopkSmem), c->stream, view == DC_VIEW_INCLUSIVE ? ival : xval, t->frame,
+              t->frame_kind, t->n_frames, kind_mask, t->N, total_p, threshold, k, bu ? 1 : 0, o1.p);
+    DC_LAUNCHED(c);
+    std::vector<dc_topk_entry> h(k + 1);
+    DC_TRY(readback(c, o1.p, (k + 1) * sizeof(dc_topk_entry), h.data()));
+    if (!h[0]._pad) {  // else: more candidates than the one-CTA path holds, general path below
+      const uint32_t nh = h[0].id;
+      for (uint32_t i = 0; i < nh; ++i) out_h[i] = h[1 + i];
+      *n_out_h = nh;
+      c->bytes_host += 8 * t->N;
+      return DC_OK;
+    }
+  }
   uint64_t n = 0;
   const uint64_t* val = nullptr;
   Buf<unsigned long long> byf;

@@ -83,14 +83,21 @@ def _rand_trace(rng, R_max=300, A_max=40):
     return paths, X, smp, S, A
 
 
-@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("seed", range(8))
 def test_random_traces_vs_oracle(seed, monkeypatch):
-    if seed % 2:  # odd seeds: the level-synchronous rollup (cooperative kernel) on small trees
+    # rollup schedules: per-column shared-memory level walk (default for small trees; seeds 2,
+    # 7), level-synchronous cooperative kernel (odd seeds but 7), ancestor push with 32-bit limbs
+    # (6), with returned u128 atomics (0, 4)
+    if seed % 2 and seed != 7:
         monkeypatch.setenv("DC_TEST_ROLLUP_LEVELS", "1")
-    if seed >= 4:  # the one-CTA level loop instead of the lexicographic-rank build
+    if seed >= 4 and seed != 6:  # the one-CTA level loop instead of the lexicographic-rank build
         monkeypatch.setenv("DC_TEST_BUILD_LEVELS", "1")
-    if seed in (0, 4):  # the ancestor push with returned u128 atomics instead of 32-bit limbs
+    if seed in (0, 4):
         monkeypatch.setenv("DC_TEST_ROLLUP_PUSH_RETURNED", "1")
+    if seed == 6:
+        monkeypatch.setenv("DC_TEST_ROLLUP_PUSH", "1")
+    if seed in (3, 5):  # views: the multi-kernel sort path instead of the one-CTA radix select
+        monkeypatch.setenv("DC_TEST_TOPK_GENERAL", "1")
     rng = np.random.default_rng(500 + seed)
     import paper_2411_02797_b200 as dc
     ctx = dc.Context(0)
@@ -103,7 +110,7 @@ def test_random_traces_vs_oracle(seed, monkeypatch):
         # views vs oracle
         fk = rng.integers(0, 6, size=A).astype(np.uint8)
         o = oracle_run(off, fr, X, X.shape[0], smp, len(paths), S)
-        for view in [0, 1, 3]:
+        for view in [0, 1, 2, 3]:
             th = float(rng.choice([-1.0, 0.0, 0.01, 0.2]))
             k = int(rng.integers(1, 12))
             m = int(rng.integers(0, X.shape[0]))
@@ -433,3 +440,29 @@ def test_path_table_overflow_retry(monkeypatch):
     a = gpu_run(off, fr, X, n_frames=60)
     assert_same(a, oracle_run(off, fr, X, 1).arrays(), ctx="path table retry")
     assert a["_ctx"].diag()["empty_paths"] == 7
+
+
+@pytest.mark.parametrize("general", [False, True])
+def test_topk_ties_and_large_k(general, monkeypatch):
+    """Top-k on a star of 5,000 leaves whose values take only 3 distinct values (massive ties:
+    the order is value desc, then id asc), k from 1 to 1,000 and thresholds around the tie
+    values; the one-CTA radix select (and the general sort path) equal the oracle's sort."""
+    if general:
+        monkeypatch.setenv("DC_TEST_TOPK_GENERAL", "1")
+    import paper_2411_02797_b200 as dc
+    W = 5000
+    rng = np.random.default_rng(77)
+    paths = [[0, 1 + j] for j in range(W)] + [[0]]
+    off, fr = _csr(paths)
+    X = np.zeros((1, len(paths)), np.uint64)
+    X[0, :W] = rng.choice(np.array([5, 7, 9], np.uint64), size=W)
+    X[0, W] = 3
+    a = gpu_run(off, fr, X, n_frames=W + 1)
+    o = oracle_run(off, fr, X, 1)
+    total = float(X.sum())
+    for view in [0, 1, 2]:
+        for k in [1, 7, 100, 1000]:
+            for th in [-1.0, 0.0, 5.5 / total, 7.0 / total, 8.0 / total]:
+                got = dc.dc_hotspots_topk(a["_ctx"], a["_cct"], view, 0, 0xFFFFFFFF, th, k)
+                exp = o.topk(view, 0, 0xFFFFFFFF, None, th, k)
+                assert got == [(int(e["id"]), int(e["value"]), float(e["fraction"])) for e in exp], (view, k, th)
