@@ -40,6 +40,9 @@ struct Ctx {
   uint64_t* scan_val = nullptr;
   unsigned long long* scan_ctr = nullptr;
   uint64_t scan_cap = 0, scan_seq = 0, scan_tickets = 0;
+  uint64_t pc_bins_hint = 0;   // bins of the last PC-histogram call (+1/8): capacity guess of the next
+  uint64_t pc_words_hint = 0;  // bitmap words of the last context reduce (+1/8): its scratch guess
+  uint64_t pc_big_hint = 0;    // bins of big contexts (counted in scratch) of the last call (+1/8)
   std::string err;
   uint32_t* d_flags = nullptr;   // [1]
   uint64_t* d_diag = nullptr;    // [DG_N]

@@ -23,6 +23,8 @@
 // pc_off >= 2^27, a context whose partial list cannot be chunked into shared memory) makes
 // the call fall back to the generic schedule (pc.cu) for the whole input — same result.
 #include <stdlib.h>
+#include <algorithm>
+#include <vector>
 
 #include "prim.cuh"
 
@@ -981,6 +983,403 @@ __global__ void __launch_bounds__(32 * BR_WARPS) k_br_count(
   }
 }
 
+// ---------------------------------------------------------------- context reduce (default)
+// Two launches and a scan, no sort, no waiting between contexts:
+//  k_ctx_hist: persistent CTAs take the context groups by ticket (any order). For its context a
+//    CTA gathers the segments' partial entries, builds the (pc', stall) presence bitmap in
+//    shared memory (pc' = pc_off >> the common trailing zero bits of the context's PCs; one
+//    32-bit word per PC), ranks the keys by the word popcount prefix (bin index within the
+//    context) and sums the counts per bin in shared memory (exact u64 as 32-bit halves), adds the
+//    context's per-stall totals into its sample columns, and stores bitmap + bin counts in a
+//    scratch slab (bump-allocated) with the context's (bins, PC nodes);
+//  an exclusive scan over the groups' (bins, PC nodes) gives every context its global bases
+//    (contexts in ascending id = canonical order);
+//  k_ctx_emit: one CTA per group writes its PC nodes and bins in canonical (pc, stall) order and
+//    copies the bin counts, coalesced.
+// A context whose PC range or segment count does not fit shared memory raises CR_WIDE (the host
+// takes the k_br_* path); outputs past the allocated capacity are not written (CR_OVER: the host
+// reallocates and reruns k_ctx_emit only).
+constexpr int CR_THREADS = 1024;
+constexpr uint32_t CR_WORDS = 8192;    // PCs per context (pc' range)
+constexpr uint32_t CR_BINS = 12288;    // bins per context counted in shared memory
+constexpr uint32_t CR_SEGS = 4096;     // segments per context
+enum { CR_WIDE = 1, CR_OVER = 2 };
+struct CtxRedSmem {
+  uint32_t bm[CR_WORDS];
+  uint32_t bpre[CR_WORDS];   // bins before word w (within the context)
+  uint32_t ppre[CR_WORDS];   // PC nodes before word w
+  // u64 sums as 32-bit halves with an exact carry (native 32-bit shared atomics; a 64-bit
+  // shared atomic add is a CAS loop)
+  uint32_t cnt_lo[CR_BINS], cnt_hi[CR_BINS];
+  uint32_t wst_lo[CR_THREADS / 32][32], wst_hi[CR_THREADS / 32][32];  // per-warp stall totals
+  uint32_t segs[CR_SEGS];
+  uint32_t nseg, g, maxk, orp;
+  unsigned long long ow, ob;
+};
+// per group record written by k_ctx_hist: ctx, W, sh | np << 8?, ...
+struct __align__(16) CtxRec {
+  unsigned long long ow, ob;  // scratch offsets: bitmap words (u32 units), bin counts (u64 units)
+  uint32_t ctx, W, sh, nb;
+};
+
+// Walks the context's entries: chunks of 32 x CR_U entries, chunk k of the concatenated
+// segments to warp k mod 32; every lane has CR_U independent loads in flight (one memory
+// latency per chunk instead of one per entry). fn(key, count) for every valid entry.
+constexpr uint32_t CR_U = 8;
+template <bool WITH_CNT, class F>
+__device__ __forceinline__ void cr_for_entries(const CtxRedSmem& sm, const uint4* __restrict__ seg, const uint32_t* __restrict__ pkey,
+                                               const unsigned long long* __restrict__ pcnt, uint32_t ns, F fn) {
+  constexpr uint32_t CH = 32 * CR_U;
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t kbase = 0;
+  for (uint32_t q = 0; q < ns; ++q) {
+    const uint4 sg = seg[sm.segs[q]];
+    const uint64_t base = (uint64_t)sg.z | ((uint64_t)sg.w << 32);
+    const uint32_t nch = (sg.y + CH - 1) / CH;
+    for (uint32_t ch = (w + 32 - kbase % 32) % 32; ch < nch; ch += 32) {
+      uint32_t kk[CR_U];
+      unsigned long long cv[CR_U];
+#pragma unroll
+      for (uint32_t u = 0; u < CR_U; ++u) {
+        const uint32_t j = ch * CH + u * 32 + lane;
+        kk[u] = j < sg.y ? __ldcg(pkey + base + j) : 0u;
+        if (WITH_CNT) cv[u] = j < sg.y ? __ldcg(pcnt + base + j) : 0ull;
+      }
+#pragma unroll
+      for (uint32_t u = 0; u < CR_U; ++u)
+        if (ch * CH + u * 32 + lane < sg.y) fn(kk[u], WITH_CNT ? cv[u] : 0ull);
+    }
+    kbase += nch;
+  }
+}
+
+__device__ __forceinline__ uint64_t cr_ld_acq(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void cr_st_rel(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// FUSED (default): one launch. After its counts are summed the CTA looks back over the
+// preceding contexts' published (bins, PC nodes) — each context publishes right after its
+// bitmap, so by then the look-back rarely waits — and writes its PC nodes, bins and counts at
+// their global positions directly. !FUSED: bitmap + counts go to the scratch slab and
+// k_ctx_emit writes them after a scan over the groups (kept for A/B measurement, DC_PC_CR=2).
+template <bool FUSED>
+__global__ void __launch_bounds__(CR_THREADS, 1) k_ctx_hist(
+    const uint4* __restrict__ seg, const unsigned int* __restrict__ d_nsegs, uint32_t cap_segs, const uint32_t* __restrict__ pkey,
+    const unsigned long long* __restrict__ pcnt, const uint64_t* __restrict__ lkey, const uint32_t* __restrict__ gfirst,
+    const uint32_t* __restrict__ d_ng, uint64_t N, uint32_t S, const uint32_t* __restrict__ g_flags,
+    unsigned long long* __restrict__ ctl,  // [0] ticket, [1] status, [2] scratch words used, [3] scratch bins used,
+                                           // [4] total bins, [5] total PC nodes, then 5 per group (FUSED look-back):
+                                           // flag, aggregate (bins, pcs), inclusive (bins, pcs)
+    uint32_t* __restrict__ wscr, uint64_t wcap, unsigned long long* __restrict__ bscr, uint64_t bcap, CtxRec* __restrict__ rec,
+    uint64_t* __restrict__ gnb, uint64_t* __restrict__ gnp, unsigned long long* __restrict__ xsamples,
+    unsigned long long* __restrict__ xstall, uint64_t cap, uint32_t* __restrict__ pc_ctx, uint32_t* __restrict__ pc_off,
+    uint32_t* __restrict__ bin_pcnode, uint16_t* __restrict__ bin_stall, uint64_t* __restrict__ bin_count) { DC_PDL_ENTER();
+  extern __shared__ __align__(16) unsigned char cr_raw[];
+  CtxRedSmem& sm = *reinterpret_cast<CtxRedSmem*>(cr_raw);
+  if (*g_flags) return;  // the owner pass fell back: the host reruns the generic schedule
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+  const uint32_t NG = *d_ng, n_segs = min(*d_nsegs, cap_segs);
+  unsigned long long* gst = ctl + 6;
+  for (;;) {
+    if (tid == 0) {
+      sm.g = (uint32_t)atomicAdd(ctl, 1ull);
+      sm.nseg = 0;
+      sm.maxk = 0;
+      sm.orp = 0;
+      sm.ow = 0;
+      sm.ob = 0;
+    }
+    __syncthreads();
+    const uint32_t g = sm.g;
+    if (g >= NG) break;
+    const uint64_t ctx = lkey[gfirst[g]];
+    bool ok = ctx < N;  // launches with an invalid leaf: no bins (flagged by the plan)
+    uint32_t W = 0, nb = 0, np = 0, ns = 0;
+    int sh = 0;
+    if (ok) {
+      // this context's segments (headers scanned 8 per thread in flight)
+      for (uint32_t i0 = 0; i0 < n_segs; i0 += 8 * CR_THREADS) {
+        uint32_t cx[8], cn[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t i = i0 + u * CR_THREADS + tid;
+          const uint2 h = i < n_segs ? __ldcg(reinterpret_cast<const uint2*>(seg + i)) : make_uint2(0xFFFFFFFFu, 0u);
+          cx[u] = h.x;
+          cn[u] = h.y;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (cx[u] == ctx && cn[u]) {
+            const uint32_t q = atomicAdd(&sm.nseg, 1u);
+            if (q < CR_SEGS) sm.segs[q] = i0 + u * CR_THREADS + tid;
+          }
+      }
+      __syncthreads();
+      // pass A: key range (max key + 1, OR of the PCs)
+      uint32_t mk = 0, orp = 0;
+      ns = min(sm.nseg, CR_SEGS);
+      cr_for_entries<false>(sm, seg, pkey, pcnt, ns, [&](uint32_t kk, unsigned long long) {
+        mk = max(mk, kk + 1);
+        orp |= kk >> 5;
+      });
+      mk = __reduce_max_sync(0xffffffffu, mk);
+      orp = __reduce_or_sync(0xffffffffu, orp);
+      if (lane == 0) {
+        atomicMax(&sm.maxk, mk);
+        atomicOr(&sm.orp, orp);
+      }
+      __syncthreads();
+      sh = sm.orp ? __ffs(sm.orp) - 1 : 0;
+      W = sm.maxk ? (((sm.maxk - 1) >> 5) >> sh) + 1 : 0;
+      if (W > CR_WORDS || sm.nseg > CR_SEGS) {
+        if (tid == 0) atomicOr(ctl + 1, (unsigned long long)CR_WIDE);
+        ok = false;
+      }
+    }
+    if (ok) {
+      // pass B: presence bits
+      for (uint32_t w = tid; w < W; w += CR_THREADS) sm.bm[w] = 0;
+      __syncthreads();
+      cr_for_entries<false>(sm, seg, pkey, pcnt, ns, [&](uint32_t kk, unsigned long long) {
+        atomicOr(&sm.bm[(kk >> 5) >> sh], 1u << (kk & 31u));
+      });
+      __syncthreads();
+      // word prefixes: thread t owns words [t * WP, (t + 1) * WP)
+      constexpr uint32_t WP = CR_WORDS / CR_THREADS;
+      uint32_t bsum = 0, psum = 0;
+#pragma unroll
+      for (uint32_t i = 0; i < WP; ++i) {
+        const uint32_t w = tid * WP + i;
+        const uint32_t b = w < W ? sm.bm[w] : 0u;
+        bsum += __popc(b);
+        psum += b != 0u;
+      }
+      uint32_t bex = block_excl_scan<uint32_t, CR_THREADS>(bsum, &nb);
+      uint32_t pex = block_excl_scan<uint32_t, CR_THREADS>(psum, &np);
+#pragma unroll
+      for (uint32_t i = 0; i < WP; ++i) {
+        const uint32_t w = tid * WP + i;
+        if (w < W) {
+          const uint32_t b = sm.bm[w];
+          sm.bpre[w] = bex;
+          sm.ppre[w] = pex;
+          bex += __popc(b);
+          pex += b != 0u;
+        }
+      }
+    }
+    const bool in_smem = nb <= CR_BINS;
+    if (tid == 0) {
+      if (FUSED) {  // publish this context's (bins, PC nodes) for the successors' look-back
+        unsigned long long* me = gst + 5ull * g;
+        if (g == 0) {
+          me[3] = nb;
+          me[4] = np;
+          cr_st_rel(me, 2ull);
+        } else {
+          me[1] = nb;
+          me[2] = np;
+          cr_st_rel(me, 1ull);
+        }
+      }
+      if (ok && (!FUSED || !in_smem)) {  // scratch: bitmap + counts (!FUSED), counts of a big context (FUSED)
+        sm.ow = FUSED ? 0 : atomicAdd(ctl + 2, (unsigned long long)W);
+        sm.ob = atomicAdd(ctl + 3, (unsigned long long)nb);
+        if (sm.ow + W > wcap || sm.ob + nb > bcap) {  // scratch too small: the host takes the k_br_* path
+          atomicOr(ctl + 1, (unsigned long long)CR_WIDE);
+          sm.ow = ~0ull;
+        }
+      }
+    }
+    for (uint32_t i = tid; i < 32 * 32; i += CR_THREADS) {
+      (&sm.wst_lo[0][0])[i] = 0;
+      (&sm.wst_hi[0][0])[i] = 0;
+    }
+    if (ok && in_smem)
+      for (uint32_t i = tid; i < nb; i += CR_THREADS) {
+        sm.cnt_lo[i] = 0;
+        sm.cnt_hi[i] = 0;
+      }
+    __syncthreads();
+    const unsigned long long ow = sm.ow, ob = sm.ob;
+    if (ow == ~0ull) ok = false;
+    if (!FUSED && !ok && tid == 0) {
+      rec[g] = CtxRec{0, 0, (uint32_t)ctx, 0, 0, 0};
+      gnb[g] = 0;
+      gnp[g] = 0;
+    }
+    if (ok) {
+      if (!in_smem)
+        for (uint32_t i = tid; i < nb; i += CR_THREADS) bscr[ob + i] = 0;
+      if (!FUSED)
+        for (uint32_t w = tid; w < W; w += CR_THREADS) wscr[ow + w] = sm.bm[w];
+      if (!in_smem) __syncthreads();
+      // pass C: counts into their bins; per-stall totals
+      cr_for_entries<true>(sm, seg, pkey, pcnt, ns, [&](uint32_t kk, unsigned long long cv) {
+        const uint32_t w = (kk >> 5) >> sh, b = kk & 31u;
+        const uint32_t r = sm.bpre[w] + __popc(sm.bm[w] & ((1u << b) - 1u));
+        const uint32_t lo = (uint32_t)cv, hi = (uint32_t)(cv >> 32);
+        if (in_smem) {
+          const uint32_t old = atomicAdd(&sm.cnt_lo[r], lo);
+          const uint32_t up = hi + (old + lo < old ? 1u : 0u);
+          if (up) atomicAdd(&sm.cnt_hi[r], up);
+        } else {
+          atomicAdd(bscr + ob + r, cv);
+        }
+        const uint32_t old = atomicAdd(&sm.wst_lo[wp][b], lo);
+        const uint32_t up = hi + (old + lo < old ? 1u : 0u);
+        if (up) atomicAdd(&sm.wst_hi[wp][b], up);
+      });
+      __syncthreads();
+      if (!FUSED && in_smem)
+        for (uint32_t i = tid; i < nb; i += CR_THREADS) bscr[ob + i] = ((unsigned long long)sm.cnt_hi[i] << 32) | sm.cnt_lo[i];
+      if (tid < 32) {
+        unsigned long long t = 0;
+        for (int w2 = 0; w2 < CR_THREADS / 32; ++w2) t += ((unsigned long long)sm.wst_hi[w2][tid] << 32) | sm.wst_lo[w2][tid];
+        if (tid < S && t) xstall[(uint64_t)tid * N + ctx] += t;
+        unsigned long long tot = tid < S ? t : 0;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        if (tid == 0) {
+          if (tot) xsamples[ctx] += tot;
+          if (!FUSED) {
+            rec[g] = CtxRec{ow, ob, (uint32_t)ctx, W, (uint32_t)sh, nb};
+            gnb[g] = nb;
+            gnp[g] = np;
+          }
+        }
+      }
+    }
+    if (FUSED) {
+      // look back (warp 0) for the global bases of this context's PC nodes and bins
+      if (wp == 0) {
+        unsigned long long bb = 0, pb = 0;
+        if (g > 0) {
+          int64_t j = (int64_t)g - 1 - (int64_t)lane;
+          for (uint64_t spins = 0;;) {
+            uint32_t st = 2;
+            if (j >= 0) st = (uint32_t)cr_ld_acq(gst + 5 * j);
+            const uint32_t incl = __ballot_sync(0xffffffffu, st == 2);
+            const int first = incl ? __ffs(incl) - 1 : 31;
+            const uint32_t need = first == 31 ? 0xffffffffu : ((2u << first) - 1u);
+            if (__ballot_sync(0xffffffffu, st == 0) & need) {
+              if (++spins > DC_SPIN_LIMIT) __trap();
+              continue;
+            }
+            unsigned long long x = 0, y = 0;
+            if ((int)lane <= first && j >= 0) {
+              x = __ldcg(gst + 5 * j + (st == 2 ? 3 : 1));
+              y = __ldcg(gst + 5 * j + (st == 2 ? 4 : 2));
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+              x += __shfl_xor_sync(0xffffffffu, x, o);
+              y += __shfl_xor_sync(0xffffffffu, y, o);
+            }
+            bb += x;
+            pb += y;
+            if (incl) break;
+            j -= 32;
+          }
+          if (lane == 0) {
+            unsigned long long* me = gst + 5ull * g;
+            me[3] = bb + nb;
+            me[4] = pb + np;
+            cr_st_rel(me, 2ull);
+          }
+        }
+        if (lane == 0) {
+          sm.ow = bb;  // reused: this context's bin base
+          sm.ob = pb;  //          and PC-node base
+          if (g == NG - 1) {
+            ctl[4] = bb + nb;
+            ctl[5] = pb + np;
+          }
+        }
+      }
+      __syncthreads();
+      const uint64_t bb = sm.ow, pb = sm.ob;
+      if (ok && nb) {
+        if (bb + nb > cap) {  // outputs past the capacity: the host reallocates and reruns
+          if (tid == 0) atomicOr(ctl + 1, (unsigned long long)CR_OVER);
+        } else {
+          for (uint32_t w = tid; w < W; w += CR_THREADS) {
+            uint32_t bits = sm.bm[w];
+            if (!bits) continue;
+            const uint64_t p = pb + sm.ppre[w];
+            pc_ctx[p] = (uint32_t)ctx;
+            pc_off[p] = w << sh;
+            uint64_t r = bb + sm.bpre[w];
+            while (bits) {
+              const uint32_t b = __ffs(bits) - 1;
+              bits &= bits - 1;
+              bin_pcnode[r] = (uint32_t)(N + p);
+              bin_stall[r] = (uint16_t)b;
+              ++r;
+            }
+          }
+          if (in_smem)
+            for (uint32_t i = tid; i < nb; i += CR_THREADS) bin_count[bb + i] = ((uint64_t)sm.cnt_hi[i] << 32) | sm.cnt_lo[i];
+          else
+            for (uint32_t i = tid; i < nb; i += CR_THREADS) bin_count[bb + i] = __ldcg(bscr + ob + i);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// one CTA per group (grid-stride): PC nodes and bins in canonical order, counts copied
+constexpr int CE_THREADS = 256;
+__global__ void __launch_bounds__(CE_THREADS) k_ctx_emit(const CtxRec* __restrict__ rec, const uint32_t* __restrict__ d_ng,
+                                                         const uint64_t* __restrict__ bbase, const uint64_t* __restrict__ pbase,
+                                                         const uint32_t* __restrict__ wscr, const unsigned long long* __restrict__ bscr,
+                                                         uint64_t N, uint64_t cap, unsigned long long* __restrict__ status,
+                                                         uint32_t* __restrict__ pc_ctx, uint32_t* __restrict__ pc_off,
+                                                         uint32_t* __restrict__ bin_pcnode, uint16_t* __restrict__ bin_stall,
+                                                         uint64_t* __restrict__ bin_count, const uint32_t* __restrict__ g_flags) { DC_PDL_ENTER();
+  if (*g_flags) return;
+  const uint32_t NG = *d_ng, tid = threadIdx.x;
+  for (uint32_t g = blockIdx.x; g < NG; g += gridDim.x) {
+    const CtxRec r = rec[g];
+    if (!r.nb) continue;
+    const uint64_t bb = bbase[g], pb = pbase[g];
+    if (bb + r.nb > cap) {
+      if (tid == 0) atomicOr(status, (unsigned long long)CR_OVER);
+      continue;
+    }
+    for (uint32_t i = tid; i < r.nb; i += CE_THREADS) bin_count[bb + i] = bscr[r.ob + i];
+    uint32_t brun = 0, prun = 0;  // bins / PC nodes before this round
+    for (uint32_t w0 = 0; w0 < r.W; w0 += CE_THREADS) {
+      const uint32_t w = w0 + tid;
+      uint32_t bits = w < r.W ? __ldcg(wscr + r.ow + w) : 0u;
+      uint32_t tb, tp;
+      const uint32_t bx = block_excl_scan<uint32_t, CE_THREADS>(__popc(bits), &tb);
+      const uint32_t px = block_excl_scan<uint32_t, CE_THREADS>(bits != 0u, &tp);
+      if (bits) {
+        const uint64_t p = pb + prun + px;
+        pc_ctx[p] = r.ctx;
+        pc_off[p] = w << r.sh;
+        uint64_t q = bb + brun + bx;
+        while (bits) {
+          const uint32_t b = __ffs(bits) - 1;
+          bits &= bits - 1;
+          bin_pcnode[q] = (uint32_t)(N + p);
+          bin_stall[q] = (uint16_t)b;
+          ++q;
+        }
+      }
+      brun += tb;
+      prun += tp;
+    }
+  }
+}
+
 // ---------------------------------------------------------------- per-context reduce
 // One CTA per context. Its partial entries (all segments of the context: several CTAs of the
 // main kernel and several flushes) are processed in key-range chunks of at most RD_CAP
@@ -1363,6 +1762,7 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
   const uint64_t st_cap = (n / 32 + n_launch + OW_ROWS - 1) / OW_ROWS + n_launch + 1;
   const uint64_t row_cap = OW_ROWS * st_cap;
   if (st_cap >= (1ull << 32)) return DC_OK;  // stage claims count in 32 bits
+  const uint64_t* lkey_out = nullptr;  // launches' contexts in ascending order (the stage plan's sort)
   {
     Region rp(c, "pc:prep");
     DC_TRY(alloc_zero(c, bad, 1));
@@ -1391,6 +1791,7 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
     }
     Region rpl(c, "prep:plan");
     const uint64_t* lkey = in1 ? k1.p : k0.p;
+    lkey_out = lkey;
     const uint32_t* order = in1 ? v1.p : v0.p;
     DC_TRY(alloc(c, lrow, n_launch + 1));
     DC_TRY(alloc(c, lsrc, n_launch));
@@ -1514,6 +1915,147 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
               "\"key_cyc\": %.0f, \"bucket_cyc\": %.0f, \"add_cyc\": %.0f, \"misses\": %.0f}}\n",
               s[0] / nw, s[1] / nw, s[2] / nw, s[3] / nw, s[4] / nw, s[5] / nw, s[6] / nw, s[7]);
     }
+    uint32_t hbad = 0;
+    if (!getenv("DC_TEST_PC_BR")) {
+      // ------------------------------------------------ context reduce (k_ctx_hist [, scan, k_ctx_emit])
+      Region rr(c, "pc:creduce");
+      const bool fused = !(getenv("DC_PC_CR") && atoi(getenv("DC_PC_CR")) == 2);
+      uint64_t cap = c->pc_bins_hint > (1ull << 20) ? c->pc_bins_hint : (1ull << 20);
+      if (cap > n) cap = n ? n : 1;
+      if (getenv("DC_TEST_PC_CAP")) cap = 1;  // test only: force the reallocate-and-rerun path
+      const uint64_t wcap = fused ? 0 : (c->pc_words_hint > (4ull << 20) ? c->pc_words_hint : (4ull << 20));
+      const uint64_t bcap = fused ? std::max<uint64_t>(c->pc_big_hint, 1ull << 20)
+                                  : (c->pc_bins_hint > (4ull << 20) ? c->pc_bins_hint : (4ull << 20));
+      Buf<unsigned long long> ctl, bscr;
+      Buf<uint32_t> wscr;
+      Buf<CtxRec> rec;
+      Buf<uint64_t> gn, gbase;  // [gnb | gnp], [bin base | pc base] (n_launch + 1 each)
+      const uint64_t ctl_n = 6 + (fused ? 5 * (n_launch + 1) : 0);
+      DC_TRY(alloc_zero(c, ctl, ctl_n));
+      DC_TRY(alloc(c, wscr, wcap));
+      DC_TRY(alloc(c, bscr, bcap));
+      if (!fused) {
+        DC_TRY(alloc(c, rec, n_launch));
+        DC_TRY(alloc_zero(c, gn, 2 * (n_launch + 1)));
+        DC_TRY(alloc(c, gbase, 2 * (n_launch + 1)));
+      }
+      auto outputs = [&](uint64_t k) -> dc_status {
+        DC_TRY(palloc(c, t->pc_ctx, k));
+        DC_TRY(palloc(c, t->pc_off, k));
+        DC_TRY(palloc(c, t->bin_pcnode, k));
+        DC_TRY(palloc(c, t->bin_stall, k));
+        return palloc(c, t->bin_count, k);
+      };
+      auto drop_outputs = [&]() {
+        void* q[] = {t->pc_ctx, t->pc_off, t->bin_pcnode, t->bin_stall, t->bin_count};
+        for (void* x : q)
+          if (x) cudaFreeAsync(x, c->stream);
+        t->pc_ctx = t->pc_off = t->bin_pcnode = nullptr;
+        t->bin_stall = nullptr;
+        t->bin_count = nullptr;
+      };
+      auto clear_cols = [&]() -> dc_status {
+        DC_CUDA(c, cudaMemsetAsync(t->xsamples, 0, N * 8, c->stream));
+        DC_CUDA(c, cudaMemsetAsync(t->xstall, 0, (uint64_t)S * N * 8, c->stream));
+        return DC_OK;
+      };
+      DC_TRY(outputs(cap));
+      const size_t csmem = sizeof(CtxRedSmem);
+      auto hist = [&](uint64_t k) -> dc_status {
+        Region rk(c, "k:ctx_hist");
+        void (*kern)(const uint4*, const unsigned int*, uint32_t, const uint32_t*, const unsigned long long*, const uint64_t*,
+                     const uint32_t*, const uint32_t*, uint64_t, uint32_t, const uint32_t*, unsigned long long*, uint32_t*, uint64_t,
+                     unsigned long long*, uint64_t, CtxRec*, uint64_t*, uint64_t*, unsigned long long*, unsigned long long*,
+                     uint64_t, uint32_t*, uint32_t*, uint32_t*, uint16_t*, uint64_t*) =
+            fused ? k_ctx_hist<true> : k_ctx_hist<false>;
+        DC_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
+        dc_launch(kern, G, CR_THREADS, csmem, c->stream, seg.p, a.g_segs, cap_segs, pkey.p, pcnt.p, lkey_out, gfirst.p,
+                  gx.p + n_launch, N, S, flags.p, ctl.p, wscr.p, wcap, bscr.p, bcap, rec.p, gn.p,
+                  fused ? nullptr : gn.p + n_launch + 1, (unsigned long long*)t->xsamples, (unsigned long long*)t->xstall, k,
+                  t->pc_ctx, t->pc_off, t->bin_pcnode, t->bin_stall, t->bin_count);
+        DC_LAUNCHED(c);
+        return DC_OK;
+      };
+      auto emit = [&](uint64_t k) -> dc_status {
+        Region rk(c, "k:ctx_emit");
+        dc_launch(k_ctx_emit, 4 * G, CE_THREADS, 0, c->stream, rec.p, gx.p + n_launch, gbase.p, gbase.p + n_launch + 1, wscr.p,
+                  bscr.p, N, k, ctl.p + 1, t->pc_ctx, t->pc_off, t->bin_pcnode, t->bin_stall, t->bin_count, flags.p);
+        DC_LAUNCHED(c);
+        return DC_OK;
+      };
+      DC_TRY(hist(cap));
+      if (!fused) {
+        DC_TRY((excl_scan_pair<uint64_t, uint64_t>(c, gn.p, gbase.p, gbase.p + n_launch, gn.p + n_launch + 1,
+                                                   gbase.p + n_launch + 1, gbase.p + 2 * n_launch + 1, n_launch)));
+        DC_TRY(emit(cap));
+      }
+      uint64_t hst[5] = {0, 0, 0, 0, 0}, htot[2] = {0, 0};
+      if (fused) {
+        DC_TRY(readback_multi(c, {{flags.p, 8, hf}, {bad.p, 4, &hbad}, {ctl.p + 1, 40, hst}, {ctr.p, 16, hc}}));
+        htot[0] = hst[3];
+        htot[1] = hst[4];
+      } else {
+        DC_TRY(readback_multi(c, {{flags.p, 8, hf}, {bad.p, 4, &hbad}, {ctl.p + 1, 24, hst}, {gbase.p + n_launch, 8, &htot[0]},
+                                  {gbase.p + 2 * n_launch + 1, 8, &htot[1]}, {ctr.p, 16, hc}}));
+      }
+      if (getenv("DC_PC_STATS"))  // measurement only
+        fprintf(stderr, "{\"pc_stats\": {\"entries\": %llu, \"segments\": %llu, \"bins\": %llu, \"pcs\": %llu, \"status\": %llu, "
+                "\"words\": %llu, \"scratch_bins\": %llu}}\n", (unsigned long long)hc[0], (unsigned long long)(hc[1] & 0xFFFFFFFFu),
+                (unsigned long long)htot[0], (unsigned long long)htot[1], (unsigned long long)hst[0], (unsigned long long)hst[1],
+                (unsigned long long)hst[2]);
+      if (getenv("DC_PC_STATS")) {  // measurement only: entries per context
+        const uint32_t nsg = (uint32_t)std::min<uint64_t>(hc[1] & 0xFFFFFFFFu, cap_segs);
+        std::vector<uint4> hs(nsg);
+        DC_TRY(readback(c, seg.p, nsg * sizeof(uint4), hs.data()));
+        std::vector<uint64_t> per(N + 1, 0), nseg(N + 1, 0);
+        for (auto& q : hs) {
+          per[q.x < N ? q.x : N] += q.y;
+          nseg[q.x < N ? q.x : N] += 1;
+        }
+        std::vector<std::pair<uint64_t, uint64_t>> v;
+        for (uint64_t i = 0; i <= N; ++i)
+          if (per[i]) v.push_back({per[i], nseg[i]});
+        std::sort(v.begin(), v.end());
+        fprintf(stderr, "{\"pc_ctx_entries\": {\"contexts\": %zu, \"median\": %llu, \"p90\": %llu, \"top\": [", v.size(),
+                (unsigned long long)v[v.size() / 2].first, (unsigned long long)v[v.size() * 9 / 10].first);
+        for (size_t i = v.size() > 12 ? v.size() - 12 : 0; i < v.size(); ++i)
+          fprintf(stderr, "[%llu, %llu]%s", (unsigned long long)v[i].first, (unsigned long long)v[i].second, i + 1 < v.size() ? ", " : "");
+        fprintf(stderr, "]}}\n");
+      }
+      if (fused) c->pc_big_hint = hst[2] + hst[2] / 8;
+      else c->pc_words_hint = hst[1] + hst[1] / 8;
+      if (hbad || hf[0]) {  // offsets inconsistent / owner fallback: generic schedule
+        drop_outputs();
+        if (hf[0] && !hbad && getenv("DC_TEST_OWNER_STRICT"))
+          return fail(c, DC_ERR_STATE, "test: owner schedule fell back (flags 0x%x)", hf[0]);
+        return DC_OK;
+      }
+      if (!(hst[0] & CR_WIDE)) {
+        const uint64_t nb = htot[0], npc = htot[1];
+        if (hst[0] & CR_OVER) {  // more bins than the capacity guess: exact outputs, write again
+          drop_outputs();
+          DC_TRY(outputs(nb));
+          if (fused) {
+            DC_TRY(clear_cols());
+            DC_CUDA(c, cudaMemsetAsync(ctl.p, 0, ctl_n * 8, c->stream));
+            DC_TRY(hist(nb));
+          } else {
+            DC_TRY(emit(nb));
+          }
+        }
+        t->Npc = npc;
+        t->Nbins = nb;
+        c->pc_bins_hint = nb + nb / 8;
+        DC_TRY(add_diag(c, ldiag.p));
+        *n_bins_out = nb;
+        *handled = 1;
+        return DC_OK;
+      }
+      if (!fused) c->pc_bins_hint = hst[2] + hst[2] / 8;
+      // a context too wide for shared memory: the global-bitmap reduce below (from scratch)
+      drop_outputs();
+      DC_TRY(clear_cols());
+    }
     // the reduce's first kernels run on the device counts, before the one host round trip
     DC_TRY(alloc_zero(c, cm, 2 * N));  // cmax | cor
     DC_TRY(alloc(c, cw, N + 1));
@@ -1531,7 +2073,6 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
       DC_LAUNCHED(c);
     }
     DC_TRY(excl_scan<uint64_t>(c, cw.p, cw.p, N, cw.p + N));  // word base per context, W at cw[N]
-    uint32_t hbad = 0;
     DC_TRY(readback_multi(c, {{ctr.p, 16, hc}, {flags.p, 8, hf}, {bad.p, 4, &hbad}, {cw.p + N, 8, &hw[0]},
                               {wide.p, 4, &hw[1]}}));
     if (hbad) return DC_OK;  // offsets inconsistent: generic schedule

@@ -175,12 +175,20 @@ def test_generic_schedule_equals_owner_schedule(monkeypatch):
     assert_same(a, c, ctx="owner (radix-sorted launches)")
 
 
+@pytest.mark.parametrize("reduce", ["ctx", "br", "cap1"])
 @pytest.mark.parametrize("n,npc,big", [(3_000_000, 2000, False), (400_000, 20_000, False), (200_000, 300, True)])
-def test_owner_high_cardinality_flush_spill_and_wrap(n, npc, big, monkeypatch):
+def test_owner_high_cardinality_flush_spill_and_wrap(n, npc, big, reduce, monkeypatch):
     """One context with up to 480k (pc, stall) keys: mid-context flushes and spills in the
     context-owner schedule; big=True uses counts up to 2^31 (32-bit shared-counter carries),
-    so every sample is spilled (many spill-chunk switches). The schedule must not fall back."""
+    so every sample is spilled (many spill-chunk switches). The schedule must not fall back.
+    Reduce: the one-pass context reduce (shared counts for <= 12,288 bins, global atomics past
+    that; 20,000 PCs exceed its shared bitmap and take the global-bitmap reduce), the global
+    bitmap reduce forced, or the context reduce with a 1-bin capacity guess (reallocate + rerun)."""
     monkeypatch.setenv("DC_TEST_OWNER_STRICT", "1")
+    if reduce == "br":
+        monkeypatch.setenv("DC_TEST_PC_BR", "1")
+    if reduce == "cap1":
+        monkeypatch.setenv("DC_TEST_PC_CAP", "1")
     rng = np.random.default_rng(n)
     s = np.zeros(n, oracle.SAMPLE_DTYPE)
     s["launch"] = 0
@@ -195,8 +203,9 @@ def test_owner_high_cardinality_flush_spill_and_wrap(n, npc, big, monkeypatch):
     assert_same(a, ref, ctx=f"owner n={n} npc={npc}")
 
 
-@pytest.mark.parametrize("n_launch,heavy", [(3, 1), (300, 40), (2000, 5)])
-def test_owner_work_stealing_skewed_contexts(n_launch, heavy, monkeypatch):
+@pytest.mark.parametrize("n_launch,heavy,pcs", [(3, 1, 30_000), (300, 40, 30_000), (2000, 5, 30_000), (300, 40, 6000),
+                                                (2000, 5, 6000)])
+def test_owner_work_stealing_skewed_contexts(n_launch, heavy, pcs, monkeypatch):
     """Stage ranges of very unequal cost: a few launches carry most samples with many distinct
     keys (flushes, spill chunks), the rest are light; with 3 launches most CTAs start with an
     empty range and only steal. Every stage must be aggregated exactly once: oracle and generic
@@ -214,7 +223,7 @@ def test_owner_work_stealing_skewed_contexts(n_launch, heavy, monkeypatch):
     s = np.zeros(n, oracle.SAMPLE_DTYPE)
     s["launch"] = np.repeat(np.arange(n_launch, dtype=np.uint32), cnt)
     heavy_s = s["launch"] < heavy
-    s["pc_off"] = np.where(heavy_s, 16 * rng.integers(0, 30_000, n), 16 * rng.integers(0, 50, n))
+    s["pc_off"] = np.where(heavy_s, 16 * rng.integers(0, pcs, n), 16 * rng.integers(0, 50, n))
     s["stall"] = rng.integers(0, 24, n)
     s["count"] = 1
     kw = dict(n_frames=5, samples=s, n_stall=24)
