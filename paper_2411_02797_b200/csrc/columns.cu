@@ -440,15 +440,29 @@ __global__ void __launch_bounds__(RC_THREADS, 1) k_roll_cols(const uint32_t* __r
     racc[i] = v;
   }
   __syncthreads();
+  const uint32_t lane = tid & 31;
   for (uint32_t d = maxd; d >= 1; --d) {
     const uint32_t lo = level_off[d], hi = level_off[d + 1];
-    for (uint32_t n = lo + tid; n < hi; n += RC_THREADS) {
-      const unsigned long long v = racc[n];
-      const uint32_t p = __ldg(parent + n);
-      if (is_min) {
-        if (v != ~0ull) atomicMin(&racc[p], v);
-      } else if (v) {
-        atomicAdd(&racc[p], v);
+    for (uint32_t b0 = lo; b0 < hi; b0 += RC_THREADS) {  // block-uniform trip count (warp shuffles below)
+      const uint32_t n = b0 + tid;
+      const bool act = n < hi;
+      unsigned long long v = act ? racc[n] : (is_min ? ~0ull : 0ull);
+      const uint32_t p = act ? __ldg(parent + n) : 0xFFFFFFFFu;
+      // siblings are contiguous: segmented reduction over the lanes with the same parent, then
+      // one shared-memory atomic per segment (its last lane)
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long u = __shfl_up_sync(0xffffffffu, v, o);
+        const uint32_t pu = __shfl_up_sync(0xffffffffu, p, o);
+        if (lane >= (uint32_t)o && pu == p) v = is_min ? (u < v ? u : v) : v + u;
+      }
+      const uint32_t pn = __shfl_down_sync(0xffffffffu, p, 1);
+      if (act && (lane == 31 || pn != p)) {
+        if (is_min) {
+          if (v != ~0ull) atomicMin(&racc[p], v);
+        } else if (v) {
+          atomicAdd(&racc[p], v);
+        }
       }
     }
     __syncthreads();

@@ -225,23 +225,24 @@ dc_status intern_frames(Ctx* c, const dc_frame_key* keys, uint64_t n, uint32_t* 
   }
   if (n >= (1ull << 32)) return fail(c, DC_ERR_CAPACITY, "dc_intern_frames: n >= 2^32 keys");
   Buf<ulonglong2> table;
-  Buf<unsigned long long> cnt, mx;
-  Buf<uint32_t> ovf;
+  Buf<unsigned long long> cnt;
   uint64_t mxh[2] = {0, 0};
-  uint64_t cap = next_pow2(2 * (n < (1ull << 20) ? n : (1ull << 20)));
+  // distinct keys are few in practice (hundreds to tens of thousands): start with a 64K-slot table
+  // (1 MB to clear and compact) and retry once with a table sized by the keys if it overflows
+  uint64_t cap = next_pow2(2 * (n < (1ull << 15) ? n : (1ull << 15)));
   if (cap < 1024) cap = 1024;
   uint64_t D = 0;
   for (int attempt = 0; attempt < 2; ++attempt) {
     DC_TRY(alloc(c, table, cap));
     DC_CUDA(c, cudaMemsetAsync(table.p, 0xFF, cap * sizeof(ulonglong2), c->stream));
-    DC_TRY(alloc_zero(c, cnt, 1));
-    DC_TRY(alloc_zero(c, ovf, 1));
-    DC_TRY(alloc_zero(c, mx, 2));
-    dc_launch(k_intern_insert, grid_for(c, (n + 3) / 4, 256), 256, 0, c->stream, keys, n, table.p, cap - 1, out_ids, cnt.p, ovf.p,
-                                                                 c->d_flags, mx.p);
+    DC_TRY(alloc_zero(c, cnt, 4));  // [0] distinct, [1] overflow flag (u32), [2..3] maxima: one clear
+    unsigned long long* mxp = cnt.p + 2;
+    uint32_t* ovp = reinterpret_cast<uint32_t*>(cnt.p + 1);
+    dc_launch(k_intern_insert, grid_for(c, (n + 3) / 4, 256), 256, 0, c->stream, keys, n, table.p, cap - 1, out_ids, cnt.p, ovp,
+                                                                 c->d_flags, mxp);
     DC_LAUNCHED(c);
     uint64_t h[2] = {0, 0};
-    DC_TRY(readback_multi(c, {{cnt.p, 8, &h[0]}, {ovf.p, 4, &h[1]}, {mx.p, 16, mxh}}));
+    DC_TRY(readback_multi(c, {{cnt.p, 8, &h[0]}, {ovp, 4, &h[1]}, {mxp, 16, mxh}}));
     D = h[0];
     bool overflow = (uint32_t)h[1] != 0;
     if (!overflow && D * 2 <= cap) break;

@@ -739,6 +739,7 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) { DC_PDL_
       for (int i = 0; i < OW_PER_LANE; ++i) sinkv ^= t[i] * (2 * i + 1);
     } else {
       uint32_t slot[OW_PER_LANE];
+      const long long c_3 = MODE == 9 ? clock64() : 0;
 #pragma unroll
       for (int i = 0; i < OW_PER_LANE; ++i) b[i] = own_bucket(t[i]);
 #pragma unroll
@@ -746,8 +747,7 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) { DC_PDL_
         const uint4 v = *reinterpret_cast<const uint4*>(&sm.key[4 * b[i]]);  // home bucket
         slot[i] = bucket_slot(v, t[i], b[i]);
       }
-      const long long c_3 = MODE == 9 ? clock64() : 0;
-      if (MODE == 9) t_bucket += c_3 - c_2;
+      if (MODE == 9) t_bucket += clock64() - c_2;
       // Hits are added directly. Misses (new or displaced keys, a few % of the samples) are
       // queued per warp and probed 32 at a time, so the slow path runs with all lanes busy.
       // (Claiming new keys inline with a CAS, or draining the queue every stage, cut the
