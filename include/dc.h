@@ -292,6 +292,21 @@ dc_status dc_export_folded(dc_ctx* ctx, const dc_cct* cct, uint32_t metric, uint
                            uint64_t* off_h, uint32_t* frames_h, uint64_t cap_lines, uint64_t cap_frames,
                            uint64_t* n_lines_h, uint64_t* n_frames_h);
 
+/* dc_cct_invert — SURVEY §8(f) NEXT-3, the bottom-up (caller-inverted) tree behind the paper's
+   "switchable top-down and bottom-up views" (§4.4). Every non-root node n of
+   cct whose exclusive value x(n) of `metric` (DC_METRIC_SAMPLES: PC samples) is non-zero
+   contributes x(n) along its call path read innermost first: its own frame, its caller's, ...,
+   the outermost frame (reading R27). *out receives a new ROLLED tree (library-owned, free with
+   dc_cct_free) whose nodes are the distinct such reversed prefixes, in canonical (depth,
+   lexicographic) order: its roots are the frames where the cost is spent (each root's inclusive
+   value = that frame's DC_VIEW_BOTTOM_UP sum), their children the callers. Its single metric
+   (index 0) holds, per inverted node q, the exact aggregate over the contributing nodes'
+   values: isum = their sum, icnt = their number, imin / isq the minimum / square sum; the
+   exclusive columns hold the nodes whose whole path reversed ends at q. The frame kinds are
+   carried over (kind masks in views apply). cct must hold exclusive values (state DIRTY or
+   ROLLED) and be complete (DC_ERR_STATE otherwise). Synchronizes. */
+dc_status dc_cct_invert(dc_ctx* ctx, const dc_cct* cct, uint32_t metric, dc_cct** out);
+
 /* dc_cpu_intervals — CPU-sample interval attribution (PAPER.md:359-363
    "subtract the previous timestamp from it, and use the result as the interval between two
    samples"; SPEC.md attribute_cpu_sample). Samples in trace order: thread[n] (u32), kind[n]

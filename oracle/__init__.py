@@ -338,3 +338,56 @@ def leaf_digest(leaf) -> str:
     """SHA-256 of the records' canonical leaf ids (u32 little-endian, trace order)."""
     import hashlib
     return hashlib.sha256(np.ascontiguousarray(np.asarray(leaf).astype("<u4", copy=False)).tobytes()).hexdigest()
+
+
+def inverted(arrays: dict, metric=0) -> dict:
+    """SURVEY §8(f) NEXT-3, the bottom-up (caller-inverted) tree ("switchable
+    top-down and bottom-up views"; reading R27), plain Python over the oracle's
+    canonical arrays, following the definition: every non-root node n with a non-zero exclusive
+    value x(n) contributes x(n) to each prefix of its call path read innermost first (its frame,
+    its caller's, ..., the outermost). Inverted nodes = the distinct such prefixes plus a root,
+    numbered by (length, lexicographic frame ids) like the CCT itself (reading R2); per node the
+    aggregate of the contributing values (count, sum, min, sum of squares); "x" columns: the
+    nodes whose whole reversed path ends there. metric: index, or METRIC_SAMPLES."""
+    parent, frame = arrays["parent"], arrays["frame"]
+    x = arrays["xsamples"] if metric == METRIC_SAMPLES else arrays["xsum"][metric]
+    inc, exc = {(): [0, 0, U64_MAX, 0]}, {}
+    for n in range(1, int(arrays["n_nodes"])):
+        v = int(x[n])
+        if v == 0:
+            continue
+        rev, a = [], n
+        while a != 0:
+            rev.append(int(frame[a]))
+            a = int(parent[a])
+        for k in range(len(rev) + 1):
+            agg = inc.setdefault(tuple(rev[:k]), [0, 0, U64_MAX, 0])
+            agg[0] += 1
+            agg[1] += v
+            agg[2] = min(agg[2], v)
+            agg[3] += v * v
+        e = exc.setdefault(tuple(rev), [0, 0, U64_MAX, 0])
+        e[0] += 1
+        e[1] += v
+        e[2] = min(e[2], v)
+        e[3] += v * v
+    keys = sorted(inc, key=lambda q: (len(q), q))
+    ids = {q: i for i, q in enumerate(keys)}
+    N = len(keys)
+    out = dict(n_nodes=N, parent=np.zeros(N, np.uint32), frame=np.zeros(N, np.uint32), depth=np.zeros(N, np.uint16))
+    for nm in ["xcnt", "icnt"]:
+        out[nm] = np.zeros(N, np.uint64)
+    for nm in ["xsum", "xmin", "xsq_lo", "xsq_hi", "isum", "imin", "isq_lo", "isq_hi"]:
+        out[nm] = np.zeros((1, N), np.uint64)
+    M64 = (1 << 64) - 1
+    for q, i in ids.items():
+        out["parent"][i] = 0xFFFFFFFF if i == 0 else ids[q[:-1]]
+        out["frame"][i] = 0xFFFFFFFF if i == 0 else q[-1]
+        out["depth"][i] = len(q)
+        c, s_, m, sq = inc[q]
+        out["icnt"][i], out["isum"][0][i], out["imin"][0][i] = c, s_, m
+        out["isq_lo"][0][i], out["isq_hi"][0][i] = sq & M64, sq >> 64
+        c, s_, m, sq = exc.get(q, [0, 0, U64_MAX, 0])
+        out["xcnt"][i], out["xsum"][0][i], out["xmin"][0][i] = c, s_, m
+        out["xsq_lo"][0][i], out["xsq_hi"][0][i] = sq & M64, sq >> 64
+    return out

@@ -366,6 +366,15 @@ def dc_export_folded(ctx: Context, cct: CCT, metric: int = 0):
     return nodes[:L].tolist(), vals[:L].tolist(), paths
 
 
+def dc_cct_invert(ctx: Context, cct: CCT, metric: int = 0) -> CCT:
+    """Bottom-up (caller-inverted) tree of the exclusive values of `metric` (include/dc.h
+    dc_cct_invert): roots = frames where the cost is spent, children = their callers. Returns a
+    new rolled-up CCT whose metric 0 aggregates the contributing nodes' values."""
+    h = ctypes.c_void_p()
+    ctx.check(lib().dc_cct_invert(ctx.h, cct.h, metric & 0xFFFFFFFF, ctypes.byref(h)), "dc_cct_invert")
+    return CCT(h, ctx)
+
+
 def folded_text(ctx: Context, cct: CCT, labels, metric: int = 0) -> str:
     """SPEC.md export_folded text: frames joined by ';' (';' inside labels replaced by ','), one
     space, the integer exclusive value; LF line endings. labels[frame id] -> str."""

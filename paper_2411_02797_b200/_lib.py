@@ -95,6 +95,7 @@ def lib():
             "dc_cpu_intervals": (i32, [P, P, P, P, u64, P, P]),
             "dc_seq_associate": (i32, [P, P, P, P, u64, P, P, P, u64, P, P, u64, ctypes.POINTER(u64), ctypes.POINTER(u64)]),
             "dc_export_folded": (i32, [P, P, u32, P, P, P, P, u64, u64, ctypes.POINTER(u64), ctypes.POINTER(u64)]),
+            "dc_cct_invert": (i32, [P, P, u32, ctypes.POINTER(P)]),
             "dc_cct_view_get": (i32, [P, ctypes.POINTER(dc_cct_view)]),
             "dc_cct_free": (None, [P]),
             "dc_nccl_unique_id": (i32, [P]),

@@ -38,6 +38,7 @@ dc_status seq_associate(Ctx* c, const int64_t* fseq, const uint64_t* foff, const
 dc_status hotspots_topk(Ctx* c, const dc_cct* t, dc_view view, uint32_t metric, uint32_t kind_mask, double threshold,
                         uint32_t k, uint32_t stall_node, dc_topk_entry* out_h, uint32_t* n_out_h);
 dc_status derived(Ctx* c, const dc_cct* t, uint32_t metric, int incl, double* mean, double* stdv);
+dc_status cct_invert(Ctx* c, const dc_cct* t, uint32_t metric, dc_cct** out);
 
 dc_status fail(Ctx* c, dc_status s, const char* fmt, ...) {
   char buf[512];
@@ -525,6 +526,14 @@ dc_status dc_export_folded(dc_ctx* ctx, const dc_cct* cct, uint32_t metric, uint
   ON_DEVICE(ctx);
   Region rg(ctx, "export");
   return export_folded(ctx, cct, metric, node_h, value_h, off_h, frames_h, cap_lines, cap_frames, n_lines_h, n_frames_h);
+}
+
+dc_status dc_cct_invert(dc_ctx* ctx, const dc_cct* cct, uint32_t metric, dc_cct** out) {
+  CHECK_CTX(ctx);
+  ARG(cct && out, "bad arguments");
+  ON_DEVICE(ctx);
+  Region rg(ctx, "invert");
+  return cct_invert(ctx, cct, metric, out);
 }
 
 dc_status dc_cpu_intervals(dc_ctx* ctx, const uint32_t* thread, const uint8_t* kind, const uint64_t* ts, uint64_t n,

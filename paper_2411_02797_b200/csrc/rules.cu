@@ -302,6 +302,87 @@ dc_status export_folded(Ctx* c, const dc_cct* t, uint32_t metric, uint32_t* node
   if (nf) DC_TRY(readback(c, frames.p, (size_t)nf * 4, frames_h));
   return DC_OK;
 }
+
+// ---------------------------------------------------------------- NEXT-3: bottom-up caller inversion
+// The bottom-up view ("switchable top-down and bottom-up views"): every
+// non-root node n with a non-zero exclusive value x(n) contributes x(n) along its call path read
+// innermost first (its own frame, then its caller's, ... up to the outermost), so the inverted
+// tree's roots are the frames where cost is spent and their children the callers (reading R27).
+// In bulk this IS a CCT build: the selected nodes become records whose paths are their reversed
+// call paths and whose metric is x(n); dc_cct_build + dc_cct_attribute_metrics + dc_cct_rollup
+// then give the inverted tree with canonical ids, inclusive value / count / min / square sum.
+__global__ void k_inv_emit(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos, const uint64_t* __restrict__ poff,
+                           const uint32_t* __restrict__ parent, const uint32_t* __restrict__ frame, const uint16_t* __restrict__ depth,
+                           const uint64_t* __restrict__ x, uint64_t N, uint32_t nl, uint64_t nf, uint64_t* __restrict__ off_out,
+                           uint64_t* __restrict__ val_out, uint32_t* __restrict__ frames_out) { DC_PDL_ENTER();
+  for (uint64_t n = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; n < N; n += (uint64_t)gridDim.x * blockDim.x) {
+    if (n == 0) off_out[nl] = nf;
+    if (!flag[n]) continue;
+    const uint32_t i = pos[n];
+    const uint64_t o = poff[n];
+    off_out[i] = o;
+    val_out[i] = x[n];
+    uint64_t k = 0;
+    const uint64_t L = depth[n];
+    for (uint32_t a = (uint32_t)n; a != 0 && k < L; a = parent[a]) frames_out[o + k++] = frame[a];
+  }
+}
+
+dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_frames, uint32_t* out_leaf, dc_cct** out);
+dc_status attribute_metrics(Ctx* c, dc_cct* t, const uint32_t* leaf, uint64_t R, const uint64_t* X, uint32_t M, uint64_t ld);
+dc_status rollup(Ctx* c, dc_cct* t);
+
+dc_status cct_invert(Ctx* c, const dc_cct* t, uint32_t metric, dc_cct** out) {
+  *out = nullptr;
+  if (t->state == 0) return fail(c, DC_ERR_STATE, "dc_cct_invert needs exclusive values (attribute metrics / samples first)");
+  if (t->partition) return fail(c, DC_ERR_STATE, "dc_cct_invert needs a complete tree (gather the partitions first)");
+  const uint64_t* x;
+  if (metric == DC_METRIC_SAMPLES) {
+    if (!t->xsamples) return fail(c, DC_ERR_STATE, "no PC samples attributed");
+    x = t->xsamples;
+  } else {
+    if (metric >= t->M) return fail(c, DC_ERR_ARG, "metric %u >= M = %u", metric, t->M);
+    x = t->col(C_XSUM, metric);
+  }
+  const uint64_t N = t->N;
+  Buf<uint32_t> flag, pos, tot32;
+  Buf<uint64_t> dep, poff, tot64;
+  DC_TRY(alloc(c, flag, N));
+  DC_TRY(alloc(c, pos, N));
+  DC_TRY(alloc(c, dep, N));
+  DC_TRY(alloc(c, poff, N));
+  DC_TRY(alloc(c, tot32, 1));
+  DC_TRY(alloc(c, tot64, 1));
+  dc_launch(k_fold_flags, grid_for(c, N, 256), 256, 0, c->stream, x, t->depth, N, flag.p, dep.p);
+  DC_LAUNCHED(c);
+  DC_TRY(excl_scan<uint32_t>(c, flag.p, pos.p, N, tot32.p));
+  DC_TRY(excl_scan<uint64_t>(c, dep.p, poff.p, N, tot64.p));
+  uint32_t nl = 0;
+  uint64_t nf = 0;
+  DC_TRY(readback_multi(c, {{tot32.p, 4, &nl}, {tot64.p, 8, &nf}}));
+  Buf<uint64_t> off, val;
+  Buf<uint32_t> frames, leaf;
+  DC_TRY(alloc(c, off, (uint64_t)nl + 1));
+  DC_TRY(alloc(c, val, nl));
+  DC_TRY(alloc(c, frames, nf));
+  DC_TRY(alloc(c, leaf, nl));
+  dc_launch(k_inv_emit, grid_for(c, N, 256), 256, 0, c->stream, flag.p, pos.p, poff.p, t->parent, t->frame, t->depth, x, N, nl, nf,
+            off.p, val.p, frames.p);
+  DC_LAUNCHED(c);
+  dc_paths ip{nl, off.p, nf ? frames.p : nullptr};
+  dc_dict kinds;  // carries the frame kinds into the inverted tree (views with kind masks)
+  kinds.D = t->n_frames;
+  kinds.kinds = t->frame_kind;
+  dc_cct* inv = nullptr;
+  DC_TRY(cct_build(c, &ip, t->frame_kind ? &kinds : nullptr, t->n_frames, leaf.p, &inv));
+  HandleGuard<dc_cct, dc_cct_free> guard{inv};
+  if (nl) DC_TRY(attribute_metrics(c, inv, leaf.p, nl, val.p, 1, nl));
+  else DC_TRY(attribute_metrics(c, inv, nullptr, 0, nullptr, 1, 0));
+  DC_TRY(rollup(c, inv));
+  guard.h = nullptr;
+  *out = inv;
+  return DC_OK;
+}
 }  // namespace dc
 
 // ---------------------------------------------------------------- NEXT-4: CPU-sample intervals

@@ -185,3 +185,55 @@ def test_seq_associate_and_bwd_fwd_rule_vs_oracle():
     for thr, floor in [(2.0, 1), (1.0, 10**5), (0.5, 0)]:
         got = dc.dc_analyze_flags(ctx, a["_cct"], dc.DC_RULE_BWD_FWD, 0, 1, 0xFFFFFFFF, thr, floor)
         assert got == ref.rule_flags(oracle.RULE_BWD_FWD, 0, 1, threshold=thr, floor=floor), (thr, floor)
+
+
+INV_KEYS = ["parent", "frame", "depth", "xcnt", "icnt", "xsum", "xmin", "xsq_lo", "xsq_hi", "isum", "imin", "isq_lo", "isq_hi"]
+
+
+def _same_inverted(got, ref, what):
+    assert got["n_nodes"] == ref["n_nodes"], what
+    for k in INV_KEYS:
+        assert np.array_equal(np.asarray(got[k]), np.asarray(ref[k])), (what, k)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_inverted_random_vs_oracle(seed):
+    """NEXT-3 bottom-up caller inversion (dc_cct_invert, reading R27): every array of the
+    inverted tree equals oracle.inverted, for a metric and for the PC-sample column."""
+    import paper_2411_02797_b200 as dc
+    rng = np.random.default_rng(9300 + seed)
+    ctx = dc.Context(0)
+    for it in range(20):
+        paths, X, samples, S = _rand_trace(rng)
+        off, fr = _csr(paths)
+        A = 1 + max([f for p in paths for f in p] + [0])
+        Xa = np.asarray(X, np.uint64).reshape(len(X), -1)
+        smp = _samples(samples)
+        a = gpu_run(off, fr, Xa, n_frames=A, samples=smp, n_stall=S, ctx=ctx)
+        ref = oracle_run(off, fr, Xa, Xa.shape[0], smp, len(paths), S).arrays()
+        for m in list(range(Xa.shape[0])) + [dc.DC_METRIC_SAMPLES]:
+            inv = dc.dc_cct_invert(ctx, a["_cct"], m)
+            _same_inverted(inv.to_numpy(), oracle.inverted(ref, oracle.METRIC_SAMPLES if m == dc.DC_METRIC_SAMPLES else m),
+                           f"seed {seed} it {it} metric {m}")
+            inv.free()
+
+
+def test_inverted_config2_vs_oracle_and_views():
+    """Config 2 (ResNet-50-shaped, 1M launches, M = 5, kinds from the dictionary): the inverted
+    tree of the kernel time equals the oracle's; its roots' hotspot view (kernel kind) equals
+    the bottom-up view of the original tree."""
+    import paper_2411_02797_b200 as dc
+    p = gen.programs.program(2)
+    tr = gen.make_trace(p, n_records=300_000)
+    a = gpu_run(tr.offsets.numpy(), keys=tr.keys.numpy(), metrics=tr.metrics.numpy())
+    oids, odict = oracle.intern(tr.keys.numpy())
+    ref = oracle_run(tr.offsets.numpy(), oids, tr.metrics.numpy(), p.n_metrics).arrays()
+    ctx, cct = a["_ctx"], a["_cct"]
+    inv = dc.dc_cct_invert(ctx, cct, 0)
+    _same_inverted(inv.to_numpy(), oracle.inverted(ref, 0), "config 2")
+    km = 1 << dc.DC_KIND_KERNEL
+    bu = dc.dc_hotspots_topk(ctx, cct, dc.DC_VIEW_BOTTOM_UP, 0, km, 0.0, 50)
+    iv = dc.dc_hotspots_topk(ctx, inv, dc.DC_VIEW_INCLUSIVE, 0, km, 0.0, 1 << 10)
+    ia = inv.to_numpy()
+    roots = [(int(ia["frame"][i]), val) for i, val, _ in iv if ia["depth"][i] == 1][:50]
+    assert roots == [(i, v) for i, v, _ in bu]

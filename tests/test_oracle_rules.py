@@ -246,3 +246,67 @@ def test_spec_fwd_bwd_rule_dlrm_fixture():
     assert abs(39_900 / 800 - 49.875) < 1e-12
     # epsilon: a forward time below the floor is skipped
     assert o.rule_flags(oracle.RULE_BWD_FWD, 0, 1, kind_mask=1 << OP, frame_kind=fk, threshold=2.0, floor=1000) == []
+
+
+# ------------------------------------------------------------------ NEXT-3: bottom-up (inverted) tree
+def test_inverted_hand_example():
+    """Reading R27 by hand (PAPER.md:444-446 bottom-up view; SPEC.md bottom-up: a kernel under
+    two call paths aggregates into one entry): frames A=0, B=1, C=2, K=3; records
+    [A,B,K]=20, [C,B,K]=10, [A,K]=5, [A,B]=7 -> reversed [K,B,A]=20, [K,B,C]=10, [K,A]=5, [B,A]=7;
+    roots B (7) and K (35 = 20 + 10 + 5); K's callers A (5) and B (30); B-under-K's callers A (20)
+    and C (10)."""
+    o = run([(0, 1, 3), (2, 1, 3), (0, 3), (0, 1)], [[20, 10, 5, 7]])
+    v = oracle.inverted(o.arrays(), 0)
+    assert v["n_nodes"] == 8
+    assert v["frame"].tolist()[1:] == [1, 3, 0, 0, 1, 0, 2]
+    assert v["parent"].tolist()[1:] == [0, 0, 1, 2, 2, 5, 5]
+    assert v["depth"].tolist() == [0, 1, 1, 2, 2, 2, 3, 3]
+    assert v["isum"][0].tolist() == [42, 7, 35, 7, 5, 30, 20, 10]
+    assert v["icnt"].tolist() == [4, 1, 3, 1, 1, 2, 1, 1]
+    assert v["imin"][0].tolist() == [5, 7, 5, 7, 5, 10, 20, 10]
+    assert v["xsum"][0].tolist() == [0, 0, 0, 7, 5, 0, 20, 10]
+
+
+def test_inverted_recursion_chain_closed_form():
+    """Paths A^k, k = 1..K, one record each of value 1: node A^j has exclusive 1, its reversed
+    path is A^j again, so the inverted tree is the same chain with inclusive count K - d + 1 at
+    depth d (a closed form, no oracle needed)."""
+    K = 40
+    o = run([(0,) * k for k in range(1, K + 1)], [[1] * K])
+    v = oracle.inverted(o.arrays(), 0)
+    assert v["n_nodes"] == K + 1
+    assert v["icnt"].tolist() == [K] + [K - d + 1 for d in range(1, K + 1)]
+    assert v["parent"].tolist()[1:] == list(range(K))
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_inverted_bruteforce_records_and_bottom_up_view(seed):
+    """Against the definition computed from the RECORDS (no CCT): group records by their whole
+    path, drop the empty path and zero sums, reverse, aggregate every prefix; the roots' values
+    also equal the oracle's own bottom-up view (C++, per-frame exclusive sums)."""
+    rng = np.random.default_rng(9100 + seed)
+    for _ in range(60):
+        paths, X, samples, S = _rand_trace(rng)
+        o = run(paths, X)
+        v = oracle.inverted(o.arrays(), 0)
+        ex = {}
+        for p, val in zip(paths, X[0]):
+            if len(p):
+                ex[tuple(p)] = ex.get(tuple(p), 0) + int(val)
+        pre = {(): [0, 0]}
+        for p, s_ in ex.items():
+            if s_ == 0:
+                continue
+            rev = tuple(reversed(p))
+            for k in range(len(rev) + 1):
+                a = pre.setdefault(rev[:k], [0, 0])
+                a[0] += 1
+                a[1] += s_
+        order = sorted(pre, key=lambda q: (len(q), q))
+        assert v["n_nodes"] == len(order)
+        assert v["frame"].tolist()[1:] == [q[-1] for q in order[1:]]
+        assert v["icnt"].tolist() == [pre[q][0] for q in order]
+        assert v["isum"][0].tolist() == [pre[q][1] for q in order]
+        bu = o.topk(oracle.VIEW_BOTTOM_UP, 0, 0xFFFFFFFF, None, -1.0, 1000)
+        roots = {int(v["frame"][i]): int(v["isum"][0][i]) for i in range(1, v["n_nodes"]) if v["depth"][i] == 1}
+        assert roots == {int(e["id"]): int(e["value"]) for e in bu if int(e["value"])}
