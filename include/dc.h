@@ -364,6 +364,15 @@ void dc_dict_free(dc_dict* d);
 /* NCCL plumbing: rank 0 calls dc_nccl_unique_id and broadcasts the 128 bytes (e.g. with
    torch.distributed); every rank then calls dc_comm_create (collective). */
 dc_status dc_nccl_unique_id(uint8_t out_h[128]);
+/* dc_merge_plan — the exchange plan of dc_cct_merge_ranks step 4 (host only, no device work;
+   exported so the multi-process host logic is testable without GPUs): given this rank's record
+   counts per destination send_counts[P][2] (node records, bin records) and the counts every
+   source sends to it recv_counts[P][2] (the all-to-all of send_counts), writes the offset of
+   each destination's slab in the send buffer send_off[P][2], the offset at which each source's
+   records land in the receive buffer recv_off[P][2] (sources in rank order) and the received
+   totals recv_total[2]. All arrays are host memory, counts in records. */
+dc_status dc_merge_plan(uint32_t P, const uint64_t* send_counts, const uint64_t* recv_counts, uint64_t* send_off,
+                        uint64_t* recv_off, uint64_t* recv_total);
 dc_status dc_comm_create(dc_ctx* ctx, const uint8_t uid[128], int nranks, int rank, dc_comm** out);
 void dc_comm_destroy(dc_comm* comm);
 

@@ -99,6 +99,7 @@ def lib():
             "dc_cct_view_get": (i32, [P, ctypes.POINTER(dc_cct_view)]),
             "dc_cct_free": (None, [P]),
             "dc_nccl_unique_id": (i32, [P]),
+            "dc_merge_plan": (i32, [u32, P, P, P, P, P]),
             "dc_comm_create": (i32, [P, P, i32, i32, ctypes.POINTER(P)]),
             "dc_comm_destroy": (None, [P]),
             "dc_cct_merge_ranks": (i32, [P, P, P, P, ctypes.POINTER(P), ctypes.POINTER(P)]),

@@ -17,6 +17,7 @@
 //      the (depth, lexicographic) node order — the same canonical CCT the single-GPU build gives.
 // dc_cct_merge_local runs steps 1-6 for P logical ranks on ONE GPU with a loopback exchange
 // (device copies instead of NCCL) — the emulated-rank test path.
+#include <memory>
 #include <vector>
 
 #include "prim.cuh"
@@ -69,11 +70,57 @@ __global__ void k_hash_level(const uint32_t* __restrict__ parent, const uint32_t
   }
 }
 
+// small trees: every level in one CTA (a barrier per level instead of a launch per level)
+__global__ void __launch_bounds__(1024) k_hash_levels_one(const uint32_t* __restrict__ parent, const uint32_t* __restrict__ frame,
+                                                          const uint32_t* __restrict__ l2g, const uint32_t* __restrict__ level_off,
+                                                          uint32_t maxd, uint64_t* h, uint64_t mask) { DC_PDL_ENTER();
+  if (threadIdx.x == 0) {
+    h[0] = H0_LO;
+    h[1] = H0_HI;
+  }
+  __syncthreads();
+  for (uint32_t d = 1; d <= maxd; ++d) {
+    const uint32_t a = level_off[d], b = level_off[d + 1];
+    for (uint32_t n = a + threadIdx.x; n < b; n += blockDim.x) {
+      const uint32_t p = parent[n];
+      uint64_t lo = __ldcg(h + 2ull * p), hi = __ldcg(h + 2ull * p + 1);
+      mix128(lo, hi, l2g ? l2g[frame[n]] : frame[n]);
+      h[2ull * n] = lo & mask;
+      h[2ull * n + 1] = hi & mask;
+    }
+    __syncthreads();
+  }
+}
+
 __device__ __forceinline__ uint32_t owner_of(uint64_t hi, uint32_t P) { return (uint32_t)__umul64hi(hi, (uint64_t)P); }
 
+// Block-cooperative slab slots: every thread of the block holds an owner o < P (or is idle);
+// ranks within the block come from shared-memory counters, then one global atomic per owner
+// per block tile (instead of one per record on P hot addresses). Returns the thread's slot in
+// its owner's slab (count_only: only adds the tile's counts). P <= PART_MAXP.
+constexpr uint32_t PART_MAXP = 1024;
+__device__ __forceinline__ uint64_t part_slot(uint32_t o, bool valid, uint32_t P, unsigned long long* cursor, bool count_only) {
+  __shared__ uint32_t s_cnt[PART_MAXP];
+  __shared__ unsigned long long s_base[PART_MAXP];
+  for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) s_cnt[i] = 0;
+  __syncthreads();
+  const uint32_t r = valid ? atomicAdd(&s_cnt[o], 1u) : 0u;
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
+    const uint32_t k = s_cnt[i];
+    s_base[i] = k ? atomicAdd(cursor + i, (unsigned long long)k) : 0ull;
+  }
+  __syncthreads();
+  const uint64_t slot = valid && !count_only ? s_base[o] + r : 0ull;
+  __syncthreads();
+  return slot;
+}
+
 __global__ void k_part_count(const uint64_t* __restrict__ h, uint64_t N, uint32_t P, unsigned long long* cnt) { DC_PDL_ENTER();
-  for (uint64_t n = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; n < N; n += (uint64_t)gridDim.x * blockDim.x)
-    atomicAdd(cnt + owner_of(h[2 * n + 1], P), 1ull);
+  for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x; b < N; b += (uint64_t)gridDim.x * blockDim.x) {  // block-uniform
+    const uint64_t n = b + threadIdx.x;
+    part_slot(n < N ? owner_of(h[2 * n + 1], P) : 0u, n < N, P, cnt, true);
+  }
 }
 
 // write node records into per-owner slabs (order inside a slab is irrelevant)
@@ -82,9 +129,10 @@ __global__ void k_part_nodes(const uint64_t* __restrict__ h, const uint32_t* __r
                              const uint64_t* __restrict__ icnt, const uint64_t* __restrict__ mcols, const uint64_t* __restrict__ xs,
                              const uint64_t* __restrict__ is, const uint64_t* __restrict__ xst, const uint64_t* __restrict__ ist,
                              uint64_t N, RecFmt f, uint32_t P, unsigned long long* cursor, uint64_t* __restrict__ out) { DC_PDL_ENTER();
-  for (uint64_t n = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; n < N; n += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t o = owner_of(h[2 * n + 1], P);
-    const unsigned long long slot = atomicAdd(cursor + o, 1ull);
+  for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x; b < N; b += (uint64_t)gridDim.x * blockDim.x) {  // block-uniform
+    const uint64_t n = b + threadIdx.x;
+    const uint64_t slot = part_slot(n < N ? owner_of(h[2 * n + 1], P) : 0u, n < N, P, cursor, false);
+    if (n >= N) continue;
     uint64_t* r = out + slot * f.W;
     r[0] = h[2 * n];
     r[1] = h[2 * n + 1];
@@ -118,13 +166,21 @@ __global__ void k_part_bins(const uint64_t* __restrict__ h, const uint32_t* __re
                             const uint64_t* __restrict__ bin_count, const uint32_t* __restrict__ pc_ctx,
                             const uint32_t* __restrict__ pc_off, uint64_t N, uint64_t nb, uint32_t P, int count_only,
                             unsigned long long* cnt_or_cursor, uint64_t* __restrict__ out) { DC_PDL_ENTER();
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nb; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t pn = bin_pcnode[i] - (uint32_t)N;
-    const uint32_t ctx = pc_ctx[pn], pc = pc_off[pn];
-    const uint64_t lo = h[2ull * ctx], hi = h[2ull * ctx + 1];
-    const uint32_t o = bin_owner(lo, hi, pc, P);
-    const unsigned long long slot = atomicAdd(cnt_or_cursor + o, 1ull);
-    if (count_only) continue;
+  for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x; b < nb; b += (uint64_t)gridDim.x * blockDim.x) {  // block-uniform
+    const uint64_t i = b + threadIdx.x;
+    const bool valid = i < nb;
+    uint32_t o = 0, pc = 0;
+    uint64_t lo = 0, hi = 0;
+    if (valid) {
+      const uint32_t pn = bin_pcnode[i] - (uint32_t)N;
+      const uint32_t ctx = pc_ctx[pn];
+      pc = pc_off[pn];
+      lo = h[2ull * ctx];
+      hi = h[2ull * ctx + 1];
+      o = bin_owner(lo, hi, pc, P);
+    }
+    const uint64_t slot = part_slot(o, valid, P, cnt_or_cursor, count_only != 0);
+    if (count_only || !valid) continue;
     uint64_t* r = out + slot * BIN_W;
     r[0] = lo;
     r[1] = hi;
@@ -134,179 +190,182 @@ __global__ void k_part_bins(const uint64_t* __restrict__ h, const uint32_t* __re
 }
 
 // ---------------------------------------------------------------- reduce received records
-__global__ void k_rec_key(const uint64_t* __restrict__ rec, uint32_t W, uint64_t n, int word, const uint32_t* __restrict__ order,
-                          uint64_t* __restrict__ key, uint32_t* __restrict__ val) { DC_PDL_ENTER();
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t src = order ? order[i] : (uint32_t)i;
-    key[i] = rec[(uint64_t)src * W + word];
-    val[i] = src;
-  }
+// Hash combine, no sort: every received record inserts its 128-bit key into an L2 hash table
+// (nodes: the full-path hash; bins: a 128-bit mix of (context hash, pc, stall)); the first
+// inserter of a key is its representative (its record index is published in the slot after the
+// key, release / acquire). Representatives are numbered by a scan over the records (output
+// order = receive order of the representatives); every record then adds / min-s its aggregate
+// words into the output record with global atomics, after checking its identity words against
+// the representative's: nodes (parent hash, global frame, depth), bins (the full key). Any
+// mismatch is a hash collision (DC_ERR_COLLISION): the merge is exact or fails loudly. A key
+// occurs at most once per source rank, so the atomics see at most P contributions per address.
+constexpr uint32_t KV_EMPTY = 0xFFFFFFFFu;
+
+__device__ __forceinline__ ulonglong2 kv_key(const uint64_t* r, bool bins) {
+  if (!bins) return make_ulonglong2(r[0], r[1]);
+  return make_ulonglong2(mix64(r[0] ^ (r[2] * 0x9E3779B97F4A7C15ull)), r[1] + mix64(r[2] + 0x632BE59BD9B4E019ull));
 }
 
-// sort record indices by (words wlo, whi) as a 128-bit key (LSD: low word, then high word)
-static dc_status sort_recs128(Ctx* c, const uint64_t* rec, uint32_t W, uint64_t n, int wlo, int whi, Buf<uint32_t>& order) {
-  Buf<uint64_t> k0, k1;
-  Buf<uint32_t> v0, v1;
-  DC_TRY(alloc(c, k0, n));
-  DC_TRY(alloc(c, k1, n));
-  DC_TRY(alloc(c, v0, n));
-  DC_TRY(alloc(c, v1, n));
-  dc_launch(k_rec_key, grid_for(c, n, 256), 256, 0, c->stream, rec, W, n, wlo, nullptr, k0.p, v0.p);
-  DC_LAUNCHED(c);
-  bool in1 = false;
-  DC_TRY(radix_sort_pairs(c, k0.p, v0.p, k1.p, v1.p, n, 0, 64, &in1));
-  uint32_t* ord = in1 ? v1.p : v0.p;
-  // second key in the current order
-  dc_launch(k_rec_key, grid_for(c, n, 256), 256, 0, c->stream, rec, W, n, whi, ord, in1 ? k0.p : k1.p, in1 ? v0.p : v1.p);
-  DC_LAUNCHED(c);
-  // the gather above wrote (key_hi, idx) into the "other" buffers; sort them stably
-  uint64_t* ka = in1 ? k0.p : k1.p;
-  uint32_t* va = in1 ? v0.p : v1.p;
-  uint64_t* kb = in1 ? k1.p : k0.p;
-  uint32_t* vb = in1 ? v1.p : v0.p;
-  bool in2 = false;
-  DC_TRY(radix_sort_pairs(c, ka, va, kb, vb, n, 0, 64, &in2));
-  DC_TRY(alloc(c, order, n));
-  DC_CUDA(c, cudaMemcpyAsync(order.p, in2 ? vb : va, n * 4, cudaMemcpyDeviceToDevice, c->stream));
-  return DC_OK;
-}
-
-__global__ void k_run_heads(const uint64_t* __restrict__ rec, uint32_t W, const uint32_t* __restrict__ order, uint64_t n, int w0,
-                            int w1, uint32_t* __restrict__ head) { DC_PDL_ENTER();
+__global__ void k_kv_insert(const uint64_t* __restrict__ rec, uint32_t W, uint64_t n, bool bins, ulonglong2* tab, uint32_t* tval,
+                            uint64_t mask, uint32_t* __restrict__ slot_of, uint32_t* d_flag) { DC_PDL_ENTER();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    bool hd = i == 0;
-    if (!hd) {
-      const uint64_t* a = rec + (uint64_t)order[i - 1] * W;
-      const uint64_t* b = rec + (uint64_t)order[i] * W;
-      for (int w = w0; w <= w1; ++w) hd |= a[w] != b[w];
-    }
-    head[i] = hd ? 1u : 0u;
-  }
-}
-
-// combine a run of node records (run heads only): sums, mins; verify parent hash, frame, depth
-__global__ void k_combine_nodes(const uint64_t* __restrict__ rec, const uint32_t* __restrict__ order, const uint32_t* __restrict__ head,
-                                const uint32_t* __restrict__ run_ix, uint64_t n, RecFmt f, uint64_t* __restrict__ out,
-                                uint32_t* d_collision) { DC_PDL_ENTER();
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    if (!head[i]) continue;
-    uint64_t* o = out + (uint64_t)run_ix[i] * f.W;
-    const uint64_t* a = rec + (uint64_t)order[i] * f.W;
-    for (uint32_t w = 0; w < f.W; ++w) o[w] = a[w];
-    for (uint64_t j = i + 1; j < n && !head[j]; ++j) {
-      const uint64_t* b = rec + (uint64_t)order[j] * f.W;
-      if (b[2] != a[2] || b[3] != a[3] || b[4] != a[4]) atomicOr(d_collision, 1u);
-      o[5] += b[5];
-      o[6] += b[6];
-      for (uint32_t m = 0; m < f.M; ++m) {
-        uint64_t* om = o + 7 + 8 * m;
-        const uint64_t* bm = b + 7 + 8 * m;
-        om[0] += bm[0];
-        om[1] = min(om[1], bm[1]);
-        uint64_t lo = om[2] + bm[2];
-        om[3] += bm[3] + (lo < om[2] ? 1u : 0u);
-        om[2] = lo;
-        om[4] += bm[4];
-        om[5] = min(om[5], bm[5]);
-        lo = om[6] + bm[6];
-        om[7] += bm[7] + (lo < om[6] ? 1u : 0u);
-        om[6] = lo;
+    const ulonglong2 k = kv_key(rec + i * W, bins);
+    uint64_t s = mix64(k.x ^ k.y) & mask;
+    for (uint64_t probe = 0;; ++probe, s = (s + 1) & mask) {
+      if (probe > mask) {  // cannot happen: the table holds 2x the records
+        atomicOr(d_flag, 2u);
+        slot_of[i] = KV_EMPTY;
+        break;
       }
-      if (f.has_pc)
-        for (uint32_t w = 7 + 8 * f.M; w < f.W; ++w) o[w] += b[w];
+      const ulonglong2 cur = ld_relaxed_v2(tab + s);
+      bool mine = cur.x == k.x && cur.y == k.y;
+      if (!mine) {
+        if (cur.x != ~0ull || cur.y != ~0ull) continue;
+        const unsigned __int128 expect = ~(unsigned __int128)0;
+        const unsigned __int128 want = ((unsigned __int128)k.y << 64) | k.x;
+        const unsigned __int128 old = atomicCAS(reinterpret_cast<unsigned __int128*>(tab + s), expect, want);
+        if (old == expect) {  // representative: publish the record index
+          asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(tval + s), "r"((uint32_t)i) : "memory");
+          slot_of[i] = (uint32_t)s;
+          break;
+        }
+        mine = old == want;
+        if (!mine) continue;
+      }
+      slot_of[i] = (uint32_t)s;
+      break;
     }
   }
 }
 
-__global__ void k_combine_bins(const uint64_t* __restrict__ rec, const uint32_t* __restrict__ order, const uint32_t* __restrict__ head,
-                               const uint32_t* __restrict__ run_ix, uint64_t n, uint64_t* __restrict__ out) { DC_PDL_ENTER();
+__device__ __forceinline__ uint32_t kv_rep(const uint32_t* tval, uint32_t s) {
+  uint32_t v;
+  for (uint64_t spin = 0;; ++spin) {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(tval + s) : "memory");
+    if (v != KV_EMPTY) return v;
+    if (spin > DC_SPIN_LIMIT) __trap();
+  }
+}
+
+__global__ void k_kv_heads(const uint32_t* __restrict__ slot_of, const uint32_t* tval, uint64_t n, uint32_t* __restrict__ head) { DC_PDL_ENTER();
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t s = slot_of[i];
+    head[i] = s != KV_EMPTY && kv_rep(tval, s) == (uint32_t)i ? 1u : 0u;
+  }
+}
+
+// representatives: output index into the slot's value (after the heads pass) + identity record
+__global__ void k_kv_init(const uint64_t* __restrict__ rec, uint32_t W, uint64_t n, bool bins, RecFmt f,
+                          const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ head, const uint32_t* __restrict__ ridx,
+                          uint32_t* tidx, uint64_t* __restrict__ out) { DC_PDL_ENTER();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     if (!head[i]) continue;
-    uint64_t* o = out + (uint64_t)run_ix[i] * BIN_W;
-    const uint64_t* a = rec + (uint64_t)order[i] * BIN_W;
-    o[0] = a[0];
-    o[1] = a[1];
-    o[2] = a[2];
-    uint64_t s = a[3];
-    for (uint64_t j = i + 1; j < n && !head[j]; ++j) s += rec[(uint64_t)order[j] * BIN_W + 3];
-    o[3] = s;
+    const uint32_t o = ridx[i];
+    tidx[slot_of[i]] = o;
+    const uint64_t* a = rec + i * W;
+    uint64_t* r = out + (uint64_t)o * W;
+    if (bins) {
+      r[0] = a[0];
+      r[1] = a[1];
+      r[2] = a[2];
+      r[3] = 0;
+      continue;
+    }
+    for (uint32_t w = 0; w < 5; ++w) r[w] = a[w];
+    for (uint32_t w = 5; w < W; ++w) r[w] = 0;
+    for (uint32_t m = 0; m < f.M; ++m) {
+      r[7 + 8 * m + 1] = ~0ull;  // xmin
+      r[7 + 8 * m + 5] = ~0ull;  // imin
+    }
   }
 }
 
-// sort + combine: records -> unique records (count returned)
-static dc_status reduce_records(Ctx* c, const uint64_t* rec, uint64_t n, uint32_t W, bool bins, const RecFmt& f,
-                                Buf<uint64_t>& out, uint64_t* n_out, uint32_t* d_collision) {
-  *n_out = 0;
-  if (n == 0) {
-    DC_TRY(alloc(c, out, 1));
-    return DC_OK;
+__global__ void k_kv_combine(const uint64_t* __restrict__ rec, uint32_t W, uint64_t n, bool bins, RecFmt f,
+                             const uint32_t* __restrict__ slot_of, const uint32_t* tval, const uint32_t* __restrict__ tidx,
+                             unsigned long long* __restrict__ out, uint32_t* d_collision) { DC_PDL_ENTER();
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t s = slot_of[i];
+    if (s == KV_EMPTY) continue;
+    const uint64_t* b = rec + i * W;
+    const uint64_t* a = rec + (uint64_t)kv_rep(tval, s) * W;
+    unsigned long long* o = out + (uint64_t)tidx[s] * W;
+    if (bins) {
+      if (a[0] != b[0] || a[1] != b[1] || a[2] != b[2]) atomicOr(d_collision, 1u);
+      atomicAdd(o + 3, (unsigned long long)b[3]);
+      continue;
+    }
+    if (a[2] != b[2] || a[3] != b[3] || a[4] != b[4]) atomicOr(d_collision, 1u);
+    if (b[5]) atomicAdd(o + 5, (unsigned long long)b[5]);
+    if (b[6]) atomicAdd(o + 6, (unsigned long long)b[6]);
+    for (uint32_t m = 0; m < f.M; ++m) {
+      unsigned long long* om = o + 7 + 8 * m;
+      const uint64_t* bm = b + 7 + 8 * m;
+      if (bm[0]) atomicAdd(om, (unsigned long long)bm[0]);
+      if (bm[1] != ~0ull) atomicMin(om + 1, (unsigned long long)bm[1]);
+      if (bm[2] | bm[3]) atomic_add_u128(om + 2, om + 3, bm[2], bm[3]);
+      if (bm[4]) atomicAdd(om + 4, (unsigned long long)bm[4]);
+      if (bm[5] != ~0ull) atomicMin(om + 5, (unsigned long long)bm[5]);
+      if (bm[6] | bm[7]) atomic_add_u128(om + 6, om + 7, bm[6], bm[7]);
+    }
+    if (f.has_pc)
+      for (uint32_t w = 7 + 8 * f.M; w < W; ++w)
+        if (b[w]) atomicAdd(o + w, (unsigned long long)b[w]);
   }
-  Buf<uint32_t> order, head, run;
+}
+
+// received node records (W words) and bin records (BIN_W) -> unique records; one host round trip
+static dc_status reduce_received(Ctx* c, const uint64_t* rn_p, uint64_t rn, const uint64_t* rb_p, uint64_t rb, const RecFmt& f,
+                                 Buf<uint64_t>& out_n, uint64_t* n_out, Buf<uint64_t>& out_b, uint64_t* b_out, uint32_t* d_collision) {
+  struct Side {
+    const uint64_t* rec;
+    uint64_t n;
+    uint32_t W;
+    bool bins;
+    uint64_t cap;
+    Buf<ulonglong2> tab;
+    Buf<uint32_t> tval, tidx, slot, head, ridx;
+  } side[2] = {{rn_p, rn, f.W, false, 0, {}, {}, {}, {}, {}, {}}, {rb_p, rb, (uint32_t)BIN_W, true, 0, {}, {}, {}, {}, {}, {}}};
   Buf<uint32_t> tot;
-  (void)bins;
-  DC_TRY(sort_recs128(c, rec, W, n, 0, 1, order));
-  DC_TRY(alloc(c, head, n));
-  DC_TRY(alloc(c, run, n));
-  DC_TRY(alloc(c, tot, 1));
-  dc_launch(k_run_heads, grid_for(c, n, 256), 256, 0, c->stream, rec, W, order.p, n, 0, 1, head.p);
-  DC_LAUNCHED(c);
-  DC_TRY(excl_scan<uint32_t>(c, head.p, run.p, n, tot.p));
-  uint32_t hn = 0;
-  DC_TRY(readback(c, tot.p, 4, &hn));
-  DC_TRY(alloc(c, out, (uint64_t)hn * W));
-  dc_launch(k_combine_nodes, grid_for(c, n, 256), 256, 0, c->stream, rec, order.p, head.p, run.p, n, f, out.p, d_collision);
-  DC_LAUNCHED(c);
-  *n_out = hn;
-  return DC_OK;
-}
-
-__global__ void k_gather_recs(const uint64_t* __restrict__ rec, uint32_t W, const uint32_t* __restrict__ order, uint64_t n,
-                              uint64_t* __restrict__ out) { DC_PDL_ENTER();
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n * W; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t r = i / W, w = i % W;
-    out[i] = rec[(uint64_t)order[r] * W + w];
-  }
-}
-
-// bins: sort by (h_lo, h_hi, pc|stall) = LSD word 2, then 0, then 1; combine counts
-static dc_status reduce_bins(Ctx* c, const uint64_t* rec, uint64_t n, Buf<uint64_t>& out, uint64_t* n_out) {
-  *n_out = 0;
-  if (n == 0) {
-    DC_TRY(alloc(c, out, 1));
-    return DC_OK;
-  }
-  Buf<uint64_t> k0, k1, sorted;
-  Buf<uint32_t> v0, v1, head, run, tot;
-  DC_TRY(alloc(c, k0, n));
-  DC_TRY(alloc(c, k1, n));
-  DC_TRY(alloc(c, v0, n));
-  DC_TRY(alloc(c, v1, n));
-  const uint32_t* ord = nullptr;
-  bool in1 = false;
-  for (int word : {2, 0, 1}) {
-    uint64_t* kin = in1 ? k1.p : k0.p;
-    uint32_t* vin = in1 ? v1.p : v0.p;
-    uint64_t* kout = in1 ? k0.p : k1.p;
-    uint32_t* vout = in1 ? v0.p : v1.p;
-    dc_launch(k_rec_key, grid_for(c, n, 256), 256, 0, c->stream, rec, BIN_W, n, word, ord, kin, vin);
+  DC_TRY(alloc_zero(c, tot, 3));  // [0] nodes, [1] bins, [2] table overflow flag
+  for (int k = 0; k < 2; ++k) {
+    Side& sd = side[k];
+    if (!sd.n) continue;
+    if (sd.n >= (1ull << 31)) return fail(c, DC_ERR_CAPACITY, "merge: %llu received records", (unsigned long long)sd.n);
+    sd.cap = 1024;
+    while (sd.cap < 2 * sd.n) sd.cap <<= 1;
+    DC_TRY(alloc(c, sd.tab, sd.cap));
+    DC_TRY(alloc(c, sd.tval, sd.cap));
+    DC_TRY(alloc(c, sd.tidx, sd.cap));
+    DC_TRY(alloc(c, sd.slot, sd.n));
+    DC_TRY(alloc(c, sd.head, sd.n));
+    DC_TRY(alloc(c, sd.ridx, sd.n));
+    DC_CUDA(c, cudaMemsetAsync(sd.tab.p, 0xFF, sd.cap * 16, c->stream));
+    DC_CUDA(c, cudaMemsetAsync(sd.tval.p, 0xFF, sd.cap * 4, c->stream));
+    dc_launch(k_kv_insert, grid_for(c, sd.n, 256), 256, 0, c->stream, sd.rec, sd.W, sd.n, sd.bins, sd.tab.p, sd.tval.p, sd.cap - 1,
+              sd.slot.p, tot.p + 2);
     DC_LAUNCHED(c);
-    bool r1 = false;
-    DC_TRY(radix_sort_pairs(c, kin, vin, kout, vout, n, 0, 64, &r1));
-    if (r1) in1 = !in1;
-    ord = in1 ? v1.p : v0.p;
+    dc_launch(k_kv_heads, grid_for(c, sd.n, 256), 256, 0, c->stream, sd.slot.p, sd.tval.p, sd.n, sd.head.p);
+    DC_LAUNCHED(c);
+    DC_TRY(excl_scan<uint32_t>(c, sd.head.p, sd.ridx.p, sd.n, tot.p + k));
   }
-  DC_TRY(alloc(c, head, n));
-  DC_TRY(alloc(c, run, n));
-  DC_TRY(alloc(c, tot, 1));
-  dc_launch(k_run_heads, grid_for(c, n, 256), 256, 0, c->stream, rec, BIN_W, ord, n, 0, 2, head.p);
-  DC_LAUNCHED(c);
-  DC_TRY(excl_scan<uint32_t>(c, head.p, run.p, n, tot.p));
-  uint32_t hn = 0;
-  DC_TRY(readback(c, tot.p, 4, &hn));
-  DC_TRY(alloc(c, out, (uint64_t)hn * BIN_W));
-  dc_launch(k_combine_bins, grid_for(c, n, 256), 256, 0, c->stream, rec, ord, head.p, run.p, n, out.p);
-  DC_LAUNCHED(c);
-  *n_out = hn;
+  uint32_t ht[3] = {0, 0, 0};
+  DC_TRY(readback(c, tot.p, 12, ht));
+  if (ht[2]) return fail(c, DC_ERR_STATE, "internal: merge hash table overflow");
+  *n_out = ht[0];
+  *b_out = ht[1];
+  DC_TRY(alloc(c, out_n, (uint64_t)ht[0] * f.W));
+  DC_TRY(alloc(c, out_b, (uint64_t)ht[1] * BIN_W));
+  for (int k = 0; k < 2; ++k) {
+    Side& sd = side[k];
+    if (!sd.n) continue;
+    uint64_t* out = k ? out_b.p : out_n.p;
+    dc_launch(k_kv_init, grid_for(c, sd.n, 256), 256, 0, c->stream, sd.rec, sd.W, sd.n, sd.bins, f, sd.slot.p, sd.head.p, sd.ridx.p,
+              sd.tidx.p, out);
+    DC_LAUNCHED(c);
+    dc_launch(k_kv_combine, grid_for(c, sd.n, 256), 256, 0, c->stream, sd.rec, sd.W, sd.n, sd.bins, f, sd.slot.p, sd.tval.p,
+              sd.tidx.p, (unsigned long long*)out, d_collision);
+    DC_LAUNCHED(c);
+  }
   return DC_OK;
 }
 
@@ -320,15 +379,20 @@ static dc_status partition(Ctx* c, const dc_cct* t, const uint32_t* l2g, uint32_
   const uint64_t N = t->N;
   Buf<uint64_t> h;
   DC_TRY(alloc(c, h, 2 * N));
-  dc_launch(k_hash_root, 1, 1, 0, c->stream, h.p);
-  DC_LAUNCHED(c);
-  std::vector<uint32_t> lo(t->max_depth + 2);
-  DC_TRY(readback(c, t->level_off, lo.size() * 4, lo.data()));
-  for (uint32_t d = 1; d <= t->max_depth; ++d) {
-    const uint32_t a = lo[d], b = lo[d + 1];
-    if (b > a) {
-      dc_launch(k_hash_level, grid_for(c, b - a, 256), 256, 0, c->stream, t->parent, t->frame, l2g, a, b, h.p, c->merge_mask);
-      DC_LAUNCHED(c);
+  if (N <= (1u << 16)) {
+    dc_launch(k_hash_levels_one, 1, 1024, 0, c->stream, t->parent, t->frame, l2g, t->level_off, t->max_depth, h.p, c->merge_mask);
+    DC_LAUNCHED(c);
+  } else {
+    dc_launch(k_hash_root, 1, 1, 0, c->stream, h.p);
+    DC_LAUNCHED(c);
+    std::vector<uint32_t> lo(t->max_depth + 2);
+    DC_TRY(readback(c, t->level_off, lo.size() * 4, lo.data()));
+    for (uint32_t d = 1; d <= t->max_depth; ++d) {
+      const uint32_t a = lo[d], b = lo[d + 1];
+      if (b > a) {
+        dc_launch(k_hash_level, grid_for(c, b - a, 256), 256, 0, c->stream, t->parent, t->frame, l2g, a, b, h.p, c->merge_mask);
+        DC_LAUNCHED(c);
+      }
     }
   }
   Buf<unsigned long long> cnt, cur;
@@ -702,6 +766,22 @@ struct dc_comm {
 
 extern "C" {
 
+dc_status dc_merge_plan(uint32_t P, const uint64_t* send_counts, const uint64_t* recv_counts, uint64_t* send_off,
+                        uint64_t* recv_off, uint64_t* recv_total) {
+  if (!P || !send_counts || !recv_counts || !send_off || !recv_off || !recv_total) return DC_ERR_ARG;
+  uint64_t so[2] = {0, 0}, ro[2] = {0, 0};
+  for (uint32_t q = 0; q < P; ++q)
+    for (int k = 0; k < 2; ++k) {
+      send_off[2 * q + k] = so[k];
+      recv_off[2 * q + k] = ro[k];
+      so[k] += send_counts[2 * q + k];
+      ro[k] += recv_counts[2 * q + k];
+    }
+  recv_total[0] = ro[0];
+  recv_total[1] = ro[1];
+  return DC_OK;
+}
+
 dc_status dc_nccl_unique_id(uint8_t out_h[128]) {
 #if DC_HAVE_NCCL
   if (!out_h) return DC_ERR_ARG;
@@ -715,7 +795,7 @@ dc_status dc_nccl_unique_id(uint8_t out_h[128]) {
 }
 
 dc_status dc_comm_create(dc_ctx* ctx, const uint8_t uid[128], int nranks, int rank, dc_comm** out) {
-  if (!ctx || !uid || !out || nranks < 1 || rank < 0 || rank >= nranks) return DC_ERR_ARG;
+  if (!ctx || !uid || !out || nranks < 1 || rank < 0 || rank >= nranks || (uint32_t)nranks > PART_MAXP) return DC_ERR_ARG;
 #if DC_HAVE_NCCL
   cudaSetDevice(ctx->device);
   dc_comm* cm = new dc_comm();
@@ -801,28 +881,23 @@ dc_status dc_cct_merge_ranks(dc_ctx* ctx, dc_comm* cm, const dc_cct* local, cons
   }
   DC_CUDA(c, cudaMemcpyAsync(sc.p, hsc.data(), 16 * P, cudaMemcpyHostToDevice, c->stream));
   NCCL_TRY(c, ncclAlltoAll(sc.p, rc.p, 2, ncclUint64, cm->comm, c->stream));
-  std::vector<uint64_t> hrc(2 * P);
+  std::vector<uint64_t> hrc(2 * P), soff(2 * P), roff(2 * P);
   DC_TRY(readback(c, rc.p, 16 * P, hrc.data()));
-  uint64_t rn = 0, rb = 0;
-  for (int q = 0; q < P; ++q) {
-    rn += hrc[2 * q];
-    rb += hrc[2 * q + 1];
-  }
+  uint64_t rtot[2];
+  DC_TRY(dc_merge_plan((uint32_t)P, hsc.data(), hrc.data(), soff.data(), roff.data(), rtot));  // host-only exchange plan
+  const uint64_t rn = rtot[0], rb = rtot[1];
   Buf<uint64_t> rnodes, rbins;
   DC_TRY(alloc(c, rnodes, rn * f.W));
   DC_TRY(alloc(c, rbins, rb * BIN_W));
   {
-    uint64_t so = 0, ro = 0, sbo = 0, rbo = 0;
     NCCL_TRY(c, ncclGroupStart());
     for (int q = 0; q < P; ++q) {
-      if (s.ncnt[q]) NCCL_TRY(c, ncclSend(s.nodes.p + so * f.W, s.ncnt[q] * f.W, ncclUint64, q, cm->comm, c->stream));
-      if (hrc[2 * q]) NCCL_TRY(c, ncclRecv(rnodes.p + ro * f.W, hrc[2 * q] * f.W, ncclUint64, q, cm->comm, c->stream));
-      if (s.bcnt[q]) NCCL_TRY(c, ncclSend(s.bins.p + sbo * BIN_W, s.bcnt[q] * BIN_W, ncclUint64, q, cm->comm, c->stream));
-      if (hrc[2 * q + 1]) NCCL_TRY(c, ncclRecv(rbins.p + rbo * BIN_W, hrc[2 * q + 1] * BIN_W, ncclUint64, q, cm->comm, c->stream));
-      so += s.ncnt[q];
-      ro += hrc[2 * q];
-      sbo += s.bcnt[q];
-      rbo += hrc[2 * q + 1];
+      if (hsc[2 * q]) NCCL_TRY(c, ncclSend(s.nodes.p + soff[2 * q] * f.W, hsc[2 * q] * f.W, ncclUint64, q, cm->comm, c->stream));
+      if (hrc[2 * q]) NCCL_TRY(c, ncclRecv(rnodes.p + roff[2 * q] * f.W, hrc[2 * q] * f.W, ncclUint64, q, cm->comm, c->stream));
+      if (hsc[2 * q + 1])
+        NCCL_TRY(c, ncclSend(s.bins.p + soff[2 * q + 1] * BIN_W, hsc[2 * q + 1] * BIN_W, ncclUint64, q, cm->comm, c->stream));
+      if (hrc[2 * q + 1])
+        NCCL_TRY(c, ncclRecv(rbins.p + roff[2 * q + 1] * BIN_W, hrc[2 * q + 1] * BIN_W, ncclUint64, q, cm->comm, c->stream));
     }
     NCCL_TRY(c, ncclGroupEnd());
   }
@@ -831,8 +906,7 @@ dc_status dc_cct_merge_ranks(dc_ctx* ctx, dc_comm* cm, const dc_cct* local, cons
   DC_TRY(alloc_zero(c, coll, 1));
   Buf<uint64_t> un, ub;
   uint64_t nun = 0, nub = 0;
-  DC_TRY(reduce_records(c, rnodes.p, rn, f.W, false, f, un, &nun, coll.p));
-  DC_TRY(reduce_bins(c, rbins.p, rb, ub, &nub));
+  DC_TRY(reduce_received(c, rnodes.p, rn, rbins.p, rb, f, un, &nun, ub, &nub, coll.p));
   uint32_t hcoll = 0;
   DC_TRY(readback(c, coll.p, 4, &hcoll));
   if (hcoll) {
@@ -900,7 +974,7 @@ dc_status dc_cct_gather(dc_ctx* ctx, dc_comm* cm, const dc_cct* part, int root, 
 
 dc_status dc_cct_merge_local(dc_ctx* ctx, uint32_t P, dc_cct* const* locals, dc_dict* const* dicts, dc_cct** out_canonical,
                              dc_dict** out_global_dict) {
-  if (!ctx || !P || !locals || !dicts || !out_canonical || !out_global_dict) return DC_ERR_ARG;
+  if (!ctx || !P || P > PART_MAXP || !locals || !dicts || !out_canonical || !out_global_dict) return DC_ERR_ARG;
   Ctx* c = ctx;
   DC_CUDA(c, cudaSetDevice(c->device));
   for (uint32_t p = 0; p < P; ++p) {
@@ -910,7 +984,9 @@ dc_status dc_cct_merge_local(dc_ctx* ctx, uint32_t P, dc_cct* const* locals, dc_
         (locals[p]->xsamples != nullptr) != (locals[0]->xsamples != nullptr))
       return fail(c, DC_ERR_ARG, "local trees disagree on metric / stall columns");
   }
+  Region r_all(c, "merge");
   // 1. dictionaries (loopback all-gather = concatenation)
+  std::unique_ptr<Region> r1(new Region(c, "merge:dict"));
   std::vector<uint64_t> koff(P + 1, 0);
   for (uint32_t p = 0; p < P; ++p) koff[p + 1] = koff[p] + dicts[p]->D;
   Buf<dc_frame_key> packed;
@@ -922,41 +998,51 @@ dc_status dc_cct_merge_local(dc_ctx* ctx, uint32_t P, dc_cct* const* locals, dc_
   std::vector<Buf<uint32_t>> l2g;
   DC_TRY(unify_dicts(c, packed.p, koff, &gd, l2g));
   const RecFmt f = fmt_of(locals[0]);
+  r1.reset();
   // 2-3. every logical rank partitions
   std::vector<Slabs> slabs(P);
-  for (uint32_t p = 0; p < P; ++p) DC_TRY(partition(c, locals[p], l2g[p].p, P, f, slabs[p]));
+  {
+    Region rp(c, "merge:partition");
+    for (uint32_t p = 0; p < P; ++p) DC_TRY(partition(c, locals[p], l2g[p].p, P, f, slabs[p]));
+  }
+  std::unique_ptr<Region> r3(new Region(c, "merge:exchange+reduce"));
   // 4. loopback exchange + 5. reduce per destination; 6. gather = concatenation of partitions
   std::vector<Buf<uint64_t>> parts_n(P), parts_b(P);
   std::vector<uint64_t> pn(P), pb(P);
   Buf<uint32_t> coll;
   DC_TRY(alloc_zero(c, coll, 1));
-  for (uint32_t q = 0; q < P; ++q) {
-    uint64_t rn = 0, rb = 0;
-    for (uint32_t p = 0; p < P; ++p) {
-      rn += slabs[p].ncnt[q];
-      rb += slabs[p].bcnt[q];
+  // the exchange plan of every logical rank (the same host-only dc_merge_plan as the NCCL path)
+  std::vector<std::vector<uint64_t>> sc(P, std::vector<uint64_t>(2 * P)), soff(P, std::vector<uint64_t>(2 * P));
+  for (uint32_t p = 0; p < P; ++p) {
+    for (uint32_t q = 0; q < P; ++q) {
+      sc[p][2 * q] = slabs[p].ncnt[q];
+      sc[p][2 * q + 1] = slabs[p].bcnt[q];
     }
+    std::vector<uint64_t> none(2 * P, 0), unused(2 * P);
+    uint64_t rt[2];
+    DC_TRY(dc_merge_plan(P, sc[p].data(), none.data(), soff[p].data(), unused.data(), rt));
+  }
+  for (uint32_t q = 0; q < P; ++q) {
+    std::vector<uint64_t> rc(2 * P), roff(2 * P), unused(2 * P);
+    for (uint32_t p = 0; p < P; ++p) {
+      rc[2 * p] = sc[p][2 * q];
+      rc[2 * p + 1] = sc[p][2 * q + 1];
+    }
+    uint64_t rtot[2];
+    DC_TRY(dc_merge_plan(P, sc[q].data(), rc.data(), unused.data(), roff.data(), rtot));
+    const uint64_t rn = rtot[0], rb = rtot[1];
     Buf<uint64_t> rnodes, rbins;
     DC_TRY(alloc(c, rnodes, rn * f.W));
     DC_TRY(alloc(c, rbins, rb * BIN_W));
-    uint64_t ro = 0, rbo = 0;
-    for (uint32_t p = 0; p < P; ++p) {
-      uint64_t so = 0, sbo = 0;
-      for (uint32_t q2 = 0; q2 < q; ++q2) {
-        so += slabs[p].ncnt[q2];
-        sbo += slabs[p].bcnt[q2];
-      }
-      if (slabs[p].ncnt[q])
-        DC_CUDA(c, cudaMemcpyAsync(rnodes.p + ro * f.W, slabs[p].nodes.p + so * f.W, slabs[p].ncnt[q] * f.W * 8,
+    for (uint32_t p = 0; p < P; ++p) {  // loopback "send": p's slab for q lands at q's receive offset for p
+      if (sc[p][2 * q])
+        DC_CUDA(c, cudaMemcpyAsync(rnodes.p + roff[2 * p] * f.W, slabs[p].nodes.p + soff[p][2 * q] * f.W, sc[p][2 * q] * f.W * 8,
                                    cudaMemcpyDeviceToDevice, c->stream));
-      if (slabs[p].bcnt[q])
-        DC_CUDA(c, cudaMemcpyAsync(rbins.p + rbo * BIN_W, slabs[p].bins.p + sbo * BIN_W, slabs[p].bcnt[q] * BIN_W * 8,
-                                   cudaMemcpyDeviceToDevice, c->stream));
-      ro += slabs[p].ncnt[q];
-      rbo += slabs[p].bcnt[q];
+      if (sc[p][2 * q + 1])
+        DC_CUDA(c, cudaMemcpyAsync(rbins.p + roff[2 * p + 1] * BIN_W, slabs[p].bins.p + soff[p][2 * q + 1] * BIN_W,
+                                   sc[p][2 * q + 1] * BIN_W * 8, cudaMemcpyDeviceToDevice, c->stream));
     }
-    DC_TRY(reduce_records(c, rnodes.p, rn, f.W, false, f, parts_n[q], &pn[q], coll.p));
-    DC_TRY(reduce_bins(c, rbins.p, rb, parts_b[q], &pb[q]));
+    DC_TRY(reduce_received(c, rnodes.p, rn, rbins.p, rb, f, parts_n[q], &pn[q], parts_b[q], &pb[q], coll.p));
   }
   uint32_t hcoll = 0;
   DC_TRY(readback(c, coll.p, 4, &hcoll));
@@ -980,8 +1066,12 @@ dc_status dc_cct_merge_local(dc_ctx* ctx, uint32_t P, dc_cct* const* locals, dc_
     o += pn[q];
     ob += pb[q];
   }
+  r3.reset();
   dc_cct* canon = nullptr;
-  DC_TRY(canonicalize(c, allv.p, tn, allb.p, tb, f, (uint32_t)gd->D, &canon));
+  {
+    Region rc(c, "merge:canonicalize");
+    DC_TRY(canonicalize(c, allv.p, tn, allb.p, tb, f, (uint32_t)gd->D, &canon));
+  }
   if (gd->D) {  // kinds for views
     DC_TRY(palloc(c, canon->frame_kind, gd->D));
     DC_CUDA(c, cudaMemcpyAsync(canon->frame_kind, gd->kinds, gd->D, cudaMemcpyDeviceToDevice, c->stream));
