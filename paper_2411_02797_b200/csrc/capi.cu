@@ -167,6 +167,39 @@ dc_status check_flags(Ctx* c) {
   return DC_OK;
 }
 
+void* arena_take(Ctx* c, size_t bytes) {
+  HostRegion hr(c, "alloc");
+  bytes = (bytes + 255) & ~(size_t)255;
+  while (c->arena_ci < c->arena.size()) {
+    auto& ch = c->arena[c->arena_ci];
+    if (c->arena_off + bytes <= ch.second) {
+      void* p = ch.first + c->arena_off;
+      c->arena_off += bytes;
+      return p;
+    }
+    ++c->arena_ci;
+    c->arena_off = 0;
+  }
+  size_t sz = (size_t)64 << 20;
+  if (!c->arena.empty() && 2 * c->arena.back().second > sz) sz = 2 * c->arena.back().second;
+  if (bytes > sz) sz = bytes;
+  void* p = nullptr;
+  if (cudaMallocFromPoolAsync(&p, sz, c->pool, c->stream) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  c->arena.push_back({(char*)p, sz});
+  c->arena_ci = c->arena.size() - 1;
+  c->arena_off = bytes;
+  return p;
+}
+
+static void arena_free(Ctx* c) {  // after a stream synchronisation
+  for (auto& ch : c->arena) cudaFreeAsync(ch.first, c->stream);
+  c->arena.clear();
+  c->arena_reset();
+}
+
 dc_status scan_state(Ctx* c, uint64_t n_tiles, uint64_t** flag, uint64_t** val, uint64_t* seq, Buf<uint64_t>& tmp) {
   constexpr uint64_t CAP = 1ull << 16;
   if (!c->scan_ctr) {  // first use: persistent, zeroed once (flags carry a call sequence number)
@@ -213,7 +246,12 @@ using namespace dc;
   do {                                                     \
     if (!(cond)) return fail(ctx, DC_ERR_ARG, __VA_ARGS__); \
   } while (0)
-#define ON_DEVICE(ctx) DC_CUDA(ctx, cudaSetDevice((ctx)->device))
+// every public call starts on the context's device with the scratch arena rewound
+#define ON_DEVICE(ctx)                                 \
+  do {                                                 \
+    DC_CUDA(ctx, cudaSetDevice((ctx)->device));        \
+    (ctx)->arena_reset();                              \
+  } while (0)
 
 extern "C" {
 
@@ -311,6 +349,8 @@ void dc_ctx_destroy(dc_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   cudaStreamSynchronize(ctx->stream);
+  arena_free(ctx);
+  cudaStreamSynchronize(ctx->stream);
   cudaFree(ctx->d_flags);
   cudaFree(ctx->d_diag);
   cudaFree(ctx->scan_flag);
@@ -351,6 +391,8 @@ dc_status dc_ctx_reserve(dc_ctx* ctx, uint64_t bytes) {
 dc_status dc_ctx_trim(dc_ctx* ctx, uint64_t keep_bytes) {
   CHECK_CTX(ctx);
   ON_DEVICE(ctx);
+  DC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  arena_free(ctx);
   DC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   DC_CUDA(ctx, cudaMemPoolTrimTo(ctx->pool, keep_bytes));
   return DC_OK;

@@ -40,6 +40,17 @@ struct Ctx {
   uint64_t* scan_val = nullptr;
   unsigned long long* scan_ctr = nullptr;
   uint64_t scan_cap = 0, scan_seq = 0, scan_tickets = 0;
+  // Scratch arena: every Buf of a public call is carved from these pool chunks by a bump pointer
+  // that rewinds at the next public call (all work is ordered on the one context stream, so the
+  // previous call's kernels are done with the memory before the next call's use it). One
+  // allocation per chunk instead of a cudaMallocAsync / cudaFreeAsync pair per scratch buffer
+  // (~150 host API calls per config-3 step). Chunks are kept until dc_ctx_trim / destroy.
+  std::vector<std::pair<char*, size_t>> arena;
+  size_t arena_ci = 0, arena_off = 0;
+  void arena_reset() {
+    arena_ci = 0;
+    arena_off = 0;
+  }
   uint64_t pc_bins_hint = 0;   // bins of the last PC-histogram call (+1/8): capacity guess of the next
   uint64_t pc_words_hint = 0;  // bitmap words of the last context reduce (+1/8): its scratch guess
   uint64_t pc_big_hint = 0;    // bins of big contexts (counted in scratch) of the last call (+1/8)
@@ -231,34 +242,50 @@ struct Buf {
   T* p = nullptr;
   size_t n = 0;
   cudaStream_t s = nullptr;
+  bool arena = false;  // carved from the context's scratch arena: nothing to free
   Buf() = default;
   Buf(const Buf&) = delete;
   Buf& operator=(const Buf&) = delete;
-  Buf(Buf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  Buf(Buf&& o) noexcept : p(o.p), n(o.n), s(o.s), arena(o.arena) { o.p = nullptr; o.n = 0; }
   Buf& operator=(Buf&& o) noexcept {
-    if (this != &o) { release(); p = o.p; n = o.n; s = o.s; o.p = nullptr; o.n = 0; }
+    if (this != &o) { release(); p = o.p; n = o.n; s = o.s; arena = o.arena; o.p = nullptr; o.n = 0; }
     return *this;
   }
   ~Buf() { release(); }
   void release() {
-    if (p) cudaFreeAsync(p, s);
+    if (p && !arena) cudaFreeAsync(p, s);
     p = nullptr;
     n = 0;
   }
-  T* release_ownership() {
-    T* q = p;
+  T* release_ownership() {  // only for pool buffers (alloc_pool): arena memory is recycled
+    T* q = arena ? nullptr : p;
     p = nullptr;
     n = 0;
     return q;
   }
 };
 
+void* arena_take(Ctx* c, size_t bytes);  // nullptr on OOM
+
+// scratch buffer (arena; lives until the next public call)
 template <class T>
 dc_status alloc(Ctx* c, Buf<T>& b, size_t n) {
+  b.release();
+  b.s = c->stream;
+  b.n = n;
+  b.arena = true;
+  b.p = (T*)arena_take(c, (n ? n : 1) * sizeof(T));
+  if (!b.p) return fail(c, DC_ERR_OOM, "device allocation of %zu bytes failed", (n ? n : 1) * sizeof(T));
+  return DC_OK;
+}
+// buffer from the pool (may be handed to a handle with release_ownership)
+template <class T>
+dc_status alloc_pool(Ctx* c, Buf<T>& b, size_t n) {
   HostRegion hr(c, "alloc");
   b.release();
   b.s = c->stream;
   b.n = n;
+  b.arena = false;
   if (n == 0) n = 1;
   cudaError_t e = cudaMallocFromPoolAsync((void**)&b.p, n * sizeof(T), c->pool, c->stream);
   if (e != cudaSuccess) {

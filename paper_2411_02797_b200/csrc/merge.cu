@@ -315,7 +315,8 @@ __global__ void k_kv_combine(const uint64_t* __restrict__ rec, uint32_t W, uint6
 
 // received node records (W words) and bin records (BIN_W) -> unique records; one host round trip
 static dc_status reduce_received(Ctx* c, const uint64_t* rn_p, uint64_t rn, const uint64_t* rb_p, uint64_t rb, const RecFmt& f,
-                                 Buf<uint64_t>& out_n, uint64_t* n_out, Buf<uint64_t>& out_b, uint64_t* b_out, uint32_t* d_collision) {
+                                 Buf<uint64_t>& out_n, uint64_t* n_out, Buf<uint64_t>& out_b, uint64_t* b_out, uint32_t* d_collision,
+                                 bool owned /* outputs handed to a partition handle: pool memory */) {
   struct Side {
     const uint64_t* rec;
     uint64_t n;
@@ -353,8 +354,13 @@ static dc_status reduce_received(Ctx* c, const uint64_t* rn_p, uint64_t rn, cons
   if (ht[2]) return fail(c, DC_ERR_STATE, "internal: merge hash table overflow");
   *n_out = ht[0];
   *b_out = ht[1];
-  DC_TRY(alloc(c, out_n, (uint64_t)ht[0] * f.W));
-  DC_TRY(alloc(c, out_b, (uint64_t)ht[1] * BIN_W));
+  if (owned) {
+    DC_TRY(alloc_pool(c, out_n, (uint64_t)ht[0] * f.W));
+    DC_TRY(alloc_pool(c, out_b, (uint64_t)ht[1] * BIN_W));
+  } else {
+    DC_TRY(alloc(c, out_n, (uint64_t)ht[0] * f.W));
+    DC_TRY(alloc(c, out_b, (uint64_t)ht[1] * BIN_W));
+  }
   for (int k = 0; k < 2; ++k) {
     Side& sd = side[k];
     if (!sd.n) continue;
@@ -832,6 +838,7 @@ dc_status dc_cct_merge_ranks(dc_ctx* ctx, dc_comm* cm, const dc_cct* local, cons
 #if DC_HAVE_NCCL
   Ctx* c = ctx;
   DC_CUDA(c, cudaSetDevice(c->device));
+  c->arena_reset();
   Region rg(c, "merge");
   const int P = cm->nranks;
   // 1. dictionaries: all-gather sizes together with each rank's record format (M, S, has_pc);
@@ -906,7 +913,7 @@ dc_status dc_cct_merge_ranks(dc_ctx* ctx, dc_comm* cm, const dc_cct* local, cons
   DC_TRY(alloc_zero(c, coll, 1));
   Buf<uint64_t> un, ub;
   uint64_t nun = 0, nub = 0;
-  DC_TRY(reduce_received(c, rnodes.p, rn, rbins.p, rb, f, un, &nun, ub, &nub, coll.p));
+  DC_TRY(reduce_received(c, rnodes.p, rn, rbins.p, rb, f, un, &nun, ub, &nub, coll.p, true));
   uint32_t hcoll = 0;
   DC_TRY(readback(c, coll.p, 4, &hcoll));
   if (hcoll) {
@@ -930,6 +937,7 @@ dc_status dc_cct_gather(dc_ctx* ctx, dc_comm* cm, const dc_cct* part, int root, 
 #if DC_HAVE_NCCL
   Ctx* c = ctx;
   DC_CUDA(c, cudaSetDevice(c->device));
+  c->arena_reset();
   const int P = cm->nranks;
   const RecFmt f = rec_fmt(part->M, part->S, part->part_has_pc);
   Buf<uint64_t> cnt;
@@ -977,6 +985,7 @@ dc_status dc_cct_merge_local(dc_ctx* ctx, uint32_t P, dc_cct* const* locals, dc_
   if (!ctx || !P || P > PART_MAXP || !locals || !dicts || !out_canonical || !out_global_dict) return DC_ERR_ARG;
   Ctx* c = ctx;
   DC_CUDA(c, cudaSetDevice(c->device));
+  c->arena_reset();
   for (uint32_t p = 0; p < P; ++p) {
     if (!locals[p] || !dicts[p] || locals[p]->state != 2) return fail(c, DC_ERR_STATE, "local tree %u is not rolled up", p);
     if (dicts[p]->D != locals[p]->n_frames) return fail(c, DC_ERR_ARG, "dictionary %u size != n_frames", p);
@@ -1042,7 +1051,7 @@ dc_status dc_cct_merge_local(dc_ctx* ctx, uint32_t P, dc_cct* const* locals, dc_
         DC_CUDA(c, cudaMemcpyAsync(rbins.p + roff[2 * p + 1] * BIN_W, slabs[p].bins.p + soff[p][2 * q + 1] * BIN_W,
                                    sc[p][2 * q + 1] * BIN_W * 8, cudaMemcpyDeviceToDevice, c->stream));
     }
-    DC_TRY(reduce_received(c, rnodes.p, rn, rbins.p, rb, f, parts_n[q], &pn[q], parts_b[q], &pb[q], coll.p));
+    DC_TRY(reduce_received(c, rnodes.p, rn, rbins.p, rb, f, parts_n[q], &pn[q], parts_b[q], &pb[q], coll.p, false));
   }
   uint32_t hcoll = 0;
   DC_TRY(readback(c, coll.p, 4, &hcoll));
