@@ -1257,7 +1257,17 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
   DC_TRY(alloc(c, hash, R));
   DC_TRY(alloc(c, slot_of_rec, R));
   DC_TRY(alloc(c, extra_rec, R));
-  DC_TRY(alloc_zero(c, cnt, 8));  // [0] distinct, [1] extra, [2] compact pos, [3] overflow, [4] empty paths
+  // path table sized for the distinct paths, not the records (retry if it passes half load)
+  uint64_t cap = 1024;
+  while (cap < 2 * (R < (1ull << 19) ? R : (1ull << 19))) cap <<= 1;
+  if (getenv("DC_TEST_PATH_CAP")) cap = 1024;  // test only: force the table-overflow retry
+  {  // every fill of the record pass in one launch
+    FillList fl;
+    DC_TRY(alloc_fill(c, fl, cnt, 8));  // [0] distinct, [1] extra, [2] compact pos, [3] overflow, [4] empty paths
+    DC_TRY(alloc_fill(c, fl, tab, cap, 0xFF));
+    DC_TRY(alloc_fill(c, fl, sumlen, 1));
+    DC_TRY(fill_flush(c, fl));
+  }
   const int tma_ok = ((uintptr_t)p->offsets % 16 == 0) && ((uintptr_t)p->frames % 16 == 0) && !getenv("DC_TEST_NO_TMA");
   // per device (context) attribute: set on every call
   DC_CUDA(c, cudaFuncSetAttribute(k_path_hash, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PathSmem)));
@@ -1271,10 +1281,6 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
                                                                      c->hash_mask, tma_ok);
     DC_LAUNCHED(c);
   }
-  // path table sized for the distinct paths, not the records (retry if it passes half load)
-  uint64_t cap = 1024;
-  while (cap < 2 * (R < (1ull << 19) ? R : (1ull << 19))) cap <<= 1;
-  if (getenv("DC_TEST_PATH_CAP")) cap = 1024;  // test only: force the table-overflow retry
   // One round trip for the whole record pass: the item arrays are sized by the records (every
   // item has its own representative record), compaction and item lengths run on the device
   // counters, and the counters, length sum, deepest path, flags and frame count come back
@@ -1287,16 +1293,19 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
   DC_TRY(alloc(c, item_len, ibound));
   DC_TRY(alloc(c, leaf_of_item, ibound));
   for (int attempt = 0;; ++attempt) {
-    DC_TRY(alloc(c, tab, cap));
-    DC_CUDA(c, cudaMemsetAsync(tab.p, 0xFF, cap * sizeof(PathSlot), c->stream));
-    DC_CUDA(c, cudaMemsetAsync(cnt.p, 0, 16, c->stream));  // [0..3]; [4] (empty paths) kept
+    if (attempt) {  // a larger table: fresh table, counters [0..3] ([4] empty paths kept), length sum
+      FillList fl;
+      DC_TRY(alloc_fill(c, fl, tab, cap, 0xFF));
+      DC_TRY(fill_add(c, fl, cnt.p, 16));
+      DC_TRY(fill_add(c, fl, sumlen.p, 8));
+      DC_TRY(fill_flush(c, fl));
+    }
     if (R) {
       dc_launch(k_path_group, grid_for(c, (R + 31) / 32 * 32, 256), 256, 0, c->stream, p->offsets, p->frames, hash.p, R, tab.p,
                                                                                 cap - 1, slot_of_rec.p, extra_rec.p, cnt.p);
       DC_LAUNCHED(c);
     }
     DC_TRY(alloc(c, pid_of_slot, cap));
-    DC_TRY(alloc_zero(c, sumlen, 1));
     dc_launch(k_path_compact, grid_for(c, cap, 256), 256, 0, c->stream, tab.p, cap, pid_of_slot.p, item_rec.p, item_len.p, cnt.p + 2);
     DC_LAUNCHED(c);
     dc_launch(k_items_finish, grid_for(c, ibound, 256), 256, 0, c->stream, item_rec.p, extra_rec.p, p->offsets, item_len.p, sumlen.p,
@@ -1394,8 +1403,8 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
   // node columns (exclusive/inclusive counts), metric columns come with attribute
   DC_TRY(palloc(c, t->xcnt, N));
   DC_TRY(palloc(c, t->icnt, N));
+  // icnt is written whole by dc_cct_rollup (every schedule) and unreadable before it
   DC_CUDA(c, cudaMemsetAsync(t->xcnt, 0, N * 8, c->stream));
-  DC_CUDA(c, cudaMemsetAsync(t->icnt, 0, N * 8, c->stream));
   // algorithmic bytes: offsets + frames of every record once, leaf, node table
   c->bytes_host += 8 * (R + 1) + 4 * F + 4 * R + 10 * N;
   c->host_levels += t->max_depth;

@@ -200,6 +200,41 @@ static void arena_free(Ctx* c) {  // after a stream synchronisation
   c->arena_reset();
 }
 
+__global__ void k_fill_multi(FillList f) { DC_PDL_ENTER();
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
+  for (int r = 0; r < f.n; ++r) {
+    const uint32_t v = f.byte[r] & 0xFFu;
+    const uint64_t pat = v * 0x0101010101010101ull;
+    const uint64_t words = f.bytes[r] / 8;
+    uint64_t* p8 = (uint64_t*)f.p[r];  // arena / pool memory: 256-byte aligned
+    if (((uintptr_t)p8 & 7) == 0) {
+      for (uint64_t i = tid; i < words; i += nt) p8[i] = pat;
+      for (uint64_t i = words * 8 + tid; i < f.bytes[r]; i += nt) ((uint8_t*)f.p[r])[i] = (uint8_t)v;
+    } else {
+      for (uint64_t i = tid; i < f.bytes[r]; i += nt) ((uint8_t*)f.p[r])[i] = (uint8_t)v;
+    }
+  }
+}
+
+dc_status fill_flush(Ctx* c, FillList& f) {
+  if (!f.n) return DC_OK;
+  uint64_t tot = 0;
+  for (int i = 0; i < f.n; ++i) tot += f.bytes[i];
+  dc_launch(k_fill_multi, grid_for(c, tot / 8 + 1, 256), 256, 0, c->stream, f);
+  DC_LAUNCHED(c);
+  f.n = 0;
+  return DC_OK;
+}
+
+dc_status fill_add(Ctx* c, FillList& f, void* p, uint64_t bytes, uint32_t v) {
+  if (f.n == FILL_MAX) DC_TRY(fill_flush(c, f));
+  f.p[f.n] = p;
+  f.bytes[f.n] = bytes;
+  f.byte[f.n] = v;
+  ++f.n;
+  return DC_OK;
+}
+
 dc_status scan_state(Ctx* c, uint64_t n_tiles, uint64_t** flag, uint64_t** val, uint64_t* seq, Buf<uint64_t>& tmp) {
   constexpr uint64_t CAP = 1ull << 16;
   if (!c->scan_ctr) {  // first use: persistent, zeroed once (flags carry a call sequence number)

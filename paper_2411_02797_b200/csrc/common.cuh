@@ -314,6 +314,26 @@ dc_status palloc(Ctx* c, T*& p, size_t n) {
   return DC_OK;
 }
 
+// Several memsets as ONE kernel launch: a memset between two kernels breaks the programmatic
+// dependent launch chain (the next kernel waits for a full launch latency), so the fills a
+// stage needs are collected and issued together (fill_flush) before the stage's first kernel.
+constexpr int FILL_MAX = 16;
+struct FillList {
+  void* p[FILL_MAX];
+  uint64_t bytes[FILL_MAX];
+  uint32_t byte[FILL_MAX];
+  int n = 0;
+};
+__global__ void k_fill_multi(FillList f);
+dc_status fill_flush(Ctx* c, FillList& f);
+// queue a fill of `bytes` bytes at p with the byte value v (flushes when the list is full)
+dc_status fill_add(Ctx* c, FillList& f, void* p, uint64_t bytes, uint32_t v = 0);
+template <class T>
+dc_status alloc_fill(Ctx* c, FillList& f, Buf<T>& b, size_t n, uint32_t v = 0) {
+  DC_TRY(alloc(c, b, n));
+  return fill_add(c, f, b.p, (n ? n : 1) * sizeof(T), v);
+}
+
 // synchronous small readback through the pinned buffer
 dc_status readback(Ctx* c, const void* dev, size_t bytes, void* host);
 dc_status check_flags(Ctx* c);  // synchronizes; DC_ERR_TRACE if a flag is set

@@ -233,9 +233,10 @@ dc_status intern_frames(Ctx* c, const dc_frame_key* keys, uint64_t n, uint32_t* 
   if (cap < 1024) cap = 1024;
   uint64_t D = 0;
   for (int attempt = 0; attempt < 2; ++attempt) {
-    DC_TRY(alloc(c, table, cap));
-    DC_CUDA(c, cudaMemsetAsync(table.p, 0xFF, cap * sizeof(ulonglong2), c->stream));
-    DC_TRY(alloc_zero(c, cnt, 4));  // [0] distinct, [1] overflow flag (u32), [2..3] maxima: one clear
+    FillList fl;
+    DC_TRY(alloc_fill(c, fl, table, cap, 0xFF));
+    DC_TRY(alloc_fill(c, fl, cnt, 5));  // [0] distinct, [1] overflow flag (u32), [2..3] maxima, [4] compact position
+    DC_TRY(fill_flush(c, fl));
     unsigned long long* mxp = cnt.p + 2;
     uint32_t* ovp = reinterpret_cast<uint32_t*>(cnt.p + 1);
     dc_launch(k_intern_insert, grid_for(c, (n + 3) / 4, 256), 256, 0, c->stream, keys, n, table.p, cap - 1, out_ids, cnt.p, ovp,
@@ -253,7 +254,6 @@ dc_status intern_frames(Ctx* c, const dc_frame_key* keys, uint64_t n, uint32_t* 
   d->D = D;
   Buf<uint64_t> ka, kb, ka2;
   Buf<uint32_t> slot_of, ord0, ord1, rank_of_slot;
-  Buf<unsigned int> pos;
   DC_TRY(alloc(c, ka, D));
   DC_TRY(alloc(c, kb, D));
   DC_TRY(alloc(c, ka2, D));
@@ -261,8 +261,8 @@ dc_status intern_frames(Ctx* c, const dc_frame_key* keys, uint64_t n, uint32_t* 
   DC_TRY(alloc(c, ord0, D));
   DC_TRY(alloc(c, ord1, D));
   DC_TRY(alloc(c, rank_of_slot, cap));
-  DC_TRY(alloc_zero(c, pos, 1));
-  dc_launch(k_intern_compact, grid_for(c, cap, 256), 256, 0, c->stream, table.p, cap, ka.p, kb.p, slot_of.p, pos.p);
+  unsigned int* pos = reinterpret_cast<unsigned int*>(cnt.p + 4);  // zeroed with the counters
+  dc_launch(k_intern_compact, grid_for(c, cap, 256), 256, 0, c->stream, table.p, cap, ka.p, kb.p, slot_of.p, pos);
   DC_LAUNCHED(c);
   if (D <= IR_MAX_D && !getenv("DC_TEST_INTERN_RADIX")) {
     DC_TRY(palloc(c, d->keys, D));

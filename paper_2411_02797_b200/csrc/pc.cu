@@ -14,8 +14,8 @@
 namespace dc {
 
 dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, const uint32_t* launch_leaf,
-                        uint64_t n_launch, const uint64_t* launch_off, uint32_t S, uint64_t* keys_out_dev,
-                        uint64_t* cnt_out_dev, uint64_t* n_bins_out, int* handled);
+                        uint64_t n_launch, const uint64_t* launch_off, uint32_t S, FillList& fl, uint64_t* n_bins_out,
+                        int* handled);
 
 __device__ __forceinline__ void block_diag_add(unsigned long long* d_diag, uint32_t bad_l, uint32_t bad_s, uint32_t zero) {
 #pragma unroll
@@ -274,7 +274,7 @@ static dc_status pc_merge_prev(Ctx* c, dc_cct* t, const PcPrev& o) {
 }
 
 static dc_status pc_attribute_once(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, const uint32_t* launch_leaf,
-                                   uint64_t n_launch, const uint64_t* launch_off, uint32_t S);
+                                   uint64_t n_launch, const uint64_t* launch_off, uint32_t S, FillList& fl);
 
 dc_status pc_attribute(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, const uint32_t* launch_leaf, uint64_t n_launch,
                        const uint64_t* launch_off, uint32_t S) {
@@ -285,11 +285,11 @@ dc_status pc_attribute(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, con
     DC_TRY(palloc(c, t->isamples, N));
     DC_TRY(palloc(c, t->xstall, (uint64_t)S * N));
     DC_TRY(palloc(c, t->istall, (uint64_t)S * N));
-    DC_CUDA(c, cudaMemsetAsync(t->xsamples, 0, N * 8, c->stream));
-    DC_CUDA(c, cudaMemsetAsync(t->isamples, 0, N * 8, c->stream));
-    DC_CUDA(c, cudaMemsetAsync(t->xstall, 0, (uint64_t)S * N * 8, c->stream));
-    DC_CUDA(c, cudaMemsetAsync(t->istall, 0, (uint64_t)S * N * 8, c->stream));
-    return pc_attribute_once(c, t, s, n, launch_leaf, n_launch, launch_off, S);
+    // (the inclusive columns are written whole by dc_cct_rollup and unreadable before it)
+    FillList fl;
+    DC_TRY(fill_add(c, fl, t->xsamples, N * 8));
+    DC_TRY(fill_add(c, fl, t->xstall, (uint64_t)S * N * 8));
+    return pc_attribute_once(c, t, s, n, launch_leaf, n_launch, launch_off, S, fl);
   }
   // a later call (e.g. the next chunk of samples, "flushes the metrics" per
   // buffer): this call's bins and exclusive columns are computed on their own, then merged
@@ -309,9 +309,10 @@ dc_status pc_attribute(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, con
   t->Npc = t->Nbins = 0;
   dc_status st = palloc(c, t->xsamples, N);
   if (st == DC_OK) st = palloc(c, t->xstall, (uint64_t)S * N);
-  if (st == DC_OK && cudaMemsetAsync(t->xsamples, 0, N * 8, c->stream) != cudaSuccess) st = fail(c, DC_ERR_CUDA, "memset");
-  if (st == DC_OK && cudaMemsetAsync(t->xstall, 0, (uint64_t)S * N * 8, c->stream) != cudaSuccess) st = fail(c, DC_ERR_CUDA, "memset");
-  if (st == DC_OK) st = pc_attribute_once(c, t, s, n, launch_leaf, n_launch, launch_off, S);
+  FillList fl;
+  if (st == DC_OK) st = fill_add(c, fl, t->xsamples, N * 8);
+  if (st == DC_OK) st = fill_add(c, fl, t->xstall, (uint64_t)S * N * 8);
+  if (st == DC_OK) st = pc_attribute_once(c, t, s, n, launch_leaf, n_launch, launch_off, S, fl);
   if (st == DC_OK) st = pc_merge_prev(c, t, o);
   if (st != DC_OK) {  // keep the earlier results: the handle stays valid, this call had no effect
     void* cur[] = {t->xsamples, t->xstall, t->pc_ctx, t->pc_off, t->bin_pcnode, t->bin_stall, t->bin_count};
@@ -334,7 +335,7 @@ dc_status pc_attribute(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, con
 }
 
 static dc_status pc_attribute_once(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, const uint32_t* launch_leaf,
-                                   uint64_t n_launch, const uint64_t* launch_off, uint32_t S) {
+                                   uint64_t n_launch, const uint64_t* launch_off, uint32_t S, FillList& fl) {
   const uint64_t N = t->N;
   // -------- histogram into (sort key, count) pairs
   Buf<uint64_t> keys, cnts, keys2;
@@ -345,7 +346,7 @@ static dc_status pc_attribute_once(Ctx* c, dc_cct* t, const dc_pc_sample* s, uin
   Buf<unsigned long long> tcnt;
   if (launch_off) {
     // context-owner schedule (pc_owner.cu); handled == 0 means "not applicable, use generic"
-    DC_TRY(pc_owner_hist(c, t, s, n, launch_leaf, n_launch, launch_off, S, nullptr, nullptr, &nb, &handled));
+    DC_TRY(pc_owner_hist(c, t, s, n, launch_leaf, n_launch, launch_off, S, fl, &nb, &handled));
     if (handled) {
       t->pc_done = true;
       t->state = 1;
@@ -353,6 +354,7 @@ static dc_status pc_attribute_once(Ctx* c, dc_cct* t, const dc_pc_sample* s, uin
       return DC_OK;
     }
   }
+  DC_TRY(fill_flush(c, fl));  // pending column fills (the owner schedule did not run / flush them)
   if (!handled) {
     uint64_t cap = np2(2 * (n < (1ull << 22) ? n : (1ull << 22)));
     if (cap < 1024) cap = 1024;

@@ -1746,11 +1746,13 @@ __global__ void k_own_gsize(const uint4* __restrict__ seg, const uint32_t* __res
 }
 
 dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, const uint32_t* launch_leaf,
-                        uint64_t n_launch, const uint64_t* launch_off, uint32_t S, uint64_t*, uint64_t*,
+                        uint64_t n_launch, const uint64_t* launch_off, uint32_t S, FillList& fl,
                         uint64_t* n_bins_out, int* handled) {
   *handled = 0;
   if (n == 0 || n_launch == 0 || n_launch >= (1ull << 31)) return DC_OK;
   const uint64_t N = t->N;
+  const uint32_t G = (uint32_t)c->num_sms;
+  const bool fused = !(getenv("DC_PC_CR") && atoi(getenv("DC_PC_CR")) == 2);
   Buf<uint32_t> bad;
   Buf<uint64_t> k0, k1;
   Buf<uint32_t> v0, v1;
@@ -1763,19 +1765,30 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
   const uint64_t row_cap = OW_ROWS * st_cap;
   if (st_cap >= (1ull << 32)) return DC_OK;  // stage claims count in 32 bits
   const uint64_t* lkey_out = nullptr;  // launches' contexts in ascending order (the stage plan's sort)
+  // every zeroed scratch of the schedule (and the caller's column fills) in one fill launch
+  const bool counting_sort = N < (1ull << 31) && !getenv("DC_TEST_OWN_RADIX");
+  Buf<uint32_t> hist;
+  Buf<unsigned long long> ctr, ldiag, ctl;
+  Buf<uint32_t> flags;
+  const uint64_t ctl_n = 6 + (fused ? 5 * (n_launch + 1) : 0);
+  DC_TRY(alloc_fill(c, fl, bad, 1));
+  if (counting_sort) DC_TRY(alloc_fill(c, fl, hist, N + 1));
+  DC_TRY(alloc_fill(c, fl, row_valid, row_cap));
+  DC_TRY(alloc_fill(c, fl, ctr, 2 + (uint64_t)G));  // entry / segment counters + per-CTA stage claims
+  DC_TRY(alloc_fill(c, fl, flags, 2));
+  DC_TRY(alloc_fill(c, fl, ldiag, DG_N));
+  DC_TRY(alloc_fill(c, fl, ctl, ctl_n));
+  DC_TRY(fill_flush(c, fl));
   {
     Region rp(c, "pc:prep");
-    DC_TRY(alloc_zero(c, bad, 1));
     // launches ordered by context
     DC_TRY(alloc(c, k0, n_launch));
     DC_TRY(alloc(c, k1, n_launch));
     DC_TRY(alloc(c, v0, n_launch));
     DC_TRY(alloc(c, v1, n_launch));
     bool in1 = false;
-    if (N < (1ull << 31) && !getenv("DC_TEST_OWN_RADIX")) {
+    if (counting_sort) {
       Region rs(c, "prep:sort");
-      Buf<uint32_t> hist;
-      DC_TRY(alloc_zero(c, hist, N + 1));
       dc_launch(k_own_hist, grid_for(c, n_launch, 256), 256, 0, c->stream, launch_leaf, launch_off, n_launch, n, N, hist.p, bad.p);
       DC_LAUNCHED(c);
       DC_TRY(excl_scan<uint32_t>(c, hist.p, hist.p, N + 1, nullptr));
@@ -1803,7 +1816,6 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
     DC_TRY(alloc(c, rowpos, n_launch));
     DC_TRY(alloc(c, tot, 1));
     DC_TRY(alloc(c, row_launch, row_cap));
-    DC_TRY(alloc_zero(c, row_valid, row_cap));
     DC_TRY(alloc(c, st_first, st_cap));
     DC_TRY(alloc(c, st_ctx, st_cap));
     dc_launch(k_plan_launch, grid_for(c, n_launch, 256), 256, 0, c->stream, launch_off, order, lkey, n_launch, lrow.p, lflag.p,
@@ -1822,16 +1834,15 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
     DC_LAUNCHED(c);
   }
   // partial outputs
-  const uint32_t G = (uint32_t)c->num_sms;
   // entry pool: table flushes + spill chunks after each CTA's first (at most n entries, plus a
   // partly used last chunk per CTA); the first chunks sit after the pool
   const uint64_t cap_entries = n + 1 + (uint64_t)G * OW_SPILL_CAP;
   const uint32_t cap_segs = (uint32_t)(n_launch + 4ull * G + n / 4096 + n / OW_SPILL_CAP + 1024);
-  Buf<uint32_t> pkey, flags, cm, wide;
+  Buf<uint32_t> pkey, cm, wide;
   Buf<uint64_t> cw;
   Buf<uint8_t> csh;
   uint64_t hw[2] = {0, 0};
-  Buf<unsigned long long> pcnt, ctr, ldiag;
+  Buf<unsigned long long> pcnt;
   Buf<uint4> seg;
   uint64_t hc[2];
   uint32_t hf[2];
@@ -1840,9 +1851,6 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
     DC_TRY(alloc(c, pkey, cap_entries + (uint64_t)G * OW_SPILL_CAP));
     DC_TRY(alloc(c, pcnt, cap_entries + (uint64_t)G * OW_SPILL_CAP));
     DC_TRY(alloc(c, seg, cap_segs));
-    DC_TRY(alloc_zero(c, ctr, 2 + (uint64_t)G));  // entry / segment counters + per-CTA stage claims
-    DC_TRY(alloc_zero(c, flags, 2));
-    DC_TRY(alloc_zero(c, ldiag, DG_N));
     OwnArgs a;
     a.smp = s;
     a.rowpos = rowpos.p;
@@ -1919,19 +1927,16 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
     if (!getenv("DC_TEST_PC_BR")) {
       // ------------------------------------------------ context reduce (k_ctx_hist [, scan, k_ctx_emit])
       Region rr(c, "pc:creduce");
-      const bool fused = !(getenv("DC_PC_CR") && atoi(getenv("DC_PC_CR")) == 2);
       uint64_t cap = c->pc_bins_hint > (1ull << 20) ? c->pc_bins_hint : (1ull << 20);
       if (cap > n) cap = n ? n : 1;
       if (getenv("DC_TEST_PC_CAP")) cap = 1;  // test only: force the reallocate-and-rerun path
       const uint64_t wcap = fused ? 0 : (c->pc_words_hint > (4ull << 20) ? c->pc_words_hint : (4ull << 20));
       const uint64_t bcap = fused ? std::max<uint64_t>(c->pc_big_hint, 1ull << 20)
                                   : (c->pc_bins_hint > (4ull << 20) ? c->pc_bins_hint : (4ull << 20));
-      Buf<unsigned long long> ctl, bscr;
+      Buf<unsigned long long> bscr;
       Buf<uint32_t> wscr;
       Buf<CtxRec> rec;
       Buf<uint64_t> gn, gbase;  // [gnb | gnp], [bin base | pc base] (n_launch + 1 each)
-      const uint64_t ctl_n = 6 + (fused ? 5 * (n_launch + 1) : 0);
-      DC_TRY(alloc_zero(c, ctl, ctl_n));
       DC_TRY(alloc(c, wscr, wcap));
       DC_TRY(alloc(c, bscr, bcap));
       if (!fused) {
