@@ -42,13 +42,14 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def traffic_for(kernel: str):
-    """dram bytes per launch of `kernel` from the committed ncu --set full summary, if any."""
+def traffic_for(kernel: str, cfg: int):
+    """dram bytes per launch of `kernel` on config `cfg` from the committed ncu --set full
+    summary (profiles/ncu_traffic.json, written by tools/ncu_summary.py), if captured."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
             t = json.load(f)
-        return t.get("k_" + kernel, t.get(kernel))
+        return t.get(f"cfg{cfg}:k_{kernel}")
     except Exception:
         return None
 
@@ -246,7 +247,7 @@ def main():
     ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--records", type=int, default=None, help="override record count (configs 2/4)")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-launches", type=int, default=1000, help="bounded oracle sample (launch records)")
+    ap.add_argument("--cpu-launches", type=int, default=4000, help="bounded oracle sample (launch records)")
     ap.add_argument("--ref-launches", type=int, default=200)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -355,17 +356,25 @@ def main():
         ms = float(t.item())
     value = recs * world / (ms / 1000.0)
 
-    # ---------------- roofline of the dominant kernel
+    # ---------------- roofline of the dominant kernel (SURVEY §8(d) algorithmic bytes per launch)
     peak, peak_src = peaks()
-    kname = next((k for k in ["k:pc_owner", "k:pc_table"] if k in timers), None)
+    R_, F_ = tr.n_records, F
+    alg = {  # kernel timer -> algorithmic bytes of one launch
+        "k:pc_owner": alg_bytes_pc_hist(n_smp, n_bins) if args.config == 3 else 0,  # 16 B/sample + 16 B/bin
+        "k:intern_insert": 20 * F_,                          # 16-B raw key read + 4-B id written per key
+        "k:path_hash": 8 * (R_ + 1) + 4 * F_ + 8 * R_,       # offsets + frames read, 8-B path hash written
+        "k:path_group": 8 * (R_ + 1) + 4 * F_ + 12 * R_,     # offsets + frames (exact verify) + hash read, slot written
+    }
+    cand = [k for k in alg if k in timers and alg[k] and (args.config != 3 or k == "k:pc_owner")]
+    kname = max(cand, key=lambda k: timers[k][1] / timers[k][0]) if cand else None
     roof = None
-    if kname and args.config == 3:
+    if kname:
         cnt, tot_ms = timers[kname]
         kms = tot_ms / cnt
-        ab = alg_bytes_pc_hist(int(tr.samples.shape[0]), n_bins)
+        ab = alg[kname]
         ach = ab / (kms / 1000.0) / 1e9
         roof = {"bound": "hbm", "kernel": kname[2:], "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(ach / peak, 4), "traffic": traffic_for(kname[2:]), "alg_bytes_per_launch": ab,
+                "frac": round(ach / peak, 4), "traffic": traffic_for(kname[2:], args.config), "alg_bytes_per_launch": ab,
                 "kernel_ms": round(kms, 4), "peak_source": peak_src,
                 "share_of_step": round(kms / ms, 4)}
     stages = {k: round(v[1] / v[0], 4) for k, v in timers.items()}

@@ -129,7 +129,7 @@ __device__ __forceinline__ void pt_hash_chunks(PathWarp& W, const uint32_t* __re
 __global__ void __launch_bounds__(PT_THREADS) k_path_hash(const uint64_t* __restrict__ off, const uint32_t* __restrict__ frames,
                                                           uint64_t R, uint32_t n_frames, uint64_t* __restrict__ hash,
                                                           unsigned int* __restrict__ d_cnt, uint32_t* d_flags,
-                                                          unsigned long long* d_diag, uint64_t hash_mask, int tma_ok) { DC_PDL_ENTER();
+                                                          unsigned long long* d_diag, uint64_t hash_mask, int tma_ok) { DC_PDL_WAIT();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PathSmem& sm = *reinterpret_cast<PathSmem*>(smem_raw);
   const uint32_t tid = threadIdx.x, lane = lane_id(), w = tid >> 5;
@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(PT_THREADS) k_path_hash(const uint64_t* __rest
 __global__ void __launch_bounds__(256) k_path_group(const uint64_t* __restrict__ off, const uint32_t* __restrict__ frames,
                                                     const uint64_t* __restrict__ hash, uint64_t R, PathSlot* __restrict__ tab,
                                                     uint64_t mask, uint32_t* __restrict__ slot_of_rec,
-                                                    uint32_t* __restrict__ extra_rec, unsigned int* __restrict__ d_cnt) { DC_PDL_ENTER();
+                                                    uint32_t* __restrict__ extra_rec, unsigned int* __restrict__ d_cnt) { DC_PDL_WAIT();
   const uint32_t lane = lane_id();
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -411,7 +411,7 @@ __global__ void k_slot_leaf(const PathSlot* __restrict__ tab, uint64_t cap, cons
 }
 
 __global__ void k_rec_leaf(const uint32_t* __restrict__ slot_of_rec, const uint32_t* __restrict__ leaf_of_slot, uint64_t cap,
-                           uint32_t P0, const uint32_t* __restrict__ leaf_of_item, uint64_t R, uint32_t* __restrict__ leaf) { DC_PDL_ENTER();
+                           uint32_t P0, const uint32_t* __restrict__ leaf_of_item, uint64_t R, uint32_t* __restrict__ leaf) { DC_PDL_WAIT();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < R; r += 4 * stride) {
     uint32_t s[4];
@@ -1276,6 +1276,7 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
     DC_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_path_hash, PT_THREADS, sizeof(PathSmem)));
     const uint64_t n_tiles = (R + PT_T - 1) / PT_T;
     const int hgrid = (int)std::min<uint64_t>(n_tiles, (uint64_t)c->num_sms * std::max(per_sm, 1));
+    Region rk(c, "k:path_hash");
     dc_launch(k_path_hash, hgrid, PT_THREADS, sizeof(PathSmem), c->stream, p->offsets, p->frames, R, n_frames, hash.p, cnt.p,
                                                                      c->d_flags, (unsigned long long*)c->d_diag,
                                                                      c->hash_mask, tma_ok);
@@ -1301,6 +1302,7 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
       DC_TRY(fill_flush(c, fl));
     }
     if (R) {
+      Region rk(c, "k:path_group");
       dc_launch(k_path_group, grid_for(c, (R + 31) / 32 * 32, 256), 256, 0, c->stream, p->offsets, p->frames, hash.p, R, tab.p,
                                                                                 cap - 1, slot_of_rec.p, extra_rec.p, cnt.p);
       DC_LAUNCHED(c);

@@ -20,7 +20,7 @@ namespace dc {
 // into the node columns. K = 1 updates the node columns directly.
 __global__ void k_attribute(const uint32_t* __restrict__ leaf, uint64_t R, const uint64_t* __restrict__ X, uint32_t M,
                             uint64_t ld, uint64_t N, unsigned long long* __restrict__ xcnt0, unsigned long long* __restrict__ mcols0,
-                            uint32_t* d_flags, uint32_t K, uint64_t cs, uint64_t ms) { DC_PDL_ENTER();
+                            uint32_t* d_flags, uint32_t K, uint64_t cs, uint64_t ms) { DC_PDL_WAIT();
   unsigned long long* xcnt = xcnt0 + (uint64_t)(blockIdx.x % K) * cs;
   unsigned long long* mcols = mcols0 + (uint64_t)(blockIdx.x % K) * ms;
   for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < R; r += (uint64_t)gridDim.x * blockDim.x) {

@@ -27,7 +27,7 @@ constexpr uint32_t IC_EMPTY = 0xFFFFFFFFu, IC_BUSY = 0xFFFFFFFEu;
 __global__ void __launch_bounds__(256) k_intern_insert(const dc_frame_key* __restrict__ keys, uint64_t n, ulonglong2* table,
                                                        uint64_t mask, uint32_t* __restrict__ out_slot,
                                                        unsigned long long* d_count, uint32_t* d_overflow, uint32_t* d_flags,
-                                                       unsigned long long* d_max) { DC_PDL_ENTER();
+                                                       unsigned long long* d_max) { DC_PDL_WAIT();
   __shared__ unsigned long long c_lo[IC_SLOTS], c_hi[IC_SLOTS];
   __shared__ uint32_t c_slot[IC_SLOTS];
   for (int i = threadIdx.x; i < IC_SLOTS; i += blockDim.x) c_slot[i] = IC_EMPTY;
@@ -239,9 +239,12 @@ dc_status intern_frames(Ctx* c, const dc_frame_key* keys, uint64_t n, uint32_t* 
     DC_TRY(fill_flush(c, fl));
     unsigned long long* mxp = cnt.p + 2;
     uint32_t* ovp = reinterpret_cast<uint32_t*>(cnt.p + 1);
-    dc_launch(k_intern_insert, grid_for(c, (n + 3) / 4, 256), 256, 0, c->stream, keys, n, table.p, cap - 1, out_ids, cnt.p, ovp,
-                                                                 c->d_flags, mxp);
-    DC_LAUNCHED(c);
+    {
+      Region rk(c, "k:intern_insert");
+      dc_launch(k_intern_insert, grid_for(c, (n + 3) / 4, 256), 256, 0, c->stream, keys, n, table.p, cap - 1, out_ids, cnt.p, ovp,
+                                                                   c->d_flags, mxp);
+      DC_LAUNCHED(c);
+    }
     uint64_t h[2] = {0, 0};
     DC_TRY(readback_multi(c, {{cnt.p, 8, &h[0]}, {ovp, 4, &h[1]}, {mxp, 16, mxh}}));
     D = h[0];

@@ -425,7 +425,7 @@ __device__ __noinline__ void own_cold(const uint4 q, uint32_t seg_launch, const 
 }
 
 template <int MODE>  // 0 = the product; 1, 2, 3, 9 = measurement variants (DC_OWN_MODE)
-__global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) { DC_PDL_ENTER();
+__global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) { DC_PDL_WAIT();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   OwnSmem& sm = *reinterpret_cast<OwnSmem*>(smem_raw);
   const uint32_t tid = threadIdx.x;

@@ -3,10 +3,10 @@
   python tools/ncu_summary.py launches <launches.csv> <out.md>
       per-kernel launch count, total and mean duration, share of the captured time, from an
       `ncu --metrics gpu__time_duration.sum --csv --log-file` launch list (cold-cache, serialised).
-  python tools/ncu_summary.py full <report.ncu-rep> <out.md> [traffic.json]
+  python tools/ncu_summary.py full <report.ncu-rep> <out.md> [traffic.json [config]]
       key `--set full` metrics per captured kernel (duration, DRAM bytes and throughput, issue
       activity, occupancy, top stall reasons) and, optionally, dram bytes per launch merged into
-      traffic.json (read by bench.py for roofline.traffic).
+      traffic.json under "cfg<config>:<kernel>" (read by bench.py for roofline.traffic).
 """
 import collections
 import csv
@@ -76,7 +76,7 @@ def to_bytes(v: float, unit: str) -> float:
     return v * mult.get(unit, 1)
 
 
-def full(rep: str, out_md: str, traffic_json: str | None):
+def full(rep: str, out_md: str, traffic_json: str | None, config: str = "3"):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units, data = rows[0], rows[1], rows[2:]
@@ -112,7 +112,7 @@ def full(rep: str, out_md: str, traffic_json: str | None):
         try:
             rd = sum(to_bytes(float(r[ix["dram__bytes_read.sum"]].replace(",", "")), units[ix["dram__bytes_read.sum"]]) for r in rs) / len(rs)
             wr = sum(to_bytes(float(r[ix["dram__bytes_write.sum"]].replace(",", "")), units[ix["dram__bytes_write.sum"]]) for r in rs) / len(rs)
-            traffic[base(k)] = int(rd + wr)
+            traffic[f"cfg{config}:{base(k)}"] = int(rd + wr)
             lines += ["", f"DRAM traffic per launch (read + write): {int(rd + wr):,} B"]
         except (KeyError, ValueError):
             pass
@@ -128,6 +128,6 @@ if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2], sys.argv[3])
     elif sys.argv[1] == "full":
-        full(sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else None)
+        full(sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else None, sys.argv[5] if len(sys.argv) > 5 else "3")
     else:
         raise SystemExit(__doc__)
