@@ -402,9 +402,16 @@ __global__ void __launch_bounds__(RC_THREADS, 1) k_roll_cols(const uint32_t* __r
                                                             uint64_t* __restrict__ icnt, uint64_t* __restrict__ mcols,
                                                             uint64_t* __restrict__ limbs, const uint64_t* __restrict__ xsamples,
                                                             uint64_t* __restrict__ isamples, const uint64_t* __restrict__ xstall,
-                                                            uint64_t* __restrict__ istall) { DC_PDL_ENTER();
+                                                            uint64_t* __restrict__ istall, int use_spar) { DC_PDL_ENTER();
   extern __shared__ unsigned long long racc[];
+  // after the column: the level offsets, and the parents as u16 when they fit (use_spar): the
+  // level loop then touches no global memory (one barrier per level is its only latency)
+  uint32_t* slev = reinterpret_cast<uint32_t*>(racc + N);
+  uint16_t* spar = reinterpret_cast<uint16_t*>(slev + ((maxd + 2 + 3) & ~3u));
   const uint32_t col = blockIdx.x, tid = threadIdx.x;
+  for (uint32_t i = tid; i < maxd + 2; i += RC_THREADS) slev[i] = level_off[i];
+  if (use_spar)
+    for (uint32_t i = tid; i < N; i += RC_THREADS) spar[i] = (uint16_t)parent[i];
   const uint64_t* src;
   uint64_t* dst;
   bool is_min = false;
@@ -442,12 +449,13 @@ __global__ void __launch_bounds__(RC_THREADS, 1) k_roll_cols(const uint32_t* __r
   __syncthreads();
   const uint32_t lane = tid & 31;
   for (uint32_t d = maxd; d >= 1; --d) {
-    const uint32_t lo = level_off[d], hi = level_off[d + 1];
+    const uint32_t lo = slev[d], hi = slev[d + 1];
     for (uint32_t b0 = lo; b0 < hi; b0 += RC_THREADS) {  // block-uniform trip count (warp shuffles below)
+      if (b0 + (tid & ~31u) >= hi) continue;             // warp-uniform: this warp has no node of the level
       const uint32_t n = b0 + tid;
       const bool act = n < hi;
       unsigned long long v = act ? racc[n] : (is_min ? ~0ull : 0ull);
-      const uint32_t p = act ? __ldg(parent + n) : 0xFFFFFFFFu;
+      const uint32_t p = act ? (use_spar ? (uint32_t)spar[n] : __ldg(parent + n)) : 0xFFFFFFFFu;
       // siblings are contiguous: segmented reduction over the lanes with the same parent, then
       // one shared-memory atomic per segment (its last lane)
 #pragma unroll
@@ -487,15 +495,17 @@ dc_status rollup(Ctx* c, dc_cct* t) {
   const uint64_t N = t->N;
   const uint32_t M = t->M, S = t->S;
   cudaStream_t s = c->stream;
-  if (N > 1 && N <= RC_MAX_N && !getenv("DC_TEST_ROLLUP_PUSH") && !getenv("DC_TEST_ROLLUP_LEVELS") &&
+  if (N > 1 && N <= RC_MAX_N && N * 8 + 4ull * (t->max_depth + 6) <= c->smem_optin && !getenv("DC_TEST_ROLLUP_PUSH") && !getenv("DC_TEST_ROLLUP_LEVELS") &&
       !getenv("DC_TEST_ROLLUP_PUSH_RETURNED")) {
     Buf<uint64_t> limbs;
     if (M) DC_TRY(alloc(c, limbs, 4ull * M * N));
     const uint32_t cols = 1 + 6 * M + (t->xsamples ? 1 + S : 0);
-    const size_t smem = N * 8;
+    const size_t base = N * 8 + 4ull * ((t->max_depth + 2 + 3) & ~3u);
+    const int use_spar = N <= 65535 && base + 2 * N <= c->smem_optin;
+    const size_t smem = base + (use_spar ? 2 * N : 0);
     DC_CUDA(c, cudaFuncSetAttribute(k_roll_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     dc_launch(k_roll_cols, cols, RC_THREADS, smem, s, t->parent, t->level_off, t->max_depth, (uint32_t)N, M, t->xcnt, t->icnt,
-              t->mcols, limbs.p, t->xsamples, t->isamples, t->xstall, t->istall);
+              t->mcols, limbs.p, t->xsamples, t->isamples, t->xstall, t->istall, use_spar);
     DC_LAUNCHED(c);
     if (M) {
       dc_launch(k_roll_fold, grid_for(c, (uint64_t)M * N, 256), 256, 0, s, N, M, limbs.p, t->mcols);

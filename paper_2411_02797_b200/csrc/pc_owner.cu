@@ -984,30 +984,33 @@ __global__ void __launch_bounds__(32 * BR_WARPS) k_br_count(
 }
 
 // ---------------------------------------------------------------- context reduce (default)
-// Two launches and a scan, no sort, no waiting between contexts:
-//  k_ctx_hist: persistent CTAs take the context groups by ticket (any order). For its context a
-//    CTA gathers the segments' partial entries, builds the (pc', stall) presence bitmap in
-//    shared memory (pc' = pc_off >> the common trailing zero bits of the context's PCs; one
-//    32-bit word per PC), ranks the keys by the word popcount prefix (bin index within the
-//    context) and sums the counts per bin in shared memory (exact u64 as 32-bit halves), adds the
-//    context's per-stall totals into its sample columns, and stores bitmap + bin counts in a
-//    scratch slab (bump-allocated) with the context's (bins, PC nodes);
-//  an exclusive scan over the groups' (bins, PC nodes) gives every context its global bases
-//    (contexts in ascending id = canonical order);
-//  k_ctx_emit: one CTA per group writes its PC nodes and bins in canonical (pc, stall) order and
-//    copies the bin counts, coalesced.
-// A context whose PC range or segment count does not fit shared memory raises CR_WIDE (the host
-// takes the k_br_* path); outputs past the allocated capacity are not written (CR_OVER: the host
-// reallocates and reruns k_ctx_emit only).
+// Three small launches and a scan, no sort, no waiting between contexts:
+//  k_ctx_order: one CTA sums each context group's partial entries (segment headers) and orders
+//    the groups largest first (log2 buckets: longest-processing-time-first over the CTAs);
+//  k_ctx_hist: persistent CTAs take the groups in that order by ticket. For its context a CTA
+//    gathers the segments' partial entries, builds the (pc', stall) presence bitmap in shared
+//    memory (pc' = pc_off >> the common trailing zero bits of the context's PCs; one 32-bit word
+//    per PC), ranks the keys by the word popcount prefix (bin index within the context) and sums
+//    the counts per bin in shared memory (exact u64 as 32-bit halves), adds the context's
+//    per-stall totals into its sample columns, and writes per word (bits, bin prefix, PC-node
+//    prefix, group) and the per-bin counts into bump-allocated scratch, with the context's
+//    (bins, PC nodes);
+//  an exclusive scan over the groups (ascending context id = canonical order) gives every
+//    context its global bin / PC-node bases;
+//  k_ctx_emit: one thread per scratch word (whole grid, coalesced) writes the word's PC node,
+//    its bins and their counts at their global positions.
+// A context whose PC range or segment count does not fit shared memory (or scratch that is too
+// small) raises CR_WIDE: the host takes the k_br_* path; outputs past the allocated capacity
+// are not written (CR_OVER: the host reallocates and reruns k_ctx_emit only).
 constexpr int CR_THREADS = 1024;
 constexpr uint32_t CR_WORDS = 8192;    // PCs per context (pc' range)
 constexpr uint32_t CR_BINS = 12288;    // bins per context counted in shared memory
 constexpr uint32_t CR_SEGS = 4096;     // segments per context
+constexpr uint32_t CR_ORDER_MAX = 8192;   // groups ordered by size (more: ascending order; static smem)
 enum { CR_WIDE = 1, CR_OVER = 2 };
 struct CtxRedSmem {
   uint32_t bm[CR_WORDS];
   uint32_t bpre[CR_WORDS];   // bins before word w (within the context)
-  uint32_t ppre[CR_WORDS];   // PC nodes before word w
   // u64 sums as 32-bit halves with an exact carry (native 32-bit shared atomics; a 64-bit
   // shared atomic add is a CAS loop)
   uint32_t cnt_lo[CR_BINS], cnt_hi[CR_BINS];
@@ -1016,10 +1019,12 @@ struct CtxRedSmem {
   uint32_t nseg, g, maxk, orp;
   unsigned long long ow, ob;
 };
-// per group record written by k_ctx_hist: ctx, W, sh | np << 8?, ...
-struct __align__(16) CtxRec {
-  unsigned long long ow, ob;  // scratch offsets: bitmap words (u32 units), bin counts (u64 units)
-  uint32_t ctx, W, sh, nb;
+struct __align__(16) CtxWord {  // scratch per bitmap word
+  uint32_t bits, bpre, ppre, g;
+};
+struct __align__(16) CtxRec {  // scratch per group
+  unsigned long long ow, ob;   // first scratch word, first scratch count
+  uint32_t ctx, sh;
 };
 
 // Walks the context's entries: chunks of 32 x CR_U entries, chunk k of the concatenated
@@ -1053,41 +1058,64 @@ __device__ __forceinline__ void cr_for_entries(const CtxRedSmem& sm, const uint4
   }
 }
 
-__device__ __forceinline__ uint64_t cr_ld_acq(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void cr_st_rel(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// one CTA: group g's partial-entry total, groups ordered by descending log2 size (LPT)
+__global__ void __launch_bounds__(1024) k_ctx_order(const uint4* __restrict__ seg, const unsigned int* __restrict__ d_nsegs,
+                                                    uint32_t cap_segs, const uint64_t* __restrict__ lkey,
+                                                    const uint32_t* __restrict__ gfirst, const uint32_t* __restrict__ d_ng,
+                                                    uint32_t* __restrict__ order) { DC_PDL_ENTER();
+  __shared__ uint32_t size[CR_ORDER_MAX];
+  __shared__ uint32_t bucket[33];
+  const uint32_t NG = *d_ng, n_segs = min(*d_nsegs, cap_segs), tid = threadIdx.x;
+  if (NG > CR_ORDER_MAX) {  // plain ascending order
+    for (uint32_t g = tid; g < NG; g += blockDim.x) order[g] = g;
+    return;
+  }
+  for (uint32_t g = tid; g < NG; g += blockDim.x) size[g] = 0;
+  if (tid < 33) bucket[tid] = 0;
+  __syncthreads();
+  for (uint32_t i = tid; i < n_segs; i += blockDim.x) {
+    const uint4 sg = seg[i];
+    if (!sg.y) continue;
+    uint32_t lo = 0, hi = NG;  // group of context sg.x: groups are in ascending context order
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (lkey[gfirst[mid]] < sg.x) lo = mid + 1;
+      else hi = mid;
+    }
+    if (lo < NG && lkey[gfirst[lo]] == sg.x) atomicAdd(&size[lo], sg.y);
+  }
+  __syncthreads();
+  for (uint32_t g = tid; g < NG; g += blockDim.x) atomicAdd(&bucket[size[g] ? 32 - __clz(size[g]) : 0], 1u);
+  __syncthreads();
+  if (tid == 0) {  // descending buckets: start of bucket b = groups in buckets > b
+    uint32_t run = 0;
+    for (int b = 32; b >= 0; --b) {
+      const uint32_t c = bucket[b];
+      bucket[b] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  for (uint32_t g = tid; g < NG; g += blockDim.x) order[atomicAdd(&bucket[size[g] ? 32 - __clz(size[g]) : 0], 1u)] = g;
 }
 
-// FUSED (default): one launch. After its counts are summed the CTA looks back over the
-// preceding contexts' published (bins, PC nodes) — each context publishes right after its
-// bitmap, so by then the look-back rarely waits — and writes its PC nodes, bins and counts at
-// their global positions directly. !FUSED: bitmap + counts go to the scratch slab and
-// k_ctx_emit writes them after a scan over the groups (kept for A/B measurement, DC_PC_CR=2).
-template <bool FUSED>
 __global__ void __launch_bounds__(CR_THREADS, 1) k_ctx_hist(
     const uint4* __restrict__ seg, const unsigned int* __restrict__ d_nsegs, uint32_t cap_segs, const uint32_t* __restrict__ pkey,
     const unsigned long long* __restrict__ pcnt, const uint64_t* __restrict__ lkey, const uint32_t* __restrict__ gfirst,
-    const uint32_t* __restrict__ d_ng, uint64_t N, uint32_t S, const uint32_t* __restrict__ g_flags,
-    unsigned long long* __restrict__ ctl,  // [0] ticket, [1] status, [2] scratch words used, [3] scratch bins used,
-                                           // [4] total bins, [5] total PC nodes, then 5 per group (FUSED look-back):
-                                           // flag, aggregate (bins, pcs), inclusive (bins, pcs)
-    uint32_t* __restrict__ wscr, uint64_t wcap, unsigned long long* __restrict__ bscr, uint64_t bcap, CtxRec* __restrict__ rec,
+    const uint32_t* __restrict__ d_ng, const uint32_t* __restrict__ order, uint64_t N, uint32_t S, const uint32_t* __restrict__ g_flags,
+    unsigned long long* __restrict__ ctl,  // [0] ticket, [1] status, [2] scratch words used, [3] scratch bins used
+    CtxWord* __restrict__ wscr, uint64_t wcap, unsigned long long* __restrict__ bscr, uint64_t bcap, CtxRec* __restrict__ rec,
     uint64_t* __restrict__ gnb, uint64_t* __restrict__ gnp, unsigned long long* __restrict__ xsamples,
-    unsigned long long* __restrict__ xstall, uint64_t cap, uint32_t* __restrict__ pc_ctx, uint32_t* __restrict__ pc_off,
-    uint32_t* __restrict__ bin_pcnode, uint16_t* __restrict__ bin_stall, uint64_t* __restrict__ bin_count) { DC_PDL_ENTER();
+    unsigned long long* __restrict__ xstall) { DC_PDL_WAIT();
   extern __shared__ __align__(16) unsigned char cr_raw[];
   CtxRedSmem& sm = *reinterpret_cast<CtxRedSmem*>(cr_raw);
   if (*g_flags) return;  // the owner pass fell back: the host reruns the generic schedule
   const uint32_t tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
   const uint32_t NG = *d_ng, n_segs = min(*d_nsegs, cap_segs);
-  unsigned long long* gst = ctl + 6;
   for (;;) {
     if (tid == 0) {
-      sm.g = (uint32_t)atomicAdd(ctl, 1ull);
+      const uint32_t t = (uint32_t)atomicAdd(ctl, 1ull);
+      sm.g = t < NG ? order[t] : 0xFFFFFFFFu;
       sm.nseg = 0;
       sm.maxk = 0;
       sm.orp = 0;
@@ -1096,7 +1124,7 @@ __global__ void __launch_bounds__(CR_THREADS, 1) k_ctx_hist(
     }
     __syncthreads();
     const uint32_t g = sm.g;
-    if (g >= NG) break;
+    if (g == 0xFFFFFFFFu) break;
     const uint64_t ctx = lkey[gfirst[g]];
     bool ok = ctx < N;  // launches with an invalid leaf: no bins (flagged by the plan)
     uint32_t W = 0, nb = 0, np = 0, ns = 0;
@@ -1161,41 +1189,30 @@ __global__ void __launch_bounds__(CR_THREADS, 1) k_ctx_hist(
       }
       uint32_t bex = block_excl_scan<uint32_t, CR_THREADS>(bsum, &nb);
       uint32_t pex = block_excl_scan<uint32_t, CR_THREADS>(psum, &np);
-#pragma unroll
-      for (uint32_t i = 0; i < WP; ++i) {
-        const uint32_t w = tid * WP + i;
-        if (w < W) {
-          const uint32_t b = sm.bm[w];
-          sm.bpre[w] = bex;
-          sm.ppre[w] = pex;
-          bex += __popc(b);
-          pex += b != 0u;
-        }
-      }
-    }
-    const bool in_smem = nb <= CR_BINS;
-    if (tid == 0) {
-      if (FUSED) {  // publish this context's (bins, PC nodes) for the successors' look-back
-        unsigned long long* me = gst + 5ull * g;
-        if (g == 0) {
-          me[3] = nb;
-          me[4] = np;
-          cr_st_rel(me, 2ull);
-        } else {
-          me[1] = nb;
-          me[2] = np;
-          cr_st_rel(me, 1ull);
-        }
-      }
-      if (ok && (!FUSED || !in_smem)) {  // scratch: bitmap + counts (!FUSED), counts of a big context (FUSED)
-        sm.ow = FUSED ? 0 : atomicAdd(ctl + 2, (unsigned long long)W);
+      if (tid == 0) {
+        sm.ow = atomicAdd(ctl + 2, (unsigned long long)W);
         sm.ob = atomicAdd(ctl + 3, (unsigned long long)nb);
         if (sm.ow + W > wcap || sm.ob + nb > bcap) {  // scratch too small: the host takes the k_br_* path
           atomicOr(ctl + 1, (unsigned long long)CR_WIDE);
           sm.ow = ~0ull;
         }
       }
+      __syncthreads();
+      const unsigned long long ow = sm.ow;
+#pragma unroll
+      for (uint32_t i = 0; i < WP; ++i) {
+        const uint32_t w = tid * WP + i;
+        if (w < W) {
+          const uint32_t b = sm.bm[w];
+          sm.bpre[w] = bex;
+          if (ow != ~0ull) wscr[ow + w] = CtxWord{b, bex, pex, g};
+          bex += __popc(b);
+          pex += b != 0u;
+        }
+      }
+      if (ow == ~0ull) ok = false;
     }
+    const bool in_smem = nb <= CR_BINS;
     for (uint32_t i = tid; i < 32 * 32; i += CR_THREADS) {
       (&sm.wst_lo[0][0])[i] = 0;
       (&sm.wst_hi[0][0])[i] = 0;
@@ -1205,20 +1222,11 @@ __global__ void __launch_bounds__(CR_THREADS, 1) k_ctx_hist(
         sm.cnt_lo[i] = 0;
         sm.cnt_hi[i] = 0;
       }
+    const unsigned long long ob = sm.ob;
+    if (ok && !in_smem)
+      for (uint32_t i = tid; i < nb; i += CR_THREADS) bscr[ob + i] = 0;
     __syncthreads();
-    const unsigned long long ow = sm.ow, ob = sm.ob;
-    if (ow == ~0ull) ok = false;
-    if (!FUSED && !ok && tid == 0) {
-      rec[g] = CtxRec{0, 0, (uint32_t)ctx, 0, 0, 0};
-      gnb[g] = 0;
-      gnp[g] = 0;
-    }
     if (ok) {
-      if (!in_smem)
-        for (uint32_t i = tid; i < nb; i += CR_THREADS) bscr[ob + i] = 0;
-      if (!FUSED)
-        for (uint32_t w = tid; w < W; w += CR_THREADS) wscr[ow + w] = sm.bm[w];
-      if (!in_smem) __syncthreads();
       // pass C: counts into their bins; per-stall totals
       cr_for_entries<true>(sm, seg, pkey, pcnt, ns, [&](uint32_t kk, unsigned long long cv) {
         const uint32_t w = (kk >> 5) >> sh, b = kk & 31u;
@@ -1236,7 +1244,7 @@ __global__ void __launch_bounds__(CR_THREADS, 1) k_ctx_hist(
         if (up) atomicAdd(&sm.wst_hi[wp][b], up);
       });
       __syncthreads();
-      if (!FUSED && in_smem)
+      if (in_smem)
         for (uint32_t i = tid; i < nb; i += CR_THREADS) bscr[ob + i] = ((unsigned long long)sm.cnt_hi[i] << 32) | sm.cnt_lo[i];
       if (tid < 32) {
         unsigned long long t = 0;
@@ -1245,137 +1253,48 @@ __global__ void __launch_bounds__(CR_THREADS, 1) k_ctx_hist(
         unsigned long long tot = tid < S ? t : 0;
 #pragma unroll
         for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-        if (tid == 0) {
-          if (tot) xsamples[ctx] += tot;
-          if (!FUSED) {
-            rec[g] = CtxRec{ow, ob, (uint32_t)ctx, W, (uint32_t)sh, nb};
-            gnb[g] = nb;
-            gnp[g] = np;
-          }
-        }
+        if (tid == 0 && tot) xsamples[ctx] += tot;
       }
     }
-    if (FUSED) {
-      // look back (warp 0) for the global bases of this context's PC nodes and bins
-      if (wp == 0) {
-        unsigned long long bb = 0, pb = 0;
-        if (g > 0) {
-          int64_t j = (int64_t)g - 1 - (int64_t)lane;
-          for (uint64_t spins = 0;;) {
-            uint32_t st = 2;
-            if (j >= 0) st = (uint32_t)cr_ld_acq(gst + 5 * j);
-            const uint32_t incl = __ballot_sync(0xffffffffu, st == 2);
-            const int first = incl ? __ffs(incl) - 1 : 31;
-            const uint32_t need = first == 31 ? 0xffffffffu : ((2u << first) - 1u);
-            if (__ballot_sync(0xffffffffu, st == 0) & need) {
-              if (++spins > DC_SPIN_LIMIT) __trap();
-              continue;
-            }
-            unsigned long long x = 0, y = 0;
-            if ((int)lane <= first && j >= 0) {
-              x = __ldcg(gst + 5 * j + (st == 2 ? 3 : 1));
-              y = __ldcg(gst + 5 * j + (st == 2 ? 4 : 2));
-            }
-#pragma unroll
-            for (int o = 16; o; o >>= 1) {
-              x += __shfl_xor_sync(0xffffffffu, x, o);
-              y += __shfl_xor_sync(0xffffffffu, y, o);
-            }
-            bb += x;
-            pb += y;
-            if (incl) break;
-            j -= 32;
-          }
-          if (lane == 0) {
-            unsigned long long* me = gst + 5ull * g;
-            me[3] = bb + nb;
-            me[4] = pb + np;
-            cr_st_rel(me, 2ull);
-          }
-        }
-        if (lane == 0) {
-          sm.ow = bb;  // reused: this context's bin base
-          sm.ob = pb;  //          and PC-node base
-          if (g == NG - 1) {
-            ctl[4] = bb + nb;
-            ctl[5] = pb + np;
-          }
-        }
-      }
-      __syncthreads();
-      const uint64_t bb = sm.ow, pb = sm.ob;
-      if (ok && nb) {
-        if (bb + nb > cap) {  // outputs past the capacity: the host reallocates and reruns
-          if (tid == 0) atomicOr(ctl + 1, (unsigned long long)CR_OVER);
-        } else {
-          for (uint32_t w = tid; w < W; w += CR_THREADS) {
-            uint32_t bits = sm.bm[w];
-            if (!bits) continue;
-            const uint64_t p = pb + sm.ppre[w];
-            pc_ctx[p] = (uint32_t)ctx;
-            pc_off[p] = w << sh;
-            uint64_t r = bb + sm.bpre[w];
-            while (bits) {
-              const uint32_t b = __ffs(bits) - 1;
-              bits &= bits - 1;
-              bin_pcnode[r] = (uint32_t)(N + p);
-              bin_stall[r] = (uint16_t)b;
-              ++r;
-            }
-          }
-          if (in_smem)
-            for (uint32_t i = tid; i < nb; i += CR_THREADS) bin_count[bb + i] = ((uint64_t)sm.cnt_hi[i] << 32) | sm.cnt_lo[i];
-          else
-            for (uint32_t i = tid; i < nb; i += CR_THREADS) bin_count[bb + i] = __ldcg(bscr + ob + i);
-        }
-      }
+    if (tid == 0) {
+      rec[g] = CtxRec{ok ? sm.ow : 0ull, ob, (uint32_t)ctx, (uint32_t)sh};
+      gnb[g] = ok ? nb : 0;
+      gnp[g] = ok ? np : 0;
     }
     __syncthreads();
   }
 }
 
-// one CTA per group (grid-stride): PC nodes and bins in canonical order, counts copied
-constexpr int CE_THREADS = 256;
-__global__ void __launch_bounds__(CE_THREADS) k_ctx_emit(const CtxRec* __restrict__ rec, const uint32_t* __restrict__ d_ng,
-                                                         const uint64_t* __restrict__ bbase, const uint64_t* __restrict__ pbase,
-                                                         const uint32_t* __restrict__ wscr, const unsigned long long* __restrict__ bscr,
-                                                         uint64_t N, uint64_t cap, unsigned long long* __restrict__ status,
-                                                         uint32_t* __restrict__ pc_ctx, uint32_t* __restrict__ pc_off,
-                                                         uint32_t* __restrict__ bin_pcnode, uint16_t* __restrict__ bin_stall,
-                                                         uint64_t* __restrict__ bin_count, const uint32_t* __restrict__ g_flags) { DC_PDL_ENTER();
-  if (*g_flags) return;
-  const uint32_t NG = *d_ng, tid = threadIdx.x;
-  for (uint32_t g = blockIdx.x; g < NG; g += gridDim.x) {
-    const CtxRec r = rec[g];
-    if (!r.nb) continue;
-    const uint64_t bb = bbase[g], pb = pbase[g];
-    if (bb + r.nb > cap) {
-      if (tid == 0) atomicOr(status, (unsigned long long)CR_OVER);
+// one thread per scratch word (grid-stride over the words used): its PC node, bins and counts
+__global__ void k_ctx_emit(const CtxWord* __restrict__ wscr, const unsigned long long* __restrict__ ctl, const CtxRec* __restrict__ rec,
+                           const uint64_t* __restrict__ bbase, const uint64_t* __restrict__ pbase,
+                           const unsigned long long* __restrict__ bscr, uint64_t N, uint64_t cap, unsigned long long* __restrict__ status,
+                           uint32_t* __restrict__ pc_ctx, uint32_t* __restrict__ pc_off, uint32_t* __restrict__ bin_pcnode,
+                           uint16_t* __restrict__ bin_stall, uint64_t* __restrict__ bin_count, const uint32_t* __restrict__ g_flags) { DC_PDL_ENTER();
+  if (*g_flags || (ctl[1] & CR_WIDE)) return;
+  const uint64_t total = ctl[2];
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+    const CtxWord cw = wscr[i];
+    uint32_t bits = cw.bits;
+    if (!bits) continue;
+    const CtxRec r = rec[cw.g];
+    const uint64_t p = pbase[cw.g] + cw.ppre;
+    uint64_t q = bbase[cw.g] + cw.bpre;
+    if (q + __popc(bits) > cap) {
+      atomicOr(status, (unsigned long long)CR_OVER);
       continue;
     }
-    for (uint32_t i = tid; i < r.nb; i += CE_THREADS) bin_count[bb + i] = bscr[r.ob + i];
-    uint32_t brun = 0, prun = 0;  // bins / PC nodes before this round
-    for (uint32_t w0 = 0; w0 < r.W; w0 += CE_THREADS) {
-      const uint32_t w = w0 + tid;
-      uint32_t bits = w < r.W ? __ldcg(wscr + r.ow + w) : 0u;
-      uint32_t tb, tp;
-      const uint32_t bx = block_excl_scan<uint32_t, CE_THREADS>(__popc(bits), &tb);
-      const uint32_t px = block_excl_scan<uint32_t, CE_THREADS>(bits != 0u, &tp);
-      if (bits) {
-        const uint64_t p = pb + prun + px;
-        pc_ctx[p] = r.ctx;
-        pc_off[p] = w << r.sh;
-        uint64_t q = bb + brun + bx;
-        while (bits) {
-          const uint32_t b = __ffs(bits) - 1;
-          bits &= bits - 1;
-          bin_pcnode[q] = (uint32_t)(N + p);
-          bin_stall[q] = (uint16_t)b;
-          ++q;
-        }
-      }
-      brun += tb;
-      prun += tp;
+    pc_ctx[p] = r.ctx;
+    pc_off[p] = (uint32_t)(i - r.ow) << r.sh;
+    const unsigned long long* src = bscr + r.ob + cw.bpre;
+    uint32_t k = 0;
+    while (bits) {
+      const uint32_t b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      bin_pcnode[q] = (uint32_t)(N + p);
+      bin_stall[q] = (uint16_t)b;
+      bin_count[q] = src[k++];
+      ++q;
     }
   }
 }
@@ -1752,7 +1671,6 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
   if (n == 0 || n_launch == 0 || n_launch >= (1ull << 31)) return DC_OK;
   const uint64_t N = t->N;
   const uint32_t G = (uint32_t)c->num_sms;
-  const bool fused = !(getenv("DC_PC_CR") && atoi(getenv("DC_PC_CR")) == 2);
   Buf<uint32_t> bad;
   Buf<uint64_t> k0, k1;
   Buf<uint32_t> v0, v1;
@@ -1770,7 +1688,7 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
   Buf<uint32_t> hist;
   Buf<unsigned long long> ctr, ldiag, ctl;
   Buf<uint32_t> flags;
-  const uint64_t ctl_n = 6 + (fused ? 5 * (n_launch + 1) : 0);
+  const uint64_t ctl_n = 4 + 2 * (n_launch + 1);  // ctl[4] and the group (bins, pcs) arrays of the context reduce
   DC_TRY(alloc_fill(c, fl, bad, 1));
   if (counting_sort) DC_TRY(alloc_fill(c, fl, hist, N + 1));
   DC_TRY(alloc_fill(c, fl, row_valid, row_cap));
@@ -1925,25 +1843,24 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
     }
     uint32_t hbad = 0;
     if (!getenv("DC_TEST_PC_BR")) {
-      // ------------------------------------------------ context reduce (k_ctx_hist [, scan, k_ctx_emit])
+      // ------------------------------------------------ context reduce (k_ctx_order, k_ctx_hist, scan, k_ctx_emit)
       Region rr(c, "pc:creduce");
       uint64_t cap = c->pc_bins_hint > (1ull << 20) ? c->pc_bins_hint : (1ull << 20);
       if (cap > n) cap = n ? n : 1;
       if (getenv("DC_TEST_PC_CAP")) cap = 1;  // test only: force the reallocate-and-rerun path
-      const uint64_t wcap = fused ? 0 : (c->pc_words_hint > (4ull << 20) ? c->pc_words_hint : (4ull << 20));
-      const uint64_t bcap = fused ? std::max<uint64_t>(c->pc_big_hint, 1ull << 20)
-                                  : (c->pc_bins_hint > (4ull << 20) ? c->pc_bins_hint : (4ull << 20));
+      const uint64_t wcap = std::max<uint64_t>(c->pc_words_hint, 4ull << 20);
+      const uint64_t bcap = std::max<uint64_t>(c->pc_bins_hint, 4ull << 20);
       Buf<unsigned long long> bscr;
-      Buf<uint32_t> wscr;
+      Buf<CtxWord> wscr;
       Buf<CtxRec> rec;
-      Buf<uint64_t> gn, gbase;  // [gnb | gnp], [bin base | pc base] (n_launch + 1 each)
+      Buf<uint32_t> order;
+      Buf<uint64_t> gbase;  // [bin base | pc base] (n_launch + 1 each)
+      uint64_t* gn = reinterpret_cast<uint64_t*>(ctl.p + 4);  // [gnb | gnp] per group, zeroed with the counters
       DC_TRY(alloc(c, wscr, wcap));
       DC_TRY(alloc(c, bscr, bcap));
-      if (!fused) {
-        DC_TRY(alloc(c, rec, n_launch));
-        DC_TRY(alloc_zero(c, gn, 2 * (n_launch + 1)));
-        DC_TRY(alloc(c, gbase, 2 * (n_launch + 1)));
-      }
+      DC_TRY(alloc(c, rec, n_launch));
+      DC_TRY(alloc(c, order, n_launch));
+      DC_TRY(alloc(c, gbase, 2 * (n_launch + 1)));
       auto outputs = [&](uint64_t k) -> dc_status {
         DC_TRY(palloc(c, t->pc_ctx, k));
         DC_TRY(palloc(c, t->pc_off, k));
@@ -1960,75 +1877,45 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
         t->bin_count = nullptr;
       };
       auto clear_cols = [&]() -> dc_status {
-        DC_CUDA(c, cudaMemsetAsync(t->xsamples, 0, N * 8, c->stream));
-        DC_CUDA(c, cudaMemsetAsync(t->xstall, 0, (uint64_t)S * N * 8, c->stream));
-        return DC_OK;
+        FillList f2;
+        DC_TRY(fill_add(c, f2, t->xsamples, N * 8));
+        DC_TRY(fill_add(c, f2, t->xstall, (uint64_t)S * N * 8));
+        return fill_flush(c, f2);
       };
       DC_TRY(outputs(cap));
+      dc_launch(k_ctx_order, 1, 1024, 0, c->stream, seg.p, a.g_segs, cap_segs, lkey_out, gfirst.p, gx.p + n_launch, order.p);
+      DC_LAUNCHED(c);
       const size_t csmem = sizeof(CtxRedSmem);
-      auto hist = [&](uint64_t k) -> dc_status {
+      DC_CUDA(c, cudaFuncSetAttribute(k_ctx_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
+      {
         Region rk(c, "k:ctx_hist");
-        void (*kern)(const uint4*, const unsigned int*, uint32_t, const uint32_t*, const unsigned long long*, const uint64_t*,
-                     const uint32_t*, const uint32_t*, uint64_t, uint32_t, const uint32_t*, unsigned long long*, uint32_t*, uint64_t,
-                     unsigned long long*, uint64_t, CtxRec*, uint64_t*, uint64_t*, unsigned long long*, unsigned long long*,
-                     uint64_t, uint32_t*, uint32_t*, uint32_t*, uint16_t*, uint64_t*) =
-            fused ? k_ctx_hist<true> : k_ctx_hist<false>;
-        DC_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
-        dc_launch(kern, G, CR_THREADS, csmem, c->stream, seg.p, a.g_segs, cap_segs, pkey.p, pcnt.p, lkey_out, gfirst.p,
-                  gx.p + n_launch, N, S, flags.p, ctl.p, wscr.p, wcap, bscr.p, bcap, rec.p, gn.p,
-                  fused ? nullptr : gn.p + n_launch + 1, (unsigned long long*)t->xsamples, (unsigned long long*)t->xstall, k,
-                  t->pc_ctx, t->pc_off, t->bin_pcnode, t->bin_stall, t->bin_count);
+        // groups past NG keep zero (bins, pcs) for the scan over the n_launch bound: k_ctx_hist
+        // writes every group < NG; the rest are cleared with the counters
+        dc_launch(k_ctx_hist, G, CR_THREADS, csmem, c->stream, seg.p, a.g_segs, cap_segs, pkey.p, pcnt.p, lkey_out, gfirst.p,
+                  gx.p + n_launch, order.p, N, S, flags.p, ctl.p, wscr.p, wcap, bscr.p, bcap, rec.p, gn, gn + n_launch + 1,
+                  (unsigned long long*)t->xsamples, (unsigned long long*)t->xstall);
         DC_LAUNCHED(c);
-        return DC_OK;
-      };
+      }
+      DC_TRY((excl_scan_pair<uint64_t, uint64_t>(c, gn, gbase.p, gbase.p + n_launch, gn + n_launch + 1,
+                                                 gbase.p + n_launch + 1, gbase.p + 2 * n_launch + 1, n_launch)));
       auto emit = [&](uint64_t k) -> dc_status {
         Region rk(c, "k:ctx_emit");
-        dc_launch(k_ctx_emit, 4 * G, CE_THREADS, 0, c->stream, rec.p, gx.p + n_launch, gbase.p, gbase.p + n_launch + 1, wscr.p,
-                  bscr.p, N, k, ctl.p + 1, t->pc_ctx, t->pc_off, t->bin_pcnode, t->bin_stall, t->bin_count, flags.p);
+        dc_launch(k_ctx_emit, grid_for(c, std::max<uint64_t>(c->pc_words_hint, 1ull << 16), 256), 256, 0, c->stream, wscr.p, ctl.p,
+                  rec.p, gbase.p, gbase.p + n_launch + 1, bscr.p, N, k, ctl.p + 1, t->pc_ctx, t->pc_off, t->bin_pcnode,
+                  t->bin_stall, t->bin_count, flags.p);
         DC_LAUNCHED(c);
         return DC_OK;
       };
-      DC_TRY(hist(cap));
-      if (!fused) {
-        DC_TRY((excl_scan_pair<uint64_t, uint64_t>(c, gn.p, gbase.p, gbase.p + n_launch, gn.p + n_launch + 1,
-                                                   gbase.p + n_launch + 1, gbase.p + 2 * n_launch + 1, n_launch)));
-        DC_TRY(emit(cap));
-      }
-      uint64_t hst[5] = {0, 0, 0, 0, 0}, htot[2] = {0, 0};
-      if (fused) {
-        DC_TRY(readback_multi(c, {{flags.p, 8, hf}, {bad.p, 4, &hbad}, {ctl.p + 1, 40, hst}, {ctr.p, 16, hc}}));
-        htot[0] = hst[3];
-        htot[1] = hst[4];
-      } else {
-        DC_TRY(readback_multi(c, {{flags.p, 8, hf}, {bad.p, 4, &hbad}, {ctl.p + 1, 24, hst}, {gbase.p + n_launch, 8, &htot[0]},
-                                  {gbase.p + 2 * n_launch + 1, 8, &htot[1]}, {ctr.p, 16, hc}}));
-      }
+      DC_TRY(emit(cap));
+      uint64_t hst[3] = {0, 0, 0}, htot[2] = {0, 0};
+      DC_TRY(readback_multi(c, {{flags.p, 8, hf}, {bad.p, 4, &hbad}, {ctl.p + 1, 24, hst}, {gbase.p + n_launch, 8, &htot[0]},
+                                {gbase.p + 2 * n_launch + 1, 8, &htot[1]}, {ctr.p, 16, hc}}));
       if (getenv("DC_PC_STATS"))  // measurement only
         fprintf(stderr, "{\"pc_stats\": {\"entries\": %llu, \"segments\": %llu, \"bins\": %llu, \"pcs\": %llu, \"status\": %llu, "
                 "\"words\": %llu, \"scratch_bins\": %llu}}\n", (unsigned long long)hc[0], (unsigned long long)(hc[1] & 0xFFFFFFFFu),
                 (unsigned long long)htot[0], (unsigned long long)htot[1], (unsigned long long)hst[0], (unsigned long long)hst[1],
                 (unsigned long long)hst[2]);
-      if (getenv("DC_PC_STATS")) {  // measurement only: entries per context
-        const uint32_t nsg = (uint32_t)std::min<uint64_t>(hc[1] & 0xFFFFFFFFu, cap_segs);
-        std::vector<uint4> hs(nsg);
-        DC_TRY(readback(c, seg.p, nsg * sizeof(uint4), hs.data()));
-        std::vector<uint64_t> per(N + 1, 0), nseg(N + 1, 0);
-        for (auto& q : hs) {
-          per[q.x < N ? q.x : N] += q.y;
-          nseg[q.x < N ? q.x : N] += 1;
-        }
-        std::vector<std::pair<uint64_t, uint64_t>> v;
-        for (uint64_t i = 0; i <= N; ++i)
-          if (per[i]) v.push_back({per[i], nseg[i]});
-        std::sort(v.begin(), v.end());
-        fprintf(stderr, "{\"pc_ctx_entries\": {\"contexts\": %zu, \"median\": %llu, \"p90\": %llu, \"top\": [", v.size(),
-                (unsigned long long)v[v.size() / 2].first, (unsigned long long)v[v.size() * 9 / 10].first);
-        for (size_t i = v.size() > 12 ? v.size() - 12 : 0; i < v.size(); ++i)
-          fprintf(stderr, "[%llu, %llu]%s", (unsigned long long)v[i].first, (unsigned long long)v[i].second, i + 1 < v.size() ? ", " : "");
-        fprintf(stderr, "]}}\n");
-      }
-      if (fused) c->pc_big_hint = hst[2] + hst[2] / 8;
-      else c->pc_words_hint = hst[1] + hst[1] / 8;
+      c->pc_words_hint = hst[1] + hst[1] / 8;
       if (hbad || hf[0]) {  // offsets inconsistent / owner fallback: generic schedule
         drop_outputs();
         if (hf[0] && !hbad && getenv("DC_TEST_OWNER_STRICT"))
@@ -2037,16 +1924,10 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
       }
       if (!(hst[0] & CR_WIDE)) {
         const uint64_t nb = htot[0], npc = htot[1];
-        if (hst[0] & CR_OVER) {  // more bins than the capacity guess: exact outputs, write again
+        if (hst[0] & CR_OVER) {  // more bins than the capacity guess: exact outputs, emit again
           drop_outputs();
           DC_TRY(outputs(nb));
-          if (fused) {
-            DC_TRY(clear_cols());
-            DC_CUDA(c, cudaMemsetAsync(ctl.p, 0, ctl_n * 8, c->stream));
-            DC_TRY(hist(nb));
-          } else {
-            DC_TRY(emit(nb));
-          }
+          DC_TRY(emit(nb));
         }
         t->Npc = npc;
         t->Nbins = nb;
@@ -2056,7 +1937,7 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
         *handled = 1;
         return DC_OK;
       }
-      if (!fused) c->pc_bins_hint = hst[2] + hst[2] / 8;
+      c->pc_bins_hint = std::max<uint64_t>(hst[2] + hst[2] / 8, c->pc_bins_hint);
       // a context too wide for shared memory: the global-bitmap reduce below (from scratch)
       drop_outputs();
       DC_TRY(clear_cols());
