@@ -119,7 +119,8 @@ def spin_waits(device: int):
 
 
 # --------------------------------------------------------------------------- workloads
-def make_workload(cfg: int, rank: int, device: str, n_records: int | None = None):
+def make_workload(cfg: int, rank: int, device: str, n_records: int | None = None, stress: bool = False,
+                  aggregated: bool = False):
     import gen
     from gen import programs
     if cfg == 3:
@@ -135,6 +136,12 @@ def make_workload(cfg: int, rank: int, device: str, n_records: int | None = None
     if cfg != 5:
         p.seed = p.seed + 7919 * rank  # weak scaling: each rank its own draws of the same program
     tr = gen.make_trace(p, n_records=n_records, device=device, raw_keys=(cfg != 4), ids=(cfg == 4), pc=(cfg == 3))
+    if stress and cfg == 3:  # variant 3s: 20k distinct contexts, samples of 8 launches interleaved
+        from gen import stress as st
+        tr = st.make_3s(tr)
+    if aggregated and cfg == 3:  # per-PC aggregated records (count > 1), as CUPTI delivers them
+        from gen import stress as st
+        tr = st.make_aggregated(tr)
     return p, tr
 
 
@@ -178,7 +185,7 @@ def alg_bytes_pc_hist(n_samples: int, n_bins: int) -> int:
 
 
 # --------------------------------------------------------------------------- oracle (CPU) legs
-def oracle_sample(cfg: int, n_launch: int, rank: int = 0):
+def oracle_sample(cfg: int, n_launch: int, rank: int = 0, stress: bool = False):
     """Bounded sample of the workload on the host: the first n_launch launch records and their
     PC samples (config 3), generated by the same generator."""
     import gen
@@ -186,6 +193,9 @@ def oracle_sample(cfg: int, n_launch: int, rank: int = 0):
     p = programs.config3() if cfg == 3 else programs.program(cfg)
     p.seed = p.seed + 7919 * rank
     tr = gen.make_trace(p, n_records=n_launch, pc=(cfg == 3), n_launch=n_launch if cfg == 3 else None)
+    if stress and cfg == 3:
+        from gen import stress as st
+        tr = st.make_3s(tr)
     return p, tr
 
 
@@ -205,8 +215,8 @@ def oracle_time(p, tr, cfg: int) -> tuple[float, int]:
     return dt, records_of(tr, cfg)
 
 
-def cpu_baseline(cfg: int, n_launch: int):
-    p, tr = oracle_sample(cfg, n_launch)
+def cpu_baseline(cfg: int, n_launch: int, stress: bool = False):
+    p, tr = oracle_sample(cfg, n_launch, stress=stress)
     dt, recs = oracle_time(p, tr, cfg)
     desc = (f"first {n_launch} launch records of config {cfg} and their {recs - n_launch} PC samples "
             f"(of 20,000 / 100,000,000)" if cfg == 3 else f"first {n_launch} records of config {cfg}")
@@ -250,6 +260,8 @@ def main():
     ap.add_argument("--cpu-launches", type=int, default=4000, help="bounded oracle sample (launch records)")
     ap.add_argument("--ref-launches", type=int, default=200)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--stress", action="store_true", help="config 3s: 20k distinct contexts, interleaved samples (generic schedule)")
+    ap.add_argument("--aggregated", action="store_true", help="config 3 with per-PC aggregated records (counts > 1)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -268,7 +280,7 @@ def main():
 
     import paper_2411_02797_b200 as dc
     dev = f"cuda:{local}"
-    p, tr = make_workload(args.config, rank, dev, args.records)
+    p, tr = make_workload(args.config, rank, dev, args.records, stress=args.stress, aggregated=args.aggregated)
     if args.config == 4:
         keys = torch.from_numpy(np.ascontiguousarray(p.pool_keys).view(np.int32).reshape(-1, 4).copy()).to(dev)
     ctx = dc.Context(local)
@@ -361,11 +373,12 @@ def main():
     R_, F_ = tr.n_records, F
     alg = {  # kernel timer -> algorithmic bytes of one launch
         "k:pc_owner": alg_bytes_pc_hist(n_smp, n_bins) if args.config == 3 else 0,  # 16 B/sample + 16 B/bin
+        "k:pc_table": alg_bytes_pc_hist(n_smp, n_bins) if args.config == 3 else 0,  # generic schedule (3s)
         "k:intern_insert": 20 * F_,                          # 16-B raw key read + 4-B id written per key
         "k:path_hash": 8 * (R_ + 1) + 4 * F_ + 8 * R_,       # offsets + frames read, 8-B path hash written
         "k:path_group": 8 * (R_ + 1) + 4 * F_ + 12 * R_,     # offsets + frames (exact verify) + hash read, slot written
     }
-    cand = [k for k in alg if k in timers and alg[k] and (args.config != 3 or k == "k:pc_owner")]
+    cand = [k for k in alg if k in timers and alg[k] and (args.config != 3 or k in ("k:pc_owner", "k:pc_table"))]
     kname = max(cand, key=lambda k: timers[k][1] / timers[k][0]) if cand else None
     roof = None
     if kname:
@@ -386,7 +399,8 @@ def main():
                 "metrics": tr.metrics.cpu().pin_memory()}
         if args.config == 3:
             host["samples"] = tr.samples.cpu().pin_memory()
-            host["launch_off"] = tr.launch_off.cpu().pin_memory()
+            if tr.launch_off is not None:
+                host["launch_off"] = tr.launch_off.cpu().pin_memory()
         devb = {k: torch.empty_like(v, device=dev) for k, v in host.items()}
         h2d = sum(v.numel() * v.element_size() for v in host.values())
         d2h = 0
@@ -396,6 +410,7 @@ def main():
         t2 = T()
         t2.ids_buf, t2.leaf_buf, t2.derived_buf, t2.n_stall = tr.ids_buf, tr.leaf_buf, None, getattr(tr, "n_stall", 24)
         t2.n_records = tr.n_records
+        t2.launch_off = None
         for k, v in devb.items():
             setattr(t2, k, v)
         gc.collect()
@@ -426,7 +441,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(args.config, args.cpu_launches)
+        cpu = cpu_baseline(args.config, args.cpu_launches, stress=args.stress)
 
     if rank == 0:
         wl = {3: "config3: LLM-inference PC-sampling trace, 20k launch records (raw 16-B frame keys, mean depth ~42) "
@@ -435,10 +450,17 @@ def main():
               1: "config1: tiny 10k-record trace", 4: "config4: JAX-shaped pre-interned trace, depth <= 256",
               5: "config5: one DDP shard per rank (config-2 program, rank-local frames, own raw-key dictionary), "
                  "125M records per rank; merged across ranks at N > 1"}[args.config]
+        if args.aggregated and args.config == 3:
+            wl = ("config3 aggregated: config 3's 100M raw samples as per-launch per-(pc, stall) records with counts "
+                  f"({int(tr.samples.shape[0])} records, as CUPTI's PC-sampling API delivers them)")
+        if args.stress and args.config == 3:
+            wl = ("config3s (stress variant): config 3 with a per-launch outermost frame (20k distinct contexts) and the "
+                  "samples of each 8 consecutive launches interleaved round robin (no per-launch offsets: generic schedule)")
         line = {"metric": METRIC, "value": value, "unit": "records/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "u64", "data": "synthetic (counter-based generator, gen/)",
-                "config": {"workload": wl, "config_id": args.config, "records_per_gpu_step": recs,
+                "config": {"workload": wl, "config_id": args.config, "variant": "3s" if args.stress else ("aggregated" if args.aggregated else None),
+                           "records_per_gpu_step": recs,
                            "pc_samples": int(tr.samples.shape[0]) if args.config == 3 else 0,
                            "launch_records": tr.n_records, "nodes": n_nodes, "bins": n_bins,
                            "l2": f"inputs larger than L2 ({step_bytes / 1e9:.2f} GB read per step); no flush",

@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(256) k_path_group(const uint64_t* __restrict__
       L = (uint32_t)(o1 >= o ? min(o1 - o, (uint64_t)DC_MAX_DEPTH) : 0);  // validated by k_path_hash
       const uint64_t H = hash[r];
       uint64_t q = (H * 0x9E3779B97F4A7C15ull >> 17) & mask;
-      for (uint64_t probe = 0; probe <= mask; ++probe, q = (q + 1) & mask) {
+      for (uint64_t probe = 0; probe <= (mask < 4096 ? mask : 4096); ++probe, q = (q + 1) & mask) {  // bounded: a long run = overflow, retried larger
         const unsigned long long cur = ld_relaxed_u64(&tab[q].key);
         if (cur == H) {
           sl = (uint32_t)q;
@@ -974,7 +974,7 @@ __global__ void k_prefix_nodes(const uint64_t* __restrict__ off, const uint32_t*
       bool mine = false;
       if (act) {
         uint64_t q = (H * 0x9E3779B97F4A7C15ull >> 17) & mask;
-        for (uint64_t probe = 0; probe <= mask; ++probe, q = (q + 1) & mask) {
+        for (uint64_t probe = 0; probe <= (mask < 4096 ? mask : 4096); ++probe, q = (q + 1) & mask) {  // bounded: a long run = overflow, retried larger
           const unsigned long long cur = ld_relaxed_u64(&tab[q].key);
           if (cur == H) {
             sl = (uint32_t)q;
@@ -1152,7 +1152,9 @@ static dc_status build_euler(Ctx* c, const dc_paths* p, const uint32_t* item_rec
   Buf<uint32_t> leaf_slot;
   Buf<unsigned int> cnt;
   DC_TRY(alloc(c, leaf_slot, P));
-  const uint64_t want = std::min<uint64_t>(sumlen + 1, 8ull * P + 1024);
+  // nodes <= sumlen + 1; a tree with little sharing has far more than 8 per path: the last
+  // call's node count (per context) keeps the first attempt from overflowing on repeated shapes
+  const uint64_t want = std::min<uint64_t>(sumlen + 1, std::max<uint64_t>(8ull * P + 1024, c->euler_nodes_hint));
   uint64_t cap = 1024;
   while (cap < 2 * want) cap <<= 1;
   uint32_t hc[4];
@@ -1177,6 +1179,7 @@ static dc_status build_euler(Ctx* c, const dc_paths* p, const uint32_t* item_rec
     cap = big;
   }
   const uint32_t Nn = hc[0];  // nodes without the root
+  c->euler_nodes_hint = (uint64_t)Nn + Nn / 4 + 1;
   Buf<uint32_t> nslot, nidx, par, frm, sv0, sv1, first_child, next_sib, canon;
   Buf<uint16_t> dep;
   Buf<uint64_t> sk0, sk1;

@@ -54,6 +54,8 @@ struct Ctx {
   uint64_t pc_bins_hint = 0;   // bins of the last PC-histogram call (+1/8): capacity guess of the next
   uint64_t pc_words_hint = 0;  // bitmap words of the last context reduce (+1/8): its scratch guess
   uint64_t pc_big_hint = 0;    // bins of big contexts (counted in scratch) of the last call (+1/8)
+  uint64_t pc_generic_hint = 0;  // distinct bins of the last generic-schedule call
+  uint64_t euler_nodes_hint = 0;  // nodes of the last Euler-tour build (+1/4): its table size guess
   std::string err;
   uint32_t* d_flags = nullptr;   // [1]
   uint64_t* d_diag = nullptr;    // [DG_N]

@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(256) k_intern_insert(const dc_frame_key* __res
     }
     if (found == 0xFFFFFFFFu) {  // ---- L2 table
       uint64_t s = h & mask;
-      for (uint64_t probe = 0; probe <= mask; ++probe, s = (s + 1) & mask) {
+      for (uint64_t probe = 0; probe <= (mask < 4096 ? mask : 4096); ++probe, s = (s + 1) & mask) {  // bounded: overflow, retried larger
         ulonglong2 cur = ld_relaxed_v2(table + s);
         if (cur.x == lo && cur.y == hi && hi != EMPTY) { found = (uint32_t)s; break; }
         bool maybe_partial = ((uint32_t)cur.x == 0xFFFFFFFFu) || cur.y == EMPTY;  // empty, or a torn read of a claim

@@ -9,6 +9,8 @@
 // distinct bins are then compacted, radix-sorted into canonical order and run-length
 // encoded into PC nodes. The context-owner schedule (pc_owner.cu) replaces the table pass
 // when per-launch sample offsets are given.
+#include <algorithm>
+
 #include "prim.cuh"
 
 namespace dc {
@@ -48,7 +50,10 @@ __global__ void k_pc_table(const dc_pc_sample* __restrict__ smp, uint64_t n, con
     const uint64_t kx = ((uint64_t)ctx << 32) | pc, ky = stall;
     uint64_t s = mix64(kx * 0x9E3779B97F4A7C15ull + ky) & mask;
     bool done = false;
-    for (uint64_t probe = 0; probe <= mask; ++probe, s = (s + 1) & mask) {
+    // a probe run this long means the table is (nearly) full: report overflow (the host retries
+    // with a table sized by the distinct bins) instead of walking the whole table per sample
+    const uint64_t max_probe = mask < 4096 ? mask : 4096;
+    for (uint64_t probe = 0; probe <= max_probe; ++probe, s = (s + 1) & mask) {
       ulonglong2 cur = ld_relaxed_v2(table + s);
       if (cur.x == kx && cur.y == ky) { done = true; break; }
       if (cur.x != ~0ull && cur.y != ~0ull) continue;
@@ -356,16 +361,21 @@ static dc_status pc_attribute_once(Ctx* c, dc_cct* t, const dc_pc_sample* s, uin
   }
   DC_TRY(fill_flush(c, fl));  // pending column fills (the owner schedule did not run / flush them)
   if (!handled) {
-    uint64_t cap = np2(2 * (n < (1ull << 22) ? n : (1ull << 22)));
+    // table sized for twice the bins of the last generic call (or 2 x min(n, 4M)); an overflow
+    // (distinct bins past half load, or a probe run past 4,096) retries with 4x the slots
+    uint64_t guess = c->pc_generic_hint ? c->pc_generic_hint : (n < (1ull << 22) ? n : (1ull << 22));
+    if (guess > n) guess = n;
+    uint64_t cap = np2(2 * guess);
     if (cap < 1024) cap = 1024;
     Buf<unsigned int> ctr;
     Buf<unsigned long long> ldiag;  // this call's diag counts (a retry recounts every sample)
     for (int attempt = 0;; ++attempt) {
-      DC_TRY(alloc(c, table, cap));
-      DC_TRY(alloc_zero(c, tcnt, cap));
-      DC_TRY(alloc_zero(c, ctr, 4));
-      DC_TRY(alloc_zero(c, ldiag, DG_N));
-      DC_CUDA(c, cudaMemsetAsync(table.p, 0xFF, cap * 16, c->stream));
+      FillList f2;
+      DC_TRY(alloc_fill(c, f2, table, cap, 0xFF));
+      DC_TRY(alloc_fill(c, f2, tcnt, cap));
+      DC_TRY(alloc_fill(c, f2, ctr, 4));
+      DC_TRY(alloc_fill(c, f2, ldiag, DG_N));
+      DC_TRY(fill_flush(c, f2));
       {
         Region rk(c, "k:pc_table");
         dc_launch(k_pc_table, grid_for(c, n, 256, 16), 256, 0, c->stream, s, n, launch_leaf, n_launch, S, N, table.p, tcnt.p,
@@ -376,11 +386,12 @@ static dc_status pc_attribute_once(Ctx* c, dc_cct* t, const dc_pc_sample* s, uin
       DC_TRY(readback(c, ctr.p, 8, h));
       if (!h[1] && (uint64_t)h[0] * 2 <= cap) {
         nb = h[0];
+        c->pc_generic_hint = nb;
         break;
       }
-      if (attempt) return fail(c, DC_ERR_CAPACITY, "PC bin table overflow (%u distinct bins)", h[0]);
-      cap = np2(4 * (uint64_t)(h[0] > n ? h[0] : n));
-      if (cap > (1ull << 31)) return fail(c, DC_ERR_CAPACITY, "PC bin table would exceed 2^31 slots");
+      if (attempt == 4 || cap >= (1ull << 31)) return fail(c, DC_ERR_CAPACITY, "PC bin table overflow (%u distinct bins)", h[0]);
+      cap = std::max<uint64_t>(4 * cap, np2(4 * (uint64_t)h[0]));
+      if (cap > (1ull << 31)) cap = 1ull << 31;
     }
     DC_TRY(add_diag(c, ldiag.p));
     Buf<unsigned int> mx;

@@ -69,6 +69,9 @@ struct OwnSmem {
   unsigned long long full[OW_STAGES], empty[OW_STAGES];
   OwMeta meta[OW_STAGES];
   uint32_t distinct;
+  // counts above 1 added to the table since the last flush (aggregated records): a flush is
+  // requested past OW_EXTRA_FLUSH so no 32-bit counter can wrap (see own_hot)
+  uint32_t extra;
   uint32_t flush_req;
   // spill allocator: word = generation << 20 | entries taken in the generation's chunk; a full
   // chunk is closed as a segment and replaced by one from the global entry pool (sp_lock)
@@ -274,7 +277,10 @@ __device__ __forceinline__ void own_flush(OwnSmem& sm, const OwnArgs& a, uint32_
     sm.cnt[s] = 0;
   }
   cons_sync();
-  if (ctid == 0) sm.distinct = 0;
+  if (ctid == 0) {
+    sm.distinct = 0;
+    sm.extra = 0;
+  }
   cons_sync();
 }
 
@@ -406,6 +412,15 @@ __device__ __noinline__ uint32_t own_reject(uint32_t launch, uint32_t stall, uin
 // Hot path: a raw sample (count 1) of its row's launch with a valid stall -> key (pc_off << 5 |
 // stall). Everything else takes own_cold: invalid samples are classified and counted, samples
 // with count > 1 (aggregated records) are kept exactly as partial entries in the spill region.
+// Counts 2 .. 2^16 - 1 (per-PC aggregated records, as CUPTI's PC-sampling API delivers them)
+// take the cold path but are added in the table too when their key is in its home bucket
+// (else an exact spill entry): a slot's counter then gains at most (samples of the CTA between
+// flushes) + (counts above 1 since the last flush); the second term is kept below
+// OW_EXTRA_FLUSH + the stages already in flight (4 x 2,048 x 65,535 < 2^30) by a flush request,
+// so a counter stays below 2^32 for fewer than 2^31 samples per CTA between flushes. The fast
+// path itself handles count == 1 only (a count test there cost 4 % of the kernel).
+constexpr uint32_t OW_MAX_HOT_COUNT = 65535u;
+constexpr uint32_t OW_EXTRA_FLUSH = 1u << 30;
 __device__ __forceinline__ bool own_hot(const uint4 q, uint32_t row_launch, uint32_t S) {
   return (q.x == row_launch) & ((q.z & 0xFFFFu) < S) & (q.w == 1u) & (q.y < (1u << 27) - 1u);
 }
@@ -414,7 +429,19 @@ __device__ __noinline__ void own_cold(const uint4 q, uint32_t seg_launch, const 
   const uint32_t stall = q.z & 0xFFFFu;
   const bool ok = (q.x == seg_launch) & (stall < a.S) & (q.w != 0) & (q.y < (1u << 27) - 1u) & ctx_ok & (q.x < a.n_launch);
   if (ok) {  // valid sample with count > 1
-    own_spill(sm, a, (q.y << 5) | stall, q.w, ctx);
+    const uint32_t key = (q.y << 5) | stall;
+    if (q.w <= OW_MAX_HOT_COUNT) {  // the table path, with the counts-above-1 budget
+      const uint32_t before = atomicAdd(&sm.extra, q.w - 1u);
+      if (before < OW_EXTRA_FLUSH && before + (q.w - 1u) >= OW_EXTRA_FLUSH) *(volatile uint32_t*)&sm.flush_req = 1u;
+      const uint32_t bb = own_bucket(key);
+      const uint4 v = ld_shared_v4_volatile(&sm.key[4 * bb]);
+      const uint32_t sl = bucket_slot(v, key, bb);
+      if (sl != OW_MISS) {
+        atomicAdd(&sm.cnt[sl], q.w);
+        return;
+      }
+    }
+    own_spill(sm, a, key, q.w, ctx);  // new / displaced key, or a count past 2^16
     return;
   }
   const uint32_t r = own_reject(q.x, stall, q.w, seg_launch, a.n_launch, a.S, ctx_ok, a.trace_flags);
@@ -443,6 +470,7 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) { DC_PDL_
       mbar_init(&sm.empty[s], OW_CONS_WARPS);
     }
     sm.distinct = 0;
+    sm.extra = 0;
     sm.flush_req = 0;
     sm.sp_word = 0;
     sm.sp_seg = 0;

@@ -475,3 +475,57 @@ def test_topk_ties_and_large_k(general, monkeypatch):
                 got = dc.dc_hotspots_topk(a["_ctx"], a["_cct"], view, 0, 0xFFFFFFFF, th, k)
                 exp = o.topk(view, 0, 0xFFFFFFFF, None, th, k)
                 assert got == [(int(e["id"]), int(e["value"]), float(e["fraction"])) for e in exp], (view, k, th)
+
+
+def test_config3s_stress_generic_schedule_vs_oracle():
+    """Config 3s (gen/stress.py): every launch its own context and the samples of 8 concurrent
+    launches interleaved (no per-launch offsets): the generic schedule, element by element
+    against the oracle on the same re-arranged trace."""
+    from gen import stress
+    p = gen.programs.config3(n_launch=3000, n_samples=3_000_000)
+    tr = stress.make_3s(gen.make_trace(p, n_records=3000, pc=True, n_launch=3000, bad_per_million=500))
+    a = gpu_run(tr.offsets.numpy(), keys=tr.keys.numpy(), metrics=tr.metrics.numpy(), samples=tr.samples.numpy(),
+                n_launch=tr.n_launch)
+    oids, _ = oracle.intern(tr.keys.numpy())
+    assert np.array_equal(a["ids"], oids)
+    ref = oracle_run(tr.offsets.numpy(), oids, tr.metrics.numpy(), p.n_metrics, tr.samples.numpy(), tr.n_launch).arrays()
+    assert_same(a, ref, ctx="config 3s")
+    assert len(np.unique(a["leaf"])) == 3000  # distinct contexts
+
+
+def test_config3_aggregated_counts_on_the_table_path(monkeypatch):
+    """Per-PC aggregated records (counts > 1, gen/stress.make_aggregated) go through the
+    context-owner table (counts < 2^16) and equal both the oracle and the raw-sample result."""
+    monkeypatch.setenv("DC_TEST_OWNER_STRICT", "1")
+    from gen import stress
+    p = gen.programs.config3(n_launch=2000, n_samples=4_000_000)
+    raw = gen.make_trace(p, n_records=2000, pc=True, n_launch=2000)
+    ag = stress.make_aggregated(raw)
+    assert int(ag.samples[:, 3].max()) > 1
+    kw = dict(keys=raw.keys.numpy(), metrics=raw.metrics.numpy(), n_launch=2000)
+    a = gpu_run(raw.offsets.numpy(), samples=ag.samples.numpy(), launch_off=ag.launch_off.numpy(), **kw)
+    b = gpu_run(raw.offsets.numpy(), samples=raw.samples.numpy(), launch_off=raw.launch_off.numpy(), **kw)
+    oids, _ = oracle.intern(raw.keys.numpy())
+    ref = oracle_run(raw.offsets.numpy(), oids, raw.metrics.numpy(), p.n_metrics, ag.samples.numpy(), 2000).arrays()
+    assert_same(a, ref, ctx="aggregated")
+    assert_same(a, b, ctx="aggregated vs raw")
+
+
+def test_owner_large_counts_extra_flush_budget(monkeypatch):
+    """2M records of one context with counts up to 65,535 (the table path) and above (spilled):
+    far more than 2^32 in total, so the counts-above-1 budget must force flushes before any
+    32-bit table counter could wrap."""
+    monkeypatch.setenv("DC_TEST_OWNER_STRICT", "1")
+    n = 2_000_000
+    rng = np.random.default_rng(5)
+    s = np.zeros(n, oracle.SAMPLE_DTYPE)
+    s["launch"] = 0
+    s["pc_off"] = 16 * rng.integers(0, 40, n)
+    s["stall"] = rng.integers(0, 24, n)
+    s["count"] = np.where(rng.random(n) < 0.01, rng.integers(65_536, 2**31, n), rng.integers(60_000, 65_536, n))
+    off, fr = _csr([(0, 1)])
+    X = np.ones((1, 1), np.uint64)
+    a = gpu_run(off, fr, X, n_frames=2, samples=s, launch_off=np.array([0, n], np.uint64), n_stall=24)
+    ref = oracle_run(off, fr, X, 1, s, 1, 24).arrays()
+    assert_same(a, ref, ctx="large counts")
+    assert int(ref["bin_count"].sum()) > 2**40
