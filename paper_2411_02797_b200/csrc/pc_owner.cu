@@ -78,8 +78,11 @@ struct OwnSmem {
   uint32_t sp_word, sp_seg, sp_lock;  // sp_seg: entries of the current chunk already in a segment
   unsigned long long sp_base[OW_SP_RING];
   uint32_t warp_cnt[OW_CONS_WARPS];
+  uint32_t warp_mx[OW_CONS_WARPS], warp_or[OW_CONS_WARPS];  // flush: per-warp key range of the segment
+  uint32_t seg_si;
   unsigned long long seg_base;
 };
+static_assert(sizeof(OwnSmem) <= 232448, "k_pc_owner shared memory past the 227 KB opt-in limit");
 
 __device__ __forceinline__ void cons_sync() { asm volatile("bar.sync 1, %0;" ::"n"(OW_CONS) : "memory"); }
 
@@ -212,6 +215,7 @@ struct OwnArgs {
   unsigned long long* pcnt;    //                  count
   uint64_t cap_entries;
   uint4* seg;                  // {ctx, n, base_lo, base_hi}
+  uint2* seg_meta;             // per segment {max key + 1, OR of pc_off}: table flushes; {~0, 0} = unknown (spills)
   uint32_t cap_segs;
   unsigned long long* g_entries;
   unsigned int* g_segs;
@@ -236,6 +240,7 @@ __device__ __forceinline__ void own_flush(OwnSmem& sm, const OwnArgs& a, uint32_
       const unsigned si = atomicAdd(a.g_segs, 1u);
       if (si < a.cap_segs && base + n <= a.cap_entries) {
         a.seg[si] = make_uint4(ctx, n, (uint32_t)base, (uint32_t)(base >> 32));
+        sm.seg_si = si;
       } else {
         atomicOr(a.g_flags, (uint32_t)OWF_OVERFLOW);
         base = ~0ull;
@@ -248,17 +253,43 @@ __device__ __forceinline__ void own_flush(OwnSmem& sm, const OwnArgs& a, uint32_
     if (sp_hi > sm.sp_seg) {
       const uint64_t sb = sm.sp_base[(wv >> 20) % OW_SP_RING] + sm.sp_seg;
       const unsigned si2 = atomicAdd(a.g_segs, 1u);
-      if (si2 < a.cap_segs) a.seg[si2] = make_uint4(ctx, sp_hi - sm.sp_seg, (uint32_t)sb, (uint32_t)(sb >> 32));
-      else atomicOr(a.g_flags, (uint32_t)OWF_OVERFLOW);
+      if (si2 < a.cap_segs) {
+        a.seg[si2] = make_uint4(ctx, sp_hi - sm.sp_seg, (uint32_t)sb, (uint32_t)(sb >> 32));
+        a.seg_meta[si2] = make_uint2(0xFFFFFFFFu, 0u);  // spill entries: range unknown
+      } else {
+        atomicOr(a.g_flags, (uint32_t)OWF_OVERFLOW);
+      }
       sm.sp_seg = sp_hi;
     }
   }
   constexpr uint32_t PER_WARP = (OW_TAB / 32 + OW_CONS_WARPS - 1) / OW_CONS_WARPS * 32;  // 416 slots, multiple of 32
   const uint32_t s_lo = w * PER_WARP, s_hi = min((uint32_t)OW_TAB, s_lo + PER_WARP);
-  uint32_t c = 0;
-  for (uint32_t s = s_lo + lane; s < s_hi; s += 32) c += __popc(__ballot_sync(0xffffffffu, sm.key[s] != EMPTY32));
-  if (lane == 0) sm.warp_cnt[w] = c;
+  uint32_t c = 0, mk = 0, orp = 0;
+  for (uint32_t s = s_lo + lane; s < s_hi; s += 32) {
+    const uint32_t k = sm.key[s];
+    const bool occ = k != EMPTY32;
+    c += __popc(__ballot_sync(0xffffffffu, occ));
+    if (occ) {
+      mk = max(mk, k + 1);
+      orp |= k >> 5;
+    }
+  }
+  mk = __reduce_max_sync(0xffffffffu, mk);
+  orp = __reduce_or_sync(0xffffffffu, orp);
+  if (lane == 0) {
+    sm.warp_cnt[w] = c;
+    sm.warp_mx[w] = mk;
+    sm.warp_or[w] = orp;
+  }
   cons_sync();
+  if (ctid == 0 && n > 0 && sm.seg_base != ~0ull) {  // the segment's key range (k_ctx_hist skips a pass)
+    uint32_t m2 = 0, o2 = 0;
+    for (int ww = 0; ww < OW_CONS_WARPS; ++ww) {
+      m2 = max(m2, sm.warp_mx[ww]);
+      o2 |= sm.warp_or[ww];
+    }
+    a.seg_meta[sm.seg_si] = make_uint2(m2, o2);
+  }
   const unsigned long long base = sm.seg_base;
   uint32_t pos = 0;
   for (uint32_t ww = 0; ww < w; ++ww) pos += sm.warp_cnt[ww];
@@ -358,8 +389,12 @@ __device__ __noinline__ void own_spill(OwnSmem& sm, const OwnArgs& a, uint32_t k
         if (OW_SPILL_CAP > sm.sp_seg) {
           const uint64_t sb = cb + sm.sp_seg;
           const unsigned si = atomicAdd(a.g_segs, 1u);
-          if (si < a.cap_segs) a.seg[si] = make_uint4(ctx, OW_SPILL_CAP - sm.sp_seg, (uint32_t)sb, (uint32_t)(sb >> 32));
-          else atomicOr(a.g_flags, (uint32_t)OWF_OVERFLOW);
+          if (si < a.cap_segs) {
+            a.seg[si] = make_uint4(ctx, OW_SPILL_CAP - sm.sp_seg, (uint32_t)sb, (uint32_t)(sb >> 32));
+            a.seg_meta[si] = make_uint2(0xFFFFFFFFu, 0u);  // spill entries: range unknown
+          } else {
+            atomicOr(a.g_flags, (uint32_t)OWF_OVERFLOW);
+          }
         }
         const unsigned long long nb = atomicAdd(a.g_entries, (unsigned long long)OW_SPILL_CAP);
         if (nb + OW_SPILL_CAP > a.cap_entries) atomicOr(a.g_flags, (uint32_t)OWF_OVERFLOW);  // cannot happen
@@ -1034,6 +1069,7 @@ constexpr int CR_THREADS = 1024;
 constexpr uint32_t CR_WORDS = 8192;    // PCs per context (pc' range)
 constexpr uint32_t CR_BINS = 12288;    // bins per context counted in shared memory
 constexpr uint32_t CR_SEGS = 4096;     // segments per context
+constexpr uint32_t CR_USEGS = 1024;    // of which with an unknown key range (more: pass A walks all)
 constexpr uint32_t CR_ORDER_MAX = 8192;   // groups ordered by size (more: ascending order; static smem)
 enum { CR_WIDE = 1, CR_OVER = 2 };
 struct CtxRedSmem {
@@ -1044,7 +1080,8 @@ struct CtxRedSmem {
   uint32_t cnt_lo[CR_BINS], cnt_hi[CR_BINS];
   uint32_t wst_lo[CR_THREADS / 32][32], wst_hi[CR_THREADS / 32][32];  // per-warp stall totals
   uint32_t segs[CR_SEGS];
-  uint32_t nseg, g, maxk, orp;
+  uint32_t useg[CR_USEGS];  // segments whose key range is unknown (spill chunks): walked by pass A
+  uint32_t nseg, nuseg, g, maxk, orp;
   unsigned long long ow, ob;
 };
 struct __align__(16) CtxWord {  // scratch per bitmap word
@@ -1060,13 +1097,13 @@ struct __align__(16) CtxRec {  // scratch per group
 // latency per chunk instead of one per entry). fn(key, count) for every valid entry.
 constexpr uint32_t CR_U = 8;
 template <bool WITH_CNT, class F>
-__device__ __forceinline__ void cr_for_entries(const CtxRedSmem& sm, const uint4* __restrict__ seg, const uint32_t* __restrict__ pkey,
+__device__ __forceinline__ void cr_for_entries(const uint32_t* segs, const uint4* __restrict__ seg, const uint32_t* __restrict__ pkey,
                                                const unsigned long long* __restrict__ pcnt, uint32_t ns, F fn) {
   constexpr uint32_t CH = 32 * CR_U;
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   uint32_t kbase = 0;
   for (uint32_t q = 0; q < ns; ++q) {
-    const uint4 sg = seg[sm.segs[q]];
+    const uint4 sg = seg[segs[q]];
     const uint64_t base = (uint64_t)sg.z | ((uint64_t)sg.w << 32);
     const uint32_t nch = (sg.y + CH - 1) / CH;
     for (uint32_t ch = (w + 32 - kbase % 32) % 32; ch < nch; ch += 32) {
@@ -1128,7 +1165,7 @@ __global__ void __launch_bounds__(1024) k_ctx_order(const uint4* __restrict__ se
 }
 
 __global__ void __launch_bounds__(CR_THREADS, 1) k_ctx_hist(
-    const uint4* __restrict__ seg, const unsigned int* __restrict__ d_nsegs, uint32_t cap_segs, const uint32_t* __restrict__ pkey,
+    const uint4* __restrict__ seg, const uint2* __restrict__ seg_meta, const unsigned int* __restrict__ d_nsegs, uint32_t cap_segs, const uint32_t* __restrict__ pkey,
     const unsigned long long* __restrict__ pcnt, const uint64_t* __restrict__ lkey, const uint32_t* __restrict__ gfirst,
     const uint32_t* __restrict__ d_ng, const uint32_t* __restrict__ order, uint64_t N, uint32_t S, const uint32_t* __restrict__ g_flags,
     unsigned long long* __restrict__ ctl,  // [0] ticket, [1] status, [2] scratch words used, [3] scratch bins used
@@ -1145,6 +1182,7 @@ __global__ void __launch_bounds__(CR_THREADS, 1) k_ctx_hist(
       const uint32_t t = (uint32_t)atomicAdd(ctl, 1ull);
       sm.g = t < NG ? order[t] : 0xFFFFFFFFu;
       sm.nseg = 0;
+      sm.nuseg = 0;
       sm.maxk = 0;
       sm.orp = 0;
       sm.ow = 0;
@@ -1176,13 +1214,32 @@ __global__ void __launch_bounds__(CR_THREADS, 1) k_ctx_hist(
           }
       }
       __syncthreads();
-      // pass A: key range (max key + 1, OR of the PCs)
+      // pass A: key range (max key + 1, OR of the PCs). A table-flush segment carries it
+      // (seg_meta, written by k_pc_owner's flush); only the spill segments' entries are walked
       uint32_t mk = 0, orp = 0;
       ns = min(sm.nseg, CR_SEGS);
-      cr_for_entries<false>(sm, seg, pkey, pcnt, ns, [&](uint32_t kk, unsigned long long) {
-        mk = max(mk, kk + 1);
-        orp |= kk >> 5;
-      });
+      for (uint32_t q = tid; q < ns; q += CR_THREADS) {
+        const uint2 m = __ldcg(seg_meta + sm.segs[q]);
+        if (m.x == 0xFFFFFFFFu) {
+          const uint32_t u = atomicAdd(&sm.nuseg, 1u);
+          if (u < CR_USEGS) sm.useg[u] = sm.segs[q];
+        } else {
+          mk = max(mk, m.x);
+          orp |= m.y;
+        }
+      }
+      __syncthreads();
+      if (sm.nuseg > CR_USEGS) {  // too many spill segments to list: walk every segment
+        cr_for_entries<false>(sm.segs, seg, pkey, pcnt, ns, [&](uint32_t kk, unsigned long long) {
+          mk = max(mk, kk + 1);
+          orp |= kk >> 5;
+        });
+      } else if (sm.nuseg) {
+        cr_for_entries<false>(sm.useg, seg, pkey, pcnt, sm.nuseg, [&](uint32_t kk, unsigned long long) {
+          mk = max(mk, kk + 1);
+          orp |= kk >> 5;
+        });
+      }
       mk = __reduce_max_sync(0xffffffffu, mk);
       orp = __reduce_or_sync(0xffffffffu, orp);
       if (lane == 0) {
@@ -1201,7 +1258,7 @@ __global__ void __launch_bounds__(CR_THREADS, 1) k_ctx_hist(
       // pass B: presence bits
       for (uint32_t w = tid; w < W; w += CR_THREADS) sm.bm[w] = 0;
       __syncthreads();
-      cr_for_entries<false>(sm, seg, pkey, pcnt, ns, [&](uint32_t kk, unsigned long long) {
+      cr_for_entries<false>(sm.segs, seg, pkey, pcnt, ns, [&](uint32_t kk, unsigned long long) {
         atomicOr(&sm.bm[(kk >> 5) >> sh], 1u << (kk & 31u));
       });
       __syncthreads();
@@ -1256,7 +1313,7 @@ __global__ void __launch_bounds__(CR_THREADS, 1) k_ctx_hist(
     __syncthreads();
     if (ok) {
       // pass C: counts into their bins; per-stall totals
-      cr_for_entries<true>(sm, seg, pkey, pcnt, ns, [&](uint32_t kk, unsigned long long cv) {
+      cr_for_entries<true>(sm.segs, seg, pkey, pcnt, ns, [&](uint32_t kk, unsigned long long cv) {
         const uint32_t w = (kk >> 5) >> sh, b = kk & 31u;
         const uint32_t r = sm.bpre[w] + __popc(sm.bm[w] & ((1u << b) - 1u));
         const uint32_t lo = (uint32_t)cv, hi = (uint32_t)(cv >> 32);
@@ -1790,6 +1847,7 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
   uint64_t hw[2] = {0, 0};
   Buf<unsigned long long> pcnt;
   Buf<uint4> seg;
+  Buf<uint2> seg_meta;
   uint64_t hc[2];
   uint32_t hf[2];
   {
@@ -1797,6 +1855,7 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
     DC_TRY(alloc(c, pkey, cap_entries + (uint64_t)G * OW_SPILL_CAP));
     DC_TRY(alloc(c, pcnt, cap_entries + (uint64_t)G * OW_SPILL_CAP));
     DC_TRY(alloc(c, seg, cap_segs));
+    DC_TRY(alloc(c, seg_meta, cap_segs));
     OwnArgs a;
     a.smp = s;
     a.rowpos = rowpos.p;
@@ -1814,6 +1873,7 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
     a.pcnt = pcnt.p;
     a.cap_entries = cap_entries;
     a.seg = seg.p;
+    a.seg_meta = seg_meta.p;
     a.cap_segs = cap_segs;
     a.g_entries = ctr.p;
     a.g_segs = (unsigned int*)(ctr.p + 1);
@@ -1919,7 +1979,7 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
         Region rk(c, "k:ctx_hist");
         // groups past NG keep zero (bins, pcs) for the scan over the n_launch bound: k_ctx_hist
         // writes every group < NG; the rest are cleared with the counters
-        dc_launch(k_ctx_hist, G, CR_THREADS, csmem, c->stream, seg.p, a.g_segs, cap_segs, pkey.p, pcnt.p, lkey_out, gfirst.p,
+        dc_launch(k_ctx_hist, G, CR_THREADS, csmem, c->stream, seg.p, seg_meta.p, a.g_segs, cap_segs, pkey.p, pcnt.p, lkey_out, gfirst.p,
                   gx.p + n_launch, order.p, N, S, flags.p, ctl.p, wscr.p, wcap, bscr.p, bcap, rec.p, gn, gn + n_launch + 1,
                   (unsigned long long*)t->xsamples, (unsigned long long*)t->xstall);
         DC_LAUNCHED(c);
