@@ -10,7 +10,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "libdc.so")
+SO_PATH = os.environ.get("DC_SO_OVERRIDE") or os.path.join(_HERE, "libdc.so")  # override: A/B builds only
 
 P = ctypes.c_void_p
 u8, u16, u32, u64, i32, f64 = ctypes.c_uint8, ctypes.c_uint16, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int, ctypes.c_double

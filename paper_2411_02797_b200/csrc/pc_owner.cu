@@ -197,6 +197,33 @@ __global__ void k_plan_rows(const uint64_t* __restrict__ E, const uint32_t* __re
   }
 }
 
+// Per stage, the TMA pieces the producer issues, precomputed so the producer warp does no
+// dependent loads per stage: 4 x uint4 = {ctx, pieces, first launch, 0} and up to OW_DPIECES
+// pieces {source sample lo, hi, samples, destination sample in the stage}. A stage with more
+// pieces (more than OW_DPIECES launches) keeps its count and is cut by the producer itself.
+constexpr uint32_t OW_DPIECES = 3;
+__global__ void k_plan_pieces(const uint64_t* __restrict__ rowpos, const uint64_t* __restrict__ lsrc, const uint64_t* __restrict__ lcnt,
+                              const uint32_t* __restrict__ st_first, const uint32_t* __restrict__ st_ctx,
+                              const uint64_t* __restrict__ st_total, uint64_t n_launch, uint4* __restrict__ desc) { DC_PDL_ENTER();
+  const uint64_t ST = *st_total;
+  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < ST; s += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t R0 = OW_ROWS * s, R1 = R0 + OW_ROWS;
+    const uint32_t f = st_first[s];
+    uint32_t np = 0;
+    for (uint64_t li = f; li < n_launch; ++li) {
+      const uint64_t rp = rowpos[li], cnt = lcnt[li], rows = (cnt + 31) / 32;
+      if (rp >= R1) break;
+      if (rows == 0 || rp + rows <= R0) continue;
+      const uint64_t r_lo = rp > R0 ? rp : R0, r_hi = rp + rows < R1 ? rp + rows : R1;
+      const uint64_t lo = 32 * (r_lo - rp), hi = 32 * (r_hi - rp) < cnt ? 32 * (r_hi - rp) : cnt;
+      const uint64_t src = lsrc[li] + lo;
+      if (np < OW_DPIECES) desc[4 * s + 1 + np] = make_uint4((uint32_t)src, (uint32_t)(src >> 32), (uint32_t)(hi - lo), (uint32_t)(32 * (r_lo - R0)));
+      ++np;
+    }
+    desc[4 * s] = make_uint4(st_ctx[s], np, f, 0u);
+  }
+}
+
 // ---------------------------------------------------------------- main kernel
 struct OwnArgs {
   const dc_pc_sample* smp;
@@ -205,6 +232,7 @@ struct OwnArgs {
   const uint64_t* lsrc;
   const uint64_t* lcnt;
   const uint32_t* st_first;    // per stage: first launch, context
+  const uint4* desc;           // per stage: TMA pieces (k_plan_pieces)
   const uint32_t* st_ctx;
   const uint32_t* row_launch;  // per row: launch id, valid samples
   const uint8_t* row_valid;
@@ -589,47 +617,26 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) { DC_PDL_
         }
       }
     };
-    // software pipeline over the stage stream: stage A is issued now, B's launch fields and C's
-    // first-launch / context words are in flight (one iteration of latency hidden each)
-    uint64_t sA = next_stage(), sB = sA != ~0ull ? next_stage() : ~0ull;
-    uint32_t fA = 0, cA = 0, fB = 0, cB = 0;
-    if (sA != ~0ull) {
-      fA = a.st_first[sA];
-      cA = a.st_ctx[sA];
-    }
-    if (sB != ~0ull) {
-      fB = a.st_first[sB];
-      cB = a.st_ctx[sB];
-    }
-    uint64_t x_rp = ~0ull, x_src = 0, x_cnt = 0;
-    auto load_launch = [&](uint32_t f) {
-      const uint64_t li = (uint64_t)f + lane;
-      x_rp = ~0ull;
-      if (li < a.n_launch) {
-        x_rp = a.rowpos[li];
-        x_src = a.lsrc[li];
-        x_cnt = a.lcnt[li];
-      }
+    // software pipeline over the stage stream: stage A is issued now, the piece descriptors of
+    // B and C are in flight (lane j < 4 holds uint4 j of a stage's descriptor)
+    auto load_desc = [&](uint64_t sx) {
+      uint4 d = make_uint4(0, 0, 0, 0);
+      if (sx != ~0ull && lane < 4) d = a.desc[4 * sx + lane];
+      return d;
     };
-    if (sA != ~0ull) load_launch(fA);
+    uint64_t sA = next_stage(), sB = sA != ~0ull ? next_stage() : ~0ull;
+    uint4 dA = load_desc(sA), dB = load_desc(sB);
     while (sA != ~0ull) {
       const long long pc0 = prof ? clock64() : 0;
       const uint64_t s = sA;
-      const uint32_t ctx = cA, f = fA;
-      uint64_t rp = x_rp, src = x_src, cnt = x_cnt;
+      const uint4 d = dA;
       const uint64_t sC = sB != ~0ull ? next_stage() : ~0ull;
-      uint32_t fC = 0, cC = 0;
-      if (sC != ~0ull) {
-        fC = a.st_first[sC];
-        cC = a.st_ctx[sC];
-      }
-      if (sB != ~0ull) load_launch(fB);
+      const uint4 dC = load_desc(sC);
       sA = sB;
-      fA = fB;
-      cA = cB;
+      dA = dB;
       sB = sC;
-      fB = fC;
-      cB = cC;
+      dB = dC;
+      const uint32_t ctx = __shfl_sync(0xffffffffu, d.x, 0), npc = __shfl_sync(0xffffffffu, d.y, 0);
       if (lane == 0) mbar_wait(&sm.empty[st], ph ^ 1u);  // the slot (and its meta) is free
       __syncwarp();
       const long long pc1 = prof ? clock64() : 0;
@@ -644,38 +651,47 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) { DC_PDL_
         sm.meta[st].flush = flush;
       }
       uint32_t npieces = 0;
-      for (uint64_t base = f;; base += 32) {  // launches of this stage, 32 at a time (one batch normally)
-        if (base != f) {  // rare: a stage with more than 32 launches
+      if (npc <= OW_DPIECES) {  // precomputed pieces: lane j in [1, npc] issues piece j - 1
+        const bool in = lane >= 1 && lane <= npc;
+        const uint32_t bytes = __reduce_add_sync(0xffffffffu, in ? d.z * 16u : 0u);
+        // expect_tx before the arrive (below) keeps the phase open however early a copy lands
+        if (lane == 0 && bytes)
+          asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&sm.full[st])), "r"(bytes) : "memory");
+        __syncwarp();
+        if (in) tma_bulk_g2s(&sm.stage[st][d.w], a.smp + (((uint64_t)d.y << 32) | d.x), d.z * 16u, &sm.full[st]);
+        npieces = npc;
+      } else {  // rare: a stage with more than OW_DPIECES launches, cut here 32 launches at a time
+        const uint32_t f = __shfl_sync(0xffffffffu, d.z, 0);
+        for (uint64_t base = f;; base += 32) {
           const uint64_t li = base + lane;
-          rp = ~0ull;
+          uint64_t rp = ~0ull, src = 0, cnt = 0;
           if (li < a.n_launch) {
             rp = a.rowpos[li];
             src = a.lsrc[li];
             cnt = a.lcnt[li];
           }
+          const uint64_t rows = (cnt + 31) / 32;
+          const bool in = rp != ~0ull && rp < R1 && rp + rows > R0 && rows > 0;
+          uint64_t lo = 0, len = 0, dst = 0;
+          if (in) {
+            const uint64_t r_lo = rp > R0 ? rp : R0;
+            const uint64_t r_hi = rp + rows < R1 ? rp + rows : R1;
+            lo = 32 * (r_lo - rp);
+            const uint64_t hi = 32 * (r_hi - rp) < cnt ? 32 * (r_hi - rp) : cnt;
+            len = hi - lo;
+            dst = 32 * (r_lo - R0);
+          }
+          const uint32_t bytes = __reduce_add_sync(0xffffffffu, (uint32_t)len * 16u);
+          const uint32_t m = __ballot_sync(0xffffffffu, in);
+          if (lane == 0 && bytes)
+            asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&sm.full[st])), "r"(bytes) : "memory");
+          __syncwarp();
+          if (in) tma_bulk_g2s(&sm.stage[st][dst], a.smp + src + lo, (uint32_t)len * 16u, &sm.full[st]);
+          npieces += __popc(m);
+          // the batch's last launch ends inside the stage: more launches may follow
+          const bool more = (rp != ~0ull) & (rp + rows < R1) & (base + 32 < a.n_launch);
+          if (!__shfl_sync(0xffffffffu, more, 31)) break;
         }
-        const uint64_t rows = (cnt + 31) / 32;
-        const bool in = rp != ~0ull && rp < R1 && rp + rows > R0 && rows > 0;
-        uint64_t lo = 0, len = 0, dst = 0;
-        if (in) {
-          const uint64_t r_lo = rp > R0 ? rp : R0;
-          const uint64_t r_hi = rp + rows < R1 ? rp + rows : R1;
-          lo = 32 * (r_lo - rp);
-          const uint64_t hi = 32 * (r_hi - rp) < cnt ? 32 * (r_hi - rp) : cnt;
-          len = hi - lo;
-          dst = 32 * (r_lo - R0);
-        }
-        const uint32_t bytes = __reduce_add_sync(0xffffffffu, (uint32_t)len * 16u);
-        const uint32_t m = __ballot_sync(0xffffffffu, in);
-        // expect_tx before the arrive (below) keeps the phase open however early a copy lands
-        if (lane == 0 && bytes)
-          asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&sm.full[st])), "r"(bytes) : "memory");
-        __syncwarp();
-        if (in) tma_bulk_g2s(&sm.stage[st][dst], a.smp + src + lo, (uint32_t)len * 16u, &sm.full[st]);
-        npieces += __popc(m);
-        // the batch's last launch ends inside the stage: more launches may follow
-        const bool more = (rp != ~0ull) & (rp + rows < R1) & (base + 32 < a.n_launch);
-        if (!__shfl_sync(0xffffffffu, more, 31)) break;
       }
       if (lane == 0) {  // row meta; the arrive releases the ctx / flush words written above
         mbar_expect_tx(&sm.full[st], (uint32_t)(OW_ROWS * 5));
@@ -1762,6 +1778,7 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
   // stage plan
   Buf<uint64_t> lrow, lsrc, lcnt, gst, rowpos, tot;
   Buf<uint32_t> lflag, gx, gfirst, row_launch, st_first, st_ctx;
+  Buf<uint4> desc;
   Buf<uint8_t> row_valid;
   // rows: sum ceil(cnt/32) <= n/32 + n_launch; context padding < OW_ROWS rows per context (<= n_launch)
   const uint64_t st_cap = (n / 32 + n_launch + OW_ROWS - 1) / OW_ROWS + n_launch + 1;
@@ -1835,6 +1852,10 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
                                                                        n_launch, row_cap, rowpos.p, row_launch.p,
                                                                        row_valid.p, st_first.p, st_ctx.p);
     DC_LAUNCHED(c);
+    DC_TRY(alloc(c, desc, 4 * st_cap));
+    dc_launch(k_plan_pieces, grid_for(c, st_cap, 256), 256, 0, c->stream, rowpos.p, lsrc.p, lcnt.p, st_first.p, st_ctx.p, tot.p,
+              n_launch, desc.p);
+    DC_LAUNCHED(c);
   }
   // partial outputs
   // entry pool: table flushes + spill chunks after each CTA's first (at most n entries, plus a
@@ -1862,6 +1883,7 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
     a.lsrc = lsrc.p;
     a.lcnt = lcnt.p;
     a.st_first = st_first.p;
+    a.desc = desc.p;
     a.st_ctx = st_ctx.p;
     a.row_launch = row_launch.p;
     a.row_valid = row_valid.p;
