@@ -50,7 +50,14 @@ constexpr uint32_t PT_FW = 8192;    // staged frame window per stage (32 KB): 2 
 // the chunk boundaries — different chunkings would give one path two hashes (two items).
 constexpr uint32_t PT_CH = 17;
 constexpr uint32_t PT_NONE = 0xFFFFFFFFu;
-constexpr int PG_U = 4;             // k_path_group: records verified per round
+constexpr int PG_U = 4;             // k_path_group: records verified per round (per-record verify)
+#ifndef DC_PG_W
+#define DC_PG_W 8
+#endif
+#ifndef DC_PG_MINB
+#define DC_PG_MINB 4
+#endif
+constexpr int PG_W = DC_PG_W;       // k_path_group: 32-frame windows per round (sweep verify)
 
 struct __align__(32) PathSlot {
   unsigned long long key;  // record hash, ~0 = empty
@@ -263,22 +270,26 @@ __global__ void __launch_bounds__(PT_THREADS) k_path_hash(const uint64_t* __rest
 
 // lane i: record r0 + i into the table; then the warp verifies each record against its
 // representative frame by frame
-__global__ void __launch_bounds__(256) k_path_group(const uint64_t* __restrict__ off, const uint32_t* __restrict__ frames,
+constexpr uint64_t PG_SKIP = 0x8000000000000000ull;  // k_path_group sweep: rank not verified
+template <bool SWEEP>
+__global__ void __launch_bounds__(256, DC_PG_MINB) k_path_group(const uint64_t* __restrict__ off, const uint32_t* __restrict__ frames,
                                                     const uint64_t* __restrict__ hash, uint64_t R, PathSlot* __restrict__ tab,
                                                     uint64_t mask, uint32_t* __restrict__ slot_of_rec,
                                                     uint32_t* __restrict__ extra_rec, unsigned int* __restrict__ d_cnt) { DC_PDL_WAIT();
+  __shared__ unsigned long long s_delta[8][32];  // per warp (256 threads): rep start - own start by nonempty rank
   const uint32_t lane = lane_id();
+  unsigned long long* const sdelta = s_delta[(threadIdx.x >> 5) & 7];
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t r0 = warp * 32; r0 < R; r0 += nw * 32) {
     const uint64_t r = r0 + lane;
     const bool act = r < R;
-    uint64_t o = 0, ro = 0;
+    uint64_t o = 0, ro = 0, o1 = 0;
     uint32_t L = 0, sl = PT_NONE, need = 0;
     bool mine = false;
     if (act) {
       o = off[r];
-      const uint64_t o1 = off[r + 1];
+      o1 = off[r + 1];
       L = (uint32_t)(o1 >= o ? min(o1 - o, (uint64_t)DC_MAX_DEPTH) : 0);  // validated by k_path_hash
       const uint64_t H = hash[r];
       uint64_t q = (H * 0x9E3779B97F4A7C15ull >> 17) & mask;
@@ -318,9 +329,58 @@ __global__ void __launch_bounds__(256) k_path_group(const uint64_t* __restrict__
       const uint32_t rl = tab[sl].len;
       need = rl != L ? 2u : (L ? 1u : 0u);
     }
-    // verify, 8 records at a time: their first 64 frames on both sides are loaded before any
-    // compare, so the DRAM latency of the own frames is paid once per group
     uint32_t todo = __ballot_sync(0xffffffffu, need == 1u);
+    // Sweep verify: the 32 records' frames are one contiguous range [Fb, Fe) (checked: every
+    // record ends where the next begins, no clamped length). The warp walks it in aligned
+    // 32-frame windows, one frame per lane (own frames: one 128-B line per load); a lane finds
+    // its frame's record by the rank of the nonempty record starts up to its position (warp OR of
+    // the starts falling in the window, popc), reads that record's rep - own delta from shared
+    // memory and compares the frame with the representative's frame at the same position.
+    if (SWEEP && todo && __all_sync(0xffffffffu, !act || o1 == o + L)) {
+      const bool nz = act && L > 0;
+      const uint32_t NZ = __ballot_sync(0xffffffffu, nz);
+      const uint32_t rk = __popc(NZ & lanemask_lt());
+      if (nz) sdelta[rk] = need == 1u ? ro - o : PG_SKIP;
+      __syncwarp();
+      const uint64_t Fb = __shfl_sync(0xffffffffu, o, 0);
+      const uint32_t last = 31 - __clz(__ballot_sync(0xffffffffu, act));
+      const uint32_t span = (uint32_t)(__shfl_sync(0xffffffffu, o + L, last) - Fb);  // <= 32 * DC_MAX_DEPTH
+      const uint32_t orel = (uint32_t)(o - Fb);
+      const uint32_t* const own = frames + Fb;
+      const uint32_t le = lanemask_lt() | (1u << lane);
+      uint32_t before = 0, badm = 0;
+      // PG_W windows per round: every window's rank and delta first, then all loads, then the
+      // compares (the own frames' DRAM latency is paid once per round, not once per window)
+      for (uint32_t wb0 = 0; wb0 < span; wb0 += 32 * PG_W) {
+        uint32_t cr[PG_W], a[PG_W], b[PG_W];
+        uint64_t dd[PG_W];
+#pragma unroll
+        for (int u = 0; u < PG_W; ++u) {
+          const uint32_t wb = wb0 + 32 * u;
+          const uint32_t sr = orel - wb;  // record start relative to the window (wraps if before)
+          const uint32_t M = __reduce_or_sync(0xffffffffu, nz && sr < 32u ? 1u << sr : 0u);
+          cr[u] = before + __popc(M & le) - 1;  // rank of my frame's record (nonempty starts at or before it, - 1)
+          before += __popc(M);
+          dd[u] = wb + lane < span ? sdelta[cr[u] & 31] : PG_SKIP;
+        }
+#pragma unroll
+        for (int u = 0; u < PG_W; ++u) {
+          const uint32_t pr = wb0 + 32 * u + lane;
+          const bool v = dd[u] != PG_SKIP;
+          a[u] = v ? ld_stream_u32(own + pr) : 0u;
+          b[u] = v ? __ldg(own + pr + dd[u]) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < PG_W; ++u)
+          if (a[u] != b[u]) badm |= 1u << (cr[u] & 31);
+      }
+      badm = __reduce_or_sync(0xffffffffu, badm);
+      if (nz && need == 1u && ((badm >> rk) & 1u)) need = 2u;
+      __syncwarp();  // sdelta reused by the next group
+      todo = 0;
+    }
+    // verify, PG_U records at a time: their first 64 frames on both sides are loaded before any
+    // compare, so the DRAM latency of the own frames is paid once per group
     while (todo) {
       int idx[PG_U];
       uint64_t oo[PG_U], rr[PG_U];
@@ -1306,7 +1366,8 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
     }
     if (R) {
       Region rk(c, "k:path_group");
-      dc_launch(k_path_group, grid_for(c, (R + 31) / 32 * 32, 256), 256, 0, c->stream, p->offsets, p->frames, hash.p, R, tab.p,
+      static const bool pg_rows = getenv("DC_PG_ROWS") != nullptr;  // A/B: the per-record verify
+      dc_launch(pg_rows ? k_path_group<false> : k_path_group<true>, grid_for(c, (R + 31) / 32 * 32, 256), 256, 0, c->stream, p->offsets, p->frames, hash.p, R, tab.p,
                                                                                 cap - 1, slot_of_rec.p, extra_rec.p, cnt.p);
       DC_LAUNCHED(c);
     }
