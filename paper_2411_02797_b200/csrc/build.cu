@@ -41,14 +41,27 @@ __device__ __forceinline__ int bits_for_dev(uint32_t v) { return v ? 32 - __clz(
 //     (coalesced on both sides). A mismatch (a hash collision) makes the record a
 //     representative of its own, so the dedup is exact whatever the hash.
 constexpr int PT_T = 128;           // records per tile (96 with a 24 KB window: 13.4 ms vs 11.0 on config 4)
-constexpr int PT_THREADS = 256;
+#ifndef DC_PT_THREADS
+#define DC_PT_THREADS 256
+#endif
+constexpr int PT_THREADS = DC_PT_THREADS;
 constexpr int PT_WARPS = PT_THREADS / 32;
 constexpr int PT_RPW = PT_T / PT_WARPS;  // records per warp (16)
-constexpr uint32_t PT_FW = 8192;    // staged frame window per stage (32 KB): 2 CTAs per SM
+#ifndef DC_PT_ST
+#define DC_PT_ST 2
+#endif
+#ifndef DC_PT_FW
+#define DC_PT_FW 8192
+#endif
+constexpr int PT_ST = DC_PT_ST;     // k_path_hash stages (tiles in flight per CTA)
+constexpr uint32_t PT_FW = DC_PT_FW;  // staged frame window per stage (32 KB)
 // chunk length (odd: bank spread). The same for staged and global tiles: the high half of the
 // hash sums each chunk's high word, so the hash of a path is a function of its frames and of
 // the chunk boundaries — different chunkings would give one path two hashes (two items).
-constexpr uint32_t PT_CH = 17;
+#ifndef DC_PT_CH
+#define DC_PT_CH 17
+#endif
+constexpr uint32_t PT_CH = DC_PT_CH;
 constexpr uint32_t PT_NONE = 0xFFFFFFFFu;
 constexpr int PG_U = 4;             // k_path_group: records verified per round (per-record verify)
 #ifndef DC_PG_W
@@ -74,12 +87,12 @@ struct PathWarp {  // per warp: its 16 records of the tile
 };
 
 struct PathSmem {
-  uint32_t fr[2][PT_FW];
-  unsigned long long offs[2][PT_T + 2];
+  uint32_t fr[PT_ST][PT_FW];
+  unsigned long long offs[PT_ST][PT_T + 2];
   uint32_t pos[DC_MAX_DEPTH];
-  unsigned long long full[2];
-  unsigned long long meta_f0[2], meta_f1[2];
-  uint32_t meta_mode[2];
+  unsigned long long full[PT_ST];
+  unsigned long long meta_f0[PT_ST], meta_f1[PT_ST];
+  uint32_t meta_mode[PT_ST];
   PathWarp wp[PT_WARPS];
 };
 
@@ -147,8 +160,7 @@ __global__ void __launch_bounds__(PT_THREADS) k_path_hash(const uint64_t* __rest
     sm.pos[j] = (uint32_t)(m >> 32) | 0x80000001u;
   }
   if (tid == 0) {
-    mbar_init(&sm.full[0], 1);
-    mbar_init(&sm.full[1], 1);
+    for (int j = 0; j < PT_ST; ++j) mbar_init(&sm.full[j], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -178,25 +190,32 @@ __global__ void __launch_bounds__(PT_THREADS) k_path_hash(const uint64_t* __rest
       mbar_arrive(&sm.full[s]);
     }
   };
+  // tiles t, t + G, ... of this CTA go round PT_ST stages: tile k + PT_ST - 1 is issued at the
+  // top of iteration k into the stage that iteration k - 1 released (its closing barrier)
   uint64_t t = blockIdx.x, nf0 = 0, nf1 = 0;
   if (tid == 0) {
-    if (t < n_tiles) issue(t, 0, off[t * PT_T], off[min(R, t * PT_T + PT_T)]);
-    if (t + G < n_tiles) {
-      nf0 = off[(t + G) * PT_T];
-      nf1 = off[min(R, (t + G) * PT_T + PT_T)];
+    for (int j = 0; j < PT_ST - 1; ++j) {
+      const uint64_t tj = t + (uint64_t)j * G;
+      if (tj < n_tiles) issue(tj, j, off[tj * PT_T], off[min(R, tj * PT_T + PT_T)]);
+    }
+    const uint64_t tn = t + (uint64_t)(PT_ST - 1) * G;
+    if (tn < n_tiles) {
+      nf0 = off[tn * PT_T];
+      nf1 = off[min(R, tn * PT_T + PT_T)];
     }
   }
   for (uint32_t k = 0; t < n_tiles; ++k, t += G) {
-    const int s = k & 1;
+    const int s = (int)(k % PT_ST);
     if (tid == 0) {
-      if (t + G < n_tiles) issue(t + G, s ^ 1, nf0, nf1);  // offsets loaded one tile ago
-      const uint64_t t2 = t + 2 * G;
+      const uint64_t ti = t + (uint64_t)(PT_ST - 1) * G;
+      if (ti < n_tiles) issue(ti, (int)((k + PT_ST - 1) % PT_ST), nf0, nf1);  // offsets loaded one tile ago
+      const uint64_t t2 = t + (uint64_t)PT_ST * G;
       if (t2 < n_tiles) {
         nf0 = off[t2 * PT_T];
         nf1 = off[min(R, t2 * PT_T + PT_T)];
       }
     }
-    mbar_wait(&sm.full[s], (k >> 1) & 1u);
+    mbar_wait(&sm.full[s], (k / PT_ST) & 1u);
     const uint64_t r0 = t * PT_T;
     const uint32_t n = (uint32_t)min((uint64_t)PT_T, R - r0);
     const uint32_t mode = sm.meta_mode[s];

@@ -33,6 +33,12 @@ namespace dc {
 constexpr int OW_CONS_WARPS = 16;
 constexpr int OW_CONS = 32 * OW_CONS_WARPS;   // 512 consumer threads
 constexpr int OW_THREADS = OW_CONS + 32;      // + producer warp
+#ifndef DC_OW_NOBR
+#define DC_OW_NOBR 1  // branch-free hit / miss bookkeeping: 0.449 -> 0.435 ms (same-box A/B)
+#endif
+#ifndef DC_OW_HINT
+#define DC_OW_HINT 0  // preferred-slot lookup (A/B builds)
+#endif
 #ifndef DC_OW_STAGES
 #define DC_OW_STAGES 4
 #endif
@@ -70,8 +76,8 @@ struct __align__(16) OwMeta {
 struct OwnSmem {
   uint4 stage[OW_STAGES][OW_STAGE];
   uint32_t key[OW_TAB];
-  uint32_t cnt[OW_TAB];
-  uint32_t pend[OW_CONS_WARPS][OW_PEND];
+  uint32_t cnt[OW_TAB + OW_CONS_WARPS];  // + one dummy counter per consumer warp (never read)
+  uint32_t pend[OW_CONS_WARPS][OW_PEND + 1];  // + a dummy tail slot (never read)
   unsigned long long full[OW_STAGES], empty[OW_STAGES];
   OwMeta meta[OW_STAGES];
   uint32_t distinct;
@@ -353,6 +359,9 @@ __device__ __forceinline__ void own_flush(OwnSmem& sm, const OwnArgs& a, uint32_
 // bucket, so a key displaced from its home slot usually still costs a single load.
 constexpr uint32_t OW_NB = OW_TAB / 4;
 __device__ __forceinline__ uint32_t own_bucket(uint32_t key) { return __umulhi(key * 0x9E3779B1u, OW_NB); }
+// preferred slot of a key within its home bucket (independent bits): new keys take it when it is
+// free, so most lookups settle with one 4-B load of that slot instead of a 16-B bucket load
+__device__ __forceinline__ uint32_t own_hint(uint32_t key) { return (key * 0x27D4EB2Fu) >> 30; }
 __device__ __forceinline__ int bucket_match(const uint4 v, uint32_t key) {
   return v.x == key ? 0 : v.y == key ? 1 : v.z == key ? 2 : v.w == key ? 3 : -1;
 }
@@ -394,6 +403,15 @@ uint32_t own_probe(OwnSmem& sm, uint32_t key, uint32_t b) {
     uint32_t empt = (v.x == EMPTY32 ? 1u : 0u) | (v.y == EMPTY32 ? 2u : 0u) | (v.z == EMPTY32 ? 4u : 0u) |
                     (v.w == EMPTY32 ? 8u : 0u);
     if (empt && full) return OW_TAB;
+    if (DC_OW_HINT && walked == 0) {  // home bucket: the key's preferred slot first
+      const uint32_t hq = own_hint(key);
+      if ((empt >> hq) & 1u) {
+        const uint32_t old = atomicCAS(&sm.key[4 * b + hq], EMPTY32, key);
+        if (old == EMPTY32) return (4 * b + hq) | 0x80000000u;
+        if (old == key) return 4 * b + hq;
+        empt &= ~(1u << hq);
+      }
+    }
     while (empt) {
       const uint32_t q = __ffs(empt) - 1;
       empt &= empt - 1;
@@ -832,10 +850,26 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) { DC_PDL_
       const long long c_3 = MODE == 9 ? clock64() : 0;
 #pragma unroll
       for (int i = 0; i < OW_PER_LANE; ++i) b[i] = own_bucket(t[i]);
+      if (DC_OW_HINT) {  // the preferred slot (4-B load), then the whole bucket for the rest
+        uint32_t hs[OW_PER_LANE], k1[OW_PER_LANE];
 #pragma unroll
-      for (int i = 0; i < OW_PER_LANE; ++i) {
-        const uint4 v = *reinterpret_cast<const uint4*>(&sm.key[4 * b[i]]);  // home bucket
-        slot[i] = bucket_slot(v, t[i], b[i]);
+        for (int i = 0; i < OW_PER_LANE; ++i) hs[i] = 4 * b[i] + own_hint(t[i]);
+#pragma unroll
+        for (int i = 0; i < OW_PER_LANE; ++i) k1[i] = sm.key[hs[i]];
+#pragma unroll
+        for (int i = 0; i < OW_PER_LANE; ++i) {
+          slot[i] = hs[i];
+          if (k1[i] != t[i] && t[i] != EMPTY32) {
+            const uint4 v = *reinterpret_cast<const uint4*>(&sm.key[4 * b[i]]);  // home bucket
+            slot[i] = bucket_slot(v, t[i], b[i]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < OW_PER_LANE; ++i) {
+          const uint4 v = *reinterpret_cast<const uint4*>(&sm.key[4 * b[i]]);  // home bucket
+          slot[i] = bucket_slot(v, t[i], b[i]);
+        }
       }
       if (MODE == 9) t_bucket += clock64() - c_2;
       // Hits are added directly. Misses (new or displaced keys, a few % of the samples) are
@@ -845,10 +879,19 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) { DC_PDL_
 #pragma unroll
       for (int i = 0; i < OW_PER_LANE; ++i) {
         const bool miss = t[i] != EMPTY32 && slot[i] == OW_MISS;
-        red_shared_inc_if(&sm.cnt[slot[i] & 0x7FFFFFFFu], t[i] != EMPTY32 && !miss);  // hit: never the spill slot
-        const uint32_t mm = __ballot_sync(0xffffffffu, miss);
-        if (miss) sm.pend[w][np + __popc(mm & lanemask_lt())] = t[i];
-        np += __popc(mm);
+        if (DC_OW_NOBR) {  // branch-free: lanes without a hit add into the warp's dummy counter and
+                           // lanes without a miss store into the queue's dummy tail slot
+          const uint32_t cs = t[i] != EMPTY32 && !miss ? slot[i] : (uint32_t)OW_TAB + w;
+          asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(smem_u32(&sm.cnt[cs])) : "memory");
+          const uint32_t mm = __ballot_sync(0xffffffffu, miss);
+          sm.pend[w][miss ? np + __popc(mm & lanemask_lt()) : (uint32_t)OW_PEND] = t[i];
+          np += __popc(mm);
+        } else {
+          red_shared_inc_if(&sm.cnt[slot[i] & 0x7FFFFFFFu], t[i] != EMPTY32 && !miss);  // hit: never the spill slot
+          const uint32_t mm = __ballot_sync(0xffffffffu, miss);
+          if (miss) sm.pend[w][np + __popc(mm & lanemask_lt())] = t[i];
+          np += __popc(mm);
+        }
       }
       if (MODE == 3) np = 0;  // measurement only: misses dropped
       if (MODE == 9 && lane == 0) n_miss += np;
