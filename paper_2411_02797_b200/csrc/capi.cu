@@ -54,11 +54,33 @@ dc_status cuda_fail(Ctx* c, cudaError_t e, const char* what) {
   return fail(c, DC_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
+// Small readbacks: one kernel copies up to RB_MAX items straight into the context's pinned
+// buffer (device-accessible under unified addressing) instead of one DMA copy per item. The
+// kernel is part of the PDL chain (launched while its predecessor runs, waiting for it with
+// griddepcontrol.wait), so the readback costs no extra launch latency before the stream drains.
+constexpr int RB_MAX = 8;
+struct RbItems {
+  const unsigned char* src[RB_MAX];
+  uint32_t bytes[RB_MAX], off[RB_MAX];
+  uint32_t n;
+  unsigned char* dst;
+};
+__global__ void k_readback(RbItems it) { DC_PDL_ENTER();
+  for (uint32_t i = 0; i < it.n; ++i)
+    for (uint32_t b = threadIdx.x; b < it.bytes[i]; b += blockDim.x) it.dst[it.off[i] + b] = it.src[i][b];
+}
+
 dc_status readback(Ctx* c, const void* dev, size_t bytes, void* host) {
   if (bytes == 0) return DC_OK;
   HostRegion hr(c, "readback");
   if (bytes <= 4096) {
-    DC_CUDA(c, cudaMemcpyAsync(c->h_pinned, dev, bytes, cudaMemcpyDeviceToHost, c->stream));
+    RbItems it{};
+    it.src[0] = (const unsigned char*)dev;
+    it.bytes[0] = (uint32_t)bytes;
+    it.n = 1;
+    it.dst = (unsigned char*)c->h_pinned;
+    dc_launch(k_readback, 1, 256, 0, c->stream, it);
+    DC_LAUNCHED(c);
     DC_CUDA(c, cudaStreamSynchronize(c->stream));
     memcpy(host, c->h_pinned, bytes);
   } else {
@@ -71,10 +93,21 @@ dc_status readback(Ctx* c, const void* dev, size_t bytes, void* host) {
 dc_status readback_multi(Ctx* c, std::initializer_list<RB> items) {
   HostRegion hr(c, "readback");
   size_t o = 0;
+  RbItems rb{};
+  rb.dst = (unsigned char*)c->h_pinned;
   for (const RB& it : items) {
-    if (o + it.bytes > 4096) return fail(c, DC_ERR_ARG, "readback_multi: more than 4 KB");
-    if (it.bytes) DC_CUDA(c, cudaMemcpyAsync((char*)c->h_pinned + o, it.dev, it.bytes, cudaMemcpyDeviceToHost, c->stream));
+    if (o + it.bytes > 4096 || rb.n == RB_MAX) return fail(c, DC_ERR_ARG, "readback_multi: more than 4 KB or %d items", RB_MAX);
+    if (it.bytes) {
+      rb.src[rb.n] = (const unsigned char*)it.dev;
+      rb.bytes[rb.n] = (uint32_t)it.bytes;
+      rb.off[rb.n] = (uint32_t)o;
+      ++rb.n;
+    }
     o += (it.bytes + 7) & ~(size_t)7;
+  }
+  if (rb.n) {
+    dc_launch(k_readback, 1, 256, 0, c->stream, rb);
+    DC_LAUNCHED(c);
   }
   DC_CUDA(c, cudaStreamSynchronize(c->stream));
   o = 0;

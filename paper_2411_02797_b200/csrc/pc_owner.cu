@@ -543,7 +543,7 @@ __device__ __noinline__ void own_cold(const uint4 q, uint32_t seg_launch, const 
   k.fallback |= r == 3;
 }
 
-template <int MODE>  // 0 = the product; 1, 2, 3, 9 = measurement variants (DC_OWN_MODE)
+template <int MODE>  // 0 = the product; 1, 2, 3, 4, 9 = measurement variants (DC_OWN_MODE)
 __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) { DC_PDL_WAIT();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   OwnSmem& sm = *reinterpret_cast<OwnSmem*>(smem_raw);
@@ -671,7 +671,7 @@ __global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) { DC_PDL_
       const long long pc1 = prof ? clock64() : 0;
       const uint64_t R0 = OW_ROWS * s, R1 = R0 + OW_ROWS;
       if (lane == 0) {
-        uint32_t flush = ctx != prev_ctx ? 1u : 0u;
+        uint32_t flush = ctx != prev_ctx && MODE != 4 ? 1u : 0u;  // MODE 4 (measurement only): no context flushes
         if (*freq) {
           *freq = 0u;
           flush = 1u;
