@@ -1328,7 +1328,7 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
   const int fbits = bits_for(n_frames > 0 ? n_frames - 1 : 0) > 0 ? bits_for(n_frames - 1) : 1;
   if (dict) {
     DC_TRY(palloc(c, t->frame_kind, n_frames));
-    DC_CUDA(c, cudaMemcpyAsync(t->frame_kind, dict->kinds, n_frames, cudaMemcpyDeviceToDevice, c->stream));
+    DC_TRY(dcopy(c, t->frame_kind, dict->kinds, n_frames));
   }
   // ---- a2: hash pass (frames streamed once), then group + exact verification
   Buf<uint32_t> slot_of_rec, extra_rec, pid_of_slot, item_rec, item_len, leaf_of_item, leafbuf;
@@ -1489,7 +1489,11 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
   DC_TRY(palloc(c, t->xcnt, N));
   DC_TRY(palloc(c, t->icnt, N));
   // icnt is written whole by dc_cct_rollup (every schedule) and unreadable before it
-  DC_CUDA(c, cudaMemsetAsync(t->xcnt, 0, N * 8, c->stream));
+  {
+    FillList fx;
+    DC_TRY(fill_add(c, fx, t->xcnt, N * 8));
+    DC_TRY(fill_flush(c, fx));
+  }
   // algorithmic bytes: offsets + frames of every record once, leaf, node table
   c->bytes_host += 8 * (R + 1) + 4 * F + 4 * R + 10 * N;
   c->host_levels += t->max_depth;

@@ -259,6 +259,25 @@ dc_status fill_flush(Ctx* c, FillList& f) {
   return DC_OK;
 }
 
+// device-to-device copy as a kernel (stays in the PDL chain; a DMA copy between two PDL-chained
+// kernels makes the next one pay a full launch latency)
+__global__ void k_copy_bytes(unsigned char* __restrict__ dst, const unsigned char* __restrict__ src, uint64_t bytes) { DC_PDL_ENTER();
+  const uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, st = (uint64_t)gridDim.x * blockDim.x;
+  if ((((uintptr_t)dst | (uintptr_t)src) & 15) == 0) {
+    const uint64_t n16 = bytes / 16;
+    for (uint64_t i = i0; i < n16; i += st) reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+    for (uint64_t i = 16 * n16 + i0; i < bytes; i += st) dst[i] = src[i];
+  } else {
+    for (uint64_t i = i0; i < bytes; i += st) dst[i] = src[i];
+  }
+}
+dc_status dcopy(Ctx* c, void* dst, const void* src, uint64_t bytes) {
+  if (!bytes) return DC_OK;
+  dc_launch(k_copy_bytes, grid_for(c, bytes / 16 + 1, 256), 256, 0, c->stream, (unsigned char*)dst, (const unsigned char*)src, bytes);
+  DC_LAUNCHED(c);
+  return DC_OK;
+}
+
 dc_status fill_add(Ctx* c, FillList& f, void* p, uint64_t bytes, uint32_t v) {
   if (f.n == FILL_MAX) DC_TRY(fill_flush(c, f));
   f.p[f.n] = p;

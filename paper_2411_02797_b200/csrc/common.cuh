@@ -338,6 +338,8 @@ struct FillList {
 };
 __global__ void k_fill_multi(FillList f);
 dc_status fill_flush(Ctx* c, FillList& f);
+// device-to-device copy by a kernel (keeps the PDL chain)
+dc_status dcopy(Ctx* c, void* dst, const void* src, uint64_t bytes);
 // queue a fill of `bytes` bytes at p with the byte value v (flushes when the list is full)
 dc_status fill_add(Ctx* c, FillList& f, void* p, uint64_t bytes, uint32_t v = 0);
 template <class T>

@@ -314,7 +314,7 @@ dc_status dict_from_sorted(Ctx* c, const dc_frame_key* keys, uint64_t D, dc_dict
   DC_TRY(palloc(c, d->keys, D));
   DC_TRY(palloc(c, d->kinds, D));
   if (D) {
-    DC_CUDA(c, cudaMemcpyAsync(d->keys, keys, D * sizeof(dc_frame_key), cudaMemcpyDeviceToDevice, c->stream));
+    DC_TRY(dcopy(c, d->keys, keys, D * sizeof(dc_frame_key)));
     dc_launch(k_kinds_of, grid_for(c, D, 256), 256, 0, c->stream, d->keys, d->kinds, D);
     DC_LAUNCHED(c);
   }

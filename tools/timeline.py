@@ -73,7 +73,7 @@ def main():
             end = max(end, f)
             busy_k[e.name[:60]] += f - s
         print(f"step: span {t1 - t0:8.1f} us  busy {busy:8.1f} us  idle {t1 - t0 - busy:7.1f} us  kernels {len(g)}")
-    n = max(len(groups), 1)
+    n = steps
     print("largest idle gaps (us per step, count per step):")
     for k, v in gaps.most_common(25):
         print(f"  {v / n:7.1f}  {gapn[k] / n:4.1f}  {k}")
