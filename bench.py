@@ -171,7 +171,12 @@ def run_step(dc, ctx, tr, cfg: int, want_views: bool = True, comm=None):
         views["hotspots"] = hot
         if cfg == 3 and hot:
             views["stall"] = dc.dc_hotspots_topk(ctx, cct, dc.DC_VIEW_STALL, k=5, stall_node=hot[0][0])
-        dc.dc_cct_derived(ctx, cct, 0, True)
+        buf = getattr(tr, "derived_buf", None)
+        if buf is None or buf[0].numel() < cct.n_nodes:  # output columns allocated once (first warm-up step)
+            n = max(cct.n_nodes, 1)
+            buf = tr.derived_buf = (torch.empty(n, dtype=torch.float64, device=f"cuda:{ctx.device}"),
+                                    torch.empty(n, dtype=torch.float64, device=f"cuda:{ctx.device}"))
+        dc.dc_cct_derived(ctx, cct, 0, True, out=buf)
     return cct, views
 
 

@@ -382,10 +382,15 @@ def folded_text(ctx: Context, cct: CCT, labels, metric: int = 0) -> str:
     return "".join(";".join(str(labels[f]).replace(";", ",") for f in path) + f" {v}\n" for path, v in zip(paths, vals))
 
 
-def dc_cct_derived(ctx: Context, cct: CCT, metric: int, incl: bool = True):
+def dc_cct_derived(ctx: Context, cct: CCT, metric: int, incl: bool = True, out: tuple | None = None):
+    """mean / population std per node (float64 [N] CUDA). out: optional (mean, std) float64 CUDA
+    tensors of at least N elements, written in place (no allocation per call)."""
     N = cct.n_nodes
-    mean = torch.empty(max(N, 1), dtype=torch.float64, device=f"cuda:{ctx.device}")
-    std = torch.empty_like(mean)
+    if out is not None and out[0].numel() >= N and out[1].numel() >= N:
+        mean, std = out
+    else:
+        mean = torch.empty(max(N, 1), dtype=torch.float64, device=f"cuda:{ctx.device}")
+        std = torch.empty_like(mean)
     ctx.check(lib().dc_cct_derived(ctx.h, cct.h, int(metric), int(bool(incl)), _ptr(mean), _ptr(std)), "dc_cct_derived")
     return mean[:N], std[:N]
 

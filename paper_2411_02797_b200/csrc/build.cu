@@ -1351,11 +1351,11 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
     DC_TRY(fill_flush(c, fl));
   }
   const int tma_ok = ((uintptr_t)p->offsets % 16 == 0) && ((uintptr_t)p->frames % 16 == 0) && !getenv("DC_TEST_NO_TMA");
-  // per device (context) attribute: set on every call
-  DC_CUDA(c, cudaFuncSetAttribute(k_path_hash, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PathSmem)));
+  DC_SMEM_OPTIN(c, k_path_hash);  // once per context
   if (R) {
-    int per_sm = 1;
-    DC_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_path_hash, PT_THREADS, sizeof(PathSmem)));
+    if (!c->path_hash_per_sm)
+      DC_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->path_hash_per_sm, k_path_hash, PT_THREADS, sizeof(PathSmem)));
+    const int per_sm = c->path_hash_per_sm;
     const uint64_t n_tiles = (R + PT_T - 1) / PT_T;
     const int hgrid = (int)std::min<uint64_t>(n_tiles, (uint64_t)c->num_sms * std::max(per_sm, 1));
     Region rk(c, "k:path_hash");
@@ -1425,7 +1425,7 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
     DC_TRY(alloc(c, srt, P));
     DC_TRY(alloc(c, lcp, P));
     DC_TRY(alloc(c, len, P));
-    DC_CUDA(c, cudaFuncSetAttribute(k_small_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rank_smem));
+    DC_SMEM_OPTIN(c, k_small_rank);
     const uint32_t G = P == 0 ? 1u : P < (uint32_t)c->num_sms ? P : (uint32_t)c->num_sms;
     dc_launch(k_small_rank, G, SR_THREADS, rank_smem, c->stream, p->offsets, p->frames, item_rec.p, item_len.p, P, srt.p, lcp.p,
               len.p, pos.p, leaf_of_item.p);
@@ -1446,7 +1446,7 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
     Buf<uint32_t> dN;
     DC_TRY(alloc(c, dN, 2));
     size_t smem = sizeof(SmallSmem);
-    DC_CUDA(c, cudaFuncSetAttribute(k_build_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    DC_SMEM_OPTIN(c, k_build_small);
     dc_launch(k_build_small, 1, SB_THREADS, smem, c->stream, p->offsets, p->frames, item_rec.p, item_len.p, P, fbits, t->parent,
                                                       t->frame, t->depth, t->level_off, leaf_of_item.p, dN.p);
     DC_LAUNCHED(c);

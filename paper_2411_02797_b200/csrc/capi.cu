@@ -81,6 +81,7 @@ dc_status readback(Ctx* c, const void* dev, size_t bytes, void* host) {
     it.dst = (unsigned char*)c->h_pinned;
     dc_launch(k_readback, 1, 256, 0, c->stream, it);
     DC_LAUNCHED(c);
+    flush_pending_frees(c);
     DC_CUDA(c, cudaStreamSynchronize(c->stream));
     memcpy(host, c->h_pinned, bytes);
   } else {
@@ -109,6 +110,7 @@ dc_status readback_multi(Ctx* c, std::initializer_list<RB> items) {
     dc_launch(k_readback, 1, 256, 0, c->stream, rb);
     DC_LAUNCHED(c);
   }
+  flush_pending_frees(c);
   DC_CUDA(c, cudaStreamSynchronize(c->stream));
   o = 0;
   for (const RB& it : items) {
@@ -139,6 +141,10 @@ struct CtxEntry {
   int device;
   bool live;
   uint64_t handles;
+  // arrays of handles freed while the context is live: their stream-ordered frees are issued at
+  // the context's next blocking point (readback, sync, trim, destroy), where the host waits for
+  // the device anyway, instead of on the host's critical path between launches
+  std::vector<void*> pending;
 };
 static std::mutex g_ctx_mu;
 static std::unordered_map<uint64_t, CtxEntry> g_ctx;  // context uid -> entry
@@ -152,7 +158,7 @@ void register_ctx(Ctx* c, bool live) {
   std::lock_guard<std::mutex> g(g_ctx_mu);
   if (live) {
     c->uid = g_next_uid++;
-    g_ctx[c->uid] = CtxEntry{c->stream, c->pool, c->device, true, 0};
+    g_ctx[c->uid] = CtxEntry{c->stream, c->pool, c->device, true, 0, {}};
     return;
   }
   auto it = g_ctx.find(c->uid);
@@ -171,9 +177,9 @@ void free_handle_ptrs(uint64_t owner_uid, void* const* ps, size_t n) {
   auto it = g_ctx.find(owner_uid);
   if (it == g_ctx.end()) return;  // not made by a context (nothing allocated)
   CtxEntry& e = it->second;
-  if (e.live) {  // stream-ordered: after every queued use on the context stream
+  if (e.live) {  // stream-ordered (after every queued use on the context stream), deferred
     for (size_t i = 0; i < n; ++i)
-      if (ps[i]) cudaFreeAsync(ps[i], e.stream);
+      if (ps[i]) e.pending.push_back(ps[i]);
   } else {  // the context is gone: free in order after all device work
     cudaSetDevice(e.device);
     cudaDeviceSynchronize();
@@ -183,6 +189,14 @@ void free_handle_ptrs(uint64_t owner_uid, void* const* ps, size_t n) {
   }
   if (e.handles) e.handles--;
   if (!e.live && e.handles == 0) drop_entry_locked(it);
+}
+
+void flush_pending_frees(Ctx* c) {
+  std::lock_guard<std::mutex> g(g_ctx_mu);
+  auto it = g_ctx.find(c->uid);
+  if (it == g_ctx.end()) return;
+  for (void* p : it->second.pending) cudaFreeAsync(p, it->second.stream);
+  it->second.pending.clear();
 }
 
 dc_status check_flags(Ctx* c) {
@@ -410,6 +424,7 @@ dc_status dc_ctx_create(int device, void* cuda_stream, dc_ctx** out) {
 dc_status dc_ctx_sync(dc_ctx* ctx) {
   CHECK_CTX(ctx);
   ON_DEVICE(ctx);
+  flush_pending_frees(ctx);
   DC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   return check_flags(ctx);
 }
@@ -434,6 +449,7 @@ dc_status dc_ctx_diag(dc_ctx* ctx, dc_diag* out_h) {
 void dc_ctx_destroy(dc_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
+  dc::flush_pending_frees(ctx);
   cudaStreamSynchronize(ctx->stream);
   cudaStreamSynchronize(ctx->stream);
   arena_free(ctx);
@@ -478,6 +494,7 @@ dc_status dc_ctx_reserve(dc_ctx* ctx, uint64_t bytes) {
 dc_status dc_ctx_trim(dc_ctx* ctx, uint64_t keep_bytes) {
   CHECK_CTX(ctx);
   ON_DEVICE(ctx);
+  flush_pending_frees(ctx);
   DC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   arena_free(ctx);
   DC_CUDA(ctx, cudaStreamSynchronize(ctx->stream));

@@ -503,7 +503,7 @@ dc_status rollup(Ctx* c, dc_cct* t) {
     const size_t base = N * 8 + 4ull * ((t->max_depth + 2 + 3) & ~3u);
     const int use_spar = N <= 65535 && base + 2 * N <= c->smem_optin;
     const size_t smem = base + (use_spar ? 2 * N : 0);
-    DC_CUDA(c, cudaFuncSetAttribute(k_roll_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    DC_SMEM_OPTIN(c, k_roll_cols);
     dc_launch(k_roll_cols, cols, RC_THREADS, smem, s, t->parent, t->level_off, t->max_depth, (uint32_t)N, M, t->xcnt, t->icnt,
               t->mcols, limbs.p, t->xsamples, t->isamples, t->xstall, t->istall, use_spar);
     DC_LAUNCHED(c);
@@ -540,7 +540,7 @@ dc_status rollup(Ctx* c, dc_cct* t) {
     Buf<unsigned long long> limbs;
     if (M) DC_TRY(alloc_zero(c, limbs, 4ull * M * N));
     const size_t smem = N * 4;
-    DC_CUDA(c, cudaFuncSetAttribute(k_push_limbs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    DC_SMEM_OPTIN(c, k_push_limbs);
     const uint64_t work = (N - 1) * G;
     uint64_t grid = (work + 1023) / 1024;
     if (grid > (uint64_t)c->num_sms) grid = c->num_sms;

@@ -62,6 +62,8 @@ struct Ctx {
   uint64_t* h_pinned = nullptr;  // small pinned readback buffer
   int num_sms = 148;
   size_t smem_optin = 0;
+  std::vector<const void*> smem_set;  // kernels whose dynamic shared-memory cap is raised to smem_optin
+  int path_hash_per_sm = 0;           // cached occupancy of k_path_hash
   uint64_t launches = 0;
   uint64_t bytes_host = 0;       // host-accumulated algorithmic bytes
   uint64_t host_levels = 0;      // tree levels built
@@ -131,6 +133,7 @@ struct dc_ctx : dc::Ctx {};
 namespace dc {
 void register_ctx(Ctx* c, bool live);
 void free_handle_ptrs(uint64_t owner_uid, void* const* ps, size_t n);
+void flush_pending_frees(Ctx* c);  // issue the deferred stream-ordered frees of freed handles
 uint64_t adopt_handle(Ctx* c);  // a new handle of context c: returns its owner uid (c->uid)
 }  // namespace dc
 
@@ -201,6 +204,23 @@ dc_status fail(Ctx* c, dc_status s, const char* fmt, ...);
 // after a kernel launch: count it and check the launch error
 #define DC_STR2(x) #x
 #define DC_STR(x) DC_STR2(x)
+// Raise a kernel's dynamic shared-memory cap to the device's opt-in maximum (less its static
+// shared memory), once per context
+// (the cap only permits larger launches; every context sets the same value, so contexts on one
+// device never lower each other's setting)
+#define DC_SMEM_OPTIN(ctx, kern)                                                                          \
+  do {                                                                                                   \
+    const void* k_ = (const void*)(kern);                                                                \
+    bool set_ = false;                                                                                   \
+    for (const void* q_ : (ctx)->smem_set) set_ |= q_ == k_;                                             \
+    if (!set_) {                                                                                         \
+      cudaFuncAttributes fa_;                                                                            \
+      DC_CUDA(ctx, cudaFuncGetAttributes(&fa_, k_));                                                     \
+      DC_CUDA(ctx, cudaFuncSetAttribute(k_, cudaFuncAttributeMaxDynamicSharedMemorySize,                 \
+                                        (int)((ctx)->smem_optin - fa_.sharedSizeBytes)));                \
+      (ctx)->smem_set.push_back(k_);                                                                     \
+    }                                                                                                    \
+  } while (0)
 #define DC_LAUNCHED(ctx)                                                                              \
   do {                                                                                                \
     (ctx)->launches++;                                                                                \

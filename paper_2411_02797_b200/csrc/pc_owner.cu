@@ -1977,7 +1977,7 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
       case 9: kern = k_pc_owner<9>; break;
       default: a.probe_mode = 0;
     }
-    DC_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    DC_SMEM_OPTIN(c, kern);
     {
       Region rk(c, "k:pc_owner");
       dc_launch(kern, G, OW_THREADS, smem, c->stream, a);
@@ -2050,7 +2050,7 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
       dc_launch(k_ctx_order, 1, 1024, 0, c->stream, seg.p, a.g_segs, cap_segs, lkey_out, gfirst.p, gx.p + n_launch, order.p);
       DC_LAUNCHED(c);
       const size_t csmem = sizeof(CtxRedSmem);
-      DC_CUDA(c, cudaFuncSetAttribute(k_ctx_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
+      DC_SMEM_OPTIN(c, k_ctx_hist);
       {
         Region rk(c, "k:ctx_hist");
         // groups past NG keep zero (bins, pcs) for the scan over the n_launch bound: k_ctx_hist
@@ -2251,7 +2251,7 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
   DC_TRY(alloc(c, pbase, n_groups));
   DC_TRY(alloc(c, tots, 2));
   const size_t rsmem = sizeof(RedSmem);
-  DC_CUDA(c, cudaFuncSetAttribute(k_own_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem));  // per device
+  DC_SMEM_OPTIN(c, k_own_reduce);  // per device
   {
     Region rk(c, "k:own_reduce");
     dc_launch(k_own_reduce, n_groups < (uint32_t)G ? n_groups : G, RD_THREADS, rsmem, c->stream, seg.p, sso, grp_start.p, n_groups, gout.p, pkey.p, pcnt.p, N, okey.p, ocnt.p, gnb.p, gnp.p, gctx.p,

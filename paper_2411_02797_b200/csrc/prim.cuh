@@ -360,7 +360,7 @@ static inline dc_status radix_sort_pairs(Ctx* c, uint64_t* k0, uint32_t* v0, uin
   *result_in_1 = false;
   if (n <= 1 || end_bit <= begin_bit) return DC_OK;
   if (n <= SS_MAX) {
-    DC_CUDA(c, cudaFuncSetAttribute(k_sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SmallSortSmem)));
+    DC_SMEM_OPTIN(c, k_sort_small);
     dc_launch(k_sort_small, 1, SS_THREADS, sizeof(SmallSortSmem), c->stream, k0, v0, k1, v1, (uint32_t)n, begin_bit, end_bit);
     DC_LAUNCHED(c);
     *result_in_1 = true;

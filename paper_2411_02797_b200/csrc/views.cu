@@ -317,7 +317,7 @@ dc_status hotspots_topk(Ctx* c, const dc_cct* t, dc_view view, uint32_t metric, 
       (!bu || t->n_frames <= TK_FRAMES) && !getenv("DC_TEST_TOPK_GENERAL")) {
     Buf<dc_topk_entry> o1;
     DC_TRY(alloc(c, o1, k + 1));
-    DC_CUDA(c, cudaFuncSetAttribute(k_topk_one, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TopkSmem)));
+    DC_SMEM_OPTIN(c, k_topk_one);
     dc_launch(k_topk_one, 1, TK_THREADS, sizeof(TopkSmem), c->stream, view == DC_VIEW_INCLUSIVE ? ival : xval, t->frame,
               t->frame_kind, t->n_frames, kind_mask, t->N, total_p, threshold, k, bu ? 1 : 0, o1.p);
     DC_LAUNCHED(c);
