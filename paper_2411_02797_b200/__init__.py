@@ -242,7 +242,7 @@ def dc_intern_frames(ctx: Context, keys: torch.Tensor, out_ids: torch.Tensor | N
     d = ctypes.c_void_p()
     ctx.check(lib().dc_intern_frames(ctx.h, _ptr(keys) if n else None, n, _ptr(out_ids) if n else None, ctypes.byref(d)),
               "dc_intern_frames")
-    return out_ids[:n], Dict(d)
+    return (out_ids if out_ids.numel() == n else out_ids[:n]), Dict(d)
 
 
 def dc_dict_from_sorted(ctx: Context, keys: torch.Tensor) -> Dict:
@@ -261,7 +261,7 @@ def dc_cct_build(ctx: Context, offsets: torch.Tensor, frames: torch.Tensor, n_fr
     h = ctypes.c_void_p()
     ctx.check(lib().dc_cct_build(ctx.h, ctypes.byref(p), dict.h if dict is not None else None, int(n_frames),
                                  _ptr(out_leaf) if want_leaf else None, ctypes.byref(h)), "dc_cct_build")
-    return CCT(h, ctx), (out_leaf[:R] if want_leaf else None)
+    return CCT(h, ctx), ((out_leaf if out_leaf.numel() == R else out_leaf[:R]) if want_leaf else None)
 
 
 def dc_cct_attribute_metrics(ctx: Context, cct: CCT, leaf: torch.Tensor, metrics: torch.Tensor):
