@@ -472,7 +472,10 @@ def main():
                            "records_per_gpu_step": recs,
                            "pc_samples": int(tr.samples.shape[0]) if args.config == 3 else 0,
                            "launch_records": tr.n_records, "nodes": n_nodes, "bins": n_bins,
-                           "l2": f"inputs larger than L2 ({step_bytes / 1e9:.2f} GB read per step); no flush",
+                           "l2": (f"inputs larger than L2 ({step_bytes / 1e9:.2f} GB read per step); no flush"
+                                  if step_bytes > 126e6 else
+                                  f"inputs fit in L2 ({step_bytes / 1e6:.1f} MB per step, not flushed: tiny "
+                                  f"latency-bound config, not a bandwidth figure)"),
                            "parallelism": (f"dp{world}: per-rank shard, local CCT + NCCL cross-rank merge "
                                            "(dc_cct_merge_ranks), weak scaling") if world > 1 else "dp1"},
                 "roofline": roof, "stages_ms": stages, "gpu_launches": int(launches),
