@@ -7,9 +7,9 @@
 // range with the most unclaimed stages (per-CTA claim words), so the slowest range does not
 // set the kernel time:
 //   * the producer warp streams each stage's launch segments (32-sample rows, see the stage
-//     plan below) into shared memory with TMA bulk copies (cp.async.bulk + mbarrier, 4 x 32 KB
+//     plan below) into shared memory with TMA bulk copies (cp.async.bulk + mbarrier, 3 x 40 KB
 //     stages) and decides the flush points;
-//   * 16 consumer warps aggregate (pc_off, stall) -> count in an 11,136-slot shared-memory
+//   * 20 consumer warps aggregate (pc_off, stall) -> count in an 11,776-slot shared-memory
 //     hash table probed in 4-slot buckets (one 16-B load settles a hit; predicated
 //     red.shared.add); misses are queued per warp and probed 32 at a time; warps run free
 //     (no per-stage CTA barrier) and only meet at flushes;
@@ -30,7 +30,14 @@
 
 namespace dc {
 
-constexpr int OW_CONS_WARPS = 16;
+#ifndef DC_OW_WARPS
+#define DC_OW_WARPS 20
+#endif
+#ifndef DC_OW_CPS
+#define DC_OW_CPS 1
+#endif
+constexpr int OW_CONS_WARPS = DC_OW_WARPS;  // consumer warps per CTA (A/B builds: others)
+constexpr int OW_CPS = DC_OW_CPS;           // k_pc_owner CTAs per SM (A/B builds: 2)
 constexpr int OW_CONS = 32 * OW_CONS_WARPS;   // 512 consumer threads
 constexpr int OW_THREADS = OW_CONS + 32;      // + producer warp
 #ifndef DC_OW_NOBR
@@ -40,16 +47,16 @@ constexpr int OW_THREADS = OW_CONS + 32;      // + producer warp
 #define DC_OW_HINT 0  // preferred-slot lookup (A/B builds)
 #endif
 #ifndef DC_OW_STAGES
-#define DC_OW_STAGES 4
+#define DC_OW_STAGES 3
 #endif
 constexpr int OW_STAGES = DC_OW_STAGES;  // (A/B builds: other counts)
 constexpr int OW_PER_LANE = 4;                // samples per lane per stage
 constexpr int OW_ROUND = 32 * OW_PER_LANE;    // samples per warp per stage
-constexpr int OW_STAGE = OW_CONS_WARPS * OW_ROUND;  // 2048 samples per stage (32 KB)
+constexpr int OW_STAGE = OW_CONS_WARPS * OW_ROUND;  // 2560 samples per stage (40 KB)
 #ifndef DC_OW_TAB
-#define DC_OW_TAB 11136
+#define DC_OW_TAB 11776
 #endif
-constexpr int OW_TAB = DC_OW_TAB;             // shared hash table slots (87 KB)
+constexpr int OW_TAB = DC_OW_TAB;             // shared hash table slots (92 KB)
 constexpr int OW_PEND = OW_ROUND + 32;        // per-warp queue of missed keys (probed 32 at a time)
 // a flush is requested at 2/3 load; past OW_SPILL_AT distinct keys new keys are not inserted
 // but appended to the CTA's spill region in HBM (kept as partial entries), so the table can
@@ -94,6 +101,7 @@ struct OwnSmem {
   uint32_t seg_si;
   unsigned long long seg_base;
 };
+static_assert(OW_CPS * (sizeof(OwnSmem) + 1024) <= 233472, "k_pc_owner shared memory past the SM");
 static_assert(sizeof(OwnSmem) <= 232448, "k_pc_owner shared memory past the 227 KB opt-in limit");
 
 __device__ __forceinline__ void cons_sync() { asm volatile("bar.sync 1, %0;" ::"n"(OW_CONS) : "memory"); }
@@ -544,7 +552,7 @@ __device__ __noinline__ void own_cold(const uint4 q, uint32_t seg_launch, const 
 }
 
 template <int MODE>  // 0 = the product; 1, 2, 3, 4, 9 = measurement variants (DC_OWN_MODE)
-__global__ void __launch_bounds__(OW_THREADS, 1) k_pc_owner(OwnArgs a) { DC_PDL_WAIT();
+__global__ void __launch_bounds__(OW_THREADS, OW_CPS) k_pc_owner(OwnArgs a) { DC_PDL_WAIT();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   OwnSmem& sm = *reinterpret_cast<OwnSmem*>(smem_raw);
   const uint32_t tid = threadIdx.x;
@@ -1825,7 +1833,8 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
   *handled = 0;
   if (n == 0 || n_launch == 0 || n_launch >= (1ull << 31)) return DC_OK;
   const uint64_t N = t->N;
-  const uint32_t G = (uint32_t)c->num_sms;
+  const uint32_t G = (uint32_t)c->num_sms * OW_CPS;  // k_pc_owner CTAs (claims, spill chunks)
+  const uint32_t Gs = (uint32_t)c->num_sms;          // one CTA per SM: the reduce kernels
   Buf<uint32_t> bad;
   Buf<uint64_t> k0, k1;
   Buf<uint32_t> v0, v1;
@@ -2055,7 +2064,7 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
         Region rk(c, "k:ctx_hist");
         // groups past NG keep zero (bins, pcs) for the scan over the n_launch bound: k_ctx_hist
         // writes every group < NG; the rest are cleared with the counters
-        dc_launch(k_ctx_hist, G, CR_THREADS, csmem, c->stream, seg.p, seg_meta.p, a.g_segs, cap_segs, pkey.p, pcnt.p, lkey_out, gfirst.p,
+        dc_launch(k_ctx_hist, Gs, CR_THREADS, csmem, c->stream, seg.p, seg_meta.p, a.g_segs, cap_segs, pkey.p, pcnt.p, lkey_out, gfirst.p,
                   gx.p + n_launch, order.p, N, S, flags.p, ctl.p, wscr.p, wcap, bscr.p, bcap, rec.p, gn, gn + n_launch + 1,
                   (unsigned long long*)t->xsamples, (unsigned long long*)t->xstall);
         DC_LAUNCHED(c);
@@ -2254,7 +2263,7 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
   DC_SMEM_OPTIN(c, k_own_reduce);  // per device
   {
     Region rk(c, "k:own_reduce");
-    dc_launch(k_own_reduce, n_groups < (uint32_t)G ? n_groups : G, RD_THREADS, rsmem, c->stream, seg.p, sso, grp_start.p, n_groups, gout.p, pkey.p, pcnt.p, N, okey.p, ocnt.p, gnb.p, gnp.p, gctx.p,
+    dc_launch(k_own_reduce, n_groups < Gs ? n_groups : Gs, RD_THREADS, rsmem, c->stream, seg.p, sso, grp_start.p, n_groups, gout.p, pkey.p, pcnt.p, N, okey.p, ocnt.p, gnb.p, gnp.p, gctx.p,
         (unsigned long long*)t->xsamples, (unsigned long long*)t->xstall, S, flags.p);
     DC_LAUNCHED(c);
   }
@@ -2276,7 +2285,7 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
   DC_TRY(palloc(c, t->bin_pcnode, nb));
   DC_TRY(palloc(c, t->bin_stall, nb));
   DC_TRY(palloc(c, t->bin_count, nb));
-  dc_launch(k_own_place, n_groups < 4u * G ? (n_groups ? n_groups : 1) : 4 * G, 256, 0, c->stream, gout.p, gnb.p, bbase.p, pbase.p, gctx.p, n_groups, okey.p, ocnt.p, N, t->pc_ctx, t->pc_off, t->bin_pcnode,
+  dc_launch(k_own_place, n_groups < 4u * Gs ? (n_groups ? n_groups : 1) : 4 * Gs, 256, 0, c->stream, gout.p, gnb.p, bbase.p, pbase.p, gctx.p, n_groups, okey.p, ocnt.p, N, t->pc_ctx, t->pc_off, t->bin_pcnode,
       t->bin_stall, t->bin_count);
   DC_LAUNCHED(c);
   DC_TRY(add_diag(c, ldiag.p));
