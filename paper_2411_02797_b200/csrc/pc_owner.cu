@@ -1143,10 +1143,27 @@ __global__ void __launch_bounds__(32 * BR_WARPS) k_br_count(
 // A context whose PC range or segment count does not fit shared memory (or scratch that is too
 // small) raises CR_WIDE: the host takes the k_br_* path; outputs past the allocated capacity
 // are not written (CR_OVER: the host reallocates and reruns k_ctx_emit only).
-constexpr int CR_THREADS = 1024;
-constexpr uint32_t CR_WORDS = 8192;    // PCs per context (pc' range)
-constexpr uint32_t CR_BINS = 12288;    // bins per context counted in shared memory
-constexpr uint32_t CR_SEGS = 4096;     // segments per context
+#ifndef DC_CR_THREADS
+#define DC_CR_THREADS 1024
+#endif
+#ifndef DC_CR_WORDS
+#define DC_CR_WORDS 8192
+#endif
+#ifndef DC_CR_BINS
+#define DC_CR_BINS 12288
+#endif
+#ifndef DC_CR_SEGS
+#define DC_CR_SEGS 4096
+#endif
+#ifndef DC_CR_CPS
+#define DC_CR_CPS 1
+#endif
+constexpr int CR_THREADS = DC_CR_THREADS;
+constexpr int CR_NW = CR_THREADS / 32;     // warps per CTA
+constexpr int CR_CPS = DC_CR_CPS;          // CTAs per SM
+constexpr uint32_t CR_WORDS = DC_CR_WORDS;  // PCs per context (pc' range)
+constexpr uint32_t CR_BINS = DC_CR_BINS;    // bins per context counted in shared memory
+constexpr uint32_t CR_SEGS = DC_CR_SEGS;    // segments per context
 constexpr uint32_t CR_USEGS = 1024;    // of which with an unknown key range (more: pass A walks all)
 constexpr uint32_t CR_ORDER_MAX = 8192;   // groups ordered by size (more: ascending order; static smem)
 enum { CR_WIDE = 1, CR_OVER = 2 };
@@ -1171,7 +1188,7 @@ struct __align__(16) CtxRec {  // scratch per group
 };
 
 // Walks the context's entries: chunks of 32 x CR_U entries, chunk k of the concatenated
-// segments to warp k mod 32; every lane has CR_U independent loads in flight (one memory
+// segments to warp k mod CR_NW; every lane has CR_U independent loads in flight (one memory
 // latency per chunk instead of one per entry). fn(key, count) for every valid entry.
 constexpr uint32_t CR_U = 8;
 template <bool WITH_CNT, class F>
@@ -1184,7 +1201,7 @@ __device__ __forceinline__ void cr_for_entries(const uint32_t* segs, const uint4
     const uint4 sg = seg[segs[q]];
     const uint64_t base = (uint64_t)sg.z | ((uint64_t)sg.w << 32);
     const uint32_t nch = (sg.y + CH - 1) / CH;
-    for (uint32_t ch = (w + 32 - kbase % 32) % 32; ch < nch; ch += 32) {
+    for (uint32_t ch = (w + CR_NW - kbase % CR_NW) % CR_NW; ch < nch; ch += CR_NW) {
       uint32_t kk[CR_U];
       unsigned long long cv[CR_U];
 #pragma unroll
@@ -1242,7 +1259,7 @@ __global__ void __launch_bounds__(1024) k_ctx_order(const uint4* __restrict__ se
   for (uint32_t g = tid; g < NG; g += blockDim.x) order[atomicAdd(&bucket[size[g] ? 32 - __clz(size[g]) : 0], 1u)] = g;
 }
 
-__global__ void __launch_bounds__(CR_THREADS, 1) k_ctx_hist(
+__global__ void __launch_bounds__(CR_THREADS, CR_CPS) k_ctx_hist(
     const uint4* __restrict__ seg, const uint2* __restrict__ seg_meta, const unsigned int* __restrict__ d_nsegs, uint32_t cap_segs, const uint32_t* __restrict__ pkey,
     const unsigned long long* __restrict__ pcnt, const uint64_t* __restrict__ lkey, const uint32_t* __restrict__ gfirst,
     const uint32_t* __restrict__ d_ng, const uint32_t* __restrict__ order, uint64_t N, uint32_t S, const uint32_t* __restrict__ g_flags,
@@ -1376,7 +1393,7 @@ __global__ void __launch_bounds__(CR_THREADS, 1) k_ctx_hist(
       if (ow == ~0ull) ok = false;
     }
     const bool in_smem = nb <= CR_BINS;
-    for (uint32_t i = tid; i < 32 * 32; i += CR_THREADS) {
+    for (uint32_t i = tid; i < CR_NW * 32; i += CR_THREADS) {
       (&sm.wst_lo[0][0])[i] = 0;
       (&sm.wst_hi[0][0])[i] = 0;
     }
@@ -2064,7 +2081,7 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
         Region rk(c, "k:ctx_hist");
         // groups past NG keep zero (bins, pcs) for the scan over the n_launch bound: k_ctx_hist
         // writes every group < NG; the rest are cleared with the counters
-        dc_launch(k_ctx_hist, Gs, CR_THREADS, csmem, c->stream, seg.p, seg_meta.p, a.g_segs, cap_segs, pkey.p, pcnt.p, lkey_out, gfirst.p,
+        dc_launch(k_ctx_hist, Gs * CR_CPS, CR_THREADS, csmem, c->stream, seg.p, seg_meta.p, a.g_segs, cap_segs, pkey.p, pcnt.p, lkey_out, gfirst.p,
                   gx.p + n_launch, order.p, N, S, flags.p, ctl.p, wscr.p, wcap, bscr.p, bcap, rec.p, gn, gn + n_launch + 1,
                   (unsigned long long*)t->xsamples, (unsigned long long*)t->xstall);
         DC_LAUNCHED(c);
