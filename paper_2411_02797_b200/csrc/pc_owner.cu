@@ -524,8 +524,9 @@ constexpr uint32_t OW_EXTRA_FLUSH = 1u << 30;
 __device__ __forceinline__ bool own_hot(const uint4 q, uint32_t row_launch, uint32_t S) {
   return (q.x == row_launch) & ((q.z & 0xFFFFu) < S) & (q.w == 1u) & (q.y < (1u << 27) - 1u);
 }
-__device__ __noinline__ void own_cold(const uint4 q, uint32_t seg_launch, const OwnArgs& a, bool ctx_ok, OwCounters& k,
-                                      OwnSmem& sm, uint32_t ctx) {
+// returns 1 when this call inserted a new key into the table (the caller publishes it)
+__device__ __noinline__ uint32_t own_cold(const uint4 q, uint32_t seg_launch, const OwnArgs& a, bool ctx_ok, OwCounters& k,
+                                          OwnSmem& sm, uint32_t ctx) {
   const uint32_t stall = q.z & 0xFFFFu;
   const bool ok = (q.x == seg_launch) & (stall < a.S) & (q.w != 0) & (q.y < (1u << 27) - 1u) & ctx_ok & (q.x < a.n_launch);
   if (ok) {  // valid sample with count > 1
@@ -535,20 +536,28 @@ __device__ __noinline__ void own_cold(const uint4 q, uint32_t seg_launch, const 
       if (before < OW_EXTRA_FLUSH && before + (q.w - 1u) >= OW_EXTRA_FLUSH) *(volatile uint32_t*)&sm.flush_req = 1u;
       const uint32_t bb = own_bucket(key);
       const uint4 v = ld_shared_v4_volatile(&sm.key[4 * bb]);
-      const uint32_t sl = bucket_slot(v, key, bb);
-      if (sl != OW_MISS) {
+      uint32_t sl = bucket_slot(v, key, bb);
+      uint32_t ins = 0;
+      if (sl == OW_MISS) {  // new or displaced key: probe, inserting it (round 2: per-PC aggregated
+                            // records used to spill every key not yet in the table)
+        const uint32_t r = own_probe(sm, key, bb);
+        ins = r >> 31;
+        sl = r & 0x7FFFFFFFu;
+      }
+      if (sl != (uint32_t)OW_TAB) {
         atomicAdd(&sm.cnt[sl], q.w);
-        return;
+        return ins;
       }
     }
-    own_spill(sm, a, key, q.w, ctx);  // new / displaced key, or a count past 2^16
-    return;
+    own_spill(sm, a, key, q.w, ctx);  // table full, or a count past 2^16
+    return 0;
   }
   const uint32_t r = own_reject(q.x, stall, q.w, seg_launch, a.n_launch, a.S, ctx_ok, a.trace_flags);
   k.bad_l += r == 0;
   k.bad_s += r == 1;
   k.zero += r == 2;
   k.fallback |= r == 3;
+  return 0;
 }
 
 template <int MODE>  // 0 = the product; 1, 2, 3, 4, 9 = measurement variants (DC_OWN_MODE)
@@ -842,7 +851,7 @@ __global__ void __launch_bounds__(OW_THREADS, OW_CPS) k_pc_owner(OwnArgs a) { DC
     if (__any_sync(0xffffffffu, cold)) {  // rare: spills and invalid samples
 #pragma unroll
       for (int i = 0; i < OW_PER_LANE; ++i)
-        if (vld[i] && t[i] == EMPTY32) own_cold(q[i], lch[i], a, ctx_ok, k, sm, mctx);
+        if (vld[i] && t[i] == EMPTY32) inserted += own_cold(q[i], lch[i], a, ctx_ok, k, sm, mctx);
     }
     const long long c_2 = MODE == 9 ? clock64() : 0;
     if (MODE == 9) t_key += c_2 - c_1;
