@@ -1385,7 +1385,7 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
     }
     if (R) {
       Region rk(c, "k:path_group");
-      static const bool pg_rows = getenv("DC_PG_ROWS") != nullptr;  // A/B: the per-record verify
+      const bool pg_rows = getenv("DC_PG_ROWS") != nullptr;  // tests / A/B: the per-record verify
       dc_launch(pg_rows ? k_path_group<false> : k_path_group<true>, grid_for(c, (R + 31) / 32 * 32, 256), 256, 0, c->stream, p->offsets, p->frames, hash.p, R, tab.p,
                                                                                 cap - 1, slot_of_rec.p, extra_rec.p, cnt.p);
       DC_LAUNCHED(c);

@@ -313,9 +313,13 @@ def test_large_P_multikernel_build():
     assert_same(a, ref, ctx="largeP")
 
 
-def test_hash_collisions_resolved_exactly(monkeypatch):
-    """DC_TEST_WEAK_HASH=6 keeps 6 bits of the path hash: thousands of collisions, same tree."""
+@pytest.mark.parametrize("verify", ["sweep", "rows"])
+def test_hash_collisions_resolved_exactly(verify, monkeypatch):
+    """DC_TEST_WEAK_HASH=6 keeps 6 bits of the path hash: thousands of collisions, same tree;
+    with k_path_group's window-sweep verify and with its per-record verify (DC_PG_ROWS)."""
     monkeypatch.setenv("DC_TEST_WEAK_HASH", "6")
+    if verify == "rows":
+        monkeypatch.setenv("DC_PG_ROWS", "1")
     import paper_2411_02797_b200 as dc
     ctx = dc.Context(0)
     rng = np.random.default_rng(4)
