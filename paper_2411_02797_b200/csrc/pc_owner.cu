@@ -781,7 +781,7 @@ __global__ void __launch_bounds__(OW_THREADS, OW_CPS) k_pc_owner(OwnArgs a) { DC
   uint32_t cur_ctx = OW_DONE, st = 0, ph = 0;
   OwCounters k{0, 0, 0, 0};
   uint32_t sinkv = 0;
-  long long t_wait = 0, t_flush = 0, t_work = 0, n_stage = 0, t_key = 0, t_bucket = 0, t_add = 0, n_miss = 0;  // MODE 9 only
+  long long t_wait = 0, t_flush = 0, t_work = 0, n_stage = 0, t_key = 0, t_bucket = 0, t_add = 0, n_miss = 0, since_flush = 0;  // MODE 9 only
   uint32_t np = 0;        // queued misses of this warp (warp-uniform)
   uint32_t inserted = 0;  // keys this lane inserted since the last publish
   auto probe_add = [&](uint32_t key, uint32_t add) {
@@ -817,6 +817,11 @@ __global__ void __launch_bounds__(OW_THREADS, OW_CPS) k_pc_owner(OwnArgs a) { DC
     if (MODE == 9) {
       t_wait += c_1 - c_0;
       t_flush += clock64() - c_1;
+      // measurement split: waits in the first ring-worth of stages after a flush (bucket slot)
+      // and the final wait for the DONE marker (miss slot)
+      if (flush) since_flush = 0;
+      if (mctx == OW_DONE) n_miss = c_1 - c_0;
+      else if (since_flush++ < OW_STAGES) t_bucket += c_1 - c_0;
     }
     if (mctx == OW_DONE) break;
     cur_ctx = mctx;
@@ -888,7 +893,6 @@ __global__ void __launch_bounds__(OW_THREADS, OW_CPS) k_pc_owner(OwnArgs a) { DC
           slot[i] = bucket_slot(v, t[i], b[i]);
         }
       }
-      if (MODE == 9) t_bucket += clock64() - c_2;
       // Hits are added directly. Misses (new or displaced keys, a few % of the samples) are
       // queued per warp and probed 32 at a time, so the slow path runs with all lanes busy.
       // (Claiming new keys inline with a CAS, or draining the queue every stage, cut the
@@ -911,8 +915,7 @@ __global__ void __launch_bounds__(OW_THREADS, OW_CPS) k_pc_owner(OwnArgs a) { DC
         }
       }
       if (MODE == 3) np = 0;  // measurement only: misses dropped
-      if (MODE == 9 && lane == 0) n_miss += np;
-      __syncwarp();
+        __syncwarp();
       while (np >= 32) {
         np -= 32;
         probe_one(sm.pend[w][np + lane]);
@@ -2037,8 +2040,8 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
       const double nw = (double)G * OW_CONS_WARPS;
       fprintf(stderr,
               "{\"own_split\": {\"wait_cyc\": %.0f, \"flush_cyc\": %.0f, \"work_cyc\": %.0f, \"stages\": %.1f, "
-              "\"key_cyc\": %.0f, \"bucket_cyc\": %.0f, \"add_cyc\": %.0f, \"misses\": %.0f}}\n",
-              s[0] / nw, s[1] / nw, s[2] / nw, s[3] / nw, s[4] / nw, s[5] / nw, s[6] / nw, s[7]);
+              "\"key_cyc\": %.0f, \"wait_after_flush_cyc\": %.0f, \"add_cyc\": %.0f, \"wait_done_cyc\": %.0f}}\n",
+              s[0] / nw, s[1] / nw, s[2] / nw, s[3] / nw, s[4] / nw, s[5] / nw, s[6] / nw, s[7] / nw);
     }
     uint32_t hbad = 0;
     if (!getenv("DC_TEST_PC_BR")) {
