@@ -43,6 +43,9 @@ constexpr int OW_THREADS = OW_CONS + 32;      // + producer warp
 #ifndef DC_OW_NOBR
 #define DC_OW_NOBR 1  // branch-free hit / miss bookkeeping: 0.449 -> 0.435 ms (same-box A/B)
 #endif
+#ifndef DC_OW_DYN
+#define DC_OW_DYN 1  // consumer row groups by ticket: 0.424 -> 0.413 ms (same-box A/B)
+#endif
 #ifndef DC_OW_HINT
 #define DC_OW_HINT 0  // preferred-slot lookup (A/B builds)
 #endif
@@ -75,7 +78,7 @@ enum { OWF_FALLBACK = 1, OWF_OVERFLOW = 2 };
 
 constexpr int OW_ROWS = OW_STAGE / 32;        // 32-sample rows per stage
 struct __align__(16) OwMeta {
-  uint32_t ctx, count, flush, pad;
+  uint32_t ctx, count, flush, epoch;  // epoch: flushes up to and including this stage (DC_OW_DYN)
   uint32_t row_launch[OW_ROWS];  // launch of each 32-sample row (pieces start on row boundaries)
   uint8_t row_valid[OW_ROWS];    // valid samples in the row (a launch's tail row is partial)
 };
@@ -100,6 +103,7 @@ struct OwnSmem {
   uint32_t warp_mx[OW_CONS_WARPS], warp_or[OW_CONS_WARPS];  // flush: per-warp key range of the segment
   uint32_t seg_si;
   unsigned long long seg_base;
+  uint32_t ticket;  // DC_OW_DYN: next row group of the stage stream
 };
 static_assert(OW_CPS * (sizeof(OwnSmem) + 1024) <= 233472, "k_pc_owner shared memory past the SM");
 static_assert(sizeof(OwnSmem) <= 232448, "k_pc_owner shared memory past the 227 KB opt-in limit");
@@ -584,6 +588,7 @@ __global__ void __launch_bounds__(OW_THREADS, OW_CPS) k_pc_owner(OwnArgs a) { DC
     sm.sp_word = 0;
     sm.sp_seg = 0;
     sm.sp_lock = 0;
+    sm.ticket = 0;
     sm.sp_base[0] = a.spill_base0 + (uint64_t)blockIdx.x * OW_SPILL_CAP;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -595,7 +600,7 @@ __global__ void __launch_bounds__(OW_THREADS, OW_CPS) k_pc_owner(OwnArgs a) { DC
     // The launch fields of stage s + 1 are loaded while stage s is issued (and the per-stage
     // first-launch / context words 32 stages at a time, one batch ahead).
     const uint32_t lane = tid;
-    uint32_t st = 0, ph = 0, prev_ctx = OW_DONE;
+    uint32_t st = 0, ph = 0, prev_ctx = OW_DONE, epoch = 0;  // epoch: lane 0's flush count
     volatile uint32_t* freq = &sm.flush_req;
     const bool prof = MODE == 2 || MODE == 9;  // measurement only
     long long p_wait = 0, p_comp = 0, p_stages = 0, p_pieces = 0;
@@ -695,6 +700,8 @@ __global__ void __launch_bounds__(OW_THREADS, OW_CPS) k_pc_owner(OwnArgs a) { DC
         }
         sm.meta[st].ctx = ctx;
         sm.meta[st].flush = flush;
+        epoch += flush;
+        sm.meta[st].epoch = epoch;
       }
       uint32_t npieces = 0;
       if (npc <= OW_DPIECES) {  // precomputed pieces: lane j in [1, npc] issues piece j - 1
@@ -762,6 +769,7 @@ __global__ void __launch_bounds__(OW_THREADS, OW_CPS) k_pc_owner(OwnArgs a) { DC
       sm.meta[st].ctx = OW_DONE;
       sm.meta[st].count = 0;
       sm.meta[st].flush = 1;
+      sm.meta[st].epoch = epoch + 1;
       mbar_arrive(&sm.full[st]);
     }
     if (prof && lane == 0) {
@@ -799,11 +807,27 @@ __global__ void __launch_bounds__(OW_THREADS, OW_CPS) k_pc_owner(OwnArgs a) { DC
       if (before < OW_FLUSH_REQ && before + ins >= OW_FLUSH_REQ) *(volatile uint32_t*)&sm.flush_req = 1u;
     }
   };
+  uint32_t my_epoch = 0, grp = w;  // DC_OW_DYN: flushes this warp took part in; row group of the stage
   while (true) {
     const long long c_0 = MODE == 9 ? clock64() : 0;
+    if (DC_OW_DYN) {
+      // Row groups by ticket: the next group of the stage stream goes to whichever warp asks, so
+      // no warp runs ahead of the others (a slot is refilled once all its groups are taken). At
+      // most one ticket per warp is outstanding, so the tickets taken while a flush barrier waits
+      // all lie in the flush stage (groups per stage = warps): the ring cannot deadlock.
+      uint32_t tk = 0;
+      if (lane == 0) tk = atomicAdd(&sm.ticket, 1u);
+      tk = __shfl_sync(0xffffffffu, tk, 0);
+      const uint32_t kst = tk / (uint32_t)OW_CONS_WARPS;
+      grp = tk - kst * (uint32_t)OW_CONS_WARPS;
+      st = kst % OW_STAGES;
+      ph = (kst / OW_STAGES) & 1u;
+    }
     mbar_wait(&sm.full[st], ph);
     const long long c_1 = MODE == 9 ? clock64() : 0;
-    const uint32_t flush = sm.meta[st].flush, mctx = sm.meta[st].ctx;
+    const uint32_t mctx = sm.meta[st].ctx;
+    const uint32_t flush = DC_OW_DYN ? (sm.meta[st].epoch != my_epoch ? 1u : 0u) : sm.meta[st].flush;
+    if (DC_OW_DYN) my_epoch = sm.meta[st].epoch;
     if (flush) {  // uniform: every consumer sees the same meta
       if (np) {  // this warp's queued misses belong to the table being flushed
         if (lane < np) probe_one(sm.pend[w][lane]);
@@ -829,7 +853,7 @@ __global__ void __launch_bounds__(OW_THREADS, OW_CPS) k_pc_owner(OwnArgs a) { DC
     if (MODE == 2) {  // measurement only: the TMA pipeline alone (stage released unread)
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[st]);
-      if (++st == OW_STAGES) {
+      if (!DC_OW_DYN && ++st == OW_STAGES) {
         st = 0;
         ph ^= 1u;
       }
@@ -840,7 +864,7 @@ __global__ void __launch_bounds__(OW_THREADS, OW_CPS) k_pc_owner(OwnArgs a) { DC
     bool vld[OW_PER_LANE];
 #pragma unroll
     for (int i = 0; i < OW_PER_LANE; ++i) {
-      const uint32_t row = w * OW_PER_LANE + i;  // warp w owns rows [4w, 4w+4) of the stage
+      const uint32_t row = grp * OW_PER_LANE + i;  // rows [4g, 4g+4) of the stage (g = w, or by ticket)
       lch[i] = sm.meta[st].row_launch[row];      // row-uniform: one broadcast load
       vld[i] = lane < sm.meta[st].row_valid[row];
       q[i] = vld[i] ? sm.stage[st][32 * row + lane] : make_uint4(0, 0, 0, 0);
@@ -928,7 +952,7 @@ __global__ void __launch_bounds__(OW_THREADS, OW_CPS) k_pc_owner(OwnArgs a) { DC
       t_work += clock64() - c_1;
       ++n_stage;
     }
-    if (++st == OW_STAGES) {
+    if (!DC_OW_DYN && ++st == OW_STAGES) {
       st = 0;
       ph ^= 1u;
     }
