@@ -396,7 +396,9 @@ def main():
         ab = alg[kname]
         ach = ab / (kms / 1000.0) / 1e9
         roof = {"bound": "hbm", "kernel": kname[2:], "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(ach / peak, 4), "traffic": traffic_for(kname[2:], args.config), "alg_bytes_per_launch": ab,
+                "frac": round(ach / peak, 4), "traffic": (traffic_for(kname[2:], args.config) if args.records is None and not args.stress
+                            and not args.aggregated else None),  # captures are of the default workloads
+                "alg_bytes_per_launch": ab,
                 "kernel_ms": round(kms, 4), "peak_source": peak_src,
                 "share_of_step": round(kms / ms, 4)}
     stages = {k: round(v[1] / v[0], 4) for k, v in timers.items()}
