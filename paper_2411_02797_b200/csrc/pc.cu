@@ -339,6 +339,52 @@ dc_status pc_attribute(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, con
   return DC_OK;
 }
 
+// -------- launch partition (round 2): samples in any order, no per-launch offsets. When the
+// launches are few enough for a per-CTA shared-memory histogram, the samples are first
+// partitioned by launch (a counting sort: per-CTA histograms, one scan in launch-major order,
+// a scatter through shared cursors; the order inside a launch is irrelevant to the bins) and
+// the context-owner schedule runs on the partitioned copy with the offsets the scan gives —
+// three passes over the samples instead of one L2-atomic table update per sample. Samples whose
+// launch is out of range go to a last bucket and are counted as DG_BAD_LAUNCH, as in k_pc_table.
+constexpr uint64_t LP_MAX = 49152;  // launches (+1 bucket) in a CTA's shared-memory histogram
+constexpr int LP_THREADS = 1024;
+__global__ void __launch_bounds__(LP_THREADS) k_lp_count(const dc_pc_sample* __restrict__ smp, uint64_t n, uint32_t n_launch,
+                                                         uint32_t* __restrict__ gh) { DC_PDL_ENTER();
+  extern __shared__ uint32_t lh[];
+  const uint32_t G = gridDim.x, b = blockIdx.x;
+  for (uint32_t l = threadIdx.x; l <= n_launch; l += LP_THREADS) lh[l] = 0;
+  __syncthreads();
+  const uint64_t lo = n * b / G, hi = n * (b + 1) / G;
+  const uint32_t* lf = reinterpret_cast<const uint32_t*>(smp);  // launch = word 0 of each 16-B sample
+  for (uint64_t j = lo + threadIdx.x; j < hi; j += LP_THREADS) {
+    const uint32_t l = __ldg(lf + 4 * j);
+    atomicAdd(&lh[l < n_launch ? l : n_launch], 1u);
+  }
+  __syncthreads();
+  for (uint32_t l = threadIdx.x; l <= n_launch; l += LP_THREADS) gh[(uint64_t)l * G + b] = lh[l];  // launch-major
+}
+__global__ void k_lp_offsets(const uint32_t* __restrict__ gh, uint32_t n_launch, uint32_t G, uint64_t n,
+                             uint64_t* __restrict__ loff, unsigned long long* __restrict__ ldiag) { DC_PDL_ENTER();
+  for (uint32_t l = blockIdx.x * blockDim.x + threadIdx.x; l <= n_launch; l += gridDim.x * blockDim.x) {
+    loff[l] = gh[(uint64_t)l * G];
+    if (l == n_launch) ldiag[DG_BAD_LAUNCH] = n - gh[(uint64_t)l * G];
+  }
+}
+__global__ void __launch_bounds__(LP_THREADS) k_lp_scatter(const dc_pc_sample* __restrict__ smp, uint64_t n, uint32_t n_launch,
+                                                           const uint32_t* __restrict__ gh, uint4* __restrict__ out) { DC_PDL_ENTER();
+  extern __shared__ uint32_t cur[];
+  const uint32_t G = gridDim.x, b = blockIdx.x;
+  for (uint32_t l = threadIdx.x; l <= n_launch; l += LP_THREADS) cur[l] = gh[(uint64_t)l * G + b];
+  __syncthreads();
+  const uint64_t lo = n * b / G, hi = n * (b + 1) / G;
+  const uint4* q = reinterpret_cast<const uint4*>(smp);
+  for (uint64_t j = lo + threadIdx.x; j < hi; j += LP_THREADS) {
+    const uint4 v = __ldg(q + j);
+    const uint32_t pos = atomicAdd(&cur[v.x < n_launch ? v.x : n_launch], 1u);
+    out[pos] = v;
+  }
+}
+
 static dc_status pc_attribute_once(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, const uint32_t* launch_leaf,
                                    uint64_t n_launch, const uint64_t* launch_off, uint32_t S, FillList& fl) {
   const uint64_t N = t->N;
@@ -356,6 +402,41 @@ static dc_status pc_attribute_once(Ctx* c, dc_cct* t, const dc_pc_sample* s, uin
       t->pc_done = true;
       t->state = 1;
       c->bytes_host += 16 * n + 16 * nb + 8 * t->Npc;
+      return DC_OK;
+    }
+  } else if (n && n_launch && n_launch <= LP_MAX && n < (1ull << 32) && !getenv("DC_TEST_PC_GENERIC")) {
+    // launch partition, then the context-owner schedule on the partitioned copy
+    const uint32_t G = (uint32_t)c->num_sms * 2;
+    const size_t lsm = ((size_t)n_launch + 1) * 4;
+    Buf<uint32_t> gh;
+    Buf<uint64_t> loff;
+    Buf<uint4> part;
+    Buf<unsigned long long> pdiag;
+    DC_TRY(alloc(c, gh, ((uint64_t)n_launch + 1) * G));
+    DC_TRY(alloc(c, loff, (uint64_t)n_launch + 1));
+    DC_TRY(alloc(c, part, n));
+    DC_TRY(alloc_zero(c, pdiag, DG_N));
+    {
+      Region rk(c, "pc:partition");
+      DC_SMEM_OPTIN(c, k_lp_count);
+      DC_SMEM_OPTIN(c, k_lp_scatter);
+      dc_launch(k_lp_count, G, LP_THREADS, lsm, c->stream, s, n, (uint32_t)n_launch, gh.p);
+      DC_LAUNCHED(c);
+      DC_TRY(excl_scan<uint32_t>(c, gh.p, gh.p, ((uint64_t)n_launch + 1) * G, nullptr));
+      dc_launch(k_lp_offsets, grid_for(c, n_launch + 1, 256), 256, 0, c->stream, gh.p, (uint32_t)n_launch, G, n, loff.p, pdiag.p);
+      DC_LAUNCHED(c);
+      dc_launch(k_lp_scatter, G, LP_THREADS, lsm, c->stream, s, n, (uint32_t)n_launch, gh.p, part.p);
+      DC_LAUNCHED(c);
+    }
+    uint64_t n_valid = 0;
+    DC_TRY(readback(c, loff.p + n_launch, 8, &n_valid));
+    DC_TRY(pc_owner_hist(c, t, reinterpret_cast<const dc_pc_sample*>(part.p), n_valid, launch_leaf, n_launch, loff.p, S, fl, &nb,
+                         &handled));
+    if (handled) {
+      DC_TRY(add_diag(c, pdiag.p));  // out-of-range launches (counted once: the generic path did not run)
+      t->pc_done = true;
+      t->state = 1;
+      c->bytes_host += 3 * 16 * n + 16 * nb + 8 * t->Npc;
       return DC_OK;
     }
   }

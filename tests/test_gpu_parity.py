@@ -481,15 +481,24 @@ def test_topk_ties_and_large_k(general, monkeypatch):
                 assert got == [(int(e["id"]), int(e["value"]), float(e["fraction"])) for e in exp], (view, k, th)
 
 
-def test_config3s_stress_generic_schedule_vs_oracle():
+@pytest.mark.parametrize("schedule", ["partition", "table"])
+def test_config3s_stress_generic_schedule_vs_oracle(schedule, monkeypatch):
     """Config 3s (gen/stress.py): every launch its own context and the samples of 8 concurrent
-    launches interleaved (no per-launch offsets): the generic schedule, element by element
-    against the oracle on the same re-arranged trace."""
+    launches interleaved (no per-launch offsets): the any-order schedules — the launch partition
+    + context-owner schedule, and the L2 table (DC_TEST_PC_GENERIC) — element by element against
+    the oracle on the same re-arranged trace, with the same invalid-sample counts."""
     from gen import stress
+    if schedule == "table":
+        monkeypatch.setenv("DC_TEST_PC_GENERIC", "1")
     p = gen.programs.config3(n_launch=3000, n_samples=3_000_000)
     tr = stress.make_3s(gen.make_trace(p, n_records=3000, pc=True, n_launch=3000, bad_per_million=500))
     a = gpu_run(tr.offsets.numpy(), keys=tr.keys.numpy(), metrics=tr.metrics.numpy(), samples=tr.samples.numpy(),
                 n_launch=tr.n_launch)
+    dg = a["_ctx"].diag()
+    smp = tr.samples.numpy().view(np.uint32).reshape(-1, 4)
+    bad_l = smp[:, 0] >= tr.n_launch
+    assert dg["samples_bad_launch"] == int(bad_l.sum())
+    assert dg["samples_bad_stall"] == int((~bad_l & ((smp[:, 2] & 0xFFFF) >= 24)).sum())
     oids, _ = oracle.intern(tr.keys.numpy())
     assert np.array_equal(a["ids"], oids)
     ref = oracle_run(tr.offsets.numpy(), oids, tr.metrics.numpy(), p.n_metrics, tr.samples.numpy(), tr.n_launch).arrays()
