@@ -241,9 +241,12 @@ dc_status intern_frames(Ctx* c, const dc_frame_key* keys, uint64_t n, uint32_t* 
     uint32_t* ovp = reinterpret_cast<uint32_t*>(cnt.p + 1);
     {
       Region rk(c, "k:intern_insert");
-      // two CTAs per SM, each walking many keys: the shared key cache warms up once per CTA
-      // (8 waves of short-lived CTAs: 30 us on config 3's 840k keys; 2 waves: 23 us)
-      dc_launch(k_intern_insert, grid_for(c, (n + 3) / 4, 256, 2), 256, 0, c->stream, keys, n, table.p, cap - 1, out_ids, cnt.p, ovp,
+      // CTAs walk at least ~4k keys each (the shared key cache warms up once per CTA), 2 to 8
+      // waves: config 3's 840k keys 30 -> 23 us with 2 waves; large inputs keep 8 waves for
+      // latency hiding (config 2's 32M keys: 0.22 ms with 8, 0.35 with 2)
+      const uint64_t kw = n / (4096ull * (uint64_t)c->num_sms);
+      const int iwaves = kw < 2 ? 2 : kw > 8 ? 8 : (int)kw;
+      dc_launch(k_intern_insert, grid_for(c, (n + 3) / 4, 256, iwaves), 256, 0, c->stream, keys, n, table.p, cap - 1, out_ids, cnt.p, ovp,
                                                                    c->d_flags, mxp);
       DC_LAUNCHED(c);
     }
