@@ -120,6 +120,53 @@ dc_status readback_multi(Ctx* c, std::initializer_list<RB> items) {
   return DC_OK;
 }
 
+struct RBPending {
+  void* host[RB_MAX];
+  uint32_t bytes[RB_MAX], off[RB_MAX];
+  uint32_t n = 0;
+  bool active = false;
+};
+dc_status readback_begin(Ctx* c, std::initializer_list<RB> items) {
+  if (!c->rb_pending) c->rb_pending = new RBPending();
+  if (!c->rb_event) DC_CUDA(c, cudaEventCreateWithFlags(&c->rb_event, cudaEventDisableTiming));
+  RBPending& pd = *c->rb_pending;
+  pd.n = 0;
+  RbItems rb{};
+  rb.dst = (unsigned char*)c->h_pinned;
+  size_t o = 0;
+  for (const RB& it : items) {
+    if (o + it.bytes > 4096 || rb.n == RB_MAX) return fail(c, DC_ERR_ARG, "readback_begin: more than 4 KB or %d items", RB_MAX);
+    if (it.bytes) {
+      rb.src[rb.n] = (const unsigned char*)it.dev;
+      rb.bytes[rb.n] = (uint32_t)it.bytes;
+      rb.off[rb.n] = (uint32_t)o;
+      pd.host[rb.n] = it.host;
+      pd.bytes[rb.n] = (uint32_t)it.bytes;
+      pd.off[rb.n] = (uint32_t)o;
+      ++rb.n;
+    }
+    o += (it.bytes + 7) & ~(size_t)7;
+  }
+  pd.n = rb.n;
+  if (rb.n) {
+    dc_launch(k_readback, 1, 256, 0, c->stream, rb);
+    DC_LAUNCHED(c);
+  }
+  DC_CUDA(c, cudaEventRecord(c->rb_event, c->stream));
+  pd.active = true;
+  return DC_OK;
+}
+dc_status readback_end(Ctx* c) {
+  HostRegion hr(c, "readback");
+  RBPending& pd = *c->rb_pending;
+  if (!pd.active) return fail(c, DC_ERR_STATE, "internal: readback_end without readback_begin");
+  pd.active = false;
+  flush_pending_frees(c);
+  DC_CUDA(c, cudaEventSynchronize(c->rb_event));
+  for (uint32_t i = 0; i < pd.n; ++i) memcpy(pd.host[i], (char*)c->h_pinned + pd.off[i], pd.bytes[i]);
+  return DC_OK;
+}
+
 dc_status flags_status(Ctx* c, uint32_t f) {
   if (f) {
     const char* why = (f & FLAG_BAD_FRAME)    ? "frame id >= n_frames"
@@ -461,6 +508,8 @@ void dc_ctx_destroy(dc_ctx* ctx) {
   cudaFree(ctx->scan_ctr);
   cudaFreeHost(ctx->h_pinned);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+  if (ctx->rb_event) cudaEventDestroy(ctx->rb_event);
+  delete ctx->rb_pending;
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   // outstanding handles keep their arrays: the pool is destroyed once the last one is freed
   // (handles outliving the context free synchronously from now on)

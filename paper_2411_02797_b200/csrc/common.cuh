@@ -26,6 +26,7 @@ enum : uint32_t {
 // device diag slots
 enum { DG_EMPTY = 0, DG_BAD_LAUNCH, DG_BAD_STALL, DG_ZERO, DG_COLL, DG_LEVELS, DG_MAXDEPTH, DG_BYTES, DG_N };
 
+struct RBPending;
 struct Ctx {
   int device = 0;
   uint64_t uid = 0;  // unique per context (handle frees look it up)
@@ -60,6 +61,8 @@ struct Ctx {
   uint32_t* d_flags = nullptr;   // [1]
   uint64_t* d_diag = nullptr;    // [DG_N]
   uint64_t* h_pinned = nullptr;  // small pinned readback buffer
+  cudaEvent_t rb_event = nullptr;  // split-phase readback (readback_begin / readback_end)
+  RBPending* rb_pending = nullptr;
   int num_sms = 148;
   size_t smem_optin = 0;
   std::vector<const void*> smem_set;  // kernels whose dynamic shared-memory cap is raised to smem_optin
@@ -378,6 +381,11 @@ struct RB {
   void* host;
 };
 dc_status readback_multi(Ctx* c, std::initializer_list<RB> items);
+// split-phase readback: _begin enqueues the copy kernel and records an event; work enqueued after
+// it keeps the device busy while the host waits in _end for the event only (speculative launches
+// whose kernels check the read values on the device themselves)
+dc_status readback_begin(Ctx* c, std::initializer_list<RB> items);
+dc_status readback_end(Ctx* c);
 dc_status flags_status(Ctx* c, uint32_t flags);  // DC_ERR_TRACE if any flag bit is set
 dc_status add_diag(Ctx* c, const unsigned long long* src_dev);  // d_diag[i] += src[i], i < DG_N
 

@@ -157,8 +157,17 @@ constexpr int IR_WARPS = 8;
 __global__ void __launch_bounds__(32 * IR_WARPS) k_intern_rank_small(const uint64_t* __restrict__ ka, const uint64_t* __restrict__ kb,
                                                                      const uint32_t* __restrict__ slot_of, const ulonglong2* __restrict__ table,
                                                                      uint32_t* __restrict__ rank_of_slot, dc_frame_key* __restrict__ dict,
-                                                                     uint8_t* __restrict__ kinds, uint32_t D) { DC_PDL_ENTER();
+                                                                     uint8_t* __restrict__ kinds, uint32_t D,
+                                                                     const unsigned long long* d_cnt, const uint32_t* d_ovf,
+                                                                     uint64_t cap) { DC_PDL_ENTER();
   __shared__ uint32_t part[IR_WARPS][32];
+  if (d_cnt) {  // speculative launch (before the host has read D): D from the device, no-op unless
+                // the insert fit (no overflow, at most half load) and D is small enough for this path
+    const uint64_t dd = *d_cnt;
+    if (*d_ovf || dd * 2 > cap || dd > IR_MAX_D) return;
+    D = (uint32_t)dd;
+  }
+  if (blockIdx.x * 32 >= D) return;  // CTA-uniform
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t i = blockIdx.x * 32 + lane;
   const bool ok = i < D;
@@ -188,7 +197,12 @@ __global__ void __launch_bounds__(32 * IR_WARPS) k_intern_rank_small(const uint6
   }
 }
 
-__global__ void k_intern_remap(uint32_t* ids, uint64_t n, const uint32_t* __restrict__ rank_of_slot) { DC_PDL_ENTER();
+__global__ void k_intern_remap(uint32_t* ids, uint64_t n, const uint32_t* __restrict__ rank_of_slot, const unsigned long long* d_cnt,
+                               const uint32_t* d_ovf, uint64_t cap) { DC_PDL_ENTER();
+  if (d_cnt) {  // speculative launch: the same guard as k_intern_rank_small
+    const uint64_t dd = *d_cnt;
+    if (*d_ovf || dd * 2 > cap || dd > IR_MAX_D) return;
+  }
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x)
     ids[j] = rank_of_slot[ids[j]];
 }
@@ -232,6 +246,9 @@ dc_status intern_frames(Ctx* c, const dc_frame_key* keys, uint64_t n, uint32_t* 
   uint64_t cap = next_pow2(2 * (n < (1ull << 15) ? n : (1ull << 15)));
   if (cap < 1024) cap = 1024;
   uint64_t D = 0;
+  Buf<uint64_t> ka, kb, ka2;
+  Buf<uint32_t> slot_of, ord0, ord1, rank_of_slot;
+  bool spec = false;  // compact + small rank + remap enqueued behind the first readback
   for (int attempt = 0; attempt < 2; ++attempt) {
     FillList fl;
     DC_TRY(alloc_fill(c, fl, table, cap, 0xFF));
@@ -251,34 +268,79 @@ dc_status intern_frames(Ctx* c, const dc_frame_key* keys, uint64_t n, uint32_t* 
       DC_LAUNCHED(c);
     }
     uint64_t h[2] = {0, 0};
-    DC_TRY(readback_multi(c, {{cnt.p, 8, &h[0]}, {ovp, 4, &h[1]}, {mxp, 16, mxh}}));
+    spec = attempt == 0 && !getenv("DC_TEST_INTERN_RADIX");
+    if (spec) {
+      // Speculative small path: the host reads (D, overflow, maxima) behind an event while the
+      // device goes on with the compaction, the small rank and the remap, which read D on the
+      // device and do nothing unless the table held the keys at most half full and D <= IR_MAX_D
+      // (then the host takes the retry / radix path below; the dictionary is sized IR_MAX_D).
+      DC_TRY(readback_begin(c, {{cnt.p, 8, &h[0]}, {ovp, 4, &h[1]}, {mxp, 16, mxh}}));
+      DC_TRY(alloc(c, ka, cap));
+      DC_TRY(alloc(c, kb, cap));
+      DC_TRY(alloc(c, slot_of, cap));
+      DC_TRY(alloc(c, rank_of_slot, cap));
+      dc_launch(k_intern_compact, grid_for(c, cap, 256), 256, 0, c->stream, table.p, cap, ka.p, kb.p, slot_of.p,
+                reinterpret_cast<unsigned int*>(cnt.p + 4));
+      DC_LAUNCHED(c);
+      DC_TRY(palloc(c, d->keys, IR_MAX_D));
+      DC_TRY(palloc(c, d->kinds, IR_MAX_D));
+      dc_launch(k_intern_rank_small, (uint32_t)(IR_MAX_D / 32), 32 * IR_WARPS, 0, c->stream, ka.p, kb.p, slot_of.p, table.p,
+                rank_of_slot.p, d->keys, d->kinds, (uint32_t)0, (const unsigned long long*)cnt.p, (const uint32_t*)ovp, cap);
+      DC_LAUNCHED(c);
+      dc_launch(k_intern_remap, grid_for(c, n, 256), 256, 0, c->stream, out_ids, n, rank_of_slot.p, (const unsigned long long*)cnt.p,
+                (const uint32_t*)ovp, cap);
+      DC_LAUNCHED(c);
+      DC_TRY(readback_end(c));
+    } else {
+      DC_TRY(readback_multi(c, {{cnt.p, 8, &h[0]}, {ovp, 4, &h[1]}, {mxp, 16, mxh}}));
+    }
     D = h[0];
     bool overflow = (uint32_t)h[1] != 0;
     if (!overflow && D * 2 <= cap) break;
     if (attempt == 1) return fail(c, DC_ERR_CAPACITY, "dc_intern_frames: hash table overflow");
+    if (spec) {  // the speculative kernels did nothing: drop their dictionary arrays
+      cudaFreeAsync(d->keys, c->stream);
+      cudaFreeAsync(d->kinds, c->stream);
+      d->keys = nullptr;
+      d->kinds = nullptr;
+      spec = false;
+    }
     cap = next_pow2(2 * n);
     if (cap < 1024) cap = 1024;
   }
   d->D = D;
-  Buf<uint64_t> ka, kb, ka2;
-  Buf<uint32_t> slot_of, ord0, ord1, rank_of_slot;
-  DC_TRY(alloc(c, ka, D));
-  DC_TRY(alloc(c, kb, D));
+  if (spec && D <= IR_MAX_D) {  // the speculative small path was right: everything is enqueued
+    c->bytes_host += 20 * n + 16 * D;
+    guard.h = nullptr;
+    *out = d;
+    return DC_OK;
+  }
+  if (spec) {  // D > IR_MAX_D: keys / slots are compacted already; the dictionary is resized below
+    cudaFreeAsync(d->keys, c->stream);
+    cudaFreeAsync(d->kinds, c->stream);
+    d->keys = nullptr;
+    d->kinds = nullptr;
+  } else {
+    DC_TRY(alloc(c, ka, D));
+    DC_TRY(alloc(c, kb, D));
+    DC_TRY(alloc(c, slot_of, D));
+    DC_TRY(alloc(c, rank_of_slot, cap));
+    dc_launch(k_intern_compact, grid_for(c, cap, 256), 256, 0, c->stream, table.p, cap, ka.p, kb.p, slot_of.p,
+              reinterpret_cast<unsigned int*>(cnt.p + 4));
+    DC_LAUNCHED(c);
+  }
   DC_TRY(alloc(c, ka2, D));
-  DC_TRY(alloc(c, slot_of, D));
   DC_TRY(alloc(c, ord0, D));
   DC_TRY(alloc(c, ord1, D));
-  DC_TRY(alloc(c, rank_of_slot, cap));
-  unsigned int* pos = reinterpret_cast<unsigned int*>(cnt.p + 4);  // zeroed with the counters
-  dc_launch(k_intern_compact, grid_for(c, cap, 256), 256, 0, c->stream, table.p, cap, ka.p, kb.p, slot_of.p, pos);
-  DC_LAUNCHED(c);
-  if (D <= IR_MAX_D && !getenv("DC_TEST_INTERN_RADIX")) {
+  if (D <= IR_MAX_D && !spec && !getenv("DC_TEST_INTERN_RADIX")) {  // small D after a retry
     DC_TRY(palloc(c, d->keys, D));
     DC_TRY(palloc(c, d->kinds, D));
     dc_launch(k_intern_rank_small, (uint32_t)((D + 31) / 32), 32 * IR_WARPS, 0, c->stream, ka.p, kb.p, slot_of.p, table.p,
-              rank_of_slot.p, d->keys, d->kinds, (uint32_t)D);
+              rank_of_slot.p, d->keys, d->kinds, (uint32_t)D, (const unsigned long long*)nullptr, (const uint32_t*)nullptr,
+              (uint64_t)0);
     DC_LAUNCHED(c);
-    dc_launch(k_intern_remap, grid_for(c, n, 256), 256, 0, c->stream, out_ids, n, rank_of_slot.p);
+    dc_launch(k_intern_remap, grid_for(c, n, 256), 256, 0, c->stream, out_ids, n, rank_of_slot.p,
+              (const unsigned long long*)nullptr, (const uint32_t*)nullptr, (uint64_t)0);
     DC_LAUNCHED(c);
     c->bytes_host += 20 * n + 16 * D;
     guard.h = nullptr;
@@ -302,7 +364,8 @@ dc_status intern_frames(Ctx* c, const dc_frame_key* keys, uint64_t n, uint32_t* 
   dc_launch(k_intern_rank, grid_for(c, D, 256), 256, 0, c->stream, final_ord, slot_of.p, table.p, rank_of_slot.p, d->keys,
                                                             d->kinds, D);
   DC_LAUNCHED(c);
-  dc_launch(k_intern_remap, grid_for(c, n, 256), 256, 0, c->stream, out_ids, n, rank_of_slot.p);
+  dc_launch(k_intern_remap, grid_for(c, n, 256), 256, 0, c->stream, out_ids, n, rank_of_slot.p,
+            (const unsigned long long*)nullptr, (const uint32_t*)nullptr, (uint64_t)0);
   DC_LAUNCHED(c);
   c->bytes_host += 20 * n + 16 * D;
   guard.h = nullptr;

@@ -404,7 +404,7 @@ def test_attribute_contended_columns(monkeypatch, direct):
     assert_same(a, ref, ctx=f"contended direct={direct}")
 
 
-@pytest.mark.parametrize("D,radix", [(3000, False), (3000, True), (20000, False), (1, False)])
+@pytest.mark.parametrize("D,radix", [(3000, False), (3000, True), (20000, False), (40000, False), (1, False)])
 def test_intern_rank_paths(D, radix, monkeypatch):
     """Frame interning: the direct-count rank (D <= 8192) and the two-pass radix sort (forced, or
     D > 8192) give the oracle's ids and sorted dictionary; keys share kinds / strings / addresses
