@@ -715,12 +715,41 @@ __device__ __forceinline__ void sr_block_sum_max(uint32_t& sum, uint32_t& mx) {
   __syncthreads();
 }
 
+// Speculative small-P build (launched behind the record pass's readback, before the host knows
+// P): the gate decides on the device exactly what the host decides after the readback (same
+// integer conditions), and k_small_rank / k_small_emit do nothing when it says no.
+struct SmallSpec {
+  uint32_t ok, P, Lmax, pad;
+};
+constexpr uint64_t SPEC_NODES = 57857;  // node arrays of a speculative build: 1 + hsum fits the rank smem
+__device__ __host__ inline bool small_spec_ok(uint32_t overflow, uint32_t flags, uint64_t P, uint64_t hsum, uint64_t Lmax,
+                                              uint64_t smem_optin) {
+  const uint64_t rank_smem = ((16ull * P + 15) & ~15ull) + 4ull * (hsum + 3ull * P);
+  return !overflow && !flags && P <= SMALL_P && rank_smem + 1024 <= smem_optin && Lmax <= DC_MAX_DEPTH && 1 + hsum <= SPEC_NODES;
+}
+__global__ void k_small_gate(const unsigned int* __restrict__ cnt, const unsigned long long* __restrict__ sumlen,
+                             const unsigned long long* __restrict__ maxd, const uint32_t* __restrict__ flags, uint64_t smem_optin,
+                             SmallSpec* __restrict__ spec) { DC_PDL_ENTER();
+  if (threadIdx.x == 0) {
+    const uint32_t P = cnt[0] + cnt[1];
+    const uint64_t Lmax = *maxd;
+    spec->ok = small_spec_ok(cnt[3], *flags, P, *sumlen, Lmax, smem_optin) ? 1u : 0u;
+    spec->P = P;
+    spec->Lmax = (uint32_t)(Lmax < DC_MAX_DEPTH ? Lmax : DC_MAX_DEPTH);
+  }
+}
+
 __global__ void __launch_bounds__(SR_THREADS, 1) k_small_rank(const uint64_t* __restrict__ off, const uint32_t* __restrict__ frames,
                                                                const uint32_t* __restrict__ item_rec, const uint32_t* __restrict__ item_len,
                                                                uint32_t P, uint32_t* __restrict__ sorted_item, uint32_t* __restrict__ lcp_s,
                                                                uint32_t* __restrict__ len_s, uint64_t* __restrict__ po_s,
-                                                               uint32_t* __restrict__ leaf_of_item) { DC_PDL_ENTER();
+                                                               uint32_t* __restrict__ leaf_of_item, const SmallSpec* spec) { DC_PDL_ENTER();
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  if (spec) {  // speculative launch: P from the gate, nothing to do unless it said yes
+    if (!spec->ok) return;
+    P = spec->P;
+  }
+  if (blockIdx.x >= (P ? P : 1u)) return;  // CTA-uniform
   uint64_t* spo = reinterpret_cast<uint64_t*>(smem_raw);     // [P] first frame of path i (global)
   uint32_t* sstart = reinterpret_cast<uint32_t*>(spo + P);   // [P] first 16-B chunk of path i
   uint32_t* slen = sstart + P;                               // [P]
@@ -815,7 +844,12 @@ __global__ void __launch_bounds__(SR_THREADS) k_small_emit(const uint64_t* __res
                                                             const uint32_t* __restrict__ len_s, uint32_t Lmax, uint32_t* __restrict__ parent,
                                                             uint32_t* __restrict__ frame_out, uint16_t* __restrict__ depth,
                                                             uint32_t* __restrict__ level_off, uint32_t* __restrict__ leaf_of_item,
-                                                            uint32_t* d_N) { DC_PDL_ENTER();
+                                                            uint32_t* d_N, const SmallSpec* spec) { DC_PDL_ENTER();
+  if (spec) {  // speculative launch (grid DC_MAX_DEPTH + 1): P and Lmax from the gate
+    if (!spec->ok || blockIdx.x > spec->Lmax) return;
+    P = spec->P;
+    Lmax = spec->Lmax;
+  }
   const uint32_t d = blockIdx.x + 1;
   // nodes above depth d and above depth d - 1 (level_off[d] - 1, level_off[d-1] - 1)
   uint32_t above = 0, above_p = 0, maxlen = 0, dups = 0;
@@ -1375,6 +1409,11 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
   DC_TRY(alloc(c, item_rec, ibound));
   DC_TRY(alloc(c, item_len, ibound));
   DC_TRY(alloc(c, leaf_of_item, ibound));
+  // speculative small-P build (see below)
+  bool spec = false, spec_ok = false;
+  Buf<SmallSpec> sspec;
+  Buf<uint32_t> sdN, ssrt, slcp, slen;
+  Buf<uint64_t> spos;
   for (int attempt = 0;; ++attempt) {
     if (attempt) {  // a larger table: fresh table, counters [0..3] ([4] empty paths kept), length sum
       FillList fl;
@@ -1396,8 +1435,50 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
     dc_launch(k_items_finish, grid_for(c, ibound, 256), 256, 0, c->stream, item_rec.p, extra_rec.p, p->offsets, item_len.p, sumlen.p,
               cnt.p, (unsigned long long*)c->d_diag);
     DC_LAUNCHED(c);
-    DC_TRY(readback_multi(c, {{cnt.p, 32, hc}, {sumlen.p, 8, &hsum}, {c->d_diag + DG_MAXDEPTH, 8, &hmaxd}, {c->d_flags, 4, &hflags},
-                              {p->offsets + R, 8, &F}}));
+    spec = attempt == 0 && !getenv("DC_TEST_BUILD_LEVELS") && !getenv("DC_TEST_BUILD_NOSPEC");
+    if (spec) {
+      // Speculative small-P build behind the readback: the device keeps ranking and emitting the
+      // tree while the host reads (P, sum of lengths, depth, flags); k_small_gate applies on the
+      // device the same test the host applies below, so both agree on whether it ran.
+      DC_TRY(readback_begin(c, {{cnt.p, 32, hc}, {sumlen.p, 8, &hsum}, {c->d_diag + DG_MAXDEPTH, 8, &hmaxd},
+                                {c->d_flags, 4, &hflags}, {p->offsets + R, 8, &F}}));
+      DC_TRY(alloc(c, sspec, 1));
+      DC_TRY(alloc(c, sdN, 3));
+      DC_TRY(alloc(c, spos, SMALL_P));
+      DC_TRY(alloc(c, ssrt, SMALL_P));
+      DC_TRY(alloc(c, slcp, SMALL_P));
+      DC_TRY(alloc(c, slen, SMALL_P));
+      DC_TRY(palloc(c, t->parent, SPEC_NODES));
+      DC_TRY(palloc(c, t->frame, SPEC_NODES));
+      DC_TRY(palloc(c, t->depth, SPEC_NODES));
+      DC_TRY(palloc(c, t->level_off, (uint64_t)DC_MAX_DEPTH + 2));
+      dc_launch(k_small_gate, 1, 32, 0, c->stream, (const unsigned int*)cnt.p, (const unsigned long long*)sumlen.p,
+                (const unsigned long long*)(c->d_diag + DG_MAXDEPTH), (const uint32_t*)c->d_flags, (uint64_t)c->smem_optin, sspec.p);
+      DC_LAUNCHED(c);
+      DC_SMEM_OPTIN(c, k_small_rank);
+      if (!c->small_rank_smem) {
+        cudaFuncAttributes fa;
+        DC_CUDA(c, cudaFuncGetAttributes(&fa, k_small_rank));
+        c->small_rank_smem = c->smem_optin - fa.sharedSizeBytes;
+      }
+      dc_launch(k_small_rank, (uint32_t)c->num_sms, SR_THREADS, c->small_rank_smem, c->stream, p->offsets, p->frames, item_rec.p,
+                item_len.p, 0u, ssrt.p, slcp.p, slen.p, spos.p, leaf_of_item.p, (const SmallSpec*)sspec.p);
+      DC_LAUNCHED(c);
+      dc_launch(k_small_emit, (uint32_t)DC_MAX_DEPTH + 1, SR_THREADS, 0, c->stream, spos.p, p->frames, 0u, ssrt.p, slcp.p, slen.p, 0u,
+                t->parent, t->frame, t->depth, t->level_off, leaf_of_item.p, sdN.p, (const SmallSpec*)sspec.p);
+      DC_LAUNCHED(c);
+      DC_TRY(readback_end(c));
+    } else {
+      DC_TRY(readback_multi(c, {{cnt.p, 32, hc}, {sumlen.p, 8, &hsum}, {c->d_diag + DG_MAXDEPTH, 8, &hmaxd}, {c->d_flags, 4, &hflags},
+                                {p->offsets + R, 8, &F}}));
+    }
+    spec_ok = spec && small_spec_ok(hc[3], hflags, (uint64_t)hc[0] + hc[1], hsum, hmaxd, c->smem_optin);
+    if (spec && !spec_ok) {  // the speculative kernels did nothing: the node arrays are sized below
+      void* q[] = {t->parent, t->frame, t->depth, t->level_off};
+      for (void* x : q) cudaFreeAsync(x, c->stream);
+      t->parent = t->frame = t->level_off = nullptr;
+      t->depth = nullptr;
+    }
     if (!hc[3]) break;
     if ((hc[3] & 2) || attempt > 2 || cap >= (1ull << 31))
       return fail(c, DC_ERR_CAPACITY, "dc_cct_build: path table overflow");
@@ -1409,14 +1490,23 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
   if (Nbound >= (1ull << 32)) return fail(c, DC_ERR_CAPACITY, "dc_cct_build: more than 2^32 nodes");
   // hmaxd is the deepest path seen on this context so far (>= this trace's): sizes level_off
   const uint32_t Lmax = (uint32_t)hmaxd;
-  DC_TRY(palloc(c, t->parent, Nbound));
-  DC_TRY(palloc(c, t->frame, Nbound));
-  DC_TRY(palloc(c, t->depth, Nbound));
-  DC_TRY(palloc(c, t->level_off, (uint64_t)Lmax + 2));
+  if (!spec_ok) {
+    DC_TRY(palloc(c, t->parent, Nbound));
+    DC_TRY(palloc(c, t->frame, Nbound));
+    DC_TRY(palloc(c, t->depth, Nbound));
+    DC_TRY(palloc(c, t->level_off, (uint64_t)Lmax + 2));
+  }
   uint64_t N = 0;
   uint32_t levels = 0;
   const uint64_t rank_smem = ((16ull * P + 15) & ~15ull) + 4ull * (hsum + 3ull * P);
-  if (P <= SMALL_P && rank_smem + 1024 <= c->smem_optin && !getenv("DC_TEST_BUILD_LEVELS")) {
+  if (spec_ok) {  // ranked and emitted already (speculative kernels): only the node count is read
+    uint32_t hN[3] = {0, 0, 0};
+    DC_TRY(readback(c, sdN.p, 12, hN));
+    N = hN[0];
+    t->max_depth = hN[1];
+    if (hN[2] > n_extra && getenv("DC_STRICT"))
+      return fail(c, DC_ERR_STATE, "internal: %u of %u path items repeat a path (%u collision extras)", hN[2], P, n_extra);
+  } else if (P <= SMALL_P && rank_smem + 1024 <= c->smem_optin && !getenv("DC_TEST_BUILD_LEVELS")) {
     // lexicographic rank of the distinct paths + one CTA per depth (no level loop)
     Buf<uint32_t> dN, srt, lcp, len;
     Buf<uint64_t> pos;
@@ -1428,10 +1518,10 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
     DC_SMEM_OPTIN(c, k_small_rank);
     const uint32_t G = P == 0 ? 1u : P < (uint32_t)c->num_sms ? P : (uint32_t)c->num_sms;
     dc_launch(k_small_rank, G, SR_THREADS, rank_smem, c->stream, p->offsets, p->frames, item_rec.p, item_len.p, P, srt.p, lcp.p,
-              len.p, pos.p, leaf_of_item.p);
+              len.p, pos.p, leaf_of_item.p, (const SmallSpec*)nullptr);
     DC_LAUNCHED(c);
     dc_launch(k_small_emit, Lmax + 1, SR_THREADS, 0, c->stream, pos.p, p->frames, P, srt.p, lcp.p, len.p, Lmax,
-              t->parent, t->frame, t->depth, t->level_off, leaf_of_item.p, dN.p);
+              t->parent, t->frame, t->depth, t->level_off, leaf_of_item.p, dN.p, (const SmallSpec*)nullptr);
     DC_LAUNCHED(c);
     uint32_t hN[3] = {0, 0, 0};
     DC_TRY(readback(c, dN.p, 12, hN));

@@ -67,6 +67,7 @@ struct Ctx {
   size_t smem_optin = 0;
   std::vector<const void*> smem_set;  // kernels whose dynamic shared-memory cap is raised to smem_optin
   int path_hash_per_sm = 0;           // cached occupancy of k_path_hash
+  size_t small_rank_smem = 0;         // k_small_rank's largest dynamic shared memory
   uint64_t launches = 0;
   uint64_t bytes_host = 0;       // host-accumulated algorithmic bytes
   uint64_t host_levels = 0;      // tree levels built

@@ -234,12 +234,15 @@ def test_owner_work_stealing_skewed_contexts(n_launch, heavy, pcs, monkeypatch):
     assert_same(a, ref, ctx=f"owner skewed n_launch={n_launch}")
 
 
-@pytest.mark.parametrize("levels", [False, True])
-def test_small_build_deep_and_prefix_paths(levels, monkeypatch):
+@pytest.mark.parametrize("builder", ["rank_spec", "rank", "levels"])
+def test_small_build_deep_and_prefix_paths(builder, monkeypatch):
     """Small-P build at the depth limit: chains up to 1000 frames, paths that are prefixes of
-    other paths, shared deep prefixes that branch late, an empty path; both small-P builders."""
-    if levels:
+    other paths, shared deep prefixes that branch late, an empty path; both small-P builders,
+    the rank builder launched speculatively (behind the record pass's readback) and not."""
+    if builder == "levels":
         monkeypatch.setenv("DC_TEST_BUILD_LEVELS", "1")
+    if builder == "rank":
+        monkeypatch.setenv("DC_TEST_BUILD_NOSPEC", "1")
     rng = np.random.default_rng(77)
     base = [int(x) for x in rng.integers(0, 40, 1000)]
     paths = [tuple(base), tuple(base[:500]), tuple(base[:499] + [41]), tuple(base[:999] + [0]), (), tuple(base[:1]),
