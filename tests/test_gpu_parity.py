@@ -252,7 +252,7 @@ def test_small_build_deep_and_prefix_paths(builder, monkeypatch):
     X = rng.integers(0, 1000, size=(1, len(paths)), dtype=np.uint64)
     a = gpu_run(off, fr, X, n_frames=42)
     ref = oracle_run(off, fr, X, 1).arrays()
-    assert_same(a, ref, ctx=f"deep small build levels={levels}")
+    assert_same(a, ref, ctx=f"deep small build {builder}")
 
 
 def test_dedup_independent_of_tile_staging():
