@@ -1499,13 +1499,10 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
   uint64_t N = 0;
   uint32_t levels = 0;
   const uint64_t rank_smem = ((16ull * P + 15) & ~15ull) + 4ull * (hsum + 3ull * P);
-  if (spec_ok) {  // ranked and emitted already (speculative kernels): only the node count is read
-    uint32_t hN[3] = {0, 0, 0};
-    DC_TRY(readback(c, sdN.p, 12, hN));
-    N = hN[0];
-    t->max_depth = hN[1];
-    if (hN[2] > n_extra && getenv("DC_STRICT"))
-      return fail(c, DC_ERR_STATE, "internal: %u of %u path items repeat a path (%u collision extras)", hN[2], P, n_extra);
+  uint32_t hN3[3] = {0, 0, 0};
+  if (spec_ok) {  // ranked and emitted already (speculative kernels): the node count is read behind
+                  // the leaf kernels and the count-column fill below (split-phase readback)
+    DC_TRY(readback_begin(c, {{sdN.p, 12, hN3}}));
   } else if (P <= SMALL_P && rank_smem + 1024 <= c->smem_optin && !getenv("DC_TEST_BUILD_LEVELS")) {
     // lexicographic rank of the distinct paths + one CTA per depth (no level loop)
     Buf<uint32_t> dN, srt, lcp, len;
@@ -1554,7 +1551,6 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
     }
   }
   // max depth of this tree
-  t->N = N;
   uint32_t* leaf = out_leaf;
   if (!leaf) {
     DC_TRY(alloc(c, leafbuf, R));
@@ -1569,20 +1565,30 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
                                                                      leaf);
     DC_LAUNCHED(c);
   }
+  // node columns (exclusive/inclusive counts), metric columns come with attribute; a speculative
+  // build sizes them by its node bound (the node count is still in flight)
+  const uint64_t Ncols = spec_ok ? SPEC_NODES : N;
+  DC_TRY(palloc(c, t->xcnt, Ncols));
+  DC_TRY(palloc(c, t->icnt, Ncols));
+  // icnt is written whole by dc_cct_rollup (every schedule) and unreadable before it
+  {
+    FillList fx;
+    DC_TRY(fill_add(c, fx, t->xcnt, Ncols * 8));
+    DC_TRY(fill_flush(c, fx));
+  }
+  if (spec_ok) {
+    DC_TRY(readback_end(c));
+    N = hN3[0];
+    t->max_depth = hN3[1];
+    if (hN3[2] > n_extra && getenv("DC_STRICT"))
+      return fail(c, DC_ERR_STATE, "internal: %u of %u path items repeat a path (%u collision extras)", hN3[2], P, n_extra);
+  }
+  t->N = N;
   // depth of the tree = largest d with a node
   if (P > SMALL_P) {
     uint16_t md = 0;
     if (N > 1) DC_TRY(readback(c, t->depth + (N - 1), 2, &md));
     t->max_depth = md;
-  }
-  // node columns (exclusive/inclusive counts), metric columns come with attribute
-  DC_TRY(palloc(c, t->xcnt, N));
-  DC_TRY(palloc(c, t->icnt, N));
-  // icnt is written whole by dc_cct_rollup (every schedule) and unreadable before it
-  {
-    FillList fx;
-    DC_TRY(fill_add(c, fx, t->xcnt, N * 8));
-    DC_TRY(fill_flush(c, fx));
   }
   // algorithmic bytes: offsets + frames of every record once, leaf, node table
   c->bytes_host += 8 * (R + 1) + 4 * F + 4 * R + 10 * N;
