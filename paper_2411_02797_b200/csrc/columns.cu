@@ -396,7 +396,10 @@ __global__ void __launch_bounds__(256) k_rollup_levels(RollArgs a) { DC_PDL_ENTE
 // inclusive column is written whole (no copy of the exclusive block first): 2 launches.
 // Column c: 0 count; 1 + 6m + {0 sum, 1 min, 2..5 square limb 0..3}; 1 + 6M samples; 2 + 6M + s stall s.
 constexpr uint32_t RC_MAX_N = 26u << 10;
-constexpr int RC_THREADS = 1024;
+#ifndef DC_RC_THREADS
+#define DC_RC_THREADS 1024
+#endif
+constexpr int RC_THREADS = DC_RC_THREADS;  // (A/B builds: 256 / 512)
 __global__ void __launch_bounds__(RC_THREADS, 1) k_roll_cols(const uint32_t* __restrict__ parent, const uint32_t* __restrict__ level_off,
                                                             uint32_t maxd, uint32_t N, uint32_t M, const uint64_t* __restrict__ xcnt,
                                                             uint64_t* __restrict__ icnt, uint64_t* __restrict__ mcols,
