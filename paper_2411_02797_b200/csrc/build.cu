@@ -696,6 +696,7 @@ __global__ void __launch_bounds__(SB_THREADS, 1) k_build_small(const uint64_t* _
 // paths staged in shared memory in 16-B chunks; LCP with the predecessor = the largest LCP over
 // the smaller paths) and one CTA per depth that numbers and writes that level.
 constexpr int SR_THREADS = 512;
+constexpr uint32_t SR_WARPS = SR_THREADS / 32;
 __device__ __forceinline__ void sr_block_sum_max(uint32_t& sum, uint32_t& mx) {
   __shared__ uint32_t s_sum[SR_THREADS / 32], s_max[SR_THREADS / 32];
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -749,7 +750,7 @@ __global__ void __launch_bounds__(SR_THREADS, 1) k_small_rank(const uint64_t* __
     if (!spec->ok) return;
     P = spec->P;
   }
-  if (blockIdx.x >= (P ? P : 1u)) return;  // CTA-uniform
+  if (blockIdx.x * SR_WARPS >= (P ? P : 1u)) return;  // CTA-uniform: no item for this CTA's warps
   uint64_t* spo = reinterpret_cast<uint64_t*>(smem_raw);     // [P] first frame of path i (global)
   uint32_t* sstart = reinterpret_cast<uint32_t*>(spo + P);   // [P] first 16-B chunk of path i
   uint32_t* slen = sstart + P;                               // [P]
@@ -801,12 +802,14 @@ __global__ void __launch_bounds__(SR_THREADS, 1) k_small_rank(const uint64_t* __
       if (qq[u] < C) chunks[qq[u]] = v[u];
   }
   __syncthreads();
-  for (uint32_t i = blockIdx.x; i < P; i += gridDim.x) {
+  // one warp per item: its lanes compare it with every path (no block barrier per item)
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t i = blockIdx.x * SR_WARPS + (threadIdx.x >> 5); i < P; i += gridDim.x * SR_WARPS) {
     const uint32_t Li = slen[i];
     const uint4* A = chunks + sstart[i];
     const uint32_t* a = fr + 4ull * sstart[i];
     uint32_t rank = 0, mlcp = 0;
-    for (uint32_t j = threadIdx.x; j < P; j += SR_THREADS) {
+    for (uint32_t j = lane; j < P; j += 32) {
       const uint32_t Lj = slen[j];
       const uint4* B = chunks + sstart[j];
       const uint32_t* b = fr + 4ull * sstart[j];
@@ -826,8 +829,9 @@ __global__ void __launch_bounds__(SR_THREADS, 1) k_small_rank(const uint64_t* __
         mlcp = max(mlcp, m);
       }
     }
-    sr_block_sum_max(rank, mlcp);
-    if (threadIdx.x == 0) {
+    rank = __reduce_add_sync(0xffffffffu, rank);
+    mlcp = __reduce_max_sync(0xffffffffu, mlcp);
+    if (lane == 0) {
       sorted_item[rank] = i;
       lcp_s[rank] = mlcp;  // the predecessor in lex order shares the longest prefix
       len_s[rank] = Li;
@@ -1513,7 +1517,8 @@ dc_status cct_build(Ctx* c, const dc_paths* p, const dc_dict* dict, uint32_t n_f
     DC_TRY(alloc(c, lcp, P));
     DC_TRY(alloc(c, len, P));
     DC_SMEM_OPTIN(c, k_small_rank);
-    const uint32_t G = P == 0 ? 1u : P < (uint32_t)c->num_sms ? P : (uint32_t)c->num_sms;
+    const uint32_t Gi = (P + SR_WARPS - 1) / SR_WARPS;  // one warp per item
+    const uint32_t G = Gi == 0 ? 1u : Gi < (uint32_t)c->num_sms ? Gi : (uint32_t)c->num_sms;
     dc_launch(k_small_rank, G, SR_THREADS, rank_smem, c->stream, p->offsets, p->frames, item_rec.p, item_len.p, P, srt.p, lcp.p,
               len.p, pos.p, leaf_of_item.p, (const SmallSpec*)nullptr);
     DC_LAUNCHED(c);
