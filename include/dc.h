@@ -185,7 +185,11 @@ typedef struct { uint32_t launch, pc_off; uint16_t stall, flags; uint32_t count;
                      s[off[l] .. off[l+1]) (as delivered per kernel activity buffer,
                      PAPER.md:355-356) and the context-owner histogram schedule is used; a
                      sample whose launch field disagrees with its segment is still
-                     attributed by its own launch field. NULL selects the generic schedule.
+                     attributed by its own launch field. NULL: samples in any order; with
+                     n_launch <= 49,152 they are first partitioned by launch on the device (a
+                     scratch copy of the samples, n x 16 B) and the context-owner schedule runs
+                     on the copy; with more launches an L2 hash-table schedule is used. Same
+                     results either way.
    n_stall           <= DC_MAX_STALL; fixed by the first call on a handle (DC_ERR_ARG if a
                      later call differs).
    Accumulates: may be called repeatedly, e.g. once per chunk / activity buffer of samples
