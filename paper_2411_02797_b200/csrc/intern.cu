@@ -63,6 +63,8 @@ __global__ void __launch_bounds__(256) k_intern_insert(const dc_frame_key* __res
     if (found == 0xFFFFFFFFu) {  // ---- L2 table
       uint64_t s = h & mask;
       for (uint64_t probe = 0; probe <= (mask < 4096 ? mask : 4096); ++probe, s = (s + 1) & mask) {  // bounded: overflow, retried larger
+        // past half load the host retries with a larger table anyway: stop walking long runs
+        if (probe == 32 && ld_relaxed_u64(d_count) * 2 > mask + 1) break;
         ulonglong2 cur = ld_relaxed_v2(table + s);
         if (cur.x == lo && cur.y == hi && hi != EMPTY) { found = (uint32_t)s; break; }
         bool maybe_partial = ((uint32_t)cur.x == 0xFFFFFFFFu) || cur.y == EMPTY;  // empty, or a torn read of a claim
@@ -223,7 +225,8 @@ static uint64_t next_pow2(uint64_t v) {
   return p;
 }
 
-dc_status intern_frames(Ctx* c, const dc_frame_key* keys, uint64_t n, uint32_t* out_ids, dc_dict** out) {
+// d_hint: expected distinct keys (0: unknown; the first table then has 64K slots)
+dc_status intern_frames(Ctx* c, const dc_frame_key* keys, uint64_t n, uint32_t* out_ids, dc_dict** out, uint64_t d_hint) {
   dc_dict* d = new dc_dict();
   HandleGuard<dc_dict, dc_dict_free> guard{d};  // frees the dictionary on any error return
   d->device = c->device;
@@ -244,6 +247,7 @@ dc_status intern_frames(Ctx* c, const dc_frame_key* keys, uint64_t n, uint32_t* 
   // distinct keys are few in practice (hundreds to tens of thousands): start with a 64K-slot table
   // (1 MB to clear and compact) and retry once with a table sized by the keys if it overflows
   uint64_t cap = next_pow2(2 * (n < (1ull << 15) ? n : (1ull << 15)));
+  if (d_hint) cap = std::max<uint64_t>(cap, next_pow2(2 * (d_hint < n ? d_hint : n)));
   if (cap < 1024) cap = 1024;
   uint64_t D = 0;
   Buf<uint64_t> ka, kb, ka2;

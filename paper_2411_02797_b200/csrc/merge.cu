@@ -26,7 +26,7 @@
 #endif
 
 namespace dc {
-dc_status intern_frames(Ctx* c, const dc_frame_key* keys, uint64_t n, uint32_t* out_ids, dc_dict** out);
+dc_status intern_frames(Ctx* c, const dc_frame_key* keys, uint64_t n, uint32_t* out_ids, dc_dict** out, uint64_t d_hint = 0);
 dc_status ensure_metric_cols(Ctx* c, dc_cct* t, uint32_t M);
 
 // record layout, in u64 words
@@ -734,7 +734,9 @@ static dc_status unify_dicts(Ctx* c, const dc_frame_key* all_keys, const std::ve
   const uint64_t total = key_off.back();
   Buf<uint32_t> ids;
   DC_TRY(alloc(c, ids, total));
-  DC_TRY(intern_frames(c, all_keys, total, ids.p, gdict));
+  uint64_t dmax = 0;  // the union has at least the largest rank's distinct keys, at most all of them
+  for (size_t p = 0; p + 1 < key_off.size(); ++p) dmax = std::max<uint64_t>(dmax, key_off[p + 1] - key_off[p]);
+  DC_TRY(intern_frames(c, all_keys, total, ids.p, gdict, std::min<uint64_t>(total, 2 * dmax)));
   l2g.resize(key_off.size() - 1);
   for (size_t p = 0; p + 1 < key_off.size(); ++p) {
     const uint64_t D = key_off[p + 1] - key_off[p];

@@ -1,8 +1,9 @@
 #!/usr/bin/env python
 """Times dc_cct_merge_local (the merge's partition / exchange / reduce / canonicalise kernels
 with a loopback exchange) over P logical ranks on one GPU, per phase (library CUDA-event
-timers), for config 3 (P traces of 100M PC samples, different seeds) or config 5 (P shards of
-125M records). Prints one JSON line. Usage: python tools/merge_bench.py [--config 3|5] [--P 8]"""
+timers), for config 3 (P traces of 100M PC samples, different seeds), config 5 (P shards of 125M
+records) or config 4 with --records (SURVEY's "5m" merge-stress variant: P shards of the cfg-4
+shape). Prints one JSON line. Usage: python tools/merge_bench.py [--config 3|4|5] [--P 8] [--records R]"""
 import argparse
 import json
 import os
@@ -31,7 +32,12 @@ def main():
         F = int(tr.offsets[-1].item())
         tr.ids_buf = torch.empty(F, dtype=torch.int32, device="cuda")
         tr.leaf_buf = torch.empty(tr.n_records, dtype=torch.int32, device="cuda")
-        ids, d = dc.dc_intern_frames(ctx, tr.keys, tr.ids_buf)
+        if args.config == 4:  # pre-interned ids: the program's sorted pool is the dictionary (as bench.py)
+            import numpy as np
+            keys = torch.from_numpy(np.ascontiguousarray(prog.pool_keys).view(np.int32).reshape(-1, 4).copy()).cuda()
+            d = tr.dict = dc.dc_dict_from_sorted(ctx, keys)
+        else:
+            ids, d = dc.dc_intern_frames(ctx, tr.keys, tr.ids_buf)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         cct, _ = bench.run_step(dc, ctx, tr, args.config, want_views=False)
         ctx.sync()
@@ -56,7 +62,7 @@ def main():
         merged.free()
     rep = ctx.timer_report()
     ctx.set_timing(False)
-    phases = {k: round(v[1] / v[0], 3) for k, v in rep.items() if k.startswith("merge")}
+    phases = {k: round(v[1] / v[0], 3) for k, v in rep.items() if k.startswith("merge") or os.environ.get("MB_ALL")}
     print(json.dumps({"merge_local": {"config": args.config, "P": args.P, "local_nodes": int(v0.n_nodes),
                                       "local_bins": int(v0.n_bins), "merged_nodes": int(mv.n_nodes),
                                       "merged_bins": int(mv.n_bins), "wall_ms_median": round(sorted(times)[len(times) // 2], 3),
