@@ -340,8 +340,12 @@ static dc_status reduce_received(Ctx* c, const uint64_t* rn_p, uint64_t rn, cons
     DC_TRY(alloc(c, sd.slot, sd.n));
     DC_TRY(alloc(c, sd.head, sd.n));
     DC_TRY(alloc(c, sd.ridx, sd.n));
-    DC_CUDA(c, cudaMemsetAsync(sd.tab.p, 0xFF, sd.cap * 16, c->stream));
-    DC_CUDA(c, cudaMemsetAsync(sd.tval.p, 0xFF, sd.cap * 4, c->stream));
+    {  // one fill kernel (a DMA memset between PDL-chained kernels costs a full launch latency)
+      FillList fl;
+      DC_TRY(fill_add(c, fl, sd.tab.p, sd.cap * 16, 0xFF));
+      DC_TRY(fill_add(c, fl, sd.tval.p, sd.cap * 4, 0xFF));
+      DC_TRY(fill_flush(c, fl));
+    }
     dc_launch(k_kv_insert, grid_for(c, sd.n, 256), 256, 0, c->stream, sd.rec, sd.W, sd.n, sd.bins, sd.tab.p, sd.tval.p, sd.cap - 1,
               sd.slot.p, tot.p + 2);
     DC_LAUNCHED(c);
