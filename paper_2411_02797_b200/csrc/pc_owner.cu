@@ -64,7 +64,10 @@ constexpr int OW_PEND = OW_ROUND + 32;        // per-warp queue of missed keys (
 // a flush is requested at 2/3 load; past OW_SPILL_AT distinct keys new keys are not inserted
 // but appended to the CTA's spill region in HBM (kept as partial entries), so the table can
 // never overflow whatever the key cardinality. `distinct` lags by at most one round per warp.
-constexpr uint32_t OW_FLUSH_REQ = OW_TAB * 2 / 3;
+#ifndef DC_OW_FLUSH_PCT
+#define DC_OW_FLUSH_PCT 75
+#endif
+constexpr uint32_t OW_FLUSH_REQ = OW_TAB * DC_OW_FLUSH_PCT / 100;  // (A/B builds: other loads)
 constexpr uint32_t OW_SPILL_AT = OW_TAB - OW_CONS_WARPS * OW_PEND - 1;
 constexpr uint32_t OW_MISS = 0xFFFFFFFEu;
 constexpr uint32_t OW_SPILL_CAP = 4096;       // spill chunk (entries); the first per CTA is preallocated
@@ -367,26 +370,49 @@ __device__ __forceinline__ void own_flush(OwnSmem& sm, const OwnArgs& a, uint32_
   cons_sync();
 }
 
-// The table is probed in 4-slot buckets: one 16-B shared load compares a key with a whole
-// bucket, so a key displaced from its home slot usually still costs a single load.
-constexpr uint32_t OW_NB = OW_TAB / 4;
+// The table is probed in OW_BW-slot buckets (4: one 16-B shared load compares a key with a whole
+// bucket, so a key displaced from its home slot usually still costs a single load; 2: 8-B loads,
+// fewer bank-conflict wavefronts per warp, more displaced keys — A/B builds).
+#ifndef DC_OW_BW
+#define DC_OW_BW 1
+#endif
+constexpr uint32_t OW_BW = DC_OW_BW;
+static_assert(OW_BW == 1 || OW_BW == 2 || OW_BW == 4, "bucket width 1, 2 or 4");
+constexpr uint32_t OW_NB = OW_TAB / OW_BW;
 __device__ __forceinline__ uint32_t own_bucket(uint32_t key) { return __umulhi(key * 0x9E3779B1u, OW_NB); }
 // preferred slot of a key within its home bucket (independent bits): new keys take it when it is
 // free, so most lookups settle with one 4-B load of that slot instead of a 16-B bucket load
-__device__ __forceinline__ uint32_t own_hint(uint32_t key) { return (key * 0x27D4EB2Fu) >> 30; }
+__device__ __forceinline__ uint32_t own_hint(uint32_t key) { return OW_BW == 1 ? 0u : (key * 0x27D4EB2Fu) >> (OW_BW == 4 ? 30 : 31); }
+// a bucket's keys as a uint4 (width 2: .z / .w are never a key and never EMPTY: slot words only)
+__device__ __forceinline__ uint4 bkt_ld(const uint32_t* p) {
+  if (OW_BW == 4) return *reinterpret_cast<const uint4*>(p);
+  if (OW_BW == 1) return make_uint4(*p, OW_MISS, OW_MISS, OW_MISS);
+  const uint2 v = *reinterpret_cast<const uint2*>(p);
+  return make_uint4(v.x, v.y, OW_MISS, OW_MISS);
+}
 __device__ __forceinline__ int bucket_match(const uint4 v, uint32_t key) {
-  return v.x == key ? 0 : v.y == key ? 1 : v.z == key ? 2 : v.w == key ? 3 : -1;
+  return v.x == key ? 0 : (OW_BW >= 2 && v.y == key) ? 1 : (OW_BW == 4 && v.z == key) ? 2 : (OW_BW == 4 && v.w == key) ? 3 : -1;
 }
 __device__ __forceinline__ uint4 ld_shared_v4_volatile(const uint32_t* p) {
   uint4 v;
-  asm volatile("ld.volatile.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "r"(smem_u32(p)));
+  if (OW_BW == 4) {
+    asm volatile("ld.volatile.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(smem_u32(p)));
+  } else if (OW_BW == 2) {
+    asm volatile("ld.volatile.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(smem_u32(p)));
+    v.z = v.w = OW_MISS;
+  } else {
+    asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v.x) : "r"(smem_u32(p)));
+    v.y = v.z = v.w = OW_MISS;
+  }
   return v;
 }
 
 // branch-free bucket lookup: keys are unique in the table, so at most one compare holds
 __device__ __forceinline__ uint32_t bucket_slot(const uint4 v, uint32_t key, uint32_t b) {
+  if (OW_BW == 1) return v.x == key ? b : (uint32_t)OW_MISS;
+  if (OW_BW == 2) return (v.x == key) | (v.y == key) ? 2 * b + (v.y == key ? 1u : 0u) : (uint32_t)OW_MISS;
   const uint32_t j = (v.y == key ? 1u : 0u) | (v.z == key ? 2u : 0u) | (v.w == key ? 3u : 0u);
   return (v.x == key) | (j != 0u) ? 4 * b + j : (uint32_t)OW_MISS;
 }
@@ -409,27 +435,27 @@ uint32_t own_probe(OwnSmem& sm, uint32_t key, uint32_t b) {
   const bool full = *(volatile uint32_t*)&sm.distinct >= OW_SPILL_AT;
   for (uint32_t walked = 0;; ++walked) {
     if (walked > 2 * OW_NB) return OW_TAB;  // cannot happen below OW_SPILL_AT; spill rather than spin
-    const uint4 v = ld_shared_v4_volatile(&sm.key[4 * b]);
+    const uint4 v = ld_shared_v4_volatile(&sm.key[OW_BW * b]);
     const int j = bucket_match(v, key);
-    if (j >= 0) return 4 * b + j;
-    uint32_t empt = (v.x == EMPTY32 ? 1u : 0u) | (v.y == EMPTY32 ? 2u : 0u) | (v.z == EMPTY32 ? 4u : 0u) |
-                    (v.w == EMPTY32 ? 8u : 0u);
+    if (j >= 0) return OW_BW * b + j;
+    uint32_t empt = (v.x == EMPTY32 ? 1u : 0u) | (OW_BW >= 2 && v.y == EMPTY32 ? 2u : 0u) |
+                    (OW_BW == 4 ? (v.z == EMPTY32 ? 4u : 0u) | (v.w == EMPTY32 ? 8u : 0u) : 0u);
     if (empt && full) return OW_TAB;
     if (DC_OW_HINT && walked == 0) {  // home bucket: the key's preferred slot first
       const uint32_t hq = own_hint(key);
       if ((empt >> hq) & 1u) {
-        const uint32_t old = atomicCAS(&sm.key[4 * b + hq], EMPTY32, key);
-        if (old == EMPTY32) return (4 * b + hq) | 0x80000000u;
-        if (old == key) return 4 * b + hq;
+        const uint32_t old = atomicCAS(&sm.key[OW_BW * b + hq], EMPTY32, key);
+        if (old == EMPTY32) return (OW_BW * b + hq) | 0x80000000u;
+        if (old == key) return OW_BW * b + hq;
         empt &= ~(1u << hq);
       }
     }
     while (empt) {
       const uint32_t q = __ffs(empt) - 1;
       empt &= empt - 1;
-      const uint32_t old = atomicCAS(&sm.key[4 * b + q], EMPTY32, key);
-      if (old == EMPTY32) return (4 * b + q) | 0x80000000u;
-      if (old == key) return 4 * b + q;
+      const uint32_t old = atomicCAS(&sm.key[OW_BW * b + q], EMPTY32, key);
+      if (old == EMPTY32) return (OW_BW * b + q) | 0x80000000u;
+      if (old == key) return OW_BW * b + q;
     }
     b = b + 1 == OW_NB ? 0u : b + 1;
   }
@@ -539,7 +565,7 @@ __device__ __noinline__ uint32_t own_cold(const uint4 q, uint32_t seg_launch, co
       const uint32_t before = atomicAdd(&sm.extra, q.w - 1u);
       if (before < OW_EXTRA_FLUSH && before + (q.w - 1u) >= OW_EXTRA_FLUSH) *(volatile uint32_t*)&sm.flush_req = 1u;
       const uint32_t bb = own_bucket(key);
-      const uint4 v = ld_shared_v4_volatile(&sm.key[4 * bb]);
+      const uint4 v = ld_shared_v4_volatile(&sm.key[OW_BW * bb]);
       uint32_t sl = bucket_slot(v, key, bb);
       uint32_t ins = 0;
       if (sl == OW_MISS) {  // new or displaced key: probe, inserting it (round 2: per-PC aggregated
@@ -899,21 +925,21 @@ __global__ void __launch_bounds__(OW_THREADS, OW_CPS) k_pc_owner(OwnArgs a) { DC
       if (DC_OW_HINT) {  // the preferred slot (4-B load), then the whole bucket for the rest
         uint32_t hs[OW_PER_LANE], k1[OW_PER_LANE];
 #pragma unroll
-        for (int i = 0; i < OW_PER_LANE; ++i) hs[i] = 4 * b[i] + own_hint(t[i]);
+        for (int i = 0; i < OW_PER_LANE; ++i) hs[i] = OW_BW * b[i] + own_hint(t[i]);
 #pragma unroll
         for (int i = 0; i < OW_PER_LANE; ++i) k1[i] = sm.key[hs[i]];
 #pragma unroll
         for (int i = 0; i < OW_PER_LANE; ++i) {
           slot[i] = hs[i];
           if (k1[i] != t[i] && t[i] != EMPTY32) {
-            const uint4 v = *reinterpret_cast<const uint4*>(&sm.key[4 * b[i]]);  // home bucket
+            const uint4 v = bkt_ld(&sm.key[OW_BW * b[i]]);  // home bucket
             slot[i] = bucket_slot(v, t[i], b[i]);
           }
         }
       } else {
 #pragma unroll
         for (int i = 0; i < OW_PER_LANE; ++i) {
-          const uint4 v = *reinterpret_cast<const uint4*>(&sm.key[4 * b[i]]);  // home bucket
+          const uint4 v = bkt_ld(&sm.key[OW_BW * b[i]]);  // home bucket
           slot[i] = bucket_slot(v, t[i], b[i]);
         }
       }
