@@ -18,27 +18,66 @@ namespace dc {
 // K > 1 (small trees with many records per node): CTA b updates copy b % K of the columns
 // (strides cs / ms), so K times fewer updates meet on one address; k_attr_fold adds the copies
 // into the node columns. K = 1 updates the node columns directly.
+#ifndef DC_ATTR_U
+#define DC_ATTR_U 4
+#endif
+// U records per thread per round (U = DC_ATTR_U for the direct columns; the K-copy path keeps
+// U = 1: config 2 0.110 ms vs 0.123 with 4, its updates meet in a few MB of L2-hot copies), U grid strides apart (every slice stays a coalesced warp
+// access): their loads, the min reads and the returned square atomics are issued U at a time, so
+// a thread pays each of those latencies once per U records instead of once per record (the
+// kernel is bound by them: ncu long-scoreboard stalls 26 per issue on config 4 with U = 1).
+// Warp-level pre-aggregation of equal leaves cannot help here: 32 consecutive records of config
+// 4 have 32 distinct leaves (config 2: 20.5 on average, and its heavily shared nodes take the K
+// column copies instead).
+template <int U>
 __global__ void k_attribute(const uint32_t* __restrict__ leaf, uint64_t R, const uint64_t* __restrict__ X, uint32_t M,
                             uint64_t ld, uint64_t N, unsigned long long* __restrict__ xcnt0, unsigned long long* __restrict__ mcols0,
                             uint32_t* d_flags, uint32_t K, uint64_t cs, uint64_t ms) { DC_PDL_WAIT();
   unsigned long long* xcnt = xcnt0 + (uint64_t)(blockIdx.x % K) * cs;
   unsigned long long* mcols = mcols0 + (uint64_t)(blockIdx.x % K) * ms;
-  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < R; r += (uint64_t)gridDim.x * blockDim.x) {
-    uint32_t n = leaf[r];
-    if (n >= N) {
-      atomicOr(d_flags, FLAG_BAD_LEAF);
-      continue;
+  const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t r0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r0 < R; r0 += U * T) {
+    uint32_t n[U];
+    bool v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      v[u] = r0 + u * T < R;
+      n[u] = v[u] ? leaf[r0 + u * T] : 0u;
     }
-    atomicAdd(xcnt + n, 1ull);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (v[u] && n[u] >= N) {
+        atomicOr(d_flags, FLAG_BAD_LEAF);
+        v[u] = false;
+      }
+      if (v[u]) atomicAdd(xcnt + n[u], 1ull);
+    }
     for (uint32_t m = 0; m < M; ++m) {
-      uint64_t x = X[m * ld + r];
-      atomicAdd(mcols + ((uint64_t)C_XSUM * M + m) * N + n, (unsigned long long)x);
+      uint64_t x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) x[u] = v[u] ? X[m * ld + r0 + u * T] : 0ull;
+      unsigned long long* sum = mcols + ((uint64_t)C_XSUM * M + m) * N;
+      unsigned long long* mn = mcols + ((uint64_t)C_XMIN * M + m) * N;
+      unsigned long long* sql = mcols + ((uint64_t)C_XSQLO * M + m) * N;
+      unsigned long long* sqh = mcols + ((uint64_t)C_XSQHI * M + m) * N;
       // min only when x can lower it: after the first few records of a node the plain read
       // (an L2 hit) settles almost every record without an atomic
-      unsigned long long* mn = mcols + ((uint64_t)C_XMIN * M + m) * N + n;
-      if (x < ld_relaxed_u64(mn)) atomicMin(mn, (unsigned long long)x);
-      uint64_t sq_lo = x * x, sq_hi = __umul64hi(x, x);
-      atomic_add_u128(mcols + ((uint64_t)C_XSQLO * M + m) * N + n, mcols + ((uint64_t)C_XSQHI * M + m) * N + n, sq_lo, sq_hi);
+      uint64_t cur[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) cur[u] = v[u] ? ld_relaxed_u64(mn + n[u]) : 0ull;
+      unsigned long long old[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (v[u]) atomicAdd(sum + n[u], (unsigned long long)x[u]);
+        old[u] = v[u] ? atomicAdd(sql + n[u], (unsigned long long)(x[u] * x[u])) : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (v[u] && x[u] < cur[u]) atomicMin(mn + n[u], (unsigned long long)x[u]);
+        // 128-bit square: the returned low word tells the carry into the high word
+        const uint64_t lo = x[u] * x[u], hi = __umul64hi(x[u], x[u]) + ((old[u] + lo) < old[u] ? 1u : 0u);
+        if (v[u] && hi) atomicAdd(sqh + n[u], (unsigned long long)hi);
+      }
     }
   }
 }
@@ -120,7 +159,7 @@ dc_status attribute_metrics(Ctx* c, dc_cct* t, const uint32_t* leaf, uint64_t R,
   // copies of the columns (a few MB at most) and fold the copies afterwards
   const uint32_t K = (N <= (1u << 16) && R >= 64 * N && !getenv("DC_TEST_ATTR_DIRECT")) ? 16u : 1u;
   if (R && K == 1) {
-    dc_launch(k_attribute, grid_for(c, R, 256), 256, 0, c->stream, leaf, R, X, M, ld, N, (unsigned long long*)t->xcnt,
+    dc_launch(k_attribute<DC_ATTR_U>, grid_for(c, R, 256), 256, 0, c->stream, leaf, R, X, M, ld, N, (unsigned long long*)t->xcnt,
                                                             (unsigned long long*)t->mcols, c->d_flags, 1, 0, 0);
     DC_LAUNCHED(c);
   } else if (R) {
@@ -129,7 +168,7 @@ dc_status attribute_metrics(Ctx* c, dc_cct* t, const uint32_t* leaf, uint64_t R,
     DC_TRY(alloc(c, ccols, (uint64_t)K * 4 * M * N + 1));
     dc_launch(k_attr_init_copies, grid_for(c, (uint64_t)K * N * (1 + 4 * M), 256), 256, 0, c->stream, ccnt.p, ccols.p, K, M, N);
     DC_LAUNCHED(c);
-    dc_launch(k_attribute, grid_for(c, R, 256), 256, 0, c->stream, leaf, R, X, M, ld, N, (unsigned long long*)ccnt.p,
+    dc_launch(k_attribute<1>, grid_for(c, R, 256), 256, 0, c->stream, leaf, R, X, M, ld, N, (unsigned long long*)ccnt.p,
                                                             (unsigned long long*)ccols.p, c->d_flags, K, N, 4ull * M * N);
     DC_LAUNCHED(c);
     dc_launch(k_attr_fold, grid_for(c, N * (1 + M), 256), 256, 0, c->stream, ccnt.p, ccols.p, K, M, N, t->xcnt, t->mcols);
