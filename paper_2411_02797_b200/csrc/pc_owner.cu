@@ -1255,7 +1255,7 @@ __global__ void __launch_bounds__(32 * BR_WARPS) k_br_count(
 //    its bins and their counts at their global positions.
 // A context whose PC range or segment count does not fit shared memory (or scratch that is too
 // small) raises CR_WIDE: the host takes the k_br_* path; outputs past the allocated capacity
-// are not written (CR_OVER: the host reallocates and reruns k_ctx_emit only).
+// are not written (the host sees more bins than the capacity, reallocates and reruns k_ctx_emit only).
 #ifndef DC_CR_THREADS
 #define DC_CR_THREADS 1024
 #endif
@@ -2209,10 +2209,14 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
         DC_LAUNCHED(c);
         return DC_OK;
       };
-      DC_TRY(emit(cap));
+      // split-phase: everything the host decides on is known after the scan, so the emission
+      // runs while the host reads it back (no host turnaround between the scan and the kernels
+      // that follow the call); a bin count past the capacity guess is seen on the host (nb > cap)
       uint64_t hst[3] = {0, 0, 0}, htot[2] = {0, 0};
-      DC_TRY(readback_multi(c, {{flags.p, 8, hf}, {bad.p, 4, &hbad}, {ctl.p + 1, 24, hst}, {gbase.p + n_launch, 8, &htot[0]},
+      DC_TRY(readback_begin(c, {{flags.p, 8, hf}, {bad.p, 4, &hbad}, {ctl.p + 1, 24, hst}, {gbase.p + n_launch, 8, &htot[0]},
                                 {gbase.p + 2 * n_launch + 1, 8, &htot[1]}, {ctr.p, 16, hc}}));
+      DC_TRY(emit(cap));
+      DC_TRY(readback_end(c));
       if (getenv("DC_PC_STATS"))  // measurement only
         fprintf(stderr, "{\"pc_stats\": {\"entries\": %llu, \"segments\": %llu, \"bins\": %llu, \"pcs\": %llu, \"status\": %llu, "
                 "\"words\": %llu, \"scratch_bins\": %llu}}\n", (unsigned long long)hc[0], (unsigned long long)(hc[1] & 0xFFFFFFFFu),
@@ -2227,7 +2231,7 @@ dc_status pc_owner_hist(Ctx* c, dc_cct* t, const dc_pc_sample* s, uint64_t n, co
       }
       if (!(hst[0] & CR_WIDE)) {
         const uint64_t nb = htot[0], npc = htot[1];
-        if (hst[0] & CR_OVER) {  // more bins than the capacity guess: exact outputs, emit again
+        if (nb > cap) {  // more bins than the capacity guess: exact outputs, emit again
           drop_outputs();
           DC_TRY(outputs(nb));
           DC_TRY(emit(nb));
