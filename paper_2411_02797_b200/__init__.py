@@ -219,7 +219,11 @@ class CCT:
 
     @property
     def n_nodes(self) -> int:
-        return int(self.view(before_rollup=True).n_nodes)
+        # fixed for the handle's lifetime (set by the call that created it): read once
+        n = getattr(self, "_n_nodes", None)
+        if n is None:
+            n = self._n_nodes = int(self.view(before_rollup=True).n_nodes)
+        return n
 
     def free(self):
         if getattr(self, "h", None):
@@ -392,7 +396,7 @@ def dc_cct_derived(ctx: Context, cct: CCT, metric: int, incl: bool = True, out: 
         mean = torch.empty(max(N, 1), dtype=torch.float64, device=f"cuda:{ctx.device}")
         std = torch.empty_like(mean)
     ctx.check(lib().dc_cct_derived(ctx.h, cct.h, int(metric), int(bool(incl)), _ptr(mean), _ptr(std)), "dc_cct_derived")
-    return mean[:N], std[:N]
+    return (mean, std) if mean.numel() == N else (mean[:N], std[:N])
 
 
 def dc_cct_view_get(cct: CCT) -> dc_cct_view:
