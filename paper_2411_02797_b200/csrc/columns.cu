@@ -375,55 +375,90 @@ __device__ __forceinline__ void warp_sum_u128(uint64_t& lo, uint64_t& hi) {
   }
 }
 
-__global__ void __launch_bounds__(256) k_rollup_levels(RollArgs a) { DC_PDL_ENTER();
+// column loads: CG = the one-CTA run of narrow levels (below), where the values were last
+// changed by this CTA's own global atomics and only a __syncthreads separates the levels, so
+// the loads must not be served from a stale L1 line (relaxed gpu-scope loads go to L2)
+template <bool CG>
+__device__ __forceinline__ uint64_t rl_ld(const unsigned long long* p) {
+  return CG ? ld_relaxed_u64(p) : *p;
+}
+
+// one level d of the rollup: items (node of the level, column group) t = tid0, tid0 + nthreads, ...
+template <bool CG>
+__device__ __forceinline__ void roll_level(const RollArgs& a, uint32_t d, uint64_t tid0, uint64_t nthreads) {
   const uint64_t N = a.N;
   const uint32_t M = a.M, lane = lane_id();
-  const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
-  for (uint32_t d = a.maxd; d >= 1; --d) {
-    const uint64_t lo = a.level_off[d], width = a.level_off[d + 1] - lo;
-    const uint64_t items = width * a.G;
-    const uint64_t rounds = (items + nthreads - 1) / nthreads;
-    for (uint64_t k = 0; k < rounds; ++k) {  // warp-uniform trip count (shuffles below)
-      const uint64_t t = k * nthreads + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-      const bool act = t < items;
-      const uint32_t g = act ? (uint32_t)(t / width) : 0xFFFFFFFFu;
-      const uint64_t m = act ? lo + t % width : 0;
-      const uint32_t p = act ? a.parent[m] : 0xFFFFFFFFu;
-      // every lane takes part in these shuffles (none inside a short-circuit)
-      const uint32_t p0 = __shfl_sync(0xffffffffu, p, 0), g0 = __shfl_sync(0xffffffffu, g, 0);
-      const bool uni = __all_sync(0xffffffffu, act && p == p0 && g == g0);
-      if (g == 0 || (uni && g0 == 0)) {
-        uint64_t v = act ? a.icnt[m] : 0;
-        if (uni) v = warp_sum_u64(v);
-        if (v && (!uni || lane == 0)) atomicAdd(a.icnt + p, (unsigned long long)v);
-      } else if (g <= M) {
-        const uint32_t mm = g - 1;
-        const uint64_t cnt = a.icnt[m];
-        uint64_t sum = a.mcols[((uint64_t)C_ISUM * M + mm) * N + m];
-        uint64_t mn = a.mcols[((uint64_t)C_IMIN * M + mm) * N + m];
-        uint64_t qlo = a.mcols[((uint64_t)C_ISQLO * M + mm) * N + m];
-        uint64_t qhi = a.mcols[((uint64_t)C_ISQHI * M + mm) * N + m];
-        if (uni) {
-          sum = warp_sum_u64(sum);
-          mn = warp_min_u64(mn);
-          warp_sum_u128(qlo, qhi);
-        }
-        const bool any = uni ? __any_sync(0xffffffffu, cnt != 0) : cnt != 0;
-        if (any && (!uni || lane == 0)) {
-          if (sum) atomicAdd(a.mcols + ((uint64_t)C_ISUM * M + mm) * N + p, (unsigned long long)sum);
-          atomicMin(a.mcols + ((uint64_t)C_IMIN * M + mm) * N + p, (unsigned long long)mn);
-          if (qlo | qhi)
-            atomic_add_u128(a.mcols + ((uint64_t)C_ISQLO * M + mm) * N + p, a.mcols + ((uint64_t)C_ISQHI * M + mm) * N + p, qlo,
-                            qhi);
-        }
-      } else if (act || uni) {
-        unsigned long long* col = g == M + 1 ? a.isamples : a.istall + (uint64_t)(g - M - 2) * N;
-        uint64_t v = act ? col[m] : 0;
-        if (uni) v = warp_sum_u64(v);
-        if (v && (!uni || lane == 0)) atomicAdd(col + p, (unsigned long long)v);
+  const uint64_t lo = a.level_off[d], width = a.level_off[d + 1] - lo;
+  const uint64_t items = width * a.G;
+  const uint64_t rounds = (items + nthreads - 1) / nthreads;
+  for (uint64_t k = 0; k < rounds; ++k) {  // warp-uniform trip count (shuffles below)
+    const uint64_t t = k * nthreads + tid0;
+    const bool act = t < items;
+    const uint32_t g = act ? (uint32_t)(t / width) : 0xFFFFFFFFu;
+    const uint64_t m = act ? lo + t % width : 0;
+    const uint32_t p = act ? a.parent[m] : 0xFFFFFFFFu;
+    // every lane takes part in these shuffles (none inside a short-circuit)
+    const uint32_t p0 = __shfl_sync(0xffffffffu, p, 0), g0 = __shfl_sync(0xffffffffu, g, 0);
+    const bool uni = __all_sync(0xffffffffu, act && p == p0 && g == g0);
+    if (g == 0 || (uni && g0 == 0)) {
+      uint64_t v = act ? rl_ld<CG>(a.icnt + m) : 0;
+      if (uni) v = warp_sum_u64(v);
+      if (v && (!uni || lane == 0)) atomicAdd(a.icnt + p, (unsigned long long)v);
+    } else if (g <= M) {
+      const uint32_t mm = g - 1;
+      const uint64_t cnt = rl_ld<CG>(a.icnt + m);
+      uint64_t sum = rl_ld<CG>(a.mcols + ((uint64_t)C_ISUM * M + mm) * N + m);
+      uint64_t mn = rl_ld<CG>(a.mcols + ((uint64_t)C_IMIN * M + mm) * N + m);
+      uint64_t qlo = rl_ld<CG>(a.mcols + ((uint64_t)C_ISQLO * M + mm) * N + m);
+      uint64_t qhi = rl_ld<CG>(a.mcols + ((uint64_t)C_ISQHI * M + mm) * N + m);
+      if (uni) {
+        sum = warp_sum_u64(sum);
+        mn = warp_min_u64(mn);
+        warp_sum_u128(qlo, qhi);
       }
+      const bool any = uni ? __any_sync(0xffffffffu, cnt != 0) : cnt != 0;
+      if (any && (!uni || lane == 0)) {
+        if (sum) atomicAdd(a.mcols + ((uint64_t)C_ISUM * M + mm) * N + p, (unsigned long long)sum);
+        atomicMin(a.mcols + ((uint64_t)C_IMIN * M + mm) * N + p, (unsigned long long)mn);
+        if (qlo | qhi)
+          atomic_add_u128(a.mcols + ((uint64_t)C_ISQLO * M + mm) * N + p, a.mcols + ((uint64_t)C_ISQHI * M + mm) * N + p, qlo, qhi);
+      }
+    } else if (act || uni) {
+      unsigned long long* col = g == M + 1 ? a.isamples : a.istall + (uint64_t)(g - M - 2) * N;
+      uint64_t v = act ? rl_ld<CG>(col + m) : 0;
+      if (uni) v = warp_sum_u64(v);
+      if (v && (!uni || lane == 0)) atomicAdd(col + p, (unsigned long long)v);
     }
-    grid_barrier(a.bar);
+  }
+}
+
+// Level-synchronous rollup for deep / large trees: one grid barrier per level. A run of
+// consecutive narrow levels (at most RL_NARROW items each: the deep recursion chains of config
+// 4) is walked by CTA 0 alone with a block barrier per level and one grid barrier for the run.
+#ifndef DC_RL_NARROW
+#define DC_RL_NARROW 1024
+#endif
+constexpr uint64_t RL_NARROW = DC_RL_NARROW;
+__global__ void __launch_bounds__(256) k_rollup_levels(RollArgs a) { DC_PDL_ENTER();
+  const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
+  auto items_of = [&](uint32_t d) -> uint64_t { return (uint64_t)(a.level_off[d + 1] - a.level_off[d]) * a.G; };
+  for (uint32_t d = a.maxd; d >= 1;) {
+    if (RL_NARROW && items_of(d) <= RL_NARROW) {
+      uint32_t e = d;  // the run [e, d] of narrow levels (every CTA computes the same run)
+      while (e > 1 && items_of(e - 1) <= RL_NARROW) --e;
+      if (blockIdx.x == 0) {
+        for (uint32_t dd = d; dd >= e; --dd) {
+          roll_level<true>(a, dd, threadIdx.x, blockDim.x);
+          __syncthreads();
+        }
+      }
+      grid_barrier(a.bar);
+      d = e - 1;
+    } else {
+      roll_level<false>(a, d, blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, nthreads);
+      grid_barrier(a.bar);
+      --d;
+    }
   }
 }
 
