@@ -439,7 +439,8 @@ __device__ __noinline__
 uint32_t own_probe(OwnSmem& sm, uint32_t key, uint32_t b) {
   // `distinct` is refreshed once per warp round (not per insert), hence the margin in OW_SPILL_AT
   const bool full = *(volatile uint32_t*)&sm.distinct >= OW_SPILL_AT;
-  if (OW_BW == 1 && DC_OW_GW) {
+#if DC_OW_BW == 1 && DC_OW_GW
+  {
     // Group walk: the home slot first (the fast path's 4-B lookup), then the aligned 4-slot
     // groups from the home slot's group on, one 16-B load each; a new key takes the home slot or
     // else the first empty slot in that order. Slots are never freed between flushes, so a group
@@ -476,6 +477,7 @@ uint32_t own_probe(OwnSmem& sm, uint32_t key, uint32_t b) {
       g = g + 4 == (uint32_t)OW_TAB ? 0u : g + 4;
     }
   }
+#else
   for (uint32_t walked = 0;; ++walked) {
     if (walked > 2 * OW_NB) return OW_TAB;  // cannot happen below OW_SPILL_AT; spill rather than spin
     const uint4 v = ld_shared_v4_volatile(&sm.key[OW_BW * b]);
@@ -502,6 +504,7 @@ uint32_t own_probe(OwnSmem& sm, uint32_t key, uint32_t b) {
     }
     b = b + 1 == OW_NB ? 0u : b + 1;
   }
+#endif
 }
 
 // One exact partial entry outside the table (table full, or a sample whose count is not 1).
@@ -1404,6 +1407,7 @@ __global__ void __launch_bounds__(CR_THREADS, CR_CPS) k_ctx_hist(
     uint32_t W = 0, nb = 0, np = 0, ns = 0;
     int sh = 0;
     if (ok) {
+      uint32_t mk = 0, orp = 0;
       // this context's segments (headers scanned 8 per thread in flight)
       for (uint32_t i0 = 0; i0 < n_segs; i0 += 8 * CR_THREADS) {
         uint32_t cx[8], cn[8];
@@ -1417,26 +1421,24 @@ __global__ void __launch_bounds__(CR_THREADS, CR_CPS) k_ctx_hist(
 #pragma unroll
         for (int u = 0; u < 8; ++u)
           if (cx[u] == ctx && cn[u]) {
+            const uint32_t si = i0 + u * CR_THREADS + tid;
             const uint32_t q = atomicAdd(&sm.nseg, 1u);
-            if (q < CR_SEGS) sm.segs[q] = i0 + u * CR_THREADS + tid;
+            if (q < CR_SEGS) sm.segs[q] = si;
+            // pass A, folded in: key range (max key + 1, OR of the PCs). A table-flush segment
+            // carries it (seg_meta, written by k_pc_owner's flush); only the spill segments'
+            // entries are walked below
+            const uint2 m = __ldcg(seg_meta + si);
+            if (m.x == 0xFFFFFFFFu) {
+              const uint32_t uu = atomicAdd(&sm.nuseg, 1u);
+              if (uu < CR_USEGS) sm.useg[uu] = si;
+            } else {
+              mk = max(mk, m.x);
+              orp |= m.y;
+            }
           }
       }
       __syncthreads();
-      // pass A: key range (max key + 1, OR of the PCs). A table-flush segment carries it
-      // (seg_meta, written by k_pc_owner's flush); only the spill segments' entries are walked
-      uint32_t mk = 0, orp = 0;
       ns = min(sm.nseg, CR_SEGS);
-      for (uint32_t q = tid; q < ns; q += CR_THREADS) {
-        const uint2 m = __ldcg(seg_meta + sm.segs[q]);
-        if (m.x == 0xFFFFFFFFu) {
-          const uint32_t u = atomicAdd(&sm.nuseg, 1u);
-          if (u < CR_USEGS) sm.useg[u] = sm.segs[q];
-        } else {
-          mk = max(mk, m.x);
-          orp |= m.y;
-        }
-      }
-      __syncthreads();
       if (sm.nuseg > CR_USEGS) {  // too many spill segments to list: walk every segment
         cr_for_entries<false>(sm.segs, seg, pkey, pcnt, ns, [&](uint32_t kk, unsigned long long) {
           mk = max(mk, kk + 1);
@@ -1480,8 +1482,13 @@ __global__ void __launch_bounds__(CR_THREADS, CR_CPS) k_ctx_hist(
         bsum += __popc(b);
         psum += b != 0u;
       }
-      uint32_t bex = block_excl_scan<uint32_t, CR_THREADS>(bsum, &nb);
-      uint32_t pex = block_excl_scan<uint32_t, CR_THREADS>(psum, &np);
+      // both prefixes in one block scan: bins (< 2^18 per context) low, PC nodes high
+      unsigned long long tot2 = 0;
+      const unsigned long long ex2 =
+          block_excl_scan<unsigned long long, CR_THREADS>((unsigned long long)bsum | ((unsigned long long)psum << 32), &tot2);
+      uint32_t bex = (uint32_t)ex2, pex = (uint32_t)(ex2 >> 32);
+      nb = (uint32_t)tot2;
+      np = (uint32_t)(tot2 >> 32);
       if (tid == 0) {
         sm.ow = atomicAdd(ctl + 2, (unsigned long long)W);
         sm.ob = atomicAdd(ctl + 3, (unsigned long long)nb);
@@ -1558,7 +1565,15 @@ __global__ void __launch_bounds__(CR_THREADS, CR_CPS) k_ctx_hist(
   }
 }
 
-// one thread per scratch word (grid-stride over the words used): its PC node, bins and counts
+// Per scratch word (grid-stride over the words used): its PC node, bins and counts.
+// DC_CE_WARP: a warp takes 32 consecutive words; each lane writes its word's PC node, then the
+// warp writes the words' bins together — bin j of the warp's list goes to lane j % 32, which finds
+// its word by a binary search over the lanes' inclusive bin counts and its stall as the k-th set
+// bit of the word — so consecutive lanes store consecutive bins (the words of one context are
+// contiguous in the output). Otherwise one thread writes all bins of its word.
+#ifndef DC_CE_WARP
+#define DC_CE_WARP 1
+#endif
 __global__ void k_ctx_emit(const CtxWord* __restrict__ wscr, const unsigned long long* __restrict__ ctl, const CtxRec* __restrict__ rec,
                            const uint64_t* __restrict__ bbase, const uint64_t* __restrict__ pbase,
                            const unsigned long long* __restrict__ bscr, uint64_t N, uint64_t cap, unsigned long long* __restrict__ status,
@@ -1566,6 +1581,59 @@ __global__ void k_ctx_emit(const CtxWord* __restrict__ wscr, const unsigned long
                            uint16_t* __restrict__ bin_stall, uint64_t* __restrict__ bin_count, const uint32_t* __restrict__ g_flags) { DC_PDL_ENTER();
   if (*g_flags || (ctl[1] & CR_WIDE)) return;
   const uint64_t total = ctl[2];
+#if DC_CE_WARP
+  {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t wg = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5, nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t base = wg * 32; base < total; base += nw * 32) {  // warp-uniform
+      const uint64_t i = base + lane;
+      uint32_t bits = 0, cnt = 0;
+      uint64_t q = 0, src = 0, pn = 0;
+      if (i < total) {
+        const CtxWord cw = wscr[i];
+        bits = cw.bits;
+        if (bits) {
+          const CtxRec r = rec[cw.g];
+          const uint64_t p = pbase[cw.g] + cw.ppre;
+          q = bbase[cw.g] + cw.bpre;
+          cnt = __popc(bits);
+          if (q + cnt > cap) {
+            atomicOr(status, (unsigned long long)CR_OVER);
+            bits = 0;
+            cnt = 0;
+          } else {
+            pc_ctx[p] = r.ctx;
+            pc_off[p] = (uint32_t)(i - r.ow) << r.sh;
+            src = r.ob + cw.bpre;
+            pn = N + p;
+          }
+        }
+      }
+      const uint32_t incl = warp_incl_scan<uint32_t>(cnt);
+      const uint32_t T = __shfl_sync(0xffffffffu, incl, 31);
+      for (uint32_t j0 = 0; j0 < T; j0 += 32) {  // warp-uniform trip count
+        const uint32_t j = j0 + lane;
+        uint32_t L = 0;  // owner lane: the number of lanes whose inclusive count is <= j
+#pragma unroll
+        for (uint32_t st = 16; st; st >>= 1) {
+          const uint32_t v = __shfl_sync(0xffffffffu, incl, L + st - 1);
+          if (v <= j) L += st;
+        }
+        L = L > 31 ? 31 : L;
+        const uint32_t incl_L = __shfl_sync(0xffffffffu, incl, L), cnt_L = __shfl_sync(0xffffffffu, cnt, L);
+        const uint32_t bits_L = __shfl_sync(0xffffffffu, bits, L);
+        const uint64_t q_L = __shfl_sync(0xffffffffu, q, L), src_L = __shfl_sync(0xffffffffu, src, L),
+                       pn_L = __shfl_sync(0xffffffffu, pn, L);
+        if (j < T) {
+          const uint32_t k = j - (incl_L - cnt_L);
+          bin_pcnode[q_L + k] = (uint32_t)pn_L;
+          bin_stall[q_L + k] = (uint16_t)__fns(bits_L, 0, (int)k + 1);
+          bin_count[q_L + k] = bscr[src_L + k];
+        }
+      }
+    }
+  }
+#else
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
     const CtxWord cw = wscr[i];
     uint32_t bits = cw.bits;
@@ -1590,6 +1658,7 @@ __global__ void k_ctx_emit(const CtxWord* __restrict__ wscr, const unsigned long
       ++q;
     }
   }
+#endif
 }
 
 // ---------------------------------------------------------------- per-context reduce
