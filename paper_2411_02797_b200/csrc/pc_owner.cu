@@ -887,13 +887,17 @@ __global__ void __launch_bounds__(OW_THREADS, OW_CPS) k_pc_owner(OwnArgs a) { DC
       // no warp runs ahead of the others (a slot is refilled once all its groups are taken). At
       // most one ticket per warp is outstanding, so the tickets taken while a flush barrier waits
       // all lie in the flush stage (groups per stage = warps): the ring cannot deadlock.
+      // The ticket counts modulo one ring period (groups x stages x 2 phases): slot, phase and
+      // group come from a small quotient, and the wrapping increment is one shared atomic (a
+      // plain atomicAdd under `lane == 0` compiles to the warp-aggregated sequence).
+      constexpr uint32_t TK_PERIOD = (uint32_t)OW_CONS_WARPS * OW_STAGES * 2;
       uint32_t tk = 0;
-      if (lane == 0) tk = atomicAdd(&sm.ticket, 1u);
+      if (lane == 0) tk = atomicInc(&sm.ticket, TK_PERIOD - 1);
       tk = __shfl_sync(0xffffffffu, tk, 0);
-      const uint32_t kst = tk / (uint32_t)OW_CONS_WARPS;
+      const uint32_t kst = tk / (uint32_t)OW_CONS_WARPS;  // < 2 * OW_STAGES
       grp = tk - kst * (uint32_t)OW_CONS_WARPS;
-      st = kst % OW_STAGES;
-      ph = (kst / OW_STAGES) & 1u;
+      ph = kst >= (uint32_t)OW_STAGES ? 1u : 0u;
+      st = kst - ph * (uint32_t)OW_STAGES;
     }
     mbar_wait(&sm.full[st], ph);
     const long long c_1 = MODE == 9 ? clock64() : 0;
@@ -949,7 +953,8 @@ __global__ void __launch_bounds__(OW_THREADS, OW_CPS) k_pc_owner(OwnArgs a) { DC
       t[i] = hot ? (q[i].y << 5) | (q[i].z & 0xFFFFu) : EMPTY32;
       cold |= vld[i] & !hot;
     }
-    if (__any_sync(0xffffffffu, cold)) {  // rare: spills and invalid samples
+    const bool any_cold = __any_sync(0xffffffffu, cold);
+    if (any_cold) {  // rare: spills and invalid samples
 #pragma unroll
       for (int i = 0; i < OW_PER_LANE; ++i)
         if (vld[i] && t[i] == EMPTY32) inserted += own_cold(q[i], lch[i], a, ctx_ok, k, sm, mctx);
@@ -1020,12 +1025,14 @@ __global__ void __launch_bounds__(OW_THREADS, OW_CPS) k_pc_owner(OwnArgs a) { DC
       }
       if (MODE == 3) np = 0;  // measurement only: misses dropped
         __syncwarp();
+      // new keys are inserted only by the miss probes and the cold path: publish after those
+      const bool pub = any_cold || np >= 32;
       while (np >= 32) {
         np -= 32;
         probe_one(sm.pend[w][np + lane]);
       }
       __syncwarp();
-      publish();
+      if (pub) publish();
       if (MODE == 9) t_add += clock64() - c_3;
     }
     if (MODE == 9) {
