@@ -428,6 +428,47 @@ __device__ __forceinline__ void red_shared_inc_if(uint32_t* p, bool pred) {  // 
       : "memory");
 }
 
+// Shared addresses as (base of the CTA's shared block, computed once) + offset: a generic ->
+// shared conversion per use (smem_u32) costs a uniform S2UR / ULEA sequence in the hot loop.
+__device__ __forceinline__ uint32_t s_off(const OwnSmem& sm, const void* p, uint32_t sb) {
+  return sb + (uint32_t)((const unsigned char*)p - (const unsigned char*)&sm);
+}
+__device__ __forceinline__ uint32_t s_ld32v(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint4 s_ld128v(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.volatile.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t s_cas32(uint32_t a, uint32_t cmp, uint32_t val) {
+  uint32_t old;
+  asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(old) : "r"(a), "r"(cmp), "r"(val) : "memory");
+  return old;
+}
+__device__ __forceinline__ uint32_t s_inc32(uint32_t a, uint32_t lim) {
+  uint32_t old;
+  asm volatile("atom.shared.inc.u32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(lim) : "memory");
+  return old;
+}
+__device__ __forceinline__ void s_mbar_wait(uint32_t a, uint32_t parity) {
+  for (uint64_t i = 0;; ++i) {
+    uint32_t ok;
+    asm volatile(
+        "{\n.reg .pred P1;\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (i > DC_SPIN_LIMIT) __trap();
+  }
+}
+__device__ __forceinline__ void s_mbar_arrive(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+
 // slow path: the key is not in its home bucket (new key, or displaced). Returns the slot, or
 // OW_TAB when the table is near full (the sample then goes to the spill region).
 // returns slot | (1 << 31 if this call inserted the key)
@@ -436,7 +477,7 @@ __device__ __forceinline__
 #else
 __device__ __noinline__
 #endif
-uint32_t own_probe(OwnSmem& sm, uint32_t key, uint32_t b) {
+uint32_t own_probe(OwnSmem& sm, uint32_t key, uint32_t b, uint32_t sb) {
   // `distinct` is refreshed once per warp round (not per insert), hence the margin in OW_SPILL_AT
   const bool full = *(volatile uint32_t*)&sm.distinct >= OW_SPILL_AT;
 #if DC_OW_BW == 1 && DC_OW_GW
@@ -445,22 +486,19 @@ uint32_t own_probe(OwnSmem& sm, uint32_t key, uint32_t b) {
     // groups from the home slot's group on, one 16-B load each; a new key takes the home slot or
     // else the first empty slot in that order. Slots are never freed between flushes, so a group
     // with an empty slot ends the walk. (One slot per step measured ~8 steps per miss at 75 % load.)
-    uint32_t k0;
-    asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(k0) : "r"(smem_u32(&sm.key[b])));
+    const uint32_t kb = s_off(sm, &sm.key[0], sb);
+    const uint32_t k0 = s_ld32v(kb + 4 * b);
     if (k0 == key) return b;
     if (k0 == EMPTY32) {
       if (full) return OW_TAB;
-      const uint32_t old = atomicCAS(&sm.key[b], EMPTY32, key);
+      const uint32_t old = s_cas32(kb + 4 * b, EMPTY32, key);
       if (old == EMPTY32) return b | 0x80000000u;
       if (old == key) return b;
     }
     uint32_t g = b & ~3u;
     for (uint32_t walked = 0;; ++walked) {
       if (walked > OW_TAB / 4 + 1) return OW_TAB;  // cannot happen below OW_SPILL_AT; spill rather than spin
-      uint4 v;
-      asm volatile("ld.volatile.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                   : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                   : "r"(smem_u32(&sm.key[g])));
+      const uint4 v = s_ld128v(kb + 4 * g);
       const uint32_t hit = (v.x == key ? 1u : 0u) | (v.y == key ? 2u : 0u) | (v.z == key ? 4u : 0u) | (v.w == key ? 8u : 0u);
       if (hit) return g + __ffs(hit) - 1;
       uint32_t empt = (v.x == EMPTY32 ? 1u : 0u) | (v.y == EMPTY32 ? 2u : 0u) | (v.z == EMPTY32 ? 4u : 0u) | (v.w == EMPTY32 ? 8u : 0u);
@@ -468,7 +506,7 @@ uint32_t own_probe(OwnSmem& sm, uint32_t key, uint32_t b) {
       while (empt) {
         const uint32_t q = __ffs(empt) - 1;
         empt &= empt - 1;
-        const uint32_t old = atomicCAS(&sm.key[g + q], EMPTY32, key);
+        const uint32_t old = s_cas32(kb + 4 * (g + q), EMPTY32, key);
         if (old == EMPTY32) return (g + q) | 0x80000000u;
         if (old == key) return g + q;
       }
@@ -616,7 +654,7 @@ __device__ __noinline__ uint32_t own_cold(const uint4 q, uint32_t seg_launch, co
       uint32_t ins = 0;
       if (sl == OW_MISS) {  // new or displaced key: probe, inserting it (round 2: per-PC aggregated
                             // records used to spill every key not yet in the table)
-        const uint32_t r = own_probe(sm, key, bb);
+        const uint32_t r = own_probe(sm, key, bb, smem_u32(&sm));
         ins = r >> 31;
         sl = r & 0x7FFFFFFFu;
       }
@@ -858,6 +896,12 @@ __global__ void __launch_bounds__(OW_THREADS, OW_CPS) k_pc_owner(OwnArgs a) { DC
   // warp w takes samples [w*OW_ROUND, (w+1)*OW_ROUND) of every stage (OW_STAGE = 16 rounds),
   // loads them into registers, releases the stage, then aggregates them
   const uint32_t ctid = tid - 32, lane = ctid & 31, w = ctid >> 5;
+  // shared address of the block, pinned in a register (a volatile move: the compiler would
+  // otherwise rematerialise the conversion in the loop); hot-loop addresses are sb + offset
+  uint32_t sb;
+  asm volatile("mov.u32 %0, %1;" : "=r"(sb) : "r"(smem_u32(&sm)));
+  const uint32_t a_full = s_off(sm, &sm.full[0], sb), a_empty = s_off(sm, &sm.empty[0], sb);
+  const uint32_t a_cnt = s_off(sm, &sm.cnt[0], sb), a_pend = s_off(sm, &sm.pend[w][0], sb);
   uint32_t cur_ctx = OW_DONE, st = 0, ph = 0;
   OwCounters k{0, 0, 0, 0};
   uint32_t sinkv = 0;
@@ -865,7 +909,7 @@ __global__ void __launch_bounds__(OW_THREADS, OW_CPS) k_pc_owner(OwnArgs a) { DC
   uint32_t np = 0;        // queued misses of this warp (warp-uniform)
   uint32_t inserted = 0;  // keys this lane inserted since the last publish
   auto probe_add = [&](uint32_t key, uint32_t add) {
-    const uint32_t r = own_probe(sm, key, own_bucket(key));
+    const uint32_t r = own_probe(sm, key, own_bucket(key), sb);
     inserted += r >> 31;
     own_add(sm, a, key, r & 0x7FFFFFFFu, add, cur_ctx);
   };
@@ -892,14 +936,14 @@ __global__ void __launch_bounds__(OW_THREADS, OW_CPS) k_pc_owner(OwnArgs a) { DC
       // plain atomicAdd under `lane == 0` compiles to the warp-aggregated sequence).
       constexpr uint32_t TK_PERIOD = (uint32_t)OW_CONS_WARPS * OW_STAGES * 2;
       uint32_t tk = 0;
-      if (lane == 0) tk = atomicInc(&sm.ticket, TK_PERIOD - 1);
+      if (lane == 0) tk = s_inc32(s_off(sm, &sm.ticket, sb), TK_PERIOD - 1);
       tk = __shfl_sync(0xffffffffu, tk, 0);
       const uint32_t kst = tk / (uint32_t)OW_CONS_WARPS;  // < 2 * OW_STAGES
       grp = tk - kst * (uint32_t)OW_CONS_WARPS;
       ph = kst >= (uint32_t)OW_STAGES ? 1u : 0u;
       st = kst - ph * (uint32_t)OW_STAGES;
     }
-    mbar_wait(&sm.full[st], ph);
+    s_mbar_wait(a_full + 8 * st, ph);
     const long long c_1 = MODE == 9 ? clock64() : 0;
     const uint32_t mctx = sm.meta[st].ctx;
     const uint32_t flush = DC_OW_DYN ? (sm.meta[st].epoch != my_epoch ? 1u : 0u) : sm.meta[st].flush;
@@ -928,7 +972,7 @@ __global__ void __launch_bounds__(OW_THREADS, OW_CPS) k_pc_owner(OwnArgs a) { DC
     const bool ctx_ok = mctx < a.N;
     if (MODE == 2) {  // measurement only: the TMA pipeline alone (stage released unread)
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.empty[st]);
+      if (lane == 0) s_mbar_arrive(a_empty + 8 * st);
       if (!DC_OW_DYN && ++st == OW_STAGES) {
         st = 0;
         ph ^= 1u;
@@ -964,7 +1008,7 @@ __global__ void __launch_bounds__(OW_THREADS, OW_CPS) k_pc_owner(OwnArgs a) { DC
     // the stage's samples and row meta are in registers: release the slot to the producer now,
     // before the table work (one more stage of prefetch in flight)
     __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.empty[st]);
+    if (lane == 0) s_mbar_arrive(a_empty + 8 * st);
     if (MODE == 1) {  // measurement: data movement + classification only
 #pragma unroll
       for (int i = 0; i < OW_PER_LANE; ++i) sinkv ^= t[i] * (2 * i + 1);
@@ -1004,12 +1048,12 @@ __global__ void __launch_bounds__(OW_THREADS, OW_CPS) k_pc_owner(OwnArgs a) { DC
         if (DC_OW_NOBR) {  // branch-free: lanes without a hit add into the warp's dummy counter and
                            // lanes without a miss store into the queue's dummy tail slot
           const uint32_t cs = t[i] != EMPTY32 && !miss ? slot[i] : (uint32_t)OW_TAB + w;
-          asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(smem_u32(&sm.cnt[cs])) : "memory");
+          asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(a_cnt + 4 * cs) : "memory");
           const uint32_t mm = __ballot_sync(0xffffffffu, miss);
 #if DC_OW_PSTORE
           // predicated store (no dummy-slot wavefront when no lane missed)
           asm volatile("{\n.reg .pred p;\nsetp.ne.u32 p, %2, 0;\n@p st.shared.u32 [%0], %1;\n}\n" ::"r"(
-                           smem_u32(&sm.pend[w][np + __popc(mm & lanemask_lt())])),
+                           a_pend + 4 * (np + __popc(mm & lanemask_lt()))),
                        "r"(t[i]), "r"((uint32_t)miss)
                        : "memory");
 #else
