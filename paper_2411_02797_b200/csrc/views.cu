@@ -194,6 +194,30 @@ __global__ void __launch_bounds__(TK_THREADS, 1) k_topk_one(const uint64_t* __re
     return;
   }
   const uint32_t c = sm.cnt, kk = min(k, c);
+  if (c <= (uint32_t)TK_THREADS) {
+    // few candidates (the usual case: the threshold keeps a handful of hotspots): every
+    // candidate's rank among all of them directly, one pass instead of up to 12 radix passes
+    if (tid < c) {
+      const uint64_t v = sm.v[tid];
+      const uint32_t id = sm.id[tid];
+      uint32_t rank = 0;
+      for (uint32_t o = 0; o < c; ++o) rank += tk_greater(sm.v[o], sm.id[o], v, id) ? 1u : 0u;
+      if (rank < kk) {
+        dc_topk_entry en;
+        en.id = id;
+        en._pad = 0;
+        en.value = v;
+        en.fraction = frac_of(v, total);
+        out[1 + rank] = en;
+      }
+    }
+    if (tid == 0) {
+      dc_topk_entry h = {};
+      h.id = kk;
+      out[0] = h;
+    }
+    return;
+  }
   // radix select of the kk-th largest (value, ~id); every candidate key is distinct
   uint64_t pv = 0;   // prefix of the value digits found so far
   uint32_t pid = 0;  // prefix of the ~id digits
