@@ -492,6 +492,26 @@ __global__ void k_slot_leaf(const PathSlot* __restrict__ tab, uint64_t cap, cons
 __global__ void k_rec_leaf(const uint32_t* __restrict__ slot_of_rec, const uint32_t* __restrict__ leaf_of_slot, uint64_t cap,
                            uint32_t P0, const uint32_t* __restrict__ leaf_of_item, uint64_t R, uint32_t* __restrict__ leaf) { DC_PDL_WAIT();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  auto map = [&](uint32_t sl) { return sl < cap ? leaf_of_slot[sl] : leaf_of_item[P0 + (uint32_t)(sl - cap)]; };
+  if ((((uintptr_t)slot_of_rec | (uintptr_t)leaf) & 15u) == 0) {
+    // 16-B aligned: 4 consecutive records per thread and 2 such groups per round (one 16-B load
+    // and one 16-B store per group, 8 L2 gathers in flight), then the tail
+    const uint64_t R4 = R / 4;
+    const uint4* s4 = reinterpret_cast<const uint4*>(slot_of_rec);
+    uint4* l4 = reinterpret_cast<uint4*>(leaf);
+    for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < R4; q += 2 * stride) {
+      const bool two = q + stride < R4;
+      const uint4 a = s4[q];
+      const uint4 b = two ? s4[q + stride] : make_uint4(0, 0, 0, 0);
+      const uint4 la = make_uint4(map(a.x), map(a.y), map(a.z), map(a.w));
+      uint4 lb = make_uint4(0, 0, 0, 0);
+      if (two) lb = make_uint4(map(b.x), map(b.y), map(b.z), map(b.w));
+      l4[q] = la;
+      if (two) l4[q + stride] = lb;
+    }
+    for (uint64_t r = 4 * R4 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < R; r += stride) leaf[r] = map(slot_of_rec[r]);
+    return;
+  }
   for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < R; r += 4 * stride) {
     uint32_t s[4];
 #pragma unroll
