@@ -290,6 +290,9 @@ __global__ void __launch_bounds__(PT_THREADS) k_path_hash(const uint64_t* __rest
 // lane i: record r0 + i into the table; then the warp verifies each record against its
 // representative frame by frame
 constexpr uint64_t PG_SKIP = 0x8000000000000000ull;  // k_path_group sweep: rank not verified
+#ifndef DC_PG_BM
+#define DC_PG_BM 1
+#endif
 template <bool SWEEP>
 __global__ void __launch_bounds__(256, DC_PG_MINB) k_path_group(const uint64_t* __restrict__ off, const uint32_t* __restrict__ frames,
                                                     const uint64_t* __restrict__ hash, uint64_t R, PathSlot* __restrict__ tab,
@@ -298,6 +301,16 @@ __global__ void __launch_bounds__(256, DC_PG_MINB) k_path_group(const uint64_t* 
   __shared__ unsigned long long s_delta[8][32];  // per warp (256 threads): rep start - own start by nonempty rank
   const uint32_t lane = lane_id();
   unsigned long long* const sdelta = s_delta[(threadIdx.x >> 5) & 7];
+#if DC_PG_BM
+  // per warp: bitmap of the 32 records' start positions over their frame span (<= 32 * 1024
+  // frames), so a window's start mask is one shared load instead of a warp OR-reduction
+  __shared__ uint32_t s_bm[SWEEP ? 8 : 1][SWEEP ? DC_MAX_DEPTH : 1];
+  uint32_t* const sbm = s_bm[SWEEP ? (threadIdx.x >> 5) & 7 : 0];
+  if (SWEEP) {
+    for (uint32_t i = lane; i < DC_MAX_DEPTH; i += 32) sbm[i] = 0;
+    __syncwarp();
+  }
+#endif
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t r0 = warp * 32; r0 < R; r0 += nw * 32) {
@@ -368,6 +381,10 @@ __global__ void __launch_bounds__(256, DC_PG_MINB) k_path_group(const uint64_t* 
       const uint32_t* const own = frames + Fb;
       const uint32_t le = lanemask_lt() | (1u << lane);
       uint32_t before = 0, badm = 0;
+#if DC_PG_BM
+      if (nz) atomicOr(&sbm[orel >> 5], 1u << (orel & 31u));
+      __syncwarp();
+#endif
       // PG_W windows per round: every window's rank and delta first, then all loads, then the
       // compares (the own frames' DRAM latency is paid once per round, not once per window)
       for (uint32_t wb0 = 0; wb0 < span; wb0 += 32 * PG_W) {
@@ -376,8 +393,12 @@ __global__ void __launch_bounds__(256, DC_PG_MINB) k_path_group(const uint64_t* 
 #pragma unroll
         for (int u = 0; u < PG_W; ++u) {
           const uint32_t wb = wb0 + 32 * u;
+#if DC_PG_BM
+          const uint32_t M = wb < span ? sbm[wb >> 5] : 0u;
+#else
           const uint32_t sr = orel - wb;  // record start relative to the window (wraps if before)
           const uint32_t M = __reduce_or_sync(0xffffffffu, nz && sr < 32u ? 1u << sr : 0u);
+#endif
           cr[u] = before + __popc(M & le) - 1;  // rank of my frame's record (nonempty starts at or before it, - 1)
           before += __popc(M);
           dd[u] = wb + lane < span ? sdelta[cr[u] & 31] : PG_SKIP;
@@ -393,6 +414,10 @@ __global__ void __launch_bounds__(256, DC_PG_MINB) k_path_group(const uint64_t* 
         for (int u = 0; u < PG_W; ++u)
           if (a[u] != b[u]) badm |= 1u << (cr[u] & 31);
       }
+#if DC_PG_BM
+      __syncwarp();
+      if (nz) sbm[orel >> 5] = 0u;  // the next group starts from a clear bitmap
+#endif
       badm = __reduce_or_sync(0xffffffffu, badm);
       if (nz && need == 1u && ((badm >> rk) & 1u)) need = 2u;
       __syncwarp();  // sdelta reused by the next group
