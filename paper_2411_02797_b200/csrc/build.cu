@@ -76,7 +76,10 @@ struct __align__(32) PathSlot {
   unsigned long long key;  // record hash, ~0 = empty
   unsigned long long off;  // representative: first frame, length, record index (rep written last)
   uint32_t len, rep;
-  unsigned long long pad;
+  // (first frame << 11) | length, one 64-bit word (~0 until published): readers spin on it with
+  // relaxed gpu-scope loads and need no acquire (an acquire load invalidates the SM's L1, where
+  // the representatives' frames are cached for the verify)
+  unsigned long long offlen;
 };
 
 struct PathWarp {  // per warp: its 16 records of the tile
@@ -348,6 +351,7 @@ __global__ void __launch_bounds__(256, DC_PG_MINB) k_path_group(const uint64_t* 
         tab[sl].off = o;
         tab[sl].len = L;
         st_release_u32(&tab[sl].rep, (uint32_t)r);
+        *(volatile unsigned long long*)&tab[sl].offlen = (o << 11) | L;  // o < 2^40, L <= 1024
         const unsigned ins = atomicAdd(d_cnt, 1u);
         if ((uint64_t)ins * 2 >= mask) atomicOr(d_cnt + 3, 1u);  // past half load: retry larger
       }
@@ -355,10 +359,11 @@ __global__ void __launch_bounds__(256, DC_PG_MINB) k_path_group(const uint64_t* 
     }
     __syncwarp();  // this warp's representatives are published
     if (act && sl != PT_NONE && !mine) {
-      for (uint64_t spin = 0; ld_acquire_u32(&tab[sl].rep) == PT_NONE; ++spin)
+      unsigned long long w;
+      for (uint64_t spin = 0; (w = ld_relaxed_u64(&tab[sl].offlen)) == ~0ull; ++spin)
         if (spin > DC_SPIN_LIMIT) __trap();
-      ro = tab[sl].off;
-      const uint32_t rl = tab[sl].len;
+      ro = w >> 11;
+      const uint32_t rl = (uint32_t)(w & 0x7FFu);
       need = rl != L ? 2u : (L ? 1u : 0u);
     }
     uint32_t todo = __ballot_sync(0xffffffffu, need == 1u);
