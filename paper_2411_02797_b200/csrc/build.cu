@@ -1174,7 +1174,9 @@ __global__ void k_prefix_nodes(const uint64_t* __restrict__ off, const uint32_t*
       __syncwarp();
       if (act && !mine && sl != PT_NONE) {
         unsigned long long pp;
-        for (uint64_t spin = 0; (pp = ld_acquire_u64(&tab[sl].pay)) == ~0ull; ++spin)
+        // relaxed: the payload word is the data (no other field is read after it), and an acquire
+        // load would invalidate the SM's L1 on every pass
+        for (uint64_t spin = 0; (pp = ld_relaxed_u64(&tab[sl].pay)) == ~0ull; ++spin)
           if (spin > DC_SPIN_LIMIT) __trap();
         if (pp != pay) atomicOr(d_cnt + 2, 1u);  // same key, different (parent, frame): collision
       }
